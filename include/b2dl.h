@@ -1,0 +1,192 @@
+/*
+ * b2dl.h — C ABI of the B200-native DeepLabv3+/FC-DenseNet training-step library
+ * (libb2dl.so).  Plain C: raw device pointers, sizes, a cudaStream_t passed as
+ * void*.  No torch types cross this boundary.
+ *
+ * Two groups of entry points:
+ *
+ *  (1) Reference-shaped convolution kernels.  These are the drop-in for the
+ *      reference's kernel-backend protocol (pkg/src/deskdl/model/kernels.py:36-40)
+ *      and its compiled core (pkg/src/deskdl/model/_convkernels.pyx:16-71):
+ *      NCHW fp32 tensors, "same" padding with the TF split
+ *      (_kernels_py.py:18-21), stride 1 only, any dilation.  Validation errors
+ *      are returned as codes that the Python shim maps to the reference's
+ *      exceptions (NotImplementedError / ValueError).
+ *
+ *  (2) The NHWC bf16 fast path used by the training step: tcgen05 implicit-GEMM
+ *      convolution (forward + dgrad share one kernel, wgrad is split-K), the
+ *      fused weighted cross-entropy, the LARC multi-tensor update and the
+ *      memory-bound pool / upsample / mask / bias-gradient kernels.
+ *
+ * Every function returns 0 on success or a B2DL_E* code.  All launches are
+ * asynchronous on the given stream; the caller owns every buffer.
+ */
+#ifndef B2DL_H
+#define B2DL_H
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define B2DL_API __attribute__((visibility("default")))
+#else
+#define B2DL_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  B2DL_OK = 0,
+  B2DL_E_NOT_IMPLEMENTED = 1, /* stride != 1            -> NotImplementedError */
+  B2DL_E_VALUE = 2,           /* shape / channel errors  -> ValueError          */
+  B2DL_E_CUDA = 3,            /* launch or driver error  -> RuntimeError        */
+  B2DL_E_ALIGN = 4,           /* TMA alignment violated  -> ValueError          */
+  B2DL_E_NONFINITE = 5        /* LARC non-finite norm    -> FloatingPointError  */
+};
+
+/* NHWC bf16 (or fp32 where stated) activation view.  `ptr` points at element
+ * (0,0,0,c_off) of a buffer whose pixel pitch is `c_stride` channels; the view
+ * covers `c` channels.  Concat buffers are shared by several views. */
+typedef struct b2dl_act {
+  void* ptr;
+  int n, h, w;
+  int c;
+  int c_stride;
+} b2dl_act;
+
+/* ---------------------------------------------------------------- (1) reference-shaped */
+
+/* Workspace bytes needed by the NCHW fp32 entry points for this shape. */
+B2DL_API size_t b2dl_conv2d_workspace_size(int n, int cin, int h, int w, int cout, int kh, int kw);
+
+/* y[n,cout,h,w] = conv(x[n,cin,h,w], w[cout,cin,kh,kw]), same padding.
+ * Replaces _kernels_py.conv2d_forward (_kernels_py.py:44-55) and
+ * _convkernels.conv2d_forward_core (_convkernels.pyx:16-32). */
+B2DL_API int b2dl_conv2d_forward(const float* x, const float* w, float* y, int n, int cin, int h, int wd, int cout,
+                        int kh, int kw, int stride, int dilation, void* workspace, size_t workspace_bytes,
+                        void* stream);
+
+/* dx[n,cin,h,w] from dy[n,cout,h,w].  Replaces _kernels_py.conv2d_backward_input
+ * (_kernels_py.py:65-83) and conv2d_backward_input_core (_convkernels.pyx:35-51). */
+B2DL_API int b2dl_conv2d_backward_input(const float* dy, const float* w, float* dx, int n, int cin, int h, int wd,
+                               int cout, int kh, int kw, int stride, int dilation, void* workspace,
+                               size_t workspace_bytes, void* stream);
+
+/* dw[cout,cin,kh,kw] from x and dy.  Replaces _kernels_py.conv2d_backward_weights
+ * (_kernels_py.py:58-62) and conv2d_backward_weights_core (_convkernels.pyx:54-71). */
+B2DL_API int b2dl_conv2d_backward_weights(const float* x, const float* dy, float* dw, int n, int cin, int h, int wd,
+                                 int cout, int kh, int kw, int dilation, void* workspace,
+                                 size_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------- (2) NHWC fast path */
+
+/* Implicit-GEMM convolution on tcgen05 (stride 1, same padding):
+ *   y = epilogue( sum_{tap,ci} x[p + off(tap), ci] * w_packed[co, tap, ci] )
+ * epilogue: +bias[co], +residual, relu, y_old + (accumulate), *(mask > 0).
+ * w_packed: bf16 [cout][kh*kw][cin_pad], cin_pad = b2dl_cin_pad(cin).
+ * Used for the forward conv and, with dgrad-packed weights and swapped pads,
+ * for the input gradient (the reference's conv2d_backward_input). */
+typedef struct b2dl_conv_args {
+  b2dl_act x;
+  const void* w_packed;
+  int cout, kh, kw, dilation, pad_top, pad_left;
+  b2dl_act y;
+  int y_f32;
+  const float* bias;
+  b2dl_act residual;
+  int relu;
+  int accumulate;
+  b2dl_act mask;
+  int block_n; /* 0 = auto */
+} b2dl_conv_args;
+
+B2DL_API int b2dl_cin_pad(int cin);
+B2DL_API int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream);
+
+/* Weight gradient (the reference's conv2d_backward_weights), split-K over
+ * pixels on tcgen05 with a deterministic reduction:
+ *   dw[tap][ci][co] (+)= sum_p x[p + off(tap), ci] * dy[p, co]      (fp32, HWIO)
+ * If bias_grad != NULL it also receives sum_p dy[p, co] (the bias_add VJP,
+ * ops.py:172-175), accumulated when accumulate != 0. */
+typedef struct b2dl_wgrad_args {
+  b2dl_act x;
+  b2dl_act dy;
+  int kh, kw, dilation, pad_top, pad_left;
+  float* dw;
+  float* bias_grad;
+  int accumulate;
+  void* workspace;
+  size_t workspace_bytes;
+  int splits; /* 0 = auto */
+} b2dl_wgrad_args;
+
+B2DL_API size_t b2dl_wgrad_workspace_size(const b2dl_wgrad_args* a);
+B2DL_API int b2dl_conv_wgrad(const b2dl_wgrad_args* a, void* stream);
+
+/* Pack fp32 HWIO master weights into the bf16 fprop layout [cout][taps][cin_pad]
+ * and (optionally) the dgrad layout [cin][taps(flipped)][cout_pad]. */
+B2DL_API int b2dl_pack_weights(const float* w_hwio, int kh, int kw, int cin, int cout, void* fprop_packed,
+                      void* dgrad_packed, void* stream);
+
+/* NCHW fp32 -> NHWC bf16 view (input tiles, reference-layout tensors). */
+B2DL_API int b2dl_nchw_to_nhwc(const float* x, b2dl_act y, void* stream);
+/* NHWC (bf16, or fp32 when src_f32) view -> NCHW fp32. */
+B2DL_API int b2dl_nhwc_to_nchw(b2dl_act x, int src_f32, float* y, void* stream);
+
+/* avgpool window k (ops.py:133-138) and its VJP (ops.py:186-189). */
+B2DL_API int b2dl_avgpool_fwd(b2dl_act x, b2dl_act y, int k, void* stream);
+B2DL_API int b2dl_avgpool_bwd(b2dl_act dy, b2dl_act dx, int k, int accumulate, b2dl_act mask, void* stream);
+/* nearest upsample factor f (ops.py:139-141) and its VJP, a block sum (ops.py:190-194). */
+B2DL_API int b2dl_upsample_fwd(b2dl_act x, b2dl_act y, int f, void* stream);
+B2DL_API int b2dl_upsample_bwd(b2dl_act dy, b2dl_act dx, int f, int accumulate, b2dl_act mask, void* stream);
+/* y (+)= x, optionally masked by (mask > 0): elementwise-add VJP / fan-out sums. */
+B2DL_API int b2dl_add(b2dl_act x, b2dl_act y, int accumulate, b2dl_act mask, void* stream);
+/* in-place g *= (act > 0): relu VJP (ops.py:176-177). */
+B2DL_API int b2dl_relu_mask(b2dl_act g, b2dl_act act, void* stream);
+/* bias gradient: out[c] (+)= sum over pixels of g (ops.py:172-175). */
+B2DL_API int b2dl_bias_grad(b2dl_act g, float* out, int accumulate, void* workspace, size_t workspace_bytes,
+                   void* stream);
+B2DL_API size_t b2dl_bias_grad_workspace_size(b2dl_act g);
+
+/* Class-weighted softmax cross-entropy (loss.py:47-93), fused:
+ *   counts[n][c]  exact per-sample label histogram (int32)
+ *   loss_out[0]   mean over samples of sum_p w_y nll / sum_p w_y  (fp32)
+ *   dlogits       (softmax - onehot) * w_y / (sum_p w_y * N) written as a bf16
+ *                 NHWC view with `classes` channels
+ *   pred          argmax over classes, ties to the lowest index (uint8)
+ * logits: fp32 NHWC view with `classes` channels; labels uint8 [N*H*W]. */
+B2DL_API int b2dl_wce(b2dl_act logits, const uint8_t* labels, const float* class_weights, int classes, float* loss_out,
+             int* counts, b2dl_act dlogits, uint8_t* pred, void* workspace, size_t workspace_bytes,
+             void* stream);
+B2DL_API size_t b2dl_wce_workspace_size(int n, int h, int w, int classes);
+
+/* LARC + SGD momentum over many tensors (optimizer.py:48-83) in two launches:
+ *   per tensor t: wn = |w_t|, gn = |g_t| * grad_scale
+ *   lr_t = lr if wn == 0 or (gn + wd*wn) < eps else min(trust*wn/(gn+wd*wn), lr)
+ *   m = beta*m + g*grad_scale + wd*w ; w -= lr_t * m
+ * Tensors are contiguous segments of flat fp32 buffers (offsets[t]..offsets[t+1]).
+ * grad_scale folds the data-parallel mean (1/P).  lr_out[t] receives lr_t;
+ * status[0] is set to 1 if any norm is non-finite (and no update is applied). */
+typedef struct b2dl_larc_args {
+  float* w;
+  float* m;
+  const float* g;
+  const int64_t* offsets; /* device, ntensors+1 */
+  int ntensors;
+  float lr, momentum, trust, weight_decay, eps, grad_scale;
+  float* lr_out;   /* device, ntensors */
+  int* status;     /* device, 1 int */
+  void* workspace; /* device scratch */
+  size_t workspace_bytes;
+} b2dl_larc_args;
+B2DL_API size_t b2dl_larc_workspace_size(int64_t total_elems, int ntensors);
+B2DL_API int b2dl_larc_update(const b2dl_larc_args* a, void* stream);
+
+/* Version / capability string (for smoke checks). */
+B2DL_API const char* b2dl_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B2DL_H */

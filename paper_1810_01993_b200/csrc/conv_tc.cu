@@ -1,0 +1,694 @@
+// Implicit-GEMM convolution on sm_100a tensor cores (tcgen05 + TMEM + TMA).
+//
+// The reference computes every convolution of the training step in
+// pkg/src/deskdl/model/_kernels_py.py:44-83 (im2col + sgemm) or
+// _convkernels.pyx:16-71 (direct loops), NCHW fp32.  Here the same three
+// products run NHWC bf16 with fp32 accumulation in TMEM:
+//
+//   fprop / dgrad  M = pixels (128-pixel rectangular box), N = output channels,
+//                  K = taps x input channels.  Each K block is one TMA box of the
+//                  input shifted by the tap offset; TMA's out-of-bounds zero fill
+//                  implements the "same" padding and any dilation.  dgrad is the
+//                  same kernel over dy with tap-flipped, ci/co-swapped weights.
+//   wgrad          M = (tap, ci) rows (two 64-channel shifted boxes), N = output
+//                  channels, K = pixels; both operands MN-major.  Split-K over
+//                  pixel boxes, fp32 partials, deterministic reduction.
+//
+// Warp roles (192 threads, one CTA per SM, persistent over tiles):
+//   warp 0  TMA producer      warp 1  MMA issuer + TMEM owner
+//   warps 2-5 epilogue (TMEM -> registers -> fused epilogue -> global)
+// Two TMEM accumulator stages let the epilogue of tile i overlap the MMAs of i+1.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+
+#include "internal.h"
+#include "sm100.cuh"
+
+namespace b2 {
+
+constexpr int BM = 128;
+constexpr int SMEM_BUDGET = 200 * 1024;
+
+__host__ __device__ constexpr uint32_t tmem_cols_for(int n) {
+  return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : n <= 256 ? 256 : 512;
+}
+template <int BN, int KBLK>
+struct FpropCfg {
+  static constexpr int A_BYTES = BM * KBLK * 2;
+  static constexpr int B_BYTES = BN * KBLK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (SMEM_BUDGET / STAGE_BYTES) > 8 ? 8 : (SMEM_BUDGET / STAGE_BYTES);
+  static constexpr uint32_t TMEM_COLS = tmem_cols_for(2 * BN);
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int CW = BN < 32 ? BN : 32;  // epilogue chunk (TMEM columns per load)
+};
+
+struct FpropParams {
+  int n, h, w;
+  int bw, bh, tiles_x, tiles_y;
+  int num_m_tiles, num_n_tiles, num_tiles;
+  int kw, dil, pad_top, pad_left;
+  int num_cblk, num_kb, cin_pad;
+  int cout;
+  void* y;
+  long long y_stride;
+  int y_f32;
+  const float* bias;
+  const __nv_bfloat16* res;
+  long long res_stride;
+  const __nv_bfloat16* mask;
+  long long mask_stride;
+  int relu, accumulate, vec_ok;
+};
+
+__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+  uint32_t a = smem_u32(p);
+  return p + ((1024 - (a & 1023)) & 1023);
+}
+
+template <int CW>
+__device__ __forceinline__ void fprop_epilogue_chunk(const FpropParams& p, float* v, long long pix, int c0) {
+  const int nvalid = min(CW, p.cout - c0);
+  if (p.bias) {
+#pragma unroll
+    for (int i = 0; i < CW; ++i)
+      if (i < nvalid) v[i] += __ldg(p.bias + c0 + i);
+  }
+  if (p.vec_ok && nvalid == CW && !p.y_f32) {
+    if (p.res) {
+      const uint4* r = reinterpret_cast<const uint4*>(p.res + pix * p.res_stride + c0);
+#pragma unroll
+      for (int q = 0; q < CW / 8; ++q) {
+        uint4 u = __ldg(r + q);
+        uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          v[q * 8 + 2 * e] += bf16lo(w4[e]);
+          v[q * 8 + 2 * e + 1] += bf16hi(w4[e]);
+        }
+      }
+    }
+    if (p.relu) {
+#pragma unroll
+      for (int i = 0; i < CW; ++i) v[i] = fmaxf(v[i], 0.f);
+    }
+    if (p.mask) {
+      const uint4* r = reinterpret_cast<const uint4*>(p.mask + pix * p.mask_stride + c0);
+#pragma unroll
+      for (int q = 0; q < CW / 8; ++q) {
+        uint4 u = __ldg(r + q);
+        uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (!(bf16lo(w4[e]) > 0.f)) v[q * 8 + 2 * e] = 0.f;
+          if (!(bf16hi(w4[e]) > 0.f)) v[q * 8 + 2 * e + 1] = 0.f;
+        }
+      }
+    }
+    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.y) + pix * p.y_stride + c0);
+    if (p.accumulate) {
+#pragma unroll
+      for (int q = 0; q < CW / 8; ++q) {
+        uint4 u = dst[q];
+        uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          v[q * 8 + 2 * e] += bf16lo(w4[e]);
+          v[q * 8 + 2 * e + 1] += bf16hi(w4[e]);
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < CW / 8; ++q) {
+      uint4 u;
+      u.x = pack_bf16x2(v[q * 8 + 0], v[q * 8 + 1]);
+      u.y = pack_bf16x2(v[q * 8 + 2], v[q * 8 + 3]);
+      u.z = pack_bf16x2(v[q * 8 + 4], v[q * 8 + 5]);
+      u.w = pack_bf16x2(v[q * 8 + 6], v[q * 8 + 7]);
+      dst[q] = u;
+    }
+    return;
+  }
+  // general (scalar) path: ragged channel counts, fp32 output, unaligned views
+  for (int i = 0; i < nvalid; ++i) {
+    float x = v[i];
+    if (p.res) x += __bfloat162float(p.res[pix * p.res_stride + c0 + i]);
+    if (p.relu) x = fmaxf(x, 0.f);
+    if (p.mask && !(__bfloat162float(p.mask[pix * p.mask_stride + c0 + i]) > 0.f)) x = 0.f;
+    if (p.y_f32) {
+      float* d = reinterpret_cast<float*>(p.y) + pix * p.y_stride + c0 + i;
+      *d = p.accumulate ? *d + x : x;
+    } else {
+      __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(p.y) + pix * p.y_stride + c0 + i;
+      if (p.accumulate) x += __bfloat162float(*d);
+      *d = __float2bfloat16_rn(x);
+    }
+  }
+}
+
+template <int BN, int KBLK>
+__global__ void __launch_bounds__(192, 1)
+    conv_fprop_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                      const FpropParams p) {
+  using C = FpropCfg<BN, KBLK>;
+  constexpr int STAGES = C::STAGES;
+  constexpr uint32_t LAYOUT = KBLK == 64 ? LAYOUT_SW128 : LAYOUT_SW32;
+  constexpr uint32_t SBO = KBLK * 2 * 8;  // 8 rows of KBLK bf16
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * C::B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = lane_id();
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int per_img = p.tiles_x * p.tiles_y;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        const int mt = tile / p.num_n_tiles, nt = tile - mt * p.num_n_tiles;
+        const int img = mt / per_img, r = mt - img * per_img;
+        const int ty = r / p.tiles_x, tx = r - ty * p.tiles_x;
+        const int y0 = ty * p.bh, x0 = tx * p.bw, n0 = nt * BN;
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          const int tap = kb / p.num_cblk, cb = kb - tap * p.num_cblk;
+          const int i = tap / p.kw, j = tap - i * p.kw;
+          tma_load_4d(sA + stage * C::A_BYTES, &tmA, &full[stage], cb * KBLK, x0 + j * p.dil - p.pad_left,
+                      y0 + i * p.dil - p.pad_top, img);
+          tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], tap * p.cin_pad + cb * KBLK, n0);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc_bf16(BM, BN, false, false);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++it) {
+        const int as = it & 1;
+        const uint32_t ap = (it >> 1) & 1;
+        mbar_wait(&tempty[as], ap ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + as * BN;
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
+          const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < KBLK / 16; ++k) {
+            const uint64_t ad = make_sdesc(a0 + k * 32, 16, SBO, LAYOUT);
+            const uint64_t bd = make_sdesc(b0 + k * 32, 16, SBO, LAYOUT);
+            umma_bf16(d, ad, bd, idesc, (kb | k) != 0);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[as]);
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const int ry = row / p.bw, rx = row - ry * p.bw;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++it) {
+      const int as = it & 1;
+      const uint32_t ap = (it >> 1) & 1;
+      const int mt = tile / p.num_n_tiles, nt = tile - mt * p.num_n_tiles;
+      const int img = mt / per_img, r = mt - img * per_img;
+      const int ty = r / p.tiles_x, tx = r - ty * p.tiles_x;
+      const int yy = ty * p.bh + ry, xx = tx * p.bw + rx;
+      const bool valid = yy < p.h && xx < p.w;
+      const long long pix = (static_cast<long long>(img) * p.h + yy) * p.w + xx;
+      mbar_wait(&tfull[as], ap);
+      tc_fence_after();
+#pragma unroll 1
+      for (int ch = 0; ch < BN / C::CW; ++ch) {
+        float v[32];
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + as * BN + ch * C::CW;
+        if constexpr (C::CW == 32)
+          tmem_ld_32x32b_x32(taddr, v);
+        else
+          tmem_ld_32x32b_x16(taddr, v);
+        const int c0 = nt * BN + ch * C::CW;
+        if (valid && c0 < p.cout) fprop_epilogue_chunk<C::CW>(p, v, pix, c0);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[as]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, C::TMEM_COLS);
+  }
+}
+
+// ------------------------------------------------------------------ wgrad
+template <int BN>
+struct WgradCfg {
+  static constexpr int CHUNK = 64 * 64 * 2;  // 64 channels x 64 pixels bf16 = 8 KB
+  static constexpr int NB = BN < 64 ? 1 : BN / 64;
+  static constexpr int A_BYTES = 2 * CHUNK;
+  static constexpr int B_BYTES = NB * CHUNK;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (SMEM_BUDGET / STAGE_BYTES) > 8 ? 8 : (SMEM_BUDGET / STAGE_BYTES);
+  static constexpr uint32_t TMEM_COLS = tmem_cols_for(2 * BN);
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int CW = BN < 32 ? BN : 32;
+};
+
+struct WgradParams {
+  int n, h, w;
+  int bwk, bhk, pbx, pby, num_pb;
+  int kw, dil, pad_top, pad_left;
+  int cblk, num_x_chunks;
+  int m_tiles, n_tiles, splits, num_tiles, pb_per_split;
+  int cin, cout;
+  long long krows;  // taps * cin
+  float* ws;        // [splits][krows][cout]
+};
+
+template <int BN>
+__global__ void __launch_bounds__(192, 1)
+    conv_wgrad_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmDY,
+                      const WgradParams p) {
+  using C = WgradCfg<BN>;
+  constexpr int STAGES = C::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * C::B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = lane_id();
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmX);
+    tma_prefetch(&tmDY);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int per_img = p.pbx * p.pby;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        const int mt = tile % p.m_tiles;
+        const int rest = tile / p.m_tiles;
+        const int nt = rest % p.n_tiles, split = rest / p.n_tiles;
+        const int pb_lo = split * p.pb_per_split, pb_hi = min(p.num_pb, pb_lo + p.pb_per_split);
+        int tx_bytes = C::B_BYTES;
+        if (2 * mt < p.num_x_chunks) tx_bytes += C::CHUNK;
+        if (2 * mt + 1 < p.num_x_chunks) tx_bytes += C::CHUNK;
+        for (int pb = pb_lo; pb < pb_hi; ++pb) {
+          const int img = pb / per_img, r = pb - img * per_img;
+          const int by = r / p.pbx, bx = r - by * p.pbx;
+          const int x0 = bx * p.bwk, y0 = by * p.bhk;
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], tx_bytes);
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const int chunk = 2 * mt + c;
+            if (chunk < p.num_x_chunks) {
+              const int tap = chunk / p.cblk, cb = chunk - tap * p.cblk;
+              const int i = tap / p.kw, j = tap - i * p.kw;
+              tma_load_4d(sA + stage * C::A_BYTES + c * C::CHUNK, &tmX, &full[stage], cb * 64,
+                          x0 + j * p.dil - p.pad_left, y0 + i * p.dil - p.pad_top, img);
+            }
+          }
+#pragma unroll
+          for (int qq = 0; qq < C::NB; ++qq)
+            tma_load_4d(sB + stage * C::B_BYTES + qq * C::CHUNK, &tmDY, &full[stage], nt * BN + qq * 64, x0, y0,
+                        img);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc_bf16(BM, BN, true, true);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++it) {
+        const int rest = tile / p.m_tiles;
+        const int split = rest / p.n_tiles;
+        const int pb_lo = split * p.pb_per_split, pb_hi = min(p.num_pb, pb_lo + p.pb_per_split);
+        const int as = it & 1;
+        const uint32_t ap = (it >> 1) & 1;
+        mbar_wait(&tempty[as], ap ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + as * BN;
+        for (int pb = pb_lo; pb < pb_hi; ++pb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
+          const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            // MN-major SW128: 64-element MN chunks LBO = 8 KB apart, 8-pixel K groups SBO = 1 KB apart
+            const uint64_t ad = make_sdesc(a0 + k * 2048, C::CHUNK, 1024, LAYOUT_SW128);
+            const uint64_t bd = make_sdesc(b0 + k * 2048, C::CHUNK, 1024, LAYOUT_SW128);
+            umma_bf16(d, ad, bd, idesc, (pb != pb_lo) || (k != 0));
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[as]);
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++it) {
+      const int as = it & 1;
+      const uint32_t ap = (it >> 1) & 1;
+      const int mt = tile % p.m_tiles;
+      const int rest = tile / p.m_tiles;
+      const int nt = rest % p.n_tiles, split = rest / p.n_tiles;
+      const int chunk = 2 * mt + (row >> 6);
+      const int tap = chunk / p.cblk;
+      const int ci = (chunk - tap * p.cblk) * 64 + (row & 63);
+      const bool valid = chunk < p.num_x_chunks && ci < p.cin;
+      float* dst = p.ws + (static_cast<long long>(split) * p.krows + static_cast<long long>(tap) * p.cin + ci) * p.cout;
+      mbar_wait(&tfull[as], ap);
+      tc_fence_after();
+#pragma unroll 1
+      for (int ch = 0; ch < BN / C::CW; ++ch) {
+        float v[32];
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + as * BN + ch * C::CW;
+        if constexpr (C::CW == 32)
+          tmem_ld_32x32b_x32(taddr, v);
+        else
+          tmem_ld_32x32b_x16(taddr, v);
+        const int c0 = nt * BN + ch * C::CW;
+        if (valid && c0 < p.cout) {
+          const int nvalid = min(C::CW, p.cout - c0);
+          if (nvalid == C::CW && (p.cout & 3) == 0) {
+#pragma unroll
+            for (int e = 0; e < C::CW; e += 4)
+              *reinterpret_cast<float4*>(dst + c0 + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+          } else {
+            for (int e = 0; e < nvalid; ++e) dst[c0 + e] = v[e];
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[as]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, C::TMEM_COLS);
+  }
+}
+
+// dw[k][co] (+)= sum_s ws[s][k][co]   (fixed summation order -> deterministic)
+__global__ void wgrad_reduce_kernel(const float* __restrict__ ws, float* __restrict__ dw, long long total,
+                                    int splits, int accumulate) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float s = accumulate ? dw[i] : 0.f;
+    for (int k = 0; k < splits; ++k) s += ws[k * total + i];
+    dw[i] = s;
+  }
+}
+
+// ------------------------------------------------------------------ host side
+template <int BN, int KBLK>
+static int launch_fprop(const CUtensorMap& ta, const CUtensorMap& tb, const FpropParams& p, cudaStream_t st) {
+  using C = FpropCfg<BN, KBLK>;
+  auto kern = conv_fprop_kernel<BN, KBLK>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) != cudaSuccess)
+      return B2DL_E_CUDA;
+    attr_set = true;
+  }
+  const int grid = std::min(p.num_tiles, num_sms());
+  kern<<<grid, 192, C::SMEM, st>>>(ta, tb, p);
+  return check_launch();
+}
+
+template <int BN>
+static int launch_wgrad(const CUtensorMap& tx, const CUtensorMap& tdy, const WgradParams& p, cudaStream_t st) {
+  using C = WgradCfg<BN>;
+  auto kern = conv_wgrad_kernel<BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) != cudaSuccess)
+      return B2DL_E_CUDA;
+    attr_set = true;
+  }
+  const int grid = std::min(p.num_tiles, num_sms());
+  kern<<<grid, 192, C::SMEM, st>>>(tx, tdy, p);
+  return check_launch();
+}
+
+static int pick_bn(int cout) {
+  if (cout > 128) return 256;
+  if (cout > 64) return 128;
+  if (cout > 32) return 64;
+  if (cout > 16) return 32;
+  return 16;
+}
+
+static bool view_aligned(const b2dl_act& a, int elem_bytes) {
+  return (reinterpret_cast<uintptr_t>(a.ptr) % 16 == 0) && ((static_cast<long long>(a.c_stride) * elem_bytes) % 16 == 0);
+}
+
+}  // namespace b2
+
+using namespace b2;
+
+extern "C" int b2dl_cin_pad(int cin) { return cin <= 16 ? 16 : round_up(cin, 64); }
+
+extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
+  if (!a || !a->x.ptr || !a->w_packed || !a->y.ptr) return B2DL_E_VALUE;
+  const b2dl_act& x = a->x;
+  const b2dl_act& y = a->y;
+  if (x.n != y.n || x.h != y.h || x.w != y.w || y.c != a->cout) return B2DL_E_VALUE;
+  if (a->kh < 1 || a->kw < 1 || a->dilation < 1 || a->cout < 1 || x.c < 1) return B2DL_E_VALUE;
+  if (!view_aligned(x, 2)) return B2DL_E_ALIGN;
+  const int kblk = x.c <= 16 ? 16 : 64;
+  const int cin_pad = b2dl_cin_pad(x.c);
+  const int bn = a->block_n ? a->block_n : pick_bn(a->cout);
+
+  FpropParams p{};
+  p.n = x.n;
+  p.h = x.h;
+  p.w = x.w;
+  p.bw = pow2_divisor(x.w, 128);
+  if (p.bw < 8 && x.w >= 8) p.bw = std::min(128, 1 << (31 - __builtin_clz(x.w)));
+  p.bh = BM / p.bw;
+  p.tiles_x = cdiv(x.w, p.bw);
+  p.tiles_y = cdiv(x.h, p.bh);
+  p.num_m_tiles = x.n * p.tiles_x * p.tiles_y;
+  p.num_n_tiles = cdiv(a->cout, bn);
+  p.num_tiles = p.num_m_tiles * p.num_n_tiles;
+  p.kw = a->kw;
+  p.dil = a->dilation;
+  p.pad_top = a->pad_top;
+  p.pad_left = a->pad_left;
+  p.num_cblk = cin_pad / kblk;
+  p.num_kb = a->kh * a->kw * p.num_cblk;
+  p.cin_pad = cin_pad;
+  p.cout = a->cout;
+  p.y = y.ptr;
+  p.y_stride = y.c_stride;
+  p.y_f32 = a->y_f32;
+  p.bias = a->bias;
+  p.res = reinterpret_cast<const __nv_bfloat16*>(a->residual.ptr);
+  p.res_stride = a->residual.c_stride;
+  p.mask = reinterpret_cast<const __nv_bfloat16*>(a->mask.ptr);
+  p.mask_stride = a->mask.c_stride;
+  p.relu = a->relu;
+  p.accumulate = a->accumulate;
+  p.vec_ok = view_aligned(y, a->y_f32 ? 4 : 2) && (!p.res || view_aligned(a->residual, 2)) &&
+             (!p.mask || view_aligned(a->mask, 2));
+
+  CUtensorMap ta, tb;
+  const CUtensorMapSwizzle sw = kblk == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B;
+  if (act_map(&ta, x, kblk, p.bw, p.bh, sw)) return B2DL_E_ALIGN;
+  const uint64_t ktot = static_cast<uint64_t>(a->kh) * a->kw * cin_pad;
+  const uint64_t wd[2] = {ktot, static_cast<uint64_t>(a->cout)};
+  const uint64_t ws[1] = {ktot * 2};
+  const uint32_t wb[2] = {static_cast<uint32_t>(kblk), static_cast<uint32_t>(bn)};
+  if (encode_tiled(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a->w_packed), wd, ws, wb, sw))
+    return B2DL_E_ALIGN;
+
+  cudaStream_t st = as_stream(stream);
+#define B2_FPROP(BNV, KB) \
+  if (bn == BNV && kblk == KB) return launch_fprop<BNV, KB>(ta, tb, p, st);
+  B2_FPROP(256, 64)
+  B2_FPROP(128, 64)
+  B2_FPROP(64, 64)
+  B2_FPROP(32, 64)
+  B2_FPROP(16, 64)
+  B2_FPROP(256, 16)
+  B2_FPROP(128, 16)
+  B2_FPROP(64, 16)
+  B2_FPROP(32, 16)
+  B2_FPROP(16, 16)
+#undef B2_FPROP
+  return B2DL_E_VALUE;
+}
+
+namespace b2 {
+struct WgradPlan {
+  WgradParams p;
+  int bn;
+  size_t ws_bytes;
+};
+static int plan_wgrad(const b2dl_wgrad_args* a, WgradPlan* out) {
+  const b2dl_act& x = a->x;
+  const b2dl_act& dy = a->dy;
+  if (x.n != dy.n || x.h != dy.h || x.w != dy.w) return B2DL_E_VALUE;
+  WgradParams p{};
+  p.n = x.n;
+  p.h = x.h;
+  p.w = x.w;
+  p.bwk = pow2_divisor(x.w, 64);
+  if (p.bwk < 8 && x.w >= 8) p.bwk = std::min(64, 1 << (31 - __builtin_clz(x.w)));
+  p.bhk = 64 / p.bwk;
+  p.pbx = cdiv(x.w, p.bwk);
+  p.pby = cdiv(x.h, p.bhk);
+  p.num_pb = x.n * p.pbx * p.pby;
+  p.kw = a->kw;
+  p.dil = a->dilation;
+  p.pad_top = a->pad_top;
+  p.pad_left = a->pad_left;
+  p.cblk = cdiv(x.c, 64);
+  p.num_x_chunks = a->kh * a->kw * p.cblk;
+  p.cin = x.c;
+  p.cout = dy.c;
+  p.krows = static_cast<long long>(a->kh) * a->kw * x.c;
+  const int bn = pick_bn(dy.c);
+  p.m_tiles = cdiv(p.num_x_chunks, 2);
+  p.n_tiles = cdiv(dy.c, bn);
+  int splits = a->splits;
+  if (splits <= 0) {
+    const int base = p.m_tiles * p.n_tiles;
+    splits = std::max(1, (2 * num_sms() + base - 1) / base);
+    // keep >= 8 pixel boxes of work per split
+    splits = std::min(splits, std::max(1, p.num_pb / 8));
+  }
+  splits = std::min(splits, p.num_pb);
+  p.pb_per_split = cdiv(p.num_pb, splits);
+  p.splits = cdiv(p.num_pb, p.pb_per_split);  // no empty splits
+  p.num_tiles = p.m_tiles * p.n_tiles * p.splits;
+  out->p = p;
+  out->bn = bn;
+  out->ws_bytes = static_cast<size_t>(p.splits) * p.krows * p.cout * sizeof(float);
+  return B2DL_OK;
+}
+}  // namespace b2
+
+extern "C" size_t b2dl_wgrad_workspace_size(const b2dl_wgrad_args* a) {
+  WgradPlan pl;
+  if (!a || plan_wgrad(a, &pl)) return 0;
+  size_t extra = a->bias_grad ? b2dl_bias_grad_workspace_size(a->dy) : 0;
+  return align_up(pl.ws_bytes, 256) + extra;
+}
+
+extern "C" int b2dl_conv_wgrad(const b2dl_wgrad_args* a, void* stream) {
+  if (!a || !a->x.ptr || !a->dy.ptr || !a->dw) return B2DL_E_VALUE;
+  if (!view_aligned(a->x, 2) || !view_aligned(a->dy, 2)) return B2DL_E_ALIGN;
+  WgradPlan pl;
+  int rc = plan_wgrad(a, &pl);
+  if (rc) return rc;
+  const size_t need = b2dl_wgrad_workspace_size(a);
+  if (!a->workspace || a->workspace_bytes < need) return B2DL_E_VALUE;
+  pl.p.ws = reinterpret_cast<float*>(a->workspace);
+  CUtensorMap tx, tdy;
+  if (act_map(&tx, a->x, 64, pl.p.bwk, pl.p.bhk, CU_TENSOR_MAP_SWIZZLE_128B)) return B2DL_E_ALIGN;
+  if (act_map(&tdy, a->dy, 64, pl.p.bwk, pl.p.bhk, CU_TENSOR_MAP_SWIZZLE_128B)) return B2DL_E_ALIGN;
+  cudaStream_t st = as_stream(stream);
+  switch (pl.bn) {
+    case 256: rc = launch_wgrad<256>(tx, tdy, pl.p, st); break;
+    case 128: rc = launch_wgrad<128>(tx, tdy, pl.p, st); break;
+    case 64: rc = launch_wgrad<64>(tx, tdy, pl.p, st); break;
+    case 32: rc = launch_wgrad<32>(tx, tdy, pl.p, st); break;
+    default: rc = launch_wgrad<16>(tx, tdy, pl.p, st); break;
+  }
+  if (rc) return rc;
+  const long long total = pl.p.krows * pl.p.cout;
+  const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 4LL * num_sms()));
+  wgrad_reduce_kernel<<<blocks, 256, 0, st>>>(pl.p.ws, a->dw, total, pl.p.splits, a->accumulate);
+  rc = check_launch();
+  if (rc) return rc;
+  if (a->bias_grad) {
+    char* extra = reinterpret_cast<char*>(a->workspace) + align_up(pl.ws_bytes, 256);
+    rc = b2dl_bias_grad(a->dy, a->bias_grad, a->accumulate, extra, a->workspace_bytes - align_up(pl.ws_bytes, 256),
+                        stream);
+  }
+  return rc;
+}

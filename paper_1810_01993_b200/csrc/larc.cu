@@ -1,0 +1,125 @@
+// LARC layer-wise rate control + SGD momentum over all parameter tensors
+// (pkg/src/deskdl/optimizer.py:48-83, applied per tensor by trainer.py:364-367).
+//
+// Launch 1: per-(tensor, slice) partial sums of w^2 and g^2 (fp64 accumulation).
+// Launch 2: one warp per tensor folds its partials in a fixed order, applies the
+//           zero-norm / eps rules and the trust-ratio clip, writes lr_t.
+// Launch 3: m = beta*m + s*g + wd*w ; w -= lr_t * m   (s = grad_scale = 1/P)
+// The reference raises FloatingPointError on a non-finite norm; here a device
+// status word is set and launch 3 leaves every tensor untouched.
+#include <algorithm>
+
+#include "internal.h"
+
+namespace b2 {
+
+constexpr int LARC_SLICES = 32;
+
+__global__ void k_larc_norms(const float* __restrict__ w, const float* __restrict__ g,
+                             const int64_t* __restrict__ off, double* __restrict__ part) {
+  const int t = blockIdx.y;
+  const int64_t lo = off[t], hi = off[t + 1];
+  double sw = 0.0, sg = 0.0;
+  for (int64_t i = lo + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < hi;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double a = w[i], b = g[i];
+    sw += a * a;
+    sg += b * b;
+  }
+  __shared__ double rw[32], rg[32];
+  for (int o = 16; o > 0; o >>= 1) {
+    sw += __shfl_xor_sync(0xffffffffu, sw, o);
+    sg += __shfl_xor_sync(0xffffffffu, sg, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    rw[threadIdx.x >> 5] = sw;
+    rg[threadIdx.x >> 5] = sg;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int k = 0; k < static_cast<int>(blockDim.x >> 5); ++k) {
+      a += rw[k];
+      b += rg[k];
+    }
+    part[(static_cast<int64_t>(t) * gridDim.x + blockIdx.x) * 2 + 0] = a;
+    part[(static_cast<int64_t>(t) * gridDim.x + blockIdx.x) * 2 + 1] = b;
+  }
+}
+
+__global__ void k_larc_rates(const double* __restrict__ part, int ntensors, int slices, float lr, float trust,
+                             float wd, float eps, float grad_scale, float* __restrict__ lr_out,
+                             int* __restrict__ status) {
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= ntensors) return;
+  double a = 0.0, b = 0.0;
+  if (lane == 0) {
+    for (int k = 0; k < slices; ++k) {
+      a += part[(static_cast<int64_t>(t) * slices + k) * 2 + 0];
+      b += part[(static_cast<int64_t>(t) * slices + k) * 2 + 1];
+    }
+    // norms rounded to fp32 like np.linalg.norm on float32 arrays (optimizer.py:54-55)
+    const float wn = static_cast<float>(sqrt(a));
+    const float gn = static_cast<float>(sqrt(b) * static_cast<double>(grad_scale));
+    float r;
+    if (!isfinite(wn) || !isfinite(gn)) {
+      atomicExch(status, 1);
+      r = 0.f;
+    } else if (wn == 0.f) {
+      r = lr;
+    } else {
+      // python-float (fp64) scalar arithmetic as in optimizer.py:58-63
+      const double denom = static_cast<double>(gn) + static_cast<double>(wd) * wn;
+      if (denom < static_cast<double>(eps))
+        r = lr;
+      else
+        r = static_cast<float>(fmin(static_cast<double>(trust) * wn / denom, static_cast<double>(lr)));
+    }
+    lr_out[t] = r;
+  }
+}
+
+__global__ void k_larc_apply(float* __restrict__ w, float* __restrict__ m, const float* __restrict__ g,
+                             const int64_t* __restrict__ off, const float* __restrict__ lr_t, float beta, float wd,
+                             float grad_scale, const int* __restrict__ status) {
+  if (*status) return;
+  const int t = blockIdx.y;
+  const int64_t lo = off[t], hi = off[t + 1];
+  const float r = lr_t[t];
+  for (int64_t i = lo + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < hi;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float mv = m[i] * beta;          // m *= beta
+    mv += g[i] * grad_scale;         // m += g
+    const float wv = w[i];
+    if (wd != 0.f) mv += wd * wv;    // m += wd * w
+    m[i] = mv;
+    w[i] = wv - r * mv;              // w -= f32(lr_eff) * m
+  }
+}
+
+}  // namespace b2
+
+using namespace b2;
+
+extern "C" size_t b2dl_larc_workspace_size(int64_t total_elems, int ntensors) {
+  (void)total_elems;
+  return static_cast<size_t>(ntensors) * LARC_SLICES * 2 * sizeof(double) + 256;
+}
+
+extern "C" int b2dl_larc_update(const b2dl_larc_args* a, void* stream) {
+  if (!a || !a->w || !a->m || !a->g || !a->offsets || a->ntensors < 1 || !a->lr_out || !a->status)
+    return B2DL_E_VALUE;
+  if (a->workspace_bytes < b2dl_larc_workspace_size(0, a->ntensors)) return B2DL_E_VALUE;
+  cudaStream_t st = as_stream(stream);
+  double* part = reinterpret_cast<double*>(a->workspace);
+  cudaMemsetAsync(a->status, 0, sizeof(int), st);
+  dim3 grid(LARC_SLICES, a->ntensors);
+  k_larc_norms<<<grid, 256, 0, st>>>(a->w, a->g, a->offsets, part);
+  const int warps_per_block = 8;
+  k_larc_rates<<<(a->ntensors + warps_per_block - 1) / warps_per_block, 32 * warps_per_block, 0, st>>>(
+      part, a->ntensors, LARC_SLICES, a->lr, a->trust, a->weight_decay, a->eps, a->grad_scale, a->lr_out, a->status);
+  k_larc_apply<<<grid, 256, 0, st>>>(a->w, a->m, a->g, a->offsets, a->lr_out, a->momentum, a->weight_decay,
+                                     a->grad_scale, a->status);
+  return check_launch();
+}

@@ -1,0 +1,182 @@
+"""Torch-tensor front end of the NHWC fast path (device memory via torch, compute via libb2dl).
+
+torch is plumbing here: it allocates device buffers and supplies the current
+CUDA stream.  Every arithmetic operation below is a launch of a kernel in
+libb2dl.so through its C ABI (include/b2dl.h).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from ._lib import LIB, NULL_ACT, Act, ConvArgs, LarcArgs, WgradArgs, check
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+@dataclass
+class View:
+    """Channel slice [c_off, c_off + c) of an NHWC buffer `buf` [N, H, W, C_total]."""
+    buf: torch.Tensor
+    c_off: int = 0
+    c: int = -1
+
+    def __post_init__(self):
+        if self.buf.dim() != 4:
+            raise ValueError("NHWC buffer must be 4-D")
+        if self.c < 0:
+            self.c = self.buf.shape[3] - self.c_off
+        if self.c_off + self.c > self.buf.shape[3]:
+            raise ValueError("view exceeds buffer channels")
+
+    @property
+    def shape(self):
+        n, h, w, _ = self.buf.shape
+        return (n, h, w, self.c)
+
+    def act(self) -> Act:
+        n, h, w, cs = self.buf.shape
+        ptr = self.buf.data_ptr() + self.c_off * self.buf.element_size()
+        return Act(ptr, n, h, w, self.c, cs)
+
+    def tensor(self) -> torch.Tensor:
+        return self.buf[..., self.c_off:self.c_off + self.c]
+
+
+def _act(v):
+    return NULL_ACT if v is None else v.act()
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def cin_pad(cin: int) -> int:
+    return LIB.b2dl_cin_pad(cin)
+
+
+def same_pads(k: int, d: int):
+    """TF 'same' split (_kernels_py.py:18-21): before = total // 2."""
+    total = (k - 1) * d
+    return total // 2, total - total // 2
+
+
+def conv_fprop(x: View, w_packed: torch.Tensor, cout: int, kh: int, kw: int, dilation: int,
+               y: View, bias=None, residual: View | None = None, relu=False, accumulate=False,
+               mask: View | None = None, y_f32=False, pads=None, block_n=0):
+    pt, pl = pads if pads is not None else (same_pads(kh, dilation)[0], same_pads(kw, dilation)[0])
+    a = ConvArgs(x.act(), ctypes.c_void_p(w_packed.data_ptr()), cout, kh, kw, dilation, pt, pl,
+                 y.act(), int(y_f32), _ptr(bias), _act(residual), int(relu), int(accumulate),
+                 _act(mask), block_n)
+    check(LIB.b2dl_conv_fprop(ctypes.byref(a), _stream()), "conv_fprop")
+
+
+def conv_dgrad(dy: View, w_dgrad: torch.Tensor, cin: int, kh: int, kw: int, dilation: int,
+               dx: View, accumulate=False, mask: View | None = None, dx_f32=False):
+    """Input gradient as a forward conv over dy with tap-flipped weights and 'after' pads."""
+    pads = (same_pads(kh, dilation)[1], same_pads(kw, dilation)[1])
+    conv_fprop(dy, w_dgrad, cin, kh, kw, dilation, dx, accumulate=accumulate, mask=mask,
+               y_f32=dx_f32, pads=pads)
+
+
+class Workspace:
+    """Grow-only device scratch buffer shared by the launches of one stream."""
+
+    def __init__(self, device="cuda"):
+        self.device = device
+        self.buf = torch.empty(0, dtype=torch.uint8, device=device)
+
+    def get(self, nbytes: int) -> torch.Tensor:
+        if self.buf.numel() < nbytes:
+            self.buf = torch.empty(int(nbytes * 1.25) + 4096, dtype=torch.uint8, device=self.device)
+        return self.buf
+
+
+def conv_wgrad(x: View, dy: View, kh: int, kw: int, dilation: int, dw: torch.Tensor,
+               ws: Workspace, bias_grad=None, accumulate=False, splits=0):
+    """dw fp32 HWIO [kh*kw][cin][cout] (+)= x^T dy per tap; bias_grad[cout] (+)= sum dy."""
+    pt, pl = same_pads(kh, dilation)[0], same_pads(kw, dilation)[0]
+    a = WgradArgs(x.act(), dy.act(), kh, kw, dilation, pt, pl, ctypes.c_void_p(dw.data_ptr()),
+                  _ptr(bias_grad), int(accumulate), None, 0, splits)
+    need = LIB.b2dl_wgrad_workspace_size(ctypes.byref(a))
+    buf = ws.get(need)
+    a.workspace = ctypes.c_void_p(buf.data_ptr())
+    a.workspace_bytes = buf.numel()
+    check(LIB.b2dl_conv_wgrad(ctypes.byref(a), _stream()), "conv_wgrad")
+
+
+def pack_weights(w_hwio: torch.Tensor, kh: int, kw: int, cin: int, cout: int, fprop=None, dgrad=None):
+    check(LIB.b2dl_pack_weights(ctypes.c_void_p(w_hwio.data_ptr()), kh, kw, cin, cout,
+                                _ptr(fprop), _ptr(dgrad), _stream()), "pack_weights")
+
+
+def nchw_to_nhwc(x: torch.Tensor, y: View):
+    check(LIB.b2dl_nchw_to_nhwc(ctypes.c_void_p(x.data_ptr()), y.act(), _stream()), "nchw_to_nhwc")
+
+
+def nhwc_to_nchw(x: View, y: torch.Tensor, src_f32=False):
+    check(LIB.b2dl_nhwc_to_nchw(x.act(), int(src_f32), ctypes.c_void_p(y.data_ptr()), _stream()),
+          "nhwc_to_nchw")
+
+
+def avgpool_fwd(x: View, y: View, k: int):
+    check(LIB.b2dl_avgpool_fwd(x.act(), y.act(), k, _stream()), "avgpool_fwd")
+
+
+def avgpool_bwd(dy: View, dx: View, k: int, accumulate=False, mask: View | None = None):
+    check(LIB.b2dl_avgpool_bwd(dy.act(), dx.act(), k, int(accumulate), _act(mask), _stream()),
+          "avgpool_bwd")
+
+
+def upsample_fwd(x: View, y: View, f: int):
+    check(LIB.b2dl_upsample_fwd(x.act(), y.act(), f, _stream()), "upsample_fwd")
+
+
+def upsample_bwd(dy: View, dx: View, f: int, accumulate=False, mask: View | None = None):
+    check(LIB.b2dl_upsample_bwd(dy.act(), dx.act(), f, int(accumulate), _act(mask), _stream()),
+          "upsample_bwd")
+
+
+def add(x: View, y: View, accumulate=True, mask: View | None = None):
+    check(LIB.b2dl_add(x.act(), y.act(), int(accumulate), _act(mask), _stream()), "add")
+
+
+def relu_mask(g: View, act: View):
+    check(LIB.b2dl_relu_mask(g.act(), act.act(), _stream()), "relu_mask")
+
+
+def bias_grad(g: View, out: torch.Tensor, ws: Workspace, accumulate=False):
+    a = g.act()
+    need = LIB.b2dl_bias_grad_workspace_size(a)
+    buf = ws.get(need)
+    check(LIB.b2dl_bias_grad(a, ctypes.c_void_p(out.data_ptr()), int(accumulate),
+                             ctypes.c_void_p(buf.data_ptr()), buf.numel(), _stream()), "bias_grad")
+
+
+def wce(logits: View, labels: torch.Tensor, class_weights: torch.Tensor, loss_out: torch.Tensor,
+        counts: torch.Tensor, dlogits: View, pred: torch.Tensor | None, ws: Workspace):
+    n, h, w, c = logits.shape
+    need = LIB.b2dl_wce_workspace_size(n, h, w, c)
+    buf = ws.get(need)
+    check(LIB.b2dl_wce(logits.act(), ctypes.c_void_p(labels.data_ptr()),
+                       ctypes.c_void_p(class_weights.data_ptr()), c,
+                       ctypes.c_void_p(loss_out.data_ptr()), ctypes.c_void_p(counts.data_ptr()),
+                       dlogits.act(), _ptr(pred), ctypes.c_void_p(buf.data_ptr()), buf.numel(),
+                       _stream()), "wce")
+
+
+def larc_update(w: torch.Tensor, m: torch.Tensor, g: torch.Tensor, offsets: torch.Tensor,
+                lr: float, momentum: float, trust: float, weight_decay: float, eps: float,
+                grad_scale: float, lr_out: torch.Tensor, status: torch.Tensor, ws: Workspace):
+    nt = offsets.numel() - 1
+    need = LIB.b2dl_larc_workspace_size(w.numel(), nt)
+    buf = ws.get(need)
+    a = LarcArgs(w.data_ptr(), m.data_ptr(), g.data_ptr(), offsets.data_ptr(), nt, lr, momentum,
+                 trust, weight_decay, eps, grad_scale, lr_out.data_ptr(), status.data_ptr(),
+                 buf.data_ptr(), buf.numel())
+    check(LIB.b2dl_larc_update(ctypes.byref(a), _stream()), "larc_update")

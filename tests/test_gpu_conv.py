@@ -1,0 +1,110 @@
+"""tcgen05 implicit-GEMM convolution vs an fp64 reference on bf16-rounded operands.
+
+The kernels compute bf16 x bf16 -> fp32; rounding the operands to bf16 first
+leaves only accumulation-order and output-rounding error, so the tolerance is
+tight (2e-3 relative, max-abs over max-abs as in the reference's tests,
+pkg/tests/test_kernels.py:17-19).
+"""
+
+import pytest
+import torch
+import torch.nn.functional as F
+
+pytestmark = pytest.mark.gpu
+
+CASES = [
+    # n, cin, h, w, cout, k, dilation
+    (1, 64, 16, 32, 64, 3, 1),
+    (2, 128, 24, 48, 256, 3, 2),
+    (2, 64, 18, 12, 64, 3, 12),
+    (2, 256, 16, 16, 512, 1, 1),
+    (1, 16, 32, 32, 64, 7, 1),
+    (1, 304, 16, 16, 256, 3, 1),
+    (2, 256, 16, 16, 3, 1, 1),
+    (1, 64, 8, 8, 48, 1, 1),
+    (1, 256, 36, 24, 256, 3, 4),
+    (2, 128, 9, 13, 128, 3, 1),
+]
+
+
+def _rel(a, b):
+    return float((a.double() - b.double()).abs().max() / b.double().abs().max().clamp_min(1e-30))
+
+
+def _bf(t):
+    return t.to(torch.bfloat16).to(torch.float64)
+
+
+def _ref_conv(x, w, d):
+    k = w.shape[2]
+    p = (k - 1) * d // 2
+    return F.conv2d(x, w, padding=p, dilation=d)
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_conv2d_forward_nchw(case):
+    from paper_1810_01993_b200.backend import conv2d_forward_device
+    n, cin, h, w, cout, k, d = case
+    g = torch.Generator(device="cuda").manual_seed(1)
+    x = torch.randn(n, cin, h, w, device="cuda", generator=g)
+    wt = torch.randn(cout, cin, k, k, device="cuda", generator=g) / (cin * k * k) ** 0.5
+    y = conv2d_forward_device(x, wt, dilation=d)
+    ref = _ref_conv(_bf(x), _bf(wt), d)
+    assert y.shape == ref.shape
+    assert _rel(y, ref) < 2e-3, case
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_conv2d_backward_input_nchw(case):
+    from paper_1810_01993_b200.backend import conv2d_backward_input_device
+    n, cin, h, w, cout, k, d = case
+    g = torch.Generator(device="cuda").manual_seed(2)
+    dy = torch.randn(n, cout, h, w, device="cuda", generator=g)
+    wt = torch.randn(cout, cin, k, k, device="cuda", generator=g)
+    dx = conv2d_backward_input_device(dy, wt, (n, cin, h, w), dilation=d)
+    xr = torch.zeros(n, cin, h, w, dtype=torch.float64, device="cuda", requires_grad=True)
+    _ref_conv(xr, _bf(wt), d).backward(_bf(dy))
+    assert _rel(dx, xr.grad) < 2e-3, case
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_conv2d_backward_weights_nchw(case):
+    from paper_1810_01993_b200.backend import conv2d_backward_weights_device
+    n, cin, h, w, cout, k, d = case
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.randn(n, cin, h, w, device="cuda", generator=g)
+    dy = torch.randn(n, cout, h, w, device="cuda", generator=g)
+    dw = conv2d_backward_weights_device(x, dy, (cout, cin, k, k), dilation=d)
+    wr = torch.zeros(cout, cin, k, k, dtype=torch.float64, device="cuda", requires_grad=True)
+    _ref_conv(_bf(x), wr, d).backward(_bf(dy))
+    assert _rel(dw, wr.grad) < 2e-3, case
+
+
+def test_fprop_fused_epilogue():
+    """bias + residual + relu, then accumulate + mask, on channel-slice views."""
+    from paper_1810_01993_b200 import nhwc
+    torch.manual_seed(0)
+    n, h, w, cin, cout = 2, 16, 32, 128, 128
+    xb = torch.randn(n, h, w, cin + 64, device="cuda").to(torch.bfloat16)
+    x = nhwc.View(xb, 64, cin)
+    w_hwio = torch.randn(9, cin, cout, device="cuda") / (9 * cin) ** 0.5
+    wp = torch.empty(cout, 9, nhwc.cin_pad(cin), dtype=torch.bfloat16, device="cuda")
+    nhwc.pack_weights(w_hwio, 3, 3, cin, cout, fprop=wp)
+    bias = torch.randn(cout, device="cuda")
+    res = torch.randn(n, h, w, cout, device="cuda").to(torch.bfloat16)
+    yb = torch.zeros(n, h, w, cout + 64, dtype=torch.bfloat16, device="cuda")
+    y = nhwc.View(yb, 64, cout)
+    nhwc.conv_fprop(x, wp, cout, 3, 3, 1, y, bias=bias, residual=nhwc.View(res), relu=True)
+    xr = x.tensor().double().permute(0, 3, 1, 2)
+    wr = w_hwio.to(torch.bfloat16).double().reshape(3, 3, cin, cout).permute(3, 2, 0, 1)
+    ref = F.conv2d(xr, wr, padding=1) + bias.double()[None, :, None, None]
+    ref = torch.relu(ref + res.double().permute(0, 3, 1, 2)).permute(0, 2, 3, 1)
+    assert _rel(y.tensor(), ref) < 1e-2
+    assert yb[..., :64].abs().max() == 0  # untouched neighbours of the slice
+    # accumulate + mask
+    mask = torch.randn(n, h, w, cout, device="cuda").to(torch.bfloat16)
+    before = y.tensor().double().clone()
+    nhwc.conv_fprop(x, wp, cout, 3, 3, 1, y, accumulate=True, mask=nhwc.View(mask))
+    conv = F.conv2d(xr, wr, padding=1).permute(0, 2, 3, 1)
+    ref2 = before + torch.where(mask.double() > 0, conv, torch.zeros_like(conv))
+    assert _rel(y.tensor(), ref2) < 1e-2
