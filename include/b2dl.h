@@ -129,8 +129,8 @@ B2DL_API int b2dl_conv_wgrad(const b2dl_wgrad_args* a, void* stream);
 B2DL_API int b2dl_pack_weights(const float* w_hwio, int kh, int kw, int cin, int cout, void* fprop_packed,
                       void* dgrad_packed, void* stream);
 
-/* NCHW fp32 -> NHWC bf16 view (input tiles, reference-layout tensors). */
-B2DL_API int b2dl_nchw_to_nhwc(const float* x, b2dl_act y, void* stream);
+/* NCHW fp32 -> NHWC view, bf16 (or fp32 when dst_f32) (input tiles, reference-layout tensors). */
+B2DL_API int b2dl_nchw_to_nhwc(const float* x, b2dl_act y, int dst_f32, void* stream);
 /* NHWC (bf16, or fp32 when src_f32) view -> NCHW fp32. */
 B2DL_API int b2dl_nhwc_to_nchw(b2dl_act x, int src_f32, float* y, void* stream);
 
@@ -157,8 +157,8 @@ B2DL_API size_t b2dl_bias_grad_workspace_size(b2dl_act g);
  *   pred          argmax over classes, ties to the lowest index (uint8)
  * logits: fp32 NHWC view with `classes` channels; labels uint8 [N*H*W]. */
 B2DL_API int b2dl_wce(b2dl_act logits, const uint8_t* labels, const float* class_weights, int classes, float* loss_out,
-             int* counts, b2dl_act dlogits, uint8_t* pred, void* workspace, size_t workspace_bytes,
-             void* stream);
+             int* counts, b2dl_act dlogits, int dlogits_f32, uint8_t* pred, void* workspace,
+             size_t workspace_bytes, void* stream);
 B2DL_API size_t b2dl_wce_workspace_size(int n, int h, int w, int classes);
 
 /* LARC + SGD momentum over many tensors (optimizer.py:48-83) in two launches:
@@ -179,6 +179,8 @@ typedef struct b2dl_larc_args {
   int* status;     /* device, 1 int */
   void* workspace; /* device scratch */
   size_t workspace_bytes;
+  int mode; /* 0: norms + rates + update; 1: rates only (larc_effective_lr);
+               2: update with the caller's lr_out (sgd_step) */
 } b2dl_larc_args;
 B2DL_API size_t b2dl_larc_workspace_size(int64_t total_elems, int ntensors);
 B2DL_API int b2dl_larc_update(const b2dl_larc_args* a, void* stream);

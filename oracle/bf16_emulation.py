@@ -1,0 +1,76 @@
+"""TEST INFRASTRUCTURE ONLY — CPU emulation of the GPU path's bf16 rounding points.
+
+Runs an op graph with torch autograd in fp32, rounding to bf16 exactly where the
+GPU engine stores tensors: conv weights, every fused-op output activation, and
+every stored activation gradient.  Compares per-tensor gradient error with an
+exact fp32 run, to tell inherent bf16 error from kernel bugs.  The GPU
+parity tests require the GPU's error against the reference to be no worse
+than this ideal bf16-storage implementation's (tests/test_gpu_model.py).
+"""
+import numpy as np
+import torch
+import torch.nn.functional as F
+
+
+class RoundGrad(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x):
+        return x.to(torch.bfloat16).float()
+
+    @staticmethod
+    def backward(ctx, g):
+        return g.to(torch.bfloat16).float()
+
+
+def run(graph, params, x, labels, cw, loss_name, emulate):
+    P = {k: torch.tensor(v, requires_grad=True) for k, v in params.items()}
+    vals = {"x": torch.tensor(x), "labels": torch.tensor(labels.astype(np.int64)), "class_weights": torch.tensor(cw)}
+    vals.update(P)
+    cons = graph.consumers()
+    for nd in graph.nodes:
+        ins = [vals[s] for s in nd.inputs]
+        k, a = nd.kind, nd.attrs
+        if k == "conv2d":
+            w = ins[1].to(torch.bfloat16).float() if emulate else ins[1]
+            xin = ins[0].to(torch.bfloat16).float() if (emulate and nd.inputs[0] == "x") else ins[0]
+            pad = (a["kh"] - 1) * a["dilation"] // 2
+            out = F.conv2d(xin, w, padding=pad, dilation=a["dilation"])
+        elif k == "bias_add":
+            out = ins[0] + ins[1].view(1, -1, 1, 1)
+        elif k == "relu":
+            out = torch.relu(ins[0])
+        elif k == "elementwise":
+            out = ins[0] + ins[1]
+        elif k == "concat":
+            out = torch.cat(ins, 1)
+        elif k == "avgpool":
+            out = F.avg_pool2d(ins[0], a["window"])
+        elif k == "upsample":
+            out = ins[0].repeat_interleave(a["factor"], 2).repeat_interleave(a["factor"], 3)
+        elif k == "softmax_ce":
+            z = ins[0]
+            lab = ins[1]
+            wy = ins[2][lab]
+            logp = torch.log_softmax(z, 1)
+            nll = -logp.gather(1, lab[:, None])[:, 0]
+            n = z.shape[0]
+            out = ((wy * nll).reshape(n, -1).sum(1) / wy.reshape(n, -1).sum(1)).mean()
+        else:
+            raise AssertionError(k)
+        # fused-op boundary = where the GPU stores a bf16 tensor (and its bf16 gradient)
+        boundary = k in ("relu", "avgpool", "upsample") or (
+            k in ("bias_add", "elementwise") and not any(c.kind in ("elementwise", "relu") for c in cons[nd.name])
+            and nd.name != loss_name)
+        if emulate and boundary and k != "softmax_ce":
+            out = RoundGrad.apply(out)
+        vals[nd.name] = out
+    loss = vals[loss_name]
+    loss.backward()
+    return float(loss.detach()), {k: v.grad.numpy() for k, v in P.items()}
+
+
+
+
+def emulated_grads(graph, params, x, labels, cw, loss_name):
+    """(loss, grads) with bf16 storage rounding at the GPU engine's fused-op boundaries."""
+    return run(graph, params, x, labels, cw, loss_name, True)

@@ -54,7 +54,7 @@ class LarcArgs(ctypes.Structure):
                 ("weight_decay", ctypes.c_float), ("eps", ctypes.c_float),
                 ("grad_scale", ctypes.c_float), ("lr_out", ctypes.c_void_p),
                 ("status", ctypes.c_void_p), ("workspace", ctypes.c_void_p),
-                ("workspace_bytes", ctypes.c_size_t)]
+                ("workspace_bytes", ctypes.c_size_t), ("mode", ctypes.c_int)]
 
 
 # every symbol include/b2dl.h declares, with its ctypes signature
@@ -69,7 +69,7 @@ _SIGS = {
     "b2dl_wgrad_workspace_size": (_sz, [ctypes.POINTER(WgradArgs)]),
     "b2dl_conv_wgrad": (_c_int, [ctypes.POINTER(WgradArgs), _vp]),
     "b2dl_pack_weights": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp]),
-    "b2dl_nchw_to_nhwc": (_c_int, [_vp, Act, _vp]),
+    "b2dl_nchw_to_nhwc": (_c_int, [_vp, Act, _c_int, _vp]),
     "b2dl_nhwc_to_nchw": (_c_int, [Act, _c_int, _vp, _vp]),
     "b2dl_avgpool_fwd": (_c_int, [Act, Act, _c_int, _vp]),
     "b2dl_avgpool_bwd": (_c_int, [Act, Act, _c_int, _c_int, Act, _vp]),
@@ -79,7 +79,7 @@ _SIGS = {
     "b2dl_relu_mask": (_c_int, [Act, Act, _vp]),
     "b2dl_bias_grad": (_c_int, [Act, _vp, _c_int, _vp, _sz, _vp]),
     "b2dl_bias_grad_workspace_size": (_sz, [Act]),
-    "b2dl_wce": (_c_int, [Act, _vp, _vp, _c_int, _vp, _vp, Act, _vp, _vp, _sz, _vp]),
+    "b2dl_wce": (_c_int, [Act, _vp, _vp, _c_int, _vp, _vp, Act, _c_int, _vp, _vp, _sz, _vp]),
     "b2dl_wce_workspace_size": (_sz, [_c_int] * 4),
     "b2dl_larc_workspace_size": (_sz, [ctypes.c_int64, _c_int]),
     "b2dl_larc_update": (_c_int, [ctypes.POINTER(LarcArgs), _vp]),

@@ -20,7 +20,7 @@ static int grid1d(long long total, int per_thread = 1) {
 }
 
 // ------------------------------------------------------------------ layout
-__global__ void k_nchw_to_nhwc(const float* __restrict__ x, __nv_bfloat16* __restrict__ y, int n, int c, int h, int w,
+__global__ void k_nchw_to_nhwc(const float* __restrict__ x, void* __restrict__ y, int f32, int n, int c, int h, int w,
                                int cs) {
   // one thread per (n, y, x, channel-pair) reading strided NCHW; fine for input tiles
   const long long hw = static_cast<long long>(h) * w;
@@ -32,7 +32,11 @@ __global__ void k_nchw_to_nhwc(const float* __restrict__ x, __nv_bfloat16* __res
     long long r = i / hw;
     int ch = static_cast<int>(r % c);
     long long img = r / c;
-    y[(img * hw + pix) * cs + ch] = __float2bfloat16_rn(x[i]);
+    const long long d = (img * hw + pix) * cs + ch;
+    if (f32)
+      reinterpret_cast<float*>(y)[d] = x[i];
+    else
+      reinterpret_cast<__nv_bfloat16*>(y)[d] = __float2bfloat16_rn(x[i]);
   }
 }
 __global__ void k_nhwc_to_nchw(const void* __restrict__ x, int f32, float* __restrict__ y, int n, int c, int h, int w,
@@ -258,10 +262,10 @@ using namespace b2;
 #define BF(p) reinterpret_cast<__nv_bfloat16*>(p)
 #define CBF(p) reinterpret_cast<const __nv_bfloat16*>(p)
 
-extern "C" int b2dl_nchw_to_nhwc(const float* x, b2dl_act y, void* stream) {
+extern "C" int b2dl_nchw_to_nhwc(const float* x, b2dl_act y, int dst_f32, void* stream) {
   if (!x || !y.ptr) return B2DL_E_VALUE;
   long long total = static_cast<long long>(y.n) * y.c * y.h * y.w;
-  k_nchw_to_nhwc<<<grid1d(total), 256, 0, as_stream(stream)>>>(x, BF(y.ptr), y.n, y.c, y.h, y.w, y.c_stride);
+  k_nchw_to_nhwc<<<grid1d(total), 256, 0, as_stream(stream)>>>(x, y.ptr, dst_f32, y.n, y.c, y.h, y.w, y.c_stride);
   return check_launch();
 }
 

@@ -175,7 +175,7 @@ extern "C" int b2dl_conv2d_forward(const float* x, const float* w, float* y, int
   void* wp = ws.take(static_cast<size_t>(cout) * taps * b2dl_cin_pad(cin) * 2);
   if (!xb || !yf || !wp) return B2DL_E_VALUE;
   b2dl_act xa = nhwc(xb, n, h, wd, cin);
-  int rc = b2dl_nchw_to_nhwc(x, xa, stream);
+  int rc = b2dl_nchw_to_nhwc(x, xa, 0, stream);
   if (rc) return rc;
   long long tot = static_cast<long long>(cout) * taps * b2dl_cin_pad(cin);
   pack_oihw_fprop<<<grid_for(tot), 256, 0, st>>>(w, reinterpret_cast<__nv_bfloat16*>(wp), cout, cin, taps,
@@ -209,7 +209,7 @@ extern "C" int b2dl_conv2d_backward_input(const float* dy, const float* w, float
   void* wp = ws.take(static_cast<size_t>(cin) * taps * b2dl_cin_pad(cout) * 2);
   if (!dyb || !dxf || !wp) return B2DL_E_VALUE;
   b2dl_act dya = nhwc(dyb, n, h, wd, cout);
-  int rc = b2dl_nchw_to_nhwc(dy, dya, stream);
+  int rc = b2dl_nchw_to_nhwc(dy, dya, 0, stream);
   if (rc) return rc;
   long long tot = static_cast<long long>(cin) * taps * b2dl_cin_pad(cout);
   pack_oihw_dgrad<<<grid_for(tot), 256, 0, st>>>(w, reinterpret_cast<__nv_bfloat16*>(wp), cout, cin, taps,
@@ -244,9 +244,9 @@ extern "C" int b2dl_conv2d_backward_weights(const float* x, const float* dy, flo
   if (!xb || !dyb || !hw) return B2DL_E_VALUE;
   b2dl_act xa = nhwc(xb, n, h, wd, cin);
   b2dl_act dya = nhwc(dyb, n, h, wd, cout);
-  int rc = b2dl_nchw_to_nhwc(x, xa, stream);
+  int rc = b2dl_nchw_to_nhwc(x, xa, 0, stream);
   if (rc) return rc;
-  if ((rc = b2dl_nchw_to_nhwc(dy, dya, stream))) return rc;
+  if ((rc = b2dl_nchw_to_nhwc(dy, dya, 0, stream))) return rc;
   b2dl_wgrad_args a{};
   a.x = xa;
   a.dy = dya;

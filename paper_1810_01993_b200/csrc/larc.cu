@@ -113,12 +113,17 @@ extern "C" int b2dl_larc_update(const b2dl_larc_args* a, void* stream) {
   if (a->workspace_bytes < b2dl_larc_workspace_size(0, a->ntensors)) return B2DL_E_VALUE;
   cudaStream_t st = as_stream(stream);
   double* part = reinterpret_cast<double*>(a->workspace);
+  if (a->mode < 0 || a->mode > 2) return B2DL_E_VALUE;
   cudaMemsetAsync(a->status, 0, sizeof(int), st);
   dim3 grid(LARC_SLICES, a->ntensors);
-  k_larc_norms<<<grid, 256, 0, st>>>(a->w, a->g, a->offsets, part);
-  const int warps_per_block = 8;
-  k_larc_rates<<<(a->ntensors + warps_per_block - 1) / warps_per_block, 32 * warps_per_block, 0, st>>>(
-      part, a->ntensors, LARC_SLICES, a->lr, a->trust, a->weight_decay, a->eps, a->grad_scale, a->lr_out, a->status);
+  if (a->mode != 2) {
+    k_larc_norms<<<grid, 256, 0, st>>>(a->w, a->g, a->offsets, part);
+    const int warps_per_block = 8;
+    k_larc_rates<<<(a->ntensors + warps_per_block - 1) / warps_per_block, 32 * warps_per_block, 0, st>>>(
+        part, a->ntensors, LARC_SLICES, a->lr, a->trust, a->weight_decay, a->eps, a->grad_scale, a->lr_out,
+        a->status);
+  }
+  if (a->mode == 1) return check_launch();
   k_larc_apply<<<grid, 256, 0, st>>>(a->w, a->m, a->g, a->offsets, a->lr_out, a->momentum, a->weight_decay,
                                      a->grad_scale, a->status);
   return check_launch();

@@ -39,7 +39,7 @@ __global__ void k_wce_hist(const uint8_t* __restrict__ labels, long long hw, int
 
 __global__ void k_wce_main(const float* __restrict__ logits, int ls, const uint8_t* __restrict__ labels,
                            const float* __restrict__ cw, const int* __restrict__ counts, long long hw, int classes,
-                           int nimg, __nv_bfloat16* __restrict__ dl, int ds, uint8_t* __restrict__ pred,
+                           int nimg, void* __restrict__ dl, int ds, int dl_f32, uint8_t* __restrict__ pred,
                            double* __restrict__ part) {
   const int img = blockIdx.y;
   __shared__ float s_w[WCE_MAX_CLASSES];
@@ -78,11 +78,13 @@ __global__ void k_wce_main(const float* __restrict__ logits, int ls, const uint8
     const float nll = lse - (zv[y] - mx);
     acc += static_cast<double>(wy) * nll;
     const float gs = wy * scale;
-    __nv_bfloat16* d = dl + p * ds;
     for (int c = 0; c < zero_to; ++c) {
       float g = 0.f;
       if (c < classes) g = (__expf(zv[c] - mx - lse) - (c == y ? 1.f : 0.f)) * gs;
-      d[c] = __float2bfloat16_rn(g);
+      if (dl_f32)
+        reinterpret_cast<float*>(dl)[p * ds + c] = g;
+      else
+        reinterpret_cast<__nv_bfloat16*>(dl)[p * ds + c] = __float2bfloat16_rn(g);
     }
     if (pred) pred[p] = static_cast<uint8_t>(am);
   }
@@ -123,8 +125,8 @@ extern "C" size_t b2dl_wce_workspace_size(int n, int h, int w, int classes) {
 }
 
 extern "C" int b2dl_wce(b2dl_act logits, const uint8_t* labels, const float* class_weights, int classes,
-                        float* loss_out, int* counts, b2dl_act dlogits, uint8_t* pred, void* workspace,
-                        size_t workspace_bytes, void* stream) {
+                        float* loss_out, int* counts, b2dl_act dlogits, int dlogits_f32, uint8_t* pred,
+                        void* workspace, size_t workspace_bytes, void* stream) {
   if (classes < 2 || classes > WCE_MAX_CLASSES || logits.c != classes || dlogits.c != classes) return B2DL_E_VALUE;
   if (!logits.ptr || !labels || !class_weights || !loss_out || !counts || !dlogits.ptr) return B2DL_E_VALUE;
   if (workspace_bytes < b2dl_wce_workspace_size(logits.n, logits.h, logits.w, classes)) return B2DL_E_VALUE;
@@ -138,8 +140,8 @@ extern "C" int b2dl_wce(b2dl_act logits, const uint8_t* labels, const float* cla
   dim3 grid(WCE_BLOCKS_PER_IMG, logits.n);
   k_wce_hist<<<grid, 256, 0, st>>>(labels, hw, classes, counts, err);
   k_wce_main<<<grid, 256, 0, st>>>(reinterpret_cast<const float*>(logits.ptr), logits.c_stride, labels, class_weights,
-                                   counts, hw, classes, logits.n, reinterpret_cast<__nv_bfloat16*>(dlogits.ptr),
-                                   dlogits.c_stride, pred, part);
+                                   counts, hw, classes, logits.n, dlogits.ptr, dlogits.c_stride, dlogits_f32,
+                                   pred, part);
   k_wce_final<<<1, 32, 0, st>>>(part, WCE_BLOCKS_PER_IMG, counts, class_weights, classes, logits.n, loss_out);
   return check_launch();
 }

@@ -1,0 +1,463 @@
+"""Lowering of an op graph to a static schedule of fused sm_100a launches.
+
+The reference executes graphs node by node with a NumPy tape
+(pkg/src/deskdl/model/ops.py:44-106).  Here a graph is planned once per input
+shape:
+
+* fusion      conv2d -> bias_add [-> elementwise add (residual)] [-> relu]
+              becomes ONE tcgen05 implicit-GEMM launch with the bias, residual
+              and relu in its epilogue; the head's bias output is written fp32.
+* concat      zero-copy: producers write straight into channel slices of the
+              concat buffer ("assembling layers in place");
+              gradient buffers alias the same way, so the concat VJP
+              (ops.py:178-182) costs nothing.
+* layout      activations NHWC bf16, gradients NHWC bf16, parameters fp32 in one
+              flat buffer (conv weights HWIO), bf16 packed copies per conv for
+              the fprop and dgrad operands.
+* backward    reverse schedule; each conv: relu VJP (in place), wgrad + bias
+              grad (split-K tcgen05, straight into the flat gradient buffer),
+              dgrad (tcgen05, accumulating into fan-in gradients), residual
+              pass-through.  First contribution to a gradient region
+              overwrites, later ones accumulate (decided at plan time).
+* loss        fused weighted CE writes dlogits into the head's gradient buffer.
+
+Every launch goes through libb2dl.so (nhwc.py); torch only allocates memory.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import nhwc
+from .graph import OpGraph, infer_shapes
+from .nhwc import View
+
+
+def _r8(c: int) -> int:
+    return (c + 7) // 8 * 8
+
+
+@dataclass
+class Op:
+    kind: str                      # conv | pool | up | concat | add | ce
+    out: str
+    ins: tuple
+    nodes: tuple = ()
+    # conv
+    w: str = ""
+    b: str = ""
+    res: str | None = None
+    relu: bool = False
+    k: int = 1
+    dil: int = 1
+    cin: int = 0
+    cout: int = 0
+    # pool / upsample
+    factor: int = 1
+    # concat
+    copy_ins: set = field(default_factory=set)
+
+
+class Plan:
+    """Static fused schedule + buffer layout for one (graph, input shape)."""
+
+    def __init__(self, graph: OpGraph, param_shapes: dict, input_shape: tuple, loss_name: str,
+                 logits_name: str):
+        self.graph = graph
+        self.loss_name, self.logits_name = loss_name, logits_name
+        n, c, h, w = input_shape
+        shapes = dict(param_shapes)
+        shapes.update(x=(n, c, h, w), labels=(n, h, w))
+        cls = graph.node(loss_name).attrs["classes"]
+        shapes["class_weights"] = (cls,)
+        self.classes = cls
+        self.shapes = infer_shapes(graph, shapes)
+        self.params = graph.param_names()
+        self.data_inputs = [k for k, r in graph.inputs.items() if r == "data"]
+        if self.data_inputs != ["x"]:
+            raise NotImplementedError("engine expects exactly one data input named 'x'")
+        self._fuse()
+        self._place()
+        self._liveness()
+
+    # ---------------------------------------------------------------- fusion
+    def _fuse(self):
+        g = self.graph
+        cons = g.consumers()
+        idx = {nd.name: i for i, nd in enumerate(g.nodes)}
+        used = set()
+        ops = []
+        for nd in g.nodes:
+            if nd.name in used:
+                continue
+            if nd.kind == "conv2d":
+                a = nd.attrs
+                if a["stride"] != 1:
+                    raise NotImplementedError("execution kernels support stride 1 only")
+                if a["kh"] != a["kw"]:
+                    raise NotImplementedError("square kernels only")
+                chain = [nd]
+                nxt = cons[nd.name]
+                if len(nxt) != 1 or nxt[0].kind != "bias_add" or nxt[0].inputs[0] != nd.name:
+                    raise NotImplementedError(f"{nd.name}: conv must feed exactly one bias_add")
+                bias = nxt[0]
+                chain.append(bias)
+                cur = bias
+                res = None
+                relu = False
+                nxt = cons[cur.name]
+                if (len(nxt) == 1 and nxt[0].kind == "elementwise" and nxt[0].attrs["fn"] == "add"
+                        and nxt[0].name not in used and cur.name != self.logits_name):
+                    add = nxt[0]
+                    other = [s for s in add.inputs if s != cur.name]
+                    if len(other) == 1:
+                        res = other[0]
+                        chain.append(add)
+                        cur = add
+                        nxt = cons[cur.name]
+                if (len(nxt) == 1 and nxt[0].kind == "relu" and nxt[0].name not in used
+                        and cur.name != self.logits_name):
+                    chain.append(nxt[0])
+                    cur = nxt[0]
+                    relu = True
+                used.update(c.name for c in chain)
+                op = Op("conv", cur.name, (nd.inputs[0],), tuple(c.name for c in chain), w=nd.inputs[1],
+                        b=bias.inputs[1], res=res, relu=relu, k=a["kh"], dil=a["dilation"], cin=a["cin"],
+                        cout=a["cout"])
+                ops.append((idx[cur.name], op))
+            elif nd.kind == "avgpool":
+                ops.append((idx[nd.name], Op("pool", nd.name, nd.inputs, (nd.name,), factor=nd.attrs["window"])))
+            elif nd.kind == "upsample":
+                ops.append((idx[nd.name], Op("up", nd.name, nd.inputs, (nd.name,), factor=nd.attrs["factor"])))
+            elif nd.kind == "concat":
+                if nd.attrs["axis"] != 1:
+                    raise NotImplementedError("channel concat only")
+                ops.append((idx[nd.name], Op("concat", nd.name, nd.inputs, (nd.name,))))
+            elif nd.kind == "elementwise" and nd.attrs["fn"] == "add":
+                ops.append((idx[nd.name], Op("add", nd.name, nd.inputs, (nd.name,))))
+            elif nd.kind == "softmax_ce":
+                if nd.inputs[1:] != ("labels", "class_weights"):
+                    raise NotImplementedError("softmax_ce must read the graph's labels / class_weights")
+                ops.append((idx[nd.name], Op("ce", nd.name, (nd.inputs[0],), (nd.name,))))
+            else:
+                raise NotImplementedError(f"{nd.name}: op kind {nd.kind} has no fused lowering")
+        ops.sort(key=lambda t: t[0])
+        self.ops = [o for _, o in ops]
+        self.producer = {o.out: o for o in self.ops}
+        if self.logits_name not in self.producer or self.producer[self.logits_name].kind != "conv":
+            raise NotImplementedError("logits must be produced by a conv + bias_add")
+
+    # ---------------------------------------------------------------- buffers
+    def chans(self, t):
+        return self.shapes[t][1]
+
+    def _place(self):
+        owner = {}
+        for op in reversed(self.ops):
+            if op.kind != "concat":
+                continue
+            off = 0
+            for s in op.ins:
+                prod = self.producer.get(s)
+                ok = (s not in owner and prod is not None and prod.kind in ("conv", "pool", "up", "concat", "add")
+                      and s != self.logits_name and off % 8 == 0)
+                if ok:
+                    owner[s] = (op.out, off)
+                else:
+                    op.copy_ins.add(s)
+                off += self.chans(s)
+        self.view_of = {}
+        self.buffers = {}
+
+        def resolve(t):
+            if t in self.view_of:
+                return self.view_of[t]
+            if t in owner:
+                par, off = owner[t]
+                root, poff = resolve(par)
+                r = (root, poff + off)
+            else:
+                r = (t, 0)
+            self.view_of[t] = r
+            return r
+
+        tensors = ["x"] + [o.out for o in self.ops if o.kind != "ce"]
+        for t in tensors:
+            root, _ = resolve(t)
+            n, c, h, w = self.shapes[root]
+            f32 = root == self.logits_name
+            self.buffers[root] = (n, h, w, c if f32 else _r8(c), f32)
+
+    def view_spec(self, t):
+        root, off = self.view_of[t]
+        return root, off, self.chans(t)
+
+    # ---------------------------------------------------------------- gradients
+    def _liveness(self):
+        live = set(self.params)
+        for op in self.ops:
+            if op.kind == "conv":
+                srcs = [op.ins[0], op.w, op.b] + ([op.res] if op.res else [])
+            else:
+                srcs = list(op.ins)
+            if any(s in live for s in srcs):
+                live.add(op.out)
+        self.live = live
+        self.grad_buffers = {}
+        for t in live:
+            if t in self.view_of:
+                root = self.view_of[t][0]
+                n, h, w, _, _ = self.buffers[root]
+                self.grad_buffers[root] = (n, h, w, _r8(self.chans(root)))
+        # static backward program with overwrite/accumulate decided per contribution
+        init = {root: [] for root in self.grad_buffers}
+
+        def claim(t):
+            root, off, c = self.view_spec(t)
+            iv = init[root]
+            lo, hi = off, off + c
+            covered = sum(max(0, min(hi, b) - max(lo, a)) for a, b in iv)
+            if covered == 0:
+                iv.append((lo, hi))
+                return False
+            if covered == hi - lo:
+                return True
+            raise NotImplementedError(f"partially initialised gradient region for {t}")
+
+        def inited(t):
+            root, off, c = self.view_spec(t)
+            return sum(max(0, min(off + c, b) - max(off, a)) for a, b in init[root]) > 0
+
+        prog = []
+        ce = [o for o in self.ops if o.kind == "ce"]
+        if len(ce) != 1 or ce[0].ins[0] != self.logits_name:
+            raise NotImplementedError("exactly one softmax_ce on the logits")
+        claim(self.logits_name)                       # written by the fused CE in forward
+        for op in reversed(self.ops):
+            if op.kind == "ce" or op.out not in self.live:
+                continue
+            if not inited(op.out):
+                raise NotImplementedError(f"{op.out}: live tensor without gradient contributions")
+            if op.kind == "conv":
+                x, res = op.ins[0], op.res
+                step = {"op": op, "dx": None, "dres": None}
+                if x in self.live:
+                    step["dx"] = claim(x)
+                if res is not None and res in self.live:
+                    step["dres"] = claim(res)
+                prog.append(step)
+            elif op.kind in ("pool", "up"):
+                x = op.ins[0]
+                if x in self.live:
+                    prog.append({"op": op, "dx": claim(x)})
+            elif op.kind == "concat":
+                # aliased inputs share the gradient region; copied inputs get the slice added
+                step = {"op": op, "copies": []}
+                off = 0
+                for s in op.ins:
+                    if s in op.copy_ins and s in self.live:
+                        step["copies"].append((s, off, claim(s)))
+                    off += self.chans(s)
+                prog.append(step)
+            elif op.kind == "add":
+                prog.append({"op": op, "acc": [(s, claim(s)) for s in op.ins if s in self.live]})
+        self.backward_program = prog
+
+
+class Engine:
+    """Device state + launches for one model at one input shape."""
+
+    def __init__(self, graph: OpGraph, params: dict, param_order, input_shape, loss_name, logits_name,
+                 device="cuda"):
+        self.device = torch.device(device)
+        self.order = list(param_order)
+        self.plan = Plan(graph, {k: v.shape for k, v in params.items()}, tuple(input_shape), loss_name,
+                         logits_name)
+        p = self.plan
+        self.ws = nhwc.Workspace(self.device)
+        bf, f32 = torch.bfloat16, torch.float32
+        self.act = {r: torch.empty((n, h, w, c), dtype=f32 if isf else bf, device=self.device)
+                    for r, (n, h, w, c, isf) in p.buffers.items()}
+        self.grad = {r: torch.empty(s, dtype=bf, device=self.device) for r, s in p.grad_buffers.items()}
+        # flat fp32 parameters / gradients / momentum in param order; conv weights HWIO
+        self.slot = {}
+        off = 0
+        offsets = []
+        for name in self.order:
+            shp = tuple(params[name].shape)
+            offsets.append(off)
+            self.slot[name] = (off, shp)
+            off += (int(np.prod(shp)) + 63) // 64 * 64
+        offsets.append(off)
+        self.numel = off
+        self.flat_w = torch.zeros(off, dtype=f32, device=self.device)
+        self.flat_g = torch.zeros(off, dtype=f32, device=self.device)
+        self.flat_m = torch.zeros(off, dtype=f32, device=self.device)
+        self.offsets = torch.tensor(offsets, dtype=torch.int64, device=self.device)
+        self.convs = [o for o in p.ops if o.kind == "conv"]
+        self.wf, self.wd = {}, {}
+        for o in self.convs:
+            t = o.k * o.k
+            self.wf[o.w] = torch.zeros((o.cout, t, nhwc.cin_pad(o.cin)), dtype=bf, device=self.device)
+            if o.ins[0] in p.live:
+                self.wd[o.w] = torch.zeros((o.cin, t, nhwc.cin_pad(o.cout)), dtype=bf, device=self.device)
+        n, c, h, w = input_shape
+        self.labels = torch.zeros(n * h * w, dtype=torch.uint8, device=self.device)
+        self.pred = torch.zeros(n * h * w, dtype=torch.uint8, device=self.device)
+        self.class_weights = torch.ones(p.classes, dtype=f32, device=self.device)
+        self.loss = torch.zeros(1, dtype=f32, device=self.device)
+        self.counts = torch.zeros(n * p.classes, dtype=torch.int32, device=self.device)
+        self.input_shape = tuple(input_shape)
+        self.launches = 0
+        self.load_params(params)
+
+    # ---------------------------------------------------------------- views
+    def v(self, t) -> View:
+        root, off, c = self.plan.view_spec(t)
+        return View(self.act[root], off, c)
+
+    def gv(self, t) -> View:
+        root, off, c = self.plan.view_spec(t)
+        return View(self.grad[root], off, c)
+
+    def wslice(self, name, buf=None):
+        off, shp = self.slot[name]
+        return (self.flat_w if buf is None else buf)[off:off + int(np.prod(shp))]
+
+    # ---------------------------------------------------------------- params
+    def load_params(self, params: dict):
+        for name in self.order:
+            a = np.asarray(params[name], dtype=np.float32)
+            t = torch.from_numpy(a)
+            if a.ndim == 4:   # OIHW -> HWIO
+                t = t.permute(2, 3, 1, 0).contiguous()
+            self.wslice(name).copy_(t.reshape(-1).to(self.device))
+        self.repack()
+
+    def _export(self, buf) -> dict:
+        out = {}
+        for name in self.order:
+            off, shp = self.slot[name]
+            t = buf[off:off + int(np.prod(shp))]
+            if len(shp) == 4:
+                co, ci, kh, kw = shp
+                t = t.view(kh, kw, ci, co).permute(3, 2, 0, 1)
+            out[name] = t.reshape(shp).cpu().numpy().copy()
+        return out
+
+    def export_params(self) -> dict:
+        return self._export(self.flat_w)
+
+    def export_grads(self) -> dict:
+        return self._export(self.flat_g)
+
+    def repack(self):
+        for o in self.convs:
+            nhwc.pack_weights(self.wslice(o.w), o.k, o.k, o.cin, o.cout, fprop=self.wf[o.w],
+                              dgrad=self.wd.get(o.w))
+            self.launches += 1
+
+    # ---------------------------------------------------------------- inputs
+    def set_batch(self, x_nchw: torch.Tensor, labels: torch.Tensor):
+        """x fp32 NCHW and labels uint8 [N,H,W] already on the device."""
+        if tuple(x_nchw.shape) != self.input_shape:
+            raise ValueError(f"batch {tuple(x_nchw.shape)} does not match planned {self.input_shape}")
+        nhwc.nchw_to_nhwc(x_nchw.contiguous(), self.v("x"))
+        self.labels.copy_(labels.reshape(-1))
+        self.launches += 1
+
+    def set_class_weights(self, w):
+        self.class_weights.copy_(torch.as_tensor(np.asarray(w, dtype=np.float32)))
+
+    # ---------------------------------------------------------------- forward
+    def forward(self):
+        p = self.plan
+        for op in p.ops:
+            if op.kind == "conv":
+                out = op.out
+                b_off, _ = self.slot[op.b]
+                nhwc.conv_fprop(self.v(op.ins[0]), self.wf[op.w], op.cout, op.k, op.k, op.dil, self.v(out),
+                                bias=self.flat_w[b_off:b_off + op.cout],
+                                residual=self.v(op.res) if op.res else None, relu=op.relu,
+                                y_f32=(out == p.logits_name))
+            elif op.kind == "pool":
+                nhwc.avgpool_fwd(self.v(op.ins[0]), self.v(op.out), op.factor)
+            elif op.kind == "up":
+                nhwc.upsample_fwd(self.v(op.ins[0]), self.v(op.out), op.factor)
+            elif op.kind == "concat":
+                off = 0
+                for s in op.ins:
+                    if s in op.copy_ins:
+                        root, coff, c = p.view_spec(op.out)
+                        nhwc.add(self.v(s), View(self.act[root], coff + off, self.plan.chans(s)),
+                                 accumulate=False)
+                        self.launches += 1
+                    off += self.plan.chans(s)
+                continue
+            elif op.kind == "add":
+                a, b = op.ins
+                nhwc.add(self.v(a), self.v(op.out), accumulate=False)
+                nhwc.add(self.v(b), self.v(op.out), accumulate=True)
+                self.launches += 1
+            elif op.kind == "ce":
+                nhwc.wce(self.v(op.ins[0]), self.labels, self.class_weights, self.loss, self.counts,
+                         self.gv(op.ins[0]), self.pred, self.ws)
+                self.launches += 2
+            self.launches += 1
+
+    # ---------------------------------------------------------------- backward
+    def backward(self, on_param_ready=None):
+        """Fill flat_g with d loss / d params (param layout HWIO for conv weights).
+
+        `on_param_ready(name)` fires as soon as a parameter's gradient has been
+        enqueued, so the trainer can start bucket all-reduces during backward."""
+        for st in self.plan.backward_program:
+            op = st["op"]
+            if op.kind == "conv":
+                gy = self.gv(op.out)
+                if op.relu:
+                    nhwc.relu_mask(gy, self.v(op.out))
+                    self.launches += 1
+                w_off, _ = self.slot[op.w]
+                b_off, _ = self.slot[op.b]
+                nhwc.conv_wgrad(self.v(op.ins[0]), gy, op.k, op.k, op.dil,
+                                self.flat_g[w_off:], self.ws, bias_grad=self.flat_g[b_off:b_off + op.cout])
+                self.launches += 4
+                if on_param_ready is not None:
+                    on_param_ready(op.w)
+                    on_param_ready(op.b)
+                if st["dx"] is not None:
+                    nhwc.conv_dgrad(gy, self.wd[op.w], op.cin, op.k, op.k, op.dil, self.gv(op.ins[0]),
+                                    accumulate=st["dx"])
+                    self.launches += 1
+                if st["dres"] is not None:
+                    nhwc.add(gy, self.gv(op.res), accumulate=st["dres"])
+                    self.launches += 1
+            elif op.kind == "pool":
+                nhwc.avgpool_bwd(self.gv(op.out), self.gv(op.ins[0]), op.factor, accumulate=st["dx"])
+                self.launches += 1
+            elif op.kind == "up":
+                nhwc.upsample_bwd(self.gv(op.out), self.gv(op.ins[0]), op.factor, accumulate=st["dx"])
+                self.launches += 1
+            elif op.kind == "concat":
+                root, coff, _ = self.plan.view_spec(op.out)
+                for s, off, acc in st["copies"]:
+                    nhwc.add(View(self.grad[root], coff + off, self.plan.chans(s)), self.gv(s), accumulate=acc)
+                    self.launches += 1
+            elif op.kind == "add":
+                for s, acc in st["acc"]:
+                    nhwc.add(self.gv(op.out), self.gv(s), accumulate=acc)
+                    self.launches += 1
+
+    def logits_nchw(self) -> torch.Tensor:
+        n, c, h, w = self.plan.shapes[self.plan.logits_name]
+        out = torch.empty((n, c, h, w), dtype=torch.float32, device=self.device)
+        nhwc.nhwc_to_nchw(self.v(self.plan.logits_name), out, src_f32=True)
+        return out
+
+    def predictions(self) -> torch.Tensor:
+        n, _, h, w = self.input_shape
+        return self.pred.view(n, h, w)

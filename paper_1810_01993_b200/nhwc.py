@@ -115,8 +115,9 @@ def pack_weights(w_hwio: torch.Tensor, kh: int, kw: int, cin: int, cout: int, fp
                                 _ptr(fprop), _ptr(dgrad), _stream()), "pack_weights")
 
 
-def nchw_to_nhwc(x: torch.Tensor, y: View):
-    check(LIB.b2dl_nchw_to_nhwc(ctypes.c_void_p(x.data_ptr()), y.act(), _stream()), "nchw_to_nhwc")
+def nchw_to_nhwc(x: torch.Tensor, y: View, dst_f32=False):
+    check(LIB.b2dl_nchw_to_nhwc(ctypes.c_void_p(x.data_ptr()), y.act(), int(dst_f32), _stream()),
+          "nchw_to_nhwc")
 
 
 def nhwc_to_nchw(x: View, y: torch.Tensor, src_f32=False):
@@ -159,24 +160,24 @@ def bias_grad(g: View, out: torch.Tensor, ws: Workspace, accumulate=False):
 
 
 def wce(logits: View, labels: torch.Tensor, class_weights: torch.Tensor, loss_out: torch.Tensor,
-        counts: torch.Tensor, dlogits: View, pred: torch.Tensor | None, ws: Workspace):
+        counts: torch.Tensor, dlogits: View, pred: torch.Tensor | None, ws: Workspace, dlogits_f32=False):
     n, h, w, c = logits.shape
     need = LIB.b2dl_wce_workspace_size(n, h, w, c)
     buf = ws.get(need)
     check(LIB.b2dl_wce(logits.act(), ctypes.c_void_p(labels.data_ptr()),
                        ctypes.c_void_p(class_weights.data_ptr()), c,
                        ctypes.c_void_p(loss_out.data_ptr()), ctypes.c_void_p(counts.data_ptr()),
-                       dlogits.act(), _ptr(pred), ctypes.c_void_p(buf.data_ptr()), buf.numel(),
+                       dlogits.act(), int(dlogits_f32), _ptr(pred), ctypes.c_void_p(buf.data_ptr()), buf.numel(),
                        _stream()), "wce")
 
 
 def larc_update(w: torch.Tensor, m: torch.Tensor, g: torch.Tensor, offsets: torch.Tensor,
                 lr: float, momentum: float, trust: float, weight_decay: float, eps: float,
-                grad_scale: float, lr_out: torch.Tensor, status: torch.Tensor, ws: Workspace):
+                grad_scale: float, lr_out: torch.Tensor, status: torch.Tensor, ws: Workspace, mode=0):
     nt = offsets.numel() - 1
     need = LIB.b2dl_larc_workspace_size(w.numel(), nt)
     buf = ws.get(need)
     a = LarcArgs(w.data_ptr(), m.data_ptr(), g.data_ptr(), offsets.data_ptr(), nt, lr, momentum,
                  trust, weight_decay, eps, grad_scale, lr_out.data_ptr(), status.data_ptr(),
-                 buf.data_ptr(), buf.numel())
+                 buf.data_ptr(), buf.numel(), mode)
     check(LIB.b2dl_larc_update(ctypes.byref(a), _stream()), "larc_update")

@@ -1,0 +1,271 @@
+"""Synchronous data-parallel training step (pkg/src/deskdl/harness/trainer.py:343-421), B200-native.
+
+One process per GPU (torchrun), NCCL over NVLink/NVSwitch for the gradient
+exchange.  Per step and rank:
+  batch -> forward (fused convs + fused weighted CE) -> backward
+  -> bucketed all-reduce(sum) of the flat fp32 gradient buffer, issued per
+     bucket while backward is still running (buckets in reverse parameter
+     order; each fires when the wgrad of its last parameter is enqueued)
+  -> multi-tensor LARC + momentum update with the 1/P mean folded in
+  -> repack bf16 operand copies of the weights.
+Lag 1 applies the previous step's reduced gradients (trainer.py:378-383,
+403-405); the current reduction then overlaps the next step's compute.
+
+The reference's control plane (readiness tree, control_plane.py) only exists to
+give every rank the same collective order; here the bucket order is static, so
+the order is identical by construction.  NCCL results are bitwise identical on
+all ranks, which the step-{1,10,end} weight digests check (trainer.py:263-315).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import nhwc
+from .flops import count_graph, train_flops_per_sample
+from .loss import ClassWeights, uniform_weights
+from .models import NetConfig
+from .net import SegmentationNet
+from .optimizer import OptimConfig
+from .scenes import SceneConfig, generated_batch
+from .stats import StepRecord, sustained_stats
+
+
+class TrainingError(Exception):
+    pass
+
+
+def param_digest(params: dict, order) -> str:
+    """SHA-256 over (name, shape, fp32 bytes) in parameter order (trainer.py:263-270)."""
+    h = hashlib.sha256()
+    for name in order:
+        v = np.ascontiguousarray(params[name], dtype=np.float32)
+        h.update(name.encode())
+        h.update(str(v.shape).encode())
+        h.update(v.tobytes())
+    return h.hexdigest()
+
+
+class DataParallelTrainer:
+    def __init__(self, net: SegmentationNet, optim: OptimConfig, input_shape, lag: int = 0,
+                 class_weights=None, bucket_mb: float = 32.0, group=None):
+        if lag not in (0, 1):
+            raise ValueError("lag must be 0 or 1")
+        self.net = net
+        self.optim = optim
+        self.lag = lag
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+        self.eng = net.engine(input_shape)
+        eng = self.eng
+        cw = uniform_weights(net.cfg.classes) if class_weights is None else class_weights
+        eng.set_class_weights(cw)
+        self.ntensors = len(net.param_order)
+        self.lr_out = torch.zeros(self.ntensors, dtype=torch.float32, device=eng.device)
+        self.status = torch.zeros(1, dtype=torch.int32, device=eng.device)
+        self.g_other = torch.zeros_like(eng.flat_g) if lag == 1 else None
+        self.have_prev = False
+        # buckets: contiguous parameter ranges, formed from the end of param order
+        limit = int(bucket_mb * 2 ** 20 / 4)
+        self.buckets = []
+        cur, size = [], 0
+        for name in reversed(net.param_order):
+            cur.append(name)
+            size += int(np.prod(eng.slot[name][1]))
+            if size >= limit:
+                self.buckets.append(cur)
+                cur, size = [], 0
+        if cur:
+            self.buckets.append(cur)
+        self.bucket_of = {n: i for i, b in enumerate(self.buckets) for n in b}
+        self.bucket_range = []
+        for b in self.buckets:
+            offs = [eng.slot[n][0] for n in b]
+            lo = min(offs)
+            hi = max(eng.slot[n][0] + (int(np.prod(eng.slot[n][1])) + 63) // 64 * 64 for n in b)
+            self.bucket_range.append((lo, hi))
+        self._works = []
+        self.steps_done = 0
+
+    # ------------------------------------------------------------------ comm
+    def _start_bucket(self, i):
+        lo, hi = self.bucket_range[i]
+        w = dist.all_reduce(self.eng.flat_g[lo:hi], op=dist.ReduceOp.SUM, group=self.group, async_op=True)
+        self._works.append(w)
+
+    def _backward_with_overlap(self):
+        if self.world == 1:
+            self.eng.backward()
+            return
+        pending = [len(b) for b in self.buckets]
+
+        def ready(name):
+            i = self.bucket_of[name]
+            pending[i] -= 1
+            if pending[i] == 0:
+                self._start_bucket(i)
+
+        self.eng.backward(on_param_ready=ready)
+
+    def _wait_comm(self):
+        for w in self._works:
+            w.wait()
+        self._works = []
+
+    # ------------------------------------------------------------------ update
+    def _apply(self, g):
+        eng = self.eng
+        o = self.optim
+        nhwc.larc_update(eng.flat_w, eng.flat_m, g, eng.offsets, o.lr, o.momentum, o.trust, o.weight_decay,
+                         o.eps, 1.0 / self.world, self.lr_out, self.status, eng.ws)
+        eng.repack()
+
+    def step(self, x: torch.Tensor, labels: torch.Tensor) -> torch.Tensor:
+        """One training step on device-resident inputs; returns the device loss (no host sync)."""
+        eng = self.eng
+        eng.set_batch(x, labels)
+        eng.forward()
+        if self.lag == 0:
+            self._backward_with_overlap()
+            self._wait_comm()
+            self._apply(eng.flat_g)
+        else:
+            # the previous step's reduction finishes under this step's compute
+            self._backward_with_overlap_lag1()
+        self.steps_done += 1
+        return eng.loss
+
+    def _backward_with_overlap_lag1(self):
+        eng = self.eng
+        prev_works = self._works
+        self._works = []
+        # this step's gradients go to the other buffer; the previous one is applied
+        g_prev = eng.flat_g
+        eng.flat_g = self.g_other
+        self.g_other = g_prev
+        self._backward_with_overlap()
+        for w in prev_works:
+            w.wait()
+        if self.have_prev:
+            self._apply(g_prev)
+        self.have_prev = True
+
+    def finish(self):
+        """Lag 1: apply the last step's reduced gradients (trainer.py:403-405)."""
+        self._wait_comm()
+        if self.lag == 1 and self.have_prev:
+            self._apply(self.eng.flat_g)
+            self.have_prev = False
+
+    def check_status(self):
+        if int(self.status.item()):
+            raise FloatingPointError("non-finite norm in LARC")
+
+    def digest(self) -> str:
+        return param_digest(self.eng.export_params(), self.net.param_order)
+
+    def hash_sync(self, step: int) -> str:
+        d = self.digest()
+        if self.world > 1:
+            got = [None] * self.world
+            dist.all_gather_object(got, d, group=self.group)
+            bad = {r: x for r, x in enumerate(got) if x != got[0]}
+            if bad:
+                raise TrainingError(f"weights diverged at step {step}: " +
+                                    "; ".join(f"rank {r}: {x[:12]}" for r, x in sorted(bad.items())))
+        return d
+
+
+@dataclass(frozen=True)
+class RunConfig:
+    """Training run description (reference harness/config.py:39-157, single-node subset)."""
+    lag: int = 0
+    steps: int = 10
+    local_batch: int = 1
+    seed: int = 0
+    optim: OptimConfig = field(default_factory=OptimConfig)
+    net: object = field(default_factory=NetConfig)
+    scene: SceneConfig = field(default_factory=SceneConfig)
+    class_weighting: str = "inv_sqrt"
+    hash_steps: tuple = ()
+
+    def __post_init__(self):
+        if self.lag not in (0, 1):
+            raise ValueError("lag must be 0 or 1")
+        if self.local_batch < 1 or self.steps < 1:
+            raise ValueError("local_batch and steps must be positive")
+        if self.class_weighting not in ("inv_sqrt", "uniform"):
+            raise ValueError("class_weighting must be inv_sqrt or uniform")
+        if self.net.channels_in != self.scene.channels:
+            raise ValueError("net input channels != scene channels")
+
+
+@dataclass
+class TrainResult:
+    records: list
+    stats: object
+    losses: list
+    digests: list
+    state: dict
+
+
+def model_flops_per_sample(net: SegmentationNet, shape) -> float:
+    n, c, h, w = shape
+    shapes = {k: v.shape for k, v in net._params.items()}
+    shapes.update(x=(n, c, h, w), labels=(n, h, w), class_weights=(net.cfg.classes,))
+    return train_flops_per_sample(count_graph(net.graph, shapes, batch=n))
+
+
+def train_run(cfg: RunConfig, net_cls=None) -> TrainResult:
+    """This rank's loop of a synchronous data-parallel run (trainer.py:343-476).
+
+    Call from every rank (torchrun); with no process group it is a 1-rank run.
+    Returns per-step records with the rank-mean rates (device-timed)."""
+    from .net import DeepLabV3Plus, MiniDenseNet
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    rank = dist.get_rank() if dist.is_initialized() else 0
+    if net_cls is None:
+        net_cls = MiniDenseNet if isinstance(cfg.net, NetConfig) else DeepLabV3Plus
+    net = net_cls(cfg.net, seed=cfg.seed)
+    sc = cfg.scene
+    shape = (cfg.local_batch, sc.channels, sc.height, sc.width)
+    cw = (uniform_weights(cfg.net.classes) if cfg.class_weighting == "uniform"
+          else ClassWeights(sc.frequencies).vector())
+    tr = DataParallelTrainer(net, cfg.optim, shape, lag=cfg.lag, class_weights=cw)
+    hash_at = {1, 10, cfg.steps} | set(cfg.hash_steps)
+    records, losses, digests = [], [], []
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for t in range(cfg.steps):
+        x, lab = generated_batch(sc, cfg.seed, t, rank, cfg.local_batch)
+        xd = torch.from_numpy(x).cuda(non_blocking=True)
+        ld = torch.from_numpy(lab).cuda(non_blocking=True)
+        ev0.record()
+        loss = tr.step(xd, ld)
+        ev1.record()
+        ev1.synchronize()
+        wall = ev0.elapsed_time(ev1) / 1e3
+        lv = float(loss.item())
+        if not math.isfinite(lv):
+            raise TrainingError(f"rank {rank}: non-finite loss at step {t + 1}")
+        rate = torch.tensor([cfg.local_batch / wall, lv, wall], dtype=torch.float64)
+        if world > 1:
+            allr = [torch.zeros_like(rate) for _ in range(world)]
+            dist.all_gather_object(allr, rate)
+        else:
+            allr = [rate]
+        rates = tuple(float(r[0]) for r in allr)
+        records.append(StepRecord(step=t + 1, rates=rates, wall=max(float(r[2]) for r in allr),
+                                  loss=float(np.mean([float(r[1]) for r in allr]))))
+        losses.append(records[-1].loss)
+        if (t + 1) in hash_at:   # like the reference, before the post-loop lag-1 apply
+            digests.append((t + 1, tr.hash_sync(t + 1)))
+    tr.finish()
+    tr.check_status()
+    stats = sustained_stats(records, per_sample_flops=model_flops_per_sample(net, shape))
+    return TrainResult(records, stats, losses, digests, net.state_dict() if rank == 0 else {})
