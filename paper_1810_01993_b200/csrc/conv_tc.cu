@@ -40,8 +40,8 @@ struct FpropCfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (SMEM_BUDGET / STAGE_BYTES) > 8 ? 8 : (SMEM_BUDGET / STAGE_BYTES);
   static constexpr uint32_t TMEM_COLS = tmem_cols_for(2 * BN);
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
   static constexpr int CW = BN < 32 ? BN : 32;  // epilogue chunk (TMEM columns per load)
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + 8 * 32 * 80;
 };
 
 struct FpropParams {
@@ -67,71 +67,136 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return p + ((1024 - (a & 1023)) & 1023);
 }
 
+// ---- epilogue staging: each epilogue warp owns a 32-row x CW-column bf16 tile in shared
+// memory (80-byte row pitch, bank-conflict free).  A thread holds one accumulator row (one
+// pixel); global traffic goes through cooperative transfers in which 4 (or 2) lanes move one
+// row's 64 (32) contiguous bytes, so every warp access is a set of full 32-byte sectors.
+constexpr int EPI_ROW = 80;
+constexpr int EPI_WARP_BYTES = 32 * EPI_ROW;
+
 template <int CW>
-__device__ __forceinline__ void fprop_epilogue_chunk(const FpropParams& p, float* v, long long pix, int c0) {
+struct CoopRows {
+  static constexpr int PIECES = CW / 8;         // 16-byte pieces per row
+  static constexpr int ROWS_PER_IT = 32 / PIECES;
+  long long pix[PIECES];
+  bool ok[PIECES];
+};
+
+template <int CW>
+__device__ __forceinline__ void coop_load(const __nv_bfloat16* base, long long stride, int c0, int cout,
+                                          const CoopRows<CW>& L, uint8_t* st, bool nc) {
+  using R = CoopRows<CW>;
+  const int lane = lane_id(), piece = lane % R::PIECES;
+  const bool pv = c0 + piece * 8 < cout;
+#pragma unroll
+  for (int k = 0; k < R::PIECES; ++k) {
+    uint4 u = make_uint4(0, 0, 0, 0);
+    if (L.ok[k] && pv) {
+      const uint4* src = reinterpret_cast<const uint4*>(base + L.pix[k] * stride + c0 + piece * 8);
+      u = nc ? __ldg(src) : *src;
+    }
+    *reinterpret_cast<uint4*>(st + (k * R::ROWS_PER_IT + lane / R::PIECES) * EPI_ROW + piece * 16) = u;
+  }
+}
+template <int CW>
+__device__ __forceinline__ void coop_store(__nv_bfloat16* base, long long stride, int c0, int cout,
+                                           const CoopRows<CW>& L, const uint8_t* st) {
+  using R = CoopRows<CW>;
+  const int lane = lane_id(), piece = lane % R::PIECES;
+  const bool pv = c0 + piece * 8 < cout;
+#pragma unroll
+  for (int k = 0; k < R::PIECES; ++k)
+    if (L.ok[k] && pv)
+      *reinterpret_cast<uint4*>(base + L.pix[k] * stride + c0 + piece * 8) =
+          *reinterpret_cast<const uint4*>(st + (k * R::ROWS_PER_IT + lane / R::PIECES) * EPI_ROW + piece * 16);
+}
+template <int CW>
+__device__ __forceinline__ void row_get(const uint8_t* st, float* v) {
+  const uint8_t* r = st + lane_id() * EPI_ROW;
+#pragma unroll
+  for (int q = 0; q < CW / 8; ++q) {
+    const uint4 u = *reinterpret_cast<const uint4*>(r + q * 16);
+    const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      v[q * 8 + 2 * e] = bf16lo(w4[e]);
+      v[q * 8 + 2 * e + 1] = bf16hi(w4[e]);
+    }
+  }
+}
+template <int CW>
+__device__ __forceinline__ void row_put(uint8_t* st, const float* v) {
+  uint8_t* r = st + lane_id() * EPI_ROW;
+#pragma unroll
+  for (int q = 0; q < CW / 8; ++q) {
+    uint4 u;
+    u.x = pack_bf16x2(v[q * 8 + 0], v[q * 8 + 1]);
+    u.y = pack_bf16x2(v[q * 8 + 2], v[q * 8 + 3]);
+    u.z = pack_bf16x2(v[q * 8 + 4], v[q * 8 + 5]);
+    u.w = pack_bf16x2(v[q * 8 + 6], v[q * 8 + 7]);
+    *reinterpret_cast<uint4*>(r + q * 16) = u;
+  }
+}
+
+// bf16 output with aligned views and cout % 8 == 0: coalesced through the staging tile
+template <int CW>
+__device__ __forceinline__ void fprop_epilogue_vec(const FpropParams& p, float* v, int c0, const CoopRows<CW>& L,
+                                                   uint8_t* st) {
+  if (p.bias) {  // one coalesced load per warp, broadcast by shuffles
+    const int lane = lane_id();
+    const float b = (lane < CW && c0 + lane < p.cout) ? __ldg(p.bias + c0 + lane) : 0.f;
+#pragma unroll
+    for (int i = 0; i < CW; ++i) v[i] += __shfl_sync(0xffffffffu, b, i);
+  }
+  float t[CW];
+  if (p.res) {
+    coop_load<CW>(p.res, p.res_stride, c0, p.cout, L, st, true);
+    __syncwarp();
+    row_get<CW>(st, t);
+#pragma unroll
+    for (int i = 0; i < CW; ++i) v[i] += t[i];
+    __syncwarp();
+  }
+  if (p.relu) {
+#pragma unroll
+    for (int i = 0; i < CW; ++i) v[i] = fmaxf(v[i], 0.f);
+  }
+  if (p.mask) {
+    coop_load<CW>(p.mask, p.mask_stride, c0, p.cout, L, st, true);
+    __syncwarp();
+    row_get<CW>(st, t);
+#pragma unroll
+    for (int i = 0; i < CW; ++i)
+      if (!(t[i] > 0.f)) v[i] = 0.f;
+    __syncwarp();
+  }
+  __nv_bfloat16* y = reinterpret_cast<__nv_bfloat16*>(p.y);
+  if (p.accumulate) {
+    coop_load<CW>(y, p.y_stride, c0, p.cout, L, st, false);
+    __syncwarp();
+    row_get<CW>(st, t);
+#pragma unroll
+    for (int i = 0; i < CW; ++i) v[i] += t[i];
+    __syncwarp();
+  }
+  row_put<CW>(st, v);
+  __syncwarp();
+  coop_store<CW>(y, p.y_stride, c0, p.cout, L, st);
+  __syncwarp();
+}
+
+template <int CW>
+__device__ __forceinline__ void fprop_epilogue_scalar(const FpropParams& p, float* v, long long pix, int c0) {
   const int nvalid = min(CW, p.cout - c0);
   if (p.bias) {
 #pragma unroll
     for (int i = 0; i < CW; ++i)
       if (i < nvalid) v[i] += __ldg(p.bias + c0 + i);
   }
-  if (p.vec_ok && nvalid == CW && !p.y_f32) {
-    if (p.res) {
-      const uint4* r = reinterpret_cast<const uint4*>(p.res + pix * p.res_stride + c0);
-#pragma unroll
-      for (int q = 0; q < CW / 8; ++q) {
-        uint4 u = __ldg(r + q);
-        uint32_t w4[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          v[q * 8 + 2 * e] += bf16lo(w4[e]);
-          v[q * 8 + 2 * e + 1] += bf16hi(w4[e]);
-        }
-      }
-    }
-    if (p.relu) {
-#pragma unroll
-      for (int i = 0; i < CW; ++i) v[i] = fmaxf(v[i], 0.f);
-    }
-    if (p.mask) {
-      const uint4* r = reinterpret_cast<const uint4*>(p.mask + pix * p.mask_stride + c0);
-#pragma unroll
-      for (int q = 0; q < CW / 8; ++q) {
-        uint4 u = __ldg(r + q);
-        uint32_t w4[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          if (!(bf16lo(w4[e]) > 0.f)) v[q * 8 + 2 * e] = 0.f;
-          if (!(bf16hi(w4[e]) > 0.f)) v[q * 8 + 2 * e + 1] = 0.f;
-        }
-      }
-    }
-    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.y) + pix * p.y_stride + c0);
-    if (p.accumulate) {
-#pragma unroll
-      for (int q = 0; q < CW / 8; ++q) {
-        uint4 u = dst[q];
-        uint32_t w4[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          v[q * 8 + 2 * e] += bf16lo(w4[e]);
-          v[q * 8 + 2 * e + 1] += bf16hi(w4[e]);
-        }
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < CW / 8; ++q) {
-      uint4 u;
-      u.x = pack_bf16x2(v[q * 8 + 0], v[q * 8 + 1]);
-      u.y = pack_bf16x2(v[q * 8 + 2], v[q * 8 + 3]);
-      u.z = pack_bf16x2(v[q * 8 + 4], v[q * 8 + 5]);
-      u.w = pack_bf16x2(v[q * 8 + 6], v[q * 8 + 7]);
-      dst[q] = u;
-    }
-    return;
-  }
   // general (scalar) path: ragged channel counts, fp32 output, unaligned views
-  for (int i = 0; i < nvalid; ++i) {
+#pragma unroll
+  for (int i = 0; i < CW; ++i) {
+    if (i >= nvalid) break;
     float x = v[i];
     if (p.res) x += __bfloat162float(p.res[pix * p.res_stride + c0 + i]);
     if (p.relu) x = fmaxf(x, 0.f);
@@ -147,8 +212,10 @@ __device__ __forceinline__ void fprop_epilogue_chunk(const FpropParams& p, float
   }
 }
 
+constexpr int FPROP_THREADS = 320;  // TMA warp, MMA warp, 8 epilogue warps
+
 template <int BN, int KBLK>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(FPROP_THREADS, 1)
     conv_fprop_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const FpropParams p) {
   using C = FpropCfg<BN, KBLK>;
@@ -164,6 +231,7 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint8_t* epi = reinterpret_cast<uint8_t*>(tmem_slot) + 16;
 
   const int warp = threadIdx.x >> 5;
   const int lane = lane_id();
@@ -176,7 +244,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 4);
+      mbar_init(&tempty[s], 8);
     }
     fence_barrier_init();
   }
@@ -244,9 +312,17 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else {
+    // 8 epilogue warps: two per TMEM lane quarter, splitting the tile's column chunks
+    const int ew = warp - 2;
     const int q = warp & 3;
+    const int half = ew >> 2;
     const int row = q * 32 + lane;
     const int ry = row / p.bw, rx = row - ry * p.bw;
+    uint8_t* st = epi + ew * EPI_WARP_BYTES;
+    const bool vec = p.vec_ok && !p.y_f32 && (p.cout % 8) == 0;
+    using R = CoopRows<C::CW>;
+    constexpr int NCH = BN / C::CW;
+    constexpr int NJ = (NCH + 1) / 2;
     int it = 0;
     for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++it) {
       const int as = it & 1;
@@ -257,18 +333,48 @@ __global__ void __launch_bounds__(192, 1)
       const int yy = ty * p.bh + ry, xx = tx * p.bw + rx;
       const bool valid = yy < p.h && xx < p.w;
       const long long pix = (static_cast<long long>(img) * p.h + yy) * p.w + xx;
+      R L;
+#pragma unroll
+      for (int k = 0; k < R::PIECES; ++k) {
+        const int rr = q * 32 + k * R::ROWS_PER_IT + lane / R::PIECES;
+        const int cy = ty * p.bh + rr / p.bw, cx = tx * p.bw + rr % p.bw;
+        L.ok[k] = cy < p.h && cx < p.w;
+        L.pix[k] = (static_cast<long long>(img) * p.h + cy) * p.w + cx;
+      }
       mbar_wait(&tfull[as], ap);
       tc_fence_after();
-#pragma unroll 1
-      for (int ch = 0; ch < BN / C::CW; ++ch) {
-        float v[32];
-        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + as * BN + ch * C::CW;
+      const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + as * BN;
+      uint32_t cur[C::CW], nxt[C::CW];
+      if (half < NCH) {
         if constexpr (C::CW == 32)
-          tmem_ld_32x32b_x32(taddr, v);
+          tmem_ld_issue_x32(tbase + half * C::CW, cur);
         else
-          tmem_ld_32x32b_x16(taddr, v);
+          tmem_ld_issue_x16(tbase + half * C::CW, cur);
+      }
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        const int ch = 2 * j + half;
+        if (ch >= NCH) break;  // warp-uniform
+        if (ch + 2 < NCH) {    // prefetch the next chunk of this warp while this one is processed
+          if constexpr (C::CW == 32)
+            tmem_ld_issue_x32(tbase + (ch + 2) * C::CW, nxt);
+          else
+            tmem_ld_issue_x16(tbase + (ch + 2) * C::CW, nxt);
+        }
+        float v[C::CW];
+#pragma unroll
+        for (int i = 0; i < C::CW; ++i) v[i] = __uint_as_float(cur[i]);
         const int c0 = nt * BN + ch * C::CW;
-        if (valid && c0 < p.cout) fprop_epilogue_chunk<C::CW>(p, v, pix, c0);
+        if (c0 < p.cout) {
+          if (vec)
+            fprop_epilogue_vec<C::CW>(p, v, c0, L, st);
+          else if (valid)
+            fprop_epilogue_scalar<C::CW>(p, v, pix, c0);
+        }
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < C::CW; ++i) cur[i] = nxt[i];
       }
       tc_fence_before();
       __syncwarp();
@@ -454,7 +560,9 @@ __global__ void __launch_bounds__(192, 1)
             for (int e = 0; e < C::CW; e += 4)
               *reinterpret_cast<float4*>(dst + c0 + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
           } else {
-            for (int e = 0; e < nvalid; ++e) dst[c0 + e] = v[e];
+#pragma unroll
+            for (int e = 0; e < C::CW; ++e)
+              if (e < nvalid) dst[c0 + e] = v[e];
           }
         }
       }
@@ -494,7 +602,7 @@ static int launch_fprop(const CUtensorMap& ta, const CUtensorMap& tb, const Fpro
     attr_set = true;
   }
   const int grid = std::min(p.num_tiles, num_sms());
-  kern<<<grid, 192, C::SMEM, st>>>(ta, tb, p);
+  kern<<<grid, FPROP_THREADS, C::SMEM, st>>>(ta, tb, p);
   return check_launch();
 }
 
@@ -540,7 +648,19 @@ extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
   if (!view_aligned(x, 2)) return B2DL_E_ALIGN;
   const int kblk = x.c <= 16 ? 16 : 64;
   const int cin_pad = b2dl_cin_pad(x.c);
-  const int bn = a->block_n ? a->block_n : pick_bn(a->cout);
+  int bn = a->block_n ? a->block_n : pick_bn(a->cout);
+  if (!a->block_n && bn == 256) {
+    // wave quantisation: a narrower N tile can fill the last wave of a small map better
+    const int bw = pow2_divisor(x.w, 128) < 8 && x.w >= 8 ? std::min(128, 1 << (31 - __builtin_clz(x.w)))
+                                                         : pow2_divisor(x.w, 128);
+    const long long mt = static_cast<long long>(x.n) * cdiv(x.w, bw) * cdiv(x.h, BM / bw);
+    auto score = [&](int b, double speed) {
+      const long long tiles = mt * cdiv(a->cout, b);
+      const long long waves = (tiles + num_sms() - 1) / num_sms();
+      return speed * static_cast<double>(tiles) / (waves * num_sms());
+    };
+    if (score(128, 0.9) > score(256, 1.0)) bn = 128;
+  }
 
   FpropParams p{};
   p.n = x.n;
@@ -636,10 +756,24 @@ static int plan_wgrad(const b2dl_wgrad_args* a, WgradPlan* out) {
   p.n_tiles = cdiv(dy.c, bn);
   int splits = a->splits;
   if (splits <= 0) {
+    // split-K count: fill whole waves of CTAs (persistent grid = #SMs) while keeping
+    // >= 32 pixel boxes of K per split so the fp32 partial traffic stays small
     const int base = p.m_tiles * p.n_tiles;
-    splits = std::max(1, (2 * num_sms() + base - 1) / base);
-    // keep >= 8 pixel boxes of work per split
-    splits = std::min(splits, std::max(1, p.num_pb / 8));
+    const int sms = num_sms();
+    const int smax = std::max(1, std::min(64, p.num_pb / 32));
+    double best = -1.0;
+    splits = 1;
+    for (int s = 1; s <= smax; ++s) {
+      const long long tiles = static_cast<long long>(base) * s;
+      const long long waves = (tiles + sms - 1) / sms;
+      const double eff = static_cast<double>(tiles) / (waves * sms);
+      const double fill = std::min(1.0, static_cast<double>(tiles) / sms);
+      const double score = eff * fill - 0.002 * s;  // mild preference for fewer partials
+      if (score > best) {
+        best = score;
+        splits = s;
+      }
+    }
   }
   splits = std::min(splits, p.num_pb);
   p.pb_per_split = cdiv(p.num_pb, splits);

@@ -55,175 +55,261 @@ __global__ void k_nhwc_to_nchw(const void* __restrict__ x, int f32, float* __res
 }
 
 // ------------------------------------------------------------------ pool / upsample
-// channel pairs per thread (views have even channel offsets and counts in practice; odd c handled scalar)
+// 8-channel (16 B) vector helpers; G = 8 on aligned views, 1 otherwise
+template <int G>
+__device__ __forceinline__ void ldv(const __nv_bfloat16* p, float* v) {
+  if constexpr (G == 8) {
+    uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      v[2 * e] = __uint_as_float(w[e] << 16);
+      v[2 * e + 1] = __uint_as_float(w[e] & 0xFFFF0000u);
+    }
+  } else {
+    v[0] = ld_bf(p);
+  }
+}
+template <int G>
+__device__ __forceinline__ void ldv_rw(const __nv_bfloat16* p, float* v) {  // plain load (data written in place)
+  if constexpr (G == 8) {
+    uint4 u = *reinterpret_cast<const uint4*>(p);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      v[2 * e] = __uint_as_float(w[e] << 16);
+      v[2 * e + 1] = __uint_as_float(w[e] & 0xFFFF0000u);
+    }
+  } else {
+    v[0] = ld_bf(p);
+  }
+}
+template <int G>
+__device__ __forceinline__ void stv(__nv_bfloat16* p, const float* v) {
+  if constexpr (G == 8) {
+    uint32_t w[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      __nv_bfloat162 t = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+      w[e] = *reinterpret_cast<uint32_t*>(&t);
+    }
+    *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+  } else {
+    *p = __float2bfloat16_rn(v[0]);
+  }
+}
+// d <- mask(m) * v  [+ d]
+template <int G>
+__device__ __forceinline__ void finish(float* v, const __nv_bfloat16* m, __nv_bfloat16* d, int acc) {
+  if (m) {
+    float mv[G];
+    ldv<G>(m, mv);
+#pragma unroll
+    for (int e = 0; e < G; ++e)
+      if (!(mv[e] > 0.f)) v[e] = 0.f;
+  }
+  if (acc) {
+    float o[G];
+    ldv_rw<G>(d, o);
+#pragma unroll
+    for (int e = 0; e < G; ++e) v[e] += o[e];
+  }
+  stv<G>(d, v);
+}
+
+template <int G>
 __global__ void k_avgpool_fwd(const __nv_bfloat16* __restrict__ x, int xs, __nv_bfloat16* __restrict__ y, int ys,
                               int n, int ho, int wo, int c, int k) {
   const int W = wo * k;
-  const long long total = static_cast<long long>(n) * ho * wo * c;
+  const int cg = c / G;
+  const long long total = static_cast<long long>(n) * ho * wo * cg;
   const float inv = 1.f / (k * k);
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    int ch = static_cast<int>(i % c);
-    long long op = i / c;
-    int ox = static_cast<int>(op % wo);
-    long long r = op / wo;
-    int oy = static_cast<int>(r % ho);
-    long long img = r / ho;
-    float s = 0.f;
+    const int ch = static_cast<int>(i % cg) * G;
+    const long long op = i / cg;
+    const int ox = static_cast<int>(op % wo);
+    const long long r = op / wo;
+    const int oy = static_cast<int>(r % ho);
+    const long long img = r / ho;
+    float s[G] = {};
     for (int a = 0; a < k; ++a) {
       const __nv_bfloat16* row = x + ((img * ho * k + oy * k + a) * W + ox * k) * xs + ch;
-      for (int b = 0; b < k; ++b) s += ld_bf(row + static_cast<long long>(b) * xs);
+      for (int b = 0; b < k; ++b) {
+        float v[G];
+        ldv<G>(row + static_cast<long long>(b) * xs, v);
+#pragma unroll
+        for (int e = 0; e < G; ++e) s[e] += v[e];
+      }
     }
-    y[op * ys + ch] = __float2bfloat16_rn(s * inv);
+#pragma unroll
+    for (int e = 0; e < G; ++e) s[e] *= inv;
+    stv<G>(y + op * ys + ch, s);
   }
 }
-// dx[p] (+)= mask(dx_fwd)[p] * dy[pool(p)] / k^2
+// dx[p] (+)= mask(x)[p] * dy[pool(p)] / k^2
+template <int G>
 __global__ void k_avgpool_bwd(const __nv_bfloat16* __restrict__ dy, int dys, __nv_bfloat16* __restrict__ dx, int dxs,
                               const __nv_bfloat16* __restrict__ mask, int ms, int n, int h, int w, int c, int k,
                               int acc) {
-  const long long total = static_cast<long long>(n) * h * w * c;
+  const int cg = c / G;
+  const long long total = static_cast<long long>(n) * h * w * cg;
   const int wo = w / k, ho = h / k;
   const float inv = 1.f / (k * k);
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    int ch = static_cast<int>(i % c);
-    long long p = i / c;
-    int xx = static_cast<int>(p % w);
-    long long r = p / w;
-    int yy = static_cast<int>(r % h);
-    long long img = r / h;
-    float v = ld_bf(dy + ((img * ho + yy / k) * wo + xx / k) * dys + ch) * inv;
-    if (mask && !(ld_bf(mask + p * ms + ch) > 0.f)) v = 0.f;
-    __nv_bfloat16* d = dx + p * dxs + ch;
-    if (acc) v += ld_bf(d);
-    *d = __float2bfloat16_rn(v);
+    const int ch = static_cast<int>(i % cg) * G;
+    const long long p = i / cg;
+    const int xx = static_cast<int>(p % w);
+    const long long r = p / w;
+    const int yy = static_cast<int>(r % h);
+    const long long img = r / h;
+    float v[G];
+    ldv<G>(dy + ((img * ho + yy / k) * wo + xx / k) * dys + ch, v);
+#pragma unroll
+    for (int e = 0; e < G; ++e) v[e] *= inv;
+    finish<G>(v, mask ? mask + p * ms + ch : nullptr, dx + p * dxs + ch, acc);
   }
 }
+template <int G>
 __global__ void k_upsample_fwd(const __nv_bfloat16* __restrict__ x, int xs, __nv_bfloat16* __restrict__ y, int ys,
                                int n, int h, int w, int c, int f) {
-  // y is [n, h*f, w*f]; 8 channels (16 B) per thread when aligned
   const int H = h * f, W = w * f;
-  const bool vec = (c % 8 == 0) && (xs % 8 == 0) && (ys % 8 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0) &&
-                   ((reinterpret_cast<uintptr_t>(y) & 15) == 0);
-  const int cg = vec ? c / 8 : c;
+  const int cg = c / G;
   const long long total = static_cast<long long>(n) * H * W * cg;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    int g = static_cast<int>(i % cg);
-    long long p = i / cg;
-    int xx = static_cast<int>(p % W);
-    long long r = p / W;
-    int yy = static_cast<int>(r % H);
-    long long img = r / H;
-    long long sp = (img * h + yy / f) * w + xx / f;
-    if (vec) {
-      *reinterpret_cast<uint4*>(y + p * ys + g * 8) = __ldg(reinterpret_cast<const uint4*>(x + sp * xs + g * 8));
-    } else {
-      y[p * ys + g] = x[sp * xs + g];
-    }
+    const int ch = static_cast<int>(i % cg) * G;
+    const long long p = i / cg;
+    const int xx = static_cast<int>(p % W);
+    const long long r = p / W;
+    const int yy = static_cast<int>(r % H);
+    const long long img = r / H;
+    const long long sp = (img * h + yy / f) * w + xx / f;
+    float v[G];
+    ldv<G>(x + sp * xs + ch, v);
+    stv<G>(y + p * ys + ch, v);
   }
 }
-// dx[q] (+)= sum over the f x f block of mask(dy_fwd) * dy
+// dx[q] (+)= mask(x)[q] * sum over the f x f block of dy
+template <int G>
 __global__ void k_upsample_bwd(const __nv_bfloat16* __restrict__ dy, int dys, __nv_bfloat16* __restrict__ dx, int dxs,
                                const __nv_bfloat16* __restrict__ mask, int ms, int n, int h, int w, int c, int f,
                                int acc) {
   const int W = w * f;
-  const long long total = static_cast<long long>(n) * h * w * c;
+  const int cg = c / G;
+  const long long total = static_cast<long long>(n) * h * w * cg;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    int ch = static_cast<int>(i % c);
-    long long q = i / c;
-    int xx = static_cast<int>(q % w);
-    long long r = q / w;
-    int yy = static_cast<int>(r % h);
-    long long img = r / h;
-    float s = 0.f;
+    const int ch = static_cast<int>(i % cg) * G;
+    const long long q = i / cg;
+    const int xx = static_cast<int>(q % w);
+    const long long r = q / w;
+    const int yy = static_cast<int>(r % h);
+    const long long img = r / h;
+    float s[G] = {};
     for (int a = 0; a < f; ++a) {
-      long long rowp = (img * h * f + yy * f + a) * W + xx * f;
+      const long long rowp = (img * h * f + yy * f + a) * W + xx * f;
       for (int b = 0; b < f; ++b) {
-        long long pp = rowp + b;
-        float v = ld_bf(dy + pp * dys + ch);
-        if (mask && !(ld_bf(mask + pp * ms + ch) > 0.f)) v = 0.f;
-        s += v;
+        float v[G];
+        ldv<G>(dy + (rowp + b) * dys + ch, v);
+#pragma unroll
+        for (int e = 0; e < G; ++e) s[e] += v[e];
       }
     }
-    __nv_bfloat16* d = dx + q * dxs + ch;
-    if (acc) s += ld_bf(d);
-    *d = __float2bfloat16_rn(s);
+    finish<G>(s, mask ? mask + q * ms + ch : nullptr, dx + q * dxs + ch, acc);
   }
 }
 
 // ------------------------------------------------------------------ add / mask
+template <int G>
 __global__ void k_add(const __nv_bfloat16* __restrict__ x, int xs, __nv_bfloat16* __restrict__ y, int ys,
                       const __nv_bfloat16* __restrict__ mask, int ms, long long npix, int c, int acc) {
-  const long long total = npix * c;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    int ch = static_cast<int>(i % c);
-    long long p = i / c;
-    float v = ld_bf(x + p * xs + ch);
-    if (mask && !(ld_bf(mask + p * ms + ch) > 0.f)) v = 0.f;
-    __nv_bfloat16* d = y + p * ys + ch;
-    if (acc) v += ld_bf(d);
-    *d = __float2bfloat16_rn(v);
-  }
-}
-__global__ void k_add_vec(const __nv_bfloat16* __restrict__ x, int xs, __nv_bfloat16* __restrict__ y, int ys,
-                          const __nv_bfloat16* __restrict__ mask, int ms, long long npix, int c, int acc) {
-  const int cg = c / 8;
+  const int cg = c / G;
   const long long total = npix * cg;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    int g = static_cast<int>(i % cg);
-    long long p = i / cg;
-    uint4 xv = __ldg(reinterpret_cast<const uint4*>(x + p * xs + g * 8));
-    uint4 mv = mask ? __ldg(reinterpret_cast<const uint4*>(mask + p * ms + g * 8)) : make_uint4(0, 0, 0, 0);
-    uint4* dp = reinterpret_cast<uint4*>(y + p * ys + g * 8);
-    uint4 yv = acc ? *dp : make_uint4(0, 0, 0, 0);
-    const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(&xv);
-    const __nv_bfloat16* mb = reinterpret_cast<const __nv_bfloat16*>(&mv);
-    __nv_bfloat16* yb = reinterpret_cast<__nv_bfloat16*>(&yv);
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      float v = __bfloat162float(xb[e]);
-      if (mask && !(__bfloat162float(mb[e]) > 0.f)) v = 0.f;
-      if (acc) v += __bfloat162float(yb[e]);
-      yb[e] = __float2bfloat16_rn(v);
-    }
-    *dp = yv;
+    const int ch = static_cast<int>(i % cg) * G;
+    const long long p = i / cg;
+    float v[G];
+    ldv_rw<G>(x + p * xs + ch, v);
+    finish<G>(v, mask ? mask + p * ms + ch : nullptr, y + p * ys + ch, acc);
   }
 }
+template <int G>
 __global__ void k_relu_mask(__nv_bfloat16* __restrict__ g, int gs, const __nv_bfloat16* __restrict__ a, int as,
                             long long npix, int c) {
-  const long long total = npix * c;
+  const int cg = c / G;
+  const long long total = npix * cg;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    int ch = static_cast<int>(i % c);
-    long long p = i / c;
-    if (!(ld_bf(a + p * as + ch) > 0.f)) g[p * gs + ch] = __float2bfloat16_rn(0.f);
+    const int ch = static_cast<int>(i % cg) * G;
+    const long long p = i / cg;
+    float v[G];
+    ldv_rw<G>(g + p * gs + ch, v);
+    finish<G>(v, a + p * as + ch, g + p * gs + ch, 0);
   }
 }
 
 // ------------------------------------------------------------------ bias gradient
-// pass 1: partial[b][c] = sum over pixels p = b, b+G, ... ; pass 2: out[c] (+)= sum_b partial[b][c]
+// pass 1: block b sums a contiguous pixel range; threads own channel groups and
+//         stride over rows, rows are folded in shared memory -> part[b][c]
+// pass 2: out[c] (+)= sum_b part[b][c] in a fixed order (deterministic)
+template <int G>
 __global__ void k_colsum_partial(const __nv_bfloat16* __restrict__ g, int gs, long long npix, int c,
                                  float* __restrict__ part) {
+  extern __shared__ float red[];
+  const int cg = c / G;
+  const int lanes = cg < static_cast<int>(blockDim.x) ? cg : static_cast<int>(blockDim.x);
+  const int rows = blockDim.x / lanes;
+  const int row = threadIdx.x / lanes, lane = threadIdx.x - row * lanes;
+  const long long per = (npix + gridDim.x - 1) / gridDim.x;
+  const long long p0 = blockIdx.x * per;
+  const long long p1 = p0 + per < npix ? p0 + per : npix;
+  if (row < rows) {
+    for (int grp = lane; grp < cg; grp += lanes) {
+      float s[G] = {};
+      for (long long p = p0 + row; p < p1; p += rows) {
+        float v[G];
+        ldv<G>(g + p * gs + grp * G, v);
+#pragma unroll
+        for (int e = 0; e < G; ++e) s[e] += v[e];
+      }
+#pragma unroll
+      for (int e = 0; e < G; ++e) red[row * c + grp * G + e] = s[e];
+    }
+  }
+  __syncthreads();
   for (int ch = threadIdx.x; ch < c; ch += blockDim.x) {
     float s = 0.f;
-    for (long long p = blockIdx.x; p < npix; p += gridDim.x) s += ld_bf(g + p * gs + ch);
+    for (int r = 0; r < rows; ++r) s += red[r * c + ch];
     part[static_cast<long long>(blockIdx.x) * c + ch] = s;
   }
 }
 __global__ void k_colsum_final(const float* __restrict__ part, int nb, int c, float* __restrict__ out, int acc) {
-  int ch = blockIdx.x * blockDim.x + threadIdx.x;
-  if (ch >= c) return;
-  double s = 0.0;
-  for (int b = 0; b < nb; ++b) s += part[static_cast<long long>(b) * c + ch];
-  out[ch] = static_cast<float>(acc ? out[ch] + s : s);
+  __shared__ float red[8][33];
+  const int ch = blockIdx.x * 32 + threadIdx.x;
+  float s = 0.f;
+  if (ch < c)
+    for (int b = threadIdx.y; b < nb; b += 8) s += part[static_cast<long long>(b) * c + ch];
+  red[threadIdx.y][threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.y == 0 && ch < c) {
+    float t = 0.f;
+    for (int y = 0; y < 8; ++y) t += red[y][threadIdx.x];
+    out[ch] = acc ? out[ch] + t : t;
+  }
 }
 
 static int colsum_blocks(long long npix) {
-  return static_cast<int>(std::max<long long>(1, std::min<long long>(npix, 4LL * num_sms())));
+  return static_cast<int>(std::max<long long>(1, std::min<long long>((npix + 31) / 32, 2LL * num_sms())));
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+static bool vec_ok(const b2dl_act& a) { return a.c % 8 == 0 && a.c_stride % 8 == 0 && aligned16(a.ptr); }
+static bool vec_ok(const b2dl_act& a, const b2dl_act& b) { return vec_ok(a) && vec_ok(b); }
+static bool vec_ok(const b2dl_act& a, const b2dl_act& b, const b2dl_act& m) {
+  return vec_ok(a, b) && (!m.ptr || (m.c_stride % 8 == 0 && aligned16(m.ptr)));
 }
 
 // ------------------------------------------------------------------ weight packing
@@ -254,8 +340,6 @@ __global__ void k_pack_dgrad(const float* __restrict__ w, __nv_bfloat16* __restr
   }
 }
 
-static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
-
 }  // namespace b2
 
 using namespace b2;
@@ -276,61 +360,64 @@ extern "C" int b2dl_nhwc_to_nchw(b2dl_act x, int src_f32, float* y, void* stream
   return check_launch();
 }
 
+#define B2_LAUNCH_G(KERN, VEC, GRIDN, ...)                                                   \
+  do {                                                                                      \
+    if (VEC)                                                                                \
+      KERN<8><<<grid1d(GRIDN, 8), 256, 0, as_stream(stream)>>>(__VA_ARGS__);                \
+    else                                                                                    \
+      KERN<1><<<grid1d(GRIDN), 256, 0, as_stream(stream)>>>(__VA_ARGS__);                   \
+  } while (0)
+
 extern "C" int b2dl_avgpool_fwd(b2dl_act x, b2dl_act y, int k, void* stream) {
   if (k < 1 || x.h % k || x.w % k || y.h != x.h / k || y.w != x.w / k || y.c != x.c || y.n != x.n) return B2DL_E_VALUE;
   long long total = static_cast<long long>(y.n) * y.h * y.w * y.c;
-  k_avgpool_fwd<<<grid1d(total), 256, 0, as_stream(stream)>>>(CBF(x.ptr), x.c_stride, BF(y.ptr), y.c_stride, y.n, y.h,
-                                                              y.w, y.c, k);
+  B2_LAUNCH_G(k_avgpool_fwd, vec_ok(x, y), total, CBF(x.ptr), x.c_stride, BF(y.ptr), y.c_stride, y.n, y.h, y.w, y.c, k);
   return check_launch();
 }
 
 extern "C" int b2dl_avgpool_bwd(b2dl_act dy, b2dl_act dx, int k, int accumulate, b2dl_act mask, void* stream) {
   if (k < 1 || dx.h != dy.h * k || dx.w != dy.w * k || dx.c != dy.c) return B2DL_E_VALUE;
   long long total = static_cast<long long>(dx.n) * dx.h * dx.w * dx.c;
-  k_avgpool_bwd<<<grid1d(total), 256, 0, as_stream(stream)>>>(CBF(dy.ptr), dy.c_stride, BF(dx.ptr), dx.c_stride,
-                                                              CBF(mask.ptr), mask.c_stride, dx.n, dx.h, dx.w, dx.c, k,
-                                                              accumulate);
+  B2_LAUNCH_G(k_avgpool_bwd, vec_ok(dy, dx, mask), total, CBF(dy.ptr), dy.c_stride, BF(dx.ptr), dx.c_stride,
+              CBF(mask.ptr), mask.c_stride, dx.n, dx.h, dx.w, dx.c, k, accumulate);
   return check_launch();
 }
 
 extern "C" int b2dl_upsample_fwd(b2dl_act x, b2dl_act y, int f, void* stream) {
   if (f < 1 || y.h != x.h * f || y.w != x.w * f || y.c != x.c) return B2DL_E_VALUE;
   long long total = static_cast<long long>(y.n) * y.h * y.w * y.c;
-  k_upsample_fwd<<<grid1d(total, 8), 256, 0, as_stream(stream)>>>(CBF(x.ptr), x.c_stride, BF(y.ptr), y.c_stride, x.n,
-                                                                  x.h, x.w, x.c, f);
+  B2_LAUNCH_G(k_upsample_fwd, vec_ok(x, y), total, CBF(x.ptr), x.c_stride, BF(y.ptr), y.c_stride, x.n, x.h, x.w, x.c,
+              f);
   return check_launch();
 }
 
 extern "C" int b2dl_upsample_bwd(b2dl_act dy, b2dl_act dx, int f, int accumulate, b2dl_act mask, void* stream) {
   if (f < 1 || dy.h != dx.h * f || dy.w != dx.w * f || dy.c != dx.c) return B2DL_E_VALUE;
   long long total = static_cast<long long>(dx.n) * dx.h * dx.w * dx.c;
-  k_upsample_bwd<<<grid1d(total), 256, 0, as_stream(stream)>>>(CBF(dy.ptr), dy.c_stride, BF(dx.ptr), dx.c_stride,
-                                                               CBF(mask.ptr), mask.c_stride, dx.n, dx.h, dx.w, dx.c, f,
-                                                               accumulate);
+  B2_LAUNCH_G(k_upsample_bwd, vec_ok(dy, dx, mask), total, CBF(dy.ptr), dy.c_stride, BF(dx.ptr), dx.c_stride,
+              CBF(mask.ptr), mask.c_stride, dx.n, dx.h, dx.w, dx.c, f, accumulate);
   return check_launch();
 }
 
 extern "C" int b2dl_add(b2dl_act x, b2dl_act y, int accumulate, b2dl_act mask, void* stream) {
   if (x.c != y.c || x.h != y.h || x.w != y.w || x.n != y.n) return B2DL_E_VALUE;
   long long npix = static_cast<long long>(x.n) * x.h * x.w;
-  bool vec = x.c % 8 == 0 && x.c_stride % 8 == 0 && y.c_stride % 8 == 0 && aligned16(x.ptr) && aligned16(y.ptr) &&
-             (!mask.ptr || (mask.c_stride % 8 == 0 && aligned16(mask.ptr)));
-  if (vec)
-    k_add_vec<<<grid1d(npix * x.c, 8), 256, 0, as_stream(stream)>>>(CBF(x.ptr), x.c_stride, BF(y.ptr), y.c_stride,
-                                                                     CBF(mask.ptr), mask.c_stride, npix, x.c,
-                                                                     accumulate);
-  else
-    k_add<<<grid1d(npix * x.c), 256, 0, as_stream(stream)>>>(CBF(x.ptr), x.c_stride, BF(y.ptr), y.c_stride,
-                                                             CBF(mask.ptr), mask.c_stride, npix, x.c, accumulate);
+  B2_LAUNCH_G(k_add, vec_ok(x, y, mask), npix * x.c, CBF(x.ptr), x.c_stride, BF(y.ptr), y.c_stride, CBF(mask.ptr),
+              mask.c_stride, npix, x.c, accumulate);
   return check_launch();
 }
 
 extern "C" int b2dl_relu_mask(b2dl_act g, b2dl_act act, void* stream) {
   if (g.c != act.c || g.h != act.h || g.w != act.w || g.n != act.n) return B2DL_E_VALUE;
   long long npix = static_cast<long long>(g.n) * g.h * g.w;
-  k_relu_mask<<<grid1d(npix * g.c), 256, 0, as_stream(stream)>>>(BF(g.ptr), g.c_stride, CBF(act.ptr), act.c_stride,
-                                                                 npix, g.c);
+  B2_LAUNCH_G(k_relu_mask, vec_ok(g, act), npix * g.c, BF(g.ptr), g.c_stride, CBF(act.ptr), act.c_stride, npix, g.c);
   return check_launch();
+}
+
+static int colsum_rows(int c, bool vec) {
+  const int cg = vec ? c / 8 : c;
+  const int lanes = cg < 256 ? cg : 256;
+  return 256 / lanes;
 }
 
 extern "C" size_t b2dl_bias_grad_workspace_size(b2dl_act g) {
@@ -344,10 +431,16 @@ extern "C" int b2dl_bias_grad(b2dl_act g, float* out, int accumulate, void* work
   if (!out || workspace_bytes < b2dl_bias_grad_workspace_size(g)) return B2DL_E_VALUE;
   const int nb = colsum_blocks(npix);
   float* part = reinterpret_cast<float*>(workspace);
-  k_colsum_partial<<<nb, 256, 0, as_stream(stream)>>>(CBF(g.ptr), g.c_stride, npix, g.c, part);
+  const bool vec = vec_ok(g);
+  const size_t smem = static_cast<size_t>(colsum_rows(g.c, vec)) * g.c * sizeof(float);
+  if (smem > 48 * 1024) return B2DL_E_VALUE;
+  if (vec)
+    k_colsum_partial<8><<<nb, 256, smem, as_stream(stream)>>>(CBF(g.ptr), g.c_stride, npix, g.c, part);
+  else
+    k_colsum_partial<1><<<nb, 256, smem, as_stream(stream)>>>(CBF(g.ptr), g.c_stride, npix, g.c, part);
   int rc = check_launch();
   if (rc) return rc;
-  k_colsum_final<<<(g.c + 127) / 128, 128, 0, as_stream(stream)>>>(part, nb, g.c, out, accumulate);
+  k_colsum_final<<<(g.c + 31) / 32, dim3(32, 8), 0, as_stream(stream)>>>(part, nb, g.c, out, accumulate);
   return check_launch();
 }
 

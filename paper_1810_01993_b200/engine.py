@@ -212,13 +212,35 @@ class Plan:
                 root = self.view_of[t][0]
                 n, h, w, _, _ = self.buffers[root]
                 self.grad_buffers[root] = (n, h, w, _r8(self.chans(root)))
-        # static backward program with overwrite/accumulate decided per contribution
+        # static backward program: overwrite/accumulate and relu masking decided per contribution.
+        # A contribution to the gradient of a "maskable" tensor (a relu output, or a pool /
+        # nearest-upsample / concat of relu outputs -- all non-negative, zero exactly where every
+        # underlying relu is inactive) is multiplied by (activation > 0) when it is written, so
+        # the producer's relu VJP (ops.py:176-177) needs no separate pass.
         init = {root: [] for root in self.grad_buffers}
+        contrib = {root: [] for root in self.grad_buffers}
+        memo = {}
 
-        def claim(t):
+        def maskable(t):
+            if t not in memo:
+                prod = self.producer.get(t)
+                if prod is None or t == self.logits_name:
+                    memo[t] = False
+                elif prod.kind == "conv":
+                    memo[t] = prod.relu
+                elif prod.kind in ("pool", "up"):
+                    memo[t] = maskable(prod.ins[0])
+                elif prod.kind == "concat":
+                    memo[t] = all(maskable(x) for x in prod.ins)
+                else:
+                    memo[t] = False
+            return memo[t]
+
+        def claim(t, masked):
             root, off, c = self.view_spec(t)
             iv = init[root]
             lo, hi = off, off + c
+            contrib[root].append((lo, hi, masked))
             covered = sum(max(0, min(hi, b) - max(lo, a)) for a, b in iv)
             if covered == 0:
                 iv.append((lo, hi))
@@ -231,11 +253,15 @@ class Plan:
             root, off, c = self.view_spec(t)
             return sum(max(0, min(off + c, b) - max(off, a)) for a, b in init[root]) > 0
 
+        def unmasked_into(t):
+            root, off, c = self.view_spec(t)
+            return any((not m) and min(off + c, b) > max(off, a) for a, b, m in contrib[root])
+
         prog = []
         ce = [o for o in self.ops if o.kind == "ce"]
         if len(ce) != 1 or ce[0].ins[0] != self.logits_name:
             raise NotImplementedError("exactly one softmax_ce on the logits")
-        claim(self.logits_name)                       # written by the fused CE in forward
+        claim(self.logits_name, False)                # written by the fused CE in forward
         for op in reversed(self.ops):
             if op.kind == "ce" or op.out not in self.live:
                 continue
@@ -243,28 +269,35 @@ class Plan:
                 raise NotImplementedError(f"{op.out}: live tensor without gradient contributions")
             if op.kind == "conv":
                 x, res = op.ins[0], op.res
-                step = {"op": op, "dx": None, "dres": None}
+                step = {"op": op, "dx": None, "dres": None, "mask_dx": False, "mask_res": False,
+                        "relu_pass": op.relu and unmasked_into(op.out)}
                 if x in self.live:
-                    step["dx"] = claim(x)
+                    step["mask_dx"] = maskable(x)
+                    step["dx"] = claim(x, step["mask_dx"])
                 if res is not None and res in self.live:
-                    step["dres"] = claim(res)
+                    step["mask_res"] = maskable(res)
+                    step["dres"] = claim(res, step["mask_res"])
                 prog.append(step)
             elif op.kind in ("pool", "up"):
                 x = op.ins[0]
                 if x in self.live:
-                    prog.append({"op": op, "dx": claim(x)})
+                    m = maskable(x)
+                    prog.append({"op": op, "mask": m, "dx": claim(x, m)})
             elif op.kind == "concat":
                 # aliased inputs share the gradient region; copied inputs get the slice added
                 step = {"op": op, "copies": []}
                 off = 0
-                for s in op.ins:
-                    if s in op.copy_ins and s in self.live:
-                        step["copies"].append((s, off, claim(s)))
-                    off += self.chans(s)
+                for s_ in op.ins:
+                    if s_ in op.copy_ins and s_ in self.live:
+                        m = maskable(s_)
+                        step["copies"].append((s_, off, claim(s_, m), m))
+                    off += self.chans(s_)
                 prog.append(step)
             elif op.kind == "add":
-                prog.append({"op": op, "acc": [(s, claim(s)) for s in op.ins if s in self.live]})
+                prog.append({"op": op, "acc": [(s_, claim(s_, maskable(s_)), maskable(s_))
+                                               for s_ in op.ins if s_ in self.live]})
         self.backward_program = prog
+        self.relu_passes = sum(1 for st in prog if st.get("relu_pass"))
 
 
 class Engine:
@@ -312,7 +345,33 @@ class Engine:
         self.counts = torch.zeros(n * p.classes, dtype=torch.int32, device=self.device)
         self.input_shape = tuple(input_shape)
         self.launches = 0
+        self.conv_timing = False
+        self.conv_events = []
         self.load_params(params)
+
+    # ---------------------------------------------------------------- roofline timing
+    def _tic(self):
+        if not self.conv_timing:
+            return None
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        return e
+
+    def _toc(self, ev, op):
+        if ev is None:
+            return
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        n, _, h, w = self.plan.shapes[op.out]
+        self.conv_events.append((ev, e, 2 * op.k * op.k * op.cin * op.cout * n * h * w))
+
+    def conv_kernel_totals(self):
+        """(ms, algorithmic FLOPs) summed over the timed conv launches (fprop, dgrad, wgrad)."""
+        torch.cuda.synchronize()
+        ms = sum(a.elapsed_time(b) for a, b, _ in self.conv_events)
+        fl = sum(f for _, _, f in self.conv_events)
+        self.conv_events = []
+        return ms, fl
 
     # ---------------------------------------------------------------- views
     def v(self, t) -> View:
@@ -358,7 +417,7 @@ class Engine:
         for o in self.convs:
             nhwc.pack_weights(self.wslice(o.w), o.k, o.k, o.cin, o.cout, fprop=self.wf[o.w],
                               dgrad=self.wd.get(o.w))
-            self.launches += 1
+            self.launches += 1 + (o.w in self.wd)
 
     # ---------------------------------------------------------------- inputs
     def set_batch(self, x_nchw: torch.Tensor, labels: torch.Tensor):
@@ -379,10 +438,12 @@ class Engine:
             if op.kind == "conv":
                 out = op.out
                 b_off, _ = self.slot[op.b]
+                ev = self._tic()
                 nhwc.conv_fprop(self.v(op.ins[0]), self.wf[op.w], op.cout, op.k, op.k, op.dil, self.v(out),
                                 bias=self.flat_w[b_off:b_off + op.cout],
                                 residual=self.v(op.res) if op.res else None, relu=op.relu,
                                 y_f32=(out == p.logits_name))
+                self._toc(ev, op)
             elif op.kind == "pool":
                 nhwc.avgpool_fwd(self.v(op.ins[0]), self.v(op.out), op.factor)
             elif op.kind == "up":
@@ -405,7 +466,7 @@ class Engine:
             elif op.kind == "ce":
                 nhwc.wce(self.v(op.ins[0]), self.labels, self.class_weights, self.loss, self.counts,
                          self.gv(op.ins[0]), self.pred, self.ws)
-                self.launches += 2
+                self.launches += 2   # histogram + loss/dlogits + final fold (3 with the +1 below)
             self.launches += 1
 
     # ---------------------------------------------------------------- backward
@@ -418,38 +479,46 @@ class Engine:
             op = st["op"]
             if op.kind == "conv":
                 gy = self.gv(op.out)
-                if op.relu:
+                if st["relu_pass"]:
                     nhwc.relu_mask(gy, self.v(op.out))
                     self.launches += 1
                 w_off, _ = self.slot[op.w]
                 b_off, _ = self.slot[op.b]
-                nhwc.conv_wgrad(self.v(op.ins[0]), gy, op.k, op.k, op.dil,
-                                self.flat_g[w_off:], self.ws, bias_grad=self.flat_g[b_off:b_off + op.cout])
-                self.launches += 4
+                ev = self._tic()
+                nhwc.conv_wgrad(self.v(op.ins[0]), gy, op.k, op.k, op.dil, self.flat_g[w_off:], self.ws)
+                self._toc(ev, op)
+                nhwc.bias_grad(gy, self.flat_g[b_off:b_off + op.cout], self.ws)
+                self.launches += 4   # wgrad GEMM + split-K reduce, bias-grad partial + final
                 if on_param_ready is not None:
                     on_param_ready(op.w)
                     on_param_ready(op.b)
                 if st["dx"] is not None:
+                    ev = self._tic()
                     nhwc.conv_dgrad(gy, self.wd[op.w], op.cin, op.k, op.k, op.dil, self.gv(op.ins[0]),
-                                    accumulate=st["dx"])
+                                    accumulate=st["dx"], mask=self.v(op.ins[0]) if st["mask_dx"] else None)
+                    self._toc(ev, op)
                     self.launches += 1
                 if st["dres"] is not None:
-                    nhwc.add(gy, self.gv(op.res), accumulate=st["dres"])
+                    nhwc.add(gy, self.gv(op.res), accumulate=st["dres"],
+                             mask=self.v(op.res) if st["mask_res"] else None)
                     self.launches += 1
             elif op.kind == "pool":
-                nhwc.avgpool_bwd(self.gv(op.out), self.gv(op.ins[0]), op.factor, accumulate=st["dx"])
+                nhwc.avgpool_bwd(self.gv(op.out), self.gv(op.ins[0]), op.factor, accumulate=st["dx"],
+                                 mask=self.v(op.ins[0]) if st["mask"] else None)
                 self.launches += 1
             elif op.kind == "up":
-                nhwc.upsample_bwd(self.gv(op.out), self.gv(op.ins[0]), op.factor, accumulate=st["dx"])
+                nhwc.upsample_bwd(self.gv(op.out), self.gv(op.ins[0]), op.factor, accumulate=st["dx"],
+                                  mask=self.v(op.ins[0]) if st["mask"] else None)
                 self.launches += 1
             elif op.kind == "concat":
                 root, coff, _ = self.plan.view_spec(op.out)
-                for s, off, acc in st["copies"]:
-                    nhwc.add(View(self.grad[root], coff + off, self.plan.chans(s)), self.gv(s), accumulate=acc)
+                for s, off, acc, m in st["copies"]:
+                    nhwc.add(View(self.grad[root], coff + off, self.plan.chans(s)), self.gv(s), accumulate=acc,
+                             mask=self.v(s) if m else None)
                     self.launches += 1
             elif op.kind == "add":
-                for s, acc in st["acc"]:
-                    nhwc.add(self.gv(op.out), self.gv(s), accumulate=acc)
+                for s, acc, m in st["acc"]:
+                    nhwc.add(self.gv(op.out), self.gv(s), accumulate=acc, mask=self.v(s) if m else None)
                     self.launches += 1
 
     def logits_nchw(self) -> torch.Tensor:

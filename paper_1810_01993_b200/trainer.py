@@ -124,6 +124,7 @@ class DataParallelTrainer:
         o = self.optim
         nhwc.larc_update(eng.flat_w, eng.flat_m, g, eng.offsets, o.lr, o.momentum, o.trust, o.weight_decay,
                          o.eps, 1.0 / self.world, self.lr_out, self.status, eng.ws)
+        eng.launches += 3
         eng.repack()
 
     def step(self, x: torch.Tensor, labels: torch.Tensor) -> torch.Tensor:

@@ -1,0 +1,44 @@
+"""One launch each of the full-resolution conv kernels (fprop, dgrad, wgrad) and the stem
+wgrad, for `ncu --set full` captures (development aid).  Timed with CUDA events too."""
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+from paper_1810_01993_b200 import nhwc  # noqa: E402
+
+torch.manual_seed(0)
+N, H, W, C = 2, 1152, 768, 256
+x = torch.randn(N, H, W, C, device="cuda").to(torch.bfloat16)
+dy = torch.randn(N, H, W, C, device="cuda").to(torch.bfloat16)
+y = torch.empty_like(x)
+w = torch.randn(9, C, C, device="cuda") * 0.02
+wf = torch.empty(C, 9, C, dtype=torch.bfloat16, device="cuda")
+wd = torch.empty(C, 9, C, dtype=torch.bfloat16, device="cuda")
+nhwc.pack_weights(w, 3, 3, C, C, fprop=wf, dgrad=wd)
+b = torch.zeros(C, device="cuda")
+dw = torch.empty(9 * C * C, device="cuda")
+ws = nhwc.Workspace()
+xs = torch.randn(N, H, W, 16, device="cuda").to(torch.bfloat16)
+ys = torch.randn(N, H, W, 64, device="cuda").to(torch.bfloat16)
+dws = torch.empty(49 * 16 * 64, device="cuda")
+ops = {
+    "fprop": lambda: nhwc.conv_fprop(nhwc.View(x), wf, C, 3, 3, 1, nhwc.View(y), bias=b, relu=True),
+    "dgrad": lambda: nhwc.conv_dgrad(nhwc.View(dy), wd, C, 3, 3, 1, nhwc.View(y), mask=nhwc.View(x)),
+    "wgrad": lambda: nhwc.conv_wgrad(nhwc.View(x), nhwc.View(dy), 3, 3, 1, dw, ws),
+    "stem_wgrad": lambda: nhwc.conv_wgrad(nhwc.View(xs), nhwc.View(ys), 7, 7, 1, dws, ws),
+}
+sel = sys.argv[1:] or list(ops)
+for k in sel:
+    ops[k]()
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+for k in sel:
+    e0.record()
+    for _ in range(3):
+        ops[k]()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 3
+    fl = 2 * 9 * C * C * N * H * W if k != "stem_wgrad" else 2 * 49 * 16 * 64 * N * H * W
+    print(f"{k:10s} {ms:.3f} ms  {fl / ms / 1e9:.1f} TF/s", flush=True)
