@@ -390,17 +390,27 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
 }
 
 // ------------------------------------------------------------------ wgrad
-template <int BN>
+// D[(tap, ci)][co] = sum_p x[p + off(tap), ci] * dy[p, co].  One CTA tile covers 256 (tap, ci)
+// rows -- NXC x-chunks of XW channels, two 128-row TMEM accumulators -- against BN output
+// channels, so every dy stage feeds two MMAs (a third less operand traffic per FLOP than a
+// single 128-row tile).  XW = 64 uses SW128 MN-major chunks, XW = 16 (the 16-channel input
+// tile of the stem) SW32 chunks, so no zero-padded channels are multiplied.
+template <int BN, int XW>
 struct WgradCfg {
-  static constexpr int CHUNK = 64 * 64 * 2;  // 64 channels x 64 pixels bf16 = 8 KB
+  static constexpr int XCHUNK = XW * 64 * 2;            // XW channels x 64 pixels, bf16
+  static constexpr int DCHUNK = 64 * 64 * 2;            // 64 out channels x 64 pixels
+  static constexpr int NXC = 256 / XW;                  // x-chunks per tile (2 accumulators)
   static constexpr int NB = BN < 64 ? 1 : BN / 64;
-  static constexpr int A_BYTES = 2 * CHUNK;
-  static constexpr int B_BYTES = NB * CHUNK;
+  static constexpr int A_BYTES = NXC * XCHUNK;
+  static constexpr int B_BYTES = NB * DCHUNK;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (SMEM_BUDGET / STAGE_BYTES) > 8 ? 8 : (SMEM_BUDGET / STAGE_BYTES);
   static constexpr uint32_t TMEM_COLS = tmem_cols_for(2 * BN);
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
   static constexpr int CW = BN < 32 ? BN : 32;
+  static constexpr uint32_t XLAYOUT = XW == 64 ? LAYOUT_SW128 : LAYOUT_SW32;
+  static constexpr uint32_t XSBO = 8 * XW * 2;          // 8 pixel rows
+  static constexpr uint32_t XKSTEP = 16 * XW * 2;       // 16 pixel rows = one UMMA K step
 };
 
 struct WgradParams {
@@ -414,11 +424,11 @@ struct WgradParams {
   float* ws;        // [splits][krows][cout]
 };
 
-template <int BN>
+template <int BN, int XW>
 __global__ void __launch_bounds__(192, 1)
     conv_wgrad_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmDY,
                       const WgradParams p) {
-  using C = WgradCfg<BN>;
+  using C = WgradCfg<BN, XW>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
@@ -427,8 +437,8 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * C::B_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = lane_id();
@@ -439,10 +449,8 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 4);
-    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 4);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
@@ -461,28 +469,25 @@ __global__ void __launch_bounds__(192, 1)
         const int rest = tile / p.m_tiles;
         const int nt = rest % p.n_tiles, split = rest / p.n_tiles;
         const int pb_lo = split * p.pb_per_split, pb_hi = min(p.num_pb, pb_lo + p.pb_per_split);
-        int tx_bytes = C::B_BYTES;
-        if (2 * mt < p.num_x_chunks) tx_bytes += C::CHUNK;
-        if (2 * mt + 1 < p.num_x_chunks) tx_bytes += C::CHUNK;
+        const int c_lo = mt * C::NXC;
+        const int nxc = min(C::NXC, p.num_x_chunks - c_lo);
+        const int tx_bytes = C::B_BYTES + nxc * C::XCHUNK;
         for (int pb = pb_lo; pb < pb_hi; ++pb) {
           const int img = pb / per_img, r = pb - img * per_img;
           const int by = r / p.pbx, bx = r - by * p.pbx;
           const int x0 = bx * p.bwk, y0 = by * p.bhk;
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], tx_bytes);
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            const int chunk = 2 * mt + c;
-            if (chunk < p.num_x_chunks) {
-              const int tap = chunk / p.cblk, cb = chunk - tap * p.cblk;
-              const int i = tap / p.kw, j = tap - i * p.kw;
-              tma_load_4d(sA + stage * C::A_BYTES + c * C::CHUNK, &tmX, &full[stage], cb * 64,
-                          x0 + j * p.dil - p.pad_left, y0 + i * p.dil - p.pad_top, img);
-            }
+          for (int c = 0; c < nxc; ++c) {
+            const int chunk = c_lo + c;
+            const int tap = chunk / p.cblk, cb = chunk - tap * p.cblk;
+            const int i = tap / p.kw, j = tap - i * p.kw;
+            tma_load_4d(sA + stage * C::A_BYTES + c * C::XCHUNK, &tmX, &full[stage], cb * XW,
+                        x0 + j * p.dil - p.pad_left, y0 + i * p.dil - p.pad_top, img);
           }
 #pragma unroll
           for (int qq = 0; qq < C::NB; ++qq)
-            tma_load_4d(sB + stage * C::B_BYTES + qq * C::CHUNK, &tmDY, &full[stage], nt * BN + qq * 64, x0, y0,
+            tma_load_4d(sB + stage * C::B_BYTES + qq * C::DCHUNK, &tmDY, &full[stage], nt * BN + qq * 64, x0, y0,
                         img);
           if (++stage == STAGES) {
             stage = 0;
@@ -498,14 +503,13 @@ __global__ void __launch_bounds__(192, 1)
       uint32_t phase = 0;
       int it = 0;
       for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++it) {
+        const int mt = tile % p.m_tiles;
         const int rest = tile / p.m_tiles;
         const int split = rest / p.n_tiles;
         const int pb_lo = split * p.pb_per_split, pb_hi = min(p.num_pb, pb_lo + p.pb_per_split);
-        const int as = it & 1;
-        const uint32_t ap = (it >> 1) & 1;
-        mbar_wait(&tempty[as], ap ^ 1);
+        const bool second = (mt * C::NXC + C::NXC / 2) < p.num_x_chunks;  // rows 128..255 hold data
+        mbar_wait(tempty, (it & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d = tmem_base + as * BN;
         for (int pb = pb_lo; pb < pb_hi; ++pb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -513,10 +517,15 @@ __global__ void __launch_bounds__(192, 1)
           const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            // MN-major SW128: 64-element MN chunks LBO = 8 KB apart, 8-pixel K groups SBO = 1 KB apart
-            const uint64_t ad = make_sdesc(a0 + k * 2048, C::CHUNK, 1024, LAYOUT_SW128);
-            const uint64_t bd = make_sdesc(b0 + k * 2048, C::CHUNK, 1024, LAYOUT_SW128);
-            umma_bf16(d, ad, bd, idesc, (pb != pb_lo) || (k != 0));
+            const uint32_t acc = (pb != pb_lo) || (k != 0);
+            const uint64_t bd = make_sdesc(b0 + k * 2048, C::DCHUNK, 1024, LAYOUT_SW128);
+            const uint64_t ad0 = make_sdesc(a0 + k * C::XKSTEP, C::XCHUNK, C::XSBO, C::XLAYOUT);
+            umma_bf16(tmem_base, ad0, bd, idesc, acc);
+            if (second) {
+              const uint64_t ad1 =
+                  make_sdesc(a0 + (C::NXC / 2) * C::XCHUNK + k * C::XKSTEP, C::XCHUNK, C::XSBO, C::XLAYOUT);
+              umma_bf16(tmem_base + BN, ad1, bd, idesc, acc);
+            }
           }
           umma_commit(&empty[stage]);
           if (++stage == STAGES) {
@@ -524,51 +533,54 @@ __global__ void __launch_bounds__(192, 1)
             phase ^= 1;
           }
         }
-        umma_commit(&tfull[as]);
+        umma_commit(tfull);
       }
     }
   } else {
     const int q = warp & 3;
-    const int row = q * 32 + lane;
     int it = 0;
     for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++it) {
-      const int as = it & 1;
-      const uint32_t ap = (it >> 1) & 1;
       const int mt = tile % p.m_tiles;
       const int rest = tile / p.m_tiles;
       const int nt = rest % p.n_tiles, split = rest / p.n_tiles;
-      const int chunk = 2 * mt + (row >> 6);
-      const int tap = chunk / p.cblk;
-      const int ci = (chunk - tap * p.cblk) * 64 + (row & 63);
-      const bool valid = chunk < p.num_x_chunks && ci < p.cin;
-      float* dst = p.ws + (static_cast<long long>(split) * p.krows + static_cast<long long>(tap) * p.cin + ci) * p.cout;
-      mbar_wait(&tfull[as], ap);
+      mbar_wait(tfull, it & 1);
       tc_fence_after();
 #pragma unroll 1
-      for (int ch = 0; ch < BN / C::CW; ++ch) {
-        float v[32];
-        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + as * BN + ch * C::CW;
-        if constexpr (C::CW == 32)
-          tmem_ld_32x32b_x32(taddr, v);
-        else
-          tmem_ld_32x32b_x16(taddr, v);
-        const int c0 = nt * BN + ch * C::CW;
-        if (valid && c0 < p.cout) {
-          const int nvalid = min(C::CW, p.cout - c0);
-          if (nvalid == C::CW && (p.cout & 3) == 0) {
+      for (int hh = 0; hh < 2; ++hh) {
+        const int row = hh * 128 + q * 32 + lane;  // tile row = (x-chunk, channel within chunk)
+        const int chunk = mt * C::NXC + row / XW;
+        const int tap = chunk / p.cblk;
+        const int ci = (chunk - tap * p.cblk) * XW + (row % XW);
+        const bool valid = chunk < p.num_x_chunks && ci < p.cin;
+        float* dst =
+            p.ws + (static_cast<long long>(split) * p.krows + static_cast<long long>(tap) * p.cin + ci) * p.cout;
+#pragma unroll 1
+        for (int ch = 0; ch < BN / C::CW; ++ch) {
+          float v[32];
+          const uint32_t taddr =
+              tmem_base + (static_cast<uint32_t>(q * 32) << 16) + hh * BN + ch * C::CW;
+          if constexpr (C::CW == 32)
+            tmem_ld_32x32b_x32(taddr, v);
+          else
+            tmem_ld_32x32b_x16(taddr, v);
+          const int c0 = nt * BN + ch * C::CW;
+          if (valid && c0 < p.cout) {
+            const int nvalid = min(C::CW, p.cout - c0);
+            if (nvalid == C::CW && (p.cout & 3) == 0) {
 #pragma unroll
-            for (int e = 0; e < C::CW; e += 4)
-              *reinterpret_cast<float4*>(dst + c0 + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
-          } else {
+              for (int e = 0; e < C::CW; e += 4)
+                *reinterpret_cast<float4*>(dst + c0 + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+            } else {
 #pragma unroll
-            for (int e = 0; e < C::CW; ++e)
-              if (e < nvalid) dst[c0 + e] = v[e];
+              for (int e = 0; e < C::CW; ++e)
+                if (e < nvalid) dst[c0 + e] = v[e];
+            }
           }
         }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[as]);
+      if (lane == 0) mbar_arrive(tempty);
     }
   }
   tc_fence_before();
@@ -606,10 +618,10 @@ static int launch_fprop(const CUtensorMap& ta, const CUtensorMap& tb, const Fpro
   return check_launch();
 }
 
-template <int BN>
+template <int BN, int XW>
 static int launch_wgrad(const CUtensorMap& tx, const CUtensorMap& tdy, const WgradParams& p, cudaStream_t st) {
-  using C = WgradCfg<BN>;
-  auto kern = conv_wgrad_kernel<BN>;
+  using C = WgradCfg<BN, XW>;
+  auto kern = conv_wgrad_kernel<BN, XW>;
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) != cudaSuccess)
@@ -725,7 +737,7 @@ extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
 namespace b2 {
 struct WgradPlan {
   WgradParams p;
-  int bn;
+  int bn, xw;
   size_t ws_bytes;
 };
 static int plan_wgrad(const b2dl_wgrad_args* a, WgradPlan* out) {
@@ -746,13 +758,14 @@ static int plan_wgrad(const b2dl_wgrad_args* a, WgradPlan* out) {
   p.dil = a->dilation;
   p.pad_top = a->pad_top;
   p.pad_left = a->pad_left;
-  p.cblk = cdiv(x.c, 64);
+  const int xw = x.c <= 16 ? 16 : 64;
+  p.cblk = cdiv(x.c, xw);
   p.num_x_chunks = a->kh * a->kw * p.cblk;
   p.cin = x.c;
   p.cout = dy.c;
   p.krows = static_cast<long long>(a->kh) * a->kw * x.c;
   const int bn = pick_bn(dy.c);
-  p.m_tiles = cdiv(p.num_x_chunks, 2);
+  p.m_tiles = cdiv(p.num_x_chunks, 256 / xw);
   p.n_tiles = cdiv(dy.c, bn);
   int splits = a->splits;
   if (splits <= 0) {
@@ -781,6 +794,7 @@ static int plan_wgrad(const b2dl_wgrad_args* a, WgradPlan* out) {
   p.num_tiles = p.m_tiles * p.n_tiles * p.splits;
   out->p = p;
   out->bn = bn;
+  out->xw = xw;
   out->ws_bytes = static_cast<size_t>(p.splits) * p.krows * p.cout * sizeof(float);
   return B2DL_OK;
 }
@@ -803,16 +817,25 @@ extern "C" int b2dl_conv_wgrad(const b2dl_wgrad_args* a, void* stream) {
   if (!a->workspace || a->workspace_bytes < need) return B2DL_E_VALUE;
   pl.p.ws = reinterpret_cast<float*>(a->workspace);
   CUtensorMap tx, tdy;
-  if (act_map(&tx, a->x, 64, pl.p.bwk, pl.p.bhk, CU_TENSOR_MAP_SWIZZLE_128B)) return B2DL_E_ALIGN;
+  if (act_map(&tx, a->x, pl.xw, pl.p.bwk, pl.p.bhk,
+              pl.xw == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B))
+    return B2DL_E_ALIGN;
   if (act_map(&tdy, a->dy, 64, pl.p.bwk, pl.p.bhk, CU_TENSOR_MAP_SWIZZLE_128B)) return B2DL_E_ALIGN;
   cudaStream_t st = as_stream(stream);
+#define B2_WG(BNV)                                                         \
+  case BNV:                                                                \
+    rc = pl.xw == 64 ? launch_wgrad<BNV, 64>(tx, tdy, pl.p, st) : launch_wgrad<BNV, 16>(tx, tdy, pl.p, st); \
+    break;
   switch (pl.bn) {
-    case 256: rc = launch_wgrad<256>(tx, tdy, pl.p, st); break;
-    case 128: rc = launch_wgrad<128>(tx, tdy, pl.p, st); break;
-    case 64: rc = launch_wgrad<64>(tx, tdy, pl.p, st); break;
-    case 32: rc = launch_wgrad<32>(tx, tdy, pl.p, st); break;
-    default: rc = launch_wgrad<16>(tx, tdy, pl.p, st); break;
+    B2_WG(256)
+    B2_WG(128)
+    B2_WG(64)
+    B2_WG(32)
+    default:
+      rc = pl.xw == 64 ? launch_wgrad<16, 64>(tx, tdy, pl.p, st) : launch_wgrad<16, 16>(tx, tdy, pl.p, st);
+      break;
   }
+#undef B2_WG
   if (rc) return rc;
   const long long total = pl.p.krows * pl.p.cout;
   const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 4LL * num_sms()));

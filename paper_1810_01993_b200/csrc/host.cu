@@ -152,13 +152,14 @@ extern "C" size_t b2dl_conv2d_workspace_size(int n, int cin, int h, int w, int c
   s += static_cast<size_t>(cout) * taps * b2dl_cin_pad(cin) * 2 + 256;                // fprop packed
   s += static_cast<size_t>(cin) * taps * b2dl_cin_pad(cout) * 2 + 256;                // dgrad packed
   s += static_cast<size_t>(cout) * taps * cin * 4 + 256;                              // hwio dw
-  // wgrad split-K partials: bounded by the auto split heuristic (<= 2*SMs tiles)
-  const int xch = taps * ((cin + 63) / 64);
-  const int mt = (xch + 1) / 2;
-  const int nt = (cout + 255) / 256;
-  const int splits = std::max(1, (2 * num_sms() + mt * nt - 1) / (mt * nt));
-  s += static_cast<size_t>(splits) * taps * cin * cout * 4 + 256;
-  s += static_cast<size_t>(cout) * 4 * 1024 + 4096;  // bias-grad partials (unused here)
+  // wgrad split-K partials: exactly what the wgrad planner will ask for
+  b2dl_wgrad_args wa{};
+  wa.x = nhwc(nullptr, n, h, w, cin);
+  wa.dy = nhwc(nullptr, n, h, w, cout);
+  wa.kh = kh;
+  wa.kw = kw;
+  wa.dilation = 1;
+  s += b2dl_wgrad_workspace_size(&wa) + 4096;
   return s;
 }
 
