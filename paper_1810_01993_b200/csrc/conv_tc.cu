@@ -390,27 +390,33 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
 }
 
 // ------------------------------------------------------------------ wgrad
-// D[(tap, ci)][co] = sum_p x[p + off(tap), ci] * dy[p, co].  One CTA tile covers 256 (tap, ci)
-// rows -- NXC x-chunks of XW channels, two 128-row TMEM accumulators -- against BN output
-// channels, so every dy stage feeds two MMAs (a third less operand traffic per FLOP than a
-// single 128-row tile).  XW = 64 uses SW128 MN-major chunks, XW = 16 (the 16-channel input
-// tile of the stem) SW32 chunks, so no zero-padded channels are multiplied.
+// D[(tap, ci)][co] = sum_p x[p + off(tap), ci] * dy[p, co].  A CTA tile covers NACC x 128
+// (tap, ci) rows -- NXC x-chunks of XW channels in NACC TMEM accumulators -- against BN output
+// channels over KP-pixel K blocks.  XW = 64: SW128 MN-major chunks, two accumulators sharing
+// every dy stage (a third less operand traffic per FLOP than one 128-row tile).  XW = 16 (the
+// 16-channel input of the stem): SW32 chunks, no zero-padded channels, 256-pixel K blocks so
+// the 49 per-tap boxes are few and large.
+// The epilogue warps, idle during the main loop, also fold the dy tiles of the row-0 tile
+// into per-channel column sums: the bias gradient (ops.py:172-175) costs no extra pass.
 template <int BN, int XW>
 struct WgradCfg {
-  static constexpr int XCHUNK = XW * 64 * 2;            // XW channels x 64 pixels, bf16
-  static constexpr int DCHUNK = 64 * 64 * 2;            // 64 out channels x 64 pixels
-  static constexpr int NXC = 256 / XW;                  // x-chunks per tile (2 accumulators)
+  static constexpr int KP = XW == 16 ? 256 : 64;          // pixels per K block
+  static constexpr int NACC = XW == 16 ? 1 : 2;           // 128-row TMEM accumulators
+  static constexpr int XCHUNK = XW * KP * 2;              // XW channels x KP pixels, bf16
+  static constexpr int DCHUNK = 64 * KP * 2;              // 64 out channels x KP pixels
+  static constexpr int NXC = NACC * 128 / XW;             // x-chunks per tile
   static constexpr int NB = BN < 64 ? 1 : BN / 64;
   static constexpr int A_BYTES = NXC * XCHUNK;
   static constexpr int B_BYTES = NB * DCHUNK;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (SMEM_BUDGET / STAGE_BYTES) > 8 ? 8 : (SMEM_BUDGET / STAGE_BYTES);
-  static constexpr uint32_t TMEM_COLS = tmem_cols_for(2 * BN);
+  static constexpr uint32_t TMEM_COLS = tmem_cols_for(NACC * BN);
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
   static constexpr int CW = BN < 32 ? BN : 32;
   static constexpr uint32_t XLAYOUT = XW == 64 ? LAYOUT_SW128 : LAYOUT_SW32;
-  static constexpr uint32_t XSBO = 8 * XW * 2;          // 8 pixel rows
-  static constexpr uint32_t XKSTEP = 16 * XW * 2;       // 16 pixel rows = one UMMA K step
+  static constexpr uint32_t XSBO = 8 * XW * 2;            // 8 pixel rows
+  static constexpr uint32_t XKSTEP = 16 * XW * 2;         // 16 pixel rows = one UMMA K step
+  static constexpr int KSTEPS = KP / 16;
 };
 
 struct WgradParams {
@@ -422,6 +428,7 @@ struct WgradParams {
   int cin, cout;
   long long krows;  // taps * cin
   float* ws;        // [splits][krows][cout]
+  float* bsum;      // [splits][cout] partial column sums of dy, or nullptr
 };
 
 template <int BN, int XW>
@@ -447,7 +454,7 @@ __global__ void __launch_bounds__(192, 1)
     tma_prefetch(&tmDY);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], 1 + 4);  // MMA commit + the 4 epilogue warps (dy column sums)
     }
     mbar_init(tfull, 1);
     mbar_init(tempty, 4);
@@ -507,7 +514,7 @@ __global__ void __launch_bounds__(192, 1)
         const int rest = tile / p.m_tiles;
         const int split = rest / p.n_tiles;
         const int pb_lo = split * p.pb_per_split, pb_hi = min(p.num_pb, pb_lo + p.pb_per_split);
-        const bool second = (mt * C::NXC + C::NXC / 2) < p.num_x_chunks;  // rows 128..255 hold data
+        const bool second = C::NACC == 2 && (mt * C::NXC + C::NXC / 2) < p.num_x_chunks;
         mbar_wait(tempty, (it & 1) ^ 1);
         tc_fence_after();
         for (int pb = pb_lo; pb < pb_hi; ++pb) {
@@ -516,7 +523,7 @@ __global__ void __launch_bounds__(192, 1)
           const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
           const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
+          for (int k = 0; k < C::KSTEPS; ++k) {
             const uint32_t acc = (pb != pb_lo) || (k != 0);
             const uint64_t bd = make_sdesc(b0 + k * 2048, C::DCHUNK, 1024, LAYOUT_SW128);
             const uint64_t ad0 = make_sdesc(a0 + k * C::XKSTEP, C::XCHUNK, C::XSBO, C::XLAYOUT);
@@ -538,15 +545,50 @@ __global__ void __launch_bounds__(192, 1)
     }
   } else {
     const int q = warp & 3;
+    const int et = threadIdx.x - 64;  // 0..127
+    // column-sum ownership: thread et sums output channels 2*et, 2*et+1 of the dy tile
+    const int cs_chunk = et / 32, cs_word = et % 32;
+    const bool cs_active = 2 * et < (C::NB * 64 < BN ? C::NB * 64 : BN);
+    int stage = 0;
+    uint32_t phase = 0;
     int it = 0;
     for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++it) {
       const int mt = tile % p.m_tiles;
       const int rest = tile / p.m_tiles;
       const int nt = rest % p.n_tiles, split = rest / p.n_tiles;
+      const int pb_lo = split * p.pb_per_split, pb_hi = min(p.num_pb, pb_lo + p.pb_per_split);
+      const bool do_sum = p.bsum != nullptr && mt == 0 && cs_active;
+      float s0 = 0.f, s1 = 0.f;
+      for (int pb = pb_lo; pb < pb_hi; ++pb) {
+        mbar_wait(&full[stage], phase);
+        if (do_sum) {
+          // dy chunk: KP pixel rows of 128 B (64 channels), 16-byte units XOR-swizzled by row % 8
+          const uint8_t* base = sB + stage * C::B_BYTES + cs_chunk * C::DCHUNK;
+          const int unit = cs_word >> 2, sub = (cs_word & 3) * 4;
+#pragma unroll 8
+          for (int r = 0; r < C::KP; ++r) {
+            const uint32_t v = *reinterpret_cast<const uint32_t*>(base + r * 128 + ((unit ^ (r & 7)) << 4) + sub);
+            s0 += bf16lo(v);
+            s1 += bf16hi(v);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (do_sum) {
+        const int co = nt * BN + 2 * et;
+        float* dst = p.bsum + static_cast<long long>(split) * p.cout;
+        if (co < p.cout) dst[co] = s0;
+        if (co + 1 < p.cout) dst[co + 1] = s1;
+      }
       mbar_wait(tfull, it & 1);
       tc_fence_after();
 #pragma unroll 1
-      for (int hh = 0; hh < 2; ++hh) {
+      for (int hh = 0; hh < C::NACC; ++hh) {
         const int row = hh * 128 + q * 32 + lane;  // tile row = (x-chunk, channel within chunk)
         const int chunk = mt * C::NXC + row / XW;
         const int tap = chunk / p.cblk;
@@ -557,8 +599,7 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll 1
         for (int ch = 0; ch < BN / C::CW; ++ch) {
           float v[32];
-          const uint32_t taddr =
-              tmem_base + (static_cast<uint32_t>(q * 32) << 16) + hh * BN + ch * C::CW;
+          const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + hh * BN + ch * C::CW;
           if constexpr (C::CW == 32)
             tmem_ld_32x32b_x32(taddr, v);
           else
@@ -589,6 +630,16 @@ __global__ void __launch_bounds__(192, 1)
     tc_fence_after();
     tmem_dealloc(tmem_base, C::TMEM_COLS);
   }
+}
+
+// out[c] (+)= sum_s part[s][c]   (fixed order)
+__global__ void bias_reduce_kernel(const float* __restrict__ part, int splits, int c, float* __restrict__ out,
+                                   int accumulate) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= c) return;
+  float s = accumulate ? out[i] : 0.f;
+  for (int k = 0; k < splits; ++k) s += part[static_cast<long long>(k) * c + i];
+  out[i] = s;
 }
 
 // dw[k][co] (+)= sum_s ws[s][k][co]   (fixed summation order -> deterministic)
@@ -671,7 +722,7 @@ extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
       const long long waves = (tiles + num_sms() - 1) / num_sms();
       return speed * static_cast<double>(tiles) / (waves * num_sms());
     };
-    if (score(128, 0.9) > score(256, 1.0)) bn = 128;
+    if (score(128, 0.7) > score(256, 1.0)) bn = 128;
   }
 
   FpropParams p{};
@@ -738,7 +789,7 @@ namespace b2 {
 struct WgradPlan {
   WgradParams p;
   int bn, xw;
-  size_t ws_bytes;
+  size_t ws_bytes, bsum_bytes;
 };
 static int plan_wgrad(const b2dl_wgrad_args* a, WgradPlan* out) {
   const b2dl_act& x = a->x;
@@ -748,9 +799,10 @@ static int plan_wgrad(const b2dl_wgrad_args* a, WgradPlan* out) {
   p.n = x.n;
   p.h = x.h;
   p.w = x.w;
-  p.bwk = pow2_divisor(x.w, 64);
-  if (p.bwk < 8 && x.w >= 8) p.bwk = std::min(64, 1 << (31 - __builtin_clz(x.w)));
-  p.bhk = 64 / p.bwk;
+  const int kp = x.c <= 16 ? 256 : 64;  // WgradCfg<.., XW>::KP
+  p.bwk = pow2_divisor(x.w, kp);
+  if (p.bwk < 8 && x.w >= 8) p.bwk = std::min(kp, 1 << (31 - __builtin_clz(x.w)));
+  p.bhk = kp / p.bwk;
   p.pbx = cdiv(x.w, p.bwk);
   p.pby = cdiv(x.h, p.bhk);
   p.num_pb = x.n * p.pbx * p.pby;
@@ -765,7 +817,7 @@ static int plan_wgrad(const b2dl_wgrad_args* a, WgradPlan* out) {
   p.cout = dy.c;
   p.krows = static_cast<long long>(a->kh) * a->kw * x.c;
   const int bn = pick_bn(dy.c);
-  p.m_tiles = cdiv(p.num_x_chunks, 256 / xw);
+  p.m_tiles = cdiv(p.num_x_chunks, xw == 16 ? 8 : 4);  // WgradCfg::NXC
   p.n_tiles = cdiv(dy.c, bn);
   int splits = a->splits;
   if (splits <= 0) {
@@ -773,7 +825,7 @@ static int plan_wgrad(const b2dl_wgrad_args* a, WgradPlan* out) {
     // >= 32 pixel boxes of K per split so the fp32 partial traffic stays small
     const int base = p.m_tiles * p.n_tiles;
     const int sms = num_sms();
-    const int smax = std::max(1, std::min(64, p.num_pb / 32));
+    const int smax = std::max(1, std::min(sms, p.num_pb / 4));
     double best = -1.0;
     splits = 1;
     for (int s = 1; s <= smax; ++s) {
@@ -796,6 +848,7 @@ static int plan_wgrad(const b2dl_wgrad_args* a, WgradPlan* out) {
   out->bn = bn;
   out->xw = xw;
   out->ws_bytes = static_cast<size_t>(p.splits) * p.krows * p.cout * sizeof(float);
+  out->bsum_bytes = static_cast<size_t>(p.splits) * p.cout * sizeof(float);
   return B2DL_OK;
 }
 }  // namespace b2
@@ -803,8 +856,7 @@ static int plan_wgrad(const b2dl_wgrad_args* a, WgradPlan* out) {
 extern "C" size_t b2dl_wgrad_workspace_size(const b2dl_wgrad_args* a) {
   WgradPlan pl;
   if (!a || plan_wgrad(a, &pl)) return 0;
-  size_t extra = a->bias_grad ? b2dl_bias_grad_workspace_size(a->dy) : 0;
-  return align_up(pl.ws_bytes, 256) + extra;
+  return align_up(pl.ws_bytes, 256) + align_up(pl.bsum_bytes, 256);
 }
 
 extern "C" int b2dl_conv_wgrad(const b2dl_wgrad_args* a, void* stream) {
@@ -816,6 +868,9 @@ extern "C" int b2dl_conv_wgrad(const b2dl_wgrad_args* a, void* stream) {
   const size_t need = b2dl_wgrad_workspace_size(a);
   if (!a->workspace || a->workspace_bytes < need) return B2DL_E_VALUE;
   pl.p.ws = reinterpret_cast<float*>(a->workspace);
+  pl.p.bsum = a->bias_grad ? reinterpret_cast<float*>(reinterpret_cast<char*>(a->workspace) +
+                                                      align_up(pl.ws_bytes, 256))
+                           : nullptr;
   CUtensorMap tx, tdy;
   if (act_map(&tx, a->x, pl.xw, pl.p.bwk, pl.p.bhk,
               pl.xw == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B))
@@ -843,9 +898,9 @@ extern "C" int b2dl_conv_wgrad(const b2dl_wgrad_args* a, void* stream) {
   rc = check_launch();
   if (rc) return rc;
   if (a->bias_grad) {
-    char* extra = reinterpret_cast<char*>(a->workspace) + align_up(pl.ws_bytes, 256);
-    rc = b2dl_bias_grad(a->dy, a->bias_grad, a->accumulate, extra, a->workspace_bytes - align_up(pl.ws_bytes, 256),
-                        stream);
+    bias_reduce_kernel<<<cdiv(pl.p.cout, 128), 128, 0, st>>>(pl.p.bsum, pl.p.splits, pl.p.cout, a->bias_grad,
+                                                             a->accumulate);
+    rc = check_launch();
   }
   return rc;
 }

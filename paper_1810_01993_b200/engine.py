@@ -485,10 +485,11 @@ class Engine:
                 w_off, _ = self.slot[op.w]
                 b_off, _ = self.slot[op.b]
                 ev = self._tic()
-                nhwc.conv_wgrad(self.v(op.ins[0]), gy, op.k, op.k, op.dil, self.flat_g[w_off:], self.ws)
+                # wgrad GEMM with the bias gradient folded in, split-K reduce, bias reduce
+                nhwc.conv_wgrad(self.v(op.ins[0]), gy, op.k, op.k, op.dil, self.flat_g[w_off:], self.ws,
+                                bias_grad=self.flat_g[b_off:b_off + op.cout])
                 self._toc(ev, op)
-                nhwc.bias_grad(gy, self.flat_g[b_off:b_off + op.cout], self.ws)
-                self.launches += 4   # wgrad GEMM + split-K reduce, bias-grad partial + final
+                self.launches += 3
                 if on_param_ready is not None:
                     on_param_ready(op.w)
                     on_param_ready(op.b)
