@@ -557,11 +557,12 @@ __global__ void __launch_bounds__(192, 1)
       const int rest = tile / p.m_tiles;
       const int nt = rest % p.n_tiles, split = rest / p.n_tiles;
       const int pb_lo = split * p.pb_per_split, pb_hi = min(p.num_pb, pb_lo + p.pb_per_split);
-      const bool do_sum = p.bsum != nullptr && mt == 0 && cs_active;
+      // every m-tile of a (split, n-tile) group sums an interleaved 1/m_tiles of the K blocks
+      const bool do_sum = p.bsum != nullptr && cs_active;
       float s0 = 0.f, s1 = 0.f;
       for (int pb = pb_lo; pb < pb_hi; ++pb) {
         mbar_wait(&full[stage], phase);
-        if (do_sum) {
+        if (do_sum && (pb - pb_lo) % p.m_tiles == mt) {
           // dy chunk: KP pixel rows of 128 B (64 channels), 16-byte units XOR-swizzled by row % 8
           const uint8_t* base = sB + stage * C::B_BYTES + cs_chunk * C::DCHUNK;
           const int unit = cs_word >> 2, sub = (cs_word & 3) * 4;
@@ -581,7 +582,7 @@ __global__ void __launch_bounds__(192, 1)
       }
       if (do_sum) {
         const int co = nt * BN + 2 * et;
-        float* dst = p.bsum + static_cast<long long>(split) * p.cout;
+        float* dst = p.bsum + (static_cast<long long>(split) * p.m_tiles + mt) * p.cout;
         if (co < p.cout) dst[co] = s0;
         if (co + 1 < p.cout) dst[co + 1] = s1;
       }
@@ -848,7 +849,7 @@ static int plan_wgrad(const b2dl_wgrad_args* a, WgradPlan* out) {
   out->bn = bn;
   out->xw = xw;
   out->ws_bytes = static_cast<size_t>(p.splits) * p.krows * p.cout * sizeof(float);
-  out->bsum_bytes = static_cast<size_t>(p.splits) * p.cout * sizeof(float);
+  out->bsum_bytes = static_cast<size_t>(p.splits) * p.m_tiles * p.cout * sizeof(float);
   return B2DL_OK;
 }
 }  // namespace b2
@@ -898,8 +899,8 @@ extern "C" int b2dl_conv_wgrad(const b2dl_wgrad_args* a, void* stream) {
   rc = check_launch();
   if (rc) return rc;
   if (a->bias_grad) {
-    bias_reduce_kernel<<<cdiv(pl.p.cout, 128), 128, 0, st>>>(pl.p.bsum, pl.p.splits, pl.p.cout, a->bias_grad,
-                                                             a->accumulate);
+    bias_reduce_kernel<<<cdiv(pl.p.cout, 128), 128, 0, st>>>(pl.p.bsum, pl.p.splits * pl.p.m_tiles, pl.p.cout,
+                                                             a->bias_grad, a->accumulate);
     rc = check_launch();
   }
   return rc;

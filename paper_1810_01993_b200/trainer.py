@@ -71,11 +71,18 @@ class DataParallelTrainer:
         self.status = torch.zeros(1, dtype=torch.int32, device=eng.device)
         self.g_other = torch.zeros_like(eng.flat_g) if lag == 1 else None
         self.have_prev = False
-        # buckets: contiguous parameter ranges, formed from the end of param order
+        self._make_buckets(bucket_mb)
+        self._works = []
+        self.steps_done = 0
+
+    def _make_buckets(self, bucket_mb: float):
+        """Contiguous parameter ranges of >= bucket_mb, formed from the end of param order
+        (the order backward produces gradients); static, hence identical on every rank."""
+        eng = self.eng
         limit = int(bucket_mb * 2 ** 20 / 4)
         self.buckets = []
         cur, size = [], 0
-        for name in reversed(net.param_order):
+        for name in reversed(self.net.param_order):
             cur.append(name)
             size += int(np.prod(eng.slot[name][1]))
             if size >= limit:
@@ -86,12 +93,9 @@ class DataParallelTrainer:
         self.bucket_of = {n: i for i, b in enumerate(self.buckets) for n in b}
         self.bucket_range = []
         for b in self.buckets:
-            offs = [eng.slot[n][0] for n in b]
-            lo = min(offs)
+            lo = min(eng.slot[n][0] for n in b)
             hi = max(eng.slot[n][0] + (int(np.prod(eng.slot[n][1])) + 63) // 64 * 64 for n in b)
             self.bucket_range.append((lo, hi))
-        self._works = []
-        self.steps_done = 0
 
     # ------------------------------------------------------------------ comm
     def _start_bucket(self, i):
