@@ -47,7 +47,7 @@ def _peaks():
 
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+    Q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
@@ -71,7 +71,14 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) >= 8:
-                self.rows.append(parts)
+                self.rows.append([time.time()] + parts[1:])
+
+    def window(self, t0, t1):
+        """Restrict to samples taken in [t0, t1] (host wall clock around the timed region);
+        falls back to all samples under load when the window holds fewer than 3."""
+        sel = [r for r in self.rows if t0 <= r[0] <= t1]
+        if len(sel) >= 3:
+            self.rows = sel
 
     def __exit__(self, *exc):
         if self.proc:
@@ -140,13 +147,14 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    times = cpu_step_time(max(1, args.steps), args.warmup)
+    # bounded: each CPU step is ~6 s on 16 cores, keep the whole arm within a few minutes
+    times = cpu_step_time(max(1, min(args.steps, 8)), min(args.warmup, 1))
     desc, frac = _sample_desc()
     ms = 1e3 * float(np.median(times))
     value = frac / (ms / 1e3)
     cores = os.cpu_count()
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": 0,
-            "steps": len(times), "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "steps": len(times), "warmup": min(args.warmup, 1), "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (make_scene)",
             "config": {"workload": "DeepLabV3+ train step, reference CPU path, bounded sample",
                        "global_batch": CPU_SAMPLE[0], "tile": list(CPU_SAMPLE[1:]), "world_requested": world},
@@ -192,6 +200,7 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    clk = ClockSampler(local).__enter__()   # sampling starts before warm-up (nvidia-smi start-up)
     for i in range(args.warmup):
         tr.step(*batches[i % pool])
     barrier()
@@ -201,13 +210,16 @@ def run_ours(args):
     eng.conv_events = []
     launches0 = eng.launches
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        barrier()
-        e0.record()
-        for i in range(args.steps):
-            tr.step(*batches[i % pool])
-        e1.record()
-        barrier()
+    barrier()
+    t_lo = time.time()
+    e0.record()
+    for i in range(args.steps):
+        tr.step(*batches[i % pool])
+    e1.record()
+    barrier()
+    t_hi = time.time()
+    clk.__exit__(None, None, None)
+    clk.window(t_lo, t_hi)
     eng.conv_timing = False
     launches = eng.launches - launches0
     ms = e0.elapsed_time(e1) / args.steps
@@ -280,7 +292,7 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
