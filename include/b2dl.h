@@ -118,11 +118,28 @@ typedef struct b2dl_wgrad_args {
   int accumulate;
   void* workspace;
   size_t workspace_bytes;
-  int splits; /* 0 = auto */
+  int splits;       /* 0 = auto */
+  int defer_reduce; /* 1: leave the split-K partials in `workspace` (layout from
+                       b2dl_wgrad_partials) for a later batched b2dl_reduce_segments */
 } b2dl_wgrad_args;
 
 B2DL_API size_t b2dl_wgrad_workspace_size(const b2dl_wgrad_args* a);
 B2DL_API int b2dl_conv_wgrad(const b2dl_wgrad_args* a, void* stream);
+/* Partial-sum layout of a deferred wgrad: weight partials [w_parts][taps*cin*cout] at byte 0,
+ * bias partials [b_parts][cout] at byte b_offset of the workspace. */
+B2DL_API int b2dl_wgrad_partials(const b2dl_wgrad_args* a, int* w_parts, int* b_parts, size_t* b_offset);
+
+/* Batched deterministic reduction of split-K partials: for every segment,
+ * dst_base[dst_off + i] (+)= sum_k src[k * n + i], k < parts.  `segs` is device memory. */
+typedef struct b2dl_segment {
+  const float* src;
+  int64_t dst_off;
+  int64_t n;
+  int32_t parts;
+  int32_t accumulate;
+} b2dl_segment;
+B2DL_API int b2dl_reduce_segments(const b2dl_segment* segs, int nseg, int64_t max_n, float* dst_base,
+                                  void* stream);
 
 /* Pack fp32 HWIO master weights into the bf16 fprop layout [cout][taps][cin_pad]
  * and (optionally) the dgrad layout [cin][taps(flipped)][cout_pad]. */

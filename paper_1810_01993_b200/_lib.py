@@ -44,7 +44,13 @@ class WgradArgs(ctypes.Structure):
                 ("dilation", ctypes.c_int), ("pad_top", ctypes.c_int), ("pad_left", ctypes.c_int),
                 ("dw", ctypes.c_void_p), ("bias_grad", ctypes.c_void_p),
                 ("accumulate", ctypes.c_int), ("workspace", ctypes.c_void_p),
-                ("workspace_bytes", ctypes.c_size_t), ("splits", ctypes.c_int)]
+                ("workspace_bytes", ctypes.c_size_t), ("splits", ctypes.c_int),
+                ("defer_reduce", ctypes.c_int)]
+
+
+class Segment(ctypes.Structure):
+    _fields_ = [("src", ctypes.c_void_p), ("dst_off", ctypes.c_int64), ("n", ctypes.c_int64),
+                ("parts", ctypes.c_int32), ("accumulate", ctypes.c_int32)]
 
 
 class LarcArgs(ctypes.Structure):
@@ -68,6 +74,9 @@ _SIGS = {
     "b2dl_conv_fprop": (_c_int, [ctypes.POINTER(ConvArgs), _vp]),
     "b2dl_wgrad_workspace_size": (_sz, [ctypes.POINTER(WgradArgs)]),
     "b2dl_conv_wgrad": (_c_int, [ctypes.POINTER(WgradArgs), _vp]),
+    "b2dl_wgrad_partials": (_c_int, [ctypes.POINTER(WgradArgs), ctypes.POINTER(_c_int), ctypes.POINTER(_c_int),
+                                     ctypes.POINTER(_sz)]),
+    "b2dl_reduce_segments": (_c_int, [_vp, _c_int, ctypes.c_int64, _vp, _vp]),
     "b2dl_pack_weights": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp]),
     "b2dl_nchw_to_nhwc": (_c_int, [_vp, Act, _c_int, _vp]),
     "b2dl_nhwc_to_nchw": (_c_int, [Act, _c_int, _vp, _vp]),

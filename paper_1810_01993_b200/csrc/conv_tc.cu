@@ -633,6 +633,28 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
+// batched segment reduction (deterministic, fixed order over parts)
+__global__ void reduce_segments_kernel(const b2dl_segment* __restrict__ segs, float* __restrict__ base) {
+  const b2dl_segment sg = segs[blockIdx.y];
+  float* dst = base + sg.dst_off;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < sg.n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float s = sg.accumulate ? dst[i] : 0.f;
+    const float* src = sg.src + i;
+    int k = 0;
+    for (; k + 4 <= sg.parts; k += 4) {
+      const float a = __ldg(src + (k + 0) * sg.n), b = __ldg(src + (k + 1) * sg.n);
+      const float c = __ldg(src + (k + 2) * sg.n), d = __ldg(src + (k + 3) * sg.n);
+      s += a;
+      s += b;
+      s += c;
+      s += d;
+    }
+    for (; k < sg.parts; ++k) s += __ldg(src + k * sg.n);
+    dst[i] = s;
+  }
+}
+
 // out[c] (+)= sum_s part[s][c]   (fixed order)
 __global__ void bias_reduce_kernel(const float* __restrict__ part, int splits, int c, float* __restrict__ out,
                                    int accumulate) {
@@ -869,6 +891,7 @@ extern "C" int b2dl_conv_wgrad(const b2dl_wgrad_args* a, void* stream) {
   const size_t need = b2dl_wgrad_workspace_size(a);
   if (!a->workspace || a->workspace_bytes < need) return B2DL_E_VALUE;
   pl.p.ws = reinterpret_cast<float*>(a->workspace);
+  const bool defer = a->defer_reduce != 0;
   pl.p.bsum = a->bias_grad ? reinterpret_cast<float*>(reinterpret_cast<char*>(a->workspace) +
                                                       align_up(pl.ws_bytes, 256))
                            : nullptr;
@@ -893,6 +916,7 @@ extern "C" int b2dl_conv_wgrad(const b2dl_wgrad_args* a, void* stream) {
   }
 #undef B2_WG
   if (rc) return rc;
+  if (defer) return B2DL_OK;
   const long long total = pl.p.krows * pl.p.cout;
   const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 4LL * num_sms()));
   wgrad_reduce_kernel<<<blocks, 256, 0, st>>>(pl.p.ws, a->dw, total, pl.p.splits, a->accumulate);
@@ -904,4 +928,24 @@ extern "C" int b2dl_conv_wgrad(const b2dl_wgrad_args* a, void* stream) {
     rc = check_launch();
   }
   return rc;
+}
+
+extern "C" int b2dl_wgrad_partials(const b2dl_wgrad_args* a, int* w_parts, int* b_parts, size_t* b_offset) {
+  if (!a || !w_parts || !b_parts || !b_offset) return B2DL_E_VALUE;
+  WgradPlan pl;
+  const int rc = plan_wgrad(a, &pl);
+  if (rc) return rc;
+  *w_parts = pl.p.splits;
+  *b_parts = pl.p.splits * pl.p.m_tiles;
+  *b_offset = align_up(pl.ws_bytes, 256);
+  return B2DL_OK;
+}
+
+extern "C" int b2dl_reduce_segments(const b2dl_segment* segs, int nseg, int64_t max_n, float* dst_base,
+                                    void* stream) {
+  if (!segs || nseg < 1 || !dst_base) return B2DL_E_VALUE;
+  const int bx = static_cast<int>(std::max<long long>(1, std::min<long long>((max_n + 255) / 256, 64)));
+  dim3 grid(bx, nseg);
+  reduce_segments_kernel<<<grid, 256, 0, as_stream(stream)>>>(segs, dst_base);
+  return check_launch();
 }

@@ -337,6 +337,25 @@ class Engine:
             self.wf[o.w] = torch.zeros((o.cout, t, nhwc.cin_pad(o.cin)), dtype=bf, device=self.device)
             if o.ins[0] in p.live:
                 self.wd[o.w] = torch.zeros((o.cin, t, nhwc.cin_pad(o.cout)), dtype=bf, device=self.device)
+        # persistent split-K partial buffers (wgrad + bias column sums), reduced per bucket
+        self.partials = {}
+        self.segs = {}
+        total, offs = 0, {}
+        for o in self.convs:
+            nbytes, wp, bp, bo = nhwc.wgrad_partials(self._probe_view(o.ins[0]), self._probe_view(o.out),
+                                                     o.k, o.k, o.dil)
+            offs[o.w] = (total, nbytes, wp, bp, bo)
+            total += (nbytes + 255) // 256 * 256
+        self.partials_buf = torch.empty(max(total, 256), dtype=torch.uint8, device=self.device)
+        for o in self.convs:
+            off, nbytes, wp, bp, bo = offs[o.w]
+            buf = self.partials_buf[off:off + nbytes]
+            self.partials[o.w] = buf
+            base = buf.data_ptr()
+            n_w = o.k * o.k * o.cin * o.cout
+            self.segs[o.w] = (base, self.slot[o.w][0], n_w, wp, 0)
+            self.segs[o.b] = (base + bo, self.slot[o.b][0], o.cout, bp, 0)
+        self.set_buckets([list(param_order)])
         n, c, h, w = input_shape
         self.labels = torch.zeros(n * h * w, dtype=torch.uint8, device=self.device)
         self.pred = torch.zeros(n * h * w, dtype=torch.uint8, device=self.device)
@@ -348,6 +367,25 @@ class Engine:
         self.conv_timing = False
         self.conv_events = []
         self.load_params(params)
+
+    def _probe_view(self, t):
+        # shape-only view for layout queries (pointer-independent)
+        root, off, c = self.plan.view_spec(t)
+        n, h, w, cs, _ = self.plan.buffers[root]
+        return View(torch.empty((n, h, w, cs), dtype=torch.bfloat16, device="meta"), off, c)
+
+    def set_buckets(self, buckets):
+        """Gradient buckets (lists of parameter names): each gets one batched split-K reduction,
+        launched as soon as backward has produced all of its partials."""
+        self.buckets = [list(b) for b in buckets]
+        self.bucket_of = {n: i for i, b in enumerate(self.buckets) for n in b}
+        self.bucket_tables = []
+        for b in self.buckets:
+            segs = [self.segs[n] for n in b if n in self.segs]
+            if not segs:
+                self.bucket_tables.append(None)
+                continue
+            self.bucket_tables.append((nhwc.segment_table(segs, self.device), len(segs), max(sg[2] for sg in segs)))
 
     # ---------------------------------------------------------------- roofline timing
     def _tic(self):
@@ -470,11 +508,19 @@ class Engine:
             self.launches += 1
 
     # ---------------------------------------------------------------- backward
-    def backward(self, on_param_ready=None):
+    def _reduce_bucket(self, i):
+        t = self.bucket_tables[i]
+        if t is not None:
+            table, nseg, max_n = t
+            nhwc.reduce_segments(table, nseg, max_n, self.flat_g)
+            self.launches += 1
+
+    def backward(self, on_bucket_ready=None):
         """Fill flat_g with d loss / d params (param layout HWIO for conv weights).
 
-        `on_param_ready(name)` fires as soon as a parameter's gradient has been
-        enqueued, so the trainer can start bucket all-reduces during backward."""
+        `on_bucket_ready(i)` fires as soon as bucket i's gradients are final (enqueued),
+        so the trainer can start that bucket's all-reduce while backward continues."""
+        pending = [len(b) for b in self.buckets]
         for st in self.plan.backward_program:
             op = st["op"]
             if op.kind == "conv":
@@ -485,14 +531,18 @@ class Engine:
                 w_off, _ = self.slot[op.w]
                 b_off, _ = self.slot[op.b]
                 ev = self._tic()
-                # wgrad GEMM with the bias gradient folded in, split-K reduce, bias reduce
-                nhwc.conv_wgrad(self.v(op.ins[0]), gy, op.k, op.k, op.dil, self.flat_g[w_off:], self.ws,
-                                bias_grad=self.flat_g[b_off:b_off + op.cout])
+                # wgrad GEMM with the bias column sums folded in; split-K partials stay in the
+                # conv's partial buffer until its bucket is reduced in one batched launch
+                nhwc.conv_wgrad_deferred(self.v(op.ins[0]), gy, op.k, op.k, op.dil, self.partials[op.w])
                 self._toc(ev, op)
-                self.launches += 3
-                if on_param_ready is not None:
-                    on_param_ready(op.w)
-                    on_param_ready(op.b)
+                self.launches += 1
+                for name in (op.w, op.b):
+                    i = self.bucket_of[name]
+                    pending[i] -= 1
+                    if pending[i] == 0:
+                        self._reduce_bucket(i)
+                        if on_bucket_ready is not None:
+                            on_bucket_ready(i)
                 if st["dx"] is not None:
                     ev = self._tic()
                     nhwc.conv_dgrad(gy, self.wd[op.w], op.cin, op.k, op.k, op.dil, self.gv(op.ins[0]),

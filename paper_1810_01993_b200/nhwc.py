@@ -12,7 +12,7 @@ from dataclasses import dataclass
 
 import torch
 
-from ._lib import LIB, NULL_ACT, Act, ConvArgs, LarcArgs, WgradArgs, check
+from ._lib import LIB, NULL_ACT, Act, ConvArgs, LarcArgs, Segment, WgradArgs, check
 
 
 def _stream():
@@ -108,6 +108,44 @@ def conv_wgrad(x: View, dy: View, kh: int, kw: int, dilation: int, dw: torch.Ten
     a.workspace = ctypes.c_void_p(buf.data_ptr())
     a.workspace_bytes = buf.numel()
     check(LIB.b2dl_conv_wgrad(ctypes.byref(a), _stream()), "conv_wgrad")
+
+
+def _wgrad_args(x: View, dy: View, kh: int, kw: int, dilation: int, defer: bool):
+    pt, pl = same_pads(kh, dilation)[0], same_pads(kw, dilation)[0]
+    return WgradArgs(x.act(), dy.act(), kh, kw, dilation, pt, pl, None, None, 0, None, 0, 0, int(defer))
+
+
+def wgrad_partials(x: View, dy: View, kh: int, kw: int, dilation: int):
+    """(workspace bytes, weight parts, bias parts, bias byte offset) of a deferred wgrad."""
+    a = _wgrad_args(x, dy, kh, kw, dilation, True)
+    a.bias_grad = ctypes.c_void_p(1)  # bias partials requested (layout query only)
+    nbytes = LIB.b2dl_wgrad_workspace_size(ctypes.byref(a))
+    wp, bp, bo = ctypes.c_int(), ctypes.c_int(), ctypes.c_size_t()
+    check(LIB.b2dl_wgrad_partials(ctypes.byref(a), ctypes.byref(wp), ctypes.byref(bp), ctypes.byref(bo)),
+          "wgrad_partials")
+    return nbytes, wp.value, bp.value, bo.value
+
+
+def conv_wgrad_deferred(x: View, dy: View, kh: int, kw: int, dilation: int, partials: torch.Tensor):
+    """wgrad + bias column sums left as split-K partials in `partials` (see wgrad_partials)."""
+    a = _wgrad_args(x, dy, kh, kw, dilation, True)
+    a.dw = ctypes.c_void_p(partials.data_ptr())        # unused in deferred mode, must be non-null
+    a.bias_grad = ctypes.c_void_p(partials.data_ptr())
+    a.workspace = ctypes.c_void_p(partials.data_ptr())
+    a.workspace_bytes = partials.numel()
+    check(LIB.b2dl_conv_wgrad(ctypes.byref(a), _stream()), "conv_wgrad")
+
+
+def segment_table(segs, device) -> torch.Tensor:
+    """Pack (src_ptr, dst_off, n, parts, accumulate) records into a device array."""
+    arr = (Segment * len(segs))(*[Segment(src, off, n, parts, acc) for src, off, n, parts, acc in segs])
+    host = torch.frombuffer(bytearray(bytes(arr)), dtype=torch.uint8)
+    return host.to(device)
+
+
+def reduce_segments(table: torch.Tensor, nseg: int, max_n: int, dst_base: torch.Tensor):
+    check(LIB.b2dl_reduce_segments(ctypes.c_void_p(table.data_ptr()), nseg, max_n,
+                                   ctypes.c_void_p(dst_base.data_ptr()), _stream()), "reduce_segments")
 
 
 def pack_weights(w_hwio: torch.Tensor, kh: int, kw: int, cin: int, cout: int, fprop=None, dgrad=None):

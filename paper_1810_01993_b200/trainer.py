@@ -72,6 +72,8 @@ class DataParallelTrainer:
         self.g_other = torch.zeros_like(eng.flat_g) if lag == 1 else None
         self.have_prev = False
         self._make_buckets(bucket_mb)
+        # one batched split-K reduction per bucket (a single one on one GPU)
+        eng.set_buckets(self.buckets if self.world > 1 else [list(net.param_order)])
         self._works = []
         self.steps_done = 0
 
@@ -107,15 +109,7 @@ class DataParallelTrainer:
         if self.world == 1:
             self.eng.backward()
             return
-        pending = [len(b) for b in self.buckets]
-
-        def ready(name):
-            i = self.bucket_of[name]
-            pending[i] -= 1
-            if pending[i] == 0:
-                self._start_bucket(i)
-
-        self.eng.backward(on_param_ready=ready)
+        self.eng.backward(on_bucket_ready=self._start_bucket)
 
     def _wait_comm(self):
         for w in self._works:

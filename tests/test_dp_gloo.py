@@ -31,13 +31,20 @@ class FakeEngine:
         self.step = 0
         self.fired = []
 
-    def backward(self, on_param_ready=None):
+    def set_buckets(self, buckets):
+        self.buckets = buckets
+        self.bucket_of = {n: i for i, b in enumerate(buckets) for n in b}
+
+    def backward(self, on_bucket_ready=None):
         self.step += 1
+        pending = [len(b) for b in self.buckets]
         for name in reversed(self.order):          # reverse parameter order, like backward
             lo, (n,) = self.slot[name]
             self.flat_g[lo:lo + n] = (self.rank + 1) * self.step + torch.arange(n) / 7.0
-            if on_param_ready:
-                on_param_ready(name)
+            i = self.bucket_of[name]
+            pending[i] -= 1
+            if pending[i] == 0 and on_bucket_ready:
+                on_bucket_ready(i)
 
 
 def _worker(rank, world, port, q):
@@ -54,6 +61,7 @@ def _worker(rank, world, port, q):
     tr.net = Net()
     # bucket construction through the real constructor logic
     DataParallelTrainer._make_buckets(tr, bucket_mb=4096 * 4 / 2 ** 20)
+    eng.set_buckets(tr.buckets)
     covered = sorted(n for b in tr.buckets for n in b)
     tr._backward_with_overlap()
     tr._wait_comm()
