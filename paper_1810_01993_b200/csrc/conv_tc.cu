@@ -139,9 +139,32 @@ __device__ __forceinline__ void row_put(uint8_t* st, const float* v) {
 }
 
 // bf16 output with aligned views and cout % 8 == 0: coalesced through the staging tile
+// Register prefetch of one cooperative 32 x CW tile (the epilogue's first global operand),
+// issued before the accumulator is ready so the DRAM latency overlaps the MMA main loop.
+template <int CW>
+__device__ __forceinline__ void coop_prefetch(const __nv_bfloat16* base, long long stride, int c0, int cout,
+                                              const CoopRows<CW>& L, uint4* r) {
+  using R = CoopRows<CW>;
+  const int piece = lane_id() % R::PIECES;
+  const bool pv = c0 + piece * 8 < cout;
+#pragma unroll
+  for (int k = 0; k < R::PIECES; ++k)
+    r[k] = (L.ok[k] && pv) ? __ldg(reinterpret_cast<const uint4*>(base + L.pix[k] * stride + c0 + piece * 8))
+                           : make_uint4(0, 0, 0, 0);
+}
+template <int CW>
+__device__ __forceinline__ void coop_stash(const uint4* r, uint8_t* st) {
+  using R = CoopRows<CW>;
+  const int lane = lane_id(), piece = lane % R::PIECES;
+#pragma unroll
+  for (int k = 0; k < R::PIECES; ++k)
+    *reinterpret_cast<uint4*>(st + (k * R::ROWS_PER_IT + lane / R::PIECES) * EPI_ROW + piece * 16) = r[k];
+}
+
+// The first of (residual, mask) present is the prefetched operand `pre` (may be null).
 template <int CW>
 __device__ __forceinline__ void fprop_epilogue_vec(const FpropParams& p, float* v, int c0, const CoopRows<CW>& L,
-                                                   uint8_t* st) {
+                                                   uint8_t* st, const uint4* pre) {
   if (p.bias) {  // one coalesced load per warp, broadcast by shuffles
     const int lane = lane_id();
     const float b = (lane < CW && c0 + lane < p.cout) ? __ldg(p.bias + c0 + lane) : 0.f;
@@ -150,7 +173,10 @@ __device__ __forceinline__ void fprop_epilogue_vec(const FpropParams& p, float* 
   }
   float t[CW];
   if (p.res) {
-    coop_load<CW>(p.res, p.res_stride, c0, p.cout, L, st, true);
+    if (pre)
+      coop_stash<CW>(pre, st);
+    else
+      coop_load<CW>(p.res, p.res_stride, c0, p.cout, L, st, true);
     __syncwarp();
     row_get<CW>(st, t);
 #pragma unroll
@@ -162,7 +188,10 @@ __device__ __forceinline__ void fprop_epilogue_vec(const FpropParams& p, float* 
     for (int i = 0; i < CW; ++i) v[i] = fmaxf(v[i], 0.f);
   }
   if (p.mask) {
-    coop_load<CW>(p.mask, p.mask_stride, c0, p.cout, L, st, true);
+    if (pre && !p.res)
+      coop_stash<CW>(pre, st);
+    else
+      coop_load<CW>(p.mask, p.mask_stride, c0, p.cout, L, st, true);
     __syncwarp();
     row_get<CW>(st, t);
 #pragma unroll
@@ -341,40 +370,40 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
         L.ok[k] = cy < p.h && cx < p.w;
         L.pix[k] = (static_cast<long long>(img) * p.h + cy) * p.w + cx;
       }
+      // prefetch the first global epilogue operand of all of this warp's chunks
+      uint4 pre[NJ][R::PIECES];
+      const __nv_bfloat16* pbase = p.res ? p.res : p.mask;
+      const long long pstride = p.res ? p.res_stride : p.mask_stride;
+      if (vec && pbase) {
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+          const int c0 = nt * BN + (2 * j + half) * C::CW;
+          if (2 * j + half < NCH && c0 < p.cout) coop_prefetch<C::CW>(pbase, pstride, c0, p.cout, L, pre[j]);
+        }
+      }
       mbar_wait(&tfull[as], ap);
       tc_fence_after();
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + as * BN;
-      uint32_t cur[C::CW], nxt[C::CW];
-      if (half < NCH) {
-        if constexpr (C::CW == 32)
-          tmem_ld_issue_x32(tbase + half * C::CW, cur);
-        else
-          tmem_ld_issue_x16(tbase + half * C::CW, cur);
-      }
-      tmem_ld_wait();
 #pragma unroll
       for (int j = 0; j < NJ; ++j) {
         const int ch = 2 * j + half;
         if (ch >= NCH) break;  // warp-uniform
-        if (ch + 2 < NCH) {    // prefetch the next chunk of this warp while this one is processed
-          if constexpr (C::CW == 32)
-            tmem_ld_issue_x32(tbase + (ch + 2) * C::CW, nxt);
-          else
-            tmem_ld_issue_x16(tbase + (ch + 2) * C::CW, nxt);
-        }
+        uint32_t cur[C::CW];
+        if constexpr (C::CW == 32)
+          tmem_ld_issue_x32(tbase + ch * C::CW, cur);
+        else
+          tmem_ld_issue_x16(tbase + ch * C::CW, cur);
+        tmem_ld_wait();
         float v[C::CW];
 #pragma unroll
         for (int i = 0; i < C::CW; ++i) v[i] = __uint_as_float(cur[i]);
         const int c0 = nt * BN + ch * C::CW;
         if (c0 < p.cout) {
           if (vec)
-            fprop_epilogue_vec<C::CW>(p, v, c0, L, st);
+            fprop_epilogue_vec<C::CW>(p, v, c0, L, st, pbase ? pre[j] : nullptr);
           else if (valid)
             fprop_epilogue_scalar<C::CW>(p, v, pix, c0);
         }
-        tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < C::CW; ++i) cur[i] = nxt[i];
       }
       tc_fence_before();
       __syncwarp();

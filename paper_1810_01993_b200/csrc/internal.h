@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <cstddef>
 #include <cstdint>
+#include <cstdio>
 
 #include "../../include/b2dl.h"
 
@@ -16,7 +17,12 @@ int encode_tiled(CUtensorMap* m, CUtensorMapDataType dt, int rank, void* ptr, co
 // 4-D NHWC bf16 activation map: dims (c, w, h, n), box (box_c, box_w, box_h, 1).
 int act_map(CUtensorMap* m, const b2dl_act& a, int box_c, int box_w, int box_h, CUtensorMapSwizzle sw);
 
-inline int check_launch() { return cudaGetLastError() == cudaSuccess ? B2DL_OK : B2DL_E_CUDA; }
+inline int check_launch() {
+  const cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) return B2DL_OK;
+  fprintf(stderr, "b2dl: CUDA error %s\n", cudaGetErrorString(e));
+  return B2DL_E_CUDA;
+}
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 inline int round_up(int a, int b) { return (a + b - 1) / b * b; }
 inline int cdiv(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
