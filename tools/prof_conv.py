@@ -22,10 +22,19 @@ ws = nhwc.Workspace()
 xs = torch.randn(N, H, W, 16, device="cuda").to(torch.bfloat16)
 ys = torch.randn(N, H, W, 64, device="cuda").to(torch.bfloat16)
 dws = torch.empty(49 * 16 * 64, device="cuda")
+x8 = torch.randn(2, 144, 96, 512, device="cuda").to(torch.bfloat16)
+r8 = torch.randn(2, 144, 96, 2048, device="cuda").to(torch.bfloat16)
+y8 = torch.empty_like(r8)
+w8 = torch.randn(1, 512, 2048, device="cuda") * 0.02
+wf8 = torch.empty(2048, 1, 512, dtype=torch.bfloat16, device="cuda")
+nhwc.pack_weights(w8, 1, 1, 512, 2048, fprop=wf8)
+b8 = torch.zeros(2048, device="cuda")
 ops = {
     "fprop": lambda: nhwc.conv_fprop(nhwc.View(x), wf, C, 3, 3, 1, nhwc.View(y), bias=b, relu=True),
     "dgrad": lambda: nhwc.conv_dgrad(nhwc.View(dy), wd, C, 3, 3, 1, nhwc.View(y), mask=nhwc.View(x)),
     "wgrad": lambda: nhwc.conv_wgrad(nhwc.View(x), nhwc.View(dy), 3, 3, 1, dw, ws),
+    "c1x1_fprop": lambda: nhwc.conv_fprop(nhwc.View(x8), wf8, 2048, 1, 1, 1, nhwc.View(y8), bias=b8,
+                                          residual=nhwc.View(r8), relu=True),
     "stem_wgrad": lambda: nhwc.conv_wgrad(nhwc.View(xs), nhwc.View(ys), 7, 7, 1, dws, ws),
 }
 sel = sys.argv[1:] or list(ops)
@@ -40,5 +49,6 @@ for k in sel:
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 3
-    fl = 2 * 9 * C * C * N * H * W if k != "stem_wgrad" else 2 * 49 * 16 * 64 * N * H * W
+    fl = {"stem_wgrad": 2 * 49 * 16 * 64 * N * H * W, "c1x1_fprop": 2 * 512 * 2048 * 2 * 144 * 96}.get(
+        k, 2 * 9 * C * C * N * H * W)
     print(f"{k:10s} {ms:.3f} ms  {fl / ms / 1e9:.1f} TF/s", flush=True)
