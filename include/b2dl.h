@@ -99,6 +99,12 @@ typedef struct b2dl_conv_args {
   int accumulate;
   b2dl_act mask;
   int block_n; /* 0 = auto */
+  /* weight source: 0 = w_packed; 1 = w_master, the forward conv's bf16 HWIO
+   * [kh*kw][cin][cout] copy read as an MN-major operand (forward); 2 = w_master of the
+   * forward conv read tap-flipped as the input gradient's K-major operand (dgrad).
+   * Modes 1/2 need the forward cout % 8 == 0; they remove all weight repacking. */
+  const void* w_master;
+  int w_mode;
 } b2dl_conv_args;
 
 B2DL_API int b2dl_cin_pad(int cin);
@@ -197,7 +203,8 @@ typedef struct b2dl_larc_args {
   void* workspace; /* device scratch */
   size_t workspace_bytes;
   int mode; /* 0: norms + rates + update; 1: rates only (larc_effective_lr);
-               2: update with the caller's lr_out (sgd_step) */
+               2: update with the caller's lr_out (sgd_step); 3: only refresh w_bf16 from w */
+  void* w_bf16; /* optional bf16 mirror of w written by the update (the conv weight operand) */
 } b2dl_larc_args;
 B2DL_API size_t b2dl_larc_workspace_size(int64_t total_elems, int ntensors);
 B2DL_API int b2dl_larc_update(const b2dl_larc_args* a, void* stream);

@@ -36,7 +36,7 @@ class ConvArgs(ctypes.Structure):
                 ("pad_top", ctypes.c_int), ("pad_left", ctypes.c_int), ("y", Act),
                 ("y_f32", ctypes.c_int), ("bias", ctypes.c_void_p), ("residual", Act),
                 ("relu", ctypes.c_int), ("accumulate", ctypes.c_int), ("mask", Act),
-                ("block_n", ctypes.c_int)]
+                ("block_n", ctypes.c_int), ("w_master", ctypes.c_void_p), ("w_mode", ctypes.c_int)]
 
 
 class WgradArgs(ctypes.Structure):
@@ -60,7 +60,7 @@ class LarcArgs(ctypes.Structure):
                 ("weight_decay", ctypes.c_float), ("eps", ctypes.c_float),
                 ("grad_scale", ctypes.c_float), ("lr_out", ctypes.c_void_p),
                 ("status", ctypes.c_void_p), ("workspace", ctypes.c_void_p),
-                ("workspace_bytes", ctypes.c_size_t), ("mode", ctypes.c_int)]
+                ("workspace_bytes", ctypes.c_size_t), ("mode", ctypes.c_int), ("w_bf16", ctypes.c_void_p)]
 
 
 # every symbol include/b2dl.h declares, with its ctypes signature

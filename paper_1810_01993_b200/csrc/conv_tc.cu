@@ -33,10 +33,13 @@ constexpr int SMEM_BUDGET = 200 * 1024;
 __host__ __device__ constexpr uint32_t tmem_cols_for(int n) {
   return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : n <= 256 ? 256 : 512;
 }
-template <int BN, int KBLK>
+template <int BN, int KBLK, bool BMN = false>
 struct FpropCfg {
   static constexpr int A_BYTES = BM * KBLK * 2;
-  static constexpr int B_BYTES = BN * KBLK * 2;
+  // MN-major B (master-layout weights): 64-channel-wide chunks of KBLK K rows
+  static constexpr int B_CHUNK = 64 * KBLK * 2;
+  static constexpr int NBC = BN < 64 ? 1 : BN / 64;
+  static constexpr int B_BYTES = BMN ? NBC * B_CHUNK : BN * KBLK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (SMEM_BUDGET / STAGE_BYTES) > 8 ? 8 : (SMEM_BUDGET / STAGE_BYTES);
   static constexpr uint32_t TMEM_COLS = tmem_cols_for(2 * BN);
@@ -60,6 +63,8 @@ struct FpropParams {
   const __nv_bfloat16* mask;
   long long mask_stride;
   int relu, accumulate, vec_ok;
+  int b_mode;  // 0 packed [cout][taps][cin_pad]; 1 master HWIO, MN-major; 2 master HWIO, dgrad (flipped taps)
+  int taps;
 };
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
@@ -243,11 +248,11 @@ __device__ __forceinline__ void fprop_epilogue_scalar(const FpropParams& p, floa
 
 constexpr int FPROP_THREADS = 320;  // TMA warp, MMA warp, 8 epilogue warps
 
-template <int BN, int KBLK>
+template <int BN, int KBLK, bool BMN>
 __global__ void __launch_bounds__(FPROP_THREADS, 1)
     conv_fprop_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const FpropParams p) {
-  using C = FpropCfg<BN, KBLK>;
+  using C = FpropCfg<BN, KBLK, BMN>;
   constexpr int STAGES = C::STAGES;
   constexpr uint32_t LAYOUT = KBLK == 64 ? LAYOUT_SW128 : LAYOUT_SW32;
   constexpr uint32_t SBO = KBLK * 2 * 8;  // 8 rows of KBLK bf16
@@ -300,7 +305,16 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
           const int i = tap / p.kw, j = tap - i * p.kw;
           tma_load_4d(sA + stage * C::A_BYTES, &tmA, &full[stage], cb * KBLK, x0 + j * p.dil - p.pad_left,
                       y0 + i * p.dil - p.pad_top, img);
-          tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], tap * p.cin_pad + cb * KBLK, n0);
+          if constexpr (BMN) {  // master HWIO weights: box (64 co, KBLK ci, 1 tap) per 64 output channels
+#pragma unroll
+            for (int qq = 0; qq < C::NBC; ++qq)
+              tma_load_3d(sB + stage * C::B_BYTES + qq * C::B_CHUNK, &tmB, &full[stage], n0 + qq * 64, cb * KBLK,
+                          tap);
+          } else if (p.b_mode == 2) {  // dgrad from master HWIO: box (KBLK co, BN ci, flipped tap)
+            tma_load_3d(sB + stage * C::B_BYTES, &tmB, &full[stage], cb * KBLK, n0, p.taps - 1 - tap);
+          } else {
+            tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], tap * p.cin_pad + cb * KBLK, n0);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -310,7 +324,7 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc = make_idesc_bf16(BM, BN, false, false);
+      constexpr uint32_t idesc = make_idesc_bf16(BM, BN, false, BMN);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -328,7 +342,8 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
 #pragma unroll
           for (int k = 0; k < KBLK / 16; ++k) {
             const uint64_t ad = make_sdesc(a0 + k * 32, 16, SBO, LAYOUT);
-            const uint64_t bd = make_sdesc(b0 + k * 32, 16, SBO, LAYOUT);
+            const uint64_t bd = BMN ? make_sdesc(b0 + k * 2048, C::B_CHUNK, 1024, LAYOUT_SW128)
+                                    : make_sdesc(b0 + k * 32, 16, SBO, LAYOUT);
             umma_bf16(d, ad, bd, idesc, (kb | k) != 0);
           }
           umma_commit(&empty[stage]);
@@ -706,10 +721,10 @@ __global__ void wgrad_reduce_kernel(const float* __restrict__ ws, float* __restr
 }
 
 // ------------------------------------------------------------------ host side
-template <int BN, int KBLK>
+template <int BN, int KBLK, bool BMN>
 static int launch_fprop(const CUtensorMap& ta, const CUtensorMap& tb, const FpropParams& p, cudaStream_t st) {
-  using C = FpropCfg<BN, KBLK>;
-  auto kern = conv_fprop_kernel<BN, KBLK>;
+  using C = FpropCfg<BN, KBLK, BMN>;
+  auto kern = conv_fprop_kernel<BN, KBLK, BMN>;
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) != cudaSuccess)
@@ -755,7 +770,7 @@ using namespace b2;
 extern "C" int b2dl_cin_pad(int cin) { return cin <= 16 ? 16 : round_up(cin, 64); }
 
 extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
-  if (!a || !a->x.ptr || !a->w_packed || !a->y.ptr) return B2DL_E_VALUE;
+  if (!a || !a->x.ptr || !a->y.ptr || a->w_mode < 0 || a->w_mode > 2) return B2DL_E_VALUE;
   const b2dl_act& x = a->x;
   const b2dl_act& y = a->y;
   if (x.n != y.n || x.h != y.h || x.w != y.w || y.c != a->cout) return B2DL_E_VALUE;
@@ -813,16 +828,42 @@ extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
   CUtensorMap ta, tb;
   const CUtensorMapSwizzle sw = kblk == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B;
   if (act_map(&ta, x, kblk, p.bw, p.bh, sw)) return B2DL_E_ALIGN;
-  const uint64_t ktot = static_cast<uint64_t>(a->kh) * a->kw * cin_pad;
-  const uint64_t wd[2] = {ktot, static_cast<uint64_t>(a->cout)};
-  const uint64_t ws[1] = {ktot * 2};
-  const uint32_t wb[2] = {static_cast<uint32_t>(kblk), static_cast<uint32_t>(bn)};
-  if (encode_tiled(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a->w_packed), wd, ws, wb, sw))
-    return B2DL_E_ALIGN;
+  const int mode = a->w_mode;
+  p.b_mode = mode;
+  p.taps = a->kh * a->kw;
+  if (mode == 0) {
+    if (!a->w_packed) return B2DL_E_VALUE;
+    const uint64_t ktot = static_cast<uint64_t>(a->kh) * a->kw * cin_pad;
+    const uint64_t wd[2] = {ktot, static_cast<uint64_t>(a->cout)};
+    const uint64_t ws[1] = {ktot * 2};
+    const uint32_t wb[2] = {static_cast<uint32_t>(kblk), static_cast<uint32_t>(bn)};
+    if (encode_tiled(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a->w_packed), wd, ws, wb, sw))
+      return B2DL_E_ALIGN;
+  } else {
+    // master HWIO bf16 [taps][cin_f][cout_f] of the forward conv; fprop: cin_f = x.c, cout_f = cout;
+    // dgrad: the forward conv's cin is our cout and its cout our input channel count
+    if (!a->w_master) return B2DL_E_VALUE;
+    const uint64_t cf = mode == 1 ? static_cast<uint64_t>(a->cout) : static_cast<uint64_t>(x.c);
+    const uint64_t kf = mode == 1 ? static_cast<uint64_t>(x.c) : static_cast<uint64_t>(a->cout);
+    if ((cf * 2) % 16 || (reinterpret_cast<uintptr_t>(a->w_master) & 15)) return B2DL_E_ALIGN;
+    const uint64_t wd[3] = {cf, kf, static_cast<uint64_t>(p.taps)};
+    const uint64_t ws[2] = {cf * 2, cf * kf * 2};
+    if (mode == 1) {
+      const uint32_t wb[3] = {64u, static_cast<uint32_t>(kblk), 1u};
+      if (encode_tiled(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(a->w_master), wd, ws, wb,
+                       CU_TENSOR_MAP_SWIZZLE_128B))
+        return B2DL_E_ALIGN;
+    } else {
+      const uint32_t wb[3] = {static_cast<uint32_t>(kblk), static_cast<uint32_t>(bn), 1u};
+      if (encode_tiled(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(a->w_master), wd, ws, wb, sw))
+        return B2DL_E_ALIGN;
+    }
+  }
 
   cudaStream_t st = as_stream(stream);
-#define B2_FPROP(BNV, KB) \
-  if (bn == BNV && kblk == KB) return launch_fprop<BNV, KB>(ta, tb, p, st);
+#define B2_FPROP(BNV, KB)                                                          \
+  if (bn == BNV && kblk == KB)                                                     \
+    return mode == 1 ? launch_fprop<BNV, KB, true>(ta, tb, p, st) : launch_fprop<BNV, KB, false>(ta, tb, p, st);
   B2_FPROP(256, 64)
   B2_FPROP(128, 64)
   B2_FPROP(64, 64)

@@ -7,6 +7,8 @@
 // Launch 3: m = beta*m + s*g + wd*w ; w -= lr_t * m   (s = grad_scale = 1/P)
 // The reference raises FloatingPointError on a non-finite norm; here a device
 // status word is set and launch 3 leaves every tensor untouched.
+#include <cuda_bf16.h>
+
 #include <algorithm>
 
 #include "internal.h"
@@ -80,21 +82,78 @@ __global__ void k_larc_rates(const double* __restrict__ part, int ntensors, int 
   }
 }
 
+// w, m, g segment update, 4 elements per thread on aligned interiors; optionally also
+// writes the bf16 mirror of w that the conv kernels read as their weight operand.
+__device__ __forceinline__ void larc_one(float* w, float* m, const float* g, __nv_bfloat16* wb, int64_t i, float r,
+                                         float beta, float wd, float gs) {
+  float mv = m[i] * beta;
+  mv += g[i] * gs;
+  const float wv = w[i];
+  if (wd != 0.f) mv += wd * wv;
+  m[i] = mv;
+  const float nw = wv - r * mv;
+  w[i] = nw;
+  if (wb) wb[i] = __float2bfloat16_rn(nw);
+}
+
 __global__ void k_larc_apply(float* __restrict__ w, float* __restrict__ m, const float* __restrict__ g,
-                             const int64_t* __restrict__ off, const float* __restrict__ lr_t, float beta, float wd,
-                             float grad_scale, const int* __restrict__ status) {
+                             __nv_bfloat16* __restrict__ wb, const int64_t* __restrict__ off,
+                             const float* __restrict__ lr_t, float beta, float wd, float grad_scale,
+                             const int* __restrict__ status, int cast_only) {
   if (*status) return;
   const int t = blockIdx.y;
   const int64_t lo = off[t], hi = off[t + 1];
-  const float r = lr_t[t];
-  for (int64_t i = lo + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < hi;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    float mv = m[i] * beta;          // m *= beta
-    mv += g[i] * grad_scale;         // m += g
-    const float wv = w[i];
-    if (wd != 0.f) mv += wd * wv;    // m += wd * w
-    m[i] = mv;
-    w[i] = wv - r * mv;              // w -= f32(lr_eff) * m
+  const float r = cast_only ? 0.f : lr_t[t];
+  const int64_t a0 = (lo + 3) & ~int64_t(3), a1 = hi & ~int64_t(3);
+  const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t nth = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  if (a0 >= a1) {
+    for (int64_t i = lo + tid; i < hi; i += nth) {
+      if (cast_only)
+        wb[i] = __float2bfloat16_rn(w[i]);
+      else
+        larc_one(w, m, g, wb, i, r, beta, wd, grad_scale);
+    }
+    return;
+  }
+  for (int64_t i = lo + tid; i < a0; i += nth) {
+    if (cast_only)
+      wb[i] = __float2bfloat16_rn(w[i]);
+    else
+      larc_one(w, m, g, wb, i, r, beta, wd, grad_scale);
+  }
+  for (int64_t i = a1 + tid; i < hi; i += nth) {
+    if (cast_only)
+      wb[i] = __float2bfloat16_rn(w[i]);
+    else
+      larc_one(w, m, g, wb, i, r, beta, wd, grad_scale);
+  }
+  for (int64_t v = a0 / 4 + tid; v < a1 / 4; v += nth) {
+    float4 wv = reinterpret_cast<float4*>(w)[v];
+    if (!cast_only) {
+      float4 mv = reinterpret_cast<float4*>(m)[v];
+      const float4 gv = reinterpret_cast<const float4*>(g)[v];
+      float* mm = &mv.x;
+      float* ww = &wv.x;
+      const float* gg = &gv.x;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float x = mm[e] * beta;        // m *= beta
+        x += gg[e] * grad_scale;       // m += g
+        if (wd != 0.f) x += wd * ww[e];  // m += wd * w
+        mm[e] = x;
+        ww[e] = ww[e] - r * x;         // w -= f32(lr_eff) * m
+      }
+      reinterpret_cast<float4*>(m)[v] = mv;
+      reinterpret_cast<float4*>(w)[v] = wv;
+    }
+    if (wb) {
+      __nv_bfloat162 lo2 = __floats2bfloat162_rn(wv.x, wv.y), hi2 = __floats2bfloat162_rn(wv.z, wv.w);
+      uint2 u;
+      u.x = *reinterpret_cast<uint32_t*>(&lo2);
+      u.y = *reinterpret_cast<uint32_t*>(&hi2);
+      reinterpret_cast<uint2*>(wb)[v] = u;
+    }
   }
 }
 
@@ -113,10 +172,11 @@ extern "C" int b2dl_larc_update(const b2dl_larc_args* a, void* stream) {
   if (a->workspace_bytes < b2dl_larc_workspace_size(0, a->ntensors)) return B2DL_E_VALUE;
   cudaStream_t st = as_stream(stream);
   double* part = reinterpret_cast<double*>(a->workspace);
-  if (a->mode < 0 || a->mode > 2) return B2DL_E_VALUE;
+  if (a->mode < 0 || a->mode > 3) return B2DL_E_VALUE;
+  if (a->mode == 3 && !a->w_bf16) return B2DL_E_VALUE;
   cudaMemsetAsync(a->status, 0, sizeof(int), st);
   dim3 grid(LARC_SLICES, a->ntensors);
-  if (a->mode != 2) {
+  if (a->mode == 0 || a->mode == 1) {
     k_larc_norms<<<grid, 256, 0, st>>>(a->w, a->g, a->offsets, part);
     const int warps_per_block = 8;
     k_larc_rates<<<(a->ntensors + warps_per_block - 1) / warps_per_block, 32 * warps_per_block, 0, st>>>(
@@ -124,7 +184,8 @@ extern "C" int b2dl_larc_update(const b2dl_larc_args* a, void* stream) {
         a->status);
   }
   if (a->mode == 1) return check_launch();
-  k_larc_apply<<<grid, 256, 0, st>>>(a->w, a->m, a->g, a->offsets, a->lr_out, a->momentum, a->weight_decay,
-                                     a->grad_scale, a->status);
+  k_larc_apply<<<grid, 256, 0, st>>>(a->w, a->m, a->g, reinterpret_cast<__nv_bfloat16*>(a->w_bf16), a->offsets,
+                                     a->lr_out, a->momentum, a->weight_decay, a->grad_scale, a->status,
+                                     a->mode == 3);
   return check_launch();
 }

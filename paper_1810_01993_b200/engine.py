@@ -331,8 +331,16 @@ class Engine:
         self.flat_m = torch.zeros(off, dtype=f32, device=self.device)
         self.offsets = torch.tensor(offsets, dtype=torch.int64, device=self.device)
         self.convs = [o for o in p.ops if o.kind == "conv"]
+        # bf16 mirror of the whole flat parameter buffer, refreshed by the LARC update itself:
+        # conv kernels read it directly as their weight operand (HWIO; MN-major for fprop,
+        # tap-flipped K-major for dgrad).  Only convs with cout % 8 != 0 (the 3-class head)
+        # keep small packed copies.
+        self.flat_wbf = torch.zeros(off, dtype=bf, device=self.device)
+        self._lr_scratch = torch.zeros(len(self.order), dtype=f32, device=self.device)
+        self._status = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.wf, self.wd = {}, {}
-        for o in self.convs:
+        self.packed = [o for o in self.convs if o.cout % 8 != 0]
+        for o in self.packed:
             t = o.k * o.k
             self.wf[o.w] = torch.zeros((o.cout, t, nhwc.cin_pad(o.cin)), dtype=bf, device=self.device)
             if o.ins[0] in p.live:
@@ -388,17 +396,23 @@ class Engine:
             self.bucket_tables.append((nhwc.segment_table(segs, self.device), len(segs), max(sg[2] for sg in segs)))
 
     # ---------------------------------------------------------------- roofline timing
+    def _event(self):
+        # inside a CUDA-graph capture the event must become a graph record node (external)
+        if getattr(self, "graph_events", False):
+            return torch.cuda.Event(enable_timing=True, external=True)
+        return torch.cuda.Event(enable_timing=True)
+
     def _tic(self):
         if not self.conv_timing:
             return None
-        e = torch.cuda.Event(enable_timing=True)
+        e = self._event()
         e.record()
         return e
 
     def _toc(self, ev, op):
         if ev is None:
             return
-        e = torch.cuda.Event(enable_timing=True)
+        e = self._event()
         e.record()
         n, _, h, w = self.plan.shapes[op.out]
         self.conv_events.append((ev, e, 2 * op.k * op.k * op.cin * op.cout * n * h * w))
@@ -451,8 +465,22 @@ class Engine:
     def export_grads(self) -> dict:
         return self._export(self.flat_g)
 
-    def repack(self):
-        for o in self.convs:
+    def wmaster(self, name):
+        off, shp = self.slot[name]
+        return self.flat_wbf[off:off + int(np.prod(shp))]
+
+    def refresh_mirror(self):
+        """bf16 mirror <- flat fp32 parameters (after loading weights from the host)."""
+        nhwc.larc_update(self.flat_w, self.flat_m, self.flat_g, self.offsets, 1.0, 0.0, 1.0, 0.0, 1.0, 1.0,
+                         self._lr_scratch, self._status, self.ws, mode=3, w_bf16=self.flat_wbf)
+        self.launches += 1
+
+    def repack(self, mirror=True):
+        """Refresh the weight operands after an update; the LARC kernel already writes the mirror
+        during training (mirror=False), leaving only the packed copies of ragged-channel convs."""
+        if mirror:
+            self.refresh_mirror()
+        for o in self.packed:
             nhwc.pack_weights(self.wslice(o.w), o.k, o.k, o.cin, o.cout, fprop=self.wf[o.w],
                               dgrad=self.wd.get(o.w))
             self.launches += 1 + (o.w in self.wd)
@@ -477,7 +505,10 @@ class Engine:
                 out = op.out
                 b_off, _ = self.slot[op.b]
                 ev = self._tic()
-                nhwc.conv_fprop(self.v(op.ins[0]), self.wf[op.w], op.cout, op.k, op.k, op.dil, self.v(out),
+                wsrc = dict(w_packed=self.wf[op.w]) if op.w in self.wf else dict(
+                    w_packed=None, w_master=self.wmaster(op.w), w_mode=1)
+                nhwc.conv_fprop(self.v(op.ins[0]), cout=op.cout, kh=op.k, kw=op.k, dilation=op.dil, y=self.v(out),
+                                **wsrc,
                                 bias=self.flat_w[b_off:b_off + op.cout],
                                 residual=self.v(op.res) if op.res else None, relu=op.relu,
                                 y_f32=(out == p.logits_name))
@@ -545,7 +576,9 @@ class Engine:
                             on_bucket_ready(i)
                 if st["dx"] is not None:
                     ev = self._tic()
-                    nhwc.conv_dgrad(gy, self.wd[op.w], op.cin, op.k, op.k, op.dil, self.gv(op.ins[0]),
+                    wsrc = dict(w_dgrad=self.wd[op.w]) if op.w in self.wd else dict(
+                        w_dgrad=None, w_master=self.wmaster(op.w))
+                    nhwc.conv_dgrad(gy, cin=op.cin, kh=op.k, kw=op.k, dilation=op.dil, dx=self.gv(op.ins[0]), **wsrc,
                                     accumulate=st["dx"], mask=self.v(op.ins[0]) if st["mask_dx"] else None)
                     self._toc(ev, op)
                     self.launches += 1

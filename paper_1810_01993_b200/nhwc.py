@@ -66,22 +66,25 @@ def same_pads(k: int, d: int):
     return total // 2, total - total // 2
 
 
-def conv_fprop(x: View, w_packed: torch.Tensor, cout: int, kh: int, kw: int, dilation: int,
+def conv_fprop(x: View, w_packed: torch.Tensor | None, cout: int, kh: int, kw: int, dilation: int,
                y: View, bias=None, residual: View | None = None, relu=False, accumulate=False,
-               mask: View | None = None, y_f32=False, pads=None, block_n=0):
+               mask: View | None = None, y_f32=False, pads=None, block_n=0, w_master=None, w_mode=0):
+    """w_mode 0: w_packed bf16 [cout][taps][cin_pad]; 1: w_master bf16 HWIO of this conv;
+    2: w_master bf16 HWIO of the forward conv whose input gradient this is (see b2dl.h)."""
     pt, pl = pads if pads is not None else (same_pads(kh, dilation)[0], same_pads(kw, dilation)[0])
-    a = ConvArgs(x.act(), ctypes.c_void_p(w_packed.data_ptr()), cout, kh, kw, dilation, pt, pl,
+    a = ConvArgs(x.act(), _ptr(w_packed), cout, kh, kw, dilation, pt, pl,
                  y.act(), int(y_f32), _ptr(bias), _act(residual), int(relu), int(accumulate),
-                 _act(mask), block_n)
+                 _act(mask), block_n, _ptr(w_master), w_mode)
     check(LIB.b2dl_conv_fprop(ctypes.byref(a), _stream()), "conv_fprop")
 
 
-def conv_dgrad(dy: View, w_dgrad: torch.Tensor, cin: int, kh: int, kw: int, dilation: int,
-               dx: View, accumulate=False, mask: View | None = None, dx_f32=False):
-    """Input gradient as a forward conv over dy with tap-flipped weights and 'after' pads."""
+def conv_dgrad(dy: View, w_dgrad: torch.Tensor | None, cin: int, kh: int, kw: int, dilation: int,
+               dx: View, accumulate=False, mask: View | None = None, dx_f32=False, w_master=None):
+    """Input gradient as a forward conv over dy with tap-flipped weights and 'after' pads;
+    weights from the dgrad-packed copy, or straight from the forward conv's bf16 HWIO master."""
     pads = (same_pads(kh, dilation)[1], same_pads(kw, dilation)[1])
     conv_fprop(dy, w_dgrad, cin, kh, kw, dilation, dx, accumulate=accumulate, mask=mask,
-               y_f32=dx_f32, pads=pads)
+               y_f32=dx_f32, pads=pads, w_master=w_master, w_mode=2 if w_master is not None else 0)
 
 
 class Workspace:
@@ -211,11 +214,12 @@ def wce(logits: View, labels: torch.Tensor, class_weights: torch.Tensor, loss_ou
 
 def larc_update(w: torch.Tensor, m: torch.Tensor, g: torch.Tensor, offsets: torch.Tensor,
                 lr: float, momentum: float, trust: float, weight_decay: float, eps: float,
-                grad_scale: float, lr_out: torch.Tensor, status: torch.Tensor, ws: Workspace, mode=0):
+                grad_scale: float, lr_out: torch.Tensor, status: torch.Tensor, ws: Workspace, mode=0,
+                w_bf16: torch.Tensor | None = None):
     nt = offsets.numel() - 1
     need = LIB.b2dl_larc_workspace_size(w.numel(), nt)
     buf = ws.get(need)
     a = LarcArgs(w.data_ptr(), m.data_ptr(), g.data_ptr(), offsets.data_ptr(), nt, lr, momentum,
                  trust, weight_decay, eps, grad_scale, lr_out.data_ptr(), status.data_ptr(),
-                 buf.data_ptr(), buf.numel(), mode)
+                 buf.data_ptr(), buf.numel(), mode, None if w_bf16 is None else w_bf16.data_ptr())
     check(LIB.b2dl_larc_update(ctypes.byref(a), _stream()), "larc_update")

@@ -120,13 +120,58 @@ class DataParallelTrainer:
     def _apply(self, g):
         eng = self.eng
         o = self.optim
+        # LARC + momentum update; the same pass writes the bf16 weight mirror the convs read
         nhwc.larc_update(eng.flat_w, eng.flat_m, g, eng.offsets, o.lr, o.momentum, o.trust, o.weight_decay,
-                         o.eps, 1.0 / self.world, self.lr_out, self.status, eng.ws)
+                         o.eps, 1.0 / self.world, self.lr_out, self.status, eng.ws, w_bf16=eng.flat_wbf)
         eng.launches += 3
-        eng.repack()
+        eng.repack(mirror=False)
+
+    def capture(self, x: torch.Tensor, labels: torch.Tensor, timed: bool = False):
+        """Record one whole training step (every launch, and on N GPUs the bucket all-reduces)
+        into a CUDA graph over static input buffers; later `step` calls copy the batch in and
+        replay it.  `timed` adds graph event nodes around every conv launch (roofline timing).
+        Call after at least one eager step (workspaces sized)."""
+        if self.lag != 0:
+            raise NotImplementedError("graph capture supports lag 0")
+        eng = self.eng
+        self.static_x = torch.empty_like(x)
+        self.static_l = torch.empty_like(labels)
+        self.static_x.copy_(x)
+        self.static_l.copy_(labels)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        launches0 = eng.launches
+        eng.conv_timing, eng.conv_events, eng.graph_events = timed, [], timed
+        with torch.cuda.graph(graph):
+            self._eager_step(self.static_x, self.static_l)
+        eng.graph_events = False
+        self.graph_conv_events = eng.conv_events if timed else []
+        eng.conv_timing, eng.conv_events = False, []
+        self.graph_launches = eng.launches - launches0
+        self.graph = graph
+        torch.cuda.synchronize()
 
     def step(self, x: torch.Tensor, labels: torch.Tensor) -> torch.Tensor:
         """One training step on device-resident inputs; returns the device loss (no host sync)."""
+        g = getattr(self, "graph", None)
+        if g is not None:
+            if x.data_ptr() != self.static_x.data_ptr():
+                self.static_x.copy_(x, non_blocking=True)
+            if labels.data_ptr() != self.static_l.data_ptr():
+                self.static_l.copy_(labels, non_blocking=True)
+            g.replay()
+            self.eng.launches += self.graph_launches
+            self.steps_done += 1
+            return self.eng.loss
+        return self._eager_step(x, labels)
+
+    def graph_conv_totals(self):
+        """(ms, FLOPs) of the conv launches of the most recent replay of a timed graph."""
+        torch.cuda.synchronize()
+        ms = sum(a.elapsed_time(b) for a, b, _ in self.graph_conv_events)
+        return ms, sum(f for _, _, f in self.graph_conv_events)
+
+    def _eager_step(self, x: torch.Tensor, labels: torch.Tensor) -> torch.Tensor:
         eng = self.eng
         eng.set_batch(x, labels)
         eng.forward()

@@ -108,3 +108,30 @@ def test_fprop_fused_epilogue():
     conv = F.conv2d(xr, wr, padding=1).permute(0, 2, 3, 1)
     ref2 = before + torch.where(mask.double() > 0, conv, torch.zeros_like(conv))
     assert _rel(y.tensor(), ref2) < 1e-2
+
+
+@pytest.mark.parametrize("case", [(2, 128, 24, 48, 256, 3, 2), (1, 256, 16, 16, 64, 1, 1), (1, 16, 32, 32, 64, 7, 1),
+                                  (2, 64, 18, 12, 48, 3, 12)])
+def test_master_layout_weight_modes(case):
+    """fprop reading the bf16 HWIO master as an MN-major operand (w_mode 1) and dgrad reading it
+    tap-flipped (w_mode 2) equal the packed-weight paths."""
+    from paper_1810_01993_b200 import nhwc
+    n, cin, h, w, cout, k, d = case
+    torch.manual_seed(1)
+    x = torch.randn(n, h, w, cin, device="cuda").to(torch.bfloat16)
+    dy = torch.randn(n, h, w, cout, device="cuda").to(torch.bfloat16)
+    w_hwio = torch.randn(k * k, cin, cout, device="cuda") / (k * k * cin) ** 0.5
+    wm = w_hwio.to(torch.bfloat16).contiguous()
+    wf = torch.empty(cout, k * k, nhwc.cin_pad(cin), dtype=torch.bfloat16, device="cuda")
+    wd = torch.empty(cin, k * k, nhwc.cin_pad(cout), dtype=torch.bfloat16, device="cuda")
+    nhwc.pack_weights(w_hwio, k, k, cin, cout, fprop=wf, dgrad=wd)
+    y0 = torch.zeros(n, h, w, cout, dtype=torch.bfloat16, device="cuda")
+    y1 = torch.zeros_like(y0)
+    nhwc.conv_fprop(nhwc.View(x), wf, cout, k, k, d, nhwc.View(y0))
+    nhwc.conv_fprop(nhwc.View(x), None, cout, k, k, d, nhwc.View(y1), w_master=wm, w_mode=1)
+    assert _rel(y1, y0) < 1e-6
+    dx0 = torch.zeros(n, h, w, cin, dtype=torch.bfloat16, device="cuda")
+    dx1 = torch.zeros_like(dx0)
+    nhwc.conv_dgrad(nhwc.View(dy), wd, cin, k, k, d, nhwc.View(dx0))
+    nhwc.conv_dgrad(nhwc.View(dy), None, cin, k, k, d, nhwc.View(dx1), w_master=wm)
+    assert _rel(dx1, dx0) < 1e-6

@@ -29,7 +29,12 @@ w8 = torch.randn(1, 512, 2048, device="cuda") * 0.02
 wf8 = torch.empty(2048, 1, 512, dtype=torch.bfloat16, device="cuda")
 nhwc.pack_weights(w8, 1, 1, 512, 2048, fprop=wf8)
 b8 = torch.zeros(2048, device="cuda")
+wbf = w.to(torch.bfloat16).contiguous()   # master HWIO bf16
 ops = {
+    "fprop_mn": lambda: nhwc.conv_fprop(nhwc.View(x), None, C, 3, 3, 1, nhwc.View(y), bias=b, relu=True,
+                                        w_master=wbf, w_mode=1),
+    "dgrad_m": lambda: nhwc.conv_dgrad(nhwc.View(dy), None, C, 3, 3, 1, nhwc.View(y), mask=nhwc.View(x),
+                                       w_master=wbf),
     "fprop": lambda: nhwc.conv_fprop(nhwc.View(x), wf, C, 3, 3, 1, nhwc.View(y), bias=b, relu=True),
     "dgrad": lambda: nhwc.conv_dgrad(nhwc.View(dy), wd, C, 3, 3, 1, nhwc.View(y), mask=nhwc.View(x)),
     "wgrad": lambda: nhwc.conv_wgrad(nhwc.View(x), nhwc.View(dy), 3, 3, 1, dw, ws),
