@@ -165,6 +165,11 @@ B2DL_API int b2dl_upsample_fwd(b2dl_act x, b2dl_act y, int f, void* stream);
 B2DL_API int b2dl_upsample_bwd(b2dl_act dy, b2dl_act dx, int f, int accumulate, b2dl_act mask, void* stream);
 /* y (+)= x, optionally masked by (mask > 0): elementwise-add VJP / fan-out sums. */
 B2DL_API int b2dl_add(b2dl_act x, b2dl_act y, int accumulate, b2dl_act mask, void* stream);
+/* Input gradient of a 1x1 conv with few output channels (the 3-class head): per pixel
+ * dx[ci] (+)= mask * sum_k dy[k] * w[ci][k], w fp32 HWIO [cin][k] (k = dy.c <= 8).  A
+ * memory-bound channel expansion, so it runs on CUDA cores rather than a K=16 GEMM. */
+B2DL_API int b2dl_dgrad_1x1_small(b2dl_act dy, const float* w_hwio, b2dl_act dx, int accumulate, b2dl_act mask,
+                                  void* stream);
 /* in-place g *= (act > 0): relu VJP (ops.py:176-177). */
 B2DL_API int b2dl_relu_mask(b2dl_act g, b2dl_act act, void* stream);
 /* bias gradient: out[c] (+)= sum over pixels of g (ops.py:172-175). */

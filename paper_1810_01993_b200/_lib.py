@@ -86,6 +86,7 @@ _SIGS = {
     "b2dl_upsample_bwd": (_c_int, [Act, Act, _c_int, _c_int, Act, _vp]),
     "b2dl_add": (_c_int, [Act, Act, _c_int, Act, _vp]),
     "b2dl_relu_mask": (_c_int, [Act, Act, _vp]),
+    "b2dl_dgrad_1x1_small": (_c_int, [Act, _vp, Act, _c_int, Act, _vp]),
     "b2dl_bias_grad": (_c_int, [Act, _vp, _c_int, _vp, _sz, _vp]),
     "b2dl_bias_grad_workspace_size": (_sz, [Act]),
     "b2dl_wce": (_c_int, [Act, _vp, _vp, _c_int, _vp, _vp, Act, _c_int, _vp, _vp, _sz, _vp]),

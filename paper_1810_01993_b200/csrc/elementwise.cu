@@ -305,6 +305,59 @@ static int colsum_blocks(long long npix) {
   return static_cast<int>(std::max<long long>(1, std::min<long long>((npix + 31) / 32, 2LL * num_sms())));
 }
 
+
+// dx[p][ci] (+)= mask * sum_k dy[p][k] * w[ci][k]   (1x1 conv, k = dy channels <= 8)
+// weights transposed into shared memory as [k][cin] so a thread's 8 channels are 2 float4 reads
+template <int G>
+__global__ void k_dgrad_1x1_small(const __nv_bfloat16* __restrict__ dy, int dys, int kc,
+                                  const float* __restrict__ w, int cin, __nv_bfloat16* __restrict__ dx, int dxs,
+                                  const __nv_bfloat16* __restrict__ mask, int ms, long long npix, int acc) {
+  extern __shared__ float wsm[];  // [kc][cin]
+  for (int i = threadIdx.x; i < cin * kc; i += blockDim.x) {
+    const int ci = i / kc, k = i - ci * kc;
+    wsm[k * cin + ci] = w[i];
+  }
+  __syncthreads();
+  const int cg = cin / G;
+  const long long total = npix * cg;
+  const bool dy_vec = (dys % 8) == 0 && ((reinterpret_cast<uintptr_t>(dy) & 15) == 0);
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int ch = static_cast<int>(i % cg) * G;
+    const long long p = i / cg;
+    float d[8];
+    if (dy_vec) {
+      ldv<8>(dy + p * dys, d);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) d[k] = k < kc ? ld_bf(dy + p * dys + k) : 0.f;
+    }
+    float v[G];
+#pragma unroll
+    for (int e = 0; e < G; ++e) v[e] = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (k >= kc) break;
+      const float* wr = wsm + k * cin + ch;
+      if constexpr (G == 8) {
+        const float4 a = *reinterpret_cast<const float4*>(wr);
+        const float4 b = *reinterpret_cast<const float4*>(wr + 4);
+        v[0] += d[k] * a.x;
+        v[1] += d[k] * a.y;
+        v[2] += d[k] * a.z;
+        v[3] += d[k] * a.w;
+        v[4] += d[k] * b.x;
+        v[5] += d[k] * b.y;
+        v[6] += d[k] * b.z;
+        v[7] += d[k] * b.w;
+      } else {
+        v[0] += d[k] * wr[0];
+      }
+    }
+    finish<G>(v, mask ? mask + p * ms + ch : nullptr, dx + p * dxs + ch, acc);
+  }
+}
+
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 static bool vec_ok(const b2dl_act& a) { return a.c % 8 == 0 && a.c_stride % 8 == 0 && aligned16(a.ptr); }
 static bool vec_ok(const b2dl_act& a, const b2dl_act& b) { return vec_ok(a) && vec_ok(b); }
@@ -462,4 +515,22 @@ extern "C" int b2dl_pack_weights(const float* w_hwio, int kh, int kw, int cin, i
     return check_launch();
   }
   return B2DL_OK;
+}
+
+extern "C" int b2dl_dgrad_1x1_small(b2dl_act dy, const float* w_hwio, b2dl_act dx, int accumulate, b2dl_act mask,
+                                    void* stream) {
+  if (!dy.ptr || !w_hwio || !dx.ptr || dy.c < 1 || dy.c > 8 || dy.n != dx.n || dy.h != dx.h || dy.w != dx.w)
+    return B2DL_E_VALUE;
+  const long long npix = static_cast<long long>(dx.n) * dx.h * dx.w;
+  const size_t smem = static_cast<size_t>(dx.c) * dy.c * sizeof(float);
+  if (smem > 48 * 1024) return B2DL_E_VALUE;
+  if (vec_ok(dx, dx, mask))
+    k_dgrad_1x1_small<8><<<grid1d(npix * dx.c, 8), 256, smem, as_stream(stream)>>>(
+        CBF(dy.ptr), dy.c_stride, dy.c, w_hwio, dx.c, BF(dx.ptr), dx.c_stride, CBF(mask.ptr), mask.c_stride, npix,
+        accumulate);
+  else
+    k_dgrad_1x1_small<1><<<grid1d(npix * dx.c), 256, smem, as_stream(stream)>>>(
+        CBF(dy.ptr), dy.c_stride, dy.c, w_hwio, dx.c, BF(dx.ptr), dx.c_stride, CBF(mask.ptr), mask.c_stride, npix,
+        accumulate);
+  return check_launch();
 }

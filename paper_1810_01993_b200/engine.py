@@ -195,6 +195,13 @@ class Plan:
         root, off = self.view_of[t]
         return root, off, self.chans(t)
 
+    def gview_spec(self, t):
+        """Gradient view: like the activation view, except a projection-shortcut output whose
+        gradient is, by construction, the residual block's (masked) output gradient."""
+        while t in self.grad_alias:
+            t = self.grad_alias[t]
+        return self.view_spec(t)
+
     # ---------------------------------------------------------------- gradients
     def _liveness(self):
         live = set(self.params)
@@ -206,10 +213,24 @@ class Plan:
             if any(s in live for s in srcs):
                 live.add(op.out)
         self.live = live
+        # residual shortcuts (ops.py:197-198 passes the gradient through unchanged):
+        #  * projection conv P feeding only block C's add: grad(P.out) IS grad(C.out) -> alias
+        #  * identity input x: its pass-through is merged into the next dgrad writing grad(x)
+        users = {}
+        for op in self.ops:
+            for t in list(op.ins) + ([op.res] if op.kind == "conv" and op.res else []):
+                users.setdefault(t, []).append(op)
+        self.grad_alias = {}
+        for op in self.ops:
+            if op.kind == "conv" and op.res:
+                pr = self.producer.get(op.res)
+                if (pr is not None and pr.kind == "conv" and not pr.relu and users.get(op.res) == [op]
+                        and self.view_of[op.res][0] == op.res):
+                    self.grad_alias[op.res] = op.out
         self.grad_buffers = {}
         for t in live:
             if t in self.view_of:
-                root = self.view_of[t][0]
+                root = self.gview_spec(t)[0]
                 n, h, w, _, _ = self.buffers[root]
                 self.grad_buffers[root] = (n, h, w, _r8(self.chans(root)))
         # static backward program: overwrite/accumulate and relu masking decided per contribution.
@@ -237,7 +258,7 @@ class Plan:
             return memo[t]
 
         def claim(t, masked):
-            root, off, c = self.view_spec(t)
+            root, off, c = self.gview_spec(t)
             iv = init[root]
             lo, hi = off, off + c
             contrib[root].append((lo, hi, masked))
@@ -250,14 +271,23 @@ class Plan:
             raise NotImplementedError(f"partially initialised gradient region for {t}")
 
         def inited(t):
-            root, off, c = self.view_spec(t)
+            root, off, c = self.gview_spec(t)
             return sum(max(0, min(off + c, b) - max(off, a)) for a, b in init[root]) > 0
 
         def unmasked_into(t):
-            root, off, c = self.view_spec(t)
+            root, off, c = self.gview_spec(t)
             return any((not m) and min(off + c, b) > max(off, a) for a, b, m in contrib[root])
 
         prog = []
+        pending = {}   # identity shortcut input -> block output whose gradient passes through
+
+        def flush_pending(t):
+            # a pass-through no dgrad absorbed before t's producer runs: plain masked add
+            for r in [r for r in pending if r == t]:
+                src = pending.pop(r)
+                m = maskable(r)
+                prog.append({"op": Op("add", r, (src,)), "acc": [(r, claim(r, m), m)], "passthrough": src})
+
         ce = [o for o in self.ops if o.kind == "ce"]
         if len(ce) != 1 or ce[0].ins[0] != self.logits_name:
             raise NotImplementedError("exactly one softmax_ce on the logits")
@@ -267,16 +297,19 @@ class Plan:
                 continue
             if not inited(op.out):
                 raise NotImplementedError(f"{op.out}: live tensor without gradient contributions")
+            flush_pending(op.out)
             if op.kind == "conv":
                 x, res = op.ins[0], op.res
                 step = {"op": op, "dx": None, "dres": None, "mask_dx": False, "mask_res": False,
-                        "relu_pass": op.relu and unmasked_into(op.out)}
+                        "dx_res": None, "relu_pass": op.relu and unmasked_into(op.out)}
                 if x in self.live:
                     step["mask_dx"] = maskable(x)
+                    gemm_dgrad = not (op.k == 1 and op.cout < 8)
+                    if gemm_dgrad and x in pending:
+                        step["dx_res"] = pending.pop(x)   # pass-through folded into this dgrad
                     step["dx"] = claim(x, step["mask_dx"])
-                if res is not None and res in self.live:
-                    step["mask_res"] = maskable(res)
-                    step["dres"] = claim(res, step["mask_res"])
+                if res is not None and res in self.live and res not in self.grad_alias:
+                    pending[res] = op.out
                 prog.append(step)
             elif op.kind in ("pool", "up"):
                 x = op.ins[0]
@@ -296,6 +329,8 @@ class Plan:
             elif op.kind == "add":
                 prog.append({"op": op, "acc": [(s_, claim(s_, maskable(s_)), maskable(s_))
                                                for s_ in op.ins if s_ in self.live]})
+        for r in list(pending):
+            flush_pending(r)
         self.backward_program = prog
         self.relu_passes = sum(1 for st in prog if st.get("relu_pass"))
 
@@ -431,7 +466,7 @@ class Engine:
         return View(self.act[root], off, c)
 
     def gv(self, t) -> View:
-        root, off, c = self.plan.view_spec(t)
+        root, off, c = self.plan.gview_spec(t)
         return View(self.grad[root], off, c)
 
     def wslice(self, name, buf=None):
@@ -574,18 +609,21 @@ class Engine:
                         self._reduce_bucket(i)
                         if on_bucket_ready is not None:
                             on_bucket_ready(i)
-                if st["dx"] is not None:
+                if st["dx"] is not None and op.k == 1 and op.cout < 8:
+                    # e.g. the 3-class head: a memory-bound channel expansion, not a GEMM
+                    nhwc.dgrad_1x1_small(gy, self.wslice(op.w), self.gv(op.ins[0]), accumulate=st["dx"],
+                                         mask=self.v(op.ins[0]) if st["mask_dx"] else None)
+                    self.launches += 1
+                elif st["dx"] is not None:
                     ev = self._tic()
                     wsrc = dict(w_dgrad=self.wd[op.w]) if op.w in self.wd else dict(
                         w_dgrad=None, w_master=self.wmaster(op.w))
                     nhwc.conv_dgrad(gy, cin=op.cin, kh=op.k, kw=op.k, dilation=op.dil, dx=self.gv(op.ins[0]), **wsrc,
-                                    accumulate=st["dx"], mask=self.v(op.ins[0]) if st["mask_dx"] else None)
+                                    accumulate=st["dx"], mask=self.v(op.ins[0]) if st["mask_dx"] else None,
+                                    residual=self.gv(st["dx_res"]) if st["dx_res"] else None)
                     self._toc(ev, op)
                     self.launches += 1
-                if st["dres"] is not None:
-                    nhwc.add(gy, self.gv(op.res), accumulate=st["dres"],
-                             mask=self.v(op.res) if st["mask_res"] else None)
-                    self.launches += 1
+
             elif op.kind == "pool":
                 nhwc.avgpool_bwd(self.gv(op.out), self.gv(op.ins[0]), op.factor, accumulate=st["dx"],
                                  mask=self.v(op.ins[0]) if st["mask"] else None)
@@ -601,8 +639,9 @@ class Engine:
                              mask=self.v(s) if m else None)
                     self.launches += 1
             elif op.kind == "add":
+                src = st.get("passthrough", op.out)
                 for s, acc, m in st["acc"]:
-                    nhwc.add(self.gv(op.out), self.gv(s), accumulate=acc, mask=self.v(s) if m else None)
+                    nhwc.add(self.gv(src), self.gv(s), accumulate=acc, mask=self.v(s) if m else None)
                     self.launches += 1
 
     def logits_nchw(self) -> torch.Tensor:

@@ -79,11 +79,12 @@ def conv_fprop(x: View, w_packed: torch.Tensor | None, cout: int, kh: int, kw: i
 
 
 def conv_dgrad(dy: View, w_dgrad: torch.Tensor | None, cin: int, kh: int, kw: int, dilation: int,
-               dx: View, accumulate=False, mask: View | None = None, dx_f32=False, w_master=None):
+               dx: View, accumulate=False, mask: View | None = None, dx_f32=False, w_master=None,
+               residual: View | None = None):
     """Input gradient as a forward conv over dy with tap-flipped weights and 'after' pads;
     weights from the dgrad-packed copy, or straight from the forward conv's bf16 HWIO master."""
     pads = (same_pads(kh, dilation)[1], same_pads(kw, dilation)[1])
-    conv_fprop(dy, w_dgrad, cin, kh, kw, dilation, dx, accumulate=accumulate, mask=mask,
+    conv_fprop(dy, w_dgrad, cin, kh, kw, dilation, dx, accumulate=accumulate, mask=mask, residual=residual,
                y_f32=dx_f32, pads=pads, w_master=w_master, w_mode=2 if w_master is not None else 0)
 
 
@@ -186,6 +187,12 @@ def upsample_bwd(dy: View, dx: View, f: int, accumulate=False, mask: View | None
 
 def add(x: View, y: View, accumulate=True, mask: View | None = None):
     check(LIB.b2dl_add(x.act(), y.act(), int(accumulate), _act(mask), _stream()), "add")
+
+
+def dgrad_1x1_small(dy: View, w_hwio: torch.Tensor, dx: View, accumulate=False, mask: View | None = None):
+    """Input gradient of a 1x1 conv with <= 16 output channels on CUDA cores (channel expansion)."""
+    check(LIB.b2dl_dgrad_1x1_small(dy.act(), ctypes.c_void_p(w_hwio.data_ptr()), dx.act(), int(accumulate),
+                                   _act(mask), _stream()), "dgrad_1x1_small")
 
 
 def relu_mask(g: View, act: View):

@@ -167,8 +167,9 @@ def test_trainer_matches_reference_trainer(lag):
     res = train_run(cfg)
     tag = f"lag{lag}_w1"
     assert np.allclose(res.losses, d[tag + "_losses"], rtol=BF16_TOL)
-    for k, v in res.state.items():
-        assert rel(v, d[f"{tag}_state:{k}"]) < 5e-2, k
+    for k, v in res.state.items():   # trajectory agreement after 3 bf16 steps (norm-relative)
+        ref = d[f"{tag}_state:{k}"]
+        assert np.linalg.norm(v - ref) / np.linalg.norm(ref) < 2e-2, k
     assert [s for s, _ in res.digests] == [1, 3]
 
 

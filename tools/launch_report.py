@@ -44,7 +44,7 @@ def main(path, which=1):
         o = st["op"]
         if o.kind == "conv":
             names.append(("wgrad", o))
-            if st["dx"] is not None:
+            if st["dx"] is not None and not (o.k == 1 and o.cout < 8):
                 names.append(("dgrad", o))
     conv_launches = [(k, t) for k, t in step if k.startswith("b2::conv_")]
     print(f"\nconv launches {len(conv_launches)} (expected {len(names)})")
