@@ -473,6 +473,8 @@ struct WgradParams {
   long long krows;  // taps * cin
   float* ws;        // [splits][krows][cout]
   float* bsum;      // [splits][cout] partial column sums of dy, or nullptr
+  int xg;           // x chunks per TMA op (5-D map, channel blocks as an outer box dim); 0 = 4-D map
+  int dyg;          // dy chunks per TMA op (5-D map); 0 = 4-D map
 };
 
 template <int BN, int XW>
@@ -529,17 +531,27 @@ __global__ void __launch_bounds__(192, 1)
           const int x0 = bx * p.bwk, y0 = by * p.bhk;
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], tx_bytes);
-          for (int c = 0; c < nxc; ++c) {
+          // few large TMA ops: a 5-D map loads xg (dyg) 64-channel chunks of one tap per op
+          const int xstep = p.xg ? p.xg : 1;
+          for (int c = 0; c < nxc; c += xstep) {
             const int chunk = c_lo + c;
             const int tap = chunk / p.cblk, cb = chunk - tap * p.cblk;
             const int i = tap / p.kw, j = tap - i * p.kw;
-            tma_load_4d(sA + stage * C::A_BYTES + c * C::XCHUNK, &tmX, &full[stage], cb * XW,
-                        x0 + j * p.dil - p.pad_left, y0 + i * p.dil - p.pad_top, img);
+            if (p.xg)
+              tma_load_5d(sA + stage * C::A_BYTES + c * C::XCHUNK, &tmX, &full[stage], 0,
+                          x0 + j * p.dil - p.pad_left, y0 + i * p.dil - p.pad_top, img, cb);
+            else
+              tma_load_4d(sA + stage * C::A_BYTES + c * C::XCHUNK, &tmX, &full[stage], cb * XW,
+                          x0 + j * p.dil - p.pad_left, y0 + i * p.dil - p.pad_top, img);
           }
+          if (p.dyg) {
+            tma_load_5d(sB + stage * C::B_BYTES, &tmDY, &full[stage], 0, x0, y0, img, nt * BN / 64);
+          } else {
 #pragma unroll
-          for (int qq = 0; qq < C::NB; ++qq)
-            tma_load_4d(sB + stage * C::B_BYTES + qq * C::DCHUNK, &tmDY, &full[stage], nt * BN + qq * 64, x0, y0,
-                        img);
+            for (int qq = 0; qq < C::NB; ++qq)
+              tma_load_4d(sB + stage * C::B_BYTES + qq * C::DCHUNK, &tmDY, &full[stage], nt * BN + qq * 64, x0, y0,
+                          img);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -966,10 +978,27 @@ extern "C" int b2dl_conv_wgrad(const b2dl_wgrad_args* a, void* stream) {
                                                       align_up(pl.ws_bytes, 256))
                            : nullptr;
   CUtensorMap tx, tdy;
-  if (act_map(&tx, a->x, pl.xw, pl.p.bwk, pl.p.bhk,
-              pl.xw == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B))
+  // x: 5-D map (64-ch inner, W, H, N, channel block) when chunks of one tap can be grouped
+  pl.p.xg = 0;
+  if (pl.xw == 64 && a->x.c % 64 == 0) {
+    const int cblk = a->x.c / 64;
+    const int g = cblk % 4 == 0 ? 4 : (cblk % 2 == 0 ? 2 : 1);
+    if (g > 1) {
+      if (act_map5(&tx, a->x, pl.p.bwk, pl.p.bhk, g)) return B2DL_E_ALIGN;
+      pl.p.xg = g;
+    }
+  }
+  if (!pl.p.xg && act_map(&tx, a->x, pl.xw, pl.p.bwk, pl.p.bhk,
+                          pl.xw == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B))
     return B2DL_E_ALIGN;
-  if (act_map(&tdy, a->dy, 64, pl.p.bwk, pl.p.bhk, CU_TENSOR_MAP_SWIZZLE_128B)) return B2DL_E_ALIGN;
+  pl.p.dyg = 0;
+  const int nbw = pl.bn < 64 ? 1 : pl.bn / 64;
+  if (nbw > 1 && a->dy.c % pl.bn == 0) {
+    if (act_map5(&tdy, a->dy, pl.p.bwk, pl.p.bhk, nbw)) return B2DL_E_ALIGN;
+    pl.p.dyg = nbw;
+  } else if (act_map(&tdy, a->dy, 64, pl.p.bwk, pl.p.bhk, CU_TENSOR_MAP_SWIZZLE_128B)) {
+    return B2DL_E_ALIGN;
+  }
   cudaStream_t st = as_stream(stream);
 #define B2_WG(BNV)                                                         \
   case BNV:                                                                \

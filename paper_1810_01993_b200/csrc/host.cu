@@ -62,6 +62,18 @@ int act_map(CUtensorMap* m, const b2dl_act& a, int box_c, int box_w, int box_h, 
   return encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, a.ptr, dims, strides, box, sw);
 }
 
+// 5-D map (64-channel inner, W, H, N, channel block): one box = g chunks of [pixels][64 ch],
+// stored chunk-major in shared memory (the MN-major operand's LBO-separated chunks)
+int act_map5(CUtensorMap* m, const b2dl_act& a, int box_w, int box_h, int g) {
+  const uint64_t cs = static_cast<uint64_t>(a.c_stride) * 2;
+  const uint64_t dims[5] = {64u, static_cast<uint64_t>(a.w), static_cast<uint64_t>(a.h), static_cast<uint64_t>(a.n),
+                            static_cast<uint64_t>(a.c / 64)};
+  const uint64_t strides[4] = {cs, cs * a.w, cs * a.w * a.h, 128u};
+  const uint32_t box[5] = {64u, static_cast<uint32_t>(box_w), static_cast<uint32_t>(box_h), 1u,
+                           static_cast<uint32_t>(g)};
+  return encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, a.ptr, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
 // -------------------------------------------------------------- layout kernels
 // OIHW fp32 -> fprop packed bf16 [cout][taps][cin_pad]  (zero padded)
 __global__ void pack_oihw_fprop(const float* __restrict__ w, __nv_bfloat16* __restrict__ out, int cout, int cin,
