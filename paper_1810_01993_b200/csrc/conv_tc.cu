@@ -33,13 +33,16 @@ constexpr int SMEM_BUDGET = 200 * 1024;
 __host__ __device__ constexpr uint32_t tmem_cols_for(int n) {
   return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : n <= 256 ? 256 : 512;
 }
-template <int BN, int KBLK, bool BMN = false>
+// CG = 2: a CTA pair (cluster of 2 on one TPC) computes a 256-pixel x BN tile with
+// cta_group::2 MMAs; each CTA stages its own 128-pixel A box and half of B's BN rows, so the
+// operand bytes per FLOP drop by a third against a single-CTA 128 x BN tile.
+template <int BN, int KBLK, bool BMN = false, int CG = 1>
 struct FpropCfg {
   static constexpr int A_BYTES = BM * KBLK * 2;
   // MN-major B (master-layout weights): 64-channel-wide chunks of KBLK K rows
   static constexpr int B_CHUNK = 64 * KBLK * 2;
-  static constexpr int NBC = BN < 64 ? 1 : BN / 64;
-  static constexpr int B_BYTES = BMN ? NBC * B_CHUNK : BN * KBLK * 2;
+  static constexpr int NBC = (BN < 64 ? 1 : BN / 64) / CG;  // chunks staged by this CTA
+  static constexpr int B_BYTES = BMN ? NBC * B_CHUNK : BN / CG * KBLK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (SMEM_BUDGET / STAGE_BYTES) > 8 ? 8 : (SMEM_BUDGET / STAGE_BYTES);
   static constexpr uint32_t TMEM_COLS = tmem_cols_for(2 * BN);
@@ -248,11 +251,11 @@ __device__ __forceinline__ void fprop_epilogue_scalar(const FpropParams& p, floa
 
 constexpr int FPROP_THREADS = 320;  // TMA warp, MMA warp, 8 epilogue warps
 
-template <int BN, int KBLK, bool BMN>
+template <int BN, int KBLK, bool BMN, int CG>
 __global__ void __launch_bounds__(FPROP_THREADS, 1)
     conv_fprop_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const FpropParams p) {
-  using C = FpropCfg<BN, KBLK, BMN>;
+  using C = FpropCfg<BN, KBLK, BMN, CG>;
   constexpr int STAGES = C::STAGES;
   constexpr uint32_t LAYOUT = KBLK == 64 ? LAYOUT_SW128 : LAYOUT_SW32;
   constexpr uint32_t SBO = KBLK * 2 * 8;  // 8 rows of KBLK bf16
@@ -269,6 +272,8 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = lane_id();
+  // CTA pair: rank 0 issues the MMAs and owns the operand-full / accumulator-empty barriers
+  const int rank = CG == 2 ? static_cast<int>(cluster_ctarank()) : 0;
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
@@ -278,42 +283,69 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 8);
+      mbar_init(&tempty[s], 8 * CG);
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  if (warp == 1) {
+    if constexpr (CG == 2)
+      tmem_alloc_pair(tmem_slot, C::TMEM_COLS);
+    else
+      tmem_alloc(tmem_slot, C::TMEM_COLS);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2)
+    cluster_sync();
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int per_img = p.tiles_x * p.tiles_y;
+  const int unit0 = blockIdx.x / CG, units = gridDim.x / CG;
 
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-        const int mt = tile / p.num_n_tiles, nt = tile - mt * p.num_n_tiles;
+      for (int tile = unit0; tile < p.num_tiles; tile += units) {
+        const int pmt = tile / p.num_n_tiles, nt = tile - pmt * p.num_n_tiles;
+        const int mt = pmt * CG + rank;
         const int img = mt / per_img, r = mt - img * per_img;
         const int ty = r / p.tiles_x, tx = r - ty * p.tiles_x;
-        const int y0 = ty * p.bh, x0 = tx * p.bw, n0 = nt * BN;
+        const int y0 = ty * p.bh, x0 = tx * p.bw, n0 = nt * BN + rank * (BN / CG);
         for (int kb = 0; kb < p.num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
           const int tap = kb / p.num_cblk, cb = kb - tap * p.num_cblk;
           const int i = tap / p.kw, j = tap - i * p.kw;
-          tma_load_4d(sA + stage * C::A_BYTES, &tmA, &full[stage], cb * KBLK, x0 + j * p.dil - p.pad_left,
-                      y0 + i * p.dil - p.pad_top, img);
-          if constexpr (BMN) {  // master HWIO weights: box (64 co, KBLK ci, 1 tap) per 64 output channels
+          uint8_t* a_dst = sA + stage * C::A_BYTES;
+          uint8_t* b_dst = sB + stage * C::B_BYTES;
+          const int ax = x0 + j * p.dil - p.pad_left, ay = y0 + i * p.dil - p.pad_top;
+          if constexpr (CG == 2) {
+            // both CTAs' loads complete on the even CTA's barrier, which expects both halves
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+            const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
+            tma_load_4d_pair(a_dst, &tmA, fb, cb * KBLK, ax, ay, img);
+            if constexpr (BMN) {
 #pragma unroll
-            for (int qq = 0; qq < C::NBC; ++qq)
-              tma_load_3d(sB + stage * C::B_BYTES + qq * C::B_CHUNK, &tmB, &full[stage], n0 + qq * 64, cb * KBLK,
-                          tap);
-          } else if (p.b_mode == 2) {  // dgrad from master HWIO: box (KBLK co, BN ci, flipped tap)
-            tma_load_3d(sB + stage * C::B_BYTES, &tmB, &full[stage], cb * KBLK, n0, p.taps - 1 - tap);
+              for (int qq = 0; qq < C::NBC; ++qq)
+                tma_load_3d_pair(b_dst + qq * C::B_CHUNK, &tmB, fb, n0 + qq * 64, cb * KBLK, tap);
+            } else if (p.b_mode == 2) {
+              tma_load_3d_pair(b_dst, &tmB, fb, cb * KBLK, n0, p.taps - 1 - tap);
+            } else {
+              tma_load_2d_pair(b_dst, &tmB, fb, tap * p.cin_pad + cb * KBLK, n0);
+            }
           } else {
-            tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], tap * p.cin_pad + cb * KBLK, n0);
+            mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+            tma_load_4d(a_dst, &tmA, &full[stage], cb * KBLK, ax, ay, img);
+            if constexpr (BMN) {  // master HWIO weights: box (64 co, KBLK ci, 1 tap) per 64 output channels
+#pragma unroll
+              for (int qq = 0; qq < C::NBC; ++qq)
+                tma_load_3d(b_dst + qq * C::B_CHUNK, &tmB, &full[stage], n0 + qq * 64, cb * KBLK, tap);
+            } else if (p.b_mode == 2) {  // dgrad from master HWIO: box (KBLK co, BN ci, flipped tap)
+              tma_load_3d(b_dst, &tmB, &full[stage], cb * KBLK, n0, p.taps - 1 - tap);
+            } else {
+              tma_load_2d(b_dst, &tmB, &full[stage], tap * p.cin_pad + cb * KBLK, n0);
+            }
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -323,12 +355,12 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = make_idesc_bf16(BM, BN, false, BMN);
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = make_idesc_bf16(BM * CG, BN, false, BMN);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++it) {
+      for (int tile = unit0; tile < p.num_tiles; tile += units, ++it) {
         const int as = it & 1;
         const uint32_t ap = (it >> 1) & 1;
         mbar_wait(&tempty[as], ap ^ 1);
@@ -344,15 +376,24 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
             const uint64_t ad = make_sdesc(a0 + k * 32, 16, SBO, LAYOUT);
             const uint64_t bd = BMN ? make_sdesc(b0 + k * 2048, C::B_CHUNK, 1024, LAYOUT_SW128)
                                     : make_sdesc(b0 + k * 32, 16, SBO, LAYOUT);
-            umma_bf16(d, ad, bd, idesc, (kb | k) != 0);
+            if constexpr (CG == 2)
+              umma_bf16_pair(d, ad, bd, idesc, (kb | k) != 0);
+            else
+              umma_bf16(d, ad, bd, idesc, (kb | k) != 0);
           }
-          umma_commit(&empty[stage]);
+          if constexpr (CG == 2)
+            umma_commit_pair(&empty[stage]);
+          else
+            umma_commit(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(&tfull[as]);
+        if constexpr (CG == 2)
+          umma_commit_pair(&tfull[as]);
+        else
+          umma_commit(&tfull[as]);
       }
     }
   } else {
@@ -368,21 +409,22 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
     constexpr int NCH = BN / C::CW;
     constexpr int NJ = (NCH + 1) / 2;
     int it = 0;
-    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++it) {
+    for (int tile = unit0; tile < p.num_tiles; tile += units, ++it) {
       const int as = it & 1;
       const uint32_t ap = (it >> 1) & 1;
-      const int mt = tile / p.num_n_tiles, nt = tile - mt * p.num_n_tiles;
+      const int pmt = tile / p.num_n_tiles, nt = tile - pmt * p.num_n_tiles;
+      const int mt = pmt * CG + rank;
       const int img = mt / per_img, r = mt - img * per_img;
       const int ty = r / p.tiles_x, tx = r - ty * p.tiles_x;
       const int yy = ty * p.bh + ry, xx = tx * p.bw + rx;
-      const bool valid = yy < p.h && xx < p.w;
+      const bool valid = img < p.n && yy < p.h && xx < p.w;  // odd pair count: the last odd CTA idles
       const long long pix = (static_cast<long long>(img) * p.h + yy) * p.w + xx;
       R L;
 #pragma unroll
       for (int k = 0; k < R::PIECES; ++k) {
         const int rr = q * 32 + k * R::ROWS_PER_IT + lane / R::PIECES;
         const int cy = ty * p.bh + rr / p.bw, cx = tx * p.bw + rr % p.bw;
-        L.ok[k] = cy < p.h && cx < p.w;
+        L.ok[k] = img < p.n && cy < p.h && cx < p.w;
         L.pix[k] = (static_cast<long long>(img) * p.h + cy) * p.w + cx;
       }
       // prefetch the first global epilogue operand of all of this warp's chunks
@@ -422,14 +464,25 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[as]);
+      if (lane == 0) {
+        if constexpr (CG == 2)
+          mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[as]), 0));
+        else
+          mbar_arrive(&tempty[as]);
+      }
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2)
+    cluster_sync();
+  else
+    __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, C::TMEM_COLS);
+    if constexpr (CG == 2)
+      tmem_dealloc_pair(tmem_base, C::TMEM_COLS);
+    else
+      tmem_dealloc(tmem_base, C::TMEM_COLS);
   }
 }
 
@@ -733,18 +786,39 @@ __global__ void wgrad_reduce_kernel(const float* __restrict__ ws, float* __restr
 }
 
 // ------------------------------------------------------------------ host side
-template <int BN, int KBLK, bool BMN>
+template <int BN, int KBLK, bool BMN, int CG>
 static int launch_fprop(const CUtensorMap& ta, const CUtensorMap& tb, const FpropParams& p, cudaStream_t st) {
-  using C = FpropCfg<BN, KBLK, BMN>;
-  auto kern = conv_fprop_kernel<BN, KBLK, BMN>;
+  using C = FpropCfg<BN, KBLK, BMN, CG>;
+  auto kern = conv_fprop_kernel<BN, KBLK, BMN, CG>;
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) != cudaSuccess)
       return B2DL_E_CUDA;
     attr_set = true;
   }
-  const int grid = std::min(p.num_tiles, num_sms());
-  kern<<<grid, FPROP_THREADS, C::SMEM, st>>>(ta, tb, p);
+  if constexpr (CG == 1) {
+    const int grid = std::min(p.num_tiles, num_sms());
+    kern<<<grid, FPROP_THREADS, C::SMEM, st>>>(ta, tb, p);
+  } else {
+    const int grid = CG * std::min(p.num_tiles, num_sms() / CG);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(FPROP_THREADS);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, p);
+    if (e != cudaSuccess) {
+      fprintf(stderr, "b2dl: CUDA error %s\n", cudaGetErrorString(e));
+      return B2DL_E_CUDA;
+    }
+  }
   return check_launch();
 }
 
@@ -761,6 +835,15 @@ static int launch_wgrad(const CUtensorMap& tx, const CUtensorMap& tdy, const Wgr
   const int grid = std::min(p.num_tiles, num_sms());
   kern<<<grid, 192, C::SMEM, st>>>(tx, tdy, p);
   return check_launch();
+}
+
+// CTA-pair fprop/dgrad for 256-wide tiles; B2DL_FPROP_PAIRS=0 selects single-CTA tiles
+static bool fprop_pairs_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("B2DL_FPROP_PAIRS");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 static int pick_bn(int cout) {
@@ -791,18 +874,22 @@ extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
   const int kblk = x.c <= 16 ? 16 : 64;
   const int cin_pad = b2dl_cin_pad(x.c);
   int bn = a->block_n ? a->block_n : pick_bn(a->cout);
+  // 256-wide N tiles run as CTA pairs (256 x 256 per pair)
+  auto pair_ok = [&](int b) { return b == 256 && kblk == 64 && fprop_pairs_enabled(); };
   if (!a->block_n && bn == 256) {
     // wave quantisation: a narrower N tile can fill the last wave of a small map better
     const int bw = pow2_divisor(x.w, 128) < 8 && x.w >= 8 ? std::min(128, 1 << (31 - __builtin_clz(x.w)))
                                                          : pow2_divisor(x.w, 128);
     const long long mt = static_cast<long long>(x.n) * cdiv(x.w, bw) * cdiv(x.h, BM / bw);
     auto score = [&](int b, double speed) {
-      const long long tiles = mt * cdiv(a->cout, b);
-      const long long waves = (tiles + num_sms() - 1) / num_sms();
-      return speed * static_cast<double>(tiles) / (waves * num_sms());
+      const int g = pair_ok(b) ? 2 : 1;
+      const long long units = (mt + g - 1) / g * cdiv(a->cout, b), slots = num_sms() / g;
+      const long long waves = (units + slots - 1) / slots;
+      return speed * static_cast<double>(units) / (waves * slots);
     };
     if (score(128, 0.7) > score(256, 1.0)) bn = 128;
   }
+  const int cg = pair_ok(bn) ? 2 : 1;
 
   FpropParams p{};
   p.n = x.n;
@@ -815,7 +902,7 @@ extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
   p.tiles_y = cdiv(x.h, p.bh);
   p.num_m_tiles = x.n * p.tiles_x * p.tiles_y;
   p.num_n_tiles = cdiv(a->cout, bn);
-  p.num_tiles = p.num_m_tiles * p.num_n_tiles;
+  p.num_tiles = cdiv(p.num_m_tiles, cg) * p.num_n_tiles;  // scheduling units: tiles or tile pairs
   p.kw = a->kw;
   p.dil = a->dilation;
   p.pad_top = a->pad_top;
@@ -848,7 +935,7 @@ extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
     const uint64_t ktot = static_cast<uint64_t>(a->kh) * a->kw * cin_pad;
     const uint64_t wd[2] = {ktot, static_cast<uint64_t>(a->cout)};
     const uint64_t ws[1] = {ktot * 2};
-    const uint32_t wb[2] = {static_cast<uint32_t>(kblk), static_cast<uint32_t>(bn)};
+    const uint32_t wb[2] = {static_cast<uint32_t>(kblk), static_cast<uint32_t>(bn / cg)};
     if (encode_tiled(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a->w_packed), wd, ws, wb, sw))
       return B2DL_E_ALIGN;
   } else {
@@ -866,16 +953,18 @@ extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
                        CU_TENSOR_MAP_SWIZZLE_128B))
         return B2DL_E_ALIGN;
     } else {
-      const uint32_t wb[3] = {static_cast<uint32_t>(kblk), static_cast<uint32_t>(bn), 1u};
+      const uint32_t wb[3] = {static_cast<uint32_t>(kblk), static_cast<uint32_t>(bn / cg), 1u};
       if (encode_tiled(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(a->w_master), wd, ws, wb, sw))
         return B2DL_E_ALIGN;
     }
   }
 
   cudaStream_t st = as_stream(stream);
-#define B2_FPROP(BNV, KB)                                                          \
-  if (bn == BNV && kblk == KB)                                                     \
-    return mode == 1 ? launch_fprop<BNV, KB, true>(ta, tb, p, st) : launch_fprop<BNV, KB, false>(ta, tb, p, st);
+#define B2_FPROP(BNV, KB)                                                                \
+  if (bn == BNV && kblk == KB)                                                           \
+    return mode == 1 ? launch_fprop<BNV, KB, true, 1>(ta, tb, p, st) : launch_fprop<BNV, KB, false, 1>(ta, tb, p, st);
+  if (cg == 2)
+    return mode == 1 ? launch_fprop<256, 64, true, 2>(ta, tb, p, st) : launch_fprop<256, 64, false, 2>(ta, tb, p, st);
   B2_FPROP(256, 64)
   B2_FPROP(128, 64)
   B2_FPROP(64, 64)

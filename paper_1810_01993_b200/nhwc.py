@@ -80,12 +80,13 @@ def conv_fprop(x: View, w_packed: torch.Tensor | None, cout: int, kh: int, kw: i
 
 def conv_dgrad(dy: View, w_dgrad: torch.Tensor | None, cin: int, kh: int, kw: int, dilation: int,
                dx: View, accumulate=False, mask: View | None = None, dx_f32=False, w_master=None,
-               residual: View | None = None):
+               residual: View | None = None, block_n=0):
     """Input gradient as a forward conv over dy with tap-flipped weights and 'after' pads;
     weights from the dgrad-packed copy, or straight from the forward conv's bf16 HWIO master."""
     pads = (same_pads(kh, dilation)[1], same_pads(kw, dilation)[1])
     conv_fprop(dy, w_dgrad, cin, kh, kw, dilation, dx, accumulate=accumulate, mask=mask, residual=residual,
-               y_f32=dx_f32, pads=pads, w_master=w_master, w_mode=2 if w_master is not None else 0)
+               y_f32=dx_f32, pads=pads, block_n=block_n, w_master=w_master,
+               w_mode=2 if w_master is not None else 0)
 
 
 class Workspace:

@@ -135,3 +135,40 @@ def test_master_layout_weight_modes(case):
     nhwc.conv_dgrad(nhwc.View(dy), wd, cin, k, k, d, nhwc.View(dx0))
     nhwc.conv_dgrad(nhwc.View(dy), None, cin, k, k, d, nhwc.View(dx1), w_master=wm)
     assert _rel(dx1, dx0) < 1e-6
+
+
+@pytest.mark.parametrize("case", [(1, 256, 36, 24, 256, 3, 4), (2, 128, 24, 48, 512, 3, 2), (1, 64, 9, 13, 320, 1, 1),
+                                  (3, 192, 8, 16, 256, 3, 1)])
+def test_cta_pair_tiles(case):
+    """256-wide N tiles run as CTA pairs (cta_group::2, 256 pixels x 256 channels per pair); odd
+    tile counts leave the last odd CTA idle.  All three weight modes plus the fused epilogue."""
+    from paper_1810_01993_b200 import nhwc
+    n, cin, h, w, cout, k, d = case
+    torch.manual_seed(4)
+    x = torch.randn(n, h, w, cin, device="cuda").to(torch.bfloat16)
+    w_hwio = torch.randn(k * k, cin, cout, device="cuda") / (k * k * cin) ** 0.5
+    wm = w_hwio.to(torch.bfloat16).contiguous()
+    wf = torch.empty(cout, k * k, nhwc.cin_pad(cin), dtype=torch.bfloat16, device="cuda")
+    wd = torch.empty(cin, k * k, nhwc.cin_pad(cout), dtype=torch.bfloat16, device="cuda")
+    nhwc.pack_weights(w_hwio, k, k, cin, cout, fprop=wf, dgrad=wd)
+    bias = torch.randn(cout, device="cuda")
+    res = torch.randn(n, h, w, cout, device="cuda").to(torch.bfloat16)
+    xr = x.double().permute(0, 3, 1, 2)
+    wr = wm.double().reshape(k, k, cin, cout).permute(3, 2, 0, 1)
+    ref = torch.relu(_ref_conv(xr, wr, d) + bias.double()[None, :, None, None]
+                     + res.double().permute(0, 3, 1, 2)).permute(0, 2, 3, 1)
+    for mode in (0, 1):
+        y = torch.zeros(n, h, w, cout, dtype=torch.bfloat16, device="cuda")
+        nhwc.conv_fprop(nhwc.View(x), wf if mode == 0 else None, cout, k, k, d, nhwc.View(y), bias=bias,
+                        residual=nhwc.View(res), relu=True, block_n=256, w_master=wm if mode else None, w_mode=mode)
+        assert _rel(y, ref) < 1e-2, (case, mode)
+    # dgrad (cin >= 256 output channels of the input gradient use pairs too)
+    dy = torch.randn(n, h, w, cout, device="cuda").to(torch.bfloat16)
+    xg = torch.zeros(n, cin, h, w, dtype=torch.float64, device="cuda", requires_grad=True)
+    _ref_conv(xg, wr, d).backward(dy.double().permute(0, 3, 1, 2))
+    gref = xg.grad.permute(0, 2, 3, 1)
+    for use_master in (False, True):
+        dx = torch.zeros(n, h, w, cin, dtype=torch.float32, device="cuda")
+        nhwc.conv_dgrad(nhwc.View(dy), None if use_master else wd, cin, k, k, d, nhwc.View(dx), dx_f32=True,
+                        w_master=wm if use_master else None, block_n=256)
+        assert _rel(dx, gref) < 2e-3, (case, use_master)
