@@ -44,11 +44,21 @@ struct FpropCfg {
   static constexpr int NBC = (BN < 64 ? 1 : BN / 64) / CG;  // chunks staged by this CTA
   static constexpr int B_BYTES = BMN ? NBC * B_CHUNK : BN / CG * KBLK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (SMEM_BUDGET / STAGE_BYTES) > 8 ? 8 : (SMEM_BUDGET / STAGE_BYTES);
   static constexpr uint32_t TMEM_COLS = tmem_cols_for(2 * BN);
   static constexpr int CW = BN < 32 ? BN : 32;  // epilogue chunk (TMEM columns per load)
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + 8 * 32 * 80;
 };
+
+// Shared memory: [A stages][B stages][epilogue buffers][barriers].  The stage count is chosen
+// per launch: whatever the epilogue's operand buffers leave of the 227 KB opt-in limit.
+constexpr int SMEM_MAX = 232448;
+constexpr int FPROP_MAX_STAGES = 8;
+constexpr int SMEM_FIXED = 1024 + 512;  // alignment slack + barriers / TMEM slot
+// TMA epilogue: one 32-pixel x 32-channel bf16 box per chunk, 64-byte rows, 64B swizzle.
+// Per warp: two operand slots of up to two operands each (residual / mask / accumulated y,
+// loaded one chunk ahead), and two output buffers (stores drain while the next chunk runs).
+constexpr int EPI_BOX = 32 * 64;
+constexpr int EPI_LEGACY_BYTES = 8 * 32 * 80;
+__host__ __device__ constexpr int epi_warp_bytes(int nops) { return (2 * nops + 2) * EPI_BOX; }
 
 struct FpropParams {
   int n, h, w;
@@ -68,6 +78,12 @@ struct FpropParams {
   int relu, accumulate, vec_ok;
   int b_mode;  // 0 packed [cout][taps][cin_pad]; 1 master HWIO, MN-major; 2 master HWIO, dgrad (flipped taps)
   int taps;
+  int stages;          // operand pipeline depth
+  int b_region;        // bytes of the B stages, rounded up to 1 KB
+  int epi_bytes;       // epilogue buffer bytes
+  int tma_epi;         // 1: TMA-staged epilogue (operands + output through swizzled boxes)
+  int epi_nops;        // operands per chunk in the TMA epilogue (residual, mask, accumulated y)
+  int bias_vec;        // bias 16-byte aligned
 };
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
@@ -251,24 +267,55 @@ __device__ __forceinline__ void fprop_epilogue_scalar(const FpropParams& p, floa
 
 constexpr int FPROP_THREADS = 320;  // TMA warp, MMA warp, 8 epilogue warps
 
+// swizzled (64B) rows of an epilogue box: lane r's 16-byte piece k sits at piece k ^ ((r >> 1) & 3)
+__device__ __forceinline__ void box_row_get(const uint8_t* box, float* t) {
+  const int r = lane_id();
+  const uint8_t* row = box + r * 64;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint4 u = *reinterpret_cast<const uint4*>(row + ((k ^ ((r >> 1) & 3)) << 4));
+    const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      t[k * 8 + 2 * e] = bf16lo(w4[e]);
+      t[k * 8 + 2 * e + 1] = bf16hi(w4[e]);
+    }
+  }
+}
+__device__ __forceinline__ void box_row_put(uint8_t* box, const float* v) {
+  const int r = lane_id();
+  uint8_t* row = box + r * 64;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    uint4 u;
+    u.x = pack_bf16x2(v[k * 8 + 0], v[k * 8 + 1]);
+    u.y = pack_bf16x2(v[k * 8 + 2], v[k * 8 + 3]);
+    u.z = pack_bf16x2(v[k * 8 + 4], v[k * 8 + 5]);
+    u.w = pack_bf16x2(v[k * 8 + 6], v[k * 8 + 7]);
+    *reinterpret_cast<uint4*>(row + ((k ^ ((r >> 1) & 3)) << 4)) = u;
+  }
+}
+
 template <int BN, int KBLK, bool BMN, int CG>
 __global__ void __launch_bounds__(FPROP_THREADS, 1)
     conv_fprop_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                      const FpropParams p) {
+                      const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmR,
+                      const __grid_constant__ CUtensorMap tmM, const FpropParams p) {
   using C = FpropCfg<BN, KBLK, BMN, CG>;
-  constexpr int STAGES = C::STAGES;
+  const int STAGES = p.stages;
   constexpr uint32_t LAYOUT = KBLK == 64 ? LAYOUT_SW128 : LAYOUT_SW32;
   constexpr uint32_t SBO = KBLK * 2 * 8;  // 8 rows of KBLK bf16
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * C::B_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  uint8_t* epi = sB + p.b_region;  // 1 KB aligned
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi + p.epi_bytes);
+  uint64_t* empty = full + FPROP_MAX_STAGES;
+  uint64_t* tfull = empty + FPROP_MAX_STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  uint8_t* epi = reinterpret_cast<uint8_t*>(tmem_slot) + 16;
+  uint64_t* inbar = tempty + 2;  // two operand-slot barriers per epilogue warp
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(inbar + 16);
 
   const int warp = threadIdx.x >> 5;
   const int lane = lane_id();
@@ -284,6 +331,12 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], 8 * CG);
+    }
+    for (int s = 0; s < 16; ++s) mbar_init(&inbar[s], 1);
+    if (p.tma_epi) {
+      tma_prefetch(&tmY);
+      if (p.res) tma_prefetch(&tmR);
+      if (p.mask) tma_prefetch(&tmM);
     }
     fence_barrier_init();
   }
@@ -403,11 +456,179 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
     const int half = ew >> 2;
     const int row = q * 32 + lane;
     const int ry = row / p.bw, rx = row - ry * p.bw;
+    constexpr int NCH = BN / C::CW;
+    constexpr int NJ = (NCH + 1) / 2;
+    if constexpr (C::CW == 32) {
+      if (p.tma_epi) {
+        // TMA epilogue.  The warp's 32 accumulator rows are a (bwx x bhx)-pixel box of the tile;
+        // each 32-channel chunk is one box: operands arrive by TMA one chunk ahead, the result
+        // leaves by TMA store from a swizzled buffer while the next chunk is computed.
+        const int nops = p.epi_nops;
+        uint8_t* wbuf = epi + ew * epi_warp_bytes(nops);
+        uint8_t* obuf = wbuf + 2 * nops * EPI_BOX;
+        uint64_t* ib = inbar + 2 * ew;
+        const int wy = (q * 32) / p.bw, wx = (q * 32) % p.bw;
+        auto locate = [&](int tile, int& img, int& x, int& y, int& nt) {
+          const int pmt = tile / p.num_n_tiles;
+          nt = tile - pmt * p.num_n_tiles;
+          const int mt = pmt * CG + rank;
+          img = mt / per_img;
+          const int r = mt - img * per_img;
+          const int ty = r / p.tiles_x, tx = r - ty * p.tiles_x;
+          y = ty * p.bh + wy;
+          x = tx * p.bw + wx;
+        };
+        auto chunks = [&](int nt) {  // valid chunks of this warp in a tile of N-tile nt
+          int n = 0;
+#pragma unroll
+          for (int j = 0; j < NJ; ++j)
+            if (2 * j + half < NCH && nt * BN + (2 * j + half) * 32 < p.cout) n = j + 1;
+          return n;
+        };
+        auto issue = [&](int tile, int j, int slot) {
+          if (lane == 0) {
+            int img, x, y, nt;
+            locate(tile, img, x, y, nt);
+            const int c0 = nt * BN + (2 * j + half) * 32;
+            uint8_t* dst = wbuf + slot * nops * EPI_BOX;
+            fence_proxy_async();
+            mbar_arrive_expect_tx(&ib[slot], nops * EPI_BOX);
+            int o = 0;
+            if (p.res) tma_load_4d(dst + (o++) * EPI_BOX, &tmR, &ib[slot], c0, x, y, img);
+            if (p.mask) tma_load_4d(dst + (o++) * EPI_BOX, &tmM, &ib[slot], c0, x, y, img);
+            if (p.accumulate) tma_load_4d(dst + o * EPI_BOX, &tmY, &ib[slot], c0, x, y, img);
+          }
+        };
+        uint32_t ph0 = 0, ph1 = 0;
+        int slot = 0, ob = 0, it = 0;
+        if (nops && unit0 < p.num_tiles) {
+          int img, x, y, nt;
+          locate(unit0, img, x, y, nt);
+          if (chunks(nt) > 0) issue(unit0, 0, 0);
+        }
+        for (int tile = unit0; tile < p.num_tiles; tile += units, ++it) {
+          const int as = it & 1;
+          const uint32_t ap = (it >> 1) & 1;
+          int img, x, y, nt;
+          locate(tile, img, x, y, nt);
+          const int nv = chunks(nt);
+          mbar_wait(&tfull[as], ap);
+          tc_fence_after();
+          const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + as * BN;
+#pragma unroll 1
+          for (int j = 0; j < NJ; ++j) {
+            if (j >= nv) break;  // warp-uniform
+            if (nops) {          // operands of the next chunk (possibly of the next tile)
+              if (j + 1 < nv) {
+                issue(tile, j + 1, slot ^ 1);
+              } else if (tile + units < p.num_tiles) {
+                int i2, x2, y2, nt2;
+                locate(tile + units, i2, x2, y2, nt2);
+                if (chunks(nt2) > 0) issue(tile + units, 0, slot ^ 1);
+              }
+            }
+            const int ch = 2 * j + half;
+            const int c0 = nt * BN + ch * 32;
+            float bv[32];  // bias loads issued ahead of the TMEM read
+            if (p.bias) {
+              if (p.bias_vec && c0 + 32 <= p.cout) {
+                const float4* b4 = reinterpret_cast<const float4*>(p.bias + c0);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                  const float4 b = __ldg(b4 + i);
+                  bv[4 * i] = b.x;
+                  bv[4 * i + 1] = b.y;
+                  bv[4 * i + 2] = b.z;
+                  bv[4 * i + 3] = b.w;
+                }
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) bv[i] = c0 + i < p.cout ? __ldg(p.bias + c0 + i) : 0.f;
+              }
+            }
+            uint32_t cur[32];
+            tmem_ld_issue_x32(tbase + ch * 32, cur);
+            tmem_ld_wait();
+            float v[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(cur[i]);
+            if (j == nv - 1) {  // accumulator fully read: release it to the MMA warp early
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) {
+                if constexpr (CG == 2)
+                  mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[as]), 0));
+                else
+                  mbar_arrive(&tempty[as]);
+              }
+            }
+            if (p.bias) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] += bv[i];
+            }
+            const uint8_t* in = wbuf + slot * nops * EPI_BOX;
+            if (nops) {
+              mbar_wait(&ib[slot], slot ? ph1 : ph0);
+              if (slot)
+                ph1 ^= 1;
+              else
+                ph0 ^= 1;
+            }
+            float t[32];
+            int o = 0;
+            if (p.res) {
+              box_row_get(in + (o++) * EPI_BOX, t);
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] += t[i];
+            }
+            if (p.relu) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+            }
+            if (p.mask) {
+              box_row_get(in + (o++) * EPI_BOX, t);
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                if (!(t[i] > 0.f)) v[i] = 0.f;
+            }
+            if (p.accumulate) {
+              box_row_get(in + o * EPI_BOX, t);
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] += t[i];
+            }
+            // output buffer `ob` was last stored two chunks ago
+            if (lane == 0) bulk_wait_read<1>();
+            __syncwarp();
+            box_row_put(obuf + ob * EPI_BOX, v);
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_4d(&tmY, obuf + ob * EPI_BOX, c0, x, y, img);
+              bulk_commit();
+            }
+            ob ^= 1;
+            slot ^= 1;
+          }
+          if (nv == 0) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+              if constexpr (CG == 2)
+                mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[as]), 0));
+              else
+                mbar_arrive(&tempty[as]);
+            }
+          }
+        }
+        if (lane == 0) bulk_wait<0>();
+        __syncwarp();
+        goto epilogue_done;
+      }
+    }
+    {
     uint8_t* st = epi + ew * EPI_WARP_BYTES;
     const bool vec = p.vec_ok && !p.y_f32 && (p.cout % 8) == 0;
     using R = CoopRows<C::CW>;
-    constexpr int NCH = BN / C::CW;
-    constexpr int NJ = (NCH + 1) / 2;
     int it = 0;
     for (int tile = unit0; tile < p.num_tiles; tile += units, ++it) {
       const int as = it & 1;
@@ -471,6 +692,8 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
           mbar_arrive(&tempty[as]);
       }
     }
+    }
+  epilogue_done:;
   }
   tc_fence_before();
   if constexpr (CG == 2)
@@ -786,25 +1009,43 @@ __global__ void wgrad_reduce_kernel(const float* __restrict__ ws, float* __restr
 }
 
 // ------------------------------------------------------------------ host side
+struct FpropMaps {
+  CUtensorMap a, b, y, r, m;
+};
+
 template <int BN, int KBLK, bool BMN, int CG>
-static int launch_fprop(const CUtensorMap& ta, const CUtensorMap& tb, const FpropParams& p, cudaStream_t st) {
+static int launch_fprop(const FpropMaps& t, FpropParams p, cudaStream_t st) {
   using C = FpropCfg<BN, KBLK, BMN, CG>;
   auto kern = conv_fprop_kernel<BN, KBLK, BMN, CG>;
   static bool attr_set = false;
   if (!attr_set) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) != cudaSuccess)
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX) != cudaSuccess)
       return B2DL_E_CUDA;
     attr_set = true;
   }
+  if (C::CW != 32) p.tma_epi = 0;
+  p.epi_nops = p.tma_epi ? (p.res != nullptr) + (p.mask != nullptr) + (p.accumulate != 0) : 0;
+  p.epi_bytes = p.tma_epi ? 8 * epi_warp_bytes(p.epi_nops) : EPI_LEGACY_BYTES;
+  // deepest operand pipeline that fits beside the epilogue buffers
+  p.stages = 1;
+  for (int s = FPROP_MAX_STAGES; s >= 1; --s) {
+    const int b_region = (s * C::B_BYTES + 1023) / 1024 * 1024;
+    if (s * C::A_BYTES + b_region + p.epi_bytes + SMEM_FIXED <= SMEM_MAX) {
+      p.stages = s;
+      break;
+    }
+  }
+  p.b_region = (p.stages * C::B_BYTES + 1023) / 1024 * 1024;
+  const int smem = p.stages * C::A_BYTES + p.b_region + p.epi_bytes + SMEM_FIXED;
   if constexpr (CG == 1) {
     const int grid = std::min(p.num_tiles, num_sms());
-    kern<<<grid, FPROP_THREADS, C::SMEM, st>>>(ta, tb, p);
+    kern<<<grid, FPROP_THREADS, smem, st>>>(t.a, t.b, t.y, t.r, t.m, p);
   } else {
     const int grid = CG * std::min(p.num_tiles, num_sms() / CG);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(FPROP_THREADS);
-    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -813,7 +1054,7 @@ static int launch_fprop(const CUtensorMap& ta, const CUtensorMap& tb, const Fpro
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, p);
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, t.a, t.b, t.y, t.r, t.m, p);
     if (e != cudaSuccess) {
       fprintf(stderr, "b2dl: CUDA error %s\n", cudaGetErrorString(e));
       return B2DL_E_CUDA;
@@ -841,6 +1082,15 @@ static int launch_wgrad(const CUtensorMap& tx, const CUtensorMap& tdy, const Wgr
 static bool fprop_pairs_enabled() {
   static const bool on = [] {
     const char* e = getenv("B2DL_FPROP_PAIRS");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// TMA-staged fprop epilogue; B2DL_TMA_EPILOGUE=0 selects the register/shared-memory path
+static bool tma_epilogue_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("B2DL_TMA_EPILOGUE");
     return !(e && e[0] == '0');
   }();
   return on;
@@ -924,9 +1174,9 @@ extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
   p.vec_ok = view_aligned(y, a->y_f32 ? 4 : 2) && (!p.res || view_aligned(a->residual, 2)) &&
              (!p.mask || view_aligned(a->mask, 2));
 
-  CUtensorMap ta, tb;
+  FpropMaps t;
   const CUtensorMapSwizzle sw = kblk == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B;
-  if (act_map(&ta, x, kblk, p.bw, p.bh, sw)) return B2DL_E_ALIGN;
+  if (act_map(&t.a, x, kblk, p.bw, p.bh, sw)) return B2DL_E_ALIGN;
   const int mode = a->w_mode;
   p.b_mode = mode;
   p.taps = a->kh * a->kw;
@@ -936,7 +1186,7 @@ extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
     const uint64_t wd[2] = {ktot, static_cast<uint64_t>(a->cout)};
     const uint64_t ws[1] = {ktot * 2};
     const uint32_t wb[2] = {static_cast<uint32_t>(kblk), static_cast<uint32_t>(bn / cg)};
-    if (encode_tiled(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a->w_packed), wd, ws, wb, sw))
+    if (encode_tiled(&t.b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a->w_packed), wd, ws, wb, sw))
       return B2DL_E_ALIGN;
   } else {
     // master HWIO bf16 [taps][cin_f][cout_f] of the forward conv; fprop: cin_f = x.c, cout_f = cout;
@@ -949,22 +1199,34 @@ extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
     const uint64_t ws[2] = {cf * 2, cf * kf * 2};
     if (mode == 1) {
       const uint32_t wb[3] = {64u, static_cast<uint32_t>(kblk), 1u};
-      if (encode_tiled(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(a->w_master), wd, ws, wb,
+      if (encode_tiled(&t.b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(a->w_master), wd, ws, wb,
                        CU_TENSOR_MAP_SWIZZLE_128B))
         return B2DL_E_ALIGN;
     } else {
       const uint32_t wb[3] = {static_cast<uint32_t>(kblk), static_cast<uint32_t>(bn / cg), 1u};
-      if (encode_tiled(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(a->w_master), wd, ws, wb, sw))
+      if (encode_tiled(&t.b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(a->w_master), wd, ws, wb, sw))
         return B2DL_E_ALIGN;
     }
+  }
+
+  // TMA epilogue: bf16 output (and operands) through 32-pixel x 32-channel swizzled boxes
+  p.bias_vec = a->bias && (reinterpret_cast<uintptr_t>(a->bias) % 16 == 0);
+  p.tma_epi = p.vec_ok && !p.y_f32 && (a->cout % 8) == 0 && bn >= 32 && tma_epilogue_enabled() &&
+              ((p.res != nullptr) + (p.mask != nullptr) + (p.accumulate != 0)) <= 2;
+  if (p.tma_epi) {
+    const int bwx = std::min(p.bw, 32), bhx = 32 / bwx;
+    if (act_map(&t.y, y, 32, bwx, bhx, CU_TENSOR_MAP_SWIZZLE_64B) ||
+        (p.res && act_map(&t.r, a->residual, 32, bwx, bhx, CU_TENSOR_MAP_SWIZZLE_64B)) ||
+        (p.mask && act_map(&t.m, a->mask, 32, bwx, bhx, CU_TENSOR_MAP_SWIZZLE_64B)))
+      p.tma_epi = 0;
   }
 
   cudaStream_t st = as_stream(stream);
 #define B2_FPROP(BNV, KB)                                                                \
   if (bn == BNV && kblk == KB)                                                           \
-    return mode == 1 ? launch_fprop<BNV, KB, true, 1>(ta, tb, p, st) : launch_fprop<BNV, KB, false, 1>(ta, tb, p, st);
+    return mode == 1 ? launch_fprop<BNV, KB, true, 1>(t, p, st) : launch_fprop<BNV, KB, false, 1>(t, p, st);
   if (cg == 2)
-    return mode == 1 ? launch_fprop<256, 64, true, 2>(ta, tb, p, st) : launch_fprop<256, 64, false, 2>(ta, tb, p, st);
+    return mode == 1 ? launch_fprop<256, 64, true, 2>(t, p, st) : launch_fprop<256, 64, false, 2>(t, p, st);
   B2_FPROP(256, 64)
   B2_FPROP(128, 64)
   B2_FPROP(64, 64)

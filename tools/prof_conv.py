@@ -30,6 +30,8 @@ wf8 = torch.empty(2048, 1, 512, dtype=torch.bfloat16, device="cuda")
 nhwc.pack_weights(w8, 1, 1, 512, 2048, fprop=wf8)
 b8 = torch.zeros(2048, device="cuda")
 wbf = w.to(torch.bfloat16).contiguous()   # master HWIO bf16
+w8bf = w8.to(torch.bfloat16).contiguous()
+d8 = torch.randn(2, 144, 96, 512, device="cuda").to(torch.bfloat16)
 ops = {
     "fprop_mn": lambda: nhwc.conv_fprop(nhwc.View(x), None, C, 3, 3, 1, nhwc.View(y), bias=b, relu=True,
                                         w_master=wbf, w_mode=1),
@@ -40,6 +42,8 @@ ops = {
     "wgrad": lambda: nhwc.conv_wgrad(nhwc.View(x), nhwc.View(dy), 3, 3, 1, dw, ws),
     "c1x1_fprop": lambda: nhwc.conv_fprop(nhwc.View(x8), wf8, 2048, 1, 1, 1, nhwc.View(y8), bias=b8,
                                           residual=nhwc.View(r8), relu=True),
+    "c1x1_dgrad": lambda: nhwc.conv_dgrad(nhwc.View(d8), None, 2048, 1, 1, 1, nhwc.View(y8), mask=nhwc.View(r8),
+                                          residual=nhwc.View(r8), w_master=w8bf),
     "stem_wgrad": lambda: nhwc.conv_wgrad(nhwc.View(xs), nhwc.View(ys), 7, 7, 1, dws, ws),
 }
 sel = sys.argv[1:] or list(ops)
@@ -54,6 +58,7 @@ for k in sel:
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 3
-    fl = {"stem_wgrad": 2 * 49 * 16 * 64 * N * H * W, "c1x1_fprop": 2 * 512 * 2048 * 2 * 144 * 96}.get(
+    fl = {"stem_wgrad": 2 * 49 * 16 * 64 * N * H * W, "c1x1_fprop": 2 * 512 * 2048 * 2 * 144 * 96,
+                                                  "c1x1_dgrad": 2 * 512 * 2048 * 2 * 144 * 96}.get(
         k, 2 * 9 * C * C * N * H * W)
     print(f"{k:10s} {ms:.3f} ms  {fl / ms / 1e9:.1f} TF/s", flush=True)
