@@ -105,6 +105,13 @@ typedef struct b2dl_conv_args {
    * Modes 1/2 need the forward cout % 8 == 0; they remove all weight repacking. */
   const void* w_master;
   int w_mode;
+  /* Row-window mode (window = kw' > 0, the reference conv's kernel width; pass kw = 1,
+   * pad_left = 0): x is stored with its horizontal "same" padding baked in as zero columns
+   * (x.w >= y.w + window - 1, x.c == x.c_stride) and the window input pixels of a kernel row
+   * are folded into one K run of window * x.c channels.  Weights are those of a kh x 1 conv
+   * over window * x.c input channels -- memory-identical to the kh x kw x cin HWIO tensor.
+   * Used for narrow inputs (the 16-channel 7x7 stem) whose per-tap K would be tiny. */
+  int window;
 } b2dl_conv_args;
 
 B2DL_API int b2dl_cin_pad(int cin);
@@ -127,6 +134,8 @@ typedef struct b2dl_wgrad_args {
   int splits;       /* 0 = auto */
   int defer_reduce; /* 1: leave the split-K partials in `workspace` (layout from
                        b2dl_wgrad_partials) for a later batched b2dl_reduce_segments */
+  int window;       /* row-window mode, as in b2dl_conv_args (dw is then [kh][window*cin][cout],
+                       memory-identical to HWIO [kh][kw][cin][cout]) */
 } b2dl_wgrad_args;
 
 B2DL_API size_t b2dl_wgrad_workspace_size(const b2dl_wgrad_args* a);
@@ -154,6 +163,10 @@ B2DL_API int b2dl_pack_weights(const float* w_hwio, int kh, int kw, int cin, int
 
 /* NCHW fp32 -> NHWC view, bf16 (or fp32 when dst_f32) (input tiles, reference-layout tensors). */
 B2DL_API int b2dl_nchw_to_nhwc(const float* x, b2dl_act y, int dst_f32, void* stream);
+/* NCHW fp32 [n][c][h][w] -> bf16 NHWC with a horizontal zero halo: y [n][h][wp][c], input
+ * column xx at column left + xx, all other columns zero (the row-window conv input). */
+B2DL_API int b2dl_nchw_to_nhwc_halo(const float* x, int n, int c, int h, int w, void* y, int wp, int left,
+                                    void* stream);
 /* NHWC (bf16, or fp32 when src_f32) view -> NCHW fp32. */
 B2DL_API int b2dl_nhwc_to_nchw(b2dl_act x, int src_f32, float* y, void* stream);
 

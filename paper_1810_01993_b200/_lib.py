@@ -36,7 +36,8 @@ class ConvArgs(ctypes.Structure):
                 ("pad_top", ctypes.c_int), ("pad_left", ctypes.c_int), ("y", Act),
                 ("y_f32", ctypes.c_int), ("bias", ctypes.c_void_p), ("residual", Act),
                 ("relu", ctypes.c_int), ("accumulate", ctypes.c_int), ("mask", Act),
-                ("block_n", ctypes.c_int), ("w_master", ctypes.c_void_p), ("w_mode", ctypes.c_int)]
+                ("block_n", ctypes.c_int), ("w_master", ctypes.c_void_p), ("w_mode", ctypes.c_int),
+                ("window", ctypes.c_int)]
 
 
 class WgradArgs(ctypes.Structure):
@@ -45,7 +46,7 @@ class WgradArgs(ctypes.Structure):
                 ("dw", ctypes.c_void_p), ("bias_grad", ctypes.c_void_p),
                 ("accumulate", ctypes.c_int), ("workspace", ctypes.c_void_p),
                 ("workspace_bytes", ctypes.c_size_t), ("splits", ctypes.c_int),
-                ("defer_reduce", ctypes.c_int)]
+                ("defer_reduce", ctypes.c_int), ("window", ctypes.c_int)]
 
 
 class Segment(ctypes.Structure):
@@ -79,6 +80,7 @@ _SIGS = {
     "b2dl_reduce_segments": (_c_int, [_vp, _c_int, ctypes.c_int64, _vp, _vp]),
     "b2dl_pack_weights": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp]),
     "b2dl_nchw_to_nhwc": (_c_int, [_vp, Act, _c_int, _vp]),
+    "b2dl_nchw_to_nhwc_halo": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _c_int, _vp]),
     "b2dl_nhwc_to_nchw": (_c_int, [Act, _c_int, _vp, _vp]),
     "b2dl_avgpool_fwd": (_c_int, [Act, Act, _c_int, _vp]),
     "b2dl_avgpool_bwd": (_c_int, [Act, Act, _c_int, _c_int, Act, _vp]),

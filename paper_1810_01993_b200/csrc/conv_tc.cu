@@ -296,6 +296,260 @@ __device__ __forceinline__ void box_row_put(uint8_t* box, const float* v) {
   }
 }
 
+// Epilogue role of the fprop kernels (8 warps, two per TMEM lane quarter splitting the tile's
+// column chunks): TMEM -> registers -> bias / residual / relu / mask / accumulate -> global.
+template <int BN, int CG>
+__device__ __forceinline__ void fprop_epilogue_role(const FpropParams& p, const CUtensorMap* tmY, const CUtensorMap* tmR,
+                                                    const CUtensorMap* tmM, uint32_t tmem_base, uint64_t* tfull,
+                                                    uint64_t* tempty, uint64_t* inbar, uint8_t* epi, int warp,
+                                                    int rank, int unit0, int units) {
+  constexpr int CW = BN < 32 ? BN : 32;
+  const int lane = lane_id();
+  const int per_img = p.tiles_x * p.tiles_y;
+    const int ew = warp - 2;
+    const int q = warp & 3;
+    const int half = ew >> 2;
+    const int row = q * 32 + lane;
+    const int ry = row / p.bw, rx = row - ry * p.bw;
+    constexpr int NCH = BN / CW;
+    constexpr int NJ = (NCH + 1) / 2;
+    if constexpr (CW == 32) {
+      if (p.tma_epi) {
+        // TMA epilogue.  The warp's 32 accumulator rows are a (bwx x bhx)-pixel box of the tile;
+        // each 32-channel chunk is one box: operands arrive by TMA one chunk ahead, the result
+        // leaves by TMA store from a swizzled buffer while the next chunk is computed.
+        const int nops = p.epi_nops;
+        uint8_t* wbuf = epi + ew * epi_warp_bytes(nops);
+        uint8_t* obuf = wbuf + 2 * nops * EPI_BOX;
+        uint64_t* ib = inbar + 2 * ew;
+        const int wy = (q * 32) / p.bw, wx = (q * 32) % p.bw;
+        auto locate = [&](int tile, int& img, int& x, int& y, int& nt) {
+          const int pmt = tile / p.num_n_tiles;
+          nt = tile - pmt * p.num_n_tiles;
+          const int mt = pmt * CG + rank;
+          img = mt / per_img;
+          const int r = mt - img * per_img;
+          const int ty = r / p.tiles_x, tx = r - ty * p.tiles_x;
+          y = ty * p.bh + wy;
+          x = tx * p.bw + wx;
+        };
+        auto chunks = [&](int nt) {  // valid chunks of this warp in a tile of N-tile nt
+          int n = 0;
+#pragma unroll
+          for (int j = 0; j < NJ; ++j)
+            if (2 * j + half < NCH && nt * BN + (2 * j + half) * 32 < p.cout) n = j + 1;
+          return n;
+        };
+        auto issue = [&](int tile, int j, int slot) {
+          if (lane == 0) {
+            int img, x, y, nt;
+            locate(tile, img, x, y, nt);
+            const int c0 = nt * BN + (2 * j + half) * 32;
+            uint8_t* dst = wbuf + slot * nops * EPI_BOX;
+            fence_proxy_async();
+            mbar_arrive_expect_tx(&ib[slot], nops * EPI_BOX);
+            int o = 0;
+            if (p.res) tma_load_4d(dst + (o++) * EPI_BOX, tmR, &ib[slot], c0, x, y, img);
+            if (p.mask) tma_load_4d(dst + (o++) * EPI_BOX, tmM, &ib[slot], c0, x, y, img);
+            if (p.accumulate) tma_load_4d(dst + o * EPI_BOX, tmY, &ib[slot], c0, x, y, img);
+          }
+        };
+        uint32_t ph0 = 0, ph1 = 0;
+        int slot = 0, ob = 0, it = 0;
+        if (nops && unit0 < p.num_tiles) {
+          int img, x, y, nt;
+          locate(unit0, img, x, y, nt);
+          if (chunks(nt) > 0) issue(unit0, 0, 0);
+        }
+        for (int tile = unit0; tile < p.num_tiles; tile += units, ++it) {
+          const int as = it & 1;
+          const uint32_t ap = (it >> 1) & 1;
+          int img, x, y, nt;
+          locate(tile, img, x, y, nt);
+          const int nv = chunks(nt);
+          mbar_wait(&tfull[as], ap);
+          tc_fence_after();
+          const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + as * BN;
+#pragma unroll 1
+          for (int j = 0; j < NJ; ++j) {
+            if (j >= nv) break;  // warp-uniform
+            if (nops) {          // operands of the next chunk (possibly of the next tile)
+              if (j + 1 < nv) {
+                issue(tile, j + 1, slot ^ 1);
+              } else if (tile + units < p.num_tiles) {
+                int i2, x2, y2, nt2;
+                locate(tile + units, i2, x2, y2, nt2);
+                if (chunks(nt2) > 0) issue(tile + units, 0, slot ^ 1);
+              }
+            }
+            const int ch = 2 * j + half;
+            const int c0 = nt * BN + ch * 32;
+            float bv[32];  // bias loads issued ahead of the TMEM read
+            if (p.bias) {
+              if (p.bias_vec && c0 + 32 <= p.cout) {
+                const float4* b4 = reinterpret_cast<const float4*>(p.bias + c0);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                  const float4 b = __ldg(b4 + i);
+                  bv[4 * i] = b.x;
+                  bv[4 * i + 1] = b.y;
+                  bv[4 * i + 2] = b.z;
+                  bv[4 * i + 3] = b.w;
+                }
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) bv[i] = c0 + i < p.cout ? __ldg(p.bias + c0 + i) : 0.f;
+              }
+            }
+            uint32_t cur[32];
+            tmem_ld_issue_x32(tbase + ch * 32, cur);
+            tmem_ld_wait();
+            float v[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(cur[i]);
+            if (j == nv - 1) {  // accumulator fully read: release it to the MMA warp early
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) {
+                if constexpr (CG == 2)
+                  mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[as]), 0));
+                else
+                  mbar_arrive(&tempty[as]);
+              }
+            }
+            if (p.bias) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] += bv[i];
+            }
+            const uint8_t* in = wbuf + slot * nops * EPI_BOX;
+            if (nops) {
+              mbar_wait(&ib[slot], slot ? ph1 : ph0);
+              if (slot)
+                ph1 ^= 1;
+              else
+                ph0 ^= 1;
+            }
+            float t[32];
+            int o = 0;
+            if (p.res) {
+              box_row_get(in + (o++) * EPI_BOX, t);
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] += t[i];
+            }
+            if (p.relu) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+            }
+            if (p.mask) {
+              box_row_get(in + (o++) * EPI_BOX, t);
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                if (!(t[i] > 0.f)) v[i] = 0.f;
+            }
+            if (p.accumulate) {
+              box_row_get(in + o * EPI_BOX, t);
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] += t[i];
+            }
+            // output buffer `ob` was last stored two chunks ago
+            if (lane == 0) bulk_wait_read<1>();
+            __syncwarp();
+            box_row_put(obuf + ob * EPI_BOX, v);
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_4d(tmY, obuf + ob * EPI_BOX, c0, x, y, img);
+              bulk_commit();
+            }
+            ob ^= 1;
+            slot ^= 1;
+          }
+          if (nv == 0) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+              if constexpr (CG == 2)
+                mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[as]), 0));
+              else
+                mbar_arrive(&tempty[as]);
+            }
+          }
+        }
+        if (lane == 0) bulk_wait<0>();
+        __syncwarp();
+        return;
+      }
+    }
+    {
+    uint8_t* st = epi + ew * EPI_WARP_BYTES;
+    const bool vec = p.vec_ok && !p.y_f32 && (p.cout % 8) == 0;
+    using R = CoopRows<CW>;
+    int it = 0;
+    for (int tile = unit0; tile < p.num_tiles; tile += units, ++it) {
+      const int as = it & 1;
+      const uint32_t ap = (it >> 1) & 1;
+      const int pmt = tile / p.num_n_tiles, nt = tile - pmt * p.num_n_tiles;
+      const int mt = pmt * CG + rank;
+      const int img = mt / per_img, r = mt - img * per_img;
+      const int ty = r / p.tiles_x, tx = r - ty * p.tiles_x;
+      const int yy = ty * p.bh + ry, xx = tx * p.bw + rx;
+      const bool valid = img < p.n && yy < p.h && xx < p.w;  // odd pair count: the last odd CTA idles
+      const long long pix = (static_cast<long long>(img) * p.h + yy) * p.w + xx;
+      R L;
+#pragma unroll
+      for (int k = 0; k < R::PIECES; ++k) {
+        const int rr = q * 32 + k * R::ROWS_PER_IT + lane / R::PIECES;
+        const int cy = ty * p.bh + rr / p.bw, cx = tx * p.bw + rr % p.bw;
+        L.ok[k] = img < p.n && cy < p.h && cx < p.w;
+        L.pix[k] = (static_cast<long long>(img) * p.h + cy) * p.w + cx;
+      }
+      // prefetch the first global epilogue operand of all of this warp's chunks
+      uint4 pre[NJ][R::PIECES];
+      const __nv_bfloat16* pbase = p.res ? p.res : p.mask;
+      const long long pstride = p.res ? p.res_stride : p.mask_stride;
+      if (vec && pbase) {
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+          const int c0 = nt * BN + (2 * j + half) * CW;
+          if (2 * j + half < NCH && c0 < p.cout) coop_prefetch<CW>(pbase, pstride, c0, p.cout, L, pre[j]);
+        }
+      }
+      mbar_wait(&tfull[as], ap);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + as * BN;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        const int ch = 2 * j + half;
+        if (ch >= NCH) break;  // warp-uniform
+        uint32_t cur[CW];
+        if constexpr (CW == 32)
+          tmem_ld_issue_x32(tbase + ch * CW, cur);
+        else
+          tmem_ld_issue_x16(tbase + ch * CW, cur);
+        tmem_ld_wait();
+        float v[CW];
+#pragma unroll
+        for (int i = 0; i < CW; ++i) v[i] = __uint_as_float(cur[i]);
+        const int c0 = nt * BN + ch * CW;
+        if (c0 < p.cout) {
+          if (vec)
+            fprop_epilogue_vec<CW>(p, v, c0, L, st, pbase ? pre[j] : nullptr);
+          else if (valid)
+            fprop_epilogue_scalar<CW>(p, v, pix, c0);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (CG == 2)
+          mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[as]), 0));
+        else
+          mbar_arrive(&tempty[as]);
+      }
+    }
+    }
+}
+
 template <int BN, int KBLK, bool BMN, int CG>
 __global__ void __launch_bounds__(FPROP_THREADS, 1)
     conv_fprop_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -450,250 +704,7 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
       }
     }
   } else {
-    // 8 epilogue warps: two per TMEM lane quarter, splitting the tile's column chunks
-    const int ew = warp - 2;
-    const int q = warp & 3;
-    const int half = ew >> 2;
-    const int row = q * 32 + lane;
-    const int ry = row / p.bw, rx = row - ry * p.bw;
-    constexpr int NCH = BN / C::CW;
-    constexpr int NJ = (NCH + 1) / 2;
-    if constexpr (C::CW == 32) {
-      if (p.tma_epi) {
-        // TMA epilogue.  The warp's 32 accumulator rows are a (bwx x bhx)-pixel box of the tile;
-        // each 32-channel chunk is one box: operands arrive by TMA one chunk ahead, the result
-        // leaves by TMA store from a swizzled buffer while the next chunk is computed.
-        const int nops = p.epi_nops;
-        uint8_t* wbuf = epi + ew * epi_warp_bytes(nops);
-        uint8_t* obuf = wbuf + 2 * nops * EPI_BOX;
-        uint64_t* ib = inbar + 2 * ew;
-        const int wy = (q * 32) / p.bw, wx = (q * 32) % p.bw;
-        auto locate = [&](int tile, int& img, int& x, int& y, int& nt) {
-          const int pmt = tile / p.num_n_tiles;
-          nt = tile - pmt * p.num_n_tiles;
-          const int mt = pmt * CG + rank;
-          img = mt / per_img;
-          const int r = mt - img * per_img;
-          const int ty = r / p.tiles_x, tx = r - ty * p.tiles_x;
-          y = ty * p.bh + wy;
-          x = tx * p.bw + wx;
-        };
-        auto chunks = [&](int nt) {  // valid chunks of this warp in a tile of N-tile nt
-          int n = 0;
-#pragma unroll
-          for (int j = 0; j < NJ; ++j)
-            if (2 * j + half < NCH && nt * BN + (2 * j + half) * 32 < p.cout) n = j + 1;
-          return n;
-        };
-        auto issue = [&](int tile, int j, int slot) {
-          if (lane == 0) {
-            int img, x, y, nt;
-            locate(tile, img, x, y, nt);
-            const int c0 = nt * BN + (2 * j + half) * 32;
-            uint8_t* dst = wbuf + slot * nops * EPI_BOX;
-            fence_proxy_async();
-            mbar_arrive_expect_tx(&ib[slot], nops * EPI_BOX);
-            int o = 0;
-            if (p.res) tma_load_4d(dst + (o++) * EPI_BOX, &tmR, &ib[slot], c0, x, y, img);
-            if (p.mask) tma_load_4d(dst + (o++) * EPI_BOX, &tmM, &ib[slot], c0, x, y, img);
-            if (p.accumulate) tma_load_4d(dst + o * EPI_BOX, &tmY, &ib[slot], c0, x, y, img);
-          }
-        };
-        uint32_t ph0 = 0, ph1 = 0;
-        int slot = 0, ob = 0, it = 0;
-        if (nops && unit0 < p.num_tiles) {
-          int img, x, y, nt;
-          locate(unit0, img, x, y, nt);
-          if (chunks(nt) > 0) issue(unit0, 0, 0);
-        }
-        for (int tile = unit0; tile < p.num_tiles; tile += units, ++it) {
-          const int as = it & 1;
-          const uint32_t ap = (it >> 1) & 1;
-          int img, x, y, nt;
-          locate(tile, img, x, y, nt);
-          const int nv = chunks(nt);
-          mbar_wait(&tfull[as], ap);
-          tc_fence_after();
-          const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + as * BN;
-#pragma unroll 1
-          for (int j = 0; j < NJ; ++j) {
-            if (j >= nv) break;  // warp-uniform
-            if (nops) {          // operands of the next chunk (possibly of the next tile)
-              if (j + 1 < nv) {
-                issue(tile, j + 1, slot ^ 1);
-              } else if (tile + units < p.num_tiles) {
-                int i2, x2, y2, nt2;
-                locate(tile + units, i2, x2, y2, nt2);
-                if (chunks(nt2) > 0) issue(tile + units, 0, slot ^ 1);
-              }
-            }
-            const int ch = 2 * j + half;
-            const int c0 = nt * BN + ch * 32;
-            float bv[32];  // bias loads issued ahead of the TMEM read
-            if (p.bias) {
-              if (p.bias_vec && c0 + 32 <= p.cout) {
-                const float4* b4 = reinterpret_cast<const float4*>(p.bias + c0);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                  const float4 b = __ldg(b4 + i);
-                  bv[4 * i] = b.x;
-                  bv[4 * i + 1] = b.y;
-                  bv[4 * i + 2] = b.z;
-                  bv[4 * i + 3] = b.w;
-                }
-              } else {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) bv[i] = c0 + i < p.cout ? __ldg(p.bias + c0 + i) : 0.f;
-              }
-            }
-            uint32_t cur[32];
-            tmem_ld_issue_x32(tbase + ch * 32, cur);
-            tmem_ld_wait();
-            float v[32];
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(cur[i]);
-            if (j == nv - 1) {  // accumulator fully read: release it to the MMA warp early
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) {
-                if constexpr (CG == 2)
-                  mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[as]), 0));
-                else
-                  mbar_arrive(&tempty[as]);
-              }
-            }
-            if (p.bias) {
-#pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] += bv[i];
-            }
-            const uint8_t* in = wbuf + slot * nops * EPI_BOX;
-            if (nops) {
-              mbar_wait(&ib[slot], slot ? ph1 : ph0);
-              if (slot)
-                ph1 ^= 1;
-              else
-                ph0 ^= 1;
-            }
-            float t[32];
-            int o = 0;
-            if (p.res) {
-              box_row_get(in + (o++) * EPI_BOX, t);
-#pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] += t[i];
-            }
-            if (p.relu) {
-#pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
-            }
-            if (p.mask) {
-              box_row_get(in + (o++) * EPI_BOX, t);
-#pragma unroll
-              for (int i = 0; i < 32; ++i)
-                if (!(t[i] > 0.f)) v[i] = 0.f;
-            }
-            if (p.accumulate) {
-              box_row_get(in + o * EPI_BOX, t);
-#pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] += t[i];
-            }
-            // output buffer `ob` was last stored two chunks ago
-            if (lane == 0) bulk_wait_read<1>();
-            __syncwarp();
-            box_row_put(obuf + ob * EPI_BOX, v);
-            fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) {
-              tma_store_4d(&tmY, obuf + ob * EPI_BOX, c0, x, y, img);
-              bulk_commit();
-            }
-            ob ^= 1;
-            slot ^= 1;
-          }
-          if (nv == 0) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-              if constexpr (CG == 2)
-                mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[as]), 0));
-              else
-                mbar_arrive(&tempty[as]);
-            }
-          }
-        }
-        if (lane == 0) bulk_wait<0>();
-        __syncwarp();
-        goto epilogue_done;
-      }
-    }
-    {
-    uint8_t* st = epi + ew * EPI_WARP_BYTES;
-    const bool vec = p.vec_ok && !p.y_f32 && (p.cout % 8) == 0;
-    using R = CoopRows<C::CW>;
-    int it = 0;
-    for (int tile = unit0; tile < p.num_tiles; tile += units, ++it) {
-      const int as = it & 1;
-      const uint32_t ap = (it >> 1) & 1;
-      const int pmt = tile / p.num_n_tiles, nt = tile - pmt * p.num_n_tiles;
-      const int mt = pmt * CG + rank;
-      const int img = mt / per_img, r = mt - img * per_img;
-      const int ty = r / p.tiles_x, tx = r - ty * p.tiles_x;
-      const int yy = ty * p.bh + ry, xx = tx * p.bw + rx;
-      const bool valid = img < p.n && yy < p.h && xx < p.w;  // odd pair count: the last odd CTA idles
-      const long long pix = (static_cast<long long>(img) * p.h + yy) * p.w + xx;
-      R L;
-#pragma unroll
-      for (int k = 0; k < R::PIECES; ++k) {
-        const int rr = q * 32 + k * R::ROWS_PER_IT + lane / R::PIECES;
-        const int cy = ty * p.bh + rr / p.bw, cx = tx * p.bw + rr % p.bw;
-        L.ok[k] = img < p.n && cy < p.h && cx < p.w;
-        L.pix[k] = (static_cast<long long>(img) * p.h + cy) * p.w + cx;
-      }
-      // prefetch the first global epilogue operand of all of this warp's chunks
-      uint4 pre[NJ][R::PIECES];
-      const __nv_bfloat16* pbase = p.res ? p.res : p.mask;
-      const long long pstride = p.res ? p.res_stride : p.mask_stride;
-      if (vec && pbase) {
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) {
-          const int c0 = nt * BN + (2 * j + half) * C::CW;
-          if (2 * j + half < NCH && c0 < p.cout) coop_prefetch<C::CW>(pbase, pstride, c0, p.cout, L, pre[j]);
-        }
-      }
-      mbar_wait(&tfull[as], ap);
-      tc_fence_after();
-      const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + as * BN;
-#pragma unroll
-      for (int j = 0; j < NJ; ++j) {
-        const int ch = 2 * j + half;
-        if (ch >= NCH) break;  // warp-uniform
-        uint32_t cur[C::CW];
-        if constexpr (C::CW == 32)
-          tmem_ld_issue_x32(tbase + ch * C::CW, cur);
-        else
-          tmem_ld_issue_x16(tbase + ch * C::CW, cur);
-        tmem_ld_wait();
-        float v[C::CW];
-#pragma unroll
-        for (int i = 0; i < C::CW; ++i) v[i] = __uint_as_float(cur[i]);
-        const int c0 = nt * BN + ch * C::CW;
-        if (c0 < p.cout) {
-          if (vec)
-            fprop_epilogue_vec<C::CW>(p, v, c0, L, st, pbase ? pre[j] : nullptr);
-          else if (valid)
-            fprop_epilogue_scalar<C::CW>(p, v, pix, c0);
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if constexpr (CG == 2)
-          mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[as]), 0));
-        else
-          mbar_arrive(&tempty[as]);
-      }
-    }
-    }
-  epilogue_done:;
+    fprop_epilogue_role<BN, CG>(p, &tmY, &tmR, &tmM, tmem_base, tfull, tempty, inbar, epi, warp, rank, unit0, units);
   }
   tc_fence_before();
   if constexpr (CG == 2)
@@ -706,6 +717,128 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
       tmem_dealloc_pair(tmem_base, C::TMEM_COLS);
     else
       tmem_dealloc(tmem_base, C::TMEM_COLS);
+  }
+}
+
+// ------------------------------------------------------------------ row-window halo fprop
+// The narrow-input stem in row-window mode (b2dl_conv_args.window): an 8 x 16-pixel tile needs
+// kh tap rows of the window image, i.e. one tall (16 + kh - 1)-row box per 64-channel K half,
+// loaded once and addressed per tap row at a 1 KB offset (one SW128 atom).  The
+// weights of all tap rows (kh x 64-wide K halves x 64 output channels) stay resident in
+// shared memory, so per tile only the tall input boxes move: ~7x less operand traffic than
+// streaming one 128-pixel box + weights per (tap row, K half).
+constexpr int HALO_BW = 8, HALO_BH = 16, HALO_BN = 64;
+constexpr int HALO_BBOX = HALO_BN * 64 * 2;  // one (tap row, K half) weight box: 64 co x 64 k
+
+__global__ void __launch_bounds__(FPROP_THREADS, 1)
+    conv_halo_fprop_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                           const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmR,
+                           const __grid_constant__ CUtensorMap tmM, const FpropParams p) {
+  const int taps = p.taps, nh = p.num_cblk;
+  const int a_stage = (HALO_BH + taps - 1) * HALO_BW * 128;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* sB = smem;
+  uint8_t* sA = smem + taps * nh * HALO_BBOX;
+  uint8_t* epi = sA + p.stages * a_stage;
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi + p.epi_bytes);
+  uint64_t* empty = full + FPROP_MAX_STAGES;
+  uint64_t* tfull = empty + FPROP_MAX_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* inbar = tempty + 2;
+  uint64_t* bfull = inbar + 16;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = lane_id();
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 8);
+    }
+    for (int s = 0; s < 16; ++s) mbar_init(&inbar[s], 1);
+    mbar_init(bfull, 1);
+    tma_prefetch(&tmY);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 2 * HALO_BN);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int per_img = p.tiles_x * p.tiles_y;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(bfull, taps * nh * HALO_BBOX);
+      for (int i = 0; i < taps; ++i)
+        for (int h = 0; h < nh; ++h)
+          tma_load_2d(sB + (i * nh + h) * HALO_BBOX, &tmB, bfull, i * p.cin_pad + h * 64, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        const int img = tile / per_img, r = tile - img * per_img;
+        const int ty = r / p.tiles_x, tx = r - ty * p.tiles_x;
+        for (int h = 0; h < nh; ++h) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], a_stage);
+          tma_load_4d(sA + stage * a_stage, &tmA, &full[stage], h * 64, tx * HALO_BW, ty * HALO_BH - p.pad_top, img);
+          if (++stage == p.stages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc_bf16(BM, HALO_BN, false, false);
+      mbar_wait(bfull, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++it) {
+        const int as = it & 1;
+        const uint32_t ap = (it >> 1) & 1;
+        mbar_wait(&tempty[as], ap ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + as * HALO_BN;
+        for (int h = 0; h < nh; ++h) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          // descriptors advance by (byte offset >> 4) in their start-address field
+          const uint64_t ad0 = make_sdesc(smem_u32(sA + stage * a_stage), 16, 1024, LAYOUT_SW128);
+          const uint64_t bd0 = make_sdesc(smem_u32(sB + h * HALO_BBOX), 16, 1024, LAYOUT_SW128);
+          for (int i = 0; i < taps; ++i) {
+            const uint64_t ai = ad0 + ((i * HALO_BW * 128) >> 4);  // tap row i: the box shifted down i rows
+            const uint64_t bi = bd0 + ((i * nh * HALO_BBOX) >> 4);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) umma_bf16(d, ai + 2 * k, bi + 2 * k, idesc, (h | i | k) != 0);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == p.stages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[as]);
+      }
+    }
+  } else {
+    fprop_epilogue_role<HALO_BN, 1>(p, &tmY, &tmR, &tmM, tmem_base, tfull, tempty, inbar, epi, warp, 0, blockIdx.x,
+                                    gridDim.x);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 2 * HALO_BN);
   }
 }
 
@@ -966,6 +1099,150 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 // batched segment reduction (deterministic, fixed order over parts)
+// ------------------------------------------------------------------ row-window halo wgrad
+// dW[(tap row i, k)][co] = sum_p xwin[p + i rows][k] * dy[p][co] for the row-window stem.  A
+// K block is an 8 x 16-pixel block: one tall (16 + kh - 1)-row x box per 64-wide K half serves
+// all kh tap rows (row offset i = 1 KB), against one dy box.  kh accumulators of 128 (k) x 64
+// (co) live in TMEM for the CTA's whole pixel range (split-K over CTAs, one partial each).
+constexpr int HW_BW = 8, HW_BH = 16;  // pixel block (one K block = 128 pixels)
+
+__global__ void __launch_bounds__(192, 1)
+    conv_halo_wgrad_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmDY,
+                           const WgradParams p, int taps, int stages) {
+  const int xbox = (HW_BH + taps - 1) * HW_BW * 128;  // one tall x box (64-wide K half)
+  const int stage_bytes = 2 * xbox + HW_BW * HW_BH * 128;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes);
+  uint64_t* empty = full + FPROP_MAX_STAGES;
+  uint64_t* tfull = empty + FPROP_MAX_STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  float* bred = reinterpret_cast<float*>(tmem_slot + 4);  // [64] bias half-sums
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = lane_id();
+  const int split = blockIdx.x;
+  const int pb_lo = split * p.pb_per_split;
+  const int pb_hi = min(p.num_pb, pb_lo + p.pb_per_split);
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmX);
+    tma_prefetch(&tmDY);
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1 + 4);  // MMA commit + the 4 epilogue warps (dy column sums)
+    }
+    mbar_init(tfull, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int per_img = p.pbx * p.pby;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int pb = pb_lo; pb < pb_hi; ++pb) {
+        const int img = pb / per_img, r = pb - img * per_img;
+        const int by = r / p.pbx, bx = r - by * p.pbx;
+        mbar_wait(&empty[stage], phase ^ 1);
+        mbar_arrive_expect_tx(&full[stage], stage_bytes);
+        uint8_t* st = smem + stage * stage_bytes;
+        for (int h = 0; h < 2; ++h)
+          tma_load_4d(st + h * xbox, &tmX, &full[stage], h * 64, bx * HW_BW, by * HW_BH - p.pad_top, img);
+        tma_load_4d(st + 2 * xbox, &tmDY, &full[stage], 0, bx * HW_BW, by * HW_BH, img);
+        if (++stage == stages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc_bf16(128, 64, true, true);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int pb = pb_lo; pb < pb_hi; ++pb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        const uint32_t x0 = smem_u32(smem + stage * stage_bytes);
+        const uint64_t ad0 = make_sdesc(x0, xbox, 1024, LAYOUT_SW128);
+        const uint64_t bd0 = make_sdesc(x0 + 2 * xbox, 16384, 1024, LAYOUT_SW128);
+        const uint32_t acc = pb > pb_lo;
+        for (int i = 0; i < taps; ++i) {
+          const uint64_t ai = ad0 + ((i * HW_BW * 128) >> 4);
+#pragma unroll
+          for (int k = 0; k < HW_BW * HW_BH / 16; ++k)  // 16 pixels (2 KB) per K step
+            umma_bf16(tmem_base + i * 64, ai + k * 128, bd0 + k * 128, idesc, acc | k);
+        }
+        umma_commit(&empty[stage]);
+        if (++stage == stages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      umma_commit(tfull);
+    }
+  } else {
+    const int t = threadIdx.x - 64;  // 0..127
+    const int co = t & 63, ph = t >> 6;
+    float bs = 0.f;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int pb = pb_lo; pb < pb_hi; ++pb) {
+      mbar_wait(&full[stage], phase);
+      if (p.bsum) {
+        const uint8_t* dyt = smem + stage * stage_bytes + 2 * xbox;
+#pragma unroll 8
+        for (int px = ph * 64; px < ph * 64 + 64; ++px)
+          bs += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(
+              dyt + px * 128 + ((((co >> 3) ^ (px & 7))) << 4) + (co & 7) * 2));
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == stages) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+    // bias partial of this split: the two pixel halves meet in shared memory
+    if (ph == 1) bred[co] = bs;
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (ph == 0 && p.bsum && co < p.cout) p.bsum[static_cast<long long>(split) * p.cout + co] = bs + bred[co];
+    // weight partial: lane = k row of the 128-row accumulators
+    mbar_wait(tfull, 0);
+    tc_fence_after();
+    const int q = warp & 3;
+    const int k = q * 32 + lane;
+    float* out = p.ws + static_cast<long long>(split) * p.krows * p.cout;
+    for (int i = 0; i < taps; ++i) {
+      float v[64];
+      tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + i * 64, v);
+      tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + i * 64 + 32, v + 32);
+      if (k < p.cin) {
+        float* row = out + (static_cast<long long>(i) * p.cin + k) * p.cout;
+        if (p.cout == 64) {
+#pragma unroll
+          for (int c = 0; c < 64; c += 4) *reinterpret_cast<float4*>(row + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 64; ++c)
+            if (c < p.cout) row[c] = v[c];
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
 __global__ void reduce_segments_kernel(const b2dl_segment* __restrict__ segs, float* __restrict__ base) {
   const b2dl_segment sg = segs[blockIdx.y];
   float* dst = base + sg.dst_off;
@@ -1087,6 +1364,14 @@ static bool fprop_pairs_enabled() {
   return on;
 }
 
+static int pick_bn(int cout) {
+  if (cout > 128) return 256;
+  if (cout > 64) return 128;
+  if (cout > 32) return 64;
+  if (cout > 16) return 32;
+  return 16;
+}
+
 // TMA-staged fprop epilogue; B2DL_TMA_EPILOGUE=0 selects the register/shared-memory path
 static bool tma_epilogue_enabled() {
   static const bool on = [] {
@@ -1096,16 +1381,85 @@ static bool tma_epilogue_enabled() {
   return on;
 }
 
-static int pick_bn(int cout) {
-  if (cout > 128) return 256;
-  if (cout > 64) return 128;
-  if (cout > 32) return 64;
-  if (cout > 16) return 32;
-  return 16;
-}
-
 static bool view_aligned(const b2dl_act& a, int elem_bytes) {
   return (reinterpret_cast<uintptr_t>(a.ptr) % 16 == 0) && ((static_cast<long long>(a.c_stride) * elem_bytes) % 16 == 0);
+}
+
+// Row-window stem through the halo kernel: packed weights, <= 64 output channels, <= 7 tap
+// rows, a 64- or 128-wide folded K, bf16 output through the TMA epilogue.
+static int launch_halo_fprop(const b2dl_conv_args* a, const b2dl_act& xv, cudaStream_t st) {
+  const b2dl_act& y = a->y;
+  FpropParams p{};
+  p.n = y.n;
+  p.h = y.h;
+  p.w = y.w;
+  p.bw = HALO_BW;
+  p.bh = HALO_BH;
+  p.tiles_x = cdiv(y.w, HALO_BW);
+  p.tiles_y = cdiv(y.h, HALO_BH);
+  p.num_m_tiles = y.n * p.tiles_x * p.tiles_y;
+  p.num_n_tiles = 1;
+  p.num_tiles = p.num_m_tiles;
+  p.kw = 1;
+  p.dil = 1;
+  p.pad_top = a->pad_top;
+  p.cin_pad = b2dl_cin_pad(xv.c);
+  p.num_cblk = p.cin_pad / 64;
+  p.taps = a->kh;
+  p.num_kb = p.taps * p.num_cblk;
+  p.cout = a->cout;
+  p.y = y.ptr;
+  p.y_stride = y.c_stride;
+  p.bias = a->bias;
+  p.bias_vec = a->bias && (reinterpret_cast<uintptr_t>(a->bias) % 16 == 0);
+  p.res = reinterpret_cast<const __nv_bfloat16*>(a->residual.ptr);
+  p.res_stride = a->residual.c_stride;
+  p.mask = reinterpret_cast<const __nv_bfloat16*>(a->mask.ptr);
+  p.mask_stride = a->mask.c_stride;
+  p.relu = a->relu;
+  p.accumulate = a->accumulate;
+  p.vec_ok = 1;
+  p.tma_epi = 1;
+  p.epi_nops = (p.res != nullptr) + (p.mask != nullptr) + (p.accumulate != 0);
+  p.epi_bytes = 8 * epi_warp_bytes(p.epi_nops);
+  const int a_stage = (HALO_BH + p.taps - 1) * HALO_BW * 128;
+  const int b_region = p.taps * p.num_cblk * HALO_BBOX;
+  p.stages = std::min(FPROP_MAX_STAGES, (SMEM_MAX - SMEM_FIXED - b_region - p.epi_bytes) / a_stage);
+  if (p.stages < 2) return B2DL_E_NOT_IMPLEMENTED;
+  const int smem = b_region + p.stages * a_stage + p.epi_bytes + SMEM_FIXED;
+
+  FpropMaps t;
+  const int bwx = std::min(p.bw, 32), bhx = 32 / bwx;
+  const uint64_t ktot = static_cast<uint64_t>(p.taps) * p.cin_pad;
+  const uint64_t wd[2] = {ktot, static_cast<uint64_t>(a->cout)};
+  const uint64_t wsd[1] = {ktot * 2};
+  const uint32_t wb[2] = {64u, static_cast<uint32_t>(HALO_BN)};
+  if (window_map(&t.a, a->x, xv.c, y.w, 64, HALO_BW, HALO_BH + p.taps - 1, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      encode_tiled(&t.b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a->w_packed), wd, wsd, wb,
+                   CU_TENSOR_MAP_SWIZZLE_128B) ||
+      act_map(&t.y, y, 32, bwx, bhx, CU_TENSOR_MAP_SWIZZLE_64B) ||
+      (p.res && act_map(&t.r, a->residual, 32, bwx, bhx, CU_TENSOR_MAP_SWIZZLE_64B)) ||
+      (p.mask && act_map(&t.m, a->mask, 32, bwx, bhx, CU_TENSOR_MAP_SWIZZLE_64B)))
+    return B2DL_E_ALIGN;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(conv_halo_fprop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX) !=
+        cudaSuccess)
+      return B2DL_E_CUDA;
+    attr_set = true;
+  }
+  const int grid = std::min(p.num_tiles, num_sms());
+  conv_halo_fprop_kernel<<<grid, FPROP_THREADS, smem, st>>>(t.a, t.b, t.y, t.r, t.m, p);
+  return check_launch();
+}
+
+static bool halo_fprop_ok(const b2dl_conv_args* a, const b2dl_act& xv) {
+  const b2dl_act& y = a->y;
+  const int nops = (a->residual.ptr != nullptr) + (a->mask.ptr != nullptr) + (a->accumulate != 0);
+  return a->window && a->w_mode == 0 && a->w_packed && a->cout <= HALO_BN && a->cout % 8 == 0 && a->kh <= 7 &&
+         a->dilation == 1 && xv.c > 16 && xv.c <= 128 && !a->y_f32 && view_aligned(y, 2) && nops <= 2 &&
+         (!a->residual.ptr || view_aligned(a->residual, 2)) && (!a->mask.ptr || view_aligned(a->mask, 2)) &&
+         tma_epilogue_enabled();
 }
 
 }  // namespace b2
@@ -1114,13 +1468,29 @@ using namespace b2;
 
 extern "C" int b2dl_cin_pad(int cin) { return cin <= 16 ? 16 : round_up(cin, 64); }
 
+namespace b2 {
+// Row-window mode: the virtual input (kw-folded channels over the output width); validates
+// the haloed storage of x.
+static int window_view(const b2dl_act& x, int window, int kw, int pad_left, int out_w, b2dl_act* xv) {
+  *xv = x;
+  if (!window) return B2DL_OK;
+  if (window < 1 || kw != 1 || pad_left != 0 || x.c != x.c_stride || x.w < out_w + window - 1)
+    return B2DL_E_VALUE;
+  xv->c = window * x.c;
+  xv->w = out_w;
+  return B2DL_OK;
+}
+}  // namespace b2
+
 extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
   if (!a || !a->x.ptr || !a->y.ptr || a->w_mode < 0 || a->w_mode > 2) return B2DL_E_VALUE;
-  const b2dl_act& x = a->x;
   const b2dl_act& y = a->y;
+  b2dl_act x;
+  if (window_view(a->x, a->window, a->kw, a->pad_left, y.w, &x)) return B2DL_E_VALUE;
   if (x.n != y.n || x.h != y.h || x.w != y.w || y.c != a->cout) return B2DL_E_VALUE;
   if (a->kh < 1 || a->kw < 1 || a->dilation < 1 || a->cout < 1 || x.c < 1) return B2DL_E_VALUE;
   if (!view_aligned(x, 2)) return B2DL_E_ALIGN;
+  if (halo_fprop_ok(a, x)) return launch_halo_fprop(a, x, as_stream(stream));
   const int kblk = x.c <= 16 ? 16 : 64;
   const int cin_pad = b2dl_cin_pad(x.c);
   int bn = a->block_n ? a->block_n : pick_bn(a->cout);
@@ -1176,7 +1546,8 @@ extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
 
   FpropMaps t;
   const CUtensorMapSwizzle sw = kblk == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B;
-  if (act_map(&t.a, x, kblk, p.bw, p.bh, sw)) return B2DL_E_ALIGN;
+  if (a->window ? window_map(&t.a, a->x, x.c, y.w, kblk, p.bw, p.bh, sw) : act_map(&t.a, x, kblk, p.bw, p.bh, sw))
+    return B2DL_E_ALIGN;
   const int mode = a->w_mode;
   p.b_mode = mode;
   p.taps = a->kh * a->kw;
@@ -1245,12 +1616,46 @@ namespace b2 {
 struct WgradPlan {
   WgradParams p;
   int bn, xw;
+  int halo;  // row-window stem kernel
   size_t ws_bytes, bsum_bytes;
 };
 static int plan_wgrad(const b2dl_wgrad_args* a, WgradPlan* out) {
-  const b2dl_act& x = a->x;
   const b2dl_act& dy = a->dy;
+  b2dl_act x;
+  if (window_view(a->x, a->window, a->kw, a->pad_left, dy.w, &x)) return B2DL_E_VALUE;
   if (x.n != dy.n || x.h != dy.h || x.w != dy.w) return B2DL_E_VALUE;
+  out->halo = 0;
+  if (a->window && dy.c <= 64 && a->kh <= 8 && x.c > 16 && x.c <= 128 && a->dilation == 1) {
+    // row-window stem: 8 x 16-pixel K blocks, one split (partial) per CTA
+    WgradParams p{};
+    p.n = x.n;
+    p.h = x.h;
+    p.w = x.w;
+    p.bwk = HW_BW;
+    p.bhk = HW_BH;
+    p.pbx = cdiv(x.w, HW_BW);
+    p.pby = cdiv(x.h, HW_BH);
+    p.num_pb = x.n * p.pbx * p.pby;
+    p.kw = 1;
+    p.dil = 1;
+    p.pad_top = a->pad_top;
+    p.cin = x.c;
+    p.cout = dy.c;
+    p.krows = static_cast<long long>(a->kh) * x.c;
+    p.m_tiles = 1;
+    p.n_tiles = 1;
+    const int splits = std::min(num_sms(), p.num_pb);
+    p.pb_per_split = cdiv(p.num_pb, splits);
+    p.splits = cdiv(p.num_pb, p.pb_per_split);
+    p.num_tiles = p.splits;
+    out->p = p;
+    out->bn = 64;
+    out->xw = 64;
+    out->halo = 1;
+    out->ws_bytes = static_cast<size_t>(p.splits) * p.krows * p.cout * sizeof(float);
+    out->bsum_bytes = static_cast<size_t>(p.splits) * p.cout * sizeof(float);
+    return B2DL_OK;
+  }
   WgradParams p{};
   p.n = x.n;
   p.h = x.h;
@@ -1329,40 +1734,64 @@ extern "C" int b2dl_conv_wgrad(const b2dl_wgrad_args* a, void* stream) {
                                                       align_up(pl.ws_bytes, 256))
                            : nullptr;
   CUtensorMap tx, tdy;
-  // x: 5-D map (64-ch inner, W, H, N, channel block) when chunks of one tap can be grouped
-  pl.p.xg = 0;
-  if (pl.xw == 64 && a->x.c % 64 == 0) {
-    const int cblk = a->x.c / 64;
-    const int g = cblk % 4 == 0 ? 4 : (cblk % 2 == 0 ? 2 : 1);
-    if (g > 1) {
-      if (act_map5(&tx, a->x, pl.p.bwk, pl.p.bhk, g)) return B2DL_E_ALIGN;
-      pl.p.xg = g;
-    }
-  }
-  if (!pl.p.xg && act_map(&tx, a->x, pl.xw, pl.p.bwk, pl.p.bhk,
-                          pl.xw == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B))
-    return B2DL_E_ALIGN;
-  pl.p.dyg = 0;
-  const int nbw = pl.bn < 64 ? 1 : pl.bn / 64;
-  if (nbw > 1 && a->dy.c % pl.bn == 0) {
-    if (act_map5(&tdy, a->dy, pl.p.bwk, pl.p.bhk, nbw)) return B2DL_E_ALIGN;
-    pl.p.dyg = nbw;
-  } else if (act_map(&tdy, a->dy, 64, pl.p.bwk, pl.p.bhk, CU_TENSOR_MAP_SWIZZLE_128B)) {
-    return B2DL_E_ALIGN;
-  }
   cudaStream_t st = as_stream(stream);
-#define B2_WG(BNV)                                                         \
-  case BNV:                                                                \
+  if (pl.halo) {
+    const int taps = a->kh;
+    if (window_map(&tx, a->x, pl.p.cin, a->dy.w, 64, HW_BW, HW_BH + taps - 1, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        act_map(&tdy, a->dy, 64, HW_BW, HW_BH, CU_TENSOR_MAP_SWIZZLE_128B))
+      return B2DL_E_ALIGN;
+    const int stage_bytes = 2 * (HW_BH + taps - 1) * HW_BW * 128 + HW_BW * HW_BH * 128;
+    const int stages = std::min(FPROP_MAX_STAGES, (SMEM_MAX - SMEM_FIXED) / stage_bytes);
+    static bool attr_set = false;
+    if (!attr_set) {
+      if (cudaFuncSetAttribute(conv_halo_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX) !=
+          cudaSuccess)
+        return B2DL_E_CUDA;
+      attr_set = true;
+    }
+    conv_halo_wgrad_kernel<<<pl.p.splits, 192, stages * stage_bytes + SMEM_FIXED, st>>>(
+        tx, tdy, pl.p, taps, stages);
+    rc = check_launch();
+    if (rc) return rc;
+  } else {
+    // x: 5-D map (64-ch inner, W, H, N, channel block) when chunks of one tap can be grouped
+    pl.p.xg = 0;
+    if (a->window) {
+      if (pl.xw != 64 || window_map(&tx, a->x, a->window * a->x.c, a->dy.w, 64, pl.p.bwk, pl.p.bhk,
+                                    CU_TENSOR_MAP_SWIZZLE_128B))
+        return B2DL_E_ALIGN;
+    } else if (pl.xw == 64 && a->x.c % 64 == 0) {
+      const int cblk = a->x.c / 64;
+      const int g = cblk % 4 == 0 ? 4 : (cblk % 2 == 0 ? 2 : 1);
+      if (g > 1) {
+        if (act_map5(&tx, a->x, pl.p.bwk, pl.p.bhk, g)) return B2DL_E_ALIGN;
+        pl.p.xg = g;
+      }
+    }
+    if (!a->window && !pl.p.xg && act_map(&tx, a->x, pl.xw, pl.p.bwk, pl.p.bhk,
+                            pl.xw == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B))
+      return B2DL_E_ALIGN;
+    pl.p.dyg = 0;
+    const int nbw = pl.bn < 64 ? 1 : pl.bn / 64;
+    if (nbw > 1 && a->dy.c % pl.bn == 0) {
+      if (act_map5(&tdy, a->dy, pl.p.bwk, pl.p.bhk, nbw)) return B2DL_E_ALIGN;
+      pl.p.dyg = nbw;
+    } else if (act_map(&tdy, a->dy, 64, pl.p.bwk, pl.p.bhk, CU_TENSOR_MAP_SWIZZLE_128B)) {
+      return B2DL_E_ALIGN;
+    }
+#define B2_WG(BNV)                                                                                      \
+  case BNV:                                                                                             \
     rc = pl.xw == 64 ? launch_wgrad<BNV, 64>(tx, tdy, pl.p, st) : launch_wgrad<BNV, 16>(tx, tdy, pl.p, st); \
     break;
-  switch (pl.bn) {
-    B2_WG(256)
-    B2_WG(128)
-    B2_WG(64)
-    B2_WG(32)
-    default:
-      rc = pl.xw == 64 ? launch_wgrad<16, 64>(tx, tdy, pl.p, st) : launch_wgrad<16, 16>(tx, tdy, pl.p, st);
-      break;
+    switch (pl.bn) {
+      B2_WG(256)
+      B2_WG(128)
+      B2_WG(64)
+      B2_WG(32)
+      default:
+        rc = pl.xw == 64 ? launch_wgrad<16, 64>(tx, tdy, pl.p, st) : launch_wgrad<16, 16>(tx, tdy, pl.p, st);
+        break;
+    }
   }
 #undef B2_WG
   if (rc) return rc;

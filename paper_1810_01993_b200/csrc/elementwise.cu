@@ -39,6 +39,38 @@ __global__ void k_nchw_to_nhwc(const float* __restrict__ x, void* __restrict__ y
       reinterpret_cast<__nv_bfloat16*>(y)[d] = __float2bfloat16_rn(x[i]);
   }
 }
+// NCHW fp32 -> haloed NHWC bf16 rows: a block moves 64 columns x c channels of one image row
+// through shared memory, so both the strided planes and the pixel-major output are coalesced.
+constexpr int HALO_COLS = 64;
+__global__ void __launch_bounds__(256) k_nchw_to_nhwc_halo(const float* __restrict__ x, __nv_bfloat16* __restrict__ y,
+                                                           int c, int h, int w, int wp, int left) {
+  extern __shared__ __nv_bfloat16 tile[];  // [HALO_COLS][c + 8]
+  const int cp = c + 8;
+  const int x0 = blockIdx.x * HALO_COLS, row = blockIdx.y, img = blockIdx.z;
+  const int t = threadIdx.x & 63;
+  const long long plane = static_cast<long long>(h) * w;
+  const float* src = x + static_cast<long long>(img) * c * plane + static_cast<long long>(row) * w + x0 + t;
+  for (int ch = threadIdx.x >> 6; ch < c; ch += 4)
+    tile[t * cp + ch] = __float2bfloat16_rn(x0 + t < w ? __ldg(src + ch * plane) : 0.f);
+  __syncthreads();
+  const int vec = c / 8;  // 16-byte pieces per pixel
+  __nv_bfloat16* dst_row = y + (static_cast<long long>(img) * h + row) * wp * c;
+  for (int i = threadIdx.x; i < HALO_COLS * vec; i += 256) {
+    const int px = i / vec, pc = i - px * vec;
+    if (x0 + px >= w) break;
+    *reinterpret_cast<uint4*>(dst_row + static_cast<long long>(left + x0 + px) * c + pc * 8) =
+        *reinterpret_cast<const uint4*>(tile + px * cp + pc * 8);
+  }
+  if (blockIdx.x == 0) {  // zero halo columns of this row
+    const int nh = wp - w;
+    for (int i = threadIdx.x; i < nh * vec; i += 256) {
+      const int k = i / vec, pc = i - k * vec;
+      const int col = k < left ? k : w + k;
+      *reinterpret_cast<uint4*>(dst_row + static_cast<long long>(col) * c + pc * 8) = make_uint4(0, 0, 0, 0);
+    }
+  }
+}
+
 __global__ void k_nhwc_to_nchw(const void* __restrict__ x, int f32, float* __restrict__ y, int n, int c, int h, int w,
                                int cs) {
   const long long hw = static_cast<long long>(h) * w;
@@ -403,6 +435,16 @@ extern "C" int b2dl_nchw_to_nhwc(const float* x, b2dl_act y, int dst_f32, void* 
   if (!x || !y.ptr) return B2DL_E_VALUE;
   long long total = static_cast<long long>(y.n) * y.c * y.h * y.w;
   k_nchw_to_nhwc<<<grid1d(total), 256, 0, as_stream(stream)>>>(x, y.ptr, dst_f32, y.n, y.c, y.h, y.w, y.c_stride);
+  return check_launch();
+}
+
+extern "C" int b2dl_nchw_to_nhwc_halo(const float* x, int n, int c, int h, int w, void* y, int wp, int left,
+                                      void* stream) {
+  if (!x || !y || n < 1 || h < 1 || w < 1 || left < 0 || wp < w + left) return B2DL_E_VALUE;
+  if (c < 8 || c > 64 || c % 8 || (reinterpret_cast<uintptr_t>(y) & 15)) return B2DL_E_ALIGN;
+  dim3 grid(cdiv(w, HALO_COLS), h, n);
+  const size_t smem = static_cast<size_t>(HALO_COLS) * (c + 8) * sizeof(__nv_bfloat16);
+  k_nchw_to_nhwc_halo<<<grid, 256, smem, as_stream(stream)>>>(x, BF(y), c, h, w, wp, left);
   return check_launch();
 }
 

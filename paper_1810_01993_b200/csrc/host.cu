@@ -62,6 +62,20 @@ int act_map(CUtensorMap* m, const b2dl_act& a, int box_c, int box_w, int box_h, 
   return encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, a.ptr, dims, strides, box, sw);
 }
 
+// Row-window view of a haloed NHWC image (conv window mode): virtual pixel (y, xx) holds the
+// c_v contiguous values x[y][xx..][..] starting at pixel xx, so neighbouring virtual pixels
+// overlap in memory (pixel stride < inner extent); TMA zero-fills virtual channels >= c_v.
+int window_map(CUtensorMap* m, const b2dl_act& x, int c_v, int w_v, int box_c, int box_w, int box_h,
+               CUtensorMapSwizzle sw) {
+  const uint64_t ps = static_cast<uint64_t>(x.c_stride) * 2;
+  const uint64_t dims[4] = {static_cast<uint64_t>(c_v), static_cast<uint64_t>(w_v), static_cast<uint64_t>(x.h),
+                            static_cast<uint64_t>(x.n)};
+  const uint64_t strides[3] = {ps, ps * x.w, ps * x.w * x.h};
+  const uint32_t box[4] = {static_cast<uint32_t>(box_c), static_cast<uint32_t>(box_w), static_cast<uint32_t>(box_h),
+                           1u};
+  return encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, x.ptr, dims, strides, box, sw);
+}
+
 // 5-D map (64-channel inner, W, H, N, channel block): one box = g chunks of [pixels][64 ch],
 // stored chunk-major in shared memory (the MN-major operand's LBO-separated chunks)
 int act_map5(CUtensorMap* m, const b2dl_act& a, int box_w, int box_h, int g) {

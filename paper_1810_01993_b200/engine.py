@@ -380,13 +380,32 @@ class Engine:
             self.wf[o.w] = torch.zeros((o.cout, t, nhwc.cin_pad(o.cin)), dtype=bf, device=self.device)
             if o.ins[0] in p.live:
                 self.wd[o.w] = torch.zeros((o.cin, t, nhwc.cin_pad(o.cout)), dtype=bf, device=self.device)
+        # Row-window stem: when the data input feeds exactly one narrow conv (the 16-channel 7x7
+        # stem), the input is stored with its horizontal padding baked in and the conv folds the
+        # kw taps of a kernel row into one K run of kw*cin channels (b2dl_conv_args.window):
+        # 14 64-wide K blocks instead of 49 16-wide ones.
+        self.win = None
+        users = [o for o in p.ops if "x" in o.ins]
+        if len(users) == 1 and users[0].kind == "conv":
+            o = users[0]
+            if (o.k > 1 and o.dil == 1 and o.cin % 8 == 0 and 16 < o.cin * o.k <= 128 and o.cout % 8 == 0
+                    and o.ins[0] == "x" and not o.res):
+                n_, c_, h_, w_ = input_shape
+                self.win = o
+                self.xwin = torch.zeros((n_, h_, w_ + o.k - 1, c_), dtype=bf, device=self.device)
+                self.wwin = torch.zeros((o.cout, o.k, nhwc.cin_pad(o.k * o.cin)), dtype=bf, device=self.device)
         # persistent split-K partial buffers (wgrad + bias column sums), reduced per bucket
         self.partials = {}
         self.segs = {}
         total, offs = 0, {}
         for o in self.convs:
-            nbytes, wp, bp, bo = nhwc.wgrad_partials(self._probe_view(o.ins[0]), self._probe_view(o.out),
-                                                     o.k, o.k, o.dil)
+            if o is self.win:
+                nbytes, wp, bp, bo = nhwc.wgrad_partials(
+                    View(torch.empty(self.xwin.shape, dtype=bf, device="meta")), self._probe_view(o.out),
+                    o.k, 1, 1, window=o.k)
+            else:
+                nbytes, wp, bp, bo = nhwc.wgrad_partials(self._probe_view(o.ins[0]), self._probe_view(o.out),
+                                                         o.k, o.k, o.dil)
             offs[o.w] = (total, nbytes, wp, bp, bo)
             total += (nbytes + 255) // 256 * 256
         self.partials_buf = torch.empty(max(total, 256), dtype=torch.uint8, device=self.device)
@@ -519,13 +538,20 @@ class Engine:
             nhwc.pack_weights(self.wslice(o.w), o.k, o.k, o.cin, o.cout, fprop=self.wf[o.w],
                               dgrad=self.wd.get(o.w))
             self.launches += 1 + (o.w in self.wd)
+        if self.win is not None:   # HWIO [k][k][cin][cout] is HWIO [k][1][k*cin][cout]
+            o = self.win
+            nhwc.pack_weights(self.wslice(o.w), o.k, 1, o.k * o.cin, o.cout, fprop=self.wwin)
+            self.launches += 1
 
     # ---------------------------------------------------------------- inputs
     def set_batch(self, x_nchw: torch.Tensor, labels: torch.Tensor):
         """x fp32 NCHW and labels uint8 [N,H,W] already on the device."""
         if tuple(x_nchw.shape) != self.input_shape:
             raise ValueError(f"batch {tuple(x_nchw.shape)} does not match planned {self.input_shape}")
-        nhwc.nchw_to_nhwc(x_nchw.contiguous(), self.v("x"))
+        if self.win is not None:
+            nhwc.nchw_to_nhwc_halo(x_nchw.contiguous(), self.xwin, (self.win.k - 1) // 2)
+        else:
+            nhwc.nchw_to_nhwc(x_nchw.contiguous(), self.v("x"))
         self.labels.copy_(labels.reshape(-1))
         self.launches += 1
 
@@ -542,7 +568,11 @@ class Engine:
                 ev = self._tic()
                 wsrc = dict(w_packed=self.wf[op.w]) if op.w in self.wf else dict(
                     w_packed=None, w_master=self.wmaster(op.w), w_mode=1)
-                nhwc.conv_fprop(self.v(op.ins[0]), cout=op.cout, kh=op.k, kw=op.k, dilation=op.dil, y=self.v(out),
+                xin, kw = self.v(op.ins[0]), op.k
+                if op is self.win:
+                    wsrc = dict(w_packed=self.wwin, window=op.k)
+                    xin, kw = View(self.xwin), 1
+                nhwc.conv_fprop(xin, cout=op.cout, kh=op.k, kw=kw, dilation=op.dil, y=self.v(out),
                                 **wsrc,
                                 bias=self.flat_w[b_off:b_off + op.cout],
                                 residual=self.v(op.res) if op.res else None, relu=op.relu,
@@ -599,7 +629,10 @@ class Engine:
                 ev = self._tic()
                 # wgrad GEMM with the bias column sums folded in; split-K partials stay in the
                 # conv's partial buffer until its bucket is reduced in one batched launch
-                nhwc.conv_wgrad_deferred(self.v(op.ins[0]), gy, op.k, op.k, op.dil, self.partials[op.w])
+                if op is self.win:
+                    nhwc.conv_wgrad_deferred(View(self.xwin), gy, op.k, 1, 1, self.partials[op.w], window=op.k)
+                else:
+                    nhwc.conv_wgrad_deferred(self.v(op.ins[0]), gy, op.k, op.k, op.dil, self.partials[op.w])
                 self._toc(ev, op)
                 self.launches += 1
                 for name in (op.w, op.b):

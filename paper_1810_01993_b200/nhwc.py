@@ -68,13 +68,14 @@ def same_pads(k: int, d: int):
 
 def conv_fprop(x: View, w_packed: torch.Tensor | None, cout: int, kh: int, kw: int, dilation: int,
                y: View, bias=None, residual: View | None = None, relu=False, accumulate=False,
-               mask: View | None = None, y_f32=False, pads=None, block_n=0, w_master=None, w_mode=0):
+               mask: View | None = None, y_f32=False, pads=None, block_n=0, w_master=None, w_mode=0, window=0):
     """w_mode 0: w_packed bf16 [cout][taps][cin_pad]; 1: w_master bf16 HWIO of this conv;
-    2: w_master bf16 HWIO of the forward conv whose input gradient this is (see b2dl.h)."""
+    2: w_master bf16 HWIO of the forward conv whose input gradient this is (see b2dl.h).
+    window > 0: row-window mode over a haloed x (pass kw=1; see b2dl_conv_args.window)."""
     pt, pl = pads if pads is not None else (same_pads(kh, dilation)[0], same_pads(kw, dilation)[0])
     a = ConvArgs(x.act(), _ptr(w_packed), cout, kh, kw, dilation, pt, pl,
                  y.act(), int(y_f32), _ptr(bias), _act(residual), int(relu), int(accumulate),
-                 _act(mask), block_n, _ptr(w_master), w_mode)
+                 _act(mask), block_n, _ptr(w_master), w_mode, window)
     check(LIB.b2dl_conv_fprop(ctypes.byref(a), _stream()), "conv_fprop")
 
 
@@ -103,11 +104,11 @@ class Workspace:
 
 
 def conv_wgrad(x: View, dy: View, kh: int, kw: int, dilation: int, dw: torch.Tensor,
-               ws: Workspace, bias_grad=None, accumulate=False, splits=0):
+               ws: Workspace, bias_grad=None, accumulate=False, splits=0, window=0):
     """dw fp32 HWIO [kh*kw][cin][cout] (+)= x^T dy per tap; bias_grad[cout] (+)= sum dy."""
     pt, pl = same_pads(kh, dilation)[0], same_pads(kw, dilation)[0]
     a = WgradArgs(x.act(), dy.act(), kh, kw, dilation, pt, pl, ctypes.c_void_p(dw.data_ptr()),
-                  _ptr(bias_grad), int(accumulate), None, 0, splits)
+                  _ptr(bias_grad), int(accumulate), None, 0, splits, 0, window)
     need = LIB.b2dl_wgrad_workspace_size(ctypes.byref(a))
     buf = ws.get(need)
     a.workspace = ctypes.c_void_p(buf.data_ptr())
@@ -115,14 +116,14 @@ def conv_wgrad(x: View, dy: View, kh: int, kw: int, dilation: int, dw: torch.Ten
     check(LIB.b2dl_conv_wgrad(ctypes.byref(a), _stream()), "conv_wgrad")
 
 
-def _wgrad_args(x: View, dy: View, kh: int, kw: int, dilation: int, defer: bool):
+def _wgrad_args(x: View, dy: View, kh: int, kw: int, dilation: int, defer: bool, window=0):
     pt, pl = same_pads(kh, dilation)[0], same_pads(kw, dilation)[0]
-    return WgradArgs(x.act(), dy.act(), kh, kw, dilation, pt, pl, None, None, 0, None, 0, 0, int(defer))
+    return WgradArgs(x.act(), dy.act(), kh, kw, dilation, pt, pl, None, None, 0, None, 0, 0, int(defer), window)
 
 
-def wgrad_partials(x: View, dy: View, kh: int, kw: int, dilation: int):
+def wgrad_partials(x: View, dy: View, kh: int, kw: int, dilation: int, window=0):
     """(workspace bytes, weight parts, bias parts, bias byte offset) of a deferred wgrad."""
-    a = _wgrad_args(x, dy, kh, kw, dilation, True)
+    a = _wgrad_args(x, dy, kh, kw, dilation, True, window)
     a.bias_grad = ctypes.c_void_p(1)  # bias partials requested (layout query only)
     nbytes = LIB.b2dl_wgrad_workspace_size(ctypes.byref(a))
     wp, bp, bo = ctypes.c_int(), ctypes.c_int(), ctypes.c_size_t()
@@ -131,9 +132,9 @@ def wgrad_partials(x: View, dy: View, kh: int, kw: int, dilation: int):
     return nbytes, wp.value, bp.value, bo.value
 
 
-def conv_wgrad_deferred(x: View, dy: View, kh: int, kw: int, dilation: int, partials: torch.Tensor):
+def conv_wgrad_deferred(x: View, dy: View, kh: int, kw: int, dilation: int, partials: torch.Tensor, window=0):
     """wgrad + bias column sums left as split-K partials in `partials` (see wgrad_partials)."""
-    a = _wgrad_args(x, dy, kh, kw, dilation, True)
+    a = _wgrad_args(x, dy, kh, kw, dilation, True, window)
     a.dw = ctypes.c_void_p(partials.data_ptr())        # unused in deferred mode, must be non-null
     a.bias_grad = ctypes.c_void_p(partials.data_ptr())
     a.workspace = ctypes.c_void_p(partials.data_ptr())
@@ -161,6 +162,13 @@ def pack_weights(w_hwio: torch.Tensor, kh: int, kw: int, cin: int, cout: int, fp
 def nchw_to_nhwc(x: torch.Tensor, y: View, dst_f32=False):
     check(LIB.b2dl_nchw_to_nhwc(ctypes.c_void_p(x.data_ptr()), y.act(), int(dst_f32), _stream()),
           "nchw_to_nhwc")
+
+
+def nchw_to_nhwc_halo(x: torch.Tensor, y: torch.Tensor, left: int):
+    """x fp32 [n][c][h][w] -> y bf16 [n][h][wp][c], column xx at left + xx, zero halo columns."""
+    n, c, h, w = x.shape
+    check(LIB.b2dl_nchw_to_nhwc_halo(ctypes.c_void_p(x.data_ptr()), n, c, h, w, ctypes.c_void_p(y.data_ptr()),
+                                     y.shape[2], left, _stream()), "nchw_to_nhwc_halo")
 
 
 def nhwc_to_nchw(x: View, y: torch.Tensor, src_f32=False):

@@ -172,3 +172,37 @@ def test_cta_pair_tiles(case):
         nhwc.conv_dgrad(nhwc.View(dy), None if use_master else wd, cin, k, k, d, nhwc.View(dx), dx_f32=True,
                         w_master=wm if use_master else None, block_n=256)
         assert _rel(dx, gref) < 2e-3, (case, use_master)
+
+
+@pytest.mark.parametrize("case", [(2, 16, 32, 48, 64, 7), (1, 16, 20, 24, 64, 7), (1, 8, 16, 16, 32, 5)])
+def test_row_window_conv(case):
+    """Row-window mode (the 7x7 stem): a haloed NHWC copy of the input, with the kw taps of a
+    kernel row folded into K, gives the ordinary conv; wgrad lands in the ordinary HWIO layout."""
+    from paper_1810_01993_b200 import nhwc
+    n, cin, h, w, cout, k = case
+    p = (k - 1) // 2
+    torch.manual_seed(5)
+    x = torch.randn(n, cin, h, w, device="cuda")
+    xw = torch.full((n, h, w + k - 1, cin), 7.0, dtype=torch.bfloat16, device="cuda")  # halo must be zeroed
+    nhwc.nchw_to_nhwc_halo(x, xw, p)
+    assert torch.equal(xw[:, :, p:p + w].float(), x.to(torch.bfloat16).float().permute(0, 2, 3, 1))
+    assert xw[:, :, :p].abs().max() == 0 and xw[:, :, p + w:].abs().max() == 0
+    w_hwio = torch.randn(k * k, cin, cout, device="cuda") / (k * k * cin) ** 0.5
+    wp = torch.empty(cout, k, nhwc.cin_pad(k * cin), dtype=torch.bfloat16, device="cuda")
+    nhwc.pack_weights(w_hwio, k, 1, k * cin, cout, fprop=wp)
+    bias = torch.randn(cout, device="cuda")
+    y = torch.zeros(n, h, w, cout, dtype=torch.bfloat16, device="cuda")
+    nhwc.conv_fprop(nhwc.View(xw), wp, cout, k, 1, 1, nhwc.View(y), bias=bias, relu=True, window=k)
+    xr = _bf(x)
+    wr = w_hwio.to(torch.bfloat16).double().reshape(k, k, cin, cout).permute(3, 2, 0, 1)
+    ref = torch.relu(F.conv2d(xr, wr, padding=p) + bias.double()[None, :, None, None]).permute(0, 2, 3, 1)
+    assert _rel(y, ref) < 1e-2
+    dy = torch.randn(n, h, w, cout, device="cuda").to(torch.bfloat16)
+    dw = torch.zeros(k * k * cin * cout, device="cuda")
+    bg = torch.zeros(cout, device="cuda")
+    nhwc.conv_wgrad(nhwc.View(xw), nhwc.View(dy), k, 1, 1, dw, nhwc.Workspace(), bias_grad=bg, window=k)
+    wg = torch.zeros(cout, cin, k, k, dtype=torch.float64, device="cuda", requires_grad=True)
+    F.conv2d(xr, wg, padding=p).backward(dy.double().permute(0, 3, 1, 2))
+    ref_dw = wg.grad.permute(2, 3, 1, 0).reshape(-1)
+    assert _rel(dw, ref_dw) < 2e-3
+    assert _rel(bg, dy.double().sum((0, 1, 2))) < 1e-4

@@ -32,7 +32,16 @@ b8 = torch.zeros(2048, device="cuda")
 wbf = w.to(torch.bfloat16).contiguous()   # master HWIO bf16
 w8bf = w8.to(torch.bfloat16).contiguous()
 d8 = torch.randn(2, 144, 96, 512, device="cuda").to(torch.bfloat16)
+xwin = torch.zeros(N, H, W + 6, 16, dtype=torch.bfloat16, device="cuda")
+xwin[:, :, 3:3 + W] = xs
+ws7 = torch.randn(49, 16, 64, device="cuda") * 0.05
+wp7 = torch.empty(64, 7, 128, dtype=torch.bfloat16, device="cuda")
+nhwc.pack_weights(ws7, 7, 1, 112, 64, fprop=wp7)
+b64 = torch.zeros(64, device="cuda")
 ops = {
+    "stem_fprop_win": lambda: nhwc.conv_fprop(nhwc.View(xwin), wp7, 64, 7, 1, 1, nhwc.View(ys), bias=b64, relu=True,
+                                              window=7),
+    "stem_wgrad_win": lambda: nhwc.conv_wgrad(nhwc.View(xwin), nhwc.View(ys), 7, 1, 1, dws, ws, window=7),
     "fprop_mn": lambda: nhwc.conv_fprop(nhwc.View(x), None, C, 3, 3, 1, nhwc.View(y), bias=b, relu=True,
                                         w_master=wbf, w_mode=1),
     "dgrad_m": lambda: nhwc.conv_dgrad(nhwc.View(dy), None, C, 3, 3, 1, nhwc.View(y), mask=nhwc.View(x),
@@ -58,7 +67,8 @@ for k in sel:
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 3
-    fl = {"stem_wgrad": 2 * 49 * 16 * 64 * N * H * W, "c1x1_fprop": 2 * 512 * 2048 * 2 * 144 * 96,
+    fl = {"stem_wgrad": 2 * 49 * 16 * 64 * N * H * W, "stem_wgrad_win": 2 * 49 * 16 * 64 * N * H * W,
+          "stem_fprop_win": 2 * 49 * 16 * 64 * N * H * W, "c1x1_fprop": 2 * 512 * 2048 * 2 * 144 * 96,
                                                   "c1x1_dgrad": 2 * 512 * 2048 * 2 * 144 * 96}.get(
         k, 2 * 9 * C * C * N * H * W)
     print(f"{k:10s} {ms:.3f} ms  {fl / ms / 1e9:.1f} TF/s", flush=True)
