@@ -183,6 +183,14 @@ B2DL_API int b2dl_add(b2dl_act x, b2dl_act y, int accumulate, b2dl_act mask, voi
  * memory-bound channel expansion, so it runs on CUDA cores rather than a K=16 GEMM. */
 B2DL_API int b2dl_dgrad_1x1_small(b2dl_act dy, const float* w_hwio, b2dl_act dx, int accumulate, b2dl_act mask,
                                   void* stream);
+/* Whole backward of such a head conv in one pass over its input x: per-block partial sums of
+ * dW[ci][k] = sum_p x[p][ci] dy[p][k] (dw_partials [parts][cin*k]) and db[k] = sum_p dy[p][k]
+ * (db_partials [parts][k]), parts = b2dl_head_backward_parts(), for a later deterministic
+ * b2dl_reduce_segments; plus, when dx.ptr != NULL, the input gradient of
+ * b2dl_dgrad_1x1_small with x itself as the relu mask (mask_dx != 0). */
+B2DL_API int b2dl_head_backward_parts(void);
+B2DL_API int b2dl_head_backward(b2dl_act dy, const float* w_hwio, b2dl_act x, b2dl_act dx, int accumulate,
+                                int mask_dx, float* dw_partials, float* db_partials, void* stream);
 /* in-place g *= (act > 0): relu VJP (ops.py:176-177). */
 B2DL_API int b2dl_relu_mask(b2dl_act g, b2dl_act act, void* stream);
 /* bias gradient: out[c] (+)= sum over pixels of g (ops.py:172-175). */

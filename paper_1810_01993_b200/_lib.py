@@ -80,6 +80,8 @@ _SIGS = {
     "b2dl_reduce_segments": (_c_int, [_vp, _c_int, ctypes.c_int64, _vp, _vp]),
     "b2dl_pack_weights": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp]),
     "b2dl_nchw_to_nhwc": (_c_int, [_vp, Act, _c_int, _vp]),
+    "b2dl_head_backward_parts": (_c_int, []),
+    "b2dl_head_backward": (_c_int, [Act, _vp, Act, Act, _c_int, _c_int, _vp, _vp, _vp]),
     "b2dl_nchw_to_nhwc_halo": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _c_int, _vp]),
     "b2dl_nhwc_to_nchw": (_c_int, [Act, _c_int, _vp, _vp]),
     "b2dl_avgpool_fwd": (_c_int, [Act, Act, _c_int, _vp]),

@@ -28,6 +28,46 @@
 namespace b2 {
 
 constexpr int BM = 128;
+
+// Programmatic dependent launch for the persistent tensor-core kernels (B2DL_PDL=0 disables).
+static bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("B2DL_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+template <typename... KArgs, typename... Args>
+static int launch_tc(void (*kern)(KArgs...), int grid, int block, int smem, cudaStream_t st, int cluster,
+                     Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (cluster > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = cluster;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  if (e != cudaSuccess) {
+    fprintf(stderr, "b2dl: CUDA error %s\n", cudaGetErrorString(e));
+    return B2DL_E_CUDA;
+  }
+  return B2DL_OK;
+}
 constexpr int SMEM_BUDGET = 200 * 1024;
 
 __host__ __device__ constexpr uint32_t tmem_cols_for(int n) {
@@ -607,6 +647,9 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // prologue done: let the next kernel's CTAs start theirs; wait for our inputs
+  griddep_launch_dependents();
+  griddep_wait();
   const int per_img = p.tiles_x * p.tiles_y;
   const int unit0 = blockIdx.x / CG, units = gridDim.x / CG;
 
@@ -772,6 +815,9 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // prologue done: let the next kernel's CTAs start theirs; wait for our inputs
+  griddep_launch_dependents();
+  griddep_wait();
   const int per_img = p.tiles_x * p.tiles_y;
 
   if (warp == 0) {
@@ -920,6 +966,9 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // prologue done: let the next kernel's CTAs start theirs; wait for our inputs
+  griddep_launch_dependents();
+  griddep_wait();
   const int per_img = p.pbx * p.pby;
 
   if (warp == 0) {
@@ -1139,6 +1188,9 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // prologue done: let the next kernel's CTAs start theirs; wait for our inputs
+  griddep_launch_dependents();
+  griddep_wait();
   const int per_img = p.pbx * p.pby;
 
   if (warp == 0) {
@@ -1314,30 +1366,9 @@ static int launch_fprop(const FpropMaps& t, FpropParams p, cudaStream_t st) {
   }
   p.b_region = (p.stages * C::B_BYTES + 1023) / 1024 * 1024;
   const int smem = p.stages * C::A_BYTES + p.b_region + p.epi_bytes + SMEM_FIXED;
-  if constexpr (CG == 1) {
-    const int grid = std::min(p.num_tiles, num_sms());
-    kern<<<grid, FPROP_THREADS, smem, st>>>(t.a, t.b, t.y, t.r, t.m, p);
-  } else {
-    const int grid = CG * std::min(p.num_tiles, num_sms() / CG);
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(FPROP_THREADS);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CG;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, t.a, t.b, t.y, t.r, t.m, p);
-    if (e != cudaSuccess) {
-      fprintf(stderr, "b2dl: CUDA error %s\n", cudaGetErrorString(e));
-      return B2DL_E_CUDA;
-    }
-  }
-  return check_launch();
+  const int grid = CG * std::min(p.num_tiles, num_sms() / CG);
+  const int rc = launch_tc(kern, grid, FPROP_THREADS, smem, st, CG, t.a, t.b, t.y, t.r, t.m, p);
+  return rc ? rc : check_launch();
 }
 
 template <int BN, int XW>
@@ -1351,8 +1382,8 @@ static int launch_wgrad(const CUtensorMap& tx, const CUtensorMap& tdy, const Wgr
     attr_set = true;
   }
   const int grid = std::min(p.num_tiles, num_sms());
-  kern<<<grid, 192, C::SMEM, st>>>(tx, tdy, p);
-  return check_launch();
+  const int rc = launch_tc(kern, grid, 192, C::SMEM, st, 1, tx, tdy, p);
+  return rc ? rc : check_launch();
 }
 
 // CTA-pair fprop/dgrad for 256-wide tiles; B2DL_FPROP_PAIRS=0 selects single-CTA tiles
@@ -1449,8 +1480,8 @@ static int launch_halo_fprop(const b2dl_conv_args* a, const b2dl_act& xv, cudaSt
     attr_set = true;
   }
   const int grid = std::min(p.num_tiles, num_sms());
-  conv_halo_fprop_kernel<<<grid, FPROP_THREADS, smem, st>>>(t.a, t.b, t.y, t.r, t.m, p);
-  return check_launch();
+  const int rc = launch_tc(conv_halo_fprop_kernel, grid, FPROP_THREADS, smem, st, 1, t.a, t.b, t.y, t.r, t.m, p);
+  return rc ? rc : check_launch();
 }
 
 static bool halo_fprop_ok(const b2dl_conv_args* a, const b2dl_act& xv) {
@@ -1749,9 +1780,9 @@ extern "C" int b2dl_conv_wgrad(const b2dl_wgrad_args* a, void* stream) {
         return B2DL_E_CUDA;
       attr_set = true;
     }
-    conv_halo_wgrad_kernel<<<pl.p.splits, 192, stages * stage_bytes + SMEM_FIXED, st>>>(
-        tx, tdy, pl.p, taps, stages);
-    rc = check_launch();
+    rc = launch_tc(conv_halo_wgrad_kernel, pl.p.splits, 192, stages * stage_bytes + SMEM_FIXED, st, 1, tx, tdy,
+                   pl.p, taps, stages);
+    if (!rc) rc = check_launch();
     if (rc) return rc;
   } else {
     // x: 5-D map (64-ch inner, W, H, N, channel block) when chunks of one tap can be grouped

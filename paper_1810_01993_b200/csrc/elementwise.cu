@@ -13,6 +13,8 @@
 namespace b2 {
 
 __device__ __forceinline__ float ld_bf(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+__device__ __forceinline__ float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }
 
 static int grid1d(long long total, int per_thread = 1) {
   long long blocks = (total / per_thread + 255) / 256;
@@ -206,21 +208,21 @@ __global__ void k_avgpool_bwd(const __nv_bfloat16* __restrict__ dy, int dys, __n
 template <int G>
 __global__ void k_upsample_fwd(const __nv_bfloat16* __restrict__ x, int xs, __nv_bfloat16* __restrict__ y, int ys,
                                int n, int h, int w, int c, int f) {
-  const int H = h * f, W = w * f;
+  // one thread per (input pixel, channel group): read once, write the f x f replicas
+  const int W = w * f;
   const int cg = c / G;
-  const long long total = static_cast<long long>(n) * H * W * cg;
+  const long long total = static_cast<long long>(n) * h * w * cg;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const int ch = static_cast<int>(i % cg) * G;
-    const long long p = i / cg;
-    const int xx = static_cast<int>(p % W);
-    const long long r = p / W;
-    const int yy = static_cast<int>(r % H);
-    const long long img = r / H;
-    const long long sp = (img * h + yy / f) * w + xx / f;
+    const long long sp = i / cg;  // (img * h + yy) * w + xx
+    const int xx = static_cast<int>(sp % w);
+    const long long r = sp / w;   // img * h + yy
     float v[G];
     ldv<G>(x + sp * xs + ch, v);
-    stv<G>(y + p * ys + ch, v);
+    const long long o = r * f * W + static_cast<long long>(xx) * f;  // output pixel (img, yy*f, xx*f)
+    for (int a = 0; a < f; ++a)
+      for (int b = 0; b < f; ++b) stv<G>(y + (o + static_cast<long long>(a) * W + b) * ys + ch, v);
   }
 }
 // dx[q] (+)= mask(x)[q] * sum over the f x f block of dy
@@ -390,6 +392,136 @@ __global__ void k_dgrad_1x1_small(const __nv_bfloat16* __restrict__ dy, int dys,
   }
 }
 
+// Backward of a 1x1 conv with few output channels (the 3-class head), one pass over its input:
+//   dW[ci][k] partial  = sum_p x[p][ci] * dy[p][k]      (per-block partials, fixed order)
+//   db[k]     partial  = sum_p dy[p][k]
+//   dx[p][ci] (+)= [x > 0] * sum_k w[ci][k] * dy[p][k]  (optional; x doubles as the relu mask)
+// A warp-sized group of threads covers one pixel's channels (8 per thread, 16-byte accesses).
+constexpr int HEAD_THREADS = 256;
+template <int KC, bool DYV>
+__global__ void __launch_bounds__(HEAD_THREADS, 2) k_head_backward(
+    const __nv_bfloat16* __restrict__ dy, int dys, const float* __restrict__ w, int cin,
+    const __nv_bfloat16* __restrict__ x, int xs, __nv_bfloat16* __restrict__ dx, int dxs, int acc, int mask_dx,
+    int npix, float* __restrict__ dwp, float* __restrict__ dbp) {
+  constexpr int kc = KC;
+  extern __shared__ float hsm[];  // w^T [kc][cin], then reduction scratch [ppb][cin * kc + kc]
+  float* wsm = hsm;
+  float* red = hsm + kc * cin;
+  for (int i = threadIdx.x; i < cin * kc; i += blockDim.x) {
+    const int ci = i / kc, k = i - ci * kc;
+    wsm[k * cin + ci] = w[i];
+  }
+  __syncthreads();
+  const int cg = cin / 8;
+  const int g = threadIdx.x % cg, pl = threadIdx.x / cg, ppb = blockDim.x / cg;
+  const int ch = g * 8;
+  float aw[8][KC];
+  float ab[KC];
+#pragma unroll
+  for (int k = 0; k < KC; ++k) ab[k] = 0.f;
+#pragma unroll
+  for (int e = 0; e < 8; ++e)
+#pragma unroll
+    for (int k = 0; k < KC; ++k) aw[e][k] = 0.f;
+  // U pixels per iteration: all their loads are issued before any use (memory-level parallelism)
+  constexpr int U = 8;
+  const int stride = gridDim.x * ppb;
+  for (int p0 = blockIdx.x * ppb + pl; p0 < npix; p0 += U * stride) {
+    uint4 xr[U];
+    float d[U][KC];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int p = p0 + u * stride;
+      xr[u] = make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int k = 0; k < KC; ++k) d[u][k] = 0.f;
+      if (p < npix) {
+        const long long pp = p;
+        xr[u] = __ldg(reinterpret_cast<const uint4*>(x + pp * xs + ch));
+        if constexpr (DYV) {
+          const uint4 r = __ldg(reinterpret_cast<const uint4*>(dy + pp * dys));
+          const uint32_t q[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+          for (int k = 0; k < KC; ++k) d[u][k] = (k & 1) ? bf16_hi(q[k >> 1]) : bf16_lo(q[k >> 1]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < KC; ++k) d[u][k] = ld_bf(dy + pp * dys + k);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int p = p0 + u * stride;
+      if (p >= npix) break;
+      const uint32_t q[4] = {xr[u].x, xr[u].y, xr[u].z, xr[u].w};
+      float xv[8];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        xv[2 * e] = bf16_lo(q[e]);
+        xv[2 * e + 1] = bf16_hi(q[e]);
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+#pragma unroll
+        for (int k = 0; k < KC; ++k) aw[e][k] += xv[e] * d[u][k];
+      if (g == 0) {
+#pragma unroll
+        for (int k = 0; k < KC; ++k) ab[k] += d[u][k];
+      }
+      if (dx) {
+        float v[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] = 0.f;
+#pragma unroll
+        for (int k = 0; k < KC; ++k) {
+          const float4 a = *reinterpret_cast<const float4*>(wsm + k * cin + ch);
+          const float4 b = *reinterpret_cast<const float4*>(wsm + k * cin + ch + 4);
+          v[0] += d[u][k] * a.x;
+          v[1] += d[u][k] * a.y;
+          v[2] += d[u][k] * a.z;
+          v[3] += d[u][k] * a.w;
+          v[4] += d[u][k] * b.x;
+          v[5] += d[u][k] * b.y;
+          v[6] += d[u][k] * b.z;
+          v[7] += d[u][k] * b.w;
+        }
+        if (mask_dx) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            if (!(xv[e] > 0.f)) v[e] = 0.f;
+        }
+        __nv_bfloat16* o = dx + static_cast<long long>(p) * dxs + ch;
+        if (acc) {
+          float old[8];
+          ldv_rw<8>(o, old);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[e] += old[e];
+        }
+        stv<8>(o, v);
+      }
+    }
+  }
+  // block partials: the ppb threads of each channel group meet in shared memory (fixed order)
+  const int row = cin * kc + kc;
+#pragma unroll
+  for (int e = 0; e < 8; ++e)
+#pragma unroll
+    for (int k = 0; k < KC; ++k) red[pl * row + (ch + e) * kc + k] = aw[e][k];
+  if (g == 0) {
+#pragma unroll
+    for (int k = 0; k < KC; ++k) red[pl * row + cin * kc + k] = ab[k];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < row; i += blockDim.x) {
+    float sum = 0.f;
+    for (int q = 0; q < ppb; ++q) sum += red[q * row + i];
+    if (i < cin * kc)
+      dwp[static_cast<long long>(blockIdx.x) * cin * kc + i] = sum;
+    else
+      dbp[static_cast<long long>(blockIdx.x) * kc + (i - cin * kc)] = sum;
+  }
+}
+
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 static bool vec_ok(const b2dl_act& a) { return a.c % 8 == 0 && a.c_stride % 8 == 0 && aligned16(a.ptr); }
 static bool vec_ok(const b2dl_act& a, const b2dl_act& b) { return vec_ok(a) && vec_ok(b); }
@@ -480,7 +612,7 @@ extern "C" int b2dl_avgpool_bwd(b2dl_act dy, b2dl_act dx, int k, int accumulate,
 
 extern "C" int b2dl_upsample_fwd(b2dl_act x, b2dl_act y, int f, void* stream) {
   if (f < 1 || y.h != x.h * f || y.w != x.w * f || y.c != x.c) return B2DL_E_VALUE;
-  long long total = static_cast<long long>(y.n) * y.h * y.w * y.c;
+  long long total = static_cast<long long>(x.n) * x.h * x.w * x.c;
   B2_LAUNCH_G(k_upsample_fwd, vec_ok(x, y), total, CBF(x.ptr), x.c_stride, BF(y.ptr), y.c_stride, x.n, x.h, x.w, x.c,
               f);
   return check_launch();
@@ -557,6 +689,47 @@ extern "C" int b2dl_pack_weights(const float* w_hwio, int kh, int kw, int cin, i
     return check_launch();
   }
   return B2DL_OK;
+}
+
+extern "C" int b2dl_head_backward_parts(void) { return 4 * num_sms(); }
+
+extern "C" int b2dl_head_backward(b2dl_act dy, const float* w_hwio, b2dl_act x, b2dl_act dx, int accumulate,
+                                  int mask_dx, float* dw_partials, float* db_partials, void* stream) {
+  if (!dy.ptr || !w_hwio || !x.ptr || !dw_partials || !db_partials || dy.c < 1 || dy.c > 8 || dy.n != x.n ||
+      dy.h != x.h || dy.w != x.w)
+    return B2DL_E_VALUE;
+  if (dx.ptr && (dx.n != x.n || dx.h != x.h || dx.w != x.w || dx.c != x.c)) return B2DL_E_VALUE;
+  const int cin = x.c;
+  if (cin % 8 || HEAD_THREADS % (cin / 8) || !vec_ok(x) || (dx.ptr && !vec_ok(dx))) return B2DL_E_ALIGN;
+  const long long npix = static_cast<long long>(x.n) * x.h * x.w;
+  if (npix > 0x7fffffffLL) return B2DL_E_VALUE;
+  const int ppb = HEAD_THREADS / (cin / 8);
+  const size_t smem = (static_cast<size_t>(dy.c) * cin + static_cast<size_t>(ppb) * (cin * dy.c + dy.c)) * sizeof(float);
+  if (smem > 48 * 1024) return B2DL_E_VALUE;
+  const bool dyv = (dy.c_stride % 8) == 0 && aligned16(dy.ptr);
+#define B2_HEAD(K)                                                                                             \
+  case K:                                                                                                      \
+    if (dyv)                                                                                                   \
+      k_head_backward<K, true><<<b2dl_head_backward_parts(), HEAD_THREADS, smem, as_stream(stream)>>>(         \
+          CBF(dy.ptr), dy.c_stride, w_hwio, cin, CBF(x.ptr), x.c_stride, BF(dx.ptr), dx.c_stride, accumulate,  \
+          mask_dx, static_cast<int>(npix), dw_partials, db_partials);                                          \
+    else                                                                                                       \
+      k_head_backward<K, false><<<b2dl_head_backward_parts(), HEAD_THREADS, smem, as_stream(stream)>>>(        \
+          CBF(dy.ptr), dy.c_stride, w_hwio, cin, CBF(x.ptr), x.c_stride, BF(dx.ptr), dx.c_stride, accumulate,  \
+          mask_dx, static_cast<int>(npix), dw_partials, db_partials);                                          \
+    break;
+  switch (dy.c) {
+    B2_HEAD(1)
+    B2_HEAD(2)
+    B2_HEAD(3)
+    B2_HEAD(4)
+    B2_HEAD(5)
+    B2_HEAD(6)
+    B2_HEAD(7)
+    B2_HEAD(8)
+  }
+#undef B2_HEAD
+  return check_launch();
 }
 
 extern "C" int b2dl_dgrad_1x1_small(b2dl_act dy, const float* w_hwio, b2dl_act dx, int accumulate, b2dl_act mask,

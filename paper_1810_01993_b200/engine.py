@@ -398,7 +398,16 @@ class Engine:
         self.partials = {}
         self.segs = {}
         total, offs = 0, {}
+        # few-output-channel 1x1 convs (the 3-class head): wgrad + dgrad in one pass over the input
+        self.heads = {o.w for o in self.convs
+                      if o.k == 1 and o.cout < 8 and o.cin % 8 == 0 and 256 % (o.cin // 8) == 0}
+        hparts = nhwc.head_backward_parts()
         for o in self.convs:
+            if o.w in self.heads:
+                nw = hparts * o.cin * o.cout * 4
+                offs[o.w] = (total, nw + hparts * o.cout * 4, hparts, hparts, nw)
+                total += (offs[o.w][1] + 255) // 256 * 256
+                continue
             if o is self.win:
                 nbytes, wp, bp, bo = nhwc.wgrad_partials(
                     View(torch.empty(self.xwin.shape, dtype=bf, device="meta")), self._probe_view(o.out),
@@ -409,10 +418,13 @@ class Engine:
             offs[o.w] = (total, nbytes, wp, bp, bo)
             total += (nbytes + 255) // 256 * 256
         self.partials_buf = torch.empty(max(total, 256), dtype=torch.uint8, device=self.device)
+        self.head_parts = {}
         for o in self.convs:
             off, nbytes, wp, bp, bo = offs[o.w]
             buf = self.partials_buf[off:off + nbytes]
             self.partials[o.w] = buf
+            if o.w in self.heads:
+                self.head_parts[o.w] = (buf[:bo].view(torch.float32), buf[bo:].view(torch.float32))
             base = buf.data_ptr()
             n_w = o.k * o.k * o.cin * o.cout
             self.segs[o.w] = (base, self.slot[o.w][0], n_w, wp, 0)
@@ -629,7 +641,12 @@ class Engine:
                 ev = self._tic()
                 # wgrad GEMM with the bias column sums folded in; split-K partials stay in the
                 # conv's partial buffer until its bucket is reduced in one batched launch
-                if op is self.win:
+                if op.w in self.heads:
+                    dwp, dbp = self.head_parts[op.w]
+                    nhwc.head_backward(gy, self.wslice(op.w), self.v(op.ins[0]),
+                                       self.gv(op.ins[0]) if st["dx"] is not None else None, dwp, dbp,
+                                       accumulate=bool(st["dx"]), mask_dx=bool(st["mask_dx"]))
+                elif op is self.win:
                     nhwc.conv_wgrad_deferred(View(self.xwin), gy, op.k, 1, 1, self.partials[op.w], window=op.k)
                 else:
                     nhwc.conv_wgrad_deferred(self.v(op.ins[0]), gy, op.k, op.k, op.dil, self.partials[op.w])
@@ -642,7 +659,9 @@ class Engine:
                         self._reduce_bucket(i)
                         if on_bucket_ready is not None:
                             on_bucket_ready(i)
-                if st["dx"] is not None and op.k == 1 and op.cout < 8:
+                if op.w in self.heads:
+                    pass   # input gradient already produced by head_backward
+                elif st["dx"] is not None and op.k == 1 and op.cout < 8:
                     # e.g. the 3-class head: a memory-bound channel expansion, not a GEMM
                     nhwc.dgrad_1x1_small(gy, self.wslice(op.w), self.gv(op.ins[0]), accumulate=st["dx"],
                                          mask=self.v(op.ins[0]) if st["mask_dx"] else None)

@@ -164,6 +164,18 @@ def nchw_to_nhwc(x: torch.Tensor, y: View, dst_f32=False):
           "nchw_to_nhwc")
 
 
+def head_backward_parts() -> int:
+    return LIB.b2dl_head_backward_parts()
+
+
+def head_backward(dy: View, w_hwio: torch.Tensor, x: View, dx: View | None, dw_partials: torch.Tensor,
+                  db_partials: torch.Tensor, accumulate=False, mask_dx=False):
+    """Few-output-channel 1x1 conv backward in one pass: dW / db block partials (+ optional dx)."""
+    check(LIB.b2dl_head_backward(dy.act(), ctypes.c_void_p(w_hwio.data_ptr()), x.act(), _act(dx), int(accumulate),
+                                 int(mask_dx), ctypes.c_void_p(dw_partials.data_ptr()),
+                                 ctypes.c_void_p(db_partials.data_ptr()), _stream()), "head_backward")
+
+
 def nchw_to_nhwc_halo(x: torch.Tensor, y: torch.Tensor, left: int):
     """x fp32 [n][c][h][w] -> y bf16 [n][h][wp][c], column xx at left + xx, zero halo columns."""
     n, c, h, w = x.shape

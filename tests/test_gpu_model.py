@@ -193,3 +193,37 @@ def test_memory_bound_kernels_vs_torch():
     nhwc.bias_grad(nhwc.View(x), out, ws)
     assert rel(out.cpu(), x.float().sum((0, 1, 2)).cpu()) < 1e-3
     del g
+
+
+@pytest.mark.parametrize("cin,k,mask,acc,with_dx", [(256, 3, True, False, True), (64, 5, False, True, True),
+                                                     (128, 3, True, False, False)])
+def test_head_backward_vs_torch(cin, k, mask, acc, with_dx):
+    """One-pass backward of the 3-class head (1x1 conv): dW / db partials reduced in fixed order,
+    dx with the input's relu mask, optional accumulate."""
+    from paper_1810_01993_b200 import nhwc
+    torch.manual_seed(3)
+    n, h, w = 2, 24, 40
+    x = torch.randn(n, h, w, cin, device="cuda").to(torch.bfloat16)
+    dyb = torch.zeros(n, h, w, 8, dtype=torch.bfloat16, device="cuda")   # padded grad buffer
+    dyb[..., :k] = torch.randn(n, h, w, k, device="cuda").to(torch.bfloat16)
+    dy = nhwc.View(dyb, 0, k)
+    wt = torch.randn(cin, k, device="cuda")
+    parts = nhwc.head_backward_parts()
+    dwp = torch.empty(parts * cin * k, device="cuda")
+    dbp = torch.empty(parts * k, device="cuda")
+    dx0 = torch.randn(n, h, w, cin, device="cuda").to(torch.bfloat16)
+    dx = dx0.clone()
+    nhwc.head_backward(dy, wt, nhwc.View(x), nhwc.View(dx) if with_dx else None, dwp, dbp, accumulate=acc,
+                       mask_dx=mask)
+    xd, dyd = x.double().reshape(-1, cin), dyb[..., :k].double().reshape(-1, k)
+    assert rel(dwp.view(parts, cin * k).sum(0).double().cpu(), (xd.t() @ dyd).reshape(-1).cpu()) < 1e-4
+    assert rel(dbp.view(parts, k).sum(0).double().cpu(), dyd.sum(0).cpu()) < 1e-4
+    if with_dx:
+        ref = (dyd @ wt.double().t()).reshape(n, h, w, cin)
+        if mask:
+            ref = torch.where(x.double() > 0, ref, torch.zeros_like(ref))
+        if acc:
+            ref = ref + dx0.double()
+        assert rel(dx.double().cpu(), ref.cpu()) < 1e-2
+    else:
+        assert torch.equal(dx, dx0)

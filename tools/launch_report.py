@@ -43,7 +43,8 @@ def main(path, which=1):
     for st in pl.backward_program:
         o = st["op"]
         if o.kind == "conv":
-            names.append(("wgrad", o))
+            if not (o.k == 1 and o.cout < 8):   # head: wgrad fused into head_backward
+                names.append(("wgrad", o))
             if st["dx"] is not None and not (o.k == 1 and o.cout < 8):
                 names.append(("dgrad", o))
     conv_launches = [(k, t) for k, t in step if k.startswith("b2::conv_")]
