@@ -21,6 +21,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cmath>
 
 #include "internal.h"
 #include "sm100.cuh"
@@ -96,9 +97,7 @@ constexpr int SMEM_FIXED = 1024 + 512;  // alignment slack + barriers / TMEM slo
 // TMA epilogue: one 32-pixel x 32-channel bf16 box per chunk, 64-byte rows, 64B swizzle.
 // Per warp: two operand slots of up to two operands each (residual / mask / accumulated y,
 // loaded one chunk ahead), and two output buffers (stores drain while the next chunk runs).
-constexpr int EPI_BOX = 32 * 64;
 constexpr int EPI_LEGACY_BYTES = 8 * 32 * 80;
-__host__ __device__ constexpr int epi_warp_bytes(int nops) { return (2 * nops + 2) * EPI_BOX; }
 
 struct FpropParams {
   int n, h, w;
@@ -336,6 +335,194 @@ __device__ __forceinline__ void box_row_put(uint8_t* box, const float* v) {
   }
 }
 
+// TMA epilogue, EW warps = EW / 4 sub-groups of 4 warps (one per TMEM lane quarter).  A
+// sub-group owns every (EW / 4)-th 32-column chunk of a tile; one chunk of the whole 128-pixel
+// tile is one 8 KB TMA box (32 channels x the tile's pixel box, 64-byte swizzled rows), so a
+// tile moves in few, large TMA operations: operands arrive one chunk ahead, the four warps pack
+// their 32 rows into a shared output box, meet at a named barrier, and one thread stores it.
+constexpr int EPI_CHUNK = 128 * 64;  // 128 pixels x 32 bf16 channels
+__host__ __device__ constexpr int epi_sub_bytes(int nops) { return (2 * nops + 2) * EPI_CHUNK; }
+
+template <int BN, int CG, int EW>
+__device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const CUtensorMap* tmY, const CUtensorMap* tmR,
+                                                   const CUtensorMap* tmM, uint32_t tmem_base, uint64_t* tfull,
+                                                   uint64_t* tempty, uint64_t* inbar, uint8_t* epi, int warp, int rank,
+                                                   int unit0, int units) {
+  constexpr int SUBS = EW / 4;                 // sub-groups
+  constexpr int NCH = BN / 32;                 // 32-column chunks per tile
+  constexpr int NJ = (NCH + SUBS - 1) / SUBS;  // chunks per sub-group
+  const int lane = lane_id();
+  const int per_img = p.tiles_x * p.tiles_y;
+  const int ew = warp - 2;
+  const int q = warp & 3;
+  const int sub = ew >> 2;
+  const bool leader = (q == 0) && (lane == 0);  // warp with lane quarter 0 of the sub-group
+  const int nops = p.epi_nops;
+  uint8_t* sbuf = epi + sub * epi_sub_bytes(nops);
+  uint8_t* obuf = sbuf + 2 * nops * EPI_CHUNK;
+  uint64_t* ib = inbar + 2 * sub;
+  auto locate = [&](int tile, int& img, int& x, int& y, int& nt) {
+    const int pmt = tile / p.num_n_tiles;
+    nt = tile - pmt * p.num_n_tiles;
+    const int mt = pmt * CG + rank;
+    img = mt / per_img;
+    const int r = mt - img * per_img;
+    const int ty = r / p.tiles_x, tx = r - ty * p.tiles_x;
+    y = ty * p.bh;
+    x = tx * p.bw;
+  };
+  auto chunks = [&](int nt) {  // valid chunks of this sub-group in a tile of N-tile nt
+    int n = 0;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+      if (SUBS * j + sub < NCH && nt * BN + (SUBS * j + sub) * 32 < p.cout) n = j + 1;
+    return n;
+  };
+  auto issue = [&](int tile, int j, int slot) {
+    if (leader) {
+      int img, x, y, nt;
+      locate(tile, img, x, y, nt);
+      const int c0 = nt * BN + (SUBS * j + sub) * 32;
+      uint8_t* dst = sbuf + slot * nops * EPI_CHUNK;
+      fence_proxy_async();
+      mbar_arrive_expect_tx(&ib[slot], nops * EPI_CHUNK);
+      int o = 0;
+      if (p.res) tma_load_4d(dst + (o++) * EPI_CHUNK, tmR, &ib[slot], c0, x, y, img);
+      if (p.mask) tma_load_4d(dst + (o++) * EPI_CHUNK, tmM, &ib[slot], c0, x, y, img);
+      if (p.accumulate) tma_load_4d(dst + o * EPI_CHUNK, tmY, &ib[slot], c0, x, y, img);
+    }
+  };
+  auto release = [&](int as) {  // accumulator stage fully read: hand it back to the MMA warp
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) {
+      if constexpr (CG == 2)
+        mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[as]), 0));
+      else
+        mbar_arrive(&tempty[as]);
+    }
+  };
+  auto sub_sync = [&]() { asm volatile("bar.sync %0, 128;" ::"r"(1 + sub) : "memory"); };
+  const int row = q * 32 + lane;          // tile row (pixel) of this thread
+  const int swz = (lane >> 1) & 3;        // 64B-swizzle phase of the row
+  uint32_t ph0 = 0, ph1 = 0;
+  int slot = 0, ob = 0, it = 0;
+  if (nops && unit0 < p.num_tiles) {
+    int img, x, y, nt;
+    locate(unit0, img, x, y, nt);
+    if (chunks(nt) > 0) issue(unit0, 0, 0);
+  }
+  for (int tile = unit0; tile < p.num_tiles; tile += units, ++it) {
+    const int as = it & 1;
+    const uint32_t ap = (it >> 1) & 1;
+    int img, x, y, nt;
+    locate(tile, img, x, y, nt);
+    const int nv = chunks(nt);
+    mbar_wait(&tfull[as], ap);
+    tc_fence_after();
+    const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + as * BN;
+#pragma unroll 1
+    for (int j = 0; j < NJ; ++j) {
+      if (j >= nv) break;  // uniform over the sub-group
+      if (nops) {          // operands of the next chunk (possibly of the next tile)
+        if (j + 1 < nv) {
+          issue(tile, j + 1, slot ^ 1);
+        } else if (tile + units < p.num_tiles) {
+          int i2, x2, y2, nt2;
+          locate(tile + units, i2, x2, y2, nt2);
+          if (chunks(nt2) > 0) issue(tile + units, 0, slot ^ 1);
+        }
+      }
+      const int c0 = nt * BN + (SUBS * j + sub) * 32;
+      uint32_t cur[32];
+      tmem_ld_issue_x32(tbase + (SUBS * j + sub) * 32, cur);
+      tmem_ld_wait();
+      if (j == nv - 1) release(as);
+      const uint8_t* in = sbuf + slot * nops * EPI_CHUNK;
+      if (nops) {
+        mbar_wait(&ib[slot], slot ? ph1 : ph0);
+        if (slot)
+          ph1 ^= 1;
+        else
+          ph0 ^= 1;
+      }
+      uint8_t* ochunk = obuf + ob * EPI_CHUNK;
+      const float4* bias4 = p.bias ? reinterpret_cast<const float4*>(p.bias + c0) : nullptr;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {  // 8-column pieces
+        const int poff = row * 64 + ((k ^ swz) << 4);
+        float v[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(cur[8 * k + e]);
+        if (bias4 && c0 + 8 * k < p.cout) {  // TMA epilogue: bias 16-byte aligned, cout % 8 == 0
+          const float4 b0 = __ldg(bias4 + 2 * k);
+          const float4 b1 = __ldg(bias4 + 2 * k + 1);
+          v[0] += b0.x;
+          v[1] += b0.y;
+          v[2] += b0.z;
+          v[3] += b0.w;
+          v[4] += b1.x;
+          v[5] += b1.y;
+          v[6] += b1.z;
+          v[7] += b1.w;
+        }
+        int o = 0;
+        if (p.res) {
+          const uint4 u = *reinterpret_cast<const uint4*>(in + (o++) * EPI_CHUNK + poff);
+          const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            v[2 * e] += bf16lo(w4[e]);
+            v[2 * e + 1] += bf16hi(w4[e]);
+          }
+        }
+        if (p.relu) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[e] = fmaxf(v[e], 0.f);
+        }
+        if (p.mask) {
+          const uint4 u = *reinterpret_cast<const uint4*>(in + (o++) * EPI_CHUNK + poff);
+          const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            if (!(bf16lo(w4[e]) > 0.f)) v[2 * e] = 0.f;
+            if (!(bf16hi(w4[e]) > 0.f)) v[2 * e + 1] = 0.f;
+          }
+        }
+        if (p.accumulate) {
+          const uint4 u = *reinterpret_cast<const uint4*>(in + o * EPI_CHUNK + poff);
+          const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            v[2 * e] += bf16lo(w4[e]);
+            v[2 * e + 1] += bf16hi(w4[e]);
+          }
+        }
+        uint4 pk;
+        pk.x = pack_bf16x2(v[0], v[1]);
+        pk.y = pack_bf16x2(v[2], v[3]);
+        pk.z = pack_bf16x2(v[4], v[5]);
+        pk.w = pack_bf16x2(v[6], v[7]);
+        *reinterpret_cast<uint4*>(ochunk + poff) = pk;
+      }
+      fence_proxy_async();
+      // the other output buffer (next chunk's) must be read out by its store before anyone
+      // packs into it: its store was the only one outstanding before this chunk's
+      if (leader) bulk_wait_read<0>();
+      sub_sync();
+      if (leader) {
+        tma_store_4d(tmY, ochunk, c0, x, y, img);
+        bulk_commit();
+      }
+      ob ^= 1;
+      slot ^= 1;
+    }
+    if (nv == 0) release(as);
+  }
+  if (leader) bulk_wait<0>();
+  __syncwarp();
+}
+
 // Epilogue role of the fprop kernels (8 warps, two per TMEM lane quarter splitting the tile's
 // column chunks): TMEM -> registers -> bias / residual / relu / mask / accumulate -> global.
 template <int BN, int CG>
@@ -355,168 +542,8 @@ __device__ __forceinline__ void fprop_epilogue_role(const FpropParams& p, const 
     constexpr int NJ = (NCH + 1) / 2;
     if constexpr (CW == 32) {
       if (p.tma_epi) {
-        // TMA epilogue.  The warp's 32 accumulator rows are a (bwx x bhx)-pixel box of the tile;
-        // each 32-channel chunk is one box: operands arrive by TMA one chunk ahead, the result
-        // leaves by TMA store from a swizzled buffer while the next chunk is computed.
-        const int nops = p.epi_nops;
-        uint8_t* wbuf = epi + ew * epi_warp_bytes(nops);
-        uint8_t* obuf = wbuf + 2 * nops * EPI_BOX;
-        uint64_t* ib = inbar + 2 * ew;
-        const int wy = (q * 32) / p.bw, wx = (q * 32) % p.bw;
-        auto locate = [&](int tile, int& img, int& x, int& y, int& nt) {
-          const int pmt = tile / p.num_n_tiles;
-          nt = tile - pmt * p.num_n_tiles;
-          const int mt = pmt * CG + rank;
-          img = mt / per_img;
-          const int r = mt - img * per_img;
-          const int ty = r / p.tiles_x, tx = r - ty * p.tiles_x;
-          y = ty * p.bh + wy;
-          x = tx * p.bw + wx;
-        };
-        auto chunks = [&](int nt) {  // valid chunks of this warp in a tile of N-tile nt
-          int n = 0;
-#pragma unroll
-          for (int j = 0; j < NJ; ++j)
-            if (2 * j + half < NCH && nt * BN + (2 * j + half) * 32 < p.cout) n = j + 1;
-          return n;
-        };
-        auto issue = [&](int tile, int j, int slot) {
-          if (lane == 0) {
-            int img, x, y, nt;
-            locate(tile, img, x, y, nt);
-            const int c0 = nt * BN + (2 * j + half) * 32;
-            uint8_t* dst = wbuf + slot * nops * EPI_BOX;
-            fence_proxy_async();
-            mbar_arrive_expect_tx(&ib[slot], nops * EPI_BOX);
-            int o = 0;
-            if (p.res) tma_load_4d(dst + (o++) * EPI_BOX, tmR, &ib[slot], c0, x, y, img);
-            if (p.mask) tma_load_4d(dst + (o++) * EPI_BOX, tmM, &ib[slot], c0, x, y, img);
-            if (p.accumulate) tma_load_4d(dst + o * EPI_BOX, tmY, &ib[slot], c0, x, y, img);
-          }
-        };
-        uint32_t ph0 = 0, ph1 = 0;
-        int slot = 0, ob = 0, it = 0;
-        if (nops && unit0 < p.num_tiles) {
-          int img, x, y, nt;
-          locate(unit0, img, x, y, nt);
-          if (chunks(nt) > 0) issue(unit0, 0, 0);
-        }
-        for (int tile = unit0; tile < p.num_tiles; tile += units, ++it) {
-          const int as = it & 1;
-          const uint32_t ap = (it >> 1) & 1;
-          int img, x, y, nt;
-          locate(tile, img, x, y, nt);
-          const int nv = chunks(nt);
-          mbar_wait(&tfull[as], ap);
-          tc_fence_after();
-          const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + as * BN;
-#pragma unroll 1
-          for (int j = 0; j < NJ; ++j) {
-            if (j >= nv) break;  // warp-uniform
-            if (nops) {          // operands of the next chunk (possibly of the next tile)
-              if (j + 1 < nv) {
-                issue(tile, j + 1, slot ^ 1);
-              } else if (tile + units < p.num_tiles) {
-                int i2, x2, y2, nt2;
-                locate(tile + units, i2, x2, y2, nt2);
-                if (chunks(nt2) > 0) issue(tile + units, 0, slot ^ 1);
-              }
-            }
-            const int ch = 2 * j + half;
-            const int c0 = nt * BN + ch * 32;
-            float bv[32];  // bias loads issued ahead of the TMEM read
-            if (p.bias) {
-              if (p.bias_vec && c0 + 32 <= p.cout) {
-                const float4* b4 = reinterpret_cast<const float4*>(p.bias + c0);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                  const float4 b = __ldg(b4 + i);
-                  bv[4 * i] = b.x;
-                  bv[4 * i + 1] = b.y;
-                  bv[4 * i + 2] = b.z;
-                  bv[4 * i + 3] = b.w;
-                }
-              } else {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) bv[i] = c0 + i < p.cout ? __ldg(p.bias + c0 + i) : 0.f;
-              }
-            }
-            uint32_t cur[32];
-            tmem_ld_issue_x32(tbase + ch * 32, cur);
-            tmem_ld_wait();
-            float v[32];
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(cur[i]);
-            if (j == nv - 1) {  // accumulator fully read: release it to the MMA warp early
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) {
-                if constexpr (CG == 2)
-                  mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[as]), 0));
-                else
-                  mbar_arrive(&tempty[as]);
-              }
-            }
-            if (p.bias) {
-#pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] += bv[i];
-            }
-            const uint8_t* in = wbuf + slot * nops * EPI_BOX;
-            if (nops) {
-              mbar_wait(&ib[slot], slot ? ph1 : ph0);
-              if (slot)
-                ph1 ^= 1;
-              else
-                ph0 ^= 1;
-            }
-            float t[32];
-            int o = 0;
-            if (p.res) {
-              box_row_get(in + (o++) * EPI_BOX, t);
-#pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] += t[i];
-            }
-            if (p.relu) {
-#pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
-            }
-            if (p.mask) {
-              box_row_get(in + (o++) * EPI_BOX, t);
-#pragma unroll
-              for (int i = 0; i < 32; ++i)
-                if (!(t[i] > 0.f)) v[i] = 0.f;
-            }
-            if (p.accumulate) {
-              box_row_get(in + o * EPI_BOX, t);
-#pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] += t[i];
-            }
-            // output buffer `ob` was last stored two chunks ago
-            if (lane == 0) bulk_wait_read<1>();
-            __syncwarp();
-            box_row_put(obuf + ob * EPI_BOX, v);
-            fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) {
-              tma_store_4d(tmY, obuf + ob * EPI_BOX, c0, x, y, img);
-              bulk_commit();
-            }
-            ob ^= 1;
-            slot ^= 1;
-          }
-          if (nv == 0) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-              if constexpr (CG == 2)
-                mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[as]), 0));
-              else
-                mbar_arrive(&tempty[as]);
-            }
-          }
-        }
-        if (lane == 0) bulk_wait<0>();
-        __syncwarp();
+        fprop_epilogue_tma<BN, CG, 8>(p, tmY, tmR, tmM, tmem_base, tfull, tempty, inbar, epi, warp, rank, unit0,
+                                      units);
         return;
       }
     }
@@ -590,8 +617,9 @@ __device__ __forceinline__ void fprop_epilogue_role(const FpropParams& p, const 
     }
 }
 
-template <int BN, int KBLK, bool BMN, int CG>
-__global__ void __launch_bounds__(FPROP_THREADS, 1)
+// EW epilogue warps: 8, or 16 for the TMA epilogue (twice the warps to hide its latency chain)
+template <int BN, int KBLK, bool BMN, int CG, int EW>
+__global__ void __launch_bounds__(64 + 32 * EW, 1)
     conv_fprop_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmR,
                       const __grid_constant__ CUtensorMap tmM, const FpropParams p) {
@@ -609,7 +637,7 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
   uint64_t* tfull = empty + FPROP_MAX_STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* inbar = tempty + 2;  // two operand-slot barriers per epilogue warp
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(inbar + 16);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(inbar + 2 * EW);
 
   const int warp = threadIdx.x >> 5;
   const int lane = lane_id();
@@ -624,9 +652,9 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 8 * CG);
+      mbar_init(&tempty[s], EW * CG);
     }
-    for (int s = 0; s < 16; ++s) mbar_init(&inbar[s], 1);
+    for (int s = 0; s < 2 * EW; ++s) mbar_init(&inbar[s], 1);
     if (p.tma_epi) {
       tma_prefetch(&tmY);
       if (p.res) tma_prefetch(&tmR);
@@ -747,7 +775,12 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
       }
     }
   } else {
-    fprop_epilogue_role<BN, CG>(p, &tmY, &tmR, &tmM, tmem_base, tfull, tempty, inbar, epi, warp, rank, unit0, units);
+    if constexpr (EW == 16)
+      fprop_epilogue_tma<BN, CG, 16>(p, &tmY, &tmR, &tmM, tmem_base, tfull, tempty, inbar, epi, warp, rank, unit0,
+                                     units);
+    else
+      fprop_epilogue_role<BN, CG>(p, &tmY, &tmR, &tmM, tmem_base, tfull, tempty, inbar, epi, warp, rank, unit0,
+                                  units);
   }
   tc_fence_before();
   if constexpr (CG == 2)
@@ -1342,10 +1375,10 @@ struct FpropMaps {
   CUtensorMap a, b, y, r, m;
 };
 
-template <int BN, int KBLK, bool BMN, int CG>
+template <int BN, int KBLK, bool BMN, int CG, int EW = 8>
 static int launch_fprop(const FpropMaps& t, FpropParams p, cudaStream_t st) {
   using C = FpropCfg<BN, KBLK, BMN, CG>;
-  auto kern = conv_fprop_kernel<BN, KBLK, BMN, CG>;
+  auto kern = conv_fprop_kernel<BN, KBLK, BMN, CG, EW>;
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX) != cudaSuccess)
@@ -1354,7 +1387,7 @@ static int launch_fprop(const FpropMaps& t, FpropParams p, cudaStream_t st) {
   }
   if (C::CW != 32) p.tma_epi = 0;
   p.epi_nops = p.tma_epi ? (p.res != nullptr) + (p.mask != nullptr) + (p.accumulate != 0) : 0;
-  p.epi_bytes = p.tma_epi ? 8 * epi_warp_bytes(p.epi_nops) : EPI_LEGACY_BYTES;
+  p.epi_bytes = p.tma_epi ? (EW / 4) * epi_sub_bytes(p.epi_nops) : EPI_LEGACY_BYTES;
   // deepest operand pipeline that fits beside the epilogue buffers
   p.stages = 1;
   for (int s = FPROP_MAX_STAGES; s >= 1; --s) {
@@ -1367,7 +1400,7 @@ static int launch_fprop(const FpropMaps& t, FpropParams p, cudaStream_t st) {
   p.b_region = (p.stages * C::B_BYTES + 1023) / 1024 * 1024;
   const int smem = p.stages * C::A_BYTES + p.b_region + p.epi_bytes + SMEM_FIXED;
   const int grid = CG * std::min(p.num_tiles, num_sms() / CG);
-  const int rc = launch_tc(kern, grid, FPROP_THREADS, smem, st, CG, t.a, t.b, t.y, t.r, t.m, p);
+  const int rc = launch_tc(kern, grid, 64 + 32 * EW, smem, st, CG, t.a, t.b, t.y, t.r, t.m, p);
   return rc ? rc : check_launch();
 }
 
@@ -1390,6 +1423,26 @@ static int launch_wgrad(const CUtensorMap& tx, const CUtensorMap& tdy, const Wgr
 static bool fprop_pairs_enabled() {
   static const bool on = [] {
     const char* e = getenv("B2DL_FPROP_PAIRS");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// CTA-pair tiles for 128-wide N (B2DL_FPROP_PAIR128=1).  Off by default: at N = 128 the pair's
+// per-SM operand reads (4 KB A + 2 KB B per 64-cycle MMA) outrun shared memory, measured ~25 %
+// slower than a 256-wide pair on the 1/8-resolution ASPP convs.
+static bool fprop_pair128_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("B2DL_FPROP_PAIR128");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+// 16 epilogue warps for TMA-epilogue launches with <= 1 operand; B2DL_EW16=0 keeps 8
+static bool ew16_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("B2DL_EW16");
     return !(e && e[0] == '0');
   }();
   return on;
@@ -1452,7 +1505,7 @@ static int launch_halo_fprop(const b2dl_conv_args* a, const b2dl_act& xv, cudaSt
   p.vec_ok = 1;
   p.tma_epi = 1;
   p.epi_nops = (p.res != nullptr) + (p.mask != nullptr) + (p.accumulate != 0);
-  p.epi_bytes = 8 * epi_warp_bytes(p.epi_nops);
+  p.epi_bytes = 2 * epi_sub_bytes(p.epi_nops);
   const int a_stage = (HALO_BH + p.taps - 1) * HALO_BW * 128;
   const int b_region = p.taps * p.num_cblk * HALO_BBOX;
   p.stages = std::min(FPROP_MAX_STAGES, (SMEM_MAX - SMEM_FIXED - b_region - p.epi_bytes) / a_stage);
@@ -1460,7 +1513,7 @@ static int launch_halo_fprop(const b2dl_conv_args* a, const b2dl_act& xv, cudaSt
   const int smem = b_region + p.stages * a_stage + p.epi_bytes + SMEM_FIXED;
 
   FpropMaps t;
-  const int bwx = std::min(p.bw, 32), bhx = 32 / bwx;
+  const int bwx = p.bw, bhx = p.bh;  // epilogue boxes: 32 channels x the whole tile
   const uint64_t ktot = static_cast<uint64_t>(p.taps) * p.cin_pad;
   const uint64_t wd[2] = {ktot, static_cast<uint64_t>(a->cout)};
   const uint64_t wsd[1] = {ktot * 2};
@@ -1488,6 +1541,7 @@ static bool halo_fprop_ok(const b2dl_conv_args* a, const b2dl_act& xv) {
   const b2dl_act& y = a->y;
   const int nops = (a->residual.ptr != nullptr) + (a->mask.ptr != nullptr) + (a->accumulate != 0);
   return a->window && a->w_mode == 0 && a->w_packed && a->cout <= HALO_BN && a->cout % 8 == 0 && a->kh <= 7 &&
+         (!a->bias || (reinterpret_cast<uintptr_t>(a->bias) % 16 == 0)) &&
          a->dilation == 1 && xv.c > 16 && xv.c <= 128 && !a->y_f32 && view_aligned(y, 2) && nops <= 2 &&
          (!a->residual.ptr || view_aligned(a->residual, 2)) && (!a->mask.ptr || view_aligned(a->mask, 2)) &&
          tma_epilogue_enabled();
@@ -1525,22 +1579,38 @@ extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
   const int kblk = x.c <= 16 ? 16 : 64;
   const int cin_pad = b2dl_cin_pad(x.c);
   int bn = a->block_n ? a->block_n : pick_bn(a->cout);
-  // 256-wide N tiles run as CTA pairs (256 x 256 per pair)
-  auto pair_ok = [&](int b) { return b == 256 && kblk == 64 && fprop_pairs_enabled(); };
-  if (!a->block_n && bn == 256) {
-    // wave quantisation: a narrower N tile can fill the last wave of a small map better
+  // 256- and 128-wide N tiles run as CTA pairs (256 pixels x BN per pair)
+  auto pair_ok = [&](int b) {
+    return (b == 256 || (b == 128 && fprop_pair128_enabled())) && kblk == 64 && fprop_pairs_enabled();
+  };
+  int cg = pair_ok(bn) ? 2 : 1;
+  if (!a->block_n && (bn == 256 || bn == 128) && kblk == 64) {
+    // wave quantisation: pick the (N tile, pairing) that fills the persistent grid best,
+    // weighted by the relative speed of each tile shape
     const int bw = pow2_divisor(x.w, 128) < 8 && x.w >= 8 ? std::min(128, 1 << (31 - __builtin_clz(x.w)))
                                                          : pow2_divisor(x.w, 128);
     const long long mt = static_cast<long long>(x.n) * cdiv(x.w, bw) * cdiv(x.h, BM / bw);
-    auto score = [&](int b, double speed) {
-      const int g = pair_ok(b) ? 2 : 1;
+    auto score = [&](int b, int g, double speed) {
       const long long units = (mt + g - 1) / g * cdiv(a->cout, b), slots = num_sms() / g;
       const long long waves = (units + slots - 1) / slots;
       return speed * static_cast<double>(units) / (waves * slots);
     };
-    if (score(128, 0.7) > score(256, 1.0)) bn = 128;
+    struct Cand {
+      int b, g;
+      double speed;
+    };
+    const Cand cands[3] = {{256, 2, 1.0}, {128, 2, 0.6}, {128, 1, 0.7}};
+    double best = -1.0;
+    for (const Cand& c : cands) {
+      if (c.b > bn || (c.g == 2 && !pair_ok(c.b)) || (c.b == 256 && a->cout <= 128)) continue;
+      const double sc = score(c.b, c.g, c.speed);
+      if (sc > best) {
+        best = sc;
+        bn = c.b;
+        cg = c.g;
+      }
+    }
   }
-  const int cg = pair_ok(bn) ? 2 : 1;
 
   FpropParams p{};
   p.n = x.n;
@@ -1614,9 +1684,10 @@ extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
   // TMA epilogue: bf16 output (and operands) through 32-pixel x 32-channel swizzled boxes
   p.bias_vec = a->bias && (reinterpret_cast<uintptr_t>(a->bias) % 16 == 0);
   p.tma_epi = p.vec_ok && !p.y_f32 && (a->cout % 8) == 0 && bn >= 32 && tma_epilogue_enabled() &&
+              (!a->bias || p.bias_vec) &&
               ((p.res != nullptr) + (p.mask != nullptr) + (p.accumulate != 0)) <= 2;
   if (p.tma_epi) {
-    const int bwx = std::min(p.bw, 32), bhx = 32 / bwx;
+    const int bwx = p.bw, bhx = p.bh;  // epilogue boxes: 32 channels x the whole tile
     if (act_map(&t.y, y, 32, bwx, bhx, CU_TENSOR_MAP_SWIZZLE_64B) ||
         (p.res && act_map(&t.r, a->residual, 32, bwx, bhx, CU_TENSOR_MAP_SWIZZLE_64B)) ||
         (p.mask && act_map(&t.m, a->mask, 32, bwx, bhx, CU_TENSOR_MAP_SWIZZLE_64B)))
@@ -1627,8 +1698,21 @@ extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
 #define B2_FPROP(BNV, KB)                                                                \
   if (bn == BNV && kblk == KB)                                                           \
     return mode == 1 ? launch_fprop<BNV, KB, true, 1>(t, p, st) : launch_fprop<BNV, KB, false, 1>(t, p, st);
-  if (cg == 2)
+  const int nops = (p.res != nullptr) + (p.mask != nullptr) + (p.accumulate != 0);
+  // 16 epilogue warps where the epilogue dominates (short K); long-K launches keep the deeper
+  // operand ring that 8 warps' smaller buffers leave room for
+  if (p.tma_epi && nops <= 1 && kblk == 64 && p.num_kb <= 16 && ew16_enabled()) {
+    if (cg == 2 && bn == 256)
+      return mode == 1 ? launch_fprop<256, 64, true, 2, 16>(t, p, st) : launch_fprop<256, 64, false, 2, 16>(t, p, st);
+    if (cg == 1 && bn == 256)
+      return mode == 1 ? launch_fprop<256, 64, true, 1, 16>(t, p, st) : launch_fprop<256, 64, false, 1, 16>(t, p, st);
+    if (cg == 1 && bn == 128)
+      return mode == 1 ? launch_fprop<128, 64, true, 1, 16>(t, p, st) : launch_fprop<128, 64, false, 1, 16>(t, p, st);
+  }
+  if (cg == 2 && bn == 256)
     return mode == 1 ? launch_fprop<256, 64, true, 2>(t, p, st) : launch_fprop<256, 64, false, 2>(t, p, st);
+  if (cg == 2 && bn == 128)
+    return mode == 1 ? launch_fprop<128, 64, true, 2>(t, p, st) : launch_fprop<128, 64, false, 2>(t, p, st);
   B2_FPROP(256, 64)
   B2_FPROP(128, 64)
   B2_FPROP(64, 64)
@@ -1713,21 +1797,23 @@ static int plan_wgrad(const b2dl_wgrad_args* a, WgradPlan* out) {
   p.n_tiles = cdiv(dy.c, bn);
   int splits = a->splits;
   if (splits <= 0) {
-    // split-K count: fill whole waves of CTAs (persistent grid = #SMs) while keeping
-    // >= 32 pixel boxes of K per split so the fp32 partial traffic stays small
+    // split-K count minimising  waves x (K blocks per split) x t_kb  +  partial traffic / HBM:
+    // more splits fill the persistent grid (#SMs), but every split writes (and the batched
+    // reduction re-reads) a krows x cout fp32 partial.  t_kb ~ 0.7 us for a 256-wide tile
+    // (two 128 x 256 x 64 MMA blocks), proportional to the tile width.
     const int base = p.m_tiles * p.n_tiles;
     const int sms = num_sms();
     const int smax = std::max(1, std::min(sms, p.num_pb / 4));
-    double best = -1.0;
+    const double t_kb = 0.7e-6 * std::max(bn, 32) / 256.0;
+    const double part_bytes = static_cast<double>(p.krows) * p.cout * 4.0 * 2.0;
+    double best = 1e30;
     splits = 1;
     for (int s = 1; s <= smax; ++s) {
       const long long tiles = static_cast<long long>(base) * s;
       const long long waves = (tiles + sms - 1) / sms;
-      const double eff = static_cast<double>(tiles) / (waves * sms);
-      const double fill = std::min(1.0, static_cast<double>(tiles) / sms);
-      const double score = eff * fill - 0.002 * s;  // mild preference for fewer partials
-      if (score > best) {
-        best = score;
+      const double t = waves * std::ceil(static_cast<double>(p.num_pb) / s) * t_kb + s * part_bytes / 6.0e12;
+      if (t < best * 0.999) {
+        best = t;
         splits = s;
       }
     }

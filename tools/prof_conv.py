@@ -38,7 +38,18 @@ ws7 = torch.randn(49, 16, 64, device="cuda") * 0.05
 wp7 = torch.empty(64, 7, 128, dtype=torch.bfloat16, device="cuda")
 nhwc.pack_weights(ws7, 7, 1, 112, 64, fprop=wp7)
 b64 = torch.zeros(64, device="cuda")
+xa = torch.randn(2, 144, 96, 2048, device="cuda").to(torch.bfloat16)
+ya = torch.empty(2, 144, 96, 256, dtype=torch.bfloat16, device="cuda")
+wa = (torch.randn(9, 2048, 256, device="cuda") * 0.01).to(torch.bfloat16)
+xb = torch.randn(2, 144, 96, 256, device="cuda").to(torch.bfloat16)
+wb = (torch.randn(9, 256, 256, device="cuda") * 0.02).to(torch.bfloat16)
 ops = {
+    "aspp_fprop": lambda: nhwc.conv_fprop(nhwc.View(xa), None, 256, 3, 3, 12, nhwc.View(ya), bias=b, relu=True,
+                                          w_master=wa, w_mode=1),
+    "s2b_fprop": lambda: nhwc.conv_fprop(nhwc.View(xb), None, 256, 3, 3, 2, nhwc.View(ya), bias=b, relu=True,
+                                         w_master=wb, w_mode=1),
+    "s2b_dgrad": lambda: nhwc.conv_dgrad(nhwc.View(ya), None, 256, 3, 3, 2, nhwc.View(xb), mask=nhwc.View(xb),
+                                         w_master=wb),
     "stem_fprop_win": lambda: nhwc.conv_fprop(nhwc.View(xwin), wp7, 64, 7, 1, 1, nhwc.View(ys), bias=b64, relu=True,
                                               window=7),
     "stem_wgrad_win": lambda: nhwc.conv_wgrad(nhwc.View(xwin), nhwc.View(ys), 7, 1, 1, dws, ws, window=7),
@@ -67,7 +78,8 @@ for k in sel:
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 3
-    fl = {"stem_wgrad": 2 * 49 * 16 * 64 * N * H * W, "stem_wgrad_win": 2 * 49 * 16 * 64 * N * H * W,
+    fl = {"aspp_fprop": 2 * 9 * 2048 * 256 * 2 * 144 * 96, "s2b_fprop": 2 * 9 * 256 * 256 * 2 * 144 * 96,
+          "s2b_dgrad": 2 * 9 * 256 * 256 * 2 * 144 * 96, "stem_wgrad": 2 * 49 * 16 * 64 * N * H * W, "stem_wgrad_win": 2 * 49 * 16 * 64 * N * H * W,
           "stem_fprop_win": 2 * 49 * 16 * 64 * N * H * W, "c1x1_fprop": 2 * 512 * 2048 * 2 * 144 * 96,
                                                   "c1x1_dgrad": 2 * 512 * 2048 * 2 * 144 * 96}.get(
         k, 2 * 9 * C * C * N * H * W)
