@@ -206,3 +206,40 @@ def test_row_window_conv(case):
     ref_dw = wg.grad.permute(2, 3, 1, 0).reshape(-1)
     assert _rel(dw, ref_dw) < 2e-3
     assert _rel(bg, dy.double().sum((0, 1, 2))) < 1e-4
+
+
+@pytest.mark.parametrize("cin,cout", [(256, 256), (512, 512), (1024, 256), (2048, 256)])
+@pytest.mark.parametrize("d", [1, 2, 4, 12, 18, 24])
+def test_atrous_sweep_shapes_vs_oracle(cin, cout, d):
+    """Config 5 shapes (tools/atrous_sweep.py times them at full size) against the reference's own
+    conv arithmetic (oracle port of _kernels_py.py:44-83) on a cropped 28 x 28 map: fprop, dgrad
+    and wgrad through the production NHWC entry points (master-layout weights)."""
+    import numpy as np
+    from oracle import deskdl_port as ref
+    from paper_1810_01993_b200 import nhwc
+    n, h, w = 1, 28, 28
+    rng = np.random.default_rng(cin + cout + d)
+    xq = rng.uniform(-1, 1, (n, cin, h, w)).astype(np.float32)
+    dyq = rng.uniform(-1, 1, (n, cout, h, w)).astype(np.float32)
+    wq = (rng.uniform(-1, 1, (cout, cin, 3, 3)) / np.sqrt(9 * cin)).astype(np.float32)
+    bf = lambda a: torch.from_numpy(a).to(torch.bfloat16)  # noqa: E731
+    xb, dyb, wb = bf(xq), bf(dyq), bf(wq)
+    x64, dy64, w64 = (t.double().numpy() for t in (xb, dyb, wb))
+    y_ref, cols = ref.conv2d_forward(x64, w64, dilation=d)
+    dx_ref = ref.conv2d_backward_input(dy64, w64, x64.shape, dilation=d)
+    dw_ref = ref.conv2d_backward_weights(cols, dy64, w64.shape, dilation=d)
+    x = xb.permute(0, 2, 3, 1).contiguous().cuda()
+    dy = dyb.permute(0, 2, 3, 1).contiguous().cuda()
+    wm = wb.permute(2, 3, 1, 0).reshape(9, cin, cout).contiguous().cuda()   # HWIO
+    y = torch.empty(n, h, w, cout, dtype=torch.float32, device="cuda")
+    nhwc.conv_fprop(nhwc.View(x), None, cout, 3, 3, d, nhwc.View(y), y_f32=True, w_master=wm, w_mode=1)
+    dx = torch.empty(n, h, w, cin, dtype=torch.float32, device="cuda")
+    nhwc.conv_dgrad(nhwc.View(dy), None, cin, 3, 3, d, nhwc.View(dx), dx_f32=True, w_master=wm)
+    dw = torch.empty(9 * cin * cout, device="cuda")
+    nhwc.conv_wgrad(nhwc.View(x), nhwc.View(dy), 3, 3, d, dw, nhwc.Workspace())
+    y_ref = torch.from_numpy(y_ref).permute(0, 2, 3, 1)
+    dx_ref = torch.from_numpy(dx_ref).permute(0, 2, 3, 1)
+    dw_ref = torch.from_numpy(dw_ref).permute(2, 3, 1, 0).reshape(-1)
+    assert _rel(y.cpu(), y_ref) < 2e-3
+    assert _rel(dx.cpu(), dx_ref) < 2e-3
+    assert _rel(dw.cpu(), dw_ref) < 2e-3

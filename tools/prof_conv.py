@@ -43,7 +43,11 @@ ya = torch.empty(2, 144, 96, 256, dtype=torch.bfloat16, device="cuda")
 wa = (torch.randn(9, 2048, 256, device="cuda") * 0.01).to(torch.bfloat16)
 xb = torch.randn(2, 144, 96, 256, device="cuda").to(torch.bfloat16)
 wb = (torch.randn(9, 256, 256, device="cuda") * 0.02).to(torch.bfloat16)
+xq = torch.randn(2, 288, 192, 256, device="cuda").to(torch.bfloat16)
+yq = torch.empty_like(xq)
 ops = {
+    "q_fprop": lambda: nhwc.conv_fprop(nhwc.View(xq), None, 256, 3, 3, 1, nhwc.View(yq), bias=b, relu=True,
+                                       w_master=wbf, w_mode=1),
     "aspp_fprop": lambda: nhwc.conv_fprop(nhwc.View(xa), None, 256, 3, 3, 12, nhwc.View(ya), bias=b, relu=True,
                                           w_master=wa, w_mode=1),
     "s2b_fprop": lambda: nhwc.conv_fprop(nhwc.View(xb), None, 256, 3, 3, 2, nhwc.View(ya), bias=b, relu=True,
@@ -78,7 +82,7 @@ for k in sel:
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 3
-    fl = {"aspp_fprop": 2 * 9 * 2048 * 256 * 2 * 144 * 96, "s2b_fprop": 2 * 9 * 256 * 256 * 2 * 144 * 96,
+    fl = {"q_fprop": 2 * 9 * 256 * 256 * 2 * 288 * 192, "aspp_fprop": 2 * 9 * 2048 * 256 * 2 * 144 * 96, "s2b_fprop": 2 * 9 * 256 * 256 * 2 * 144 * 96,
           "s2b_dgrad": 2 * 9 * 256 * 256 * 2 * 144 * 96, "stem_wgrad": 2 * 49 * 16 * 64 * N * H * W, "stem_wgrad_win": 2 * 49 * 16 * 64 * N * H * W,
           "stem_fprop_win": 2 * 49 * 16 * 64 * N * H * W, "c1x1_fprop": 2 * 512 * 2048 * 2 * 144 * 96,
                                                   "c1x1_dgrad": 2 * 512 * 2048 * 2 * 144 * 96}.get(
