@@ -142,6 +142,13 @@ def _sample_desc():
             f"linearly with pixels, so images/s = {frac:.4f} / step time"), frac
 
 
+def _config(world):
+    return {"workload": "config 2/3: DeepLabV3+ (ResNet-50 OS8, ASPP 12/18/24, full-res decoder) "
+                        "bf16 train step, fused weighted CE + LARC", "model": "DeepLabV3+",
+            "global_batch": world * LOCAL_BATCH, "local_batch": LOCAL_BATCH, "tile": [C, H, W],
+            "parallelism": f"dp{world}", "l2": "working set ~11 GB/GPU >> 126 MB L2, no flush"}
+
+
 def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -153,14 +160,15 @@ def run_reference(args):
     ms = 1e3 * float(np.median(times))
     value = frac / (ms / 1e3)
     cores = os.cpu_count()
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": 0,
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world,
             "steps": len(times), "warmup": min(args.warmup, 1), "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (make_scene)",
-            "config": {"workload": "DeepLabV3+ train step, reference CPU path, bounded sample",
-                       "global_batch": CPU_SAMPLE[0], "tile": list(CPU_SAMPLE[1:]), "world_requested": world},
+            "config": dict(_config(world), reference_arm="reference CPU step (oracle port, all host threads) on a "
+                           "bounded sample of the same workload, rank 0 only", sample_batch=CPU_SAMPLE[0],
+                           sample_tile=list(CPU_SAMPLE[1:])),
             "cpu_baseline": {"value": value, "unit": "images/s", "cores": cores, "kind": "port", "sample": desc},
             "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -282,10 +290,7 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (GPU-generated scenes, resident in HBM)",
-            "config": {"workload": "config 2/3: DeepLabV3+ (ResNet-50 OS8, ASPP 12/18/24, full-res decoder) "
-                                   "bf16 train step, fused weighted CE + LARC", "model": "DeepLabV3+",
-                       "global_batch": world * LOCAL_BATCH, "local_batch": LOCAL_BATCH, "tile": [C, H, W],
-                       "parallelism": f"dp{world}", "l2": "working set ~11 GB/GPU >> 126 MB L2, no flush"},
+            "config": _config(world),
             "sustained_tflops": sust_tf, "flops_per_image": flops_img, "flops_per_image_exact": flops_img_exact,
             "frac_of_peak": sust_tf / peak,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -298,13 +303,32 @@ def run_ours(args):
             "gpu_launches": launches, "cuda_graph": graphed, "clocks": clk.summary(), "cpu_baseline": cpu,
             "last_loss": lv,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
+    tr.release_graph()
     if world > 1:
+        dist.barrier()
         dist.destroy_process_group()
     return 0
 
 
+def _json_stdout():
+    """Keep fd 1 for the one JSON line: library banners written to stdout (e.g. the NCCL version
+    line) are redirected to stderr at the file-descriptor level."""
+    global JSON_OUT
+    sys.stdout.flush()
+    JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+
+
+JSON_OUT = sys.stdout
+
+
+def emit(line):
+    print(json.dumps(line), file=JSON_OUT, flush=True)
+
+
 def main():
+    _json_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)

@@ -207,6 +207,14 @@ class DataParallelTrainer:
             self._apply(self.eng.flat_g)
             self.have_prev = False
 
+    def release_graph(self):
+        """Drop the captured step graph (it references NCCL communicators: release it before the
+        process group is destroyed)."""
+        if getattr(self, "graph", None) is not None:
+            torch.cuda.synchronize()
+            self.graph.reset()
+            self.graph = None
+
     def check_status(self):
         if int(self.status.item()):
             raise FloatingPointError("non-finite norm in LARC")

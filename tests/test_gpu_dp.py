@@ -58,6 +58,6 @@ def test_two_gpu_nccl_matches_reference(lag):
     tag = f"lag{lag}_w2"
     assert np.allclose(out[0][0], d[tag + "_losses"], rtol=2e-2)
     assert out[0][1] == out[1][1]                      # cross-rank weight digests agree
-    for k, v in out[0][2].items():
+    for k, v in out[0][2].items():   # trajectory agreement after 3 bf16 steps (norm-relative)
         ref = d[f"{tag}_state:{k}"]
-        assert np.max(np.abs(v - ref)) / np.max(np.abs(ref)) < 5e-2, k
+        assert np.linalg.norm(v - ref) / np.linalg.norm(ref) < 2e-2, k
