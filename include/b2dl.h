@@ -236,6 +236,25 @@ B2DL_API size_t b2dl_larc_workspace_size(int64_t total_elems, int ntensors);
 B2DL_API int b2dl_larc_update(const b2dl_larc_args* a, void* stream);
 
 /* Version / capability string (for smoke checks). */
+/* ---------------------------------------------------------------- (3) fp32 parity mode
+ * The reference's own arithmetic type end to end (north star: loss and gradients within 1e-3 in
+ * fp32 mode): every b2dl_act below is NHWC fp32, weights are the fp32 HWIO master, FMA
+ * accumulation in fp32 on the CUDA cores.  Same semantics as the bf16 entry points above. */
+/* conv forward (w_mode 1: w_master = this conv's HWIO) or input gradient (w_mode 2: w_master =
+ * the forward conv's HWIO, tap-flipped, "after" pads); fused bias / residual / relu / mask /
+ * accumulate epilogue as in b2dl_conv_fprop.  w_packed, block_n, y_f32 and window are ignored. */
+B2DL_API int b2dl_f32_conv_fprop(const b2dl_conv_args* a, void* stream);
+/* dw fp32 HWIO (+)= wgrad, bias_grad (+)= column sums; split-K partials in `workspace`, reduced
+ * in a fixed order before return (defer_reduce, splits and window are ignored / rejected). */
+B2DL_API size_t b2dl_f32_wgrad_workspace_size(const b2dl_wgrad_args* a);
+B2DL_API int b2dl_f32_conv_wgrad(const b2dl_wgrad_args* a, void* stream);
+B2DL_API int b2dl_f32_avgpool_fwd(b2dl_act x, b2dl_act y, int k, void* stream);
+B2DL_API int b2dl_f32_avgpool_bwd(b2dl_act dy, b2dl_act dx, int k, int accumulate, b2dl_act mask, void* stream);
+B2DL_API int b2dl_f32_upsample_fwd(b2dl_act x, b2dl_act y, int f, void* stream);
+B2DL_API int b2dl_f32_upsample_bwd(b2dl_act dy, b2dl_act dx, int f, int accumulate, b2dl_act mask, void* stream);
+/* y (+)= x, masked by (mask > 0); with x == y and accumulate == 0 it is the in-place relu VJP. */
+B2DL_API int b2dl_f32_add(b2dl_act x, b2dl_act y, int accumulate, b2dl_act mask, void* stream);
+
 B2DL_API const char* b2dl_version(void);
 
 #ifdef __cplusplus

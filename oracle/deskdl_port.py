@@ -155,7 +155,7 @@ def _ancestors(graph, targets):
     return keep[::-1]
 
 
-def _fwd(nd, ins):
+def _fwd(nd, ins, relu_mask=None):
     k, a = nd.kind, nd.attrs
     if k == "conv2d":
         return conv2d_forward(ins[0], ins[1], a["stride"], a["dilation"])
@@ -164,6 +164,8 @@ def _fwd(nd, ins):
     if k == "bias_add":
         return ins[0] + ins[1].reshape((1, -1) + (1,) * (ins[0].ndim - 2)), None
     if k == "relu":
+        if relu_mask is not None:   # sign decisions imposed (flip-matched comparisons)
+            return np.where(relu_mask, ins[0], 0).astype(ins[0].dtype), relu_mask
         return np.maximum(ins[0], 0), None
     if k == "concat":
         return np.concatenate(ins, axis=a["axis"]), None
@@ -201,7 +203,8 @@ def _bwd(nd, ins, out, cache, g, need):
         axes = tuple(i for i in range(g.ndim) if i != 1)
         return (g if need[0] else None), (g.sum(axis=axes) if need[1] else None)
     if k == "relu":
-        return ((out > 0) * g if need[0] else None,)
+        m = (out > 0) if cache is None else cache
+        return (m * g if need[0] else None,)
     if k == "concat":
         cuts = np.cumsum([x.shape[a["axis"]] for x in ins[:-1]])
         return tuple(p if q else None for p, q in zip(np.split(g, cuts, axis=a["axis"]), need))
@@ -224,14 +227,19 @@ def _bwd(nd, ins, out, cache, g, need):
     raise AssertionError(k)
 
 
-def run_forward(graph, values, targets=None):
-    """Tape forward over the ancestor closure of targets (ops.py:44-70)."""
+def run_forward(graph, values, targets=None, relu_masks=None):
+    """Tape forward over the ancestor closure of targets (ops.py:44-70).
+
+    relu_masks (test use only): {relu node: boolean NCHW mask} imposes the on/off decision of
+    those relus (forward and VJP), so two implementations can be compared without the relu
+    sign flips that round-off at near-zero pre-activations causes."""
     if targets is None:
         targets = [nd.name for nd in graph.nodes]
     tape = Tape()
     tape.values.update({k: np.asarray(v) for k, v in values.items()})
+    masks = relu_masks or {}
     for nd in _ancestors(graph, targets):
-        out, cache = _fwd(nd, [tape.values[s] for s in nd.inputs])
+        out, cache = _fwd(nd, [tape.values[s] for s in nd.inputs], masks.get(nd.name))
         tape.values[nd.name] = out
         tape.caches[nd.name] = cache
         tape.order.append(nd)
@@ -321,14 +329,14 @@ def sustained(rates_per_step, warmup=1):
 # ---------------------------------------------------------------- one full step
 
 def train_step(graph, params, param_order, x, labels, cw, loss_name, logits_name, opt=None,
-               moms=None):
+               moms=None, relu_masks=None):
     """forward_loss + backward + per-tensor LARC (net.py:132-146, trainer.py:364-387).
 
     Updates params / moms in place when `opt` is given; returns (loss, logits, grads, lrs).
     """
     vals = dict(params)
     vals.update(x=x, labels=labels, class_weights=cw)
-    out, tape = run_forward(graph, vals, targets=[loss_name, logits_name])
+    out, tape = run_forward(graph, vals, targets=[loss_name, logits_name], relu_masks=relu_masks)
     grads = run_backward(graph, tape, loss_name, wrt=param_order)
     lrs = {}
     if opt is not None:

@@ -80,6 +80,14 @@ _SIGS = {
     "b2dl_reduce_segments": (_c_int, [_vp, _c_int, ctypes.c_int64, _vp, _vp]),
     "b2dl_pack_weights": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp]),
     "b2dl_nchw_to_nhwc": (_c_int, [_vp, Act, _c_int, _vp]),
+    "b2dl_f32_conv_fprop": (_c_int, [ctypes.POINTER(ConvArgs), _vp]),
+    "b2dl_f32_wgrad_workspace_size": (ctypes.c_size_t, [ctypes.POINTER(WgradArgs)]),
+    "b2dl_f32_conv_wgrad": (_c_int, [ctypes.POINTER(WgradArgs), _vp]),
+    "b2dl_f32_avgpool_fwd": (_c_int, [Act, Act, _c_int, _vp]),
+    "b2dl_f32_avgpool_bwd": (_c_int, [Act, Act, _c_int, _c_int, Act, _vp]),
+    "b2dl_f32_upsample_fwd": (_c_int, [Act, Act, _c_int, _vp]),
+    "b2dl_f32_upsample_bwd": (_c_int, [Act, Act, _c_int, _c_int, Act, _vp]),
+    "b2dl_f32_add": (_c_int, [Act, Act, _c_int, Act, _vp]),
     "b2dl_head_backward_parts": (_c_int, []),
     "b2dl_head_backward": (_c_int, [Act, _vp, Act, Act, _c_int, _c_int, _vp, _vp, _vp]),
     "b2dl_nchw_to_nhwc_halo": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _c_int, _vp]),

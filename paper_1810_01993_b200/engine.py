@@ -339,7 +339,13 @@ class Engine:
     """Device state + launches for one model at one input shape."""
 
     def __init__(self, graph: OpGraph, params: dict, param_order, input_shape, loss_name, logits_name,
-                 device="cuda"):
+                 device="cuda", precision="bf16"):
+        if precision not in ("bf16", "fp32"):
+            raise ValueError(f"precision must be 'bf16' or 'fp32', not {precision!r}")
+        # fp32: the parity mode -- fp32 NHWC buffers, fp32 HWIO weights, CUDA-core kernels
+        # (b2dl.h group 3); same program, same fusion points
+        self.fp32 = precision == "fp32"
+        self.precision = precision
         self.device = torch.device(device)
         self.order = list(param_order)
         self.plan = Plan(graph, {k: v.shape for k, v in params.items()}, tuple(input_shape), loss_name,
@@ -347,9 +353,10 @@ class Engine:
         p = self.plan
         self.ws = nhwc.Workspace(self.device)
         bf, f32 = torch.bfloat16, torch.float32
-        self.act = {r: torch.empty((n, h, w, c), dtype=f32 if isf else bf, device=self.device)
+        adt = f32 if self.fp32 else bf
+        self.act = {r: torch.empty((n, h, w, c), dtype=f32 if isf else adt, device=self.device)
                     for r, (n, h, w, c, isf) in p.buffers.items()}
-        self.grad = {r: torch.empty(s, dtype=bf, device=self.device) for r, s in p.grad_buffers.items()}
+        self.grad = {r: torch.empty(s, dtype=adt, device=self.device) for r, s in p.grad_buffers.items()}
         # flat fp32 parameters / gradients / momentum in param order; conv weights HWIO
         self.slot = {}
         off = 0
@@ -374,7 +381,7 @@ class Engine:
         self._lr_scratch = torch.zeros(len(self.order), dtype=f32, device=self.device)
         self._status = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.wf, self.wd = {}, {}
-        self.packed = [o for o in self.convs if o.cout % 8 != 0]
+        self.packed = [] if self.fp32 else [o for o in self.convs if o.cout % 8 != 0]
         for o in self.packed:
             t = o.k * o.k
             self.wf[o.w] = torch.zeros((o.cout, t, nhwc.cin_pad(o.cin)), dtype=bf, device=self.device)
@@ -386,7 +393,7 @@ class Engine:
         # 14 64-wide K blocks instead of 49 16-wide ones.
         self.win = None
         users = [o for o in p.ops if "x" in o.ins]
-        if len(users) == 1 and users[0].kind == "conv":
+        if len(users) == 1 and users[0].kind == "conv" and not self.fp32:
             o = users[0]
             if (o.k > 1 and o.dil == 1 and o.cin % 8 == 0 and 16 < o.cin * o.k <= 128 and o.cout % 8 == 0
                     and o.ins[0] == "x" and not o.res):
@@ -399,10 +406,13 @@ class Engine:
         self.segs = {}
         total, offs = 0, {}
         # few-output-channel 1x1 convs (the 3-class head): wgrad + dgrad in one pass over the input
-        self.heads = {o.w for o in self.convs
-                      if o.k == 1 and o.cout < 8 and o.cin % 8 == 0 and 256 % (o.cin // 8) == 0}
+        self.heads = set() if self.fp32 else {o.w for o in self.convs
+                                              if o.k == 1 and o.cout < 8 and o.cin % 8 == 0
+                                              and 256 % (o.cin // 8) == 0}
         hparts = nhwc.head_backward_parts()
         for o in self.convs:
+            if self.fp32:   # fp32 wgrad reduces its split-K partials itself, into flat_g
+                continue
             if o.w in self.heads:
                 nw = hparts * o.cin * o.cout * 4
                 offs[o.w] = (total, nw + hparts * o.cout * 4, hparts, hparts, nw)
@@ -420,6 +430,8 @@ class Engine:
         self.partials_buf = torch.empty(max(total, 256), dtype=torch.uint8, device=self.device)
         self.head_parts = {}
         for o in self.convs:
+            if self.fp32:
+                continue
             off, nbytes, wp, bp, bo = offs[o.w]
             buf = self.partials_buf[off:off + nbytes]
             self.partials[o.w] = buf
@@ -537,6 +549,8 @@ class Engine:
 
     def refresh_mirror(self):
         """bf16 mirror <- flat fp32 parameters (after loading weights from the host)."""
+        if self.fp32:
+            return
         nhwc.larc_update(self.flat_w, self.flat_m, self.flat_g, self.offsets, 1.0, 0.0, 1.0, 0.0, 1.0, 1.0,
                          self._lr_scratch, self._status, self.ws, mode=3, w_bf16=self.flat_wbf)
         self.launches += 1
@@ -563,7 +577,7 @@ class Engine:
         if self.win is not None:
             nhwc.nchw_to_nhwc_halo(x_nchw.contiguous(), self.xwin, (self.win.k - 1) // 2)
         else:
-            nhwc.nchw_to_nhwc(x_nchw.contiguous(), self.v("x"))
+            nhwc.nchw_to_nhwc(x_nchw.contiguous(), self.v("x"), dst_f32=self.fp32)
         self.labels.copy_(labels.reshape(-1))
         self.launches += 1
 
@@ -574,7 +588,14 @@ class Engine:
     def forward(self):
         p = self.plan
         for op in p.ops:
-            if op.kind == "conv":
+            if op.kind == "conv" and self.fp32:
+                b_off, _ = self.slot[op.b]
+                ev = self._tic()
+                nhwc.f32_conv(self.v(op.ins[0]), self.wslice(op.w), op.cout, op.k, op.k, op.dil, self.v(op.out),
+                              bias=self.flat_w[b_off:b_off + op.cout],
+                              residual=self.v(op.res) if op.res else None, relu=op.relu)
+                self._toc(ev, op)
+            elif op.kind == "conv":
                 out = op.out
                 b_off, _ = self.slot[op.b]
                 ev = self._tic()
@@ -591,27 +612,29 @@ class Engine:
                                 y_f32=(out == p.logits_name))
                 self._toc(ev, op)
             elif op.kind == "pool":
-                nhwc.avgpool_fwd(self.v(op.ins[0]), self.v(op.out), op.factor)
+                (nhwc.f32_avgpool_fwd if self.fp32 else nhwc.avgpool_fwd)(self.v(op.ins[0]), self.v(op.out),
+                                                                          op.factor)
             elif op.kind == "up":
-                nhwc.upsample_fwd(self.v(op.ins[0]), self.v(op.out), op.factor)
+                (nhwc.f32_upsample_fwd if self.fp32 else nhwc.upsample_fwd)(self.v(op.ins[0]), self.v(op.out),
+                                                                            op.factor)
             elif op.kind == "concat":
                 off = 0
                 for s in op.ins:
                     if s in op.copy_ins:
                         root, coff, c = p.view_spec(op.out)
-                        nhwc.add(self.v(s), View(self.act[root], coff + off, self.plan.chans(s)),
-                                 accumulate=False)
+                        self._add(self.v(s), View(self.act[root], coff + off, self.plan.chans(s)),
+                                  accumulate=False)
                         self.launches += 1
                     off += self.plan.chans(s)
                 continue
             elif op.kind == "add":
                 a, b = op.ins
-                nhwc.add(self.v(a), self.v(op.out), accumulate=False)
-                nhwc.add(self.v(b), self.v(op.out), accumulate=True)
+                self._add(self.v(a), self.v(op.out), accumulate=False)
+                self._add(self.v(b), self.v(op.out), accumulate=True)
                 self.launches += 1
             elif op.kind == "ce":
                 nhwc.wce(self.v(op.ins[0]), self.labels, self.class_weights, self.loss, self.counts,
-                         self.gv(op.ins[0]), self.pred, self.ws)
+                         self.gv(op.ins[0]), self.pred, self.ws, dlogits_f32=self.fp32)
                 self.launches += 2   # histogram + loss/dlogits + final fold (3 with the +1 below)
             self.launches += 1
 
@@ -631,7 +654,31 @@ class Engine:
         pending = [len(b) for b in self.buckets]
         for st in self.plan.backward_program:
             op = st["op"]
-            if op.kind == "conv":
+            if op.kind == "conv" and self.fp32:
+                gy = self.gv(op.out)
+                if st["relu_pass"]:
+                    nhwc.f32_relu_mask(gy, self.v(op.out))
+                    self.launches += 1
+                w_off, _ = self.slot[op.w]
+                b_off, _ = self.slot[op.b]
+                ev = self._tic()
+                nhwc.f32_conv_wgrad(self.v(op.ins[0]), gy, op.k, op.k, op.dil, self.wslice(op.w, self.flat_g),
+                                    self.ws, bias_grad=self.flat_g[b_off:b_off + op.cout])
+                self._toc(ev, op)
+                self.launches += 3
+                for name in (op.w, op.b):
+                    i = self.bucket_of[name]
+                    pending[i] -= 1
+                    if pending[i] == 0 and on_bucket_ready is not None:
+                        on_bucket_ready(i)
+                if st["dx"] is not None:
+                    ev = self._tic()
+                    nhwc.f32_conv_dgrad(gy, self.wslice(op.w), op.cin, op.k, op.k, op.dil, self.gv(op.ins[0]),
+                                        accumulate=st["dx"], mask=self.v(op.ins[0]) if st["mask_dx"] else None,
+                                        residual=self.gv(st["dx_res"]) if st["dx_res"] else None)
+                    self._toc(ev, op)
+                    self.launches += 1
+            elif op.kind == "conv":
                 gy = self.gv(op.out)
                 if st["relu_pass"]:
                     nhwc.relu_mask(gy, self.v(op.out))
@@ -677,24 +724,29 @@ class Engine:
                     self.launches += 1
 
             elif op.kind == "pool":
-                nhwc.avgpool_bwd(self.gv(op.out), self.gv(op.ins[0]), op.factor, accumulate=st["dx"],
-                                 mask=self.v(op.ins[0]) if st["mask"] else None)
+                (nhwc.f32_avgpool_bwd if self.fp32 else nhwc.avgpool_bwd)(
+                    self.gv(op.out), self.gv(op.ins[0]), op.factor, accumulate=st["dx"],
+                    mask=self.v(op.ins[0]) if st["mask"] else None)
                 self.launches += 1
             elif op.kind == "up":
-                nhwc.upsample_bwd(self.gv(op.out), self.gv(op.ins[0]), op.factor, accumulate=st["dx"],
-                                  mask=self.v(op.ins[0]) if st["mask"] else None)
+                (nhwc.f32_upsample_bwd if self.fp32 else nhwc.upsample_bwd)(
+                    self.gv(op.out), self.gv(op.ins[0]), op.factor, accumulate=st["dx"],
+                    mask=self.v(op.ins[0]) if st["mask"] else None)
                 self.launches += 1
             elif op.kind == "concat":
                 root, coff, _ = self.plan.view_spec(op.out)
                 for s, off, acc, m in st["copies"]:
-                    nhwc.add(View(self.grad[root], coff + off, self.plan.chans(s)), self.gv(s), accumulate=acc,
-                             mask=self.v(s) if m else None)
+                    self._add(View(self.grad[root], coff + off, self.plan.chans(s)), self.gv(s), accumulate=acc,
+                              mask=self.v(s) if m else None)
                     self.launches += 1
             elif op.kind == "add":
                 src = st.get("passthrough", op.out)
                 for s, acc, m in st["acc"]:
-                    nhwc.add(self.gv(src), self.gv(s), accumulate=acc, mask=self.v(s) if m else None)
+                    self._add(self.gv(src), self.gv(s), accumulate=acc, mask=self.v(s) if m else None)
                     self.launches += 1
+
+    def _add(self, x, y, accumulate=False, mask=None):
+        (nhwc.f32_add if self.fp32 else nhwc.add)(x, y, accumulate=accumulate, mask=mask)
 
     def logits_nchw(self) -> torch.Tensor:
         n, c, h, w = self.plan.shapes[self.plan.logits_name]

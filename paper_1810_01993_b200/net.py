@@ -58,8 +58,10 @@ def _dev(a, dtype):
 class SegmentationNet:
     """Shared implementation: seeded graph + params, one GPU engine per input shape."""
 
-    def __init__(self, cfg, seed: int = 0):
+    def __init__(self, cfg, seed: int = 0, precision: str = "bf16"):
+        """precision: "bf16" (tensor-core path) or "fp32" (parity mode, b2dl.h group 3)."""
         self.cfg = cfg
+        self.precision = precision
         self.graph, params, self.logits_name, self.loss_name = models.build(cfg, seed)
         self.param_order = list(params)
         self._params = params
@@ -108,7 +110,8 @@ class SegmentationNet:
         eng = self._engines.get(shape)
         if eng is None:
             params = self.params
-            eng = Engine(self.graph, params, self.param_order, shape, self.loss_name, self.logits_name)
+            eng = Engine(self.graph, params, self.param_order, shape, self.loss_name, self.logits_name,
+                         precision=self.precision)
             self._engines[shape] = eng
         elif self._active is not None and self._active is not eng:
             eng.load_params(self.params)
@@ -158,12 +161,12 @@ class SegmentationNet:
 class MiniDenseNet(SegmentationNet):
     """The reference's FC-DenseNet / Tiramisu-style network (net.py:44-174)."""
 
-    def __init__(self, cfg: NetConfig = NetConfig(), seed: int = 0):
-        super().__init__(cfg, seed)
+    def __init__(self, cfg: NetConfig = NetConfig(), seed: int = 0, precision: str = "bf16"):
+        super().__init__(cfg, seed, precision)
 
 
 class DeepLabV3Plus(SegmentationNet):
     """DeepLabV3+ (OS8, ASPP 12/18/24, full-resolution decoder) of the headline benchmark."""
 
-    def __init__(self, cfg: DeepLabConfig = DeepLabConfig(), seed: int = 0):
-        super().__init__(cfg, seed)
+    def __init__(self, cfg: DeepLabConfig = DeepLabConfig(), seed: int = 0, precision: str = "bf16"):
+        super().__init__(cfg, seed, precision)

@@ -251,3 +251,57 @@ def larc_update(w: torch.Tensor, m: torch.Tensor, g: torch.Tensor, offsets: torc
                  trust, weight_decay, eps, grad_scale, lr_out.data_ptr(), status.data_ptr(),
                  buf.data_ptr(), buf.numel(), mode, None if w_bf16 is None else w_bf16.data_ptr())
     check(LIB.b2dl_larc_update(ctypes.byref(a), _stream()), "larc_update")
+
+
+# ---------------------------------------------------------------- fp32 parity mode (b2dl.h group 3)
+def f32_conv(x: View, w_hwio: torch.Tensor, cout: int, kh: int, kw: int, dilation: int, y: View, bias=None,
+             residual: View | None = None, relu=False, accumulate=False, mask: View | None = None, pads=None,
+             w_mode=1):
+    """fp32 NHWC conv (w_mode 1) or input gradient (w_mode 2, w_hwio = the forward conv's HWIO)."""
+    pt, pl = pads if pads is not None else (same_pads(kh, dilation)[0], same_pads(kw, dilation)[0])
+    a = ConvArgs(x.act(), None, cout, kh, kw, dilation, pt, pl, y.act(), 1, _ptr(bias), _act(residual),
+                 int(relu), int(accumulate), _act(mask), 0, ctypes.c_void_p(w_hwio.data_ptr()), w_mode, 0)
+    check(LIB.b2dl_f32_conv_fprop(ctypes.byref(a), _stream()), "f32_conv")
+
+
+def f32_conv_dgrad(dy: View, w_hwio: torch.Tensor, cin: int, kh: int, kw: int, dilation: int, dx: View,
+                   accumulate=False, mask: View | None = None, residual: View | None = None):
+    pads = (same_pads(kh, dilation)[1], same_pads(kw, dilation)[1])
+    f32_conv(dy, w_hwio, cin, kh, kw, dilation, dx, residual=residual, accumulate=accumulate, mask=mask, pads=pads,
+             w_mode=2)
+
+
+def f32_conv_wgrad(x: View, dy: View, kh: int, kw: int, dilation: int, dw: torch.Tensor, ws: Workspace,
+                   bias_grad=None, accumulate=False):
+    pt, pl = same_pads(kh, dilation)[0], same_pads(kw, dilation)[0]
+    a = WgradArgs(x.act(), dy.act(), kh, kw, dilation, pt, pl, ctypes.c_void_p(dw.data_ptr()), _ptr(bias_grad),
+                  int(accumulate), None, 0, 0, 0, 0)
+    buf = ws.get(LIB.b2dl_f32_wgrad_workspace_size(ctypes.byref(a)))
+    a.workspace = ctypes.c_void_p(buf.data_ptr())
+    a.workspace_bytes = buf.numel()
+    check(LIB.b2dl_f32_conv_wgrad(ctypes.byref(a), _stream()), "f32_conv_wgrad")
+
+
+def f32_avgpool_fwd(x: View, y: View, k: int):
+    check(LIB.b2dl_f32_avgpool_fwd(x.act(), y.act(), k, _stream()), "f32_avgpool_fwd")
+
+
+def f32_avgpool_bwd(dy: View, dx: View, k: int, accumulate=False, mask: View | None = None):
+    check(LIB.b2dl_f32_avgpool_bwd(dy.act(), dx.act(), k, int(accumulate), _act(mask), _stream()), "f32_avgpool_bwd")
+
+
+def f32_upsample_fwd(x: View, y: View, f: int):
+    check(LIB.b2dl_f32_upsample_fwd(x.act(), y.act(), f, _stream()), "f32_upsample_fwd")
+
+
+def f32_upsample_bwd(dy: View, dx: View, f: int, accumulate=False, mask: View | None = None):
+    check(LIB.b2dl_f32_upsample_bwd(dy.act(), dx.act(), f, int(accumulate), _act(mask), _stream()),
+          "f32_upsample_bwd")
+
+
+def f32_add(x: View, y: View, accumulate=False, mask: View | None = None):
+    check(LIB.b2dl_f32_add(x.act(), y.act(), int(accumulate), _act(mask), _stream()), "f32_add")
+
+
+def f32_relu_mask(g: View, act: View):
+    f32_add(g, g, accumulate=False, mask=act)

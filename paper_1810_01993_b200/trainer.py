@@ -122,7 +122,8 @@ class DataParallelTrainer:
         o = self.optim
         # LARC + momentum update; the same pass writes the bf16 weight mirror the convs read
         nhwc.larc_update(eng.flat_w, eng.flat_m, g, eng.offsets, o.lr, o.momentum, o.trust, o.weight_decay,
-                         o.eps, 1.0 / self.world, self.lr_out, self.status, eng.ws, w_bf16=eng.flat_wbf)
+                         o.eps, 1.0 / self.world, self.lr_out, self.status, eng.ws,
+                         w_bf16=None if eng.fp32 else eng.flat_wbf)
         eng.launches += 3
         eng.repack(mirror=False)
 
@@ -246,6 +247,7 @@ class RunConfig:
     scene: SceneConfig = field(default_factory=SceneConfig)
     class_weighting: str = "inv_sqrt"
     hash_steps: tuple = ()
+    precision: str = "bf16"   # "fp32": the parity mode (b2dl.h group 3)
 
     def __post_init__(self):
         if self.lag not in (0, 1):
@@ -284,7 +286,7 @@ def train_run(cfg: RunConfig, net_cls=None) -> TrainResult:
     rank = dist.get_rank() if dist.is_initialized() else 0
     if net_cls is None:
         net_cls = MiniDenseNet if isinstance(cfg.net, NetConfig) else DeepLabV3Plus
-    net = net_cls(cfg.net, seed=cfg.seed)
+    net = net_cls(cfg.net, seed=cfg.seed, precision=cfg.precision)
     sc = cfg.scene
     shape = (cfg.local_batch, sc.channels, sc.height, sc.width)
     cw = (uniform_weights(cfg.net.classes) if cfg.class_weighting == "uniform"
