@@ -186,7 +186,8 @@ def run_ours(args):
     world, rank, local = _dist_init(args)
     dev = torch.device("cuda", local)
     shape = (LOCAL_BATCH, C, H, W)
-    net = DeepLabV3Plus(DeepLabConfig(), seed=0)
+    variant = getattr(args, "variant", "reference-ops")
+    net = DeepLabV3Plus(DeepLabConfig(batchnorm=variant == "bn-bilinear", bilinear=variant == "bn-bilinear"), seed=0)
     scene = SceneConfig(channels=C, height=H, width=W)
     cw = ClassWeights(scene.frequencies).vector()
     tr = DataParallelTrainer(net, OptimConfig(lr=0.01, momentum=0.9, trust=0.02), shape, class_weights=cw)
@@ -290,7 +291,7 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (GPU-generated scenes, resident in HBM)",
-            "config": _config(world),
+            "config": dict(_config(world), variant=variant) if variant != "reference-ops" else _config(world),
             "sustained_tflops": sust_tf, "flops_per_image": flops_img, "flops_per_image_exact": flops_img_exact,
             "frac_of_peak": sust_tf / peak,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -336,6 +337,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a captured CUDA graph")
+    ap.add_argument("--variant", default="reference-ops", choices=["reference-ops", "bn-bilinear"],
+                    help="model variant: the frozen reference-op DeepLabV3+ (headline) or the north-star one with "
+                         "batch norm after every conv and bilinear decoder upsampling")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -236,6 +236,28 @@ B2DL_API size_t b2dl_larc_workspace_size(int64_t total_elems, int ntensors);
 B2DL_API int b2dl_larc_update(const b2dl_larc_args* a, void* stream);
 
 /* Version / capability string (for smoke checks). */
+/* ---------------------------------------------------------------- batch norm + bilinear
+ * North-star extensions without a reference implementation; float64 oracle in
+ * oracle/deskdl_port.py pinned by finite differences.  f32 != 0: fp32 views, else bf16. */
+/* scratch for b2dl_bn_forward / b2dl_bn_backward on c channels */
+B2DL_API size_t b2dl_bn_workspace_size(int c);
+/* training-mode batch norm over N, H, W (biased variance) fused with an optional residual add and
+ * relu: y = relu?(gamma * (x - mean) * rstd + beta (+ residual)); stats[4][c] receives mean, rstd,
+ * scale = gamma*rstd and shift = beta - mean*scale (the backward reads mean and rstd). */
+B2DL_API int b2dl_bn_forward(b2dl_act x, const float* gamma, const float* beta, float eps, b2dl_act residual,
+                             int relu, b2dl_act y, float* stats, void* workspace, size_t workspace_bytes, int f32,
+                             void* stream);
+/* dgamma (+)= sum gy*xhat, dbeta (+)= sum gy (param_accumulate), and when dx.ptr != NULL
+ * dx (+)= gamma*rstd*(gy - dbeta/M - xhat*dgamma/M) (accumulate); gy already relu-masked. */
+B2DL_API int b2dl_bn_backward(b2dl_act x, b2dl_act gy, const float* gamma, const float* stats, float* dgamma,
+                              float* dbeta, int param_accumulate, b2dl_act dx, int accumulate, void* workspace,
+                              size_t workspace_bytes, int f32, void* stream);
+/* bilinear upsampling by integer factor f (half-pixel centres, align_corners=False) and its VJP
+ * (a deterministic gather; dx (+)= mask(>0) * ...). */
+B2DL_API int b2dl_bilinear_fwd(b2dl_act x, b2dl_act y, int f, int f32, void* stream);
+B2DL_API int b2dl_bilinear_bwd(b2dl_act dy, b2dl_act dx, int f, int accumulate, b2dl_act mask, int f32,
+                               void* stream);
+
 /* ---------------------------------------------------------------- (3) fp32 parity mode
  * The reference's own arithmetic type end to end (north star: loss and gradients within 1e-3 in
  * fp32 mode): every b2dl_act below is NHWC fp32, weights are the fp32 HWIO master, FMA

@@ -47,6 +47,10 @@ def run(graph, params, x, labels, cw, loss_name, emulate):
             out = F.avg_pool2d(ins[0], a["window"])
         elif k == "upsample":
             out = ins[0].repeat_interleave(a["factor"], 2).repeat_interleave(a["factor"], 3)
+        elif k == "upsample_bilinear":
+            out = F.interpolate(ins[0], scale_factor=a["factor"], mode="bilinear", align_corners=False)
+        elif k == "batchnorm":
+            out = F.batch_norm(ins[0], None, None, ins[1], ins[2], training=True, eps=a["eps"])
         elif k == "softmax_ce":
             z = ins[0]
             lab = ins[1]
@@ -58,14 +62,15 @@ def run(graph, params, x, labels, cw, loss_name, emulate):
         else:
             raise AssertionError(k)
         # fused-op boundary = where the GPU stores a bf16 tensor (and its bf16 gradient)
-        boundary = k in ("relu", "avgpool", "upsample") or (
-            k in ("bias_add", "elementwise") and not any(c.kind in ("elementwise", "relu") for c in cons[nd.name])
-            and nd.name != loss_name)
+        boundary = k in ("relu", "avgpool", "upsample", "upsample_bilinear") or (
+            k in ("bias_add", "elementwise", "batchnorm")
+            and not any(c.kind in ("elementwise", "relu") for c in cons[nd.name]) and nd.name != loss_name)
         if emulate and boundary and k != "softmax_ce":
             out = RoundGrad.apply(out)
         vals[nd.name] = out
     loss = vals[loss_name]
     loss.backward()
+    run.last_values = vals
     return float(loss.detach()), {k: v.grad.numpy() for k, v in P.items()}
 
 
@@ -74,3 +79,9 @@ def run(graph, params, x, labels, cw, loss_name, emulate):
 def emulated_grads(graph, params, x, labels, cw, loss_name):
     """(loss, grads) with bf16 storage rounding at the GPU engine's fused-op boundaries."""
     return run(graph, params, x, labels, cw, loss_name, True)
+
+
+def emulated_step(graph, params, x, labels, cw, loss_name, logits_name):
+    """(loss, logits, grads) of the bf16-storage emulation."""
+    loss, grads = run(graph, params, x, labels, cw, loss_name, True)
+    return loss, run.last_values[logits_name].detach().numpy(), grads

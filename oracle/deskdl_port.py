@@ -146,6 +146,65 @@ class Tape:
         self.values, self.caches, self.order = {}, {}, []
 
 
+# ---------------------------------------------------------------- north-star extensions
+# Training-mode batch normalisation and bilinear upsampling have no reference implementation
+# (SURVEY §8(c) "parity unpinned" items); restated here from their definitions and pinned by
+# finite differences in tests/test_oracle.py.
+
+def batchnorm_forward(x, gamma, beta, eps):
+    """y = gamma * (x - mean) / sqrt(var + eps) + beta, batch statistics over N, H, W (biased)."""
+    axes = (0, 2, 3)
+    mean = x.mean(axis=axes, keepdims=True)
+    var = ((x - mean) ** 2).mean(axis=axes, keepdims=True)
+    rstd = 1.0 / np.sqrt(var + eps)
+    xhat = (x - mean) * rstd
+    y = gamma.reshape(1, -1, 1, 1) * xhat + beta.reshape(1, -1, 1, 1)
+    return y.astype(x.dtype), (xhat, rstd)
+
+
+def batchnorm_backward(g, cache, gamma):
+    xhat, rstd = cache
+    axes = (0, 2, 3)
+    m = g.shape[0] * g.shape[2] * g.shape[3]
+    dbeta = g.sum(axis=axes)
+    dgamma = (g * xhat).sum(axis=axes)
+    dx = gamma.reshape(1, -1, 1, 1) * rstd * (g - dbeta.reshape(1, -1, 1, 1) / m
+                                              - xhat * dgamma.reshape(1, -1, 1, 1) / m)
+    return dx.astype(g.dtype), dgamma.astype(g.dtype), dbeta.astype(g.dtype)
+
+
+def _bilinear_taps(n_in, f):
+    """Per output index: (i0, i1, w0, w1) for half-pixel centres, source clamped at 0."""
+    o = np.arange(n_in * f, dtype=np.float64)
+    src = np.maximum((o + 0.5) / f - 0.5, 0.0)
+    i0 = np.floor(src).astype(np.int64)
+    i1 = np.minimum(i0 + 1, n_in - 1)
+    w1 = src - i0
+    return i0, i1, 1.0 - w1, w1
+
+
+def bilinear_upsample(x, f):
+    n, c, h, w = x.shape
+    y0, y1, wy0, wy1 = _bilinear_taps(h, f)
+    x0, x1, wx0, wx1 = _bilinear_taps(w, f)
+    rows = x[:, :, y0, :] * wy0[None, None, :, None] + x[:, :, y1, :] * wy1[None, None, :, None]
+    out = rows[:, :, :, x0] * wx0 + rows[:, :, :, x1] * wx1
+    return out.astype(x.dtype)
+
+
+def bilinear_upsample_backward(g, f, x_shape):
+    n, c, h, w = x_shape
+    y0, y1, wy0, wy1 = _bilinear_taps(h, f)
+    x0, x1, wx0, wx1 = _bilinear_taps(w, f)
+    gr = np.zeros((n, c, g.shape[2], w), dtype=np.float64)
+    np.add.at(gr, (slice(None), slice(None), slice(None), x0), g * wx0)
+    np.add.at(gr, (slice(None), slice(None), slice(None), x1), g * wx1)
+    gx = np.zeros((n, c, h, w), dtype=np.float64)
+    np.add.at(gx, (slice(None), slice(None), y0, slice(None)), gr * wy0[None, None, :, None])
+    np.add.at(gx, (slice(None), slice(None), y1, slice(None)), gr * wy1[None, None, :, None])
+    return gx.astype(g.dtype)
+
+
 def _ancestors(graph, targets):
     want, keep = set(targets), []
     for nd in reversed(graph.nodes):
@@ -179,6 +238,10 @@ def _fwd(nd, ins, relu_mask=None):
     if k == "upsample":
         f = a["factor"]
         return ins[0].repeat(f, axis=2).repeat(f, axis=3), None
+    if k == "batchnorm":
+        return batchnorm_forward(ins[0], ins[1], ins[2], a["eps"])
+    if k == "upsample_bilinear":
+        return bilinear_upsample(ins[0], a["factor"]), None
     if k == "elementwise":
         fn = a["fn"]
         if fn == "add":
@@ -217,6 +280,11 @@ def _bwd(nd, ins, out, cache, g, need):
         f = a["factor"]
         n, c, h, w = g.shape
         return (g.reshape(n, c, h // f, f, w // f, f).sum(axis=(3, 5)) if need[0] else None,)
+    if k == "batchnorm":
+        gx, gg, gb = batchnorm_backward(g, cache, ins[1])
+        return (gx if need[0] else None, gg if need[1] else None, gb if need[2] else None)
+    if k == "upsample_bilinear":
+        return (bilinear_upsample_backward(g, a["factor"], ins[0].shape) if need[0] else None,)
     if k == "elementwise":
         fn = a["fn"]
         if fn == "add":

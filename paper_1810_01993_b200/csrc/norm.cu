@@ -1,0 +1,465 @@
+// Training-mode batch normalisation (+ residual + relu, fused into the normalising pass) and
+// bilinear upsampling, NHWC, bf16 or fp32 storage -- the north-star items the reference lacks
+// (float64 oracle in oracle/deskdl_port.py pinned by finite differences).
+//
+//   forward   stats: per-block partial sums of x and x^2 (fp64, fixed order) -> per-channel
+//             mean / rstd / scale = gamma*rstd / shift = beta - mean*scale;
+//             apply: y = relu?(x*scale + shift (+ residual))
+//   backward  reduce: per-block partial sums of gy and gy*xhat (fp64, fixed order) ->
+//             dbeta, dgamma and dx = gamma*rstd*(gy - dbeta/M - xhat*dgamma/M)
+//   bilinear  half-pixel centres, source clamped at 0 (align_corners=False); the VJP gathers
+//             each input pixel's contributions from the outputs whose taps reach it, so it is
+//             deterministic (no atomics).
+// All passes are HBM streams: 16-byte vectors over channels, pixels split across blocks.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+
+#include "internal.h"
+
+namespace b2 {
+
+// ---- element access: V consecutive channels of type T as floats
+template <typename T, int V>
+struct Vec;
+template <>
+struct Vec<__nv_bfloat16, 8> {
+  static __device__ __forceinline__ void load(const __nv_bfloat16* p, float* v) {
+    const uint4 u = *reinterpret_cast<const uint4*>(p);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      v[2 * e] = __uint_as_float(w[e] << 16);
+      v[2 * e + 1] = __uint_as_float(w[e] & 0xFFFF0000u);
+    }
+  }
+  static __device__ __forceinline__ void store(__nv_bfloat16* p, const float* v) {
+    uint4 u;
+    uint32_t* w = reinterpret_cast<uint32_t*>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+      w[e] = *reinterpret_cast<const uint32_t*>(&h);
+    }
+    *reinterpret_cast<uint4*>(p) = u;
+  }
+};
+template <>
+struct Vec<float, 4> {
+  static __device__ __forceinline__ void load(const float* p, float* v) {
+    const float4 u = *reinterpret_cast<const float4*>(p);
+    v[0] = u.x;
+    v[1] = u.y;
+    v[2] = u.z;
+    v[3] = u.w;
+  }
+  static __device__ __forceinline__ void store(float* p, const float* v) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  }
+};
+template <typename T>
+struct Vec<T, 1> {
+  static __device__ __forceinline__ void load(const T* p, float* v) { v[0] = static_cast<float>(*p); }
+  static __device__ __forceinline__ void store(T* p, const float* v) { *p = static_cast<T>(v[0]); }
+};
+template <>
+struct Vec<__nv_bfloat16, 1> {
+  static __device__ __forceinline__ void load(const __nv_bfloat16* p, float* v) { v[0] = __bfloat162float(*p); }
+  static __device__ __forceinline__ void store(__nv_bfloat16* p, const float* v) { *p = __float2bfloat16_rn(v[0]); }
+};
+
+constexpr int BN_THREADS = 256;
+
+// partial[b][0][c] = sum of a, partial[b][1][c] = sum of a*b' over block b's pixels, where for the
+// forward a = x, b' = x; for the backward a = gy, b' = xhat = (x - mean) * rstd.
+template <typename T, int V, bool BWD>
+__global__ void __launch_bounds__(BN_THREADS) k_bn_reduce(const T* __restrict__ x, int xs, const T* __restrict__ gy,
+                                                          int gs, const float* __restrict__ stats, long long npix,
+                                                          int c, double* __restrict__ part) {
+  extern __shared__ double red[];  // [rows][2][c]
+  const int groups = c / V;
+  const int lanes = groups < BN_THREADS ? groups : BN_THREADS;
+  const int rows = BN_THREADS / lanes;
+  const int row = threadIdx.x / lanes, lane = threadIdx.x - row * lanes;
+  const long long per = (npix + gridDim.x - 1) / gridDim.x;
+  const long long p0 = blockIdx.x * per, p1 = min(npix, p0 + per);
+  for (int g = lane; g < groups; g += lanes) {
+    double s[V], q[V];
+#pragma unroll
+    for (int e = 0; e < V; ++e) s[e] = q[e] = 0.0;
+    float mean[V], rstd[V];
+    if constexpr (BWD) {
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        mean[e] = stats[g * V + e];
+        rstd[e] = stats[c + g * V + e];
+      }
+    }
+    if (threadIdx.x < rows * lanes) {
+      for (long long p = p0 + row; p < p1; p += rows) {
+        float xv[V];
+        Vec<T, V>::load(x + p * xs + g * V, xv);
+        if constexpr (BWD) {
+          float gv[V];
+          Vec<T, V>::load(gy + p * gs + g * V, gv);
+#pragma unroll
+          for (int e = 0; e < V; ++e) {
+            s[e] += gv[e];
+            q[e] += static_cast<double>(gv[e]) * ((xv[e] - mean[e]) * rstd[e]);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < V; ++e) {
+            s[e] += xv[e];
+            q[e] += static_cast<double>(xv[e]) * xv[e];
+          }
+        }
+      }
+    }
+    if (threadIdx.x < rows * lanes) {
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        red[(row * 2 + 0) * c + g * V + e] = s[e];
+        red[(row * 2 + 1) * c + g * V + e] = q[e];
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 2 * c; i += blockDim.x) {
+    const int k = i / c, ch = i - k * c;
+    double t = 0.0;
+    for (int r = 0; r < rows; ++r) t += red[(r * 2 + k) * c + ch];
+    part[(static_cast<long long>(blockIdx.x) * 2 + k) * c + ch] = t;
+  }
+}
+
+// stats [4][c]: mean, rstd, scale, shift
+__global__ void k_bn_finalize(const double* __restrict__ part, int blocks, int c, double m, float eps,
+                              const float* __restrict__ gamma, const float* __restrict__ beta, float* __restrict__ stats) {
+  const int ch = blockIdx.x * blockDim.x + threadIdx.x;
+  if (ch >= c) return;
+  double s = 0.0, q = 0.0;
+  for (int b = 0; b < blocks; ++b) {
+    s += part[(static_cast<long long>(b) * 2) * c + ch];
+    q += part[(static_cast<long long>(b) * 2 + 1) * c + ch];
+  }
+  const double mean = s / m;
+  const double var = fmax(q / m - mean * mean, 0.0);
+  const double rstd = 1.0 / sqrt(var + static_cast<double>(eps));
+  const double scale = static_cast<double>(gamma[ch]) * rstd;
+  stats[ch] = static_cast<float>(mean);
+  stats[c + ch] = static_cast<float>(rstd);
+  stats[2 * c + ch] = static_cast<float>(scale);
+  stats[3 * c + ch] = static_cast<float>(static_cast<double>(beta[ch]) - mean * scale);
+}
+
+// dbeta = sum gy, dgamma = sum gy*xhat; coef [3][c]: gamma*rstd, dbeta/M, dgamma/M
+__global__ void k_bn_bwd_finalize(const double* __restrict__ part, int blocks, int c, double m,
+                                  const float* __restrict__ gamma, const float* __restrict__ stats,
+                                  float* __restrict__ dgamma, float* __restrict__ dbeta, int acc,
+                                  float* __restrict__ coef) {
+  const int ch = blockIdx.x * blockDim.x + threadIdx.x;
+  if (ch >= c) return;
+  double s = 0.0, q = 0.0;
+  for (int b = 0; b < blocks; ++b) {
+    s += part[(static_cast<long long>(b) * 2) * c + ch];
+    q += part[(static_cast<long long>(b) * 2 + 1) * c + ch];
+  }
+  if (dbeta) dbeta[ch] = static_cast<float>(acc ? dbeta[ch] + s : s);
+  if (dgamma) dgamma[ch] = static_cast<float>(acc ? dgamma[ch] + q : q);
+  coef[ch] = gamma[ch] * stats[c + ch];
+  coef[c + ch] = static_cast<float>(s / m);
+  coef[2 * c + ch] = static_cast<float>(q / m);
+}
+
+// forward apply: y = relu?(x*scale + shift (+ res))
+template <typename T, int V>
+__global__ void k_bn_apply(const T* __restrict__ x, int xs, const float* __restrict__ stats, const T* __restrict__ res,
+                           int rs, int relu, T* __restrict__ y, int ys, long long npix, int c) {
+  const int groups = c / V;
+  const long long total = npix * groups;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int g = static_cast<int>(i % groups);
+    const long long p = i / groups;
+    float v[V];
+    Vec<T, V>::load(x + p * xs + g * V, v);
+#pragma unroll
+    for (int e = 0; e < V; ++e) v[e] = v[e] * stats[2 * c + g * V + e] + stats[3 * c + g * V + e];
+    if (res) {
+      float r[V];
+      Vec<T, V>::load(res + p * rs + g * V, r);
+#pragma unroll
+      for (int e = 0; e < V; ++e) v[e] += r[e];
+    }
+    if (relu) {
+#pragma unroll
+      for (int e = 0; e < V; ++e) v[e] = fmaxf(v[e], 0.f);
+    }
+    Vec<T, V>::store(y + p * ys + g * V, v);
+  }
+}
+
+// backward apply: dx (+)= gamma*rstd * (gy - dbeta/M - xhat * dgamma/M)
+template <typename T, int V>
+__global__ void k_bn_bwd_apply(const T* __restrict__ x, int xs, const T* __restrict__ gy, int gs,
+                               const float* __restrict__ stats, const float* __restrict__ coef, T* __restrict__ dx,
+                               int dxs, int acc, long long npix, int c) {
+  const int groups = c / V;
+  const long long total = npix * groups;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int g = static_cast<int>(i % groups);
+    const long long p = i / groups;
+    float xv[V], gv[V], o[V];
+    Vec<T, V>::load(x + p * xs + g * V, xv);
+    Vec<T, V>::load(gy + p * gs + g * V, gv);
+    if (acc) Vec<T, V>::load(dx + p * dxs + g * V, o);
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      const int ch = g * V + e;
+      const float xhat = (xv[e] - stats[ch]) * stats[c + ch];
+      const float d = coef[ch] * (gv[e] - coef[c + ch] - xhat * coef[2 * c + ch]);
+      o[e] = acc ? o[e] + d : d;
+    }
+    Vec<T, V>::store(dx + p * dxs + g * V, o);
+  }
+}
+
+// ---- bilinear (half-pixel centres, clamp at 0), integer factor f
+__device__ __forceinline__ void bl_tap(int o, int n_in, int f, int& i0, int& i1, float& w0, float& w1) {
+  float src = (o + 0.5f) / f - 0.5f;
+  src = src < 0.f ? 0.f : src;
+  i0 = static_cast<int>(src);  // floor (src >= 0)
+  i1 = i0 + 1 < n_in ? i0 + 1 : n_in - 1;
+  w1 = src - i0;
+  w0 = 1.f - w1;
+}
+
+template <typename T, int V>
+__global__ void k_bilinear_fwd(const T* __restrict__ x, int xs, T* __restrict__ y, int ys, int n, int h, int w, int c,
+                               int f) {
+  const int H = h * f, W = w * f, groups = c / V;
+  const long long total = static_cast<long long>(n) * H * W * groups;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int g = static_cast<int>(i % groups);
+    const long long q = i / groups;
+    const int X = static_cast<int>(q % W);
+    const long long r = q / W;
+    const int Y = static_cast<int>(r % H);
+    const long long img = r / H;
+    int y0, y1, x0, x1;
+    float wy0, wy1, wx0, wx1;
+    bl_tap(Y, h, f, y0, y1, wy0, wy1);
+    bl_tap(X, w, f, x0, x1, wx0, wx1);
+    const T* base = x + img * h * w * static_cast<long long>(xs) + g * V;
+    float a[V], b[V], cc[V], d[V], o[V];
+    Vec<T, V>::load(base + (static_cast<long long>(y0) * w + x0) * xs, a);
+    Vec<T, V>::load(base + (static_cast<long long>(y0) * w + x1) * xs, b);
+    Vec<T, V>::load(base + (static_cast<long long>(y1) * w + x0) * xs, cc);
+    Vec<T, V>::load(base + (static_cast<long long>(y1) * w + x1) * xs, d);
+#pragma unroll
+    for (int e = 0; e < V; ++e) o[e] = wy0 * (wx0 * a[e] + wx1 * b[e]) + wy1 * (wx0 * cc[e] + wx1 * d[e]);
+    Vec<T, V>::store(y + q * ys + g * V, o);
+  }
+}
+
+// dx[y][x] (+)= mask * sum over outputs (Y, X) whose taps include (y, x) of weight * dy[Y][X]
+template <typename T, int V>
+__global__ void k_bilinear_bwd(const T* __restrict__ dy, int dys, T* __restrict__ dx, int dxs,
+                               const T* __restrict__ mask, int ms, int n, int h, int w, int c, int f, int acc) {
+  const int H = h * f, W = w * f, groups = c / V;
+  const long long total = static_cast<long long>(n) * h * w * groups;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int g = static_cast<int>(i % groups);
+    const long long q = i / groups;
+    const int xx = static_cast<int>(q % w);
+    const long long r = q / w;
+    const int yy = static_cast<int>(r % h);
+    const long long img = r / h;
+    // outputs whose source coordinate lies in [yy - 1, yy + 1]
+    const int Y0 = max(0, (yy - 1) * f), Y1 = min(H - 1, (yy + 2) * f);
+    const int X0 = max(0, (xx - 1) * f), X1 = min(W - 1, (xx + 2) * f);
+    float s[V];
+#pragma unroll
+    for (int e = 0; e < V; ++e) s[e] = 0.f;
+    for (int Y = Y0; Y <= Y1; ++Y) {
+      int y0, y1;
+      float wy0, wy1;
+      bl_tap(Y, h, f, y0, y1, wy0, wy1);
+      const float wy = (y0 == yy ? wy0 : 0.f) + (y1 == yy ? wy1 : 0.f);
+      if (wy == 0.f) continue;
+      for (int X = X0; X <= X1; ++X) {
+        int x0, x1;
+        float wx0, wx1;
+        bl_tap(X, w, f, x0, x1, wx0, wx1);
+        const float wx = (x0 == xx ? wx0 : 0.f) + (x1 == xx ? wx1 : 0.f);
+        if (wx == 0.f) continue;
+        float v[V];
+        Vec<T, V>::load(dy + ((img * H + Y) * W + X) * dys + g * V, v);
+#pragma unroll
+        for (int e = 0; e < V; ++e) s[e] += wy * wx * v[e];
+      }
+    }
+    if (mask) {
+      float m[V];
+      Vec<T, V>::load(mask + q * ms + g * V, m);
+#pragma unroll
+      for (int e = 0; e < V; ++e)
+        if (!(m[e] > 0.f)) s[e] = 0.f;
+    }
+    if (acc) {
+      float o[V];
+      Vec<T, V>::load(dx + q * dxs + g * V, o);
+#pragma unroll
+      for (int e = 0; e < V; ++e) s[e] += o[e];
+    }
+    Vec<T, V>::store(dx + q * dxs + g * V, s);
+  }
+}
+
+static int bn_blocks() { return 2 * num_sms(); }
+static int grid_of(long long total) {
+  return static_cast<int>(std::max<long long>(1, std::min<long long>((total + 255) / 256, 16LL * num_sms())));
+}
+static bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+static bool vec_act(const b2dl_act& a, int v) { return !a.ptr || (a.c % v == 0 && a.c_stride % v == 0 && al16(a.ptr)); }
+static size_t bn_red_smem(int c, int v) {
+  const int groups = c / v;
+  const int lanes = groups < BN_THREADS ? groups : BN_THREADS;
+  return static_cast<size_t>(BN_THREADS / lanes) * 2 * c * sizeof(double);
+}
+
+// dispatch on (fp32?, vector width)
+#define B2_TV(F32, VEC, ...)                        \
+  do {                                              \
+    if (F32) {                                      \
+      if (VEC) {                                    \
+        using T = float;                            \
+        constexpr int V = 4;                        \
+        __VA_ARGS__;                                \
+      } else {                                      \
+        using T = float;                            \
+        constexpr int V = 1;                        \
+        __VA_ARGS__;                                \
+      }                                             \
+    } else {                                        \
+      if (VEC) {                                    \
+        using T = __nv_bfloat16;                    \
+        constexpr int V = 8;                        \
+        __VA_ARGS__;                                \
+      } else {                                      \
+        using T = __nv_bfloat16;                    \
+        constexpr int V = 1;                        \
+        __VA_ARGS__;                                \
+      }                                             \
+    }                                               \
+  } while (0)
+
+}  // namespace b2
+
+using namespace b2;
+
+extern "C" size_t b2dl_bn_workspace_size(int c) {
+  return static_cast<size_t>(bn_blocks()) * 2 * c * sizeof(double) + 3 * c * sizeof(float) + 256;
+}
+
+extern "C" int b2dl_bn_forward(b2dl_act x, const float* gamma, const float* beta, float eps, b2dl_act residual,
+                               int relu, b2dl_act y, float* stats, void* workspace, size_t workspace_bytes, int f32,
+                               void* stream) {
+  if (!x.ptr || !y.ptr || !gamma || !beta || !stats || x.n != y.n || x.h != y.h || x.w != y.w || x.c != y.c)
+    return B2DL_E_VALUE;
+  if (!workspace || workspace_bytes < b2dl_bn_workspace_size(x.c)) return B2DL_E_VALUE;
+  const int c = x.c;
+  const long long npix = static_cast<long long>(x.n) * x.h * x.w;
+  const int vw = f32 ? 4 : 8;
+  const bool vec = vec_act(x, vw) && vec_act(y, vw) && vec_act(residual, vw);
+  const int blocks = bn_blocks();
+  double* part = reinterpret_cast<double*>(workspace);
+  cudaStream_t st = as_stream(stream);
+  const size_t smem = bn_red_smem(c, vec ? vw : 1);
+  if (smem > 200 * 1024) return B2DL_E_VALUE;
+  B2_TV(f32, vec, {
+    auto kern = k_bn_reduce<T, V, false>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    kern<<<blocks, BN_THREADS, smem, st>>>(reinterpret_cast<const T*>(x.ptr), x.c_stride, nullptr, 0, nullptr,
+                                           npix, c, part);
+  });
+  int rc = check_launch();
+  if (rc) return rc;
+  k_bn_finalize<<<cdiv(c, 128), 128, 0, st>>>(part, blocks, c, static_cast<double>(npix), eps, gamma, beta, stats);
+  if ((rc = check_launch())) return rc;
+  B2_TV(f32, vec, {
+    k_bn_apply<T, V><<<grid_of(npix * (c / V)), 256, 0, st>>>(
+        reinterpret_cast<const T*>(x.ptr), x.c_stride, stats, reinterpret_cast<const T*>(residual.ptr),
+        residual.c_stride, relu, reinterpret_cast<T*>(y.ptr), y.c_stride, npix, c);
+  });
+  return check_launch();
+}
+
+extern "C" int b2dl_bn_backward(b2dl_act x, b2dl_act gy, const float* gamma, const float* stats, float* dgamma,
+                                float* dbeta, int param_accumulate, b2dl_act dx, int accumulate, void* workspace,
+                                size_t workspace_bytes, int f32, void* stream) {
+  if (!x.ptr || !gy.ptr || !gamma || !stats || x.n != gy.n || x.h != gy.h || x.w != gy.w || x.c != gy.c)
+    return B2DL_E_VALUE;
+  if (dx.ptr && (dx.n != x.n || dx.h != x.h || dx.w != x.w || dx.c != x.c)) return B2DL_E_VALUE;
+  if (!workspace || workspace_bytes < b2dl_bn_workspace_size(x.c)) return B2DL_E_VALUE;
+  const int c = x.c;
+  const long long npix = static_cast<long long>(x.n) * x.h * x.w;
+  const int vw = f32 ? 4 : 8;
+  const bool vec = vec_act(x, vw) && vec_act(gy, vw) && vec_act(dx, vw);
+  const int blocks = bn_blocks();
+  double* part = reinterpret_cast<double*>(workspace);
+  float* coef = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) +
+                                         align_up(static_cast<size_t>(blocks) * 2 * c * sizeof(double), 256));
+  cudaStream_t st = as_stream(stream);
+  const size_t smem = bn_red_smem(c, vec ? vw : 1);
+  if (smem > 200 * 1024) return B2DL_E_VALUE;
+  B2_TV(f32, vec, {
+    auto kern = k_bn_reduce<T, V, true>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    kern<<<blocks, BN_THREADS, smem, st>>>(reinterpret_cast<const T*>(x.ptr), x.c_stride,
+                                           reinterpret_cast<const T*>(gy.ptr), gy.c_stride, stats, npix, c, part);
+  });
+  int rc = check_launch();
+  if (rc) return rc;
+  k_bn_bwd_finalize<<<cdiv(c, 128), 128, 0, st>>>(part, blocks, c, static_cast<double>(npix), gamma, stats, dgamma,
+                                                   dbeta, param_accumulate, coef);
+  if ((rc = check_launch()) || !dx.ptr) return rc;
+  B2_TV(f32, vec, {
+    k_bn_bwd_apply<T, V><<<grid_of(npix * (c / V)), 256, 0, st>>>(
+        reinterpret_cast<const T*>(x.ptr), x.c_stride, reinterpret_cast<const T*>(gy.ptr), gy.c_stride, stats, coef,
+        reinterpret_cast<T*>(dx.ptr), dx.c_stride, accumulate, npix, c);
+  });
+  return check_launch();
+}
+
+extern "C" int b2dl_bilinear_fwd(b2dl_act x, b2dl_act y, int f, int f32, void* stream) {
+  if (!x.ptr || !y.ptr || f < 1 || y.h != x.h * f || y.w != x.w * f || y.c != x.c || y.n != x.n) return B2DL_E_VALUE;
+  const int vw = f32 ? 4 : 8;
+  const bool vec = vec_act(x, vw) && vec_act(y, vw);
+  cudaStream_t st = as_stream(stream);
+  B2_TV(f32, vec, {
+    k_bilinear_fwd<T, V><<<grid_of(static_cast<long long>(y.n) * y.h * y.w * (y.c / V)), 256, 0, st>>>(
+        reinterpret_cast<const T*>(x.ptr), x.c_stride, reinterpret_cast<T*>(y.ptr), y.c_stride, x.n, x.h, x.w, x.c,
+        f);
+  });
+  return check_launch();
+}
+
+extern "C" int b2dl_bilinear_bwd(b2dl_act dy, b2dl_act dx, int f, int accumulate, b2dl_act mask, int f32,
+                                 void* stream) {
+  if (!dy.ptr || !dx.ptr || f < 1 || dy.h != dx.h * f || dy.w != dx.w * f || dy.c != dx.c || dy.n != dx.n)
+    return B2DL_E_VALUE;
+  const int vw = f32 ? 4 : 8;
+  const bool vec = vec_act(dy, vw) && vec_act(dx, vw) && vec_act(mask, vw);
+  cudaStream_t st = as_stream(stream);
+  B2_TV(f32, vec, {
+    k_bilinear_bwd<T, V><<<grid_of(static_cast<long long>(dx.n) * dx.h * dx.w * (dx.c / V)), 256, 0, st>>>(
+        reinterpret_cast<const T*>(dy.ptr), dy.c_stride, reinterpret_cast<T*>(dx.ptr), dx.c_stride,
+        reinterpret_cast<const T*>(mask.ptr), mask.c_stride, dx.n, dx.h, dx.w, dx.c, f, accumulate);
+  });
+  return check_launch();
+}

@@ -59,6 +59,9 @@ class Op:
     factor: int = 1
     # concat
     copy_ins: set = field(default_factory=set)
+    # up: "nearest" | "bilinear"; bn: epsilon
+    mode: str = "nearest"
+    eps: float = 1e-5
 
 
 class Plan:
@@ -128,6 +131,35 @@ class Plan:
                         b=bias.inputs[1], res=res, relu=relu, k=a["kh"], dil=a["dilation"], cin=a["cin"],
                         cout=a["cout"])
                 ops.append((idx[cur.name], op))
+            elif nd.kind == "batchnorm":
+                # training-mode batch norm, with a following residual add and relu fused into its
+                # normalising pass (BN-add-relu)
+                chain = [nd]
+                cur = nd
+                res = None
+                relu = False
+                nxt = cons[cur.name]
+                if (len(nxt) == 1 and nxt[0].kind == "elementwise" and nxt[0].attrs["fn"] == "add"
+                        and nxt[0].name not in used):
+                    add = nxt[0]
+                    other = [s_ for s_ in add.inputs if s_ != cur.name]
+                    if len(other) == 1:
+                        res = other[0]
+                        chain.append(add)
+                        cur = add
+                        nxt = cons[cur.name]
+                if len(nxt) == 1 and nxt[0].kind == "relu" and nxt[0].name not in used:
+                    chain.append(nxt[0])
+                    cur = nxt[0]
+                    relu = True
+                used.update(c.name for c in chain)
+                ops.append((idx[cur.name], Op("bn", cur.name, (nd.inputs[0],), tuple(c.name for c in chain),
+                                              w=nd.inputs[1], b=nd.inputs[2], res=res, relu=relu,
+                                              cin=self.shapes[nd.name][1], cout=self.shapes[nd.name][1],
+                                              eps=nd.attrs["eps"])))
+            elif nd.kind == "upsample_bilinear":
+                ops.append((idx[nd.name], Op("up", nd.name, nd.inputs, (nd.name,), factor=nd.attrs["factor"],
+                                             mode="bilinear")))
             elif nd.kind == "avgpool":
                 ops.append((idx[nd.name], Op("pool", nd.name, nd.inputs, (nd.name,), factor=nd.attrs["window"])))
             elif nd.kind == "upsample":
@@ -162,7 +194,8 @@ class Plan:
             off = 0
             for s in op.ins:
                 prod = self.producer.get(s)
-                ok = (s not in owner and prod is not None and prod.kind in ("conv", "pool", "up", "concat", "add")
+                ok = (s not in owner and prod is not None
+                      and prod.kind in ("conv", "bn", "pool", "up", "concat", "add")
                       and s != self.logits_name and off % 8 == 0)
                 if ok:
                     owner[s] = (op.out, off)
@@ -206,7 +239,7 @@ class Plan:
     def _liveness(self):
         live = set(self.params)
         for op in self.ops:
-            if op.kind == "conv":
+            if op.kind in ("conv", "bn"):
                 srcs = [op.ins[0], op.w, op.b] + ([op.res] if op.res else [])
             else:
                 srcs = list(op.ins)
@@ -218,13 +251,13 @@ class Plan:
         #  * identity input x: its pass-through is merged into the next dgrad writing grad(x)
         users = {}
         for op in self.ops:
-            for t in list(op.ins) + ([op.res] if op.kind == "conv" and op.res else []):
+            for t in list(op.ins) + ([op.res] if op.kind in ("conv", "bn") and op.res else []):
                 users.setdefault(t, []).append(op)
         self.grad_alias = {}
         for op in self.ops:
-            if op.kind == "conv" and op.res:
+            if op.kind in ("conv", "bn") and op.res:
                 pr = self.producer.get(op.res)
-                if (pr is not None and pr.kind == "conv" and not pr.relu and users.get(op.res) == [op]
+                if (pr is not None and pr.kind in ("conv", "bn") and not pr.relu and users.get(op.res) == [op]
                         and self.view_of[op.res][0] == op.res):
                     self.grad_alias[op.res] = op.out
         self.grad_buffers = {}
@@ -247,9 +280,9 @@ class Plan:
                 prod = self.producer.get(t)
                 if prod is None or t == self.logits_name:
                     memo[t] = False
-                elif prod.kind == "conv":
+                elif prod.kind in ("conv", "bn"):
                     memo[t] = prod.relu
-                elif prod.kind in ("pool", "up"):
+                elif prod.kind == "pool" or (prod.kind == "up" and prod.mode == "nearest"):
                     memo[t] = maskable(prod.ins[0])
                 elif prod.kind == "concat":
                     memo[t] = all(maskable(x) for x in prod.ins)
@@ -308,6 +341,14 @@ class Plan:
                     if gemm_dgrad and x in pending:
                         step["dx_res"] = pending.pop(x)   # pass-through folded into this dgrad
                     step["dx"] = claim(x, step["mask_dx"])
+                if res is not None and res in self.live and res not in self.grad_alias:
+                    pending[res] = op.out
+                prog.append(step)
+            elif op.kind == "bn":
+                x, res = op.ins[0], op.res
+                step = {"op": op, "dx": None, "relu_pass": op.relu and unmasked_into(op.out)}
+                if x in self.live:
+                    step["dx"] = claim(x, False)     # pre-normalisation conv output: never masked
                 if res is not None and res in self.live and res not in self.grad_alias:
                     pending[res] = op.out
                 prog.append(step)
@@ -373,6 +414,9 @@ class Engine:
         self.flat_m = torch.zeros(off, dtype=f32, device=self.device)
         self.offsets = torch.tensor(offsets, dtype=torch.int64, device=self.device)
         self.convs = [o for o in p.ops if o.kind == "conv"]
+        # per batch-norm op: [4][C] mean, rstd, scale, shift of the current step
+        self.bn_stats = {o.out: torch.zeros(4 * o.cout, dtype=f32, device=self.device)
+                         for o in p.ops if o.kind == "bn"}
         # bf16 mirror of the whole flat parameter buffer, refreshed by the LARC update itself:
         # conv kernels read it directly as their weight operand (HWIO; MN-major for fprop,
         # tap-flipped K-major for dgrad).  Only convs with cout % 8 != 0 (the 3-class head)
@@ -611,6 +655,13 @@ class Engine:
                                 residual=self.v(op.res) if op.res else None, relu=op.relu,
                                 y_f32=(out == p.logits_name))
                 self._toc(ev, op)
+            elif op.kind == "bn":
+                nhwc.bn_forward(self.v(op.ins[0]), self.wslice(op.w), self.wslice(op.b), op.eps, self.v(op.out),
+                                self.bn_stats[op.out], self.ws, residual=self.v(op.res) if op.res else None,
+                                relu=op.relu)
+                self.launches += 2
+            elif op.kind == "up" and op.mode == "bilinear":
+                nhwc.bilinear_fwd(self.v(op.ins[0]), self.v(op.out), op.factor)
             elif op.kind == "pool":
                 (nhwc.f32_avgpool_fwd if self.fp32 else nhwc.avgpool_fwd)(self.v(op.ins[0]), self.v(op.out),
                                                                           op.factor)
@@ -669,8 +720,10 @@ class Engine:
                 for name in (op.w, op.b):
                     i = self.bucket_of[name]
                     pending[i] -= 1
-                    if pending[i] == 0 and on_bucket_ready is not None:
-                        on_bucket_ready(i)
+                    if pending[i] == 0:
+                        self._reduce_bucket(i)
+                        if on_bucket_ready is not None:
+                            on_bucket_ready(i)
                 if st["dx"] is not None:
                     ev = self._tic()
                     nhwc.f32_conv_dgrad(gy, self.wslice(op.w), op.cin, op.k, op.k, op.dil, self.gv(op.ins[0]),
@@ -723,6 +776,29 @@ class Engine:
                     self._toc(ev, op)
                     self.launches += 1
 
+            elif op.kind == "bn":
+                gy = self.gv(op.out)
+                if st["relu_pass"]:
+                    (nhwc.f32_relu_mask if self.fp32 else nhwc.relu_mask)(gy, self.v(op.out))
+                    self.launches += 1
+                g_off, _ = self.slot[op.w]
+                b_off, _ = self.slot[op.b]
+                nhwc.bn_backward(self.v(op.ins[0]), gy, self.wslice(op.w), self.bn_stats[op.out],
+                                 self.flat_g[g_off:g_off + op.cout], self.flat_g[b_off:b_off + op.cout],
+                                 self.gv(op.ins[0]) if st["dx"] is not None else None, self.ws,
+                                 accumulate=bool(st["dx"]))
+                self.launches += 3
+                for name in (op.w, op.b):
+                    i = self.bucket_of[name]
+                    pending[i] -= 1
+                    if pending[i] == 0:
+                        self._reduce_bucket(i)
+                        if on_bucket_ready is not None:
+                            on_bucket_ready(i)
+            elif op.kind == "up" and op.mode == "bilinear":
+                nhwc.bilinear_bwd(self.gv(op.out), self.gv(op.ins[0]), op.factor, accumulate=st["dx"],
+                                  mask=self.v(op.ins[0]) if st["mask"] else None)
+                self.launches += 1
             elif op.kind == "pool":
                 (nhwc.f32_avgpool_bwd if self.fp32 else nhwc.avgpool_bwd)(
                     self.gv(op.out), self.gv(op.ins[0]), op.factor, accumulate=st["dx"],

@@ -72,6 +72,10 @@ class DeepLabConfig:
     decoder_channels: int = 256
     full_res_convs: int = 3
     res_scale: float = 0.1
+    # north-star variant: batch norm after every conv but the head, and
+    # bilinear instead of nearest upsampling in the decoder
+    batchnorm: bool = False
+    bilinear: bool = False
 
     @property
     def downsample_factor(self) -> int:
@@ -107,7 +111,7 @@ class _Builder:
         self.params = {}
         self.conv_meta = {}
 
-    def conv(self, x, name, cin, cout, k=3, dilation=1, act=True, scale=1.0):
+    def conv(self, x, name, cin, cout, k=3, dilation=1, act=True, scale=1.0, bn=False):
         g = self.g
         wname = g.add_input(f"{name}.w", role="param")
         bname = g.add_input(f"{name}.b", role="param")
@@ -120,6 +124,12 @@ class _Builder:
         out = g.conv2d(x, wname, f"{name}.conv", kh=k, kw=k, cin=cin, cout=cout,
                        dilation=dilation)
         out = g.bias_add(out, bname, f"{name}.bias")
+        if bn:   # training-mode batch norm; scale 1, shift 0 at init
+            gname = g.add_input(f"{name}.gamma", role="param")
+            bename = g.add_input(f"{name}.beta", role="param")
+            self.params[gname] = np.ones(cout, dtype=np.float32)
+            self.params[bename] = np.zeros(cout, dtype=np.float32)
+            out = g.batchnorm(out, gname, bename, f"{name}.bn")
         if act:
             out = g.relu(out, f"{name}.relu")
         return out
@@ -173,15 +183,17 @@ def build_deeplab(cfg: DeepLabConfig, seed: int = 0):
     b = _Builder(g, np.random.default_rng(seed))
     x = _io(g)
 
+    bn = cfg.batchnorm
+
     def bottleneck(inp, name, cin, mid, cout, dil):
-        a = b.conv(inp, f"{name}.a", cin, mid, k=1)
-        m = b.conv(a, f"{name}.b", mid, mid, k=3, dilation=dil)
-        c = b.conv(m, f"{name}.c", mid, cout, k=1, act=False, scale=cfg.res_scale)
-        sc = inp if cin == cout else b.conv(inp, f"{name}.proj", cin, cout, k=1, act=False)
+        a = b.conv(inp, f"{name}.a", cin, mid, k=1, bn=bn)
+        m = b.conv(a, f"{name}.b", mid, mid, k=3, dilation=dil, bn=bn)
+        c = b.conv(m, f"{name}.c", mid, cout, k=1, act=False, scale=cfg.res_scale, bn=bn)
+        sc = inp if cin == cout else b.conv(inp, f"{name}.proj", cin, cout, k=1, act=False, bn=bn)
         s = g.elementwise([c, sc], f"{name}.add", fn="add")
         return g.relu(s, f"{name}.relu")
 
-    cur = b.conv(x, "stem", cfg.channels_in, cfg.stem_channels, k=cfg.stem_kernel)
+    cur = b.conv(x, "stem", cfg.channels_in, cfg.stem_channels, k=cfg.stem_kernel, bn=bn)
     cur = g.avgpool(cur, "stem.pool", window=cfg.stem_pool)
     ch = cfg.stem_channels
     low, low_ch = None, None
@@ -196,20 +208,21 @@ def build_deeplab(cfg: DeepLabConfig, seed: int = 0):
         if s == 0:
             low, low_ch = cur, ch
     a = cfg.aspp_channels
-    branches = [b.conv(cur, "aspp.c1x1", ch, a, k=1)]
+    branches = [b.conv(cur, "aspp.c1x1", ch, a, k=1, bn=bn)]
     for d in cfg.aspp_dilations:
-        branches.append(b.conv(cur, f"aspp.d{d}", ch, a, k=3, dilation=d))
+        branches.append(b.conv(cur, f"aspp.d{d}", ch, a, k=3, dilation=d, bn=bn))
     cur = g.concat(branches, "aspp.cat")
-    cur = b.conv(cur, "aspp.proj", a * len(branches), a, k=1)
-    cur = g.upsample(cur, "dec.up", factor=cfg.decoder_up)
-    ll = b.conv(low, "dec.low", low_ch, cfg.lowlevel_channels, k=1)
+    cur = b.conv(cur, "aspp.proj", a * len(branches), a, k=1, bn=bn)
+    up = g.upsample_bilinear if cfg.bilinear else g.upsample
+    cur = up(cur, "dec.up", factor=cfg.decoder_up)
+    ll = b.conv(low, "dec.low", low_ch, cfg.lowlevel_channels, k=1, bn=bn)
     cur = g.concat([cur, ll], "dec.cat")
     dch = cfg.decoder_channels
-    cur = b.conv(cur, "dec.c0", a + cfg.lowlevel_channels, dch, k=3)
-    cur = b.conv(cur, "dec.c1", dch, dch, k=3)
-    cur = g.upsample(cur, "full.up", factor=cfg.stem_pool)
+    cur = b.conv(cur, "dec.c0", a + cfg.lowlevel_channels, dch, k=3, bn=bn)
+    cur = b.conv(cur, "dec.c1", dch, dch, k=3, bn=bn)
+    cur = up(cur, "full.up", factor=cfg.stem_pool)
     for i in range(cfg.full_res_convs):
-        cur = b.conv(cur, f"full.c{i}", dch, dch, k=3)
+        cur = b.conv(cur, f"full.c{i}", dch, dch, k=3, bn=bn)
     head = b.conv(cur, "head", dch, cfg.classes, k=1, act=False)
     loss = g.softmax_ce(head, "labels", "class_weights", "loss", classes=cfg.classes)
     return g, b.params, head, loss

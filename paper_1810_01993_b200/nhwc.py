@@ -305,3 +305,34 @@ def f32_add(x: View, y: View, accumulate=False, mask: View | None = None):
 
 def f32_relu_mask(g: View, act: View):
     f32_add(g, g, accumulate=False, mask=act)
+
+
+# ---------------------------------------------------------------- batch norm + bilinear
+def _is_f32(v: View) -> int:
+    return int(v.buf.dtype == torch.float32)
+
+
+def bn_forward(x: View, gamma: torch.Tensor, beta: torch.Tensor, eps: float, y: View, stats: torch.Tensor,
+               ws: Workspace, residual: View | None = None, relu=False):
+    """Training-mode batch norm (+ residual, relu); stats [4][C] <- mean, rstd, scale, shift."""
+    buf = ws.get(LIB.b2dl_bn_workspace_size(x.c))
+    check(LIB.b2dl_bn_forward(x.act(), _ptr(gamma), _ptr(beta), float(eps), _act(residual), int(relu), y.act(),
+                              _ptr(stats), ctypes.c_void_p(buf.data_ptr()), buf.numel(), _is_f32(x), _stream()),
+          "bn_forward")
+
+
+def bn_backward(x: View, gy: View, gamma: torch.Tensor, stats: torch.Tensor, dgamma, dbeta, dx: View | None,
+                ws: Workspace, accumulate=False, param_accumulate=False):
+    buf = ws.get(LIB.b2dl_bn_workspace_size(x.c))
+    check(LIB.b2dl_bn_backward(x.act(), gy.act(), _ptr(gamma), _ptr(stats), _ptr(dgamma), _ptr(dbeta),
+                               int(param_accumulate), _act(dx), int(accumulate), ctypes.c_void_p(buf.data_ptr()),
+                               buf.numel(), _is_f32(x), _stream()), "bn_backward")
+
+
+def bilinear_fwd(x: View, y: View, f: int):
+    check(LIB.b2dl_bilinear_fwd(x.act(), y.act(), f, _is_f32(x), _stream()), "bilinear_fwd")
+
+
+def bilinear_bwd(dy: View, dx: View, f: int, accumulate=False, mask: View | None = None):
+    check(LIB.b2dl_bilinear_bwd(dy.act(), dx.act(), f, int(accumulate), _act(mask), _is_f32(dy), _stream()),
+          "bilinear_bwd")

@@ -1,0 +1,160 @@
+"""Batch norm (training mode, fused with residual add + relu) and bilinear upsampling -- the
+north-star ops the reference lacks -- against the float64 oracle restatement (pinned by finite
+differences in tests/test_oracle.py), as single kernels and inside a DeepLabV3+ with batch norm
+and bilinear decoder upsampling (bf16 and fp32 modes)."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-30))
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("c,res,relu", [(64, True, True), (24, False, True), (3, False, False), (256, True, False)])
+def test_bn_forward_backward_vs_oracle(dtype, c, res, relu):
+    from oracle import deskdl_port as O
+    from paper_1810_01993_b200 import nhwc
+    rng = np.random.default_rng(c)
+    n, h, w = 2, 12, 20
+    q = lambda a: torch.from_numpy(a.astype(np.float32)).to(dtype)  # noqa: E731
+    x = q(rng.normal(size=(n, h, w, c)) * 1.5 + 0.7)
+    r = q(rng.normal(size=(n, h, w, c)))
+    gy = q(rng.normal(size=(n, h, w, c)))
+    gamma = torch.from_numpy(rng.uniform(0.5, 1.5, c).astype(np.float32))
+    beta = torch.from_numpy(rng.normal(size=c).astype(np.float32))
+    x64, r64, g64 = (t.double().numpy().transpose(0, 3, 1, 2) for t in (x, r, gy))
+    yref, cache = O.batchnorm_forward(x64, gamma.double().numpy(), beta.double().numpy(), 1e-5)
+    pre = yref + (r64 if res else 0)
+    out_ref = np.maximum(pre, 0) if relu else pre
+    gin = g64 * (pre > 0) if relu else g64
+    dx_ref, dg_ref, db_ref = O.batchnorm_backward(gin, cache, gamma.double().numpy())
+    ws = nhwc.Workspace()
+    xd, rd, gyd = x.cuda(), r.cuda(), gy.cuda()
+    y = torch.empty_like(xd)
+    stats = torch.empty(4 * c, device="cuda")
+    gam, bet = gamma.cuda(), beta.cuda()
+    nhwc.bn_forward(nhwc.View(xd), gam, bet, 1e-5, nhwc.View(y), stats, ws,
+                    residual=nhwc.View(rd) if res else None, relu=relu)
+    tol = 1e-2 if dtype == torch.bfloat16 else 1e-4
+    assert rel(y.double().cpu().numpy().transpose(0, 3, 1, 2), out_ref) < tol
+    gmask = gyd.clone()
+    if relu:   # the engine hands the BN backward a relu-masked gradient
+        gmask = torch.where(y > 0, gyd, torch.zeros_like(gyd))
+    dx = torch.empty_like(xd)
+    dg = torch.empty(c, device="cuda")
+    db = torch.empty(c, device="cuda")
+    nhwc.bn_backward(nhwc.View(xd), nhwc.View(gmask), gam, stats, dg, db, nhwc.View(dx), ws)
+    tolg = 2e-2 if dtype == torch.bfloat16 else 1e-3
+    assert rel(dg.cpu().numpy(), dg_ref) < tolg
+    assert rel(db.cpu().numpy(), db_ref) < tolg
+    assert rel(dx.double().cpu().numpy().transpose(0, 3, 1, 2), dx_ref) < tolg
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("f,c", [(2, 32), (4, 256), (4, 5)])
+def test_bilinear_vs_oracle(dtype, f, c):
+    from oracle import deskdl_port as O
+    from paper_1810_01993_b200 import nhwc
+    rng = np.random.default_rng(f * 100 + c)
+    n, h, w = 2, 9, 14
+    x = torch.from_numpy(rng.normal(size=(n, h, w, c)).astype(np.float32)).to(dtype)
+    g = torch.from_numpy(rng.normal(size=(n, h * f, w * f, c)).astype(np.float32)).to(dtype)
+    m = torch.from_numpy(rng.normal(size=(n, h, w, c)).astype(np.float32)).to(dtype)
+    x64 = x.double().numpy().transpose(0, 3, 1, 2)
+    g64 = g.double().numpy().transpose(0, 3, 1, 2)
+    yref = O.bilinear_upsample(x64, f)
+    gxref = O.bilinear_upsample_backward(g64, f, x64.shape) * (m.double().numpy().transpose(0, 3, 1, 2) > 0)
+    y = torch.empty(n, h * f, w * f, c, dtype=dtype, device="cuda")
+    nhwc.bilinear_fwd(nhwc.View(x.cuda()), nhwc.View(y), f)
+    tol = 1e-2 if dtype == torch.bfloat16 else 1e-5
+    assert rel(y.double().cpu().numpy().transpose(0, 3, 1, 2), yref) < tol
+    gx = torch.empty(n, h, w, c, dtype=dtype, device="cuda")
+    nhwc.bilinear_bwd(nhwc.View(g.cuda()), nhwc.View(gx), f, mask=nhwc.View(m.cuda()))
+    assert rel(gx.double().cpu().numpy().transpose(0, 3, 1, 2), gxref) < tol
+
+
+def _bn_net(precision):
+    from paper_1810_01993_b200.models import deeplab_small
+    from paper_1810_01993_b200.net import DeepLabV3Plus
+    return DeepLabV3Plus(deeplab_small(batchnorm=True, bilinear=True), seed=7, precision=precision)
+
+
+def _batch():
+    from paper_1810_01993_b200.scenes import SceneConfig, make_scene, scene_rng
+    xs, ls = [], []
+    for j in range(2):
+        f, lab = make_scene(SceneConfig(channels=16, height=64, width=48), scene_rng(3, 0, j))
+        xs.append(f)
+        ls.append(lab)
+    return np.stack(xs), np.stack(ls)
+
+
+def test_deeplab_batchnorm_bilinear_bf16_vs_oracle():
+    """DeepLabV3+ with batch norm after every conv but the head and bilinear decoder upsampling,
+    bf16 mode: loss within 2e-2; logits and gradients within max(2e-2, 4x the ideal bf16-storage
+    emulation) per tensor (as tests/test_gpu_model.py), median no worse than that emulation."""
+    from oracle import deskdl_port as O
+    from oracle.bf16_emulation import emulated_step
+    net = _bn_net("bf16")
+    x, labels = _batch()
+    cw = O.class_weights((0.982, 0.017, 0.001))
+    p64 = {k: v.astype(np.float64) for k, v in net.params.items()}
+    loss_ref, logits_ref, grads_ref, _ = O.train_step(net.graph, p64, net.param_order, x.astype(np.float64), labels,
+                                                     cw.astype(np.float64), net.loss_name, net.logits_name)
+    _, emu_logits, emu = emulated_step(net.graph, net.params, x, labels, cw, net.loss_name, net.logits_name)
+    loss, logits, tape = net.forward_loss(x, labels, cw)
+    assert abs(loss - loss_ref) < 2e-2 * abs(loss_ref)
+    # batch norm re-amplifies bf16 storage error of low-variance channels: the bar for the logits
+    # is the same max(2e-2, 4 x ideal-bf16-emulation) rule as for the gradients
+    assert rel(logits.cpu().numpy(), logits_ref) < max(2e-2, 4 * rel(emu_logits, logits_ref))
+    grads = net.backward(tape)
+    bad = {}
+    errs, emu_errs = [], []
+    for k in net.param_order:
+        e, ee = rel(grads[k], grads_ref[k]), rel(emu[k], grads_ref[k])
+        if np.max(np.abs(grads_ref[k])) > 1e-10:   # conv biases feeding a batch norm: gradient == 0
+            errs.append(e)
+            emu_errs.append(ee)
+        if e > max(2e-2, 4 * ee):
+            bad[k] = (e, ee)
+    assert not bad, bad
+    # The batch-norm VJP subtracts the channel means of gy and gy*xhat from gy: with gy stored in
+    # bf16 that cancellation leaves even the ideal bf16-storage emulation at 25-65 % max-abs error
+    # per tensor here (fp32 storage: ~5e-4, see the fp32 test).  The GPU must be no worse than it.
+    assert np.median(errs) <= 1.5 * np.median(emu_errs), (np.median(errs), np.median(emu_errs))
+
+
+def test_deeplab_batchnorm_bilinear_fp32_vs_oracle():
+    """Same network in fp32 mode: every gradient within 1e-3 of the float64 oracle (relu decisions
+    matched as in tests/test_gpu_fp32.py)."""
+    from oracle import deskdl_port as O
+    net = _bn_net("fp32")
+    x, labels = _batch()
+    cw = O.class_weights((0.982, 0.017, 0.001))
+    loss, logits, tape = net.forward_loss(x, labels, cw)
+    eng = tape.engine
+    masks = {nd.name: eng.v(nd.name).tensor().float().cpu().numpy().transpose(0, 3, 1, 2) > 0
+             for nd in net.graph.nodes if nd.kind == "relu"}
+    p64 = {k: v.astype(np.float64) for k, v in net.params.items()}
+    loss_ref, logits_ref, grads_ref, _ = O.train_step(net.graph, p64, net.param_order, x.astype(np.float64), labels,
+                                                     cw.astype(np.float64), net.loss_name, net.logits_name,
+                                                     relu_masks=masks)
+    assert abs(loss - loss_ref) < 1e-3 * abs(loss_ref)
+    assert rel(logits.cpu().numpy(), logits_ref) < 1e-3
+    grads = net.backward(tape)
+    scale = max(np.max(np.abs(g)) for g in grads_ref.values())
+    bad = {}
+    for k in net.param_order:
+        if np.max(np.abs(grads_ref[k])) > 1e-10:
+            if rel(grads[k], grads_ref[k]) > 1e-3:
+                bad[k] = rel(grads[k], grads_ref[k])
+        elif np.max(np.abs(grads[k])) > 1e-5 * scale:   # conv bias before a batch norm: ~0
+            bad[k] = float(np.max(np.abs(grads[k])))
+    assert not bad, bad

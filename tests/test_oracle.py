@@ -206,3 +206,48 @@ def test_oracle_dp_trainer_matches_reference_trainer(lag, world, lb):
     assert np.allclose(losses, d[tag + "_losses"], rtol=1e-5, atol=0)
     for k, v in params.items():
         assert rel(v, d[f"{tag}_state:{k}"]) < 1e-4, k
+
+
+# ---- north-star extensions (no reference implementation): pinned by finite differences
+def _fd_check(fn, args, gout, analytic, idx_arg, h=1e-6, n=12, seed=0):
+    rng = np.random.default_rng(seed)
+    a = args[idx_arg]
+    flat = a.reshape(-1)
+    for i in rng.choice(flat.size, size=min(n, flat.size), replace=False):
+        old = flat[i]
+        flat[i] = old + h
+        fp = float((fn(*args) * gout).sum())
+        flat[i] = old - h
+        fm = float((fn(*args) * gout).sum())
+        flat[i] = old
+        num = (fp - fm) / (2 * h)
+        assert abs(num - analytic.reshape(-1)[i]) <= 1e-6 * max(1.0, abs(num)), (idx_arg, i, num)
+
+
+def test_batchnorm_oracle_vjp_matches_finite_differences():
+    from oracle import deskdl_port as O
+    rng = np.random.default_rng(1)
+    x = rng.normal(size=(2, 3, 4, 5)) * 2 + 1
+    gamma, beta = rng.normal(size=3), rng.normal(size=3)
+    g = rng.normal(size=x.shape)
+    y, cache = O.batchnorm_forward(x, gamma, beta, 1e-5)
+    assert np.allclose(y.mean(axis=(0, 2, 3)), beta) and np.allclose(y.std(axis=(0, 2, 3)), np.abs(gamma), rtol=1e-4)
+    gx, gg, gb = O.batchnorm_backward(g, cache, gamma)
+    f = lambda x_, ga, be: O.batchnorm_forward(x_, ga, be, 1e-5)[0]  # noqa: E731
+    _fd_check(f, [x, gamma, beta], g, gx, 0)
+    _fd_check(f, [x, gamma, beta], g, gg, 1, n=3)
+    _fd_check(f, [x, gamma, beta], g, gb, 2, n=3)
+
+
+@pytest.mark.parametrize("f", [2, 4])
+def test_bilinear_oracle_matches_torch_and_finite_differences(f):
+    import torch
+    from oracle import deskdl_port as O
+    rng = np.random.default_rng(2)
+    x = rng.normal(size=(2, 3, 5, 7))
+    y = O.bilinear_upsample(x, f)
+    ref = torch.nn.functional.interpolate(torch.from_numpy(x), scale_factor=f, mode="bilinear", align_corners=False)
+    assert np.allclose(y, ref.numpy(), atol=1e-12)
+    g = rng.normal(size=y.shape)
+    gx = O.bilinear_upsample_backward(g, f, x.shape)
+    _fd_check(lambda x_: O.bilinear_upsample(x_, f), [x], g, gx, 0)
