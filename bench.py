@@ -187,7 +187,15 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     shape = (LOCAL_BATCH, C, H, W)
     variant = getattr(args, "variant", "reference-ops")
-    net = DeepLabV3Plus(DeepLabConfig(batchnorm=variant == "bn-bilinear", bilinear=variant == "bn-bilinear"), seed=0)
+    metric = METRIC
+    if variant == "tiramisu":   # config 4 (the paper's Tiramisu / FC-DenseNet, frozen definition)
+        from paper_1810_01993_b200.models import tiramisu_config4
+        from paper_1810_01993_b200.net import MiniDenseNet
+        net = MiniDenseNet(tiramisu_config4(), seed=0)
+        metric = "Tiramisu (FC-DenseNet, config 4) train images/s & sustained TF/s, 1152×768×16"
+    else:
+        net = DeepLabV3Plus(DeepLabConfig(batchnorm=variant == "bn-bilinear", bilinear=variant == "bn-bilinear"),
+                            seed=0)
     scene = SceneConfig(channels=C, height=H, width=W)
     cw = ClassWeights(scene.frequencies).vector()
     tr = DataParallelTrainer(net, OptimConfig(lr=0.01, momentum=0.9, trust=0.02), shape, class_weights=cw)
@@ -288,10 +296,11 @@ def run_ours(args):
     if rank == 0:
         sust_tf = value * flops_img / 1e12
         line = {
-            "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
+            "metric": metric, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (GPU-generated scenes, resident in HBM)",
-            "config": dict(_config(world), variant=variant) if variant != "reference-ops" else _config(world),
+            "config": (dict(_config(world), variant=variant, model=type(net).__name__)
+                       if variant != "reference-ops" else _config(world)),
             "sustained_tflops": sust_tf, "flops_per_image": flops_img, "flops_per_image_exact": flops_img_exact,
             "frac_of_peak": sust_tf / peak,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -337,9 +346,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a captured CUDA graph")
-    ap.add_argument("--variant", default="reference-ops", choices=["reference-ops", "bn-bilinear"],
-                    help="model variant: the frozen reference-op DeepLabV3+ (headline) or the north-star one with "
-                         "batch norm after every conv and bilinear decoder upsampling")
+    ap.add_argument("--variant", default="reference-ops", choices=["reference-ops", "bn-bilinear", "tiramisu"],
+                    help="model: the frozen reference-op DeepLabV3+ (headline), the north-star DeepLabV3+ with "
+                         "batch norm after every conv and bilinear decoder upsampling, or config 4's Tiramisu")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -517,7 +517,16 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
       ob ^= 1;
       slot ^= 1;
     }
-    if (nv == 0) release(as);
+    if (nv == 0) {
+      release(as);
+      // no chunk of this tile was ours, so nothing chained the next tile's first operands:
+      // issue them now into the still-free slot
+      if (nops && tile + units < p.num_tiles) {
+        int i2, x2, y2, nt2;
+        locate(tile + units, i2, x2, y2, nt2);
+        if (chunks(nt2) > 0) issue(tile + units, 0, slot);
+      }
+    }
   }
   if (leader) bulk_wait<0>();
   __syncwarp();

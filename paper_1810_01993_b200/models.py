@@ -34,20 +34,34 @@ GROWTH_CHOICES = (16, 32)
 
 @dataclass(frozen=True)
 class NetConfig:
-    """MiniDenseNet hyper-parameters (reference net.py:23-41)."""
+    """MiniDenseNet hyper-parameters (reference net.py:23-41).
+
+    Extensions for config 4 (the paper's Tiramisu): `block_layers` may be
+    a tuple with one entry per down level plus the bottleneck (the up path mirrors the down path),
+    and `kernel` sets the dense-layer convolution size (the reference is uniform 3x3)."""
     channels_in: int = 16
     growth: int = 16
-    block_layers: int = 2
+    block_layers: object = 2
     levels: int = 2
     classes: int = 3
+    kernel: int = 3
 
     def __post_init__(self):
         if self.growth not in GROWTH_CHOICES:
             raise ValueError(f"growth must be one of {GROWTH_CHOICES}")
-        if self.channels_in < 1 or self.block_layers < 1 or self.classes < 2:
+        layers = self.block_layers if isinstance(self.block_layers, tuple) else (self.block_layers,)
+        if self.channels_in < 1 or min(layers) < 1 or self.classes < 2 or self.kernel < 1 or self.kernel % 2 == 0:
             raise ValueError("bad network configuration")
         if self.levels < 0:
             raise ValueError("levels must be non-negative")
+        if isinstance(self.block_layers, tuple) and len(self.block_layers) != self.levels + 1:
+            raise ValueError("block_layers tuple needs one entry per level plus the bottleneck")
+
+    def layers_at(self, level: int) -> int:
+        """Dense-block depth at down level `level` (== levels: the bottleneck)."""
+        if isinstance(self.block_layers, tuple):
+            return self.block_layers[level]
+        return self.block_layers
 
     @property
     def downsample_factor(self) -> int:
@@ -142,6 +156,15 @@ def _io(g: OpGraph):
     return x
 
 
+def tiramisu_config4(**kw) -> NetConfig:
+    """Config 4, frozen: the paper's Tiramisu / FC-DenseNet at the reference's op set -- 5
+    resolution levels (4 pooling steps), dense blocks of (2, 2, 2, 4) layers down + 5 in the
+    bottleneck (mirrored up), growth 32, 5x5 dense-layer convs."""
+    base = dict(channels_in=16, growth=32, block_layers=(2, 2, 2, 4, 5), levels=4, kernel=5)
+    base.update(kw)
+    return NetConfig(**base)
+
+
 def build_minidensenet(cfg: NetConfig, seed: int = 0):
     """Graph + params of the reference network (net.py:83-112)."""
     g = OpGraph()
@@ -149,10 +172,10 @@ def build_minidensenet(cfg: NetConfig, seed: int = 0):
     x = _io(g)
     k = cfg.growth
 
-    def dense(inp, name, cin):
+    def dense(inp, name, cin, nlayers):
         feats, ch = inp, cin
-        for j in range(cfg.block_layers):
-            fresh = b.conv(feats, f"{name}.l{j}", ch, k)
+        for j in range(nlayers):
+            fresh = b.conv(feats, f"{name}.l{j}", ch, k, k=cfg.kernel)
             feats = g.concat([feats, fresh], f"{name}.cat{j}")
             ch += k
         return feats, ch
@@ -161,17 +184,17 @@ def build_minidensenet(cfg: NetConfig, seed: int = 0):
     ch = k
     skips = []
     for lvl in range(cfg.levels):
-        cur, ch = dense(cur, f"down{lvl}", ch)
+        cur, ch = dense(cur, f"down{lvl}", ch, cfg.layers_at(lvl))
         skips.append((cur, ch))
         cur = g.avgpool(cur, f"pool{lvl}", window=2)
-    cur, ch = dense(cur, "mid", ch)
+    cur, ch = dense(cur, "mid", ch, cfg.layers_at(cfg.levels))
     for lvl in reversed(range(cfg.levels)):
         skip, sch = skips[lvl]
         cur = g.upsample(cur, f"up{lvl}.grow", factor=2)
         cur = g.concat([cur, skip], f"up{lvl}.cat")
         cur = b.conv(cur, f"up{lvl}.squeeze", ch + sch, sch, k=1)
         ch = sch
-        cur, ch = dense(cur, f"up{lvl}", ch)
+        cur, ch = dense(cur, f"up{lvl}", ch, cfg.layers_at(lvl))
     head = b.conv(cur, "head", ch, cfg.classes, k=1, act=False)
     loss = g.softmax_ce(head, "labels", "class_weights", "loss", classes=cfg.classes)
     return g, b.params, head, loss

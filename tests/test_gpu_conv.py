@@ -243,3 +243,24 @@ def test_atrous_sweep_shapes_vs_oracle(cin, cout, d):
     assert _rel(y.cpu(), y_ref) < 2e-3
     assert _rel(dx.cpu(), dx_ref) < 2e-3
     assert _rel(dw.cpu(), dw_ref) < 2e-3
+
+
+@pytest.mark.parametrize("cout,k", [(320, 1), (864, 1), (352, 3)])
+def test_partial_last_n_tile_many_tiles_per_cta(cout, k):
+    """Output channels that leave whole epilogue sub-groups without a chunk in the last N tile,
+    with several tiles per persistent CTA and a TMA-loaded operand (mask): the operand prefetch
+    chain must skip over tiles a sub-group has no work in (regression: Tiramisu squeeze dgrad)."""
+    from paper_1810_01993_b200 import nhwc
+    torch.manual_seed(9)
+    n, h, w, cin = 2, 96, 96, 64
+    x = torch.randn(n, h, w, cin, device="cuda").to(torch.bfloat16)
+    wm = (torch.randn(k * k, cin, cout, device="cuda") / (k * k * cin) ** 0.5).to(torch.bfloat16)
+    mask = torch.randn(n, h, w, cout, device="cuda").to(torch.bfloat16)
+    y = torch.zeros(n, h, w, cout, dtype=torch.bfloat16, device="cuda")
+    nhwc.conv_fprop(nhwc.View(x), None, cout, k, k, 1, nhwc.View(y), mask=nhwc.View(mask), w_master=wm, w_mode=1)
+    torch.cuda.synchronize()
+    xr = x.double().permute(0, 3, 1, 2)
+    wr = wm.double().reshape(k, k, cin, cout).permute(3, 2, 0, 1)
+    ref = F.conv2d(xr, wr, padding=(k - 1) // 2).permute(0, 2, 3, 1)
+    ref = torch.where(mask.double() > 0, ref, torch.zeros_like(ref))
+    assert _rel(y, ref) < 1e-2
