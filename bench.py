@@ -142,6 +142,28 @@ def _sample_desc():
             f"linearly with pixels, so images/s = {frac:.4f} / step time"), frac
 
 
+KERNEL_OF_PASS = {
+    "fprop": "conv_fprop_kernel, tcgen05 implicit GEMM (CTA pairs for 256-wide N; the row-window halo "
+             "kernel for the stem)",
+    "dgrad": "conv_fprop_kernel over dy with tap-flipped master weights (CTA pairs)",
+    "wgrad": "conv_wgrad_kernel, tcgen05 implicit GEMM, split-K with deferred fixed-order reduction",
+}
+
+
+def _traffic(dom):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
+    (profiles/round1/roofline_traffic.json, written by tools/ncu_summary.py), else None."""
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "round1", "roofline_traffic.json")
+    try:
+        d = json.load(open(p))
+        e = d.get(dom)
+        if e:
+            return float(e["dram_bytes_per_launch"]), f"{os.path.relpath(p)}: {e['launch']}"
+    except (OSError, ValueError, KeyError):
+        pass
+    return None, None
+
+
 def _config(world):
     return {"workload": "config 2/3: DeepLabV3+ (ResNet-50 OS8, ASPP 12/18/24, full-res decoder) "
                         "bf16 train step, fused weighted CE + LARC", "model": "DeepLabV3+",
@@ -249,12 +271,13 @@ def run_ours(args):
     clk.window(t_lo, t_hi)
     launches = eng.launches - launches0
     ms = e0.elapsed_time(e1) / args.steps
-    if graphed:   # conv launches of the last step of the timed region
-        conv_ms, conv_flops = tr.graph_conv_totals()
-        conv_ms, conv_flops = conv_ms * args.steps, conv_flops * args.steps
+    if graphed:   # conv launches of the last step of the timed region (events are graph nodes)
+        per_pass = {k: (m * args.steps, f * args.steps) for k, (m, f) in tr.graph_conv_totals(by_pass=True).items()}
     else:
         eng.conv_timing = False
-        conv_ms, conv_flops = eng.conv_kernel_totals()
+        per_pass = eng.conv_kernel_totals(by_pass=True)
+    conv_ms = sum(m for m, _ in per_pass.values())
+    conv_flops = sum(f for _, f in per_pass.values())
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -292,7 +315,12 @@ def run_ours(args):
                "kind": "port", "sample": desc, "step_s": float(np.median(times))}
 
     peak, peak_sust, hbm, src = _peaks()
-    achieved = conv_flops / (conv_ms / 1e3) / 1e12 if conv_ms > 0 else 0.0
+    achieved_all = conv_flops / (conv_ms / 1e3) / 1e12 if conv_ms > 0 else 0.0
+    # dominant kernel: the conv pass (fprop | dgrad | wgrad launches) with the most device time
+    dom = max(per_pass, key=lambda k: per_pass[k][0]) if per_pass else "fprop"
+    dom_ms, dom_fl = per_pass.get(dom, (0.0, 0))
+    achieved = dom_fl / (dom_ms / 1e3) / 1e12 if dom_ms > 0 else 0.0
+    traffic, traffic_src = _traffic(dom)
     if rank == 0:
         sust_tf = value * flops_img / 1e12
         line = {
@@ -304,10 +332,15 @@ def run_ours(args):
             "sustained_tflops": sust_tf, "flops_per_image": flops_img, "flops_per_image_exact": flops_img_exact,
             "frac_of_peak": sust_tf / peak,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": None,
-                         "kernel": "conv_fprop/conv_wgrad tcgen05 implicit GEMMs (all conv launches of the step)",
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                         "kernel": f"{dom}: {KERNEL_OF_PASS[dom]} (all {dom} launches of the step; algorithmic "
+                                   f"2*k*k*Cin*Cout FLOPs per output pixel / CUDA-event time)",
                          "peak_source": src, "peak_sustained": peak_sust,
-                         "conv_ms_per_step": conv_ms / args.steps},
+                         "per_pass": {k: {"ms_per_step": m / args.steps,
+                                          "tflops": (f / (m / 1e3) / 1e12) if m > 0 else 0.0}
+                                      for k, (m, f) in sorted(per_pass.items())},
+                         "all_convs": {"achieved": achieved_all, "frac": achieved_all / peak,
+                                       "conv_ms_per_step": conv_ms / args.steps}},
             "e2e": {"value": world * LOCAL_BATCH / (e_ms / 1e3), "unit": "images/s",
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 4, "ms_per_step": e_ms},
             "gpu_launches": launches, "cuda_graph": graphed, "clocks": clk.summary(), "cpu_baseline": cpu,

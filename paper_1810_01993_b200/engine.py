@@ -376,6 +376,17 @@ class Plan:
         self.relu_passes = sum(1 for st in prog if st.get("relu_pass"))
 
 
+def conv_event_totals(events, by_pass=False):
+    """Sum (ms, FLOPs) over recorded (start, end, FLOPs, pass) conv events."""
+    if not by_pass:
+        return (sum(a.elapsed_time(b) for a, b, _, _ in events), sum(f for _, _, f, _ in events))
+    out = {}
+    for a, b, f, t in events:
+        ms, fl = out.get(t, (0.0, 0))
+        out[t] = (ms + a.elapsed_time(b), fl + f)
+    return out
+
+
 class Engine:
     """Device state + launches for one model at one input shape."""
 
@@ -531,21 +542,21 @@ class Engine:
         e.record()
         return e
 
-    def _toc(self, ev, op):
+    def _toc(self, ev, op, tag="fprop"):
         if ev is None:
             return
         e = self._event()
         e.record()
         n, _, h, w = self.plan.shapes[op.out]
-        self.conv_events.append((ev, e, 2 * op.k * op.k * op.cin * op.cout * n * h * w))
+        self.conv_events.append((ev, e, 2 * op.k * op.k * op.cin * op.cout * n * h * w, tag))
 
-    def conv_kernel_totals(self):
-        """(ms, algorithmic FLOPs) summed over the timed conv launches (fprop, dgrad, wgrad)."""
+    def conv_kernel_totals(self, by_pass=False):
+        """(ms, algorithmic FLOPs) summed over the timed conv launches (fprop, dgrad, wgrad);
+        by_pass: {pass: (ms, FLOPs)} instead."""
         torch.cuda.synchronize()
-        ms = sum(a.elapsed_time(b) for a, b, _ in self.conv_events)
-        fl = sum(f for _, _, f in self.conv_events)
+        out = conv_event_totals(self.conv_events, by_pass)
         self.conv_events = []
-        return ms, fl
+        return out
 
     # ---------------------------------------------------------------- views
     def v(self, t) -> View:
@@ -715,7 +726,7 @@ class Engine:
                 ev = self._tic()
                 nhwc.f32_conv_wgrad(self.v(op.ins[0]), gy, op.k, op.k, op.dil, self.wslice(op.w, self.flat_g),
                                     self.ws, bias_grad=self.flat_g[b_off:b_off + op.cout])
-                self._toc(ev, op)
+                self._toc(ev, op, "wgrad")
                 self.launches += 3
                 for name in (op.w, op.b):
                     i = self.bucket_of[name]
@@ -729,7 +740,7 @@ class Engine:
                     nhwc.f32_conv_dgrad(gy, self.wslice(op.w), op.cin, op.k, op.k, op.dil, self.gv(op.ins[0]),
                                         accumulate=st["dx"], mask=self.v(op.ins[0]) if st["mask_dx"] else None,
                                         residual=self.gv(st["dx_res"]) if st["dx_res"] else None)
-                    self._toc(ev, op)
+                    self._toc(ev, op, "dgrad")
                     self.launches += 1
             elif op.kind == "conv":
                 gy = self.gv(op.out)
@@ -750,7 +761,7 @@ class Engine:
                     nhwc.conv_wgrad_deferred(View(self.xwin), gy, op.k, 1, 1, self.partials[op.w], window=op.k)
                 else:
                     nhwc.conv_wgrad_deferred(self.v(op.ins[0]), gy, op.k, op.k, op.dil, self.partials[op.w])
-                self._toc(ev, op)
+                self._toc(ev, op, "wgrad")
                 self.launches += 1
                 for name in (op.w, op.b):
                     i = self.bucket_of[name]
@@ -773,7 +784,7 @@ class Engine:
                     nhwc.conv_dgrad(gy, cin=op.cin, kh=op.k, kw=op.k, dilation=op.dil, dx=self.gv(op.ins[0]), **wsrc,
                                     accumulate=st["dx"], mask=self.v(op.ins[0]) if st["mask_dx"] else None,
                                     residual=self.gv(st["dx_res"]) if st["dx_res"] else None)
-                    self._toc(ev, op)
+                    self._toc(ev, op, "dgrad")
                     self.launches += 1
 
             elif op.kind == "bn":

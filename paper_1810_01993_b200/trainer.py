@@ -166,11 +166,12 @@ class DataParallelTrainer:
             return self.eng.loss
         return self._eager_step(x, labels)
 
-    def graph_conv_totals(self):
-        """(ms, FLOPs) of the conv launches of the most recent replay of a timed graph."""
+    def graph_conv_totals(self, by_pass=False):
+        """(ms, FLOPs) of the conv launches of the most recent replay of a timed graph
+        (by_pass: {fprop|dgrad|wgrad: (ms, FLOPs)})."""
+        from .engine import conv_event_totals
         torch.cuda.synchronize()
-        ms = sum(a.elapsed_time(b) for a, b, _ in self.graph_conv_events)
-        return ms, sum(f for _, _, f in self.graph_conv_events)
+        return conv_event_totals(self.graph_conv_events, by_pass)
 
     def _eager_step(self, x: torch.Tensor, labels: torch.Tensor) -> torch.Tensor:
         eng = self.eng
