@@ -595,6 +595,14 @@ class Engine:
     def export_params(self) -> dict:
         return self._export(self.flat_w)
 
+    def import_flat(self, buf, tensors: dict):
+        """Write reference-layout (OIHW) tensors into a flat buffer (params / momentum / grads)."""
+        for name in self.order:
+            a = torch.from_numpy(np.ascontiguousarray(tensors[name], dtype=np.float32))
+            if a.dim() == 4:   # OIHW -> HWIO
+                a = a.permute(2, 3, 1, 0).contiguous()
+            self.wslice(name, buf).copy_(a.reshape(-1).to(self.device))
+
     def export_grads(self) -> dict:
         return self._export(self.flat_g)
 

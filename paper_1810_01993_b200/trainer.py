@@ -209,6 +209,31 @@ class DataParallelTrainer:
             self._apply(self.eng.flat_g)
             self.have_prev = False
 
+    # ------------------------------------------------------------------ run state (resume)
+    def export_state(self) -> dict:
+        """Weights, momentum, the reduced gradient a lag-1 run has yet to apply, and counters
+        (reference-layout NumPy tensors; see checkpoint.save_train_state)."""
+        self._wait_comm()
+        torch.cuda.synchronize()
+        eng = self.eng
+        return {"params": eng.export_params(), "momentum": eng._export(eng.flat_m),
+                "lag_grad": eng._export(eng.flat_g) if (self.lag == 1 and self.have_prev) else None,
+                "steps": self.steps_done, "have_prev": bool(self.lag == 1 and self.have_prev)}
+
+    def import_state(self, st: dict):
+        eng = self.eng
+        self._wait_comm()
+        eng.load_params(st["params"])             # also refreshes the bf16 weight mirror
+        eng.import_flat(eng.flat_m, st["momentum"])
+        if st.get("have_prev"):
+            if self.lag != 1:
+                raise ValueError("state carries a pending lag-1 gradient but the trainer has lag 0")
+            eng.import_flat(eng.flat_g, st["lag_grad"])
+        self.have_prev = bool(st.get("have_prev")) and self.lag == 1
+        self.steps_done = int(st.get("steps", 0))
+        self.net._params = eng.export_params()
+        torch.cuda.synchronize()
+
     def release_graph(self):
         """Drop the captured step graph (it references NCCL communicators: release it before the
         process group is destroyed)."""

@@ -223,7 +223,25 @@ def gen_trainer():
     save("trainer.npz", **out)
 
 
+def gen_checkpoint():
+    """A CKP1 file written by the reference's own save_checkpoint (model/checkpoint.py:18-28)."""
+    from deskdl.model.checkpoint import save_checkpoint
+    rng = np.random.default_rng(11)
+    params = {"conv.w": rng.normal(size=(4, 3, 3, 3)).astype(np.float32),
+              "conv.b": rng.normal(size=(4,)).astype(np.float32),
+              "scalar": np.array(2.5, dtype=np.float32),
+              "µ-unicode/name": rng.normal(size=(2, 5)).astype(np.float32)}
+    save_checkpoint(os.path.join(HERE, "ckp1_reference.bin"), params)
+    save("ckp1_reference_arrays.npz", **{f"a{i}": v for i, v in enumerate(params.values())},
+         names=np.array(list(params.keys())))
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:   # e.g. `make_golden.py gen_checkpoint`: regenerate selected fixtures
+        for fn in sys.argv[1:]:
+            globals()[fn]()
+        sys.exit(0)
+    gen_checkpoint()
     gen_conv()
     gen_loss()
     gen_larc()
