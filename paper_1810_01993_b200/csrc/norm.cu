@@ -133,16 +133,40 @@ __global__ void __launch_bounds__(BN_THREADS) k_bn_reduce(const T* __restrict__ 
   }
 }
 
-// stats [4][c]: mean, rstd, scale, shift
-__global__ void k_bn_finalize(const double* __restrict__ part, int blocks, int c, double m, float eps,
-                              const float* __restrict__ gamma, const float* __restrict__ beta, float* __restrict__ stats) {
-  const int ch = blockIdx.x * blockDim.x + threadIdx.x;
-  if (ch >= c) return;
-  double s = 0.0, q = 0.0;
-  for (int b = 0; b < blocks; ++b) {
-    s += part[(static_cast<long long>(b) * 2) * c + ch];
-    q += part[(static_cast<long long>(b) * 2 + 1) * c + ch];
-  }
+// Sum of the per-block partials of channel ch in a fixed order: FIN_ROWS threads per channel
+// each take every FIN_ROWS-th block, then a fixed-shape tree over the rows (deterministic).
+constexpr int FIN_CH = 32, FIN_ROWS = 8;
+__device__ __forceinline__ void fin_sums(const double* __restrict__ part, int blocks, int c, double* red, double& s,
+                                         double& q) {
+  const int lc = threadIdx.x % FIN_CH, r = threadIdx.x / FIN_CH;
+  const int ch = blockIdx.x * FIN_CH + lc;
+  double a = 0.0, b = 0.0;
+  if (ch < c)
+    for (int k = r; k < blocks; k += FIN_ROWS) {
+      a += part[(static_cast<long long>(k) * 2) * c + ch];
+      b += part[(static_cast<long long>(k) * 2 + 1) * c + ch];
+    }
+  red[(r * 2) * FIN_CH + lc] = a;
+  red[(r * 2 + 1) * FIN_CH + lc] = b;
+  __syncthreads();
+  s = q = 0.0;
+  if (r == 0)
+    for (int k = 0; k < FIN_ROWS; ++k) {
+      s += red[(k * 2) * FIN_CH + lc];
+      q += red[(k * 2 + 1) * FIN_CH + lc];
+    }
+}
+
+// stats [4][c]: mean, rstd, scale = gamma*rstd, shift = beta - mean*scale
+__global__ void __launch_bounds__(FIN_CH * FIN_ROWS) k_bn_finalize(const double* __restrict__ part, int blocks, int c,
+                                                                   double m, float eps, const float* __restrict__ gamma,
+                                                                   const float* __restrict__ beta,
+                                                                   float* __restrict__ stats) {
+  __shared__ double red[FIN_ROWS * 2 * FIN_CH];
+  double s, q;
+  fin_sums(part, blocks, c, red, s, q);
+  const int ch = blockIdx.x * FIN_CH + threadIdx.x;
+  if (threadIdx.x >= FIN_CH || ch >= c) return;
   const double mean = s / m;
   const double var = fmax(q / m - mean * mean, 0.0);
   const double rstd = 1.0 / sqrt(var + static_cast<double>(eps));
@@ -153,76 +177,99 @@ __global__ void k_bn_finalize(const double* __restrict__ part, int blocks, int c
   stats[3 * c + ch] = static_cast<float>(static_cast<double>(beta[ch]) - mean * scale);
 }
 
-// dbeta = sum gy, dgamma = sum gy*xhat; coef [3][c]: gamma*rstd, dbeta/M, dgamma/M
-__global__ void k_bn_bwd_finalize(const double* __restrict__ part, int blocks, int c, double m,
-                                  const float* __restrict__ gamma, const float* __restrict__ stats,
-                                  float* __restrict__ dgamma, float* __restrict__ dbeta, int acc,
-                                  float* __restrict__ coef) {
-  const int ch = blockIdx.x * blockDim.x + threadIdx.x;
-  if (ch >= c) return;
-  double s = 0.0, q = 0.0;
-  for (int b = 0; b < blocks; ++b) {
-    s += part[(static_cast<long long>(b) * 2) * c + ch];
-    q += part[(static_cast<long long>(b) * 2 + 1) * c + ch];
-  }
+// dbeta = sum gy, dgamma = sum gy*xhat.  dx = gamma*rstd*(gy - dbeta/M - xhat*dgamma/M) is
+// folded to dx = A*gy + K1*x + K0 per channel: coef [3][c] = A, K1, K0.
+__global__ void __launch_bounds__(FIN_CH * FIN_ROWS) k_bn_bwd_finalize(
+    const double* __restrict__ part, int blocks, int c, double m, const float* __restrict__ gamma,
+    const float* __restrict__ stats, float* __restrict__ dgamma, float* __restrict__ dbeta, int acc,
+    float* __restrict__ coef) {
+  __shared__ double red[FIN_ROWS * 2 * FIN_CH];
+  double s, q;
+  fin_sums(part, blocks, c, red, s, q);
+  const int ch = blockIdx.x * FIN_CH + threadIdx.x;
+  if (threadIdx.x >= FIN_CH || ch >= c) return;
   if (dbeta) dbeta[ch] = static_cast<float>(acc ? dbeta[ch] + s : s);
   if (dgamma) dgamma[ch] = static_cast<float>(acc ? dgamma[ch] + q : q);
-  coef[ch] = gamma[ch] * stats[c + ch];
-  coef[c + ch] = static_cast<float>(s / m);
-  coef[2 * c + ch] = static_cast<float>(q / m);
+  const double mean = stats[ch], rstd = stats[c + ch];
+  const double A = static_cast<double>(gamma[ch]) * rstd;
+  const double k1 = -A * rstd * q / m;
+  coef[ch] = static_cast<float>(A);
+  coef[c + ch] = static_cast<float>(k1);
+  coef[2 * c + ch] = static_cast<float>(-A * s / m - k1 * mean);
 }
 
-// forward apply: y = relu?(x*scale + shift (+ res))
+// Streams over (pixel, channel group): a thread keeps one channel group and walks pixels, so
+// the per-channel coefficients live in registers.  y = relu?(x*scale + shift (+ res)).
 template <typename T, int V>
-__global__ void k_bn_apply(const T* __restrict__ x, int xs, const float* __restrict__ stats, const T* __restrict__ res,
-                           int rs, int relu, T* __restrict__ y, int ys, long long npix, int c) {
+__global__ void __launch_bounds__(BN_THREADS) k_bn_apply(const T* __restrict__ x, int xs,
+                                                         const float* __restrict__ stats, const T* __restrict__ res,
+                                                         int rs, int relu, T* __restrict__ y, int ys, long long npix,
+                                                         int c) {
   const int groups = c / V;
-  const long long total = npix * groups;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int g = static_cast<int>(i % groups);
-    const long long p = i / groups;
-    float v[V];
-    Vec<T, V>::load(x + p * xs + g * V, v);
+  const int lanes = groups < BN_THREADS ? groups : BN_THREADS;
+  const int rows = BN_THREADS / lanes;
+  const int row = threadIdx.x / lanes, lane = threadIdx.x - row * lanes;
+  if (row >= rows) return;
+  for (int g = lane; g < groups; g += lanes) {
+    float sc[V], sh[V];
 #pragma unroll
-    for (int e = 0; e < V; ++e) v[e] = v[e] * stats[2 * c + g * V + e] + stats[3 * c + g * V + e];
-    if (res) {
-      float r[V];
-      Vec<T, V>::load(res + p * rs + g * V, r);
-#pragma unroll
-      for (int e = 0; e < V; ++e) v[e] += r[e];
+    for (int e = 0; e < V; ++e) {
+      sc[e] = stats[2 * c + g * V + e];
+      sh[e] = stats[3 * c + g * V + e];
     }
-    if (relu) {
+    for (long long p = static_cast<long long>(blockIdx.x) * rows + row; p < npix;
+         p += static_cast<long long>(gridDim.x) * rows) {
+      float v[V];
+      Vec<T, V>::load(x + p * xs + g * V, v);
 #pragma unroll
-      for (int e = 0; e < V; ++e) v[e] = fmaxf(v[e], 0.f);
+      for (int e = 0; e < V; ++e) v[e] = fmaf(v[e], sc[e], sh[e]);
+      if (res) {
+        float r[V];
+        Vec<T, V>::load(res + p * rs + g * V, r);
+#pragma unroll
+        for (int e = 0; e < V; ++e) v[e] += r[e];
+      }
+      if (relu) {
+#pragma unroll
+        for (int e = 0; e < V; ++e) v[e] = fmaxf(v[e], 0.f);
+      }
+      Vec<T, V>::store(y + p * ys + g * V, v);
     }
-    Vec<T, V>::store(y + p * ys + g * V, v);
   }
 }
 
-// backward apply: dx (+)= gamma*rstd * (gy - dbeta/M - xhat * dgamma/M)
+// dx (+)= A*gy + K1*x + K0
 template <typename T, int V>
-__global__ void k_bn_bwd_apply(const T* __restrict__ x, int xs, const T* __restrict__ gy, int gs,
-                               const float* __restrict__ stats, const float* __restrict__ coef, T* __restrict__ dx,
-                               int dxs, int acc, long long npix, int c) {
+__global__ void __launch_bounds__(BN_THREADS) k_bn_bwd_apply(const T* __restrict__ x, int xs, const T* __restrict__ gy,
+                                                             int gs, const float* __restrict__ coef,
+                                                             T* __restrict__ dx, int dxs, int acc, long long npix,
+                                                             int c) {
   const int groups = c / V;
-  const long long total = npix * groups;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int g = static_cast<int>(i % groups);
-    const long long p = i / groups;
-    float xv[V], gv[V], o[V];
-    Vec<T, V>::load(x + p * xs + g * V, xv);
-    Vec<T, V>::load(gy + p * gs + g * V, gv);
-    if (acc) Vec<T, V>::load(dx + p * dxs + g * V, o);
+  const int lanes = groups < BN_THREADS ? groups : BN_THREADS;
+  const int rows = BN_THREADS / lanes;
+  const int row = threadIdx.x / lanes, lane = threadIdx.x - row * lanes;
+  if (row >= rows) return;
+  for (int g = lane; g < groups; g += lanes) {
+    float ca[V], c1[V], c0[V];
 #pragma unroll
     for (int e = 0; e < V; ++e) {
-      const int ch = g * V + e;
-      const float xhat = (xv[e] - stats[ch]) * stats[c + ch];
-      const float d = coef[ch] * (gv[e] - coef[c + ch] - xhat * coef[2 * c + ch]);
-      o[e] = acc ? o[e] + d : d;
+      ca[e] = coef[g * V + e];
+      c1[e] = coef[c + g * V + e];
+      c0[e] = coef[2 * c + g * V + e];
     }
-    Vec<T, V>::store(dx + p * dxs + g * V, o);
+    for (long long p = static_cast<long long>(blockIdx.x) * rows + row; p < npix;
+         p += static_cast<long long>(gridDim.x) * rows) {
+      float xv[V], gv[V], o[V];
+      Vec<T, V>::load(x + p * xs + g * V, xv);
+      Vec<T, V>::load(gy + p * gs + g * V, gv);
+      if (acc) Vec<T, V>::load(dx + p * dxs + g * V, o);
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        const float d = fmaf(ca[e], gv[e], fmaf(c1[e], xv[e], c0[e]));
+        o[e] = acc ? o[e] + d : d;
+      }
+      Vec<T, V>::store(dx + p * dxs + g * V, o);
+    }
   }
 }
 
@@ -321,6 +368,12 @@ __global__ void k_bilinear_bwd(const T* __restrict__ dy, int dys, T* __restrict_
 }
 
 static int bn_blocks() { return 2 * num_sms(); }
+// blocks for the per-thread-channel-group streams: enough rows of pixels to fill the GPU
+static int stream_blocks(long long npix, int groups) {
+  const int lanes = groups < BN_THREADS ? groups : BN_THREADS;
+  const long long rows = BN_THREADS / lanes;
+  return static_cast<int>(std::max<long long>(1, std::min<long long>((npix + rows - 1) / rows, 8LL * num_sms())));
+}
 static int grid_of(long long total) {
   return static_cast<int>(std::max<long long>(1, std::min<long long>((total + 255) / 256, 16LL * num_sms())));
 }
@@ -389,10 +442,11 @@ extern "C" int b2dl_bn_forward(b2dl_act x, const float* gamma, const float* beta
   });
   int rc = check_launch();
   if (rc) return rc;
-  k_bn_finalize<<<cdiv(c, 128), 128, 0, st>>>(part, blocks, c, static_cast<double>(npix), eps, gamma, beta, stats);
+  k_bn_finalize<<<cdiv(c, FIN_CH), FIN_CH * FIN_ROWS, 0, st>>>(part, blocks, c, static_cast<double>(npix), eps, gamma,
+                                                                beta, stats);
   if ((rc = check_launch())) return rc;
   B2_TV(f32, vec, {
-    k_bn_apply<T, V><<<grid_of(npix * (c / V)), 256, 0, st>>>(
+    k_bn_apply<T, V><<<stream_blocks(npix, c / V), BN_THREADS, 0, st>>>(
         reinterpret_cast<const T*>(x.ptr), x.c_stride, stats, reinterpret_cast<const T*>(residual.ptr),
         residual.c_stride, relu, reinterpret_cast<T*>(y.ptr), y.c_stride, npix, c);
   });
@@ -425,12 +479,13 @@ extern "C" int b2dl_bn_backward(b2dl_act x, b2dl_act gy, const float* gamma, con
   });
   int rc = check_launch();
   if (rc) return rc;
-  k_bn_bwd_finalize<<<cdiv(c, 128), 128, 0, st>>>(part, blocks, c, static_cast<double>(npix), gamma, stats, dgamma,
+  k_bn_bwd_finalize<<<cdiv(c, FIN_CH), FIN_CH * FIN_ROWS, 0, st>>>(part, blocks, c, static_cast<double>(npix), gamma,
+                                                                    stats, dgamma,
                                                    dbeta, param_accumulate, coef);
   if ((rc = check_launch()) || !dx.ptr) return rc;
   B2_TV(f32, vec, {
-    k_bn_bwd_apply<T, V><<<grid_of(npix * (c / V)), 256, 0, st>>>(
-        reinterpret_cast<const T*>(x.ptr), x.c_stride, reinterpret_cast<const T*>(gy.ptr), gy.c_stride, stats, coef,
+    k_bn_bwd_apply<T, V><<<stream_blocks(npix, c / V), BN_THREADS, 0, st>>>(
+        reinterpret_cast<const T*>(x.ptr), x.c_stride, reinterpret_cast<const T*>(gy.ptr), gy.c_stride, coef,
         reinterpret_cast<T*>(dx.ptr), dx.c_stride, accumulate, npix, c);
   });
   return check_launch();
