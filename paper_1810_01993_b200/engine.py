@@ -516,17 +516,26 @@ class Engine:
         return View(torch.empty((n, h, w, cs), dtype=torch.bfloat16, device="meta"), off, c)
 
     def set_buckets(self, buckets):
-        """Gradient buckets (lists of parameter names): each gets one batched split-K reduction,
-        launched as soon as backward has produced all of its partials."""
+        """Gradient buckets (lists of parameter names, the all-reduce granularity).  Each conv's
+        split-K partials are reduced right after its wgrad, while they are still in L2 (one small
+        fixed-order launch per conv); a bucket is ready once all of its parameters are."""
         self.buckets = [list(b) for b in buckets]
         self.bucket_of = {n: i for i, b in enumerate(self.buckets) for n in b}
-        self.bucket_tables = []
-        for b in self.buckets:
-            segs = [self.segs[n] for n in b if n in self.segs]
-            if not segs:
-                self.bucket_tables.append(None)
-                continue
-            self.bucket_tables.append((nhwc.segment_table(segs, self.device), len(segs), max(sg[2] for sg in segs)))
+        self.bucket_tables = [None] * len(self.buckets)
+        if not hasattr(self, "conv_tables"):
+            self.conv_tables = {}
+            for o in self.convs:
+                segs = [self.segs[n] for n in (o.w, o.b) if n in self.segs]
+                if segs:
+                    self.conv_tables[o.w] = (nhwc.segment_table(segs, self.device), len(segs),
+                                             max(sg[2] for sg in segs))
+
+    def _reduce_conv(self, op):
+        t = self.conv_tables.get(op.w)
+        if t is not None:
+            table, nseg, max_n = t
+            nhwc.reduce_segments(table, nseg, max_n, self.flat_g)
+            self.launches += 1
 
     # ---------------------------------------------------------------- roofline timing
     def _event(self):
@@ -759,7 +768,7 @@ class Engine:
                 b_off, _ = self.slot[op.b]
                 ev = self._tic()
                 # wgrad GEMM with the bias column sums folded in; split-K partials stay in the
-                # conv's partial buffer until its bucket is reduced in one batched launch
+                # conv's partial buffer and are reduced right after it (fixed order, L2-hot)
                 if op.w in self.heads:
                     dwp, dbp = self.head_parts[op.w]
                     nhwc.head_backward(gy, self.wslice(op.w), self.v(op.ins[0]),
@@ -771,6 +780,7 @@ class Engine:
                     nhwc.conv_wgrad_deferred(self.v(op.ins[0]), gy, op.k, op.k, op.dil, self.partials[op.w])
                 self._toc(ev, op, "wgrad")
                 self.launches += 1
+                self._reduce_conv(op)
                 for name in (op.w, op.b):
                     i = self.bucket_of[name]
                     pending[i] -= 1

@@ -67,7 +67,7 @@ def test_fp32_deeplab_full_config1_matches_oracle():
     At this size a handful of pre-activations sit within fp32 round-off of zero, so *any* two fp32
     implementations (the reference's own fp32 step included) disagree on a few relu decisions, and
     a single flipped pixel moves the max-abs gradient metric of the layers behind it by ~1e-3
-    (tools/fp32_flips.py: 1-2 flips per affected tensor, the same count as the reference's own
+    (tests/diagnostics/fp32_flips.py: 1-2 flips per affected tensor, the same count as the reference's own
     fp32 step against float64).  The oracle is therefore run in float64 with the GPU's relu
     decisions imposed (relu_masks) -- the flips are counted and bounded separately -- and every
     gradient must then agree to 1e-3."""
