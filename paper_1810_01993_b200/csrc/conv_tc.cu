@@ -1949,7 +1949,9 @@ extern "C" int b2dl_wgrad_partials(const b2dl_wgrad_args* a, int* w_parts, int* 
 extern "C" int b2dl_reduce_segments(const b2dl_segment* segs, int nseg, int64_t max_n, float* dst_base,
                                     void* stream) {
   if (!segs || nseg < 1 || !dst_base) return B2DL_E_VALUE;
-  const int bx = static_cast<int>(std::max<long long>(1, std::min<long long>((max_n + 255) / 256, 64)));
+  // fill the GPU (~8 blocks per SM) whether the table holds one conv's two segments or many
+  const long long want = std::max<long long>(1, (8LL * num_sms() + nseg - 1) / nseg);
+  const int bx = static_cast<int>(std::max<long long>(1, std::min<long long>((max_n + 255) / 256, want)));
   dim3 grid(bx, nseg);
   reduce_segments_kernel<<<grid, 256, 0, as_stream(stream)>>>(segs, dst_base);
   return check_launch();
