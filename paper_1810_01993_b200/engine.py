@@ -26,6 +26,8 @@ Every launch goes through libb2dl.so (nhwc.py); torch only allocates memory.
 
 from __future__ import annotations
 
+import contextlib
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -506,6 +508,9 @@ class Engine:
         self.input_shape = tuple(input_shape)
         self.launches = 0
         self.conv_timing = False
+        # side stream for wgrad || dgrad overlap (B2DL_CONCURRENT=0 serialises them)
+        self.side = (torch.cuda.Stream(device=self.device)
+                     if os.environ.get("B2DL_CONCURRENT", "1") != "0" and self.device.type == "cuda" else None)
         self.conv_events = []
         self.load_params(params)
 
@@ -658,64 +663,106 @@ class Engine:
 
     # ---------------------------------------------------------------- forward
     def forward(self):
+        """Fused forward program.  Runs of convs reading the same input (the ASPP branches) are
+        spread over the main and side streams so their tail waves overlap."""
+        forks, side_ops, joins = self._side_runs()
+        for idx, op in enumerate(self.plan.ops):
+            if idx in forks:
+                ev = torch.cuda.Event()
+                ev.record()
+                self.side.wait_event(ev)
+            if idx in side_ops:
+                with torch.cuda.stream(self.side):
+                    self._fwd_op(op)
+            else:
+                self._fwd_op(op)
+            if idx in joins:   # end of the run: the main stream waits for the side stream's ops
+                ev = torch.cuda.Event()
+                ev.record(self.side)
+                torch.cuda.current_stream().wait_event(ev)
+
+    def _side_runs(self):
+        """(fork indices, side-stream op indices, join indices): runs of >= 2 consecutive bf16
+        convs with the same input and no residual operand (outputs are distinct buffers or concat
+        slices) alternate between the main and the side stream."""
+        if getattr(self, "_runs", None) is not None:
+            return self._runs
+        forks, side, joins = set(), set(), set()
+        ops = self.plan.ops
+        if self.side is not None and not self.fp32:
+            i = 0
+            while i < len(ops):
+                j = i
+                while (j + 1 < len(ops) and ops[i].kind == "conv" and ops[j + 1].kind == "conv"
+                       and ops[j + 1].ins[0] == ops[i].ins[0] and not ops[i].res and not ops[j + 1].res
+                       and ops[i] is not self.win):
+                    j += 1
+                if j > i:
+                    forks.add(i)
+                    side.update(k for k in range(i, j + 1) if (k - i) % 2 == 1)
+                    joins.add(j)
+                i = j + 1
+        self._runs = (forks, side, joins)
+        return self._runs
+
+    def _fwd_op(self, op):
         p = self.plan
-        for op in p.ops:
-            if op.kind == "conv" and self.fp32:
-                b_off, _ = self.slot[op.b]
-                ev = self._tic()
-                nhwc.f32_conv(self.v(op.ins[0]), self.wslice(op.w), op.cout, op.k, op.k, op.dil, self.v(op.out),
-                              bias=self.flat_w[b_off:b_off + op.cout],
-                              residual=self.v(op.res) if op.res else None, relu=op.relu)
-                self._toc(ev, op)
-            elif op.kind == "conv":
-                out = op.out
-                b_off, _ = self.slot[op.b]
-                ev = self._tic()
-                wsrc = dict(w_packed=self.wf[op.w]) if op.w in self.wf else dict(
-                    w_packed=None, w_master=self.wmaster(op.w), w_mode=1)
-                xin, kw = self.v(op.ins[0]), op.k
-                if op is self.win:
-                    wsrc = dict(w_packed=self.wwin, window=op.k)
-                    xin, kw = View(self.xwin), 1
-                nhwc.conv_fprop(xin, cout=op.cout, kh=op.k, kw=kw, dilation=op.dil, y=self.v(out),
-                                **wsrc,
-                                bias=self.flat_w[b_off:b_off + op.cout],
-                                residual=self.v(op.res) if op.res else None, relu=op.relu,
-                                y_f32=(out == p.logits_name))
-                self._toc(ev, op)
-            elif op.kind == "bn":
-                nhwc.bn_forward(self.v(op.ins[0]), self.wslice(op.w), self.wslice(op.b), op.eps, self.v(op.out),
-                                self.bn_stats[op.out], self.ws, residual=self.v(op.res) if op.res else None,
-                                relu=op.relu)
-                self.launches += 2
-            elif op.kind == "up" and op.mode == "bilinear":
-                nhwc.bilinear_fwd(self.v(op.ins[0]), self.v(op.out), op.factor)
-            elif op.kind == "pool":
-                (nhwc.f32_avgpool_fwd if self.fp32 else nhwc.avgpool_fwd)(self.v(op.ins[0]), self.v(op.out),
-                                                                          op.factor)
-            elif op.kind == "up":
-                (nhwc.f32_upsample_fwd if self.fp32 else nhwc.upsample_fwd)(self.v(op.ins[0]), self.v(op.out),
-                                                                            op.factor)
-            elif op.kind == "concat":
-                off = 0
-                for s in op.ins:
-                    if s in op.copy_ins:
-                        root, coff, c = p.view_spec(op.out)
-                        self._add(self.v(s), View(self.act[root], coff + off, self.plan.chans(s)),
-                                  accumulate=False)
-                        self.launches += 1
-                    off += self.plan.chans(s)
-                continue
-            elif op.kind == "add":
-                a, b = op.ins
-                self._add(self.v(a), self.v(op.out), accumulate=False)
-                self._add(self.v(b), self.v(op.out), accumulate=True)
-                self.launches += 1
-            elif op.kind == "ce":
-                nhwc.wce(self.v(op.ins[0]), self.labels, self.class_weights, self.loss, self.counts,
-                         self.gv(op.ins[0]), self.pred, self.ws, dlogits_f32=self.fp32)
-                self.launches += 2   # histogram + loss/dlogits + final fold (3 with the +1 below)
+        if op.kind == "conv" and self.fp32:
+            b_off, _ = self.slot[op.b]
+            ev = self._tic()
+            nhwc.f32_conv(self.v(op.ins[0]), self.wslice(op.w), op.cout, op.k, op.k, op.dil, self.v(op.out),
+                          bias=self.flat_w[b_off:b_off + op.cout],
+                          residual=self.v(op.res) if op.res else None, relu=op.relu)
+            self._toc(ev, op)
+        elif op.kind == "conv":
+            out = op.out
+            b_off, _ = self.slot[op.b]
+            ev = self._tic()
+            wsrc = dict(w_packed=self.wf[op.w]) if op.w in self.wf else dict(
+                w_packed=None, w_master=self.wmaster(op.w), w_mode=1)
+            xin, kw = self.v(op.ins[0]), op.k
+            if op is self.win:
+                wsrc = dict(w_packed=self.wwin, window=op.k)
+                xin, kw = View(self.xwin), 1
+            nhwc.conv_fprop(xin, cout=op.cout, kh=op.k, kw=kw, dilation=op.dil, y=self.v(out),
+                            **wsrc,
+                            bias=self.flat_w[b_off:b_off + op.cout],
+                            residual=self.v(op.res) if op.res else None, relu=op.relu,
+                            y_f32=(out == p.logits_name))
+            self._toc(ev, op)
+        elif op.kind == "bn":
+            nhwc.bn_forward(self.v(op.ins[0]), self.wslice(op.w), self.wslice(op.b), op.eps, self.v(op.out),
+                            self.bn_stats[op.out], self.ws, residual=self.v(op.res) if op.res else None,
+                            relu=op.relu)
+            self.launches += 2
+        elif op.kind == "up" and op.mode == "bilinear":
+            nhwc.bilinear_fwd(self.v(op.ins[0]), self.v(op.out), op.factor)
+        elif op.kind == "pool":
+            (nhwc.f32_avgpool_fwd if self.fp32 else nhwc.avgpool_fwd)(self.v(op.ins[0]), self.v(op.out),
+                                                                      op.factor)
+        elif op.kind == "up":
+            (nhwc.f32_upsample_fwd if self.fp32 else nhwc.upsample_fwd)(self.v(op.ins[0]), self.v(op.out),
+                                                                        op.factor)
+        elif op.kind == "concat":
+            off = 0
+            for s in op.ins:
+                if s in op.copy_ins:
+                    root, coff, c = p.view_spec(op.out)
+                    self._add(self.v(s), View(self.act[root], coff + off, self.plan.chans(s)),
+                              accumulate=False)
+                    self.launches += 1
+                off += self.plan.chans(s)
+            return
+        elif op.kind == "add":
+            a, b = op.ins
+            self._add(self.v(a), self.v(op.out), accumulate=False)
+            self._add(self.v(b), self.v(op.out), accumulate=True)
             self.launches += 1
+        elif op.kind == "ce":
+            nhwc.wce(self.v(op.ins[0]), self.labels, self.class_weights, self.loss, self.counts,
+                     self.gv(op.ins[0]), self.pred, self.ws, dlogits_f32=self.fp32)
+            self.launches += 2   # histogram + loss/dlogits + final fold (3 with the +1 below)
+        self.launches += 1
 
     # ---------------------------------------------------------------- backward
     def _reduce_bucket(self, i):
@@ -764,30 +811,42 @@ class Engine:
                 if st["relu_pass"]:
                     nhwc.relu_mask(gy, self.v(op.out))
                     self.launches += 1
-                w_off, _ = self.slot[op.w]
-                b_off, _ = self.slot[op.b]
-                ev = self._tic()
-                # wgrad GEMM with the bias column sums folded in; split-K partials stay in the
-                # conv's partial buffer and are reduced right after it (fixed order, L2-hot)
-                if op.w in self.heads:
-                    dwp, dbp = self.head_parts[op.w]
-                    nhwc.head_backward(gy, self.wslice(op.w), self.v(op.ins[0]),
-                                       self.gv(op.ins[0]) if st["dx"] is not None else None, dwp, dbp,
-                                       accumulate=bool(st["dx"]), mask_dx=bool(st["mask_dx"]))
-                elif op is self.win:
-                    nhwc.conv_wgrad_deferred(View(self.xwin), gy, op.k, 1, 1, self.partials[op.w], window=op.k)
-                else:
-                    nhwc.conv_wgrad_deferred(self.v(op.ins[0]), gy, op.k, op.k, op.dil, self.partials[op.w])
-                self._toc(ev, op, "wgrad")
-                self.launches += 1
-                self._reduce_conv(op)
-                for name in (op.w, op.b):
-                    i = self.bucket_of[name]
-                    pending[i] -= 1
-                    if pending[i] == 0:
-                        self._reduce_bucket(i)
-                        if on_bucket_ready is not None:
-                            on_bucket_ready(i)
+                # wgrad and dgrad of a conv are independent (both only read dy): the wgrad (+ its
+                # split-K reduction and the bucket's all-reduce start) runs on a side stream so the
+                # two persistent kernels fill each other's tail waves; they join before the next op
+                gemm_dgrad = (st["dx"] is not None and op.w not in self.heads and not (op.k == 1 and op.cout < 8))
+                side = self.side if (gemm_dgrad and self.side is not None) else None
+                if side is not None:
+                    fork = torch.cuda.Event()
+                    fork.record()
+                    side.wait_event(fork)
+                with (torch.cuda.stream(side) if side is not None else contextlib.nullcontext()):
+                    ev = self._tic()
+                    # wgrad GEMM with the bias column sums folded in; split-K partials stay in the
+                    # conv's partial buffer and are reduced right after it (fixed order, L2-hot)
+                    if op.w in self.heads:
+                        dwp, dbp = self.head_parts[op.w]
+                        nhwc.head_backward(gy, self.wslice(op.w), self.v(op.ins[0]),
+                                           self.gv(op.ins[0]) if st["dx"] is not None else None, dwp, dbp,
+                                           accumulate=bool(st["dx"]), mask_dx=bool(st["mask_dx"]))
+                    elif op is self.win:
+                        nhwc.conv_wgrad_deferred(View(self.xwin), gy, op.k, 1, 1, self.partials[op.w],
+                                                 window=op.k)
+                    else:
+                        nhwc.conv_wgrad_deferred(self.v(op.ins[0]), gy, op.k, op.k, op.dil, self.partials[op.w])
+                    self._toc(ev, op, "wgrad")
+                    self.launches += 1
+                    self._reduce_conv(op)
+                    for name in (op.w, op.b):
+                        i = self.bucket_of[name]
+                        pending[i] -= 1
+                        if pending[i] == 0:
+                            self._reduce_bucket(i)
+                            if on_bucket_ready is not None:
+                                on_bucket_ready(i)
+                    if side is not None:
+                        join = torch.cuda.Event()
+                        join.record()
                 if op.w in self.heads:
                     pass   # input gradient already produced by head_backward
                 elif st["dx"] is not None and op.k == 1 and op.cout < 8:
@@ -804,6 +863,8 @@ class Engine:
                                     residual=self.gv(st["dx_res"]) if st["dx_res"] else None)
                     self._toc(ev, op, "dgrad")
                     self.launches += 1
+                if side is not None:
+                    torch.cuda.current_stream().wait_event(join)
 
             elif op.kind == "bn":
                 gy = self.gv(op.out)
