@@ -127,29 +127,44 @@ class DataParallelTrainer:
         eng.launches += 3
         eng.repack(mirror=False)
 
-    def capture(self, x: torch.Tensor, labels: torch.Tensor, timed: bool = False):
+    def capture(self, x: torch.Tensor, labels: torch.Tensor, timed: bool = False, buffers: int = 1):
         """Record one whole training step (every launch, and on N GPUs the bucket all-reduces)
         into a CUDA graph over static input buffers; later `step` calls copy the batch in and
         replay it.  `timed` adds graph event nodes around every conv launch (roofline timing).
+        `buffers` = 2 records a second graph over a second input buffer pair, so `stage` can
+        copy the next batch from the host while the current step runs (`step_staged`).
         Call after at least one eager step (workspaces sized)."""
         if self.lag != 0:
             raise NotImplementedError("graph capture supports lag 0")
         eng = self.eng
-        self.static_x = torch.empty_like(x)
-        self.static_l = torch.empty_like(labels)
-        self.static_x.copy_(x)
-        self.static_l.copy_(labels)
+        self.static_xs = [torch.empty_like(x) for _ in range(buffers)]
+        self.static_ls = [torch.empty_like(labels) for _ in range(buffers)]
+        for sx, sl in zip(self.static_xs, self.static_ls):
+            sx.copy_(x)
+            sl.copy_(labels)
+        self.static_x, self.static_l = self.static_xs[0], self.static_ls[0]
         torch.cuda.synchronize()
-        graph = torch.cuda.CUDAGraph()
-        launches0 = eng.launches
-        eng.conv_timing, eng.conv_events, eng.graph_events = timed, [], timed
-        with torch.cuda.graph(graph):
-            self._eager_step(self.static_x, self.static_l)
-        eng.graph_events = False
-        self.graph_conv_events = eng.conv_events if timed else []
-        eng.conv_timing, eng.conv_events = False, []
-        self.graph_launches = eng.launches - launches0
-        self.graph = graph
+        self.graphs = []
+        for k in range(buffers):
+            graph = torch.cuda.CUDAGraph()
+            launches0 = eng.launches
+            t = timed and k == 0
+            eng.conv_timing, eng.conv_events, eng.graph_events = t, [], t
+            with torch.cuda.graph(graph):
+                self._eager_step(self.static_xs[k], self.static_ls[k])
+            eng.graph_events = False
+            if k == 0:
+                self.graph_conv_events = eng.conv_events if t else []
+                self.graph_launches = eng.launches - launches0
+            eng.conv_timing, eng.conv_events = False, []
+            self.graphs.append(graph)
+        self.graph = self.graphs[0]
+        self.copy_stream = torch.cuda.Stream(device=eng.device)
+        self._ready = [torch.cuda.Event() for _ in range(buffers)]
+        self._consumed = [torch.cuda.Event() for _ in range(buffers)]
+        for e in self._consumed:
+            e.record()
+        self._stage_k, self._staged = 0, []
         torch.cuda.synchronize()
 
     def step(self, x: torch.Tensor, labels: torch.Tensor) -> torch.Tensor:
@@ -161,10 +176,34 @@ class DataParallelTrainer:
             if labels.data_ptr() != self.static_l.data_ptr():
                 self.static_l.copy_(labels, non_blocking=True)
             g.replay()
+            self._consumed[0].record()
             self.eng.launches += self.graph_launches
             self.steps_done += 1
             return self.eng.loss
         return self._eager_step(x, labels)
+
+    def stage(self, hx: torch.Tensor, hl: torch.Tensor):
+        """Asynchronously copy a host batch (pinned) into the next free input buffer on a copy
+        stream -- it overlaps the step that is running (needs capture(buffers=2))."""
+        k = self._stage_k
+        cs = self.copy_stream
+        cs.wait_event(self._consumed[k])          # that buffer's previous step has read it
+        with torch.cuda.stream(cs):
+            self.static_xs[k].copy_(hx, non_blocking=True)
+            self.static_ls[k].copy_(hl, non_blocking=True)
+            self._ready[k].record()
+        self._staged.append(k)
+        self._stage_k = (k + 1) % len(self.graphs)
+
+    def step_staged(self) -> torch.Tensor:
+        """Run the training step on the oldest staged batch; returns the device loss."""
+        k = self._staged.pop(0)
+        torch.cuda.current_stream().wait_event(self._ready[k])
+        self.graphs[k].replay()
+        self._consumed[k].record()
+        self.eng.launches += self.graph_launches
+        self.steps_done += 1
+        return self.eng.loss
 
     def graph_conv_totals(self, by_pass=False):
         """(ms, FLOPs) of the conv launches of the most recent replay of a timed graph
@@ -239,8 +278,9 @@ class DataParallelTrainer:
         process group is destroyed)."""
         if getattr(self, "graph", None) is not None:
             torch.cuda.synchronize()
-            self.graph.reset()
-            self.graph = None
+            for g in self.graphs:
+                g.reset()
+            self.graph, self.graphs = None, []
 
     def check_status(self):
         if int(self.status.item()):
