@@ -844,9 +844,6 @@ class Engine:
                             self._reduce_bucket(i)
                             if on_bucket_ready is not None:
                                 on_bucket_ready(i)
-                    if side is not None:
-                        join = torch.cuda.Event()
-                        join.record()
                 if op.w in self.heads:
                     pass   # input gradient already produced by head_backward
                 elif st["dx"] is not None and op.k == 1 and op.cout < 8:
@@ -863,8 +860,9 @@ class Engine:
                                     residual=self.gv(st["dx_res"]) if st["dx_res"] else None)
                     self._toc(ev, op, "dgrad")
                     self.launches += 1
-                if side is not None:
-                    torch.cuda.current_stream().wait_event(join)
+                # no per-layer join: gradient buffers are never reused within a step (one per
+                # activation root) and backward never writes grad(op.out) again, so the side
+                # stream's wgrads may trail the main stream's dgrads; they join at the end
 
             elif op.kind == "bn":
                 gy = self.gv(op.out)
@@ -910,6 +908,10 @@ class Engine:
                 for s, acc, m in st["acc"]:
                     self._add(self.gv(src), self.gv(s), accumulate=acc, mask=self.v(s) if m else None)
                     self.launches += 1
+        if self.side is not None and not self.fp32:   # all wgrads (and their reductions) done
+            ev = torch.cuda.Event()
+            ev.record(self.side)
+            torch.cuda.current_stream().wait_event(ev)
 
     def _add(self, x, y, accumulate=False, mask=None):
         (nhwc.f32_add if self.fp32 else nhwc.add)(x, y, accumulate=accumulate, mask=mask)
