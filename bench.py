@@ -220,7 +220,9 @@ def run_ours(args):
                             seed=0)
     scene = SceneConfig(channels=C, height=H, width=W)
     cw = ClassWeights(scene.frequencies).vector()
-    tr = DataParallelTrainer(net, OptimConfig(lr=0.01, momentum=0.9, trust=0.02), shape, class_weights=cw)
+    hier = tuple(int(v) for v in args.hierarchy.split("x")) if getattr(args, "hierarchy", "") else None
+    tr = DataParallelTrainer(net, OptimConfig(lr=0.01, momentum=0.9, trust=0.02), shape, class_weights=cw,
+                             hierarchy=hier)
     eng = tr.eng
     # synthetic pool, resident in HBM, different tiles per rank
     pool = 4
@@ -337,8 +339,9 @@ def run_ours(args):
             "metric": metric, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (GPU-generated scenes, resident in HBM)",
-            "config": (dict(_config(world), variant=variant, model=type(net).__name__)
-                       if variant != "reference-ops" else _config(world)),
+            "config": dict((dict(_config(world), variant=variant, model=type(net).__name__)
+                            if variant != "reference-ops" else _config(world)),
+                           **({"allreduce": f"hierarchical {args.hierarchy}"} if hier else {})),
             "sustained_tflops": sust_tf, "flops_per_image": flops_img, "flops_per_image_exact": flops_img_exact,
             "frac_of_peak": sust_tf / peak,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -389,6 +392,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a captured CUDA graph")
+    ap.add_argument("--hierarchy", default="", help="GxL: three-stage hierarchical all-reduce over G groups of L "
+                                                     "ranks (the paper's scheme) instead of one flat NCCL all-reduce")
     ap.add_argument("--variant", default="reference-ops", choices=["reference-ops", "bn-bilinear", "tiramisu"],
                     help="model: the frozen reference-op DeepLabV3+ (headline), the north-star DeepLabV3+ with "
                          "batch norm after every conv and bilinear decoder upsampling, or config 4's Tiramisu")

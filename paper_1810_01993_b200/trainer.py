@@ -54,7 +54,12 @@ def param_digest(params: dict, order) -> str:
 
 class DataParallelTrainer:
     def __init__(self, net: SegmentationNet, optim: OptimConfig, input_shape, lag: int = 0,
-                 class_weights=None, bucket_mb: float = 32.0, group=None):
+                 class_weights=None, bucket_mb: float = 32.0, group=None, hierarchy=None):
+        """hierarchy = (groups, per_group): reduce each bucket in the paper's three stages
+        (collectives.py:157-200 hybrid_allreduce): reduce-scatter inside each group of per_group
+        consecutive ranks, all-reduce of the shards across groups, all-gather inside the group --
+        the 2x4 split-communicator mirror of the reference's hierarchical all-reduce.  None: one
+        NCCL all-reduce per bucket (on one NVSwitch node that is the whole of stage 1)."""
         if lag not in (0, 1):
             raise ValueError("lag must be 0 or 1")
         self.net = net
@@ -76,6 +81,23 @@ class DataParallelTrainer:
         eng.set_buckets(self.buckets if self.world > 1 else [list(net.param_order)])
         self._works = []
         self.steps_done = 0
+        self.hier = None
+        if hierarchy is not None and self.world > 1:
+            ng, per = hierarchy
+            if ng * per != self.world or 64 % per:
+                raise ValueError(f"hierarchy {hierarchy} does not tile {self.world} ranks (per_group must divide 64)")
+            rank = dist.get_rank()
+            local = cross = None
+            for gi in range(ng):   # every rank creates every group, in the same order
+                grp = dist.new_group([gi * per + j for j in range(per)])
+                if rank // per == gi:
+                    local = grp
+            for j in range(per):
+                grp = dist.new_group([gi * per + j for gi in range(ng)])
+                if rank % per == j:
+                    cross = grp
+            self.hier = (local, cross, per, rank % per)
+            self.comm_stream = torch.cuda.Stream(device=eng.device)
 
     def _make_buckets(self, bucket_mb: float):
         """Contiguous parameter ranges of >= bucket_mb, formed from the end of param order
@@ -102,7 +124,21 @@ class DataParallelTrainer:
     # ------------------------------------------------------------------ comm
     def _start_bucket(self, i):
         lo, hi = self.bucket_range[i]
-        w = dist.all_reduce(self.eng.flat_g[lo:hi], op=dist.ReduceOp.SUM, group=self.group, async_op=True)
+        if getattr(self, "hier", None) is None:
+            w = dist.all_reduce(self.eng.flat_g[lo:hi], op=dist.ReduceOp.SUM, group=self.group, async_op=True)
+            self._works.append(w)
+            return
+        # three stages on a communication stream (bucket bounds are 64-float aligned, so the
+        # bucket splits evenly into per_group shards; in-place NCCL reduce-scatter / all-gather)
+        local, cross, per, me = self.hier
+        buf = self.eng.flat_g[lo:hi]
+        shard = buf.view(per, -1)[me]
+        cs = self.comm_stream
+        cs.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cs):
+            dist.reduce_scatter_tensor(shard, buf, op=dist.ReduceOp.SUM, group=local, async_op=True).wait()
+            dist.all_reduce(shard, op=dist.ReduceOp.SUM, group=cross, async_op=True).wait()
+            w = dist.all_gather_into_tensor(buf, shard, group=local, async_op=True)
         self._works.append(w)
 
     def _backward_with_overlap(self):
@@ -314,6 +350,7 @@ class RunConfig:
     class_weighting: str = "inv_sqrt"
     hash_steps: tuple = ()
     precision: str = "bf16"   # "fp32": the parity mode (b2dl.h group 3)
+    hierarchy: tuple | None = None   # (groups, per_group): three-stage hierarchical all-reduce
 
     def __post_init__(self):
         if self.lag not in (0, 1):
@@ -357,7 +394,7 @@ def train_run(cfg: RunConfig, net_cls=None) -> TrainResult:
     shape = (cfg.local_batch, sc.channels, sc.height, sc.width)
     cw = (uniform_weights(cfg.net.classes) if cfg.class_weighting == "uniform"
           else ClassWeights(sc.frequencies).vector())
-    tr = DataParallelTrainer(net, cfg.optim, shape, lag=cfg.lag, class_weights=cw)
+    tr = DataParallelTrainer(net, cfg.optim, shape, lag=cfg.lag, class_weights=cw, hierarchy=cfg.hierarchy)
     hash_at = {1, 10, cfg.steps} | set(cfg.hash_steps)
     records, losses, digests = [], [], []
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

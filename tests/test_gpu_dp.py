@@ -61,3 +61,50 @@ def test_two_gpu_nccl_matches_reference(lag):
     for k, v in out[0][2].items():   # trajectory agreement after 3 bf16 steps (norm-relative)
         ref = d[f"{tag}_state:{k}"]
         assert np.linalg.norm(v - ref) / np.linalg.norm(ref) < 2e-2, k
+
+
+def _worker4(rank, world, port, hierarchy, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    from paper_1810_01993_b200.models import NetConfig
+    from paper_1810_01993_b200.optimizer import OptimConfig
+    from paper_1810_01993_b200.scenes import SceneConfig
+    from paper_1810_01993_b200.trainer import RunConfig, train_run
+    sc = SceneConfig(channels=8, height=16, width=16, streak_channels=(0, 1), blob_channels=(2, 3))
+    cfg = RunConfig(lag=0, steps=3, local_batch=1, seed=4, optim=OptimConfig(lr=0.1),
+                    net=NetConfig(channels_in=8, growth=16, block_layers=1, levels=1), scene=sc,
+                    hierarchy=hierarchy)
+    res = train_run(cfg)
+    q.put((rank, res.losses, res.digests, res.state))
+    dist.destroy_process_group()
+
+
+def _run4(hierarchy):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker4, args=(r, 4, port, hierarchy, q)) for r in range(4)]
+    for p in procs:
+        p.start()
+    out = {}
+    for _ in range(4):
+        r, losses, digests, state = q.get(timeout=600)
+        out[r] = (losses, digests, state)
+    for p in procs:
+        p.join(timeout=60)
+    return out
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 4, reason="needs 4 GPUs")
+def test_hierarchical_allreduce_matches_flat_on_four_gpus():
+    """2 x 2 three-stage all-reduce (reduce-scatter in group, all-reduce across groups,
+    all-gather in group; collectives.py:157-200) vs one flat all-reduce: same training
+    trajectory, weights identical on every rank within each run."""
+    flat, hier = _run4(None), _run4((2, 2))
+    for out in (flat, hier):
+        assert len({out[r][1][-1][1] for r in range(4)}) == 1      # cross-rank digests agree
+    assert np.allclose(flat[0][0], hier[0][0], rtol=1e-5)
+    for k, v in flat[0][2].items():
+        assert np.max(np.abs(v - hier[0][2][k])) <= 1e-5 * max(np.max(np.abs(v)), 1e-12), k
