@@ -351,6 +351,8 @@ class RunConfig:
     hash_steps: tuple = ()
     precision: str = "bf16"   # "fp32": the parity mode (b2dl.h group 3)
     hierarchy: tuple | None = None   # (groups, per_group): three-stage hierarchical all-reduce
+    prefetch_workers: int = 0        # > 0: scenes made by a W-worker bounded prefetch pipeline
+    prefetch_capacity: int = 4
 
     def __post_init__(self):
         if self.lag not in (0, 1):
@@ -398,10 +400,20 @@ def train_run(cfg: RunConfig, net_cls=None) -> TrainResult:
     hash_at = {1, 10, cfg.steps} | set(cfg.hash_steps)
     records, losses, digests = [], [], []
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    feed = None
+    if cfg.prefetch_workers > 0:   # pinned host batches, step order, W workers ahead
+        from .pipeline import PrefetchPipeline
+        feed = iter(PrefetchPipeline(lambda t: generated_batch(sc, cfg.seed, t, rank, cfg.local_batch), cfg.steps,
+                                     workers=cfg.prefetch_workers, capacity=cfg.prefetch_capacity))
     for t in range(cfg.steps):
-        x, lab = generated_batch(sc, cfg.seed, t, rank, cfg.local_batch)
-        xd = torch.from_numpy(x).cuda(non_blocking=True)
-        ld = torch.from_numpy(lab).cuda(non_blocking=True)
+        if feed is not None:
+            hx, hl = next(feed)
+            xd = hx.cuda(non_blocking=True)
+            ld = hl.cuda(non_blocking=True)
+        else:
+            x, lab = generated_batch(sc, cfg.seed, t, rank, cfg.local_batch)
+            xd = torch.from_numpy(x).cuda(non_blocking=True)
+            ld = torch.from_numpy(lab).cuda(non_blocking=True)
         ev0.record()
         loss = tr.step(xd, ld)
         ev1.record()

@@ -50,3 +50,20 @@ def test_resume_is_bitwise(lag, tmp_path):
     resumed = c.eng.export_params()
     for k in straight:
         assert np.array_equal(straight[k], resumed[k]), k
+
+
+def test_prefetch_pipeline_run_is_identical():
+    """train_run fed by the W-worker prefetch pipeline (pinned host batches, step order) follows
+    exactly the trajectory of the synchronous feed."""
+    from paper_1810_01993_b200.models import NetConfig
+    from paper_1810_01993_b200.optimizer import OptimConfig
+    from paper_1810_01993_b200.scenes import SceneConfig
+    from paper_1810_01993_b200.trainer import RunConfig, train_run
+    sc = SceneConfig(channels=8, height=16, width=16, streak_channels=(0, 1), blob_channels=(2, 3))
+    base = dict(lag=0, steps=4, local_batch=2, seed=4, optim=OptimConfig(lr=0.1),
+                net=NetConfig(channels_in=8, growth=16, block_layers=1, levels=1), scene=sc)
+    a = train_run(RunConfig(**base))
+    b = train_run(RunConfig(**base, prefetch_workers=3, prefetch_capacity=2))
+    assert a.losses == b.losses
+    for k in a.state:
+        assert np.array_equal(a.state[k], b.state[k]), k
