@@ -122,6 +122,7 @@ struct FpropParams {
   int epi_bytes;       // epilogue buffer bytes
   int tma_epi;         // 1: TMA-staged epilogue (operands + output through swizzled boxes)
   int epi_nops;        // operands per chunk in the TMA epilogue (residual, mask, accumulated y)
+  int epi_slots;       // operand slots per sub-group (prefetch depth + 1)
   int bias_vec;        // bias 16-byte aligned
 };
 
@@ -341,7 +342,10 @@ __device__ __forceinline__ void box_row_put(uint8_t* box, const float* v) {
 // tile moves in few, large TMA operations: operands arrive one chunk ahead, the four warps pack
 // their 32 rows into a shared output box, meet at a named barrier, and one thread stores it.
 constexpr int EPI_CHUNK = 128 * 64;  // 128 pixels x 32 bf16 channels
-__host__ __device__ constexpr int epi_sub_bytes(int nops) { return (2 * nops + 2) * EPI_CHUNK; }
+// per sub-group: `slots` operand slots of nops chunks (operands run slots-1 chunks ahead) + 2
+// output buffers
+__host__ __device__ constexpr int epi_sub_bytes(int nops, int slots = 2) { return (slots * nops + 2) * EPI_CHUNK; }
+constexpr int EPI_MAX_SLOTS = 4;
 
 template <int BN, int CG, int EW>
 __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const CUtensorMap* tmY, const CUtensorMap* tmR,
@@ -358,9 +362,10 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
   const int sub = ew >> 2;
   const bool leader = (q == 0) && (lane == 0);  // warp with lane quarter 0 of the sub-group
   const int nops = p.epi_nops;
-  uint8_t* sbuf = epi + sub * epi_sub_bytes(nops);
-  uint8_t* obuf = sbuf + 2 * nops * EPI_CHUNK;
-  uint64_t* ib = inbar + 2 * sub;
+  const int S = p.epi_slots;   // operand slots: loads run S-1 chunks ahead of use
+  uint8_t* sbuf = epi + sub * epi_sub_bytes(nops, S);
+  uint8_t* obuf = sbuf + S * nops * EPI_CHUNK;
+  uint64_t* ib = inbar + EPI_MAX_SLOTS * sub;
   auto locate = [&](int tile, int& img, int& x, int& y, int& nt) {
     const int pmt = tile / p.num_n_tiles;
     nt = tile - pmt * p.num_n_tiles;
@@ -405,13 +410,29 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
   auto sub_sync = [&]() { asm volatile("bar.sync %0, 128;" ::"r"(1 + sub) : "memory"); };
   const int row = q * 32 + lane;          // tile row (pixel) of this thread
   const int swz = (lane >> 1) & 3;        // 64B-swizzle phase of the row
-  uint32_t ph0 = 0, ph1 = 0;
-  int slot = 0, ob = 0, it = 0;
-  if (nops && unit0 < p.num_tiles) {
-    int img, x, y, nt;
-    locate(unit0, img, x, y, nt);
-    if (chunks(nt) > 0) issue(unit0, 0, 0);
-  }
+  // operand issue cursor: walks the same (tile, chunk) sequence as the consumer, S-1 items ahead,
+  // skipping tiles in which this sub-group has no chunk
+  int itile = unit0, ij = 0, issued = 0;
+  auto chunks_of = [&](int tile) {
+    int i2, x2, y2, nt2;
+    locate(tile, i2, x2, y2, nt2);
+    return chunks(nt2);
+  };
+  while (itile < p.num_tiles && chunks_of(itile) == 0) itile += units;
+  auto issue_next = [&]() {
+    if (!nops || itile >= p.num_tiles) return;
+    issue(itile, ij, issued % S);
+    ++issued;
+    if (++ij >= chunks_of(itile)) {
+      ij = 0;
+      do {
+        itile += units;
+      } while (itile < p.num_tiles && chunks_of(itile) == 0);
+    }
+  };
+  for (int k = 0; k < S - 1; ++k) issue_next();
+  uint32_t phbits = 0;   // wait parity per slot
+  int consumed = 0, ob = 0, it = 0;
   for (int tile = unit0; tile < p.num_tiles; tile += units, ++it) {
     const int as = it & 1;
     const uint32_t ap = (it >> 1) & 1;
@@ -424,15 +445,8 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
 #pragma unroll 1
     for (int j = 0; j < NJ; ++j) {
       if (j >= nv) break;  // uniform over the sub-group
-      if (nops) {          // operands of the next chunk (possibly of the next tile)
-        if (j + 1 < nv) {
-          issue(tile, j + 1, slot ^ 1);
-        } else if (tile + units < p.num_tiles) {
-          int i2, x2, y2, nt2;
-          locate(tile + units, i2, x2, y2, nt2);
-          if (chunks(nt2) > 0) issue(tile + units, 0, slot ^ 1);
-        }
-      }
+      issue_next();        // keeps S-1 chunks of operands in flight
+      const int slot = consumed % S;
       const int c0 = nt * BN + (SUBS * j + sub) * 32;
       uint32_t cur[32];
       tmem_ld_issue_x32(tbase + (SUBS * j + sub) * 32, cur);
@@ -440,11 +454,8 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
       if (j == nv - 1) release(as);
       const uint8_t* in = sbuf + slot * nops * EPI_CHUNK;
       if (nops) {
-        mbar_wait(&ib[slot], slot ? ph1 : ph0);
-        if (slot)
-          ph1 ^= 1;
-        else
-          ph0 ^= 1;
+        mbar_wait(&ib[slot], (phbits >> slot) & 1u);
+        phbits ^= 1u << slot;
       }
       uint8_t* ochunk = obuf + ob * EPI_CHUNK;
       const float4* bias4 = p.bias ? reinterpret_cast<const float4*>(p.bias + c0) : nullptr;
@@ -515,18 +526,9 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
         bulk_commit();
       }
       ob ^= 1;
-      slot ^= 1;
+      ++consumed;
     }
-    if (nv == 0) {
-      release(as);
-      // no chunk of this tile was ours, so nothing chained the next tile's first operands:
-      // issue them now into the still-free slot
-      if (nops && tile + units < p.num_tiles) {
-        int i2, x2, y2, nt2;
-        locate(tile + units, i2, x2, y2, nt2);
-        if (chunks(nt2) > 0) issue(tile + units, 0, slot);
-      }
-    }
+    if (nv == 0) release(as);
   }
   if (leader) bulk_wait<0>();
   __syncwarp();
@@ -1396,7 +1398,11 @@ static int launch_fprop(const FpropMaps& t, FpropParams p, cudaStream_t st) {
   }
   if (C::CW != 32) p.tma_epi = 0;
   p.epi_nops = p.tma_epi ? (p.res != nullptr) + (p.mask != nullptr) + (p.accumulate != 0) : 0;
-  p.epi_bytes = p.tma_epi ? (EW / 4) * epi_sub_bytes(p.epi_nops) : EPI_LEGACY_BYTES;
+  // operand prefetch depth (slots - 1 chunks ahead).  Measured: a third slot does not speed up
+  // the epilogue-bound 1x1 layers (their chunks wait on instruction latency, not on the loads)
+  // and costs operand stages, so two it is.
+  p.epi_slots = 2;
+  p.epi_bytes = p.tma_epi ? (EW / 4) * epi_sub_bytes(p.epi_nops, p.epi_slots) : EPI_LEGACY_BYTES;
   // deepest operand pipeline that fits beside the epilogue buffers
   p.stages = 1;
   for (int s = FPROP_MAX_STAGES; s >= 1; --s) {
@@ -1514,7 +1520,8 @@ static int launch_halo_fprop(const b2dl_conv_args* a, const b2dl_act& xv, cudaSt
   p.vec_ok = 1;
   p.tma_epi = 1;
   p.epi_nops = (p.res != nullptr) + (p.mask != nullptr) + (p.accumulate != 0);
-  p.epi_bytes = 2 * epi_sub_bytes(p.epi_nops);
+  p.epi_slots = 2;
+  p.epi_bytes = 2 * epi_sub_bytes(p.epi_nops, 2);
   const int a_stage = (HALO_BH + p.taps - 1) * HALO_BW * 128;
   const int b_region = p.taps * p.num_cblk * HALO_BBOX;
   p.stages = std::min(FPROP_MAX_STAGES, (SMEM_MAX - SMEM_FIXED - b_region - p.epi_bytes) / a_stage);
