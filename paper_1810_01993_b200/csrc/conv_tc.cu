@@ -410,29 +410,34 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
   auto sub_sync = [&]() { asm volatile("bar.sync %0, 128;" ::"r"(1 + sub) : "memory"); };
   const int row = q * 32 + lane;          // tile row (pixel) of this thread
   const int swz = (lane >> 1) & 3;        // 64B-swizzle phase of the row
-  // operand issue cursor: walks the same (tile, chunk) sequence as the consumer, S-1 items ahead,
-  // skipping tiles in which this sub-group has no chunk
-  int itile = unit0, ij = 0, issued = 0;
-  auto chunks_of = [&](int tile) {
-    int i2, x2, y2, nt2;
-    locate(tile, i2, x2, y2, nt2);
-    return chunks(nt2);
+  // operand issue cursor (leader thread only): walks the consumer's (tile, chunk) sequence S-1
+  // items ahead, skipping tiles in which this sub-group has no chunk.  Only the last N tile can
+  // be partial, so a tile's chunk count follows from its N index, tracked without divisions.
+  const int nv_full = chunks(0), nv_last = chunks(p.num_n_tiles - 1);
+  const int units_nt = units % p.num_n_tiles;
+  int itile = unit0, int_nt = unit0 % p.num_n_tiles, ij = 0, islot = 0;
+  auto nv_at = [&](int ntv) { return ntv == p.num_n_tiles - 1 ? nv_last : nv_full; };
+  auto step_tile = [&]() {
+    itile += units;
+    int_nt += units_nt;
+    if (int_nt >= p.num_n_tiles) int_nt -= p.num_n_tiles;
   };
-  while (itile < p.num_tiles && chunks_of(itile) == 0) itile += units;
+  if (leader)
+    while (itile < p.num_tiles && nv_at(int_nt) == 0) step_tile();
   auto issue_next = [&]() {
-    if (!nops || itile >= p.num_tiles) return;
-    issue(itile, ij, issued % S);
-    ++issued;
-    if (++ij >= chunks_of(itile)) {
+    if (!leader || !nops || itile >= p.num_tiles) return;
+    issue(itile, ij, islot);
+    islot = islot + 1 == S ? 0 : islot + 1;
+    if (++ij >= nv_at(int_nt)) {
       ij = 0;
       do {
-        itile += units;
-      } while (itile < p.num_tiles && chunks_of(itile) == 0);
+        step_tile();
+      } while (itile < p.num_tiles && nv_at(int_nt) == 0);
     }
   };
   for (int k = 0; k < S - 1; ++k) issue_next();
   uint32_t phbits = 0;   // wait parity per slot
-  int consumed = 0, ob = 0, it = 0;
+  int slot = 0, ob = 0, it = 0;
   for (int tile = unit0; tile < p.num_tiles; tile += units, ++it) {
     const int as = it & 1;
     const uint32_t ap = (it >> 1) & 1;
@@ -446,7 +451,6 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
     for (int j = 0; j < NJ; ++j) {
       if (j >= nv) break;  // uniform over the sub-group
       issue_next();        // keeps S-1 chunks of operands in flight
-      const int slot = consumed % S;
       const int c0 = nt * BN + (SUBS * j + sub) * 32;
       uint32_t cur[32];
       tmem_ld_issue_x32(tbase + (SUBS * j + sub) * 32, cur);
@@ -526,7 +530,7 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
         bulk_commit();
       }
       ob ^= 1;
-      ++consumed;
+      slot = slot + 1 == S ? 0 : slot + 1;
     }
     if (nv == 0) release(as);
   }
