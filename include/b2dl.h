@@ -253,10 +253,12 @@ B2DL_API int b2dl_bn_backward(b2dl_act x, b2dl_act gy, const float* gamma, const
                               float* dbeta, int param_accumulate, b2dl_act dx, int accumulate, void* workspace,
                               size_t workspace_bytes, int f32, void* stream);
 /* bilinear upsampling by integer factor f (half-pixel centres, align_corners=False) and its VJP
- * (a deterministic gather; dx (+)= mask(>0) * ...). */
+ * (separable and deterministic: a row pass into an fp32 workspace of dy.n*dy.h*(dy.w/f)*dy.c
+ * floats, then a column pass; dx (+)= mask(>0) * ...). */
 B2DL_API int b2dl_bilinear_fwd(b2dl_act x, b2dl_act y, int f, int f32, void* stream);
+B2DL_API size_t b2dl_bilinear_workspace_size(b2dl_act dy, int f);
 B2DL_API int b2dl_bilinear_bwd(b2dl_act dy, b2dl_act dx, int f, int accumulate, b2dl_act mask, int f32,
-                               void* stream);
+                               void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---------------------------------------------------------------- (3) fp32 parity mode
  * The reference's own arithmetic type end to end (north star: loss and gradients within 1e-3 in

@@ -86,7 +86,8 @@ _SIGS = {
     "b2dl_bn_backward": (_c_int, [Act, Act, _vp, _vp, _vp, _vp, _c_int, Act, _c_int, _vp, ctypes.c_size_t, _c_int,
                                   _vp]),
     "b2dl_bilinear_fwd": (_c_int, [Act, Act, _c_int, _c_int, _vp]),
-    "b2dl_bilinear_bwd": (_c_int, [Act, Act, _c_int, _c_int, Act, _c_int, _vp]),
+    "b2dl_bilinear_workspace_size": (ctypes.c_size_t, [Act, _c_int]),
+    "b2dl_bilinear_bwd": (_c_int, [Act, Act, _c_int, _c_int, Act, _c_int, _vp, ctypes.c_size_t, _vp]),
     "b2dl_f32_conv_fprop": (_c_int, [ctypes.POINTER(ConvArgs), _vp]),
     "b2dl_f32_wgrad_workspace_size": (ctypes.c_size_t, [ctypes.POINTER(WgradArgs)]),
     "b2dl_f32_conv_wgrad": (_c_int, [ctypes.POINTER(WgradArgs), _vp]),

@@ -283,73 +283,96 @@ __device__ __forceinline__ void bl_tap(int o, int n_in, int f, int& i0, int& i1,
   w0 = 1.f - w1;
 }
 
+// one block per output row (row taps computed once), threads over (column, channel group)
 template <typename T, int V>
 __global__ void k_bilinear_fwd(const T* __restrict__ x, int xs, T* __restrict__ y, int ys, int n, int h, int w, int c,
                                int f) {
   const int H = h * f, W = w * f, groups = c / V;
-  const long long total = static_cast<long long>(n) * H * W * groups;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int g = static_cast<int>(i % groups);
-    const long long q = i / groups;
-    const int X = static_cast<int>(q % W);
-    const long long r = q / W;
-    const int Y = static_cast<int>(r % H);
-    const long long img = r / H;
-    int y0, y1, x0, x1;
-    float wy0, wy1, wx0, wx1;
-    bl_tap(Y, h, f, y0, y1, wy0, wy1);
+  const int Y = blockIdx.x, img = blockIdx.y;
+  int y0, y1, x0, x1;
+  float wy0, wy1, wx0, wx1;
+  bl_tap(Y, h, f, y0, y1, wy0, wy1);
+  const T* r0 = x + (static_cast<long long>(img) * h + y0) * w * static_cast<long long>(xs);
+  const T* r1 = x + (static_cast<long long>(img) * h + y1) * w * static_cast<long long>(xs);
+  T* out = y + (static_cast<long long>(img) * H + Y) * W * static_cast<long long>(ys);
+  for (int i = threadIdx.x; i < W * groups; i += blockDim.x) {
+    const int X = i / groups, g = i - X * groups;
     bl_tap(X, w, f, x0, x1, wx0, wx1);
-    const T* base = x + img * h * w * static_cast<long long>(xs) + g * V;
     float a[V], b[V], cc[V], d[V], o[V];
-    Vec<T, V>::load(base + (static_cast<long long>(y0) * w + x0) * xs, a);
-    Vec<T, V>::load(base + (static_cast<long long>(y0) * w + x1) * xs, b);
-    Vec<T, V>::load(base + (static_cast<long long>(y1) * w + x0) * xs, cc);
-    Vec<T, V>::load(base + (static_cast<long long>(y1) * w + x1) * xs, d);
+    Vec<T, V>::load(r0 + static_cast<long long>(x0) * xs + g * V, a);
+    Vec<T, V>::load(r0 + static_cast<long long>(x1) * xs + g * V, b);
+    Vec<T, V>::load(r1 + static_cast<long long>(x0) * xs + g * V, cc);
+    Vec<T, V>::load(r1 + static_cast<long long>(x1) * xs + g * V, d);
 #pragma unroll
     for (int e = 0; e < V; ++e) o[e] = wy0 * (wx0 * a[e] + wx1 * b[e]) + wy1 * (wx0 * cc[e] + wx1 * d[e]);
-    Vec<T, V>::store(y + q * ys + g * V, o);
+    Vec<T, V>::store(out + static_cast<long long>(X) * ys + g * V, o);
   }
 }
 
-// dx[y][x] (+)= mask * sum over outputs (Y, X) whose taps include (y, x) of weight * dy[Y][X]
+// The VJP is separable: dx[y][x] = sum_Y wy(Y, y) * R[Y][x] with R[Y][x] = sum_X wx(X, x) * dy[Y][X].
+// Pass 1 (one block per output row Y) forms R in fp32 at low-res columns, pass 2 (one block per
+// input row y) sums the ~2f contributing rows of R -- each dy element is read once, no atomics.
+__device__ __forceinline__ void bl_range(int i, int n_in, int f, int n_out, int& lo, int& hi) {
+  // outputs whose floor tap is i - 1 or i: src = (o + 0.5) / f - 0.5 in [i - 1, i + 1); the last
+  // input also takes the clamped outputs beyond it
+  lo = max(0, static_cast<int>(ceilf(f * (i - 1) + 0.5f * f - 0.5f)));
+  hi = i == n_in - 1 ? n_out - 1 : min(n_out - 1, static_cast<int>(ceilf(f * (i + 1) + 0.5f * f - 0.5f)) - 1);
+}
+__device__ __forceinline__ float bl_weight(int o, int i, int n_in, int f) {
+  int i0, i1;
+  float w0, w1;
+  bl_tap(o, n_in, f, i0, i1, w0, w1);
+  return (i0 == i ? w0 : 0.f) + (i1 == i ? w1 : 0.f);
+}
+
 template <typename T, int V>
-__global__ void k_bilinear_bwd(const T* __restrict__ dy, int dys, T* __restrict__ dx, int dxs,
-                               const T* __restrict__ mask, int ms, int n, int h, int w, int c, int f, int acc) {
+__global__ void k_bilinear_bwd_rows(const T* __restrict__ dy, int dys, float* __restrict__ R, int h, int w, int c,
+                                    int f) {
   const int H = h * f, W = w * f, groups = c / V;
-  const long long total = static_cast<long long>(n) * h * w * groups;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int g = static_cast<int>(i % groups);
-    const long long q = i / groups;
-    const int xx = static_cast<int>(q % w);
-    const long long r = q / w;
-    const int yy = static_cast<int>(r % h);
-    const long long img = r / h;
-    // outputs whose source coordinate lies in [yy - 1, yy + 1]
-    const int Y0 = max(0, (yy - 1) * f), Y1 = min(H - 1, (yy + 2) * f);
-    const int X0 = max(0, (xx - 1) * f), X1 = min(W - 1, (xx + 2) * f);
+  const int Y = blockIdx.x, img = blockIdx.y;
+  const T* row = dy + (static_cast<long long>(img) * H + Y) * W * static_cast<long long>(dys);
+  float* out = R + (static_cast<long long>(img) * H + Y) * w * static_cast<long long>(c);
+  for (int i = threadIdx.x; i < w * groups; i += blockDim.x) {
+    const int xx = i / groups, g = i - xx * groups;
+    int X0, X1;
+    bl_range(xx, w, f, W, X0, X1);
+    float s[V];
+#pragma unroll
+    for (int e = 0; e < V; ++e) s[e] = 0.f;
+    for (int X = X0; X <= X1; ++X) {
+      const float wx = bl_weight(X, xx, w, f);
+      if (wx == 0.f) continue;
+      float v[V];
+      Vec<T, V>::load(row + static_cast<long long>(X) * dys + g * V, v);
+#pragma unroll
+      for (int e = 0; e < V; ++e) s[e] += wx * v[e];
+    }
+#pragma unroll
+    for (int e = 0; e < V; ++e) out[static_cast<long long>(xx) * c + g * V + e] = s[e];
+  }
+}
+
+template <typename T, int V>
+__global__ void k_bilinear_bwd_cols(const float* __restrict__ R, T* __restrict__ dx, int dxs,
+                                    const T* __restrict__ mask, int ms, int h, int w, int c, int f, int acc) {
+  const int H = h * f, groups = c / V;
+  const int yy = blockIdx.x, img = blockIdx.y;
+  int Y0, Y1;
+  bl_range(yy, h, f, H, Y0, Y1);
+  const long long q0 = (static_cast<long long>(img) * h + yy) * w;
+  for (int i = threadIdx.x; i < w * groups; i += blockDim.x) {
+    const int xx = i / groups, g = i - xx * groups;
     float s[V];
 #pragma unroll
     for (int e = 0; e < V; ++e) s[e] = 0.f;
     for (int Y = Y0; Y <= Y1; ++Y) {
-      int y0, y1;
-      float wy0, wy1;
-      bl_tap(Y, h, f, y0, y1, wy0, wy1);
-      const float wy = (y0 == yy ? wy0 : 0.f) + (y1 == yy ? wy1 : 0.f);
+      const float wy = bl_weight(Y, yy, h, f);
       if (wy == 0.f) continue;
-      for (int X = X0; X <= X1; ++X) {
-        int x0, x1;
-        float wx0, wx1;
-        bl_tap(X, w, f, x0, x1, wx0, wx1);
-        const float wx = (x0 == xx ? wx0 : 0.f) + (x1 == xx ? wx1 : 0.f);
-        if (wx == 0.f) continue;
-        float v[V];
-        Vec<T, V>::load(dy + ((img * H + Y) * W + X) * dys + g * V, v);
+      const float* r = R + ((static_cast<long long>(img) * H + Y) * w + xx) * c + g * V;
 #pragma unroll
-        for (int e = 0; e < V; ++e) s[e] += wy * wx * v[e];
-      }
+      for (int e = 0; e < V; ++e) s[e] += wy * r[e];
     }
+    const long long q = q0 + xx;
     if (mask) {
       float m[V];
       Vec<T, V>::load(mask + q * ms + g * V, m);
@@ -497,24 +520,37 @@ extern "C" int b2dl_bilinear_fwd(b2dl_act x, b2dl_act y, int f, int f32, void* s
   const bool vec = vec_act(x, vw) && vec_act(y, vw);
   cudaStream_t st = as_stream(stream);
   B2_TV(f32, vec, {
-    k_bilinear_fwd<T, V><<<grid_of(static_cast<long long>(y.n) * y.h * y.w * (y.c / V)), 256, 0, st>>>(
+    k_bilinear_fwd<T, V><<<dim3(y.h, y.n), 256, 0, st>>>(
         reinterpret_cast<const T*>(x.ptr), x.c_stride, reinterpret_cast<T*>(y.ptr), y.c_stride, x.n, x.h, x.w, x.c,
         f);
   });
   return check_launch();
 }
 
+extern "C" size_t b2dl_bilinear_workspace_size(b2dl_act dy, int f) {
+  if (f < 1) return 0;
+  return static_cast<size_t>(dy.n) * dy.h * (dy.w / f) * dy.c * sizeof(float) + 256;
+}
+
 extern "C" int b2dl_bilinear_bwd(b2dl_act dy, b2dl_act dx, int f, int accumulate, b2dl_act mask, int f32,
-                                 void* stream) {
+                                 void* workspace, size_t workspace_bytes, void* stream) {
   if (!dy.ptr || !dx.ptr || f < 1 || dy.h != dx.h * f || dy.w != dx.w * f || dy.c != dx.c || dy.n != dx.n)
     return B2DL_E_VALUE;
+  if (!workspace || workspace_bytes < b2dl_bilinear_workspace_size(dy, f)) return B2DL_E_VALUE;
   const int vw = f32 ? 4 : 8;
   const bool vec = vec_act(dy, vw) && vec_act(dx, vw) && vec_act(mask, vw);
+  float* R = reinterpret_cast<float*>(workspace);
   cudaStream_t st = as_stream(stream);
   B2_TV(f32, vec, {
-    k_bilinear_bwd<T, V><<<grid_of(static_cast<long long>(dx.n) * dx.h * dx.w * (dx.c / V)), 256, 0, st>>>(
-        reinterpret_cast<const T*>(dy.ptr), dy.c_stride, reinterpret_cast<T*>(dx.ptr), dx.c_stride,
-        reinterpret_cast<const T*>(mask.ptr), mask.c_stride, dx.n, dx.h, dx.w, dx.c, f, accumulate);
+    k_bilinear_bwd_rows<T, V><<<dim3(dy.h, dy.n), 256, 0, st>>>(reinterpret_cast<const T*>(dy.ptr), dy.c_stride, R,
+                                                                dx.h, dx.w, dx.c, f);
+  });
+  int rc = check_launch();
+  if (rc) return rc;
+  B2_TV(f32, vec, {
+    k_bilinear_bwd_cols<T, V><<<dim3(dx.h, dx.n), 256, 0, st>>>(
+        R, reinterpret_cast<T*>(dx.ptr), dx.c_stride, reinterpret_cast<const T*>(mask.ptr), mask.c_stride, dx.h, dx.w,
+        dx.c, f, accumulate);
   });
   return check_launch();
 }

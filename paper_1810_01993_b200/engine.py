@@ -885,7 +885,7 @@ class Engine:
                             on_bucket_ready(i)
             elif op.kind == "up" and op.mode == "bilinear":
                 nhwc.bilinear_bwd(self.gv(op.out), self.gv(op.ins[0]), op.factor, accumulate=st["dx"],
-                                  mask=self.v(op.ins[0]) if st["mask"] else None)
+                                  mask=self.v(op.ins[0]) if st["mask"] else None, ws=self.ws)
                 self.launches += 1
             elif op.kind == "pool":
                 (nhwc.f32_avgpool_bwd if self.fp32 else nhwc.avgpool_bwd)(

@@ -333,6 +333,16 @@ def bilinear_fwd(x: View, y: View, f: int):
     check(LIB.b2dl_bilinear_fwd(x.act(), y.act(), f, _is_f32(x), _stream()), "bilinear_fwd")
 
 
-def bilinear_bwd(dy: View, dx: View, f: int, accumulate=False, mask: View | None = None):
-    check(LIB.b2dl_bilinear_bwd(dy.act(), dx.act(), f, int(accumulate), _act(mask), _is_f32(dy), _stream()),
-          "bilinear_bwd")
+def bilinear_bwd(dy: View, dx: View, f: int, accumulate=False, mask: View | None = None,
+                 ws: Workspace | None = None):
+    global _BL_WS
+    if ws is None:
+        if _BL_WS is None:
+            _BL_WS = Workspace(dy.buf.device)
+        ws = _BL_WS
+    buf = ws.get(LIB.b2dl_bilinear_workspace_size(dy.act(), f))
+    check(LIB.b2dl_bilinear_bwd(dy.act(), dx.act(), f, int(accumulate), _act(mask), _is_f32(dy),
+                                ctypes.c_void_p(buf.data_ptr()), buf.numel(), _stream()), "bilinear_bwd")
+
+
+_BL_WS = None
