@@ -112,6 +112,12 @@ typedef struct b2dl_conv_args {
    * over window * x.c input channels -- memory-identical to the kh x kw x cin HWIO tensor.
    * Used for narrow inputs (the 16-channel 7x7 stem) whose per-tap K would be tiny. */
   int window;
+  /* Input stride s >= 1 (0 = 1): output pixel (y, x) reads x at (s*y + i*dilation - pad_top,
+   * s*x + j*dilation - pad_left); x.h == s*y.h, x.w == s*y.w.  With the merged weights of
+   * b2dl_pack_upsampled_dgrad this is the input gradient of a conv whose input was a nearest
+   * upsampling by s, already summed over each s x s block (the upsample VJP): one conv at the
+   * low resolution instead of a full-resolution dgrad plus a block sum. */
+  int in_stride;
 } b2dl_conv_args;
 
 B2DL_API int b2dl_cin_pad(int cin);
@@ -160,6 +166,12 @@ B2DL_API int b2dl_reduce_segments(const b2dl_segment* segs, int nseg, int64_t ma
  * and (optionally) the dgrad layout [cin][taps(flipped)][cout_pad]. */
 B2DL_API int b2dl_pack_weights(const float* w_hwio, int kh, int kw, int cin, int cout, void* fprop_packed,
                       void* dgrad_packed, void* stream);
+
+/* Merged weights for the strided input gradient above: conv k x k (HWIO fp32 [k*k][cin][cout],
+ * same padding (k-1)/2) applied to a nearest upsampling by f; out is packed bf16
+ * [cin][(k+f-1)^2][cin_pad(cout)] with W'(o) = sum over taps t, block offsets b with b - t = o of
+ * W(t)^T (pads: pad_top = pad_left = (k-1)/2, in_stride f, kernel k+f-1, w_mode 0). */
+B2DL_API int b2dl_pack_upsampled_dgrad(const float* w_hwio, int k, int cin, int cout, int f, void* out, void* stream);
 
 /* NCHW fp32 -> NHWC view, bf16 (or fp32 when dst_f32) (input tiles, reference-layout tensors). */
 B2DL_API int b2dl_nchw_to_nhwc(const float* x, b2dl_act y, int dst_f32, void* stream);

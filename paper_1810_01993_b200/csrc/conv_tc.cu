@@ -124,6 +124,7 @@ struct FpropParams {
   int epi_nops;        // operands per chunk in the TMA epilogue (residual, mask, accumulated y)
   int epi_slots;       // operand slots per sub-group (prefetch depth + 1)
   int bias_vec;        // bias 16-byte aligned
+  int in_stride;       // input pixels per output pixel (strided reads of the input)
 };
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
@@ -712,7 +713,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
           const int i = tap / p.kw, j = tap - i * p.kw;
           uint8_t* a_dst = sA + stage * C::A_BYTES;
           uint8_t* b_dst = sB + stage * C::B_BYTES;
-          const int ax = x0 + j * p.dil - p.pad_left, ay = y0 + i * p.dil - p.pad_top;
+          const int ax = x0 * p.in_stride + j * p.dil - p.pad_left, ay = y0 * p.in_stride + i * p.dil - p.pad_top;
           if constexpr (CG == 2) {
             // both CTAs' loads complete on the even CTA's barrier, which expects both halves
             if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
@@ -1592,6 +1593,12 @@ extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
   const b2dl_act& y = a->y;
   b2dl_act x;
   if (window_view(a->x, a->window, a->kw, a->pad_left, y.w, &x)) return B2DL_E_VALUE;
+  const int s_in = a->in_stride > 0 ? a->in_stride : 1;
+  if (s_in > 1 && (a->window || x.h != s_in * y.h || x.w != s_in * y.w || s_in > 8)) return B2DL_E_VALUE;
+  if (s_in > 1) {   // the kernel tiles the output; the input map is strided (checked above)
+    x.h = y.h;
+    x.w = y.w;
+  }
   if (x.n != y.n || x.h != y.h || x.w != y.w || y.c != a->cout) return B2DL_E_VALUE;
   if (a->kh < 1 || a->kw < 1 || a->dilation < 1 || a->cout < 1 || x.c < 1) return B2DL_E_VALUE;
   if (!view_aligned(x, 2)) return B2DL_E_ALIGN;
@@ -1636,8 +1643,10 @@ extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
   p.n = x.n;
   p.h = x.h;
   p.w = x.w;
+  p.in_stride = s_in;
   p.bw = pow2_divisor(x.w, 128);
   if (p.bw < 8 && x.w >= 8) p.bw = std::min(128, 1 << (31 - __builtin_clz(x.w)));
+  while (p.bw * s_in > 256) p.bw >>= 1;   // strided input box: traversal extent <= 256
   p.bh = BM / p.bw;
   p.tiles_x = cdiv(x.w, p.bw);
   p.tiles_y = cdiv(x.h, p.bh);
@@ -1667,7 +1676,9 @@ extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
 
   FpropMaps t;
   const CUtensorMapSwizzle sw = kblk == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B;
-  if (a->window ? window_map(&t.a, a->x, x.c, y.w, kblk, p.bw, p.bh, sw) : act_map(&t.a, x, kblk, p.bw, p.bh, sw))
+  if (a->window ? window_map(&t.a, a->x, x.c, y.w, kblk, p.bw, p.bh, sw)
+                : s_in > 1 ? act_map_strided(&t.a, a->x, kblk, p.bw, p.bh, s_in, sw)
+                           : act_map(&t.a, x, kblk, p.bw, p.bh, sw))
     return B2DL_E_ALIGN;
   const int mode = a->w_mode;
   p.b_mode = mode;

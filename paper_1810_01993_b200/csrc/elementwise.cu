@@ -691,6 +691,45 @@ extern "C" int b2dl_pack_weights(const float* w_hwio, int kh, int kw, int cin, i
   return B2DL_OK;
 }
 
+// W'[ci][i*K'+j][co] = sum over taps (ti, tj) of W_hwio[ti*k+tj][ci][co] whose block offset
+// b = i + t - (k - 1) lies in [0, f) on both axes (K' = k + f - 1): the input gradient of a k x k
+// "same" conv over a nearest x f upsampling, summed over each f x f block, as one K'-tap conv
+// with input stride f over dy.
+__global__ void k_pack_upsampled_dgrad(const float* __restrict__ w, __nv_bfloat16* __restrict__ out, int k, int cin,
+                                       int cout, int f, int cp) {
+  const int kk = k + f - 1;
+  const long long total = static_cast<long long>(cin) * kk * kk * cp;
+  for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int co = static_cast<int>(idx % cp);
+    const long long r = idx / cp;
+    const int o = static_cast<int>(r % (kk * kk));
+    const int ci = static_cast<int>(r / (kk * kk));
+    const int i = o / kk, j = o - i * kk;
+    float v = 0.f;
+    if (co < cout)
+      for (int ti = 0; ti < k; ++ti) {
+        const int bi = i + ti - (k - 1);
+        if (bi < 0 || bi >= f) continue;
+        for (int tj = 0; tj < k; ++tj) {
+          const int bj = j + tj - (k - 1);
+          if (bj < 0 || bj >= f) continue;
+          v += w[(static_cast<long long>(ti * k + tj) * cin + ci) * cout + co];
+        }
+      }
+    out[idx] = __float2bfloat16_rn(v);
+  }
+}
+
+extern "C" int b2dl_pack_upsampled_dgrad(const float* w_hwio, int k, int cin, int cout, int f, void* out,
+                                         void* stream) {
+  if (!w_hwio || !out || k < 1 || k % 2 == 0 || f < 1 || cin < 1 || cout < 1) return B2DL_E_VALUE;
+  const int cp = b2dl_cin_pad(cout), kk = k + f - 1;
+  k_pack_upsampled_dgrad<<<grid1d(static_cast<long long>(cin) * kk * kk * cp), 256, 0, as_stream(stream)>>>(
+      w_hwio, BF(out), k, cin, cout, f, cp);
+  return check_launch();
+}
+
 extern "C" int b2dl_head_backward_parts(void) { return 4 * num_sms(); }
 
 extern "C" int b2dl_head_backward(b2dl_act dy, const float* w_hwio, b2dl_act x, b2dl_act dx, int accumulate,

@@ -35,7 +35,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 int encode_tiled(CUtensorMap* m, CUtensorMapDataType dt, int rank, void* ptr, const uint64_t* dims,
-                 const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle sw) {
+                 const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle sw,
+                 const uint32_t* elem_strides) {
   auto fn = encode_fn();
   if (!fn) return B2DL_E_CUDA;
   cuuint64_t d[5];
@@ -44,7 +45,7 @@ int encode_tiled(CUtensorMap* m, CUtensorMapDataType dt, int rank, void* ptr, co
   for (int i = 0; i < rank; ++i) {
     d[i] = dims[i];
     b[i] = box[i];
-    e[i] = 1;
+    e[i] = elem_strides ? elem_strides[i] : 1;
     if (i + 1 < rank) s[i] = strides_bytes[i];
   }
   CUresult r = fn(m, dt, rank, ptr, d, s, b, e, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -60,6 +61,20 @@ int act_map(CUtensorMap* m, const b2dl_act& a, int box_c, int box_w, int box_h, 
   const uint32_t box[4] = {static_cast<uint32_t>(box_c), static_cast<uint32_t>(box_w), static_cast<uint32_t>(box_h),
                            1u};
   return encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, a.ptr, dims, strides, box, sw);
+}
+
+// Strided traversal: a box of bw x bh pixels taken every `stride` pixels in W and H (the TMA
+// box spans bw*stride x bh*stride input pixels; elementStrides select every stride-th one).
+int act_map_strided(CUtensorMap* m, const b2dl_act& a, int box_c, int box_w, int box_h, int stride,
+                    CUtensorMapSwizzle sw) {
+  const uint64_t cs = static_cast<uint64_t>(a.c_stride) * 2;
+  const uint64_t dims[4] = {static_cast<uint64_t>(a.c), static_cast<uint64_t>(a.w), static_cast<uint64_t>(a.h),
+                            static_cast<uint64_t>(a.n)};
+  const uint64_t strides[3] = {cs, cs * a.w, cs * a.w * a.h};
+  const uint32_t box[4] = {static_cast<uint32_t>(box_c), static_cast<uint32_t>(box_w * stride),
+                           static_cast<uint32_t>(box_h * stride), 1u};
+  const uint32_t es[4] = {1u, static_cast<uint32_t>(stride), static_cast<uint32_t>(stride), 1u};
+  return encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, a.ptr, dims, strides, box, sw, es);
 }
 
 // Row-window view of a haloed NHWC image (conv window mode): virtual pixel (y, xx) holds the

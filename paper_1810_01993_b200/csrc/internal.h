@@ -13,11 +13,14 @@ namespace b2 {
 int num_sms();
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda needed).
 int encode_tiled(CUtensorMap* m, CUtensorMapDataType dt, int rank, void* ptr, const uint64_t* dims,
-                 const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle sw);
+                 const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle sw,
+                 const uint32_t* elem_strides = nullptr);
 // 4-D NHWC bf16 activation map: dims (c, w, h, n), box (box_c, box_w, box_h, 1).
 int act_map(CUtensorMap* m, const b2dl_act& a, int box_c, int box_w, int box_h, CUtensorMapSwizzle sw);
 int window_map(CUtensorMap* m, const b2dl_act& x, int c_v, int w_v, int box_c, int box_w, int box_h,
                CUtensorMapSwizzle sw);
+int act_map_strided(CUtensorMap* m, const b2dl_act& a, int box_c, int box_w, int box_h, int stride,
+                    CUtensorMapSwizzle sw);
 int act_map5(CUtensorMap* m, const b2dl_act& a, int box_w, int box_h, int g);
 
 inline int check_launch() {

@@ -466,6 +466,13 @@ class Engine:
         self.heads = set() if self.fp32 else {o.w for o in self.convs
                                               if o.k == 1 and o.cout < 8 and o.cin % 8 == 0
                                               and 256 % (o.cin // 8) == 0}
+        # Conv over a nearest upsampling (DeepLab's full.c0 after the x4 full.up): the conv's input
+        # gradient and the upsample's VJP are one conv over dy at LOW resolution with input stride f
+        # and merged (k+f-1)^2-tap weights (b2dl_pack_upsampled_dgrad): (1 + (f-1)/k)^2 / f^2 of the
+        # full-resolution dgrad's MMA work, and no full-resolution input gradient written or re-read.
+        self.up_dgrad, self.wup, self.skip_up = {}, {}, set()
+        if not self.fp32 and os.environ.get("B2DL_UP_DGRAD", "1") != "0":
+            self._plan_up_dgrad()
         hparts = nhwc.head_backward_parts()
         for o in self.convs:
             if self.fp32:   # fp32 wgrad reduces its split-K partials itself, into flat_g
@@ -514,6 +521,29 @@ class Engine:
         self.conv_events = []
         self.load_params(params)
 
+    def _plan_up_dgrad(self):
+        p = self.plan
+        users = {}
+        for o in p.ops:
+            for t in list(o.ins) + ([o.res] if o.kind in ("conv", "bn") and o.res else []):
+                users.setdefault(t, []).append(o)
+        prog = p.backward_program
+        for i, st in enumerate(prog[:-1]):
+            o, nxt = st["op"], prog[i + 1]
+            up = nxt["op"]
+            x = o.ins[0]
+            # the upsample's backward step must directly follow the conv's (nothing else writes
+            # grad of its input in between), and the upsampled tensor must be the conv's alone
+            if (o.kind != "conv" or st["dx"] is None or st["dx_res"] or o.dil != 1 or o.cout % 8
+                    or o is self.win or up.kind != "up" or up.mode != "nearest" or up.out != x
+                    or not 1 < up.factor <= 8 or users.get(x) != [o] or p.view_spec(x)[0] != x):
+                continue
+            kk = o.k + up.factor - 1
+            self.up_dgrad[o.out] = (up, nxt)
+            self.skip_up.add(up.out)
+            self.wup[o.w] = torch.zeros((o.cin, kk * kk, nhwc.cin_pad(o.cout)), dtype=torch.bfloat16,
+                                        device=self.device)
+
     def _probe_view(self, t):
         # shape-only view for layout queries (pointer-independent)
         root, off, c = self.plan.view_spec(t)
@@ -556,13 +586,13 @@ class Engine:
         e.record()
         return e
 
-    def _toc(self, ev, op, tag="fprop"):
+    def _toc(self, ev, op, tag="fprop", flops=None):
         if ev is None:
             return
         e = self._event()
         e.record()
         n, _, h, w = self.plan.shapes[op.out]
-        self.conv_events.append((ev, e, 2 * op.k * op.k * op.cin * op.cout * n * h * w, tag))
+        self.conv_events.append((ev, e, flops or 2 * op.k * op.k * op.cin * op.cout * n * h * w, tag))
 
     def conv_kernel_totals(self, by_pass=False):
         """(ms, algorithmic FLOPs) summed over the timed conv launches (fprop, dgrad, wgrad);
@@ -645,6 +675,11 @@ class Engine:
             o = self.win
             nhwc.pack_weights(self.wslice(o.w), o.k, 1, o.k * o.cin, o.cout, fprop=self.wwin)
             self.launches += 1
+        for o in self.convs:
+            if o.w in self.wup:
+                up = self.up_dgrad[o.out][0]
+                nhwc.pack_upsampled_dgrad(self.wslice(o.w), o.k, o.cin, o.cout, up.factor, self.wup[o.w])
+                self.launches += 1
 
     # ---------------------------------------------------------------- inputs
     def set_batch(self, x_nchw: torch.Tensor, labels: torch.Tensor):
@@ -851,6 +886,16 @@ class Engine:
                     nhwc.dgrad_1x1_small(gy, self.wslice(op.w), self.gv(op.ins[0]), accumulate=st["dx"],
                                          mask=self.v(op.ins[0]) if st["mask_dx"] else None)
                     self.launches += 1
+                elif op.out in self.up_dgrad:
+                    # dgrad + the upsample's VJP in one strided low-resolution conv (executed FLOPs)
+                    up, ust = self.up_dgrad[op.out]
+                    f, kk = up.factor, op.k + up.factor - 1
+                    n, _, h, w = self.plan.shapes[up.ins[0]]
+                    ev = self._tic()
+                    nhwc.upsampled_dgrad(gy, self.wup[op.w], op.cin, op.k, f, self.gv(up.ins[0]),
+                                         accumulate=ust["dx"], mask=self.v(up.ins[0]) if ust["mask"] else None)
+                    self._toc(ev, op, "dgrad", flops=2 * kk * kk * op.cin * op.cout * n * h * w)
+                    self.launches += 1
                 elif st["dx"] is not None:
                     ev = self._tic()
                     wsrc = dict(w_dgrad=self.wd[op.w]) if op.w in self.wd else dict(
@@ -892,6 +937,8 @@ class Engine:
                     self.gv(op.out), self.gv(op.ins[0]), op.factor, accumulate=st["dx"],
                     mask=self.v(op.ins[0]) if st["mask"] else None)
                 self.launches += 1
+            elif op.kind == "up" and op.out in self.skip_up:
+                pass   # folded into the consuming conv's dgrad
             elif op.kind == "up":
                 (nhwc.f32_upsample_bwd if self.fp32 else nhwc.upsample_bwd)(
                     self.gv(op.out), self.gv(op.ins[0]), op.factor, accumulate=st["dx"],

@@ -68,14 +68,15 @@ def same_pads(k: int, d: int):
 
 def conv_fprop(x: View, w_packed: torch.Tensor | None, cout: int, kh: int, kw: int, dilation: int,
                y: View, bias=None, residual: View | None = None, relu=False, accumulate=False,
-               mask: View | None = None, y_f32=False, pads=None, block_n=0, w_master=None, w_mode=0, window=0):
+               mask: View | None = None, y_f32=False, pads=None, block_n=0, w_master=None, w_mode=0, window=0,
+               in_stride=0):
     """w_mode 0: w_packed bf16 [cout][taps][cin_pad]; 1: w_master bf16 HWIO of this conv;
     2: w_master bf16 HWIO of the forward conv whose input gradient this is (see b2dl.h).
     window > 0: row-window mode over a haloed x (pass kw=1; see b2dl_conv_args.window)."""
     pt, pl = pads if pads is not None else (same_pads(kh, dilation)[0], same_pads(kw, dilation)[0])
     a = ConvArgs(x.act(), _ptr(w_packed), cout, kh, kw, dilation, pt, pl,
                  y.act(), int(y_f32), _ptr(bias), _act(residual), int(relu), int(accumulate),
-                 _act(mask), block_n, _ptr(w_master), w_mode, window)
+                 _act(mask), block_n, _ptr(w_master), w_mode, window, in_stride)
     check(LIB.b2dl_conv_fprop(ctypes.byref(a), _stream()), "conv_fprop")
 
 
@@ -174,6 +175,20 @@ def head_backward(dy: View, w_hwio: torch.Tensor, x: View, dx: View | None, dw_p
     check(LIB.b2dl_head_backward(dy.act(), ctypes.c_void_p(w_hwio.data_ptr()), x.act(), _act(dx), int(accumulate),
                                  int(mask_dx), ctypes.c_void_p(dw_partials.data_ptr()),
                                  ctypes.c_void_p(db_partials.data_ptr()), _stream()), "head_backward")
+
+
+def pack_upsampled_dgrad(w_hwio: torch.Tensor, k: int, cin: int, cout: int, f: int, out: torch.Tensor):
+    """Merged weights of the (dgrad + nearest-upsample VJP) of a k x k conv over an x f upsampling."""
+    check(LIB.b2dl_pack_upsampled_dgrad(ctypes.c_void_p(w_hwio.data_ptr()), k, cin, cout, f,
+                                        ctypes.c_void_p(out.data_ptr()), _stream()), "pack_upsampled_dgrad")
+
+
+def upsampled_dgrad(dy: View, w_merged: torch.Tensor, cin: int, k: int, f: int, dx: View, accumulate=False,
+                    mask: View | None = None):
+    """dx (low resolution) (+)= block-summed input gradient of a k x k 'same' conv whose input was a
+    nearest x f upsampling of dx's tensor: one (k+f-1)^2-tap conv over dy with input stride f."""
+    kk, pad = k + f - 1, k - 1 - (k - 1) // 2
+    conv_fprop(dy, w_merged, cin, kk, kk, 1, dx, accumulate=accumulate, mask=mask, pads=(pad, pad), in_stride=f)
 
 
 def nchw_to_nhwc_halo(x: torch.Tensor, y: torch.Tensor, left: int):

@@ -264,3 +264,27 @@ def test_partial_last_n_tile_many_tiles_per_cta(cout, k):
     ref = F.conv2d(xr, wr, padding=(k - 1) // 2).permute(0, 2, 3, 1)
     ref = torch.where(mask.double() > 0, ref, torch.zeros_like(ref))
     assert _rel(y, ref) < 1e-2
+
+
+@pytest.mark.parametrize("n,cin,h,w,cout,k,f", [(2, 64, 9, 12, 64, 3, 4), (1, 256, 8, 6, 256, 3, 4),
+                                                 (2, 32, 7, 5, 48, 3, 2), (1, 64, 6, 8, 64, 5, 2)])
+def test_upsampled_dgrad_equals_dgrad_plus_block_sum(n, cin, h, w, cout, k, f):
+    """Input gradient of a k x k conv over a nearest x f upsampling, block-summed (the upsample VJP),
+    computed as one strided conv with merged weights == autograd through upsample + conv (fp64)."""
+    from paper_1810_01993_b200 import nhwc
+    torch.manual_seed(11)
+    w_hwio = torch.randn(k * k, cin, cout, device="cuda") / (k * k * cin) ** 0.5
+    dy = torch.randn(n, h * f, w * f, cout, device="cuda").to(torch.bfloat16)
+    mask = torch.randn(n, h, w, cin, device="cuda").to(torch.bfloat16)
+    kk = k + f - 1
+    wm = torch.empty(cin, kk * kk, nhwc.cin_pad(cout), dtype=torch.bfloat16, device="cuda")
+    nhwc.pack_upsampled_dgrad(w_hwio, k, cin, cout, f, wm)
+    dx = torch.empty(n, h, w, cin, dtype=torch.bfloat16, device="cuda")
+    nhwc.upsampled_dgrad(nhwc.View(dy), wm, cin, k, f, nhwc.View(dx), mask=nhwc.View(mask))
+    x = torch.zeros(n, cin, h, w, dtype=torch.float64, device="cuda", requires_grad=True)
+    xu = x.repeat_interleave(f, 2).repeat_interleave(f, 3)
+    wr = w_hwio.double().reshape(k, k, cin, cout).permute(3, 2, 0, 1)
+    F.conv2d(xu, wr, padding=(k - 1) // 2).backward(dy.double().permute(0, 3, 1, 2))
+    ref = x.grad.permute(0, 2, 3, 1)
+    ref = torch.where(mask.double() > 0, ref, torch.zeros_like(ref))
+    assert _rel(dx, ref) < 1e-2   # merged weights are rounded to bf16 once
