@@ -118,6 +118,13 @@ typedef struct b2dl_conv_args {
    * upsampling by s, already summed over each s x s block (the upsample VJP): one conv at the
    * low resolution instead of a full-resolution dgrad plus a block sum. */
   int in_stride;
+  /* Output phase view (out_stride f > 1): y is the full-resolution tensor and the conv writes
+   * output pixel (i, j) to y pixel (f*i + out_phase_h, f*j + out_phase_w); y.h == f*x.h,
+   * y.w == f*x.w.  No residual / mask / accumulate, bf16 y.  With the merged weights of
+   * b2dl_pack_upsampled_fprop, the f*f phase launches are the forward of a conv over a nearest
+   * upsampling by f, computed from the low-resolution input (no upsampled tensor). */
+  int out_stride;
+  int out_phase_h, out_phase_w;
 } b2dl_conv_args;
 
 B2DL_API int b2dl_cin_pad(int cin);
@@ -171,6 +178,13 @@ B2DL_API int b2dl_pack_weights(const float* w_hwio, int kh, int kw, int cin, int
  * same padding (k-1)/2) applied to a nearest upsampling by f; out is packed bf16
  * [cin][(k+f-1)^2][cin_pad(cout)] with W'(o) = sum over taps t, block offsets b with b - t = o of
  * W(t)^T (pads: pad_top = pad_left = (k-1)/2, in_stride f, kernel k+f-1, w_mode 0). */
+/* Phase weights of a "same" k x k conv over a nearest x f upsampling: for output phase
+ * (a, b) (row-major) a bf16 HWIO block [ka*kb][cin][cout] where ka spans the low-resolution
+ * row offsets floor((a + t - (k-1)/2) / f), t = 0..k-1, and taps landing on one offset are
+ * summed.  b2dl_upsampled_fprop_taps(k, f) = total taps over all phases (the buffer holds
+ * taps * cin * cout bf16). */
+B2DL_API int b2dl_upsampled_fprop_taps(int k, int f);
+B2DL_API int b2dl_pack_upsampled_fprop(const float* w_hwio, int k, int cin, int cout, int f, void* out, void* stream);
 B2DL_API int b2dl_pack_upsampled_dgrad(const float* w_hwio, int k, int cin, int cout, int f, void* out, void* stream);
 
 /* NCHW fp32 -> NHWC view, bf16 (or fp32 when dst_f32) (input tiles, reference-layout tensors). */

@@ -37,7 +37,8 @@ class ConvArgs(ctypes.Structure):
                 ("y_f32", ctypes.c_int), ("bias", ctypes.c_void_p), ("residual", Act),
                 ("relu", ctypes.c_int), ("accumulate", ctypes.c_int), ("mask", Act),
                 ("block_n", ctypes.c_int), ("w_master", ctypes.c_void_p), ("w_mode", ctypes.c_int),
-                ("window", ctypes.c_int), ("in_stride", ctypes.c_int)]
+                ("window", ctypes.c_int), ("in_stride", ctypes.c_int), ("out_stride", ctypes.c_int),
+                ("out_phase_h", ctypes.c_int), ("out_phase_w", ctypes.c_int)]
 
 
 class WgradArgs(ctypes.Structure):
@@ -99,6 +100,8 @@ _SIGS = {
     "b2dl_head_backward_parts": (_c_int, []),
     "b2dl_head_backward": (_c_int, [Act, _vp, Act, Act, _c_int, _c_int, _vp, _vp, _vp]),
     "b2dl_pack_upsampled_dgrad": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp]),
+    "b2dl_pack_upsampled_fprop": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp]),
+    "b2dl_upsampled_fprop_taps": (_c_int, [_c_int, _c_int]),
     "b2dl_nchw_to_nhwc_halo": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _c_int, _vp]),
     "b2dl_nhwc_to_nchw": (_c_int, [Act, _c_int, _vp, _vp]),
     "b2dl_avgpool_fwd": (_c_int, [Act, Act, _c_int, _vp]),

@@ -125,6 +125,7 @@ struct FpropParams {
   int epi_slots;       // operand slots per sub-group (prefetch depth + 1)
   int bias_vec;        // bias 16-byte aligned
   int in_stride;       // input pixels per output pixel (strided reads of the input)
+  int y_phase;         // output is a phase view of a larger tensor: TMA epilogue only
 };
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
@@ -1347,8 +1348,93 @@ __global__ void __launch_bounds__(192, 1)
 __global__ void reduce_segments_kernel(const b2dl_segment* __restrict__ segs, float* __restrict__ base) {
   const b2dl_segment sg = segs[blockIdx.y];
   float* dst = base + sg.dst_off;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < sg.n;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  const long long t0 = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  const bool vec = (sg.n & 3) == 0 && ((reinterpret_cast<uintptr_t>(sg.src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+  if (sg.parts >= 16 && sg.n <= (vec ? 16384 : 4096) && blockDim.x == 256) {
+    // short rows, many partials (bias column sums: splits x m-tiles rows; the head's 4 x #SMs
+    // parts): G = 256 / cols thread groups each sum every G-th partial of a column, then group 0
+    // folds the G group sums in order -- a fixed tree (deterministic) with G independent load
+    // chains instead of one
+    __shared__ float4 red[256];
+    const long long nu = vec ? sg.n >> 2 : sg.n;   // 16-byte or 4-byte units per row
+    int cols = sg.parts >= 64 ? 8 : 32;
+    while (cols > 1 && cols / 2 >= nu) cols >>= 1;
+    const int groups = 256 / cols;
+    const int col = threadIdx.x % cols, g = threadIdx.x / cols;
+    const float4* src4 = reinterpret_cast<const float4*>(sg.src);
+    float4* dst4 = reinterpret_cast<float4*>(dst);
+    for (long long c0 = static_cast<long long>(blockIdx.x) * cols; c0 < nu; c0 += static_cast<long long>(gridDim.x) * cols) {
+      const long long i = c0 + col;
+      float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (i < nu) {
+#pragma unroll 4
+        for (int k = g; k < sg.parts; k += groups) {
+          if (vec) {
+            const float4 v = __ldcs(src4 + k * nu + i);
+            s.x += v.x;
+            s.y += v.y;
+            s.z += v.z;
+            s.w += v.w;
+          } else {
+            s.x += __ldcs(sg.src + k * nu + i);
+          }
+        }
+      }
+      red[threadIdx.x] = s;
+      __syncthreads();
+      if (g == 0 && i < nu) {
+        float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (sg.accumulate) {
+          if (vec) t = dst4[i];
+          else t.x = dst[i];
+        }
+        for (int u = 0; u < groups; ++u) {
+          const float4 v = red[u * cols + col];
+          t.x += v.x;
+          t.y += v.y;
+          t.z += v.z;
+          t.w += v.w;
+        }
+        if (vec) dst4[i] = t;
+        else dst[i] = t.x;
+      }
+      __syncthreads();
+    }
+    return;
+  }
+  if (vec) {
+    // 16-byte lanes, 8 partial rows in flight per thread (same per-element summation order)
+    const long long n4 = sg.n >> 2;
+    const float4* src4 = reinterpret_cast<const float4*>(sg.src);
+    float4* dst4 = reinterpret_cast<float4*>(dst);
+    for (long long i = t0; i < n4; i += stride) {
+      float4 s = sg.accumulate ? dst4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+      int k = 0;
+      for (; k + 8 <= sg.parts; k += 8) {
+        float4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcs(src4 + (k + u) * n4 + i);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          s.x += v[u].x;
+          s.y += v[u].y;
+          s.z += v[u].z;
+          s.w += v[u].w;
+        }
+      }
+      for (; k < sg.parts; ++k) {
+        const float4 v = __ldcs(src4 + k * n4 + i);
+        s.x += v.x;
+        s.y += v.y;
+        s.z += v.z;
+        s.w += v.w;
+      }
+      dst4[i] = s;
+    }
+    return;
+  }
+  for (long long i = t0; i < sg.n; i += stride) {
     float s = sg.accumulate ? dst[i] : 0.f;
     const float* src = sg.src + i;
     int k = 0;
@@ -1402,6 +1488,7 @@ static int launch_fprop(const FpropMaps& t, FpropParams p, cudaStream_t st) {
     attr_set = true;
   }
   if (C::CW != 32) p.tma_epi = 0;
+  if (p.y_phase && !p.tma_epi) return B2DL_E_VALUE;
   p.epi_nops = p.tma_epi ? (p.res != nullptr) + (p.mask != nullptr) + (p.accumulate != 0) : 0;
   // operand prefetch depth (slots - 1 chunks ahead).  Measured: a third slot does not speed up
   // the epilogue-bound 1x1 layers (their chunks wait on instruction latency, not on the loads)
@@ -1590,7 +1677,16 @@ static int window_view(const b2dl_act& x, int window, int kw, int pad_left, int 
 
 extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
   if (!a || !a->x.ptr || !a->y.ptr || a->w_mode < 0 || a->w_mode > 2) return B2DL_E_VALUE;
-  const b2dl_act& y = a->y;
+  b2dl_act y = a->y;
+  const int s_out = a->out_stride > 0 ? a->out_stride : 1;
+  if (s_out > 1) {   // phase view: the kernel tiles the (h/f, w/f) output; the store map is strided
+    if (s_out > 8 || a->out_phase_h < 0 || a->out_phase_h >= s_out || a->out_phase_w < 0 ||
+        a->out_phase_w >= s_out || y.h % s_out || y.w % s_out || a->residual.ptr || a->mask.ptr || a->accumulate ||
+        a->y_f32 || a->window || a->in_stride > 1)
+      return B2DL_E_VALUE;
+    y.h /= s_out;
+    y.w /= s_out;
+  }
   b2dl_act x;
   if (window_view(a->x, a->window, a->kw, a->pad_left, y.w, &x)) return B2DL_E_VALUE;
   const int s_in = a->in_stride > 0 ? a->in_stride : 1;
@@ -1717,12 +1813,18 @@ extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
   p.tma_epi = p.vec_ok && !p.y_f32 && (a->cout % 8) == 0 && bn >= 32 && tma_epilogue_enabled() &&
               (!a->bias || p.bias_vec) &&
               ((p.res != nullptr) + (p.mask != nullptr) + (p.accumulate != 0)) <= 2;
+  p.y_phase = s_out > 1;
+  if (p.y_phase && !p.tma_epi) return B2DL_E_VALUE;
   if (p.tma_epi) {
     const int bwx = p.bw, bhx = p.bh;  // epilogue boxes: 32 channels x the whole tile
-    if (act_map(&t.y, y, 32, bwx, bhx, CU_TENSOR_MAP_SWIZZLE_64B) ||
+    if ((s_out > 1 ? act_map_phase(&t.y, a->y, s_out, a->out_phase_h, a->out_phase_w, 32, bwx, bhx,
+                                   CU_TENSOR_MAP_SWIZZLE_64B)
+                   : act_map(&t.y, y, 32, bwx, bhx, CU_TENSOR_MAP_SWIZZLE_64B)) ||
         (p.res && act_map(&t.r, a->residual, 32, bwx, bhx, CU_TENSOR_MAP_SWIZZLE_64B)) ||
-        (p.mask && act_map(&t.m, a->mask, 32, bwx, bhx, CU_TENSOR_MAP_SWIZZLE_64B)))
+        (p.mask && act_map(&t.m, a->mask, 32, bwx, bhx, CU_TENSOR_MAP_SWIZZLE_64B))) {
+      if (p.y_phase) return B2DL_E_ALIGN;
       p.tma_epi = 0;
+    }
   }
 
   cudaStream_t st = as_stream(stream);
@@ -1973,7 +2075,8 @@ extern "C" int b2dl_reduce_segments(const b2dl_segment* segs, int nseg, int64_t 
   if (!segs || nseg < 1 || !dst_base) return B2DL_E_VALUE;
   // fill the GPU (~8 blocks per SM) whether the table holds one conv's two segments or many
   const long long want = std::max<long long>(1, (8LL * num_sms() + nseg - 1) / nseg);
-  const int bx = static_cast<int>(std::max<long long>(1, std::min<long long>((max_n + 255) / 256, want)));
+  // (short segments are reduced 8 columns per block, see the kernel)
+  const int bx = static_cast<int>(std::max<long long>(1, std::min<long long>(std::max((max_n / 4 + 255) / 256, (max_n + 7) / 8), want)));
   dim3 grid(bx, nseg);
   reduce_segments_kernel<<<grid, 256, 0, as_stream(stream)>>>(segs, dst_base);
   return check_launch();

@@ -730,6 +730,63 @@ extern "C" int b2dl_pack_upsampled_dgrad(const float* w_hwio, int k, int cin, in
   return check_launch();
 }
 
+// Phase decomposition of a "same" k x k conv over a nearest x f upsampling: output row f*i + a
+// reads upsampled row f*i + a + t - P (P = (k-1)/2), i.e. low-resolution row i + d(a, t) with
+// d(a, t) = floor((a + t - P) / f).  Per phase a the offsets form the range [d(a,0), d(a,k-1)];
+// merged weights sum the taps that land on the same offset.  Output: the phases (a, b) in
+// row-major order, each a bf16 HWIO block [ka * kb][cin][cout] (ka = d(a,k-1) - d(a,0) + 1).
+__device__ __host__ inline int up_floordiv(int v, int f) { return v >= 0 ? v / f : -((-v + f - 1) / f); }
+
+__global__ void k_pack_upsampled_fprop(const float* __restrict__ w, __nv_bfloat16* __restrict__ out, int k, int cin,
+                                       int cout, int f) {
+  const int P = (k - 1) / 2;
+  const int kmax = up_floordiv(k - 1 + f - 1 - P, f) - up_floordiv(-P, f) + 1;
+  const long long per = static_cast<long long>(cin) * cout;
+  const long long total = static_cast<long long>(f) * f * kmax * kmax * per;
+  int S = 0;
+  for (int b = 0; b < f; ++b) S += up_floordiv(b + k - 1 - P, f) - up_floordiv(b - P, f) + 1;
+  for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long e = idx % per;
+    const long long r = idx / per;
+    const int dx = static_cast<int>(r % kmax), dy = static_cast<int>((r / kmax) % kmax);
+    const int ph = static_cast<int>(r / (kmax * kmax));
+    const int a = ph / f, b = ph % f;
+    const int a0 = up_floordiv(a - P, f), ka = up_floordiv(a + k - 1 - P, f) - a0 + 1;
+    const int b0 = up_floordiv(b - P, f), kb = up_floordiv(b + k - 1 - P, f) - b0 + 1;
+    if (dy >= ka || dx >= kb) continue;
+    int rows_before = 0, cols_before = 0;
+    for (int u = 0; u < a; ++u) rows_before += up_floordiv(u + k - 1 - P, f) - up_floordiv(u - P, f) + 1;
+    for (int u = 0; u < b; ++u) cols_before += up_floordiv(u + k - 1 - P, f) - up_floordiv(u - P, f) + 1;
+    const long long block = static_cast<long long>(rows_before) * S + static_cast<long long>(ka) * cols_before;
+    float v = 0.f;
+    for (int ty = 0; ty < k; ++ty) {
+      if (up_floordiv(a + ty - P, f) - a0 != dy) continue;
+      for (int tx = 0; tx < k; ++tx)
+        if (up_floordiv(b + tx - P, f) - b0 == dx) v += w[(ty * k + tx) * per + e];
+    }
+    out[(block + dy * kb + dx) * per + e] = __float2bfloat16_rn(v);
+  }
+}
+
+extern "C" int b2dl_upsampled_fprop_taps(int k, int f) {
+  if (k < 1 || k % 2 == 0 || f < 1) return -1;
+  const int P = (k - 1) / 2;
+  int S = 0;
+  for (int a = 0; a < f; ++a) S += up_floordiv(a + k - 1 - P, f) - up_floordiv(a - P, f) + 1;
+  return S * S;
+}
+
+extern "C" int b2dl_pack_upsampled_fprop(const float* w_hwio, int k, int cin, int cout, int f, void* out,
+                                         void* stream) {
+  if (!w_hwio || !out || k < 1 || k % 2 == 0 || f < 2 || f > 8 || cin < 1 || cout < 1) return B2DL_E_VALUE;
+  const int P = (k - 1) / 2;
+  const int kmax = up_floordiv(k - 1 + f - 1 - P, f) - up_floordiv(-P, f) + 1;
+  k_pack_upsampled_fprop<<<grid1d(static_cast<long long>(f) * f * kmax * kmax * cin * cout), 256, 0,
+                           as_stream(stream)>>>(w_hwio, BF(out), k, cin, cout, f);
+  return check_launch();
+}
+
 extern "C" int b2dl_head_backward_parts(void) { return 4 * num_sms(); }
 
 extern "C" int b2dl_head_backward(b2dl_act dy, const float* w_hwio, b2dl_act x, b2dl_act dx, int accumulate,

@@ -77,6 +77,20 @@ int act_map_strided(CUtensorMap* m, const b2dl_act& a, int box_c, int box_w, int
   return encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, a.ptr, dims, strides, box, sw, es);
 }
 
+// Phase view of a full-resolution NHWC tensor: pixel (i, j) of the (h/f, w/f) view is pixel
+// (f*i + ph, f*j + pw) -- plain strides of f pixels / f rows from a shifted base.
+int act_map_phase(CUtensorMap* m, const b2dl_act& a, int f, int ph, int pw, int box_c, int box_w, int box_h,
+                  CUtensorMapSwizzle sw) {
+  const uint64_t cs = static_cast<uint64_t>(a.c_stride) * 2;
+  const uint64_t dims[4] = {static_cast<uint64_t>(a.c), static_cast<uint64_t>(a.w / f),
+                            static_cast<uint64_t>(a.h / f), static_cast<uint64_t>(a.n)};
+  const uint64_t strides[3] = {cs * f, cs * a.w * f, cs * a.w * a.h};
+  const uint32_t box[4] = {static_cast<uint32_t>(box_c), static_cast<uint32_t>(box_w), static_cast<uint32_t>(box_h),
+                           1u};
+  char* base = static_cast<char*>(a.ptr) + (static_cast<uint64_t>(ph) * a.w + pw) * cs;
+  return encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, sw);
+}
+
 // Row-window view of a haloed NHWC image (conv window mode): virtual pixel (y, xx) holds the
 // c_v contiguous values x[y][xx..][..] starting at pixel xx, so neighbouring virtual pixels
 // overlap in memory (pixel stride < inner extent); TMA zero-fills virtual channels >= c_v.

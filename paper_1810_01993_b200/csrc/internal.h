@@ -19,6 +19,8 @@ int encode_tiled(CUtensorMap* m, CUtensorMapDataType dt, int rank, void* ptr, co
 int act_map(CUtensorMap* m, const b2dl_act& a, int box_c, int box_w, int box_h, CUtensorMapSwizzle sw);
 int window_map(CUtensorMap* m, const b2dl_act& x, int c_v, int w_v, int box_c, int box_w, int box_h,
                CUtensorMapSwizzle sw);
+int act_map_phase(CUtensorMap* m, const b2dl_act& a, int f, int ph, int pw, int box_c, int box_w, int box_h,
+                  CUtensorMapSwizzle sw);
 int act_map_strided(CUtensorMap* m, const b2dl_act& a, int box_c, int box_w, int box_h, int stride,
                     CUtensorMapSwizzle sw);
 int act_map5(CUtensorMap* m, const b2dl_act& a, int box_w, int box_h, int g);

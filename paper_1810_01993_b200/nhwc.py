@@ -69,14 +69,14 @@ def same_pads(k: int, d: int):
 def conv_fprop(x: View, w_packed: torch.Tensor | None, cout: int, kh: int, kw: int, dilation: int,
                y: View, bias=None, residual: View | None = None, relu=False, accumulate=False,
                mask: View | None = None, y_f32=False, pads=None, block_n=0, w_master=None, w_mode=0, window=0,
-               in_stride=0):
+               in_stride=0, out_stride=0, out_phase=(0, 0)):
     """w_mode 0: w_packed bf16 [cout][taps][cin_pad]; 1: w_master bf16 HWIO of this conv;
     2: w_master bf16 HWIO of the forward conv whose input gradient this is (see b2dl.h).
     window > 0: row-window mode over a haloed x (pass kw=1; see b2dl_conv_args.window)."""
     pt, pl = pads if pads is not None else (same_pads(kh, dilation)[0], same_pads(kw, dilation)[0])
     a = ConvArgs(x.act(), _ptr(w_packed), cout, kh, kw, dilation, pt, pl,
                  y.act(), int(y_f32), _ptr(bias), _act(residual), int(relu), int(accumulate),
-                 _act(mask), block_n, _ptr(w_master), w_mode, window, in_stride)
+                 _act(mask), block_n, _ptr(w_master), w_mode, window, in_stride, out_stride, *out_phase)
     check(LIB.b2dl_conv_fprop(ctypes.byref(a), _stream()), "conv_fprop")
 
 
@@ -189,6 +189,45 @@ def upsampled_dgrad(dy: View, w_merged: torch.Tensor, cin: int, k: int, f: int, 
     nearest x f upsampling of dx's tensor: one (k+f-1)^2-tap conv over dy with input stride f."""
     kk, pad = k + f - 1, k - 1 - (k - 1) // 2
     conv_fprop(dy, w_merged, cin, kk, kk, 1, dx, accumulate=accumulate, mask=mask, pads=(pad, pad), in_stride=f)
+
+
+def upsampled_fprop_phases(k: int, f: int):
+    """Per output phase (a, b) of a 'same' k x k conv over a nearest x f upsampling:
+    (a, b, ka, kb, pad_top, pad_left, first tap) -- the layout b2dl_pack_upsampled_fprop writes."""
+    P = (k - 1) // 2
+    rng = [((a - P) // f, (a + k - 1 - P) // f) for a in range(f)]
+    S = sum(hi - lo + 1 for lo, hi in rng)
+    out, rows = [], 0
+    for a, (la, ha) in enumerate(rng):
+        ka, cols = ha - la + 1, 0
+        for b, (lb, hb) in enumerate(rng):
+            kb = hb - lb + 1
+            out.append((a, b, ka, kb, -la, -lb, rows * S + ka * cols))
+            cols += kb
+        rows += ka
+    return out
+
+
+def pack_upsampled_fprop(w_hwio: torch.Tensor, k: int, cin: int, cout: int, f: int, out: torch.Tensor):
+    """Merged phase weights (bf16 HWIO blocks, upsampled_fprop_phases order) of a k x k conv over
+    a nearest x f upsampling; out holds b2dl_upsampled_fprop_taps(k, f) * cin * cout values."""
+    check(LIB.b2dl_pack_upsampled_fprop(ctypes.c_void_p(w_hwio.data_ptr()), k, cin, cout, f,
+                                        ctypes.c_void_p(out.data_ptr()), _stream()), "pack_upsampled_fprop")
+
+
+def upsampled_fprop_taps(k: int, f: int) -> int:
+    return LIB.b2dl_upsampled_fprop_taps(k, f)
+
+
+def upsampled_fprop(x: View, w_phases: torch.Tensor, cin: int, cout: int, k: int, f: int, y: View, bias=None,
+                    relu=False):
+    """y (full resolution) = conv_k(nearest_up_f(x)) + bias (relu), from the low-resolution x: one
+    launch per output phase, each a <= ceil-sized conv over x with merged weights writing a
+    stride-f phase view of y (no upsampled tensor; ~(1 + (k-1)/f)^2 / k^2 of the MACs)."""
+    per = cin * cout
+    for a, b, ka, kb, pt, pl, t0 in upsampled_fprop_phases(k, f):
+        conv_fprop(x, None, cout, ka, kb, 1, y, bias=bias, relu=relu, pads=(pt, pl),
+                   w_master=w_phases[t0 * per:(t0 + ka * kb) * per], w_mode=1, out_stride=f, out_phase=(a, b))
 
 
 def nchw_to_nhwc_halo(x: torch.Tensor, y: torch.Tensor, left: int):

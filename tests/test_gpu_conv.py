@@ -288,3 +288,58 @@ def test_upsampled_dgrad_equals_dgrad_plus_block_sum(n, cin, h, w, cout, k, f):
     ref = x.grad.permute(0, 2, 3, 1)
     ref = torch.where(mask.double() > 0, ref, torch.zeros_like(ref))
     assert _rel(dx, ref) < 1e-2   # merged weights are rounded to bf16 once
+
+
+@pytest.mark.gpu
+def test_reduce_segments_paths():
+    """Split-K partial reduction over a table of segments covering every kernel path (long rows in
+    16-byte lanes, short rows with many partials -- vector and scalar -- and unaligned rows):
+    equal to the fp64 sum, and bitwise repeatable."""
+    from paper_1810_01993_b200 import nhwc
+    torch.manual_seed(5)
+    cases = [(590_000, 16, 0, 0), (256, 144, 1, 0), (768, 592, 0, 0), (3, 592, 1, 0), (1001, 7, 1, 1),
+             (64, 40, 0, 2), (20_000, 3, 1, 0)]
+    srcs, segs, ref = [], [], []
+    dst = torch.randn(sum(n + 8 for n, *_ in cases), device="cuda")
+    dst0 = dst.clone()
+    off = 0
+    for n, parts, acc, mis in cases:
+        buf = torch.randn(parts * n + mis, device="cuda")
+        srcs.append(buf)
+        src = buf[mis:]
+        segs.append((src.data_ptr(), off + mis, n, parts, acc))
+        r = src.double().view(parts, n).sum(0)
+        if acc:
+            r = r + dst0[off + mis:off + mis + n].double()
+        ref.append((off + mis, n, r))
+        off += n + 8
+    table = nhwc.segment_table(segs, "cuda")
+    max_n = max(n for n, *_ in cases)
+    nhwc.reduce_segments(table, len(segs), max_n, dst)
+    first = dst.clone()
+    for o, n, r in ref:
+        assert torch.allclose(dst[o:o + n].double(), r, rtol=1e-5, atol=1e-4)
+    dst.copy_(dst0)
+    nhwc.reduce_segments(table, len(segs), max_n, dst)
+    assert torch.equal(dst, first)
+
+
+@pytest.mark.parametrize("n,cin,h,w,cout,k,f", [(1, 64, 6, 8, 64, 3, 4), (2, 256, 9, 12, 256, 3, 4), (1, 128, 8, 8, 64, 3, 2),
+                                                (1, 64, 5, 7, 128, 5, 4), (1, 64, 4, 6, 64, 1, 4)])
+def test_upsampled_fprop_equals_conv_of_upsampling(n, cin, h, w, cout, k, f):
+    """Forward of a k x k conv over a nearest x f upsampling, computed per output phase from the
+    low-resolution input with merged weights (stride-f phase views of y) == conv2d(upsample) (fp64)."""
+    from paper_1810_01993_b200 import nhwc
+    torch.manual_seed(12)
+    w_hwio = torch.randn(k * k, cin, cout, device="cuda") / (k * k * cin) ** 0.5
+    x = torch.randn(n, h, w, cin, device="cuda").to(torch.bfloat16)
+    bias = torch.randn(cout, device="cuda")
+    wp = torch.empty(nhwc.upsampled_fprop_taps(k, f) * cin * cout, dtype=torch.bfloat16, device="cuda")
+    nhwc.pack_upsampled_fprop(w_hwio, k, cin, cout, f, wp)
+    y = torch.full((n, h * f, w * f, cout), float("nan"), dtype=torch.bfloat16, device="cuda")
+    nhwc.upsampled_fprop(nhwc.View(x), wp, cin, cout, k, f, nhwc.View(y), bias=bias, relu=True)
+    xu = x.double().permute(0, 3, 1, 2).repeat_interleave(f, 2).repeat_interleave(f, 3)
+    wr = w_hwio.double().reshape(k, k, cin, cout).permute(3, 2, 0, 1)
+    ref = torch.relu(F.conv2d(xu, wr, padding=(k - 1) // 2) + bias.double()[None, :, None, None]).permute(0, 2, 3, 1)
+    assert not torch.isnan(y).any()
+    assert _rel(y, ref) < 1e-2   # merged weights are rounded to bf16 once
