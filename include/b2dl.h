@@ -185,6 +185,14 @@ B2DL_API int b2dl_pack_weights(const float* w_hwio, int kh, int kw, int cin, int
  * taps * cin * cout bf16). */
 B2DL_API int b2dl_upsampled_fprop_taps(int k, int f);
 B2DL_API int b2dl_pack_upsampled_fprop(const float* w_hwio, int k, int cin, int cout, int f, void* out, void* stream);
+/* Weight gradient of a "same" k x k conv (k in {1, 3}) over a nearest x f upsampling without the
+ * upsampled tensor: g[n][h/f][w/f][k*k][c] (bf16) = the f x f block sums of dy shifted by
+ * (k-1)/2 - t for every tap t; then dW = x_low^T g is a 1x1 wgrad with k*k*c output channels
+ * (b2dl_conv_wgrad, defer_reduce) whose split-K partials b2dl_upsampled_wgrad_reduce sums in
+ * fixed order into HWIO dw[k*k][cin][cout], and db[cout] from the centre tap's column sums. */
+B2DL_API int b2dl_upsampled_wgrad_sums(b2dl_act dy, int k, int f, void* g, void* stream);
+B2DL_API int b2dl_upsampled_wgrad_reduce(const void* partials, int w_parts, int b_parts, size_t b_offset, int cin,
+                                         int k, int cout, float* dw, float* db, void* stream);
 B2DL_API int b2dl_pack_upsampled_dgrad(const float* w_hwio, int k, int cin, int cout, int f, void* out, void* stream);
 
 /* NCHW fp32 -> NHWC view, bf16 (or fp32 when dst_f32) (input tiles, reference-layout tensors). */

@@ -102,6 +102,9 @@ _SIGS = {
     "b2dl_pack_upsampled_dgrad": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp]),
     "b2dl_pack_upsampled_fprop": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp]),
     "b2dl_upsampled_fprop_taps": (_c_int, [_c_int, _c_int]),
+    "b2dl_upsampled_wgrad_sums": (_c_int, [Act, _c_int, _c_int, _vp, _vp]),
+    "b2dl_upsampled_wgrad_reduce": (_c_int, [_vp, _c_int, _c_int, ctypes.c_size_t, _c_int, _c_int, _c_int, _vp, _vp,
+                                             _vp]),
     "b2dl_nchw_to_nhwc_halo": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _c_int, _vp]),
     "b2dl_nhwc_to_nchw": (_c_int, [Act, _c_int, _vp, _vp]),
     "b2dl_avgpool_fwd": (_c_int, [Act, Act, _c_int, _vp]),

@@ -787,6 +787,139 @@ extern "C" int b2dl_pack_upsampled_fprop(const float* w_hwio, int k, int cin, in
   return check_launch();
 }
 
+// Weight gradient of a "same" K x K conv over a nearest x f upsampling, from the low-resolution
+// input: dW[t] = sum_q x_up[q] dy[q + P - t] = sum_i x[i] G_t[i] with
+//   G_t[i] = sum over the f x f block of low-resolution pixel i of dy shifted by P - t
+// (zero outside the image).  One thread per (pixel i, 8 channels): the (f+K-1)^2 dy pixels
+// around the block, K horizontal window sums per row, accumulated into the K*K outputs.
+// G: [n][h][w][K*K][c] bf16, so dW = x^T G is one 1x1 wgrad with K*K*c output channels.
+template <int K>
+__global__ void k_upsampled_wgrad_sums(const __nv_bfloat16* __restrict__ dy, int dys, int n, int H, int W, int c,
+                                       int f, __nv_bfloat16* __restrict__ g) {
+  constexpr int P = (K - 1) / 2;
+  const int h = H / f, w = W / f, cv = c / 8;
+  const long long total = static_cast<long long>(n) * h * w * cv;
+  for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int ch = static_cast<int>(idx % cv) * 8;
+    long long r = idx / cv;
+    const int j = static_cast<int>(r % w);
+    r /= w;
+    const int i = static_cast<int>(r % h);
+    const int b = static_cast<int>(r / h);
+    float acc[K * K][8];
+#pragma unroll
+    for (int t = 0; t < K * K; ++t)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[t][e] = 0.f;
+    // rows f*i + rr for rr in [P - (K-1), f - 1 + P]; row window of tap ty: [P - ty, P - ty + f - 1]
+    for (int rr = P - (K - 1); rr <= f - 1 + P; ++rr) {
+      const int y = f * i + rr;
+      if (y < 0 || y >= H) continue;
+      float rs[K][8];
+#pragma unroll
+      for (int tx = 0; tx < K; ++tx)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) rs[tx][e] = 0.f;
+      const __nv_bfloat16* row = dy + (static_cast<long long>(b) * H + y) * W * dys + ch;
+      for (int cc = P - (K - 1); cc <= f - 1 + P; ++cc) {
+        const int x = f * j + cc;
+        if (x < 0 || x >= W) continue;
+        float v[8];
+        ldv<8>(row + static_cast<long long>(x) * dys, v);
+#pragma unroll
+        for (int tx = 0; tx < K; ++tx)
+          if (cc >= P - tx && cc <= P - tx + f - 1)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) rs[tx][e] += v[e];
+      }
+#pragma unroll
+      for (int ty = 0; ty < K; ++ty)
+        if (rr >= P - ty && rr <= P - ty + f - 1)
+#pragma unroll
+          for (int tx = 0; tx < K; ++tx)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[ty * K + tx][e] += rs[tx][e];
+    }
+    __nv_bfloat16* out = g + (((static_cast<long long>(b) * h + i) * w + j) * (K * K)) * c + ch;
+#pragma unroll
+    for (int t = 0; t < K * K; ++t) stv<8>(out + static_cast<long long>(t) * c, acc[t]);
+  }
+}
+
+// dW[t][ci][co] = sum_s ws[s][ci][t][co]; db[co] = sum_b bsum[b][center][co]   (fixed order)
+__global__ void k_upsampled_wgrad_reduce(const float* __restrict__ ws, int wp, const float* __restrict__ bsum, int bp,
+                                         int cin, int taps, int cout, int center, float* __restrict__ dw,
+                                         float* __restrict__ db) {
+  const int c4 = cout / 4;
+  const long long nw = static_cast<long long>(taps) * cin * c4;
+  const long long part = static_cast<long long>(cin) * taps * cout;
+  for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < nw + c4;
+       idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (idx < nw) {
+      const int co = static_cast<int>(idx % c4) * 4;
+      const long long r = idx / c4;
+      const int ci = static_cast<int>(r % cin), t = static_cast<int>(r / cin);
+      const float* src = ws + (static_cast<long long>(ci) * taps + t) * cout + co;
+#pragma unroll 8
+      for (int k = 0; k < wp; ++k) {
+        const float4 v = __ldcs(reinterpret_cast<const float4*>(src + k * part));
+        s.x += v.x;
+        s.y += v.y;
+        s.z += v.z;
+        s.w += v.w;
+      }
+      *reinterpret_cast<float4*>(dw + (static_cast<long long>(t) * cin + ci) * cout + co) = s;
+    } else if (db) {
+      const int co = static_cast<int>(idx - nw) * 4;
+      const float* src = bsum + static_cast<long long>(center) * cout + co;
+#pragma unroll 8
+      for (int k = 0; k < bp; ++k) {
+        const float4 v = __ldcs(reinterpret_cast<const float4*>(src + static_cast<long long>(k) * taps * cout));
+        s.x += v.x;
+        s.y += v.y;
+        s.z += v.z;
+        s.w += v.w;
+      }
+      *reinterpret_cast<float4*>(db + co) = s;
+    }
+  }
+}
+
+extern "C" int b2dl_upsampled_wgrad_sums(b2dl_act dy, int k, int f, void* g, void* stream) {
+  if (!dy.ptr || !g || f < 2 || f > 8 || dy.h % f || dy.w % f) return B2DL_E_VALUE;
+  if (dy.c % 8 || !vec_ok(dy)) return B2DL_E_ALIGN;
+  const long long total = static_cast<long long>(dy.n) * (dy.h / f) * (dy.w / f) * (dy.c / 8);
+  switch (k) {
+    case 1:
+      k_upsampled_wgrad_sums<1><<<grid1d(total), 256, 0, as_stream(stream)>>>(CBF(dy.ptr), dy.c_stride, dy.n, dy.h,
+                                                                              dy.w, dy.c, f, BF(g));
+      break;
+    case 3:
+      k_upsampled_wgrad_sums<3><<<grid1d(total), 256, 0, as_stream(stream)>>>(CBF(dy.ptr), dy.c_stride, dy.n, dy.h,
+                                                                              dy.w, dy.c, f, BF(g));
+      break;
+    default:
+      return B2DL_E_VALUE;
+  }
+  return check_launch();
+}
+
+extern "C" int b2dl_upsampled_wgrad_reduce(const void* partials, int w_parts, int b_parts, size_t b_offset, int cin,
+                                           int k, int cout, float* dw, float* db, void* stream) {
+  if (!partials || !dw || cin < 1 || cout % 4 || k < 1 || k % 2 == 0 || w_parts < 1 ||
+      (reinterpret_cast<uintptr_t>(partials) | reinterpret_cast<uintptr_t>(dw) | b_offset) & 15 ||
+      (db && (reinterpret_cast<uintptr_t>(db) & 15)))
+    return B2DL_E_VALUE;
+  const int taps = k * k, center = (k / 2) * k + k / 2;
+  const float* ws = static_cast<const float*>(partials);
+  const float* bs = reinterpret_cast<const float*>(static_cast<const char*>(partials) + b_offset);
+  k_upsampled_wgrad_reduce<<<grid1d(static_cast<long long>(taps) * cin * cout / 4 + cout / 4), 256, 0,
+                             as_stream(stream)>>>(ws, w_parts, bs, b_parts, cin, taps, cout, center, dw, db);
+  return check_launch();
+}
+
 extern "C" int b2dl_head_backward_parts(void) { return 4 * num_sms(); }
 
 extern "C" int b2dl_head_backward(b2dl_act dy, const float* w_hwio, b2dl_act x, b2dl_act dx, int accumulate,

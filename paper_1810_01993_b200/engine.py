@@ -485,9 +485,28 @@ class Engine:
                     self.up_fprop[o.out] = up
                     self.wupf[o.w] = torch.zeros(nhwc.upsampled_fprop_taps(o.k, up.factor) * o.cin * o.cout,
                                                  dtype=torch.bfloat16, device=self.device)
+        # ... and its weight gradient: x_low^T (shifted f x f block sums of dy), one 1x1 wgrad at the
+        # low resolution (b2dl_upsampled_wgrad_sums / _reduce).  With all three the upsampled
+        # tensor itself is never formed.
+        self.up_wgrad, self.gsum, self.up_layout = {}, {}, {}
+        if not self.fp32 and os.environ.get("B2DL_UP_WGRAD", "1") != "0":
+            for o in self.convs:
+                up = self.up_fprop.get(o.out)
+                if up is not None and o.k in (1, 3):
+                    n_, _, h_, w_ = p.shapes[up.ins[0]]
+                    self.up_wgrad[o.out] = up
+                    self.gsum[o.w] = torch.empty(n_ * h_ * w_ * o.k * o.k * o.cout, dtype=torch.bfloat16,
+                                                 device=self.device)
+        self.dead_up = {self.up_fprop[o].out for o in self.up_wgrad if o in self.up_dgrad}
         hparts = nhwc.head_backward_parts()
         for o in self.convs:
             if self.fp32:   # fp32 wgrad reduces its split-K partials itself, into flat_g
+                continue
+            if o.out in self.up_wgrad:
+                lay = nhwc.upsampled_wgrad_layout(self._probe_view(self.up_wgrad[o.out].ins[0]), o.cout, o.k)
+                self.up_layout[o.w] = lay
+                offs[o.w] = (total,) + tuple(lay)
+                total += (lay[0] + 255) // 256 * 256
                 continue
             if o.w in self.heads:
                 nw = hparts * o.cin * o.cout * 4
@@ -513,6 +532,8 @@ class Engine:
             self.partials[o.w] = buf
             if o.w in self.heads:
                 self.head_parts[o.w] = (buf[:bo].view(torch.float32), buf[bo:].view(torch.float32))
+            if o.out in self.up_wgrad:
+                continue   # reduced (and permuted to HWIO) by b2dl_upsampled_wgrad_reduce
             base = buf.data_ptr()
             n_w = o.k * o.k * o.cin * o.cout
             self.segs[o.w] = (base, self.slot[o.w][0], n_w, wp, 0)
@@ -801,6 +822,8 @@ class Engine:
         elif op.kind == "pool":
             (nhwc.f32_avgpool_fwd if self.fp32 else nhwc.avgpool_fwd)(self.v(op.ins[0]), self.v(op.out),
                                                                       op.factor)
+        elif op.kind == "up" and op.out in self.dead_up:
+            return   # its only consumer reads the low-resolution input directly (fwd, dgrad, wgrad)
         elif op.kind == "up":
             (nhwc.f32_upsample_fwd if self.fp32 else nhwc.upsample_fwd)(self.v(op.ins[0]), self.v(op.out),
                                                                         op.factor)
@@ -893,9 +916,20 @@ class Engine:
                     elif op is self.win:
                         nhwc.conv_wgrad_deferred(View(self.xwin), gy, op.k, 1, 1, self.partials[op.w],
                                                  window=op.k)
+                    elif op.out in self.up_wgrad:
+                        up = self.up_wgrad[op.out]
+                        w_off, _ = self.slot[op.w]
+                        b_off, _ = self.slot[op.b]
+                        nhwc.upsampled_wgrad(self.v(up.ins[0]), gy, op.k, up.factor, self.gsum[op.w],
+                                             self.partials[op.w], self.up_layout[op.w],
+                                             self.flat_g[w_off:w_off + op.k * op.k * op.cin * op.cout],
+                                             self.flat_g[b_off:b_off + op.cout])
+                        n, _, h, w = self.plan.shapes[up.ins[0]]
+                        self.launches += 2
+                        wflops = 2 * op.k * op.k * op.cin * op.cout * n * h * w
                     else:
                         nhwc.conv_wgrad_deferred(self.v(op.ins[0]), gy, op.k, op.k, op.dil, self.partials[op.w])
-                    self._toc(ev, op, "wgrad")
+                    self._toc(ev, op, "wgrad", flops=wflops if op.out in self.up_wgrad else None)
                     self.launches += 1
                     self._reduce_conv(op)
                     for name in (op.w, op.b):

@@ -230,6 +230,34 @@ def upsampled_fprop(x: View, w_phases: torch.Tensor, cin: int, cout: int, k: int
                    w_master=w_phases[t0 * per:(t0 + ka * kb) * per], w_mode=1, out_stride=f, out_phase=(a, b))
 
 
+def upsampled_wgrad_sums(dy: View, k: int, f: int, g: torch.Tensor):
+    """g [n][h/f][w/f][k*k][c] bf16 = shifted f x f block sums of dy (see b2dl_upsampled_wgrad_sums)."""
+    check(LIB.b2dl_upsampled_wgrad_sums(dy.act(), k, f, ctypes.c_void_p(g.data_ptr()), _stream()),
+          "upsampled_wgrad_sums")
+
+
+def upsampled_wgrad_layout(x: View, cout: int, k: int):
+    """Partial-buffer layout (bytes, weight parts, bias parts, bias offset) of the 1x1 wgrad
+    x_low^T g of a k x k conv over a nearest upsampling."""
+    n, h, w, _ = x.shape
+    g = View(torch.empty((n, h, w, k * k * cout), dtype=torch.bfloat16, device="meta"))
+    return wgrad_partials(x, g, 1, 1, 1)
+
+
+def upsampled_wgrad(x: View, dy: View, k: int, f: int, g: torch.Tensor, partials: torch.Tensor, layout,
+                    dw: torch.Tensor, db: torch.Tensor | None):
+    """dw HWIO [k*k][cin][cout] (fp32) and db[cout] of a k x k 'same' conv whose input was the nearest
+    x f upsampling of x: block sums of dy, one 1x1 wgrad at the low resolution, a permuting reduce."""
+    upsampled_wgrad_sums(dy, k, f, g)
+    n, h, w, cin = x.shape
+    cout = dy.c
+    conv_wgrad_deferred(x, View(g.view(n, h, w, k * k * cout)), 1, 1, 1, partials)
+    _, wp, bp, bo = layout
+    check(LIB.b2dl_upsampled_wgrad_reduce(ctypes.c_void_p(partials.data_ptr()), wp, bp, bo, cin, k, cout,
+                                          ctypes.c_void_p(dw.data_ptr()), _ptr(db), _stream()),
+          "upsampled_wgrad_reduce")
+
+
 def nchw_to_nhwc_halo(x: torch.Tensor, y: torch.Tensor, left: int):
     """x fp32 [n][c][h][w] -> y bf16 [n][h][wp][c], column xx at left + xx, zero halo columns."""
     n, c, h, w = x.shape

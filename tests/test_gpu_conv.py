@@ -343,3 +343,27 @@ def test_upsampled_fprop_equals_conv_of_upsampling(n, cin, h, w, cout, k, f):
     ref = torch.relu(F.conv2d(xu, wr, padding=(k - 1) // 2) + bias.double()[None, :, None, None]).permute(0, 2, 3, 1)
     assert not torch.isnan(y).any()
     assert _rel(y, ref) < 1e-2   # merged weights are rounded to bf16 once
+
+
+@pytest.mark.parametrize("n,cin,h,w,cout,k,f", [(1, 64, 6, 8, 64, 3, 4), (2, 256, 9, 12, 256, 3, 4), (1, 128, 8, 8, 64, 3, 2),
+                                                (1, 64, 4, 6, 128, 1, 4)])
+def test_upsampled_wgrad_equals_wgrad_of_upsampling(n, cin, h, w, cout, k, f):
+    """Weight + bias gradient of a k x k conv over a nearest x f upsampling from the low-resolution
+    input (shifted block sums of dy, a 1x1 wgrad, a permuting reduce) == autograd (fp64)."""
+    from paper_1810_01993_b200 import nhwc
+    torch.manual_seed(13)
+    x = torch.randn(n, h, w, cin, device="cuda").to(torch.bfloat16)
+    dy = torch.randn(n, h * f, w * f, cout, device="cuda").to(torch.bfloat16)
+    lay = nhwc.upsampled_wgrad_layout(nhwc.View(x), cout, k)
+    parts = torch.empty(lay[0], dtype=torch.uint8, device="cuda")
+    g = torch.empty(n * h * w * k * k * cout, dtype=torch.bfloat16, device="cuda")
+    dw = torch.full((k * k * cin * cout,), float("nan"), device="cuda")
+    db = torch.full((cout,), float("nan"), device="cuda")
+    nhwc.upsampled_wgrad(nhwc.View(x), nhwc.View(dy), k, f, g, parts, lay, dw, db)
+    xu = x.double().permute(0, 3, 1, 2).repeat_interleave(f, 2).repeat_interleave(f, 3)
+    wr = torch.zeros(cout, cin, k, k, dtype=torch.float64, device="cuda", requires_grad=True)
+    br = torch.zeros(cout, dtype=torch.float64, device="cuda", requires_grad=True)
+    F.conv2d(xu, wr, br, padding=(k - 1) // 2).backward(dy.double().permute(0, 3, 1, 2))
+    ref_w = wr.grad.permute(2, 3, 1, 0).reshape(-1)   # HWIO
+    assert _rel(dw, ref_w) < 1e-2   # block sums are rounded to bf16 once
+    assert _rel(db, br.grad) < 1e-2
