@@ -737,35 +737,21 @@ extern "C" int b2dl_pack_upsampled_dgrad(const float* w_hwio, int k, int cin, in
 // row-major order, each a bf16 HWIO block [ka * kb][cin][cout] (ka = d(a,k-1) - d(a,0) + 1).
 __device__ __host__ inline int up_floordiv(int v, int f) { return v >= 0 ? v / f : -((-v + f - 1) / f); }
 
-__global__ void k_pack_upsampled_fprop(const float* __restrict__ w, __nv_bfloat16* __restrict__ out, int k, int cin,
-                                       int cout, int f) {
-  const int P = (k - 1) / 2;
-  const int kmax = up_floordiv(k - 1 + f - 1 - P, f) - up_floordiv(-P, f) + 1;
-  const long long per = static_cast<long long>(cin) * cout;
-  const long long total = static_cast<long long>(f) * f * kmax * kmax * per;
-  int S = 0;
-  for (int b = 0; b < f; ++b) S += up_floordiv(b + k - 1 - P, f) - up_floordiv(b - P, f) + 1;
+struct UpTaps {
+  uint32_t mask[256];   // per merged tap (phase blocks in order): bit ty*k+tx set if that tap is summed in
+};
+
+__global__ void k_pack_upsampled_fprop(const float* __restrict__ w, __nv_bfloat16* __restrict__ out, long long per,
+                                       int taps, int kk, const UpTaps tab) {
+  const long long total = static_cast<long long>(taps) * per;
   for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
        idx += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long e = idx % per;
-    const long long r = idx / per;
-    const int dx = static_cast<int>(r % kmax), dy = static_cast<int>((r / kmax) % kmax);
-    const int ph = static_cast<int>(r / (kmax * kmax));
-    const int a = ph / f, b = ph % f;
-    const int a0 = up_floordiv(a - P, f), ka = up_floordiv(a + k - 1 - P, f) - a0 + 1;
-    const int b0 = up_floordiv(b - P, f), kb = up_floordiv(b + k - 1 - P, f) - b0 + 1;
-    if (dy >= ka || dx >= kb) continue;
-    int rows_before = 0, cols_before = 0;
-    for (int u = 0; u < a; ++u) rows_before += up_floordiv(u + k - 1 - P, f) - up_floordiv(u - P, f) + 1;
-    for (int u = 0; u < b; ++u) cols_before += up_floordiv(u + k - 1 - P, f) - up_floordiv(u - P, f) + 1;
-    const long long block = static_cast<long long>(rows_before) * S + static_cast<long long>(ka) * cols_before;
+    const uint32_t m = tab.mask[idx / per];
     float v = 0.f;
-    for (int ty = 0; ty < k; ++ty) {
-      if (up_floordiv(a + ty - P, f) - a0 != dy) continue;
-      for (int tx = 0; tx < k; ++tx)
-        if (up_floordiv(b + tx - P, f) - b0 == dx) v += w[(ty * k + tx) * per + e];
-    }
-    out[(block + dy * kb + dx) * per + e] = __float2bfloat16_rn(v);
+    for (int t = 0; t < kk; ++t)
+      if (m >> t & 1u) v += w[t * per + e];
+    out[idx] = __float2bfloat16_rn(v);
   }
 }
 
@@ -779,11 +765,27 @@ extern "C" int b2dl_upsampled_fprop_taps(int k, int f) {
 
 extern "C" int b2dl_pack_upsampled_fprop(const float* w_hwio, int k, int cin, int cout, int f, void* out,
                                          void* stream) {
-  if (!w_hwio || !out || k < 1 || k % 2 == 0 || f < 2 || f > 8 || cin < 1 || cout < 1) return B2DL_E_VALUE;
+  if (!w_hwio || !out || k < 1 || k % 2 == 0 || k > 5 || f < 2 || f > 8 || cin < 1 || cout < 1) return B2DL_E_VALUE;
   const int P = (k - 1) / 2;
-  const int kmax = up_floordiv(k - 1 + f - 1 - P, f) - up_floordiv(-P, f) + 1;
-  k_pack_upsampled_fprop<<<grid1d(static_cast<long long>(f) * f * kmax * kmax * cin * cout), 256, 0,
-                           as_stream(stream)>>>(w_hwio, BF(out), k, cin, cout, f);
+  UpTaps tab{};
+  int T = 0;
+  for (int a = 0; a < f; ++a) {
+    const int a0 = up_floordiv(a - P, f), ka = up_floordiv(a + k - 1 - P, f) - a0 + 1;
+    for (int b = 0; b < f; ++b) {
+      const int b0 = up_floordiv(b - P, f), kb = up_floordiv(b + k - 1 - P, f) - b0 + 1;
+      for (int dy = 0; dy < ka; ++dy)
+        for (int dx = 0; dx < kb; ++dx) {
+          if (T >= 256) return B2DL_E_VALUE;
+          uint32_t m = 0;
+          for (int ty = 0; ty < k; ++ty)
+            for (int tx = 0; tx < k; ++tx)
+              if (up_floordiv(a + ty - P, f) - a0 == dy && up_floordiv(b + tx - P, f) - b0 == dx) m |= 1u << (ty * k + tx);
+          tab.mask[T++] = m;
+        }
+    }
+  }
+  const long long per = static_cast<long long>(cin) * cout;
+  k_pack_upsampled_fprop<<<grid1d(T * per), 256, 0, as_stream(stream)>>>(w_hwio, BF(out), per, T, k * k, tab);
   return check_launch();
 }
 
@@ -793,58 +795,85 @@ extern "C" int b2dl_pack_upsampled_fprop(const float* w_hwio, int k, int cin, in
 // (zero outside the image).  One thread per (pixel i, 8 channels): the (f+K-1)^2 dy pixels
 // around the block, K horizontal window sums per row, accumulated into the K*K outputs.
 // G: [n][h][w][K*K][c] bf16, so dW = x^T G is one 1x1 wgrad with K*K*c output channels.
-template <int K>
-__global__ void k_upsampled_wgrad_sums(const __nv_bfloat16* __restrict__ dy, int dys, int n, int H, int W, int c,
-                                       int f, __nv_bfloat16* __restrict__ g) {
-  constexpr int P = (K - 1) / 2;
-  const int h = H / f, w = W / f, cv = c / 8;
-  const long long total = static_cast<long long>(n) * h * w * cv;
-  for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
-       idx += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int ch = static_cast<int>(idx % cv) * 8;
-    long long r = idx / cv;
-    const int j = static_cast<int>(r % w);
-    r /= w;
-    const int i = static_cast<int>(r % h);
-    const int b = static_cast<int>(r / h);
-    float acc[K * K][8];
+// The K*K shifted F x F block sums of a (F+K-1)^2 window of bf16 channel pairs: horizontal window
+// sums per row first, then vertical sums of those (each element converted once).
+template <int K, int F>
+__device__ __forceinline__ void upw_block_sums(const uint32_t (&v)[F + K - 1][F + K - 1], float (&o)[K * K][2]) {
+  float rs[F + K - 1][K][2];
 #pragma unroll
-    for (int t = 0; t < K * K; ++t)
+  for (int rr = 0; rr < F + K - 1; ++rr) {
+    float lo[F + K - 1], hi[F + K - 1];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) acc[t][e] = 0.f;
-    // rows f*i + rr for rr in [P - (K-1), f - 1 + P]; row window of tap ty: [P - ty, P - ty + f - 1]
-    for (int rr = P - (K - 1); rr <= f - 1 + P; ++rr) {
-      const int y = f * i + rr;
-      if (y < 0 || y >= H) continue;
-      float rs[K][8];
-#pragma unroll
-      for (int tx = 0; tx < K; ++tx)
-#pragma unroll
-        for (int e = 0; e < 8; ++e) rs[tx][e] = 0.f;
-      const __nv_bfloat16* row = dy + (static_cast<long long>(b) * H + y) * W * dys + ch;
-      for (int cc = P - (K - 1); cc <= f - 1 + P; ++cc) {
-        const int x = f * j + cc;
-        if (x < 0 || x >= W) continue;
-        float v[8];
-        ldv<8>(row + static_cast<long long>(x) * dys, v);
-#pragma unroll
-        for (int tx = 0; tx < K; ++tx)
-          if (cc >= P - tx && cc <= P - tx + f - 1)
-#pragma unroll
-            for (int e = 0; e < 8; ++e) rs[tx][e] += v[e];
-      }
-#pragma unroll
-      for (int ty = 0; ty < K; ++ty)
-        if (rr >= P - ty && rr <= P - ty + f - 1)
-#pragma unroll
-          for (int tx = 0; tx < K; ++tx)
-#pragma unroll
-            for (int e = 0; e < 8; ++e) acc[ty * K + tx][e] += rs[tx][e];
+    for (int cc = 0; cc < F + K - 1; ++cc) {
+      lo[cc] = bf16_lo(v[rr][cc]);
+      hi[cc] = bf16_hi(v[rr][cc]);
     }
-    __nv_bfloat16* out = g + (((static_cast<long long>(b) * h + i) * w + j) * (K * K)) * c + ch;
 #pragma unroll
-    for (int t = 0; t < K * K; ++t) stv<8>(out + static_cast<long long>(t) * c, acc[t]);
+    for (int tx = 0; tx < K; ++tx) {
+      float a = 0.f, b = 0.f;
+#pragma unroll
+      for (int q = 0; q < F; ++q) {
+        a += lo[K - 1 - tx + q];
+        b += hi[K - 1 - tx + q];
+      }
+      rs[rr][tx][0] = a;
+      rs[rr][tx][1] = b;
+    }
   }
+#pragma unroll
+  for (int ty = 0; ty < K; ++ty)
+#pragma unroll
+    for (int tx = 0; tx < K; ++tx) {
+      float a = 0.f, b = 0.f;
+#pragma unroll
+      for (int u = 0; u < F; ++u) {
+        a += rs[K - 1 - ty + u][tx][0];
+        b += rs[K - 1 - ty + u][tx][1];
+      }
+      o[ty * K + tx][0] = a;
+      o[ty * K + tx][1] = b;
+    }
+}
+
+template <int K, int F>
+__global__ void __launch_bounds__(256) k_upsampled_wgrad_sums(const __nv_bfloat16* __restrict__ dy, int dys, int H,
+                                                              int W, int c, __nv_bfloat16* __restrict__ g) {
+  // grid (w * c/2 / 256, h, n): one thread per (low-resolution pixel, 2 channels); a warp covers 64
+  // channels of one pixel, so every dy row segment it reads is a 128-byte line.  32-bit index math
+  // and an unpredicated interior path: the kernel is otherwise instruction-bound.
+  constexpr int P = (K - 1) / 2, R = F + K - 1;
+  const int h = H / F, w = W / F, cv = c >> 1;
+  const int t = blockIdx.x * 256 + threadIdx.x;
+  if (t >= w * cv) return;
+  const int j = t / cv, ch = (t - j * cv) * 2;
+  const int i = blockIdx.y, b = blockIdx.z;
+  const int y0 = F * i - (K - 1 - P), x0 = F * j - (K - 1 - P);
+  const __nv_bfloat16* img = dy + static_cast<size_t>(b) * H * W * dys + ch;
+  uint32_t v[R][R];
+  if (y0 >= 0 && y0 + R <= H && x0 >= 0 && x0 + R <= W) {
+    const __nv_bfloat16* p0 = img + (static_cast<size_t>(y0) * W + x0) * dys;
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr)
+#pragma unroll
+      for (int cc = 0; cc < R; ++cc) v[rr][cc] = __ldg(reinterpret_cast<const uint32_t*>(p0 + (rr * W + cc) * dys));
+  } else {
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr)
+#pragma unroll
+      for (int cc = 0; cc < R; ++cc) {
+        const int y = y0 + rr, x = x0 + cc;
+        v[rr][cc] = (y >= 0 && y < H && x >= 0 && x < W)
+                        ? __ldg(reinterpret_cast<const uint32_t*>(img + (static_cast<size_t>(y) * W + x) * dys))
+                        : 0u;
+      }
+  }
+  __nv_bfloat16* out = g + ((static_cast<size_t>(b) * h + i) * w + j) * (K * K) * c + ch;
+  // tap (ty, tx) sums rows / cols [K-1-ty, K-1-ty+F) of the loaded window
+  float o[K * K][2];
+  upw_block_sums<K, F>(v, o);
+#pragma unroll
+  for (int q = 0; q < K * K; ++q)
+    *reinterpret_cast<__nv_bfloat162*>(out + q * c) = __floats2bfloat162_rn(o[q][0], o[q][1]);
 }
 
 // dW[t][ci][co] = sum_s ws[s][ci][t][co]; db[co] = sum_b bsum[b][center][co]   (fixed order)
@@ -889,21 +918,22 @@ __global__ void k_upsampled_wgrad_reduce(const float* __restrict__ ws, int wp, c
 
 extern "C" int b2dl_upsampled_wgrad_sums(b2dl_act dy, int k, int f, void* g, void* stream) {
   if (!dy.ptr || !g || f < 2 || f > 8 || dy.h % f || dy.w % f) return B2DL_E_VALUE;
-  if (dy.c % 8 || !vec_ok(dy)) return B2DL_E_ALIGN;
-  const long long total = static_cast<long long>(dy.n) * (dy.h / f) * (dy.w / f) * (dy.c / 8);
-  switch (k) {
-    case 1:
-      k_upsampled_wgrad_sums<1><<<grid1d(total), 256, 0, as_stream(stream)>>>(CBF(dy.ptr), dy.c_stride, dy.n, dy.h,
-                                                                              dy.w, dy.c, f, BF(g));
-      break;
-    case 3:
-      k_upsampled_wgrad_sums<3><<<grid1d(total), 256, 0, as_stream(stream)>>>(CBF(dy.ptr), dy.c_stride, dy.n, dy.h,
-                                                                              dy.w, dy.c, f, BF(g));
-      break;
-    default:
-      return B2DL_E_VALUE;
+  if (dy.c % 2 || dy.c_stride % 2 || reinterpret_cast<uintptr_t>(dy.ptr) & 3) return B2DL_E_ALIGN;
+  if (dy.n > 65535 || dy.h / f > 65535 || static_cast<long long>(dy.w / f) * dy.c / 2 > 0x7fffffffLL)
+    return B2DL_E_VALUE;
+  const dim3 grid(cdiv(static_cast<long long>(dy.w / f) * (dy.c / 2), 256), dy.h / f, dy.n);
+#define B2_UPW(KV, FV)                                                                                      \
+  if (k == KV && f == FV) {                                                                                \
+    k_upsampled_wgrad_sums<KV, FV><<<grid, 256, 0, as_stream(stream)>>>(CBF(dy.ptr), dy.c_stride, dy.h, dy.w, \
+                                                                       dy.c, BF(g));                        \
+    return check_launch();                                                                                 \
   }
-  return check_launch();
+  B2_UPW(3, 4)
+  B2_UPW(3, 2)
+  B2_UPW(1, 4)
+  B2_UPW(1, 2)
+#undef B2_UPW
+  return B2DL_E_VALUE;
 }
 
 extern "C" int b2dl_upsampled_wgrad_reduce(const void* partials, int w_parts, int b_parts, size_t b_offset, int cin,

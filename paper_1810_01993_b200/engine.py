@@ -492,7 +492,7 @@ class Engine:
         if not self.fp32 and os.environ.get("B2DL_UP_WGRAD", "1") != "0":
             for o in self.convs:
                 up = self.up_fprop.get(o.out)
-                if up is not None and o.k in (1, 3):
+                if up is not None and o.k in (1, 3) and up.factor in (2, 4):
                     n_, _, h_, w_ = p.shapes[up.ins[0]]
                     self.up_wgrad[o.out] = up
                     self.gsum[o.w] = torch.empty(n_ * h_ * w_ * o.k * o.k * o.cout, dtype=torch.bfloat16,
@@ -576,6 +576,15 @@ class Engine:
             self.skip_up.add(up.out)
             self.wup[o.w] = torch.zeros((o.cin, kk * kk, nhwc.cin_pad(o.cout)), dtype=torch.bfloat16,
                                         device=self.device)
+
+    def serialize(self, on: bool):
+        """Run every launch on the current stream (no wgrad || dgrad or ASPP overlap): used to time
+        each conv kernel on its own."""
+        if on and self.side is not None:
+            self._side_keep, self.side = self.side, None
+        elif not on and getattr(self, "_side_keep", None) is not None:
+            self.side, self._side_keep = self._side_keep, None
+        self._runs = None
 
     def _probe_view(self, t):
         # shape-only view for layout queries (pointer-independent)

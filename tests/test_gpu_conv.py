@@ -346,7 +346,8 @@ def test_upsampled_fprop_equals_conv_of_upsampling(n, cin, h, w, cout, k, f):
 
 
 @pytest.mark.parametrize("n,cin,h,w,cout,k,f", [(1, 64, 6, 8, 64, 3, 4), (2, 256, 9, 12, 256, 3, 4), (1, 128, 8, 8, 64, 3, 2),
-                                                (1, 64, 4, 6, 128, 1, 4)])
+                                                (1, 64, 4, 6, 128, 1, 4), (1, 64, 5, 19, 72, 3, 4),
+                                                (2, 64, 3, 40, 256, 3, 4)])
 def test_upsampled_wgrad_equals_wgrad_of_upsampling(n, cin, h, w, cout, k, f):
     """Weight + bias gradient of a k x k conv over a nearest x f upsampling from the low-resolution
     input (shifted block sums of dy, a 1x1 wgrad, a permuting reduce) == autograd (fp64)."""

@@ -4,32 +4,17 @@ import collections
 import sys
 
 sys.path.insert(0, ".")
-from tools.launch_report import load  # noqa: E402
-from paper_1810_01993_b200.engine import Plan  # noqa: E402
-from paper_1810_01993_b200.models import DeepLabConfig, build  # noqa: E402
+from tools.launch_report import conv_schedule, load  # noqa: E402
 
 
 def main(path, which=1):
     ks = load(path)
     starts = [i for i, (k, _) in enumerate(ks) if "nchw_to_nhwc" in k]
     step = ks[starts[which]:starts[which + 1] if which + 1 < len(starts) else len(ks)]
-    g, p, head, loss = build(DeepLabConfig(), 0)
-    pl = Plan(g, {k: v.shape for k, v in p.items()}, (2, 16, 1152, 768), loss, head)
-    names = [("fprop", o) for o in pl.ops if o.kind == "conv"]
-    for st in pl.backward_program:
-        o = st["op"]
-        if o.kind == "conv":
-            if not (o.k == 1 and o.cout < 8):   # head: wgrad fused into head_backward
-                names.append(("wgrad", o))
-            if st["dx"] is not None and not (o.k == 1 and o.cout < 8):
-                names.append(("dgrad", o))
+    names = conv_schedule()
     cl = [(k, t) for k, t in step if "conv_" in k and "kernel" in k]
     rows = []
-    for (kind, o), (k, t) in zip(names, cl):
-        n, _, h, w = pl.shapes[o.out]
-        P = n * h * w
-        fl = 2 * o.k * o.k * o.cin * o.cout * P
-        by = P * (o.cin + o.cout) * 2 + (P * o.cin * 2 if kind == "dgrad" else 0)
+    for (kind, o, h, fl, by), (k, t) in zip(names, cl):
         tmin = max(fl / 1.6e15, by / 6.0e12) * 1e6
         rows.append((t - tmin, t, tmin, kind, o.out, o.cin, o.cout, o.k, h, k))
     rows.sort(reverse=True)

@@ -48,6 +48,7 @@ bet = torch.zeros(256, device="cuda")
 dg = torch.empty(256, device="cuda")
 db = torch.empty(256, device="cuda")
 ws = nhwc.Workspace()
+gsum = torch.empty(N * (H // 4) * (W // 4) * 9 * 256, dtype=torch.bfloat16, device="cuda")
 E = x.numel() * 2   # bytes of one full-resolution 256-channel bf16 tensor
 ops = {
     "head_backward": (lambda: nhwc.head_backward(nhwc.View(dyb, 0, 3), wt, nhwc.View(x), nhwc.View(dx), dwp, dbp,
@@ -67,6 +68,7 @@ ops = {
     "bn_backward": (lambda: nhwc.bn_backward(nhwc.View(x), nhwc.View(g2), gam, stats, dg, db, nhwc.View(dx), ws),
                     5 * E),
     "bilinear4_fwd": (lambda: nhwc.bilinear_fwd(nhwc.View(lo), nhwc.View(dx), 4), E + E // 16),
+    "upsampled_wgrad_sums": (lambda: nhwc.upsampled_wgrad_sums(nhwc.View(x), 3, 4, gsum), E + E * 9 // 16),
     "bilinear4_bwd": (lambda: nhwc.bilinear_bwd(nhwc.View(x), nhwc.View(lo2), 4), E + E // 16),
 }
 args = [a for a in sys.argv[1:] if not a.startswith("--")]
