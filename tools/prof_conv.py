@@ -47,6 +47,8 @@ xq = torch.randn(2, 288, 192, 256, device="cuda").to(torch.bfloat16)
 yq = torch.empty_like(xq)
 wm = torch.empty(C, 36, C, dtype=torch.bfloat16, device="cuda")
 nhwc.pack_upsampled_dgrad(w, 3, C, C, 4, wm)
+wpf = torch.empty(nhwc.upsampled_fprop_taps(3, 4) * C * C, dtype=torch.bfloat16, device="cuda")
+nhwc.pack_upsampled_fprop(w, 3, C, C, 4, wpf)
 ops = {
     "q_fprop": lambda: nhwc.conv_fprop(nhwc.View(xq), None, 256, 3, 3, 1, nhwc.View(yq), bias=b, relu=True,
                                        w_master=wbf, w_mode=1),
@@ -71,6 +73,7 @@ ops = {
     "c1x1_dgrad": lambda: nhwc.conv_dgrad(nhwc.View(d8), None, 2048, 1, 1, 1, nhwc.View(y8), mask=nhwc.View(r8),
                                           residual=nhwc.View(r8), w_master=w8bf),
     "up_dgrad": lambda: nhwc.upsampled_dgrad(nhwc.View(dy), wm, C, 3, 4, nhwc.View(yq), mask=nhwc.View(xq)),
+    "up_fprop": lambda: nhwc.upsampled_fprop(nhwc.View(xq), wpf, C, C, 3, 4, nhwc.View(y), bias=b, relu=True),
     "stem_wgrad": lambda: nhwc.conv_wgrad(nhwc.View(xs), nhwc.View(ys), 7, 7, 1, dws, ws),
 }
 sel = sys.argv[1:] or list(ops)
@@ -89,6 +92,6 @@ for k in sel:
           "s2b_dgrad": 2 * 9 * 256 * 256 * 2 * 144 * 96, "stem_wgrad": 2 * 49 * 16 * 64 * N * H * W, "stem_wgrad_win": 2 * 49 * 16 * 64 * N * H * W,
           "stem_fprop_win": 2 * 49 * 16 * 64 * N * H * W, "c1x1_fprop": 2 * 512 * 2048 * 2 * 144 * 96,
                                                   "c1x1_dgrad": 2 * 512 * 2048 * 2 * 144 * 96,
-          "up_dgrad": 2 * 36 * C * C * 2 * 288 * 192}.get(
+          "up_dgrad": 2 * 36 * C * C * 2 * 288 * 192, "up_fprop": 2 * 36 * C * C * 2 * 288 * 192}.get(
         k, 2 * 9 * C * C * N * H * W)
     print(f"{k:10s} {ms:.3f} ms  {fl / ms / 1e9:.1f} TF/s", flush=True)
