@@ -227,3 +227,32 @@ def test_head_backward_vs_torch(cin, k, mask, acc, with_dx):
         assert rel(dx.double().cpu(), ref.cpu()) < 1e-2
     else:
         assert torch.equal(dx, dx0)
+
+
+def test_upsampled_conv_fusions_match_unfused(monkeypatch):
+    """full.c0 (3x3 over the x4 nearest full.up) computed from the low-resolution tensor -- phase
+    forward, strided dgrad with the upsample VJP folded in, block-sum wgrad, no upsampled tensor --
+    against the plain full-resolution path of the same engine (config-1 shapes, same seed)."""
+    from paper_1810_01993_b200.models import DeepLabConfig
+    from paper_1810_01993_b200.net import DeepLabV3Plus
+    from paper_1810_01993_b200.scenes import SceneConfig, make_scene, scene_rng
+    from paper_1810_01993_b200.loss import ClassWeights
+    f, lab = make_scene(SceneConfig(channels=16, height=288, width=192), scene_rng(0, 0, 1))
+    x, labels = f[None], lab[None]
+    cw = ClassWeights((0.982, 0.017, 0.001)).vector()
+    out = {}
+    for mode in ("fused", "plain"):
+        for k in ("B2DL_UP_FPROP", "B2DL_UP_WGRAD", "B2DL_UP_DGRAD"):
+            monkeypatch.setenv(k, "1" if mode == "fused" else "0")
+        net = DeepLabV3Plus(DeepLabConfig(), seed=0)
+        loss, logits, tape = net.forward_loss(x, labels, cw)
+        eng = tape.engine
+        assert bool(eng.dead_up) == (mode == "fused") and bool(eng.up_fprop) == (mode == "fused")
+        out[mode] = (loss, logits.cpu().numpy(), net.backward(tape))
+    lf, gf, df = out["fused"]
+    lp, gp, dp = out["plain"]
+    assert abs(lf - lp) < 1e-2 * abs(lp)
+    assert rel(gf, gp) < BF16_TOL
+    errs = {k: rel(df[k], dp[k]) for k in dp}
+    assert max(errs[k] for k in errs if k.startswith("full.c0")) < BF16_TOL, errs
+    assert np.median(list(errs.values())) < BF16_TOL / 2
