@@ -186,23 +186,30 @@ template <int G>
 __global__ void k_avgpool_bwd(const __nv_bfloat16* __restrict__ dy, int dys, __nv_bfloat16* __restrict__ dx, int dxs,
                               const __nv_bfloat16* __restrict__ mask, int ms, int n, int h, int w, int c, int k,
                               int acc) {
+  // one thread per (pooled pixel, channel group): dy read once, the k x k outputs written from it;
+  // 32-bit index math (the launcher checks the pooled element count fits)
   const int cg = c / G;
-  const long long total = static_cast<long long>(n) * h * w * cg;
   const int wo = w / k, ho = h / k;
+  const int total = n * ho * wo * cg;
   const float inv = 1.f / (k * k);
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int ch = static_cast<int>(i % cg) * G;
-    const long long p = i / cg;
-    const int xx = static_cast<int>(p % w);
-    const long long r = p / w;
-    const int yy = static_cast<int>(r % h);
-    const long long img = r / h;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int ch = (i % cg) * G;
+    const int q = i / cg;  // (img * ho + yo) * wo + xo
+    const int xo = q % wo, r = q / wo;
+    const int yo = r % ho, img = r / ho;
     float v[G];
-    ldv<G>(dy + ((img * ho + yy / k) * wo + xx / k) * dys + ch, v);
+    ldv<G>(dy + static_cast<long long>(q) * dys + ch, v);
 #pragma unroll
     for (int e = 0; e < G; ++e) v[e] *= inv;
-    finish<G>(v, mask ? mask + p * ms + ch : nullptr, dx + p * dxs + ch, acc);
+    const long long p0 = (static_cast<long long>(img) * h + yo * k) * w + xo * k;
+    for (int a = 0; a < k; ++a)
+      for (int b = 0; b < k; ++b) {
+        const long long p = p0 + static_cast<long long>(a) * w + b;
+        float o[G];
+#pragma unroll
+        for (int e = 0; e < G; ++e) o[e] = v[e];
+        finish<G>(o, mask ? mask + p * ms + ch : nullptr, dx + p * dxs + ch, acc);
+      }
   }
 }
 template <int G>
@@ -605,6 +612,8 @@ extern "C" int b2dl_avgpool_fwd(b2dl_act x, b2dl_act y, int k, void* stream) {
 extern "C" int b2dl_avgpool_bwd(b2dl_act dy, b2dl_act dx, int k, int accumulate, b2dl_act mask, void* stream) {
   if (k < 1 || dx.h != dy.h * k || dx.w != dy.w * k || dx.c != dy.c) return B2DL_E_VALUE;
   long long total = static_cast<long long>(dx.n) * dx.h * dx.w * dx.c;
+  if (static_cast<long long>(dy.n) * dy.h * dy.w * dy.c > 0x7fffffffLL) return B2DL_E_VALUE;
+  total /= static_cast<long long>(k) * k;   // threads walk pooled pixels
   B2_LAUNCH_G(k_avgpool_bwd, vec_ok(dy, dx, mask), total, CBF(dy.ptr), dy.c_stride, BF(dx.ptr), dx.c_stride,
               CBF(mask.ptr), mask.c_stride, dx.n, dx.h, dx.w, dx.c, k, accumulate);
   return check_launch();

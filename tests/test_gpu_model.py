@@ -195,6 +195,27 @@ def test_memory_bound_kernels_vs_torch():
     del g
 
 
+@pytest.mark.parametrize("c,k,mask,acc", [(64, 4, True, False), (64, 2, False, True), (12, 4, True, True),
+                                          (256, 4, False, False)])
+def test_avgpool_bwd_vs_torch(c, k, mask, acc):
+    """avgpool VJP (ops.py:186-189): dx (+)= mask * repeat(dy) / k^2 on 8-channel vectors and the
+    scalar path (c % 8 != 0)."""
+    from paper_1810_01993_b200 import nhwc
+    torch.manual_seed(3)
+    n, ho, wo = 2, 7, 5
+    dy = torch.randn(n, ho, wo, c, device="cuda").to(torch.bfloat16)
+    m = torch.randn(n, ho * k, wo * k, c, device="cuda").to(torch.bfloat16)
+    dx0 = torch.randn(n, ho * k, wo * k, c, device="cuda").to(torch.bfloat16)
+    dx = dx0.clone()
+    nhwc.avgpool_bwd(nhwc.View(dy), nhwc.View(dx), k, accumulate=acc, mask=nhwc.View(m) if mask else None)
+    ref = dy.float().repeat_interleave(k, 1).repeat_interleave(k, 2) / (k * k)
+    if mask:
+        ref = torch.where(m.float() > 0, ref, torch.zeros_like(ref))
+    if acc:
+        ref = ref + dx0.float()
+    assert rel(dx.float().cpu(), ref.cpu()) < 1e-2
+
+
 @pytest.mark.parametrize("cin,k,mask,acc,with_dx", [(256, 3, True, False, True), (64, 5, False, True, True),
                                                      (128, 3, True, False, False)])
 def test_head_backward_vs_torch(cin, k, mask, acc, with_dx):
