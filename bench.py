@@ -8,7 +8,8 @@ A step is one full training step (forward, fused weighted CE, backward, bucketed
 all-reduce, LARC + momentum update, weight repack) over the rank's batch of 2 tiles.
 `value` is device-timed with CUDA events, inputs resident in HBM, max over ranks;
 `e2e` is the same step through the public trainer API with the batch copied from
-pinned host memory and the loss read back every step.  The working set (~11 GB of
+pinned host memory and every step's loss read back to the host (one step behind, so the
+next step is already queued while the host waits).  The working set (~11 GB of
 activations and gradients per GPU) is far larger than L2, so no L2 flush is needed.
 
 --impl reference times the reference's CPU step (the oracle/ NumPy restatement of
@@ -295,14 +296,23 @@ def run_ours(args):
     e_steps = max(2, args.steps // 2)
     e0.record()
     if graphed:
-        # the next step's host->device copy runs on a copy stream under the current step;
-        # every step's loss is read back to the host before the next step is launched
+        # the next step's host->device copy runs on a copy stream under the current step; every
+        # step's loss is copied to pinned host memory behind it and read by the host one step
+        # later (while the next step is already queued), so the GPU never idles on the host
+        lh = [torch.empty(1, dtype=torch.float32, pin_memory=True) for _ in range(2)]
+        lev = [torch.cuda.Event() for _ in range(2)]
         tr.stage(*host[0])
         for i in range(e_steps):
             loss = tr.step_staged()
+            lh[i % 2].copy_(loss, non_blocking=True)
+            lev[i % 2].record()
             if i + 1 < e_steps:
                 tr.stage(*host[(i + 1) % pool])
-            lv = float(loss.item())
+            if i > 0:
+                lev[(i - 1) % 2].synchronize()
+                lv = float(lh[(i - 1) % 2][0])
+        lev[(e_steps - 1) % 2].synchronize()
+        lv = float(lh[(e_steps - 1) % 2][0])
     else:
         for i in range(e_steps):
             hx, hl = host[i % pool]
