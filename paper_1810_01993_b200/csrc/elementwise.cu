@@ -804,85 +804,106 @@ extern "C" int b2dl_pack_upsampled_fprop(const float* w_hwio, int k, int cin, in
 // (zero outside the image).  One thread per (pixel i, 8 channels): the (f+K-1)^2 dy pixels
 // around the block, K horizontal window sums per row, accumulated into the K*K outputs.
 // G: [n][h][w][K*K][c] bf16, so dW = x^T G is one 1x1 wgrad with K*K*c output channels.
-// The K*K shifted F x F block sums of a (F+K-1)^2 window of bf16 channel pairs: horizontal window
-// sums per row first, then vertical sums of those (each element converted once).
-template <int K, int F>
-__device__ __forceinline__ void upw_block_sums(const uint32_t (&v)[F + K - 1][F + K - 1], float (&o)[K * K][2]) {
-  float rs[F + K - 1][K][2];
+// The K*K shifted F x F block sums of a (F+K-1)^2 window of W words (2 bf16 channels each):
+// horizontal window sums per row first, then vertical sums of those (each element converted once).
+template <int K, int F, int W>
+__device__ __forceinline__ void upw_block_sums(const uint32_t (&v)[F + K - 1][F + K - 1][W], float (&o)[K * K][2 * W]) {
+  float rs[F + K - 1][K][2 * W];
 #pragma unroll
   for (int rr = 0; rr < F + K - 1; ++rr) {
-    float lo[F + K - 1], hi[F + K - 1];
+    float e[F + K - 1][2 * W];
 #pragma unroll
-    for (int cc = 0; cc < F + K - 1; ++cc) {
-      lo[cc] = bf16_lo(v[rr][cc]);
-      hi[cc] = bf16_hi(v[rr][cc]);
-    }
+    for (int cc = 0; cc < F + K - 1; ++cc)
 #pragma unroll
-    for (int tx = 0; tx < K; ++tx) {
-      float a = 0.f, b = 0.f;
-#pragma unroll
-      for (int q = 0; q < F; ++q) {
-        a += lo[K - 1 - tx + q];
-        b += hi[K - 1 - tx + q];
+      for (int u = 0; u < W; ++u) {
+        e[cc][2 * u] = bf16_lo(v[rr][cc][u]);
+        e[cc][2 * u + 1] = bf16_hi(v[rr][cc][u]);
       }
-      rs[rr][tx][0] = a;
-      rs[rr][tx][1] = b;
-    }
+#pragma unroll
+    for (int tx = 0; tx < K; ++tx)
+#pragma unroll
+      for (int ch = 0; ch < 2 * W; ++ch) {
+        float a = 0.f;
+#pragma unroll
+        for (int q = 0; q < F; ++q) a += e[K - 1 - tx + q][ch];
+        rs[rr][tx][ch] = a;
+      }
   }
 #pragma unroll
   for (int ty = 0; ty < K; ++ty)
 #pragma unroll
-    for (int tx = 0; tx < K; ++tx) {
-      float a = 0.f, b = 0.f;
+    for (int tx = 0; tx < K; ++tx)
 #pragma unroll
-      for (int u = 0; u < F; ++u) {
-        a += rs[K - 1 - ty + u][tx][0];
-        b += rs[K - 1 - ty + u][tx][1];
+      for (int ch = 0; ch < 2 * W; ++ch) {
+        float a = 0.f;
+#pragma unroll
+        for (int u = 0; u < F; ++u) a += rs[K - 1 - ty + u][tx][ch];
+        o[ty * K + tx][ch] = a;
       }
-      o[ty * K + tx][0] = a;
-      o[ty * K + tx][1] = b;
-    }
 }
 
-template <int K, int F>
+// W words (2W channels) per thread: grid (w * c/(2W) / 256, h, n), one thread per (low-resolution
+// pixel, 2W channels); a warp covers 64W channels of one pixel (128-byte lines per dy row segment
+// for W = 1, 256 for W = 2).  32-bit index math and an unpredicated interior path: the kernel is
+// instruction-bound, so wider words amortise the address arithmetic over more channels.
+template <int K, int F, int W>
 __global__ void __launch_bounds__(256) k_upsampled_wgrad_sums(const __nv_bfloat16* __restrict__ dy, int dys, int H,
-                                                              int W, int c, __nv_bfloat16* __restrict__ g) {
-  // grid (w * c/2 / 256, h, n): one thread per (low-resolution pixel, 2 channels); a warp covers 64
-  // channels of one pixel, so every dy row segment it reads is a 128-byte line.  32-bit index math
-  // and an unpredicated interior path: the kernel is otherwise instruction-bound.
-  constexpr int P = (K - 1) / 2, R = F + K - 1;
-  const int h = H / F, w = W / F, cv = c >> 1;
+                                                              int Wd, int c, __nv_bfloat16* __restrict__ g) {
+  constexpr int P = (K - 1) / 2, R = F + K - 1, CPT = 2 * W;
+  const int h = H / F, w = Wd / F, cv = c / CPT;
   const int t = blockIdx.x * 256 + threadIdx.x;
   if (t >= w * cv) return;
-  const int j = t / cv, ch = (t - j * cv) * 2;
+  const int j = t / cv, ch = (t - j * cv) * CPT;
   const int i = blockIdx.y, b = blockIdx.z;
   const int y0 = F * i - (K - 1 - P), x0 = F * j - (K - 1 - P);
-  const __nv_bfloat16* img = dy + static_cast<size_t>(b) * H * W * dys + ch;
-  uint32_t v[R][R];
-  if (y0 >= 0 && y0 + R <= H && x0 >= 0 && x0 + R <= W) {
-    const __nv_bfloat16* p0 = img + (static_cast<size_t>(y0) * W + x0) * dys;
+  const __nv_bfloat16* img = dy + static_cast<size_t>(b) * H * Wd * dys + ch;
+  uint32_t v[R][R][W];
+  auto ld = [&](const __nv_bfloat16* ptr, uint32_t (&dst)[W]) {
+    if constexpr (W == 2) {
+      const uint2 u = __ldg(reinterpret_cast<const uint2*>(ptr));
+      dst[0] = u.x;
+      dst[1] = u.y;
+    } else {
+      dst[0] = __ldg(reinterpret_cast<const uint32_t*>(ptr));
+    }
+  };
+  if (y0 >= 0 && y0 + R <= H && x0 >= 0 && x0 + R <= Wd) {
+    const __nv_bfloat16* p0 = img + (static_cast<size_t>(y0) * Wd + x0) * dys;
 #pragma unroll
     for (int rr = 0; rr < R; ++rr)
 #pragma unroll
-      for (int cc = 0; cc < R; ++cc) v[rr][cc] = __ldg(reinterpret_cast<const uint32_t*>(p0 + (rr * W + cc) * dys));
+      for (int cc = 0; cc < R; ++cc) ld(p0 + (rr * Wd + cc) * dys, v[rr][cc]);
   } else {
 #pragma unroll
     for (int rr = 0; rr < R; ++rr)
 #pragma unroll
       for (int cc = 0; cc < R; ++cc) {
         const int y = y0 + rr, x = x0 + cc;
-        v[rr][cc] = (y >= 0 && y < H && x >= 0 && x < W)
-                        ? __ldg(reinterpret_cast<const uint32_t*>(img + (static_cast<size_t>(y) * W + x) * dys))
-                        : 0u;
+        if (y >= 0 && y < H && x >= 0 && x < Wd) {
+          ld(img + (static_cast<size_t>(y) * Wd + x) * dys, v[rr][cc]);
+        } else {
+#pragma unroll
+          for (int u = 0; u < W; ++u) v[rr][cc][u] = 0u;
+        }
       }
   }
   __nv_bfloat16* out = g + ((static_cast<size_t>(b) * h + i) * w + j) * (K * K) * c + ch;
   // tap (ty, tx) sums rows / cols [K-1-ty, K-1-ty+F) of the loaded window
-  float o[K * K][2];
-  upw_block_sums<K, F>(v, o);
+  float o[K * K][CPT];
+  upw_block_sums<K, F, W>(v, o);
 #pragma unroll
-  for (int q = 0; q < K * K; ++q)
-    *reinterpret_cast<__nv_bfloat162*>(out + q * c) = __floats2bfloat162_rn(o[q][0], o[q][1]);
+  for (int q = 0; q < K * K; ++q) {
+    uint32_t wd[W];
+#pragma unroll
+    for (int u = 0; u < W; ++u) {
+      const __nv_bfloat162 hv = __floats2bfloat162_rn(o[q][2 * u], o[q][2 * u + 1]);
+      wd[u] = *reinterpret_cast<const uint32_t*>(&hv);
+    }
+    if constexpr (W == 2)
+      *reinterpret_cast<uint2*>(out + q * c) = make_uint2(wd[0], wd[1]);
+    else
+      *reinterpret_cast<uint32_t*>(out + q * c) = wd[0];
+  }
 }
 
 // dW[t][ci][co] = sum_s ws[s][ci][t][co]; db[co] = sum_b bsum[b][center][co]   (fixed order)
@@ -930,12 +951,19 @@ extern "C" int b2dl_upsampled_wgrad_sums(b2dl_act dy, int k, int f, void* g, voi
   if (dy.c % 2 || dy.c_stride % 2 || reinterpret_cast<uintptr_t>(dy.ptr) & 3) return B2DL_E_ALIGN;
   if (dy.n > 65535 || dy.h / f > 65535 || static_cast<long long>(dy.w / f) * dy.c / 2 > 0x7fffffffLL)
     return B2DL_E_VALUE;
-  const dim3 grid(cdiv(static_cast<long long>(dy.w / f) * (dy.c / 2), 256), dy.h / f, dy.n);
-#define B2_UPW(KV, FV)                                                                                      \
-  if (k == KV && f == FV) {                                                                                \
-    k_upsampled_wgrad_sums<KV, FV><<<grid, 256, 0, as_stream(stream)>>>(CBF(dy.ptr), dy.c_stride, dy.h, dy.w, \
-                                                                       dy.c, BF(g));                        \
-    return check_launch();                                                                                 \
+  // 4 channels per thread where 8-byte loads are aligned
+  const bool w2 = dy.c % 4 == 0 && dy.c_stride % 4 == 0 && (reinterpret_cast<uintptr_t>(dy.ptr) & 7) == 0;
+  const int cpt = w2 ? 4 : 2;
+  const dim3 grid(cdiv(static_cast<long long>(dy.w / f) * (dy.c / cpt), 256), dy.h / f, dy.n);
+#define B2_UPW(KV, FV)                                                                                     \
+  if (k == KV && f == FV) {                                                                               \
+    if (w2)                                                                                               \
+      k_upsampled_wgrad_sums<KV, FV, 2><<<grid, 256, 0, as_stream(stream)>>>(CBF(dy.ptr), dy.c_stride, dy.h,  \
+                                                                            dy.w, dy.c, BF(g));           \
+    else                                                                                                  \
+      k_upsampled_wgrad_sums<KV, FV, 1><<<grid, 256, 0, as_stream(stream)>>>(CBF(dy.ptr), dy.c_stride, dy.h,  \
+                                                                            dy.w, dy.c, BF(g));           \
+    return check_launch();                                                                                \
   }
   B2_UPW(3, 4)
   B2_UPW(3, 2)

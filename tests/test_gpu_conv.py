@@ -368,3 +368,20 @@ def test_upsampled_wgrad_equals_wgrad_of_upsampling(n, cin, h, w, cout, k, f):
     ref_w = wr.grad.permute(2, 3, 1, 0).reshape(-1)   # HWIO
     assert _rel(dw, ref_w) < 1e-2   # block sums are rounded to bf16 once
     assert _rel(db, br.grad) < 1e-2
+
+
+@pytest.mark.parametrize("c", [6, 64])
+def test_upsampled_wgrad_sums_vs_torch(c):
+    """Shifted 4 x 4 block sums of dy (2- and 4-channel thread paths): G_t[i] = sum of the padded dy
+    over rows / cols [4i + 2 - t, 4i + 6 - t)."""
+    from paper_1810_01993_b200 import nhwc
+    torch.manual_seed(14)
+    n, H, W, f, k = 2, 16, 20, 4, 3
+    dy = torch.randn(n, H, W, c, device="cuda").to(torch.bfloat16)
+    g = torch.empty(n * (H // f) * (W // f) * k * k * c, dtype=torch.bfloat16, device="cuda")
+    nhwc.upsampled_wgrad_sums(nhwc.View(dy), k, f, g)
+    dyp = F.pad(dy.double().permute(0, 3, 1, 2), (1, 1, 1, 1))
+    ref = torch.stack([F.avg_pool2d(dyp[:, :, 2 - ty:2 - ty + H, 2 - tx:2 - tx + W], f) * f * f
+                       for ty in range(k) for tx in range(k)], 1)      # [n, taps, c, h, w]
+    ref = ref.permute(0, 3, 4, 1, 2)                                   # [n, h, w, taps, c]
+    assert _rel(g.view(ref.shape), ref) < 1e-2
