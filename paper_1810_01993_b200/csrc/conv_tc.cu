@@ -1477,6 +1477,27 @@ struct FpropMaps {
   CUtensorMap a, b, y, r, m;
 };
 
+// Development knobs (defaults are the measured choice): B2DL_EW16_NOPS = most epilogue operands
+// for which 16 epilogue warps are used; B2DL_EPI_SLOTS_<EW>_<nops> = operand slots.
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e && e[0] ? atoi(e) : dflt;
+}
+static int ew16_max_nops() {
+  static const int v = env_int("B2DL_EW16_NOPS", 1);
+  return v;
+}
+static int epi_slots_for(int ew, int nops) {
+  static int cache[2][4] = {{-1, -1, -1, -1}, {-1, -1, -1, -1}};
+  int& c = cache[ew == 16][nops & 3];
+  if (c < 0) {
+    char name[40];
+    snprintf(name, sizeof(name), "B2DL_EPI_SLOTS_%d_%d", ew, nops);
+    c = std::max(1, std::min(EPI_MAX_SLOTS, env_int(name, 2)));
+  }
+  return c;
+}
+
 template <int BN, int KBLK, bool BMN, int CG, int EW = 8>
 static int launch_fprop(const FpropMaps& t, FpropParams p, cudaStream_t st) {
   using C = FpropCfg<BN, KBLK, BMN, CG>;
@@ -1493,7 +1514,7 @@ static int launch_fprop(const FpropMaps& t, FpropParams p, cudaStream_t st) {
   // operand prefetch depth (slots - 1 chunks ahead).  Measured: a third slot does not speed up
   // the epilogue-bound 1x1 layers (their chunks wait on instruction latency, not on the loads)
   // and costs operand stages, so two it is.
-  p.epi_slots = 2;
+  p.epi_slots = epi_slots_for(EW, p.epi_nops);
   p.epi_bytes = p.tma_epi ? (EW / 4) * epi_sub_bytes(p.epi_nops, p.epi_slots) : EPI_LEGACY_BYTES;
   // deepest operand pipeline that fits beside the epilogue buffers
   p.stages = 1;
@@ -1834,7 +1855,7 @@ extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
   const int nops = (p.res != nullptr) + (p.mask != nullptr) + (p.accumulate != 0);
   // 16 epilogue warps where the epilogue dominates (short K); long-K launches keep the deeper
   // operand ring that 8 warps' smaller buffers leave room for
-  if (p.tma_epi && nops <= 1 && kblk == 64 && p.num_kb <= 16 && ew16_enabled()) {
+  if (p.tma_epi && nops <= ew16_max_nops() && kblk == 64 && p.num_kb <= 16 && ew16_enabled()) {
     if (cg == 2 && bn == 256)
       return mode == 1 ? launch_fprop<256, 64, true, 2, 16>(t, p, st) : launch_fprop<256, 64, false, 2, 16>(t, p, st);
     if (cg == 1 && bn == 256)
