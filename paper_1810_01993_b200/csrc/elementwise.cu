@@ -43,32 +43,42 @@ __global__ void k_nchw_to_nhwc(const float* __restrict__ x, void* __restrict__ y
 }
 // NCHW fp32 -> haloed NHWC bf16 rows: a block moves 64 columns x c channels of one image row
 // through shared memory, so both the strided planes and the pixel-major output are coalesced.
-constexpr int HALO_COLS = 64;
-__global__ void __launch_bounds__(256) k_nchw_to_nhwc_halo(const float* __restrict__ x, __nv_bfloat16* __restrict__ y,
-                                                           int c, int h, int w, int wp, int left) {
-  extern __shared__ __nv_bfloat16 tile[];  // [HALO_COLS][c + 8]
-  const int cp = c + 8;
-  const int x0 = blockIdx.x * HALO_COLS, row = blockIdx.y, img = blockIdx.z;
-  const int t = threadIdx.x & 63;
+constexpr int HALO_COLS = 256;  // one thread per pixel column of a row
+__device__ __forceinline__ uint32_t halo_pack2(float a, float b) {  // a -> low half
+  const __nv_bfloat162 t = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&t);
+}
+// NCHW fp32 -> NHWC bf16 with zeroed halo columns.  One thread per pixel: each of its c channel
+// loads is a coalesced 128-byte warp access of one plane row, and its 2c output bytes are
+// written as 16-byte pieces adjacent to the neighbouring threads' (no shared-memory transpose).
+__global__ void __launch_bounds__(HALO_COLS) k_nchw_to_nhwc_halo(const float* __restrict__ x,
+                                                                 __nv_bfloat16* __restrict__ y, int c, int h, int w,
+                                                                 int wp, int left) {
+  const int col = blockIdx.x * HALO_COLS + threadIdx.x, row = blockIdx.y, img = blockIdx.z;
   const long long plane = static_cast<long long>(h) * w;
-  const float* src = x + static_cast<long long>(img) * c * plane + static_cast<long long>(row) * w + x0 + t;
-  for (int ch = threadIdx.x >> 6; ch < c; ch += 4)
-    tile[t * cp + ch] = __float2bfloat16_rn(x0 + t < w ? __ldg(src + ch * plane) : 0.f);
-  __syncthreads();
-  const int vec = c / 8;  // 16-byte pieces per pixel
   __nv_bfloat16* dst_row = y + (static_cast<long long>(img) * h + row) * wp * c;
-  for (int i = threadIdx.x; i < HALO_COLS * vec; i += 256) {
-    const int px = i / vec, pc = i - px * vec;
-    if (x0 + px >= w) break;
-    *reinterpret_cast<uint4*>(dst_row + static_cast<long long>(left + x0 + px) * c + pc * 8) =
-        *reinterpret_cast<const uint4*>(tile + px * cp + pc * 8);
+  const int vec = c / 8;  // 16-byte pieces per pixel
+  if (col < w) {
+    const float* src = x + static_cast<long long>(img) * c * plane + static_cast<long long>(row) * w + col;
+    uint4* dst = reinterpret_cast<uint4*>(dst_row + static_cast<long long>(left + col) * c);
+    for (int pc = 0; pc < vec; ++pc) {
+      float v[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[e] = __ldg(src + (pc * 8 + e) * plane);
+      uint4 o;
+      o.x = halo_pack2(v[0], v[1]);
+      o.y = halo_pack2(v[2], v[3]);
+      o.z = halo_pack2(v[4], v[5]);
+      o.w = halo_pack2(v[6], v[7]);
+      dst[pc] = o;
+    }
   }
   if (blockIdx.x == 0) {  // zero halo columns of this row
     const int nh = wp - w;
-    for (int i = threadIdx.x; i < nh * vec; i += 256) {
+    for (int i = threadIdx.x; i < nh * vec; i += HALO_COLS) {
       const int k = i / vec, pc = i - k * vec;
-      const int col = k < left ? k : w + k;
-      *reinterpret_cast<uint4*>(dst_row + static_cast<long long>(col) * c + pc * 8) = make_uint4(0, 0, 0, 0);
+      const int hc = k < left ? k : w + k;
+      *reinterpret_cast<uint4*>(dst_row + static_cast<long long>(hc) * c + pc * 8) = make_uint4(0, 0, 0, 0);
     }
   }
 }
@@ -202,6 +212,30 @@ __global__ void k_avgpool_bwd(const __nv_bfloat16* __restrict__ dy, int dys, __n
 #pragma unroll
     for (int e = 0; e < G; ++e) v[e] *= inv;
     const long long p0 = (static_cast<long long>(img) * h + yo * k) * w + xo * k;
+    if constexpr (G == 8) {
+      if (k == 4 && mask && !acc) {  // the stem pool: all 16 mask loads in flight before any store
+        uint4 mr[16];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+            mr[4 * a + b] = __ldg(reinterpret_cast<const uint4*>(mask + (p0 + a * w + b) * ms + ch));
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const uint32_t mw[4] = {mr[4 * a + b].x, mr[4 * a + b].y, mr[4 * a + b].z, mr[4 * a + b].w};
+            float o[8];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              o[2 * e] = __uint_as_float(mw[e] << 16) > 0.f ? v[2 * e] : 0.f;
+              o[2 * e + 1] = __uint_as_float(mw[e] & 0xFFFF0000u) > 0.f ? v[2 * e + 1] : 0.f;
+            }
+            stv<8>(dx + (p0 + a * w + b) * dxs + ch, o);
+          }
+        continue;
+      }
+    }
     for (int a = 0; a < k; ++a)
       for (int b = 0; b < k; ++b) {
         const long long p = p0 + static_cast<long long>(a) * w + b;
@@ -582,8 +616,7 @@ extern "C" int b2dl_nchw_to_nhwc_halo(const float* x, int n, int c, int h, int w
   if (!x || !y || n < 1 || h < 1 || w < 1 || left < 0 || wp < w + left) return B2DL_E_VALUE;
   if (c < 8 || c > 64 || c % 8 || (reinterpret_cast<uintptr_t>(y) & 15)) return B2DL_E_ALIGN;
   dim3 grid(cdiv(w, HALO_COLS), h, n);
-  const size_t smem = static_cast<size_t>(HALO_COLS) * (c + 8) * sizeof(__nv_bfloat16);
-  k_nchw_to_nhwc_halo<<<grid, 256, smem, as_stream(stream)>>>(x, BF(y), c, h, w, wp, left);
+  k_nchw_to_nhwc_halo<<<grid, HALO_COLS, 0, as_stream(stream)>>>(x, BF(y), c, h, w, wp, left);
   return check_launch();
 }
 
