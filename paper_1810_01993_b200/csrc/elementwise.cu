@@ -41,8 +41,6 @@ __global__ void k_nchw_to_nhwc(const float* __restrict__ x, void* __restrict__ y
       reinterpret_cast<__nv_bfloat16*>(y)[d] = __float2bfloat16_rn(x[i]);
   }
 }
-// NCHW fp32 -> haloed NHWC bf16 rows: a block moves 64 columns x c channels of one image row
-// through shared memory, so both the strided planes and the pixel-major output are coalesced.
 constexpr int HALO_COLS = 256;  // one thread per pixel column of a row
 __device__ __forceinline__ uint32_t halo_pack2(float a, float b) {  // a -> low half
   const __nv_bfloat162 t = __floats2bfloat162_rn(a, b);
