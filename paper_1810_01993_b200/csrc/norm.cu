@@ -275,7 +275,8 @@ __global__ void __launch_bounds__(BN_THREADS) k_bn_bwd_apply(const T* __restrict
 
 // ---- bilinear (half-pixel centres, clamp at 0), integer factor f
 __device__ __forceinline__ void bl_tap(int o, int n_in, int f, int& i0, int& i1, float& w0, float& w1) {
-  float src = (o + 0.5f) / f - 0.5f;
+  // power-of-two factors: multiplying by 1/f is exact, i.e. bit-identical to the division
+  float src = ((f & (f - 1)) == 0 ? (o + 0.5f) * __frcp_rn(static_cast<float>(f)) : (o + 0.5f) / f) - 0.5f;
   src = src < 0.f ? 0.f : src;
   i0 = static_cast<int>(src);  // floor (src >= 0)
   i1 = i0 + 1 < n_in ? i0 + 1 : n_in - 1;
@@ -295,8 +296,12 @@ __global__ void k_bilinear_fwd(const T* __restrict__ x, int xs, T* __restrict__ 
   const T* r0 = x + (static_cast<long long>(img) * h + y0) * w * static_cast<long long>(xs);
   const T* r1 = x + (static_cast<long long>(img) * h + y1) * w * static_cast<long long>(xs);
   T* out = y + (static_cast<long long>(img) * H + Y) * W * static_cast<long long>(ys);
-  for (int i = threadIdx.x; i < W * groups; i += blockDim.x) {
-    const int X = i / groups, g = i - X * groups;
+  // when the channel groups divide the block, a thread's group is fixed and its column steps by
+  // blockDim / groups (no per-element integer division)
+  const bool fixed_g = (blockDim.x % groups) == 0;
+  const int g_fixed = threadIdx.x % groups, x_step = blockDim.x / groups;
+  for (int i = threadIdx.x, Xs = threadIdx.x / groups; i < W * groups; i += blockDim.x, Xs += x_step) {
+    const int X = fixed_g ? Xs : i / groups, g = fixed_g ? g_fixed : i - X * groups;
     bl_tap(X, w, f, x0, x1, wx0, wx1);
     float a[V], b[V], cc[V], d[V], o[V];
     Vec<T, V>::load(r0 + static_cast<long long>(x0) * xs + g * V, a);
