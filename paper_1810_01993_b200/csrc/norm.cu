@@ -337,8 +337,10 @@ __global__ void k_bilinear_bwd_rows(const T* __restrict__ dy, int dys, float* __
   const int Y = blockIdx.x, img = blockIdx.y;
   const T* row = dy + (static_cast<long long>(img) * H + Y) * W * static_cast<long long>(dys);
   float* out = R + (static_cast<long long>(img) * H + Y) * w * static_cast<long long>(c);
-  for (int i = threadIdx.x; i < w * groups; i += blockDim.x) {
-    const int xx = i / groups, g = i - xx * groups;
+  const bool fixed_g = (blockDim.x % groups) == 0;
+  const int g_fixed = threadIdx.x % groups, x_step = blockDim.x / groups;
+  for (int i = threadIdx.x, xs = threadIdx.x / groups; i < w * groups; i += blockDim.x, xs += x_step) {
+    const int xx = fixed_g ? xs : i / groups, g = fixed_g ? g_fixed : i - xx * groups;
     int X0, X1;
     bl_range(xx, w, f, W, X0, X1);
     float s[V];
@@ -352,8 +354,14 @@ __global__ void k_bilinear_bwd_rows(const T* __restrict__ dy, int dys, float* __
 #pragma unroll
       for (int e = 0; e < V; ++e) s[e] += wx * v[e];
     }
+    float* o = out + static_cast<long long>(xx) * c + g * V;
+    if constexpr (V % 4 == 0) {  // 16-byte stores (c % V == 0 and a 256-byte aligned workspace)
 #pragma unroll
-    for (int e = 0; e < V; ++e) out[static_cast<long long>(xx) * c + g * V + e] = s[e];
+      for (int e = 0; e < V; e += 4) *reinterpret_cast<float4*>(o + e) = make_float4(s[e], s[e + 1], s[e + 2], s[e + 3]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < V; ++e) o[e] = s[e];
+    }
   }
 }
 
@@ -365,17 +373,37 @@ __global__ void k_bilinear_bwd_cols(const float* __restrict__ R, T* __restrict__
   int Y0, Y1;
   bl_range(yy, h, f, H, Y0, Y1);
   const long long q0 = (static_cast<long long>(img) * h + yy) * w;
-  for (int i = threadIdx.x; i < w * groups; i += blockDim.x) {
-    const int xx = i / groups, g = i - xx * groups;
+  // the block's row weights, computed once (same values and order as per element)
+  constexpr int BL_MAXY = 64;
+  __shared__ float swy[BL_MAXY];
+  const bool wy_cached = Y1 - Y0 + 1 <= BL_MAXY;
+  if (wy_cached)
+    for (int t = threadIdx.x; t <= Y1 - Y0; t += blockDim.x) swy[t] = bl_weight(Y0 + t, yy, h, f);
+  __syncthreads();
+  const bool fixed_g = (blockDim.x % groups) == 0;
+  const int g_fixed = threadIdx.x % groups, x_step = blockDim.x / groups;
+  for (int i = threadIdx.x, xs = threadIdx.x / groups; i < w * groups; i += blockDim.x, xs += x_step) {
+    const int xx = fixed_g ? xs : i / groups, g = fixed_g ? g_fixed : i - xx * groups;
     float s[V];
 #pragma unroll
     for (int e = 0; e < V; ++e) s[e] = 0.f;
     for (int Y = Y0; Y <= Y1; ++Y) {
-      const float wy = bl_weight(Y, yy, h, f);
+      const float wy = wy_cached ? swy[Y - Y0] : bl_weight(Y, yy, h, f);
       if (wy == 0.f) continue;
       const float* r = R + ((static_cast<long long>(img) * H + Y) * w + xx) * c + g * V;
+      if constexpr (V % 4 == 0) {
 #pragma unroll
-      for (int e = 0; e < V; ++e) s[e] += wy * r[e];
+        for (int e = 0; e < V; e += 4) {
+          const float4 r4 = *reinterpret_cast<const float4*>(r + e);
+          s[e] += wy * r4.x;
+          s[e + 1] += wy * r4.y;
+          s[e + 2] += wy * r4.z;
+          s[e + 3] += wy * r4.w;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < V; ++e) s[e] += wy * r[e];
+      }
     }
     const long long q = q0 + xx;
     if (mask) {
