@@ -175,6 +175,30 @@ __global__ void k_avgpool_fwd(const __nv_bfloat16* __restrict__ x, int xs, __nv_
     const int oy = static_cast<int>(r % ho);
     const long long img = r / ho;
     float s[G] = {};
+    if constexpr (G == 8) {
+      if (k == 4) {  // the stem pool: all 16 loads in flight, then summed in the generic order
+        uint4 raw[16];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+            raw[4 * a + b] = __ldg(reinterpret_cast<const uint4*>(
+                x + ((img * ho * 4 + oy * 4 + a) * W + ox * 4 + b) * xs + ch));
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+          const uint32_t w4[4] = {raw[t].x, raw[t].y, raw[t].z, raw[t].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            s[2 * e] += __uint_as_float(w4[e] << 16);
+            s[2 * e + 1] += __uint_as_float(w4[e] & 0xFFFF0000u);
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < G; ++e) s[e] *= inv;
+        stv<G>(y + op * ys + ch, s);
+        continue;
+      }
+    }
     for (int a = 0; a < k; ++a) {
       const __nv_bfloat16* row = x + ((img * ho * k + oy * k + a) * W + ox * k) * xs + ch;
       for (int b = 0; b < k; ++b) {

@@ -173,6 +173,23 @@ def test_trainer_matches_reference_trainer(lag):
     assert [s for s, _ in res.digests] == [1, 3]
 
 
+@pytest.mark.parametrize("c", [64, 12])
+def test_avgpool_fwd_k4_bitexact(c):
+    """avgpool forward (ops.py:133-136) at the stem's k = 4: the 16-loads-in-flight path (c = 64)
+    and the scalar path (c = 12) both sum the window row-major in fp32, then scale by 1/16."""
+    from paper_1810_01993_b200 import nhwc
+    torch.manual_seed(1)
+    x = torch.randn(2, 16, 20, c, device="cuda").to(torch.bfloat16)
+    y = torch.empty(2, 4, 5, c, dtype=torch.bfloat16, device="cuda")
+    nhwc.avgpool_fwd(nhwc.View(x), nhwc.View(y), 4)
+    xf = x.float().cpu().reshape(2, 4, 4, 5, 4, c)
+    s = torch.zeros(2, 4, 5, c)
+    for a in range(4):
+        for b in range(4):
+            s = s + xf[:, :, a, :, b, :]
+    assert torch.equal(y.cpu(), (s * (1.0 / 16)).to(torch.bfloat16))
+
+
 def test_memory_bound_kernels_vs_torch():
     from paper_1810_01993_b200 import nhwc
     torch.manual_seed(0)
