@@ -6,8 +6,10 @@ here load with the reference's `load_checkpoint` and vice versa (tests/golden/ck
 
 `save_train_state` / `load_train_state` extend a parameter checkpoint with everything a resumed
 run needs: per-tensor momentum ("momentum:<name>"), the reduced gradient a lag-1
-run still has to apply ("lag_grad:<name>"), and counters ("meta:steps", "meta:have_prev") --
-still a plain CKP1 file, so the reference's reader sees the weights plus extra named tensors.
+run still has to apply ("lag_grad:<name>", stored as the rank MEAN, so a run may resume on a
+different number of ranks), and counters ("meta:steps" as two exact 16-bit halves [lo, hi],
+"meta:have_prev", "meta:world" = the writer's rank count) -- still a plain CKP1 file, so the
+reference's reader sees the weights plus extra named tensors.
 """
 
 from __future__ import annotations
@@ -71,8 +73,12 @@ def save_train_state(path: str, trainer) -> None:
     tensors.update({f"momentum:{k}": v for k, v in st["momentum"].items()})
     if st["lag_grad"] is not None:
         tensors.update({f"lag_grad:{k}": v for k, v in st["lag_grad"].items()})
-    tensors["meta:steps"] = np.array([st["steps"]], dtype=np.float32)
+    steps = int(st["steps"])
+    if not 0 <= steps < 2 ** 32:
+        raise ValueError(f"step count {steps} out of range")
+    tensors["meta:steps"] = np.array([steps & 0xFFFF, steps >> 16], dtype=np.float32)   # exact halves
     tensors["meta:have_prev"] = np.array([1.0 if st["have_prev"] else 0.0], dtype=np.float32)
+    tensors["meta:world"] = np.array([st.get("world", 1)], dtype=np.float32)
     save_checkpoint(path, tensors)
 
 
@@ -85,5 +91,7 @@ def load_train_state(path: str, trainer) -> None:
         raise KeyError(f"{path}: missing tensors for {missing[:3]}")
     have_prev = bool(t.get("meta:have_prev", np.zeros(1))[0])
     lag = {k: t[f"lag_grad:{k}"] for k in order} if have_prev else None
+    ms = t["meta:steps"]
+    steps = int(ms[0]) + (int(ms[1]) << 16 if ms.size > 1 else 0)
     trainer.import_state({"params": {k: t[k] for k in order}, "momentum": {k: t[f"momentum:{k}"] for k in order},
-                          "lag_grad": lag, "steps": int(t["meta:steps"][0]), "have_prev": have_prev})
+                          "lag_grad": lag, "steps": steps, "have_prev": have_prev})

@@ -865,6 +865,51 @@ class Engine:
             nhwc.reduce_segments(table, nseg, max_n, self.flat_g)
             self.launches += 1
 
+    def _param_done(self, names, pending, on_bucket_ready):
+        """Count parameters whose gradients are enqueued; fire each bucket that completes.
+
+        A bucket's gradients are written from BOTH compute streams (most wgrads and their split-K
+        reductions run on the side stream, the stem's / batch norm's on the main stream, and
+        side-stream wgrads trail main-stream dgrads across layers), so the all-reduce must not be
+        issued from whichever stream happens to be current: it is issued from a bucket stream that
+        first waits on both, which orders the collective after every write into the bucket (the
+        reference reduces a tensor only once it is final, trainer.py:222-241) without making the
+        compute streams wait on each other."""
+        for name in names:
+            i = self.bucket_of[name]
+            pending[i] -= 1
+            if pending[i] != 0:
+                continue
+            self._reduce_bucket(i)
+            if on_bucket_ready is None:
+                continue
+            if self.side is None or os.environ.get("B2DL_BUCKET_JOIN", "1") == "0":
+                on_bucket_ready(i)   # B2DL_BUCKET_JOIN=0: the unjoined issue (negative control only)
+                continue
+            bs = self._bucket_stream()
+            for s in (torch.cuda.current_stream(), self.side):
+                ev = torch.cuda.Event()
+                ev.record(s)
+                bs.wait_event(ev)
+            with torch.cuda.stream(bs):
+                on_bucket_ready(i)
+
+    def _bucket_stream(self):
+        if getattr(self, "_bstream", None) is None:
+            self._bstream = torch.cuda.Stream(device=self.device)
+        return self._bstream
+
+    def _stress_side(self, op):
+        """Test knob (B2DL_STRESS_SIDE_US): delay the side stream before the wgrads of the
+        convs named by B2DL_STRESS_CONVS (prefix match), so a collective that is not ordered after
+        them would read stale gradients."""
+        us = int(os.environ.get("B2DL_STRESS_SIDE_US", "0"))
+        if us <= 0:
+            return
+        pref = os.environ.get("B2DL_STRESS_CONVS", "s0.")
+        if any(op.w.startswith(p) for p in pref.split(",")):
+            torch.cuda._sleep(int(us * 1900))   # ~1.9 cycles per ns at the boost clock
+
     def backward(self, on_bucket_ready=None):
         """Fill flat_g with d loss / d params (param layout HWIO for conv weights).
 
@@ -885,13 +930,7 @@ class Engine:
                                     self.ws, bias_grad=self.flat_g[b_off:b_off + op.cout])
                 self._toc(ev, op, "wgrad")
                 self.launches += 3
-                for name in (op.w, op.b):
-                    i = self.bucket_of[name]
-                    pending[i] -= 1
-                    if pending[i] == 0:
-                        self._reduce_bucket(i)
-                        if on_bucket_ready is not None:
-                            on_bucket_ready(i)
+                self._param_done((op.w, op.b), pending, on_bucket_ready)
                 if st["dx"] is not None:
                     ev = self._tic()
                     nhwc.f32_conv_dgrad(gy, self.wslice(op.w), op.cin, op.k, op.k, op.dil, self.gv(op.ins[0]),
@@ -914,6 +953,8 @@ class Engine:
                     fork.record()
                     side.wait_event(fork)
                 with (torch.cuda.stream(side) if side is not None else contextlib.nullcontext()):
+                    if side is not None:
+                        self._stress_side(op)
                     ev = self._tic()
                     # wgrad GEMM with the bias column sums folded in; split-K partials stay in the
                     # conv's partial buffer and are reduced right after it (fixed order, L2-hot)
@@ -941,13 +982,7 @@ class Engine:
                     self._toc(ev, op, "wgrad", flops=wflops if op.out in self.up_wgrad else None)
                     self.launches += 1
                     self._reduce_conv(op)
-                    for name in (op.w, op.b):
-                        i = self.bucket_of[name]
-                        pending[i] -= 1
-                        if pending[i] == 0:
-                            self._reduce_bucket(i)
-                            if on_bucket_ready is not None:
-                                on_bucket_ready(i)
+                    self._param_done((op.w, op.b), pending, on_bucket_ready)
                 if op.w in self.heads:
                     pass   # input gradient already produced by head_backward
                 elif st["dx"] is not None and op.k == 1 and op.cout < 8:
@@ -990,13 +1025,7 @@ class Engine:
                                  self.gv(op.ins[0]) if st["dx"] is not None else None, self.ws,
                                  accumulate=bool(st["dx"]))
                 self.launches += 3
-                for name in (op.w, op.b):
-                    i = self.bucket_of[name]
-                    pending[i] -= 1
-                    if pending[i] == 0:
-                        self._reduce_bucket(i)
-                        if on_bucket_ready is not None:
-                            on_bucket_ready(i)
+                self._param_done((op.w, op.b), pending, on_bucket_ready)
             elif op.kind == "up" and op.mode == "bilinear":
                 nhwc.bilinear_bwd(self.gv(op.out), self.gv(op.ins[0]), op.factor, accumulate=st["dx"],
                                   mask=self.v(op.ins[0]) if st["mask"] else None, ws=self.ws)
@@ -1027,6 +1056,10 @@ class Engine:
         if self.side is not None and not self.fp32:   # all wgrads (and their reductions) done
             ev = torch.cuda.Event()
             ev.record(self.side)
+            torch.cuda.current_stream().wait_event(ev)
+        if getattr(self, "_bstream", None) is not None:   # rejoin the bucket stream (graph capture)
+            ev = torch.cuda.Event()
+            ev.record(self._bstream)
             torch.cuda.current_stream().wait_event(ev)
 
     def _add(self, x, y, accumulate=False, mask=None):

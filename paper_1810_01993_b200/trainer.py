@@ -291,9 +291,13 @@ class DataParallelTrainer:
         self._wait_comm()
         torch.cuda.synchronize()
         eng = self.eng
+        pending = self.lag == 1 and self.have_prev
+        # the pending lag-1 gradient is the rank SUM (the 1/P is applied in the update): export
+        # the mean so the state is independent of the number of ranks that wrote it
         return {"params": eng.export_params(), "momentum": eng._export(eng.flat_m),
-                "lag_grad": eng._export(eng.flat_g) if (self.lag == 1 and self.have_prev) else None,
-                "steps": self.steps_done, "have_prev": bool(self.lag == 1 and self.have_prev)}
+                "lag_grad": ({k: v / np.float32(self.world) for k, v in eng._export(eng.flat_g).items()}
+                             if pending else None),
+                "steps": self.steps_done, "have_prev": bool(pending), "world": self.world}
 
     def import_state(self, st: dict):
         eng = self.eng
@@ -303,7 +307,10 @@ class DataParallelTrainer:
         if st.get("have_prev"):
             if self.lag != 1:
                 raise ValueError("state carries a pending lag-1 gradient but the trainer has lag 0")
-            eng.import_flat(eng.flat_g, st["lag_grad"])
+            # mean -> this run's rank sum (bitwise when the world sizes match: x / P * P with P a
+            # power of two is exact)
+            eng.import_flat(eng.flat_g, {k: np.asarray(v, np.float32) * np.float32(self.world)
+                                         for k, v in st["lag_grad"].items()})
         self.have_prev = bool(st.get("have_prev")) and self.lag == 1
         self.steps_done = int(st.get("steps", 0))
         self.net._params = eng.export_params()
@@ -422,6 +429,9 @@ def train_run(cfg: RunConfig, net_cls=None) -> TrainResult:
         lv = float(loss.item())
         if not math.isfinite(lv):
             raise TrainingError(f"rank {rank}: non-finite loss at step {t + 1}")
+        # the LARC status of this step's update (reset by every update): a non-finite norm raises
+        # on the step it happens, like optimizer.py:56-57, not at the end of the run
+        tr.check_status()
         rate = torch.tensor([cfg.local_batch / wall, lv, wall], dtype=torch.float64)
         if world > 1:
             allr = [torch.zeros_like(rate) for _ in range(world)]

@@ -108,3 +108,82 @@ def test_hierarchical_allreduce_matches_flat_on_four_gpus():
     assert np.allclose(flat[0][0], hier[0][0], rtol=1e-5)
     for k, v in flat[0][2].items():
         assert np.max(np.abs(v - hier[0][2][k])) <= 1e-5 * max(np.max(np.abs(v)), 1e-12), k
+
+
+# ---------------------------------------------------------------------------------------------
+# DeepLabV3+ at config-1 scale (16 x 288 x 192): split invariance of the data-parallel step
+# (reference trainer.py:70-79 draws sample j of step t from default_rng((seed, 0, t, j)) and
+# reduces a tensor only once it is final, trainer.py:222-241): 2 ranks x batch 1 must follow
+# 1 rank x batch 2.  The side stream is delayed before the stage-0 wgrads (B2DL_STRESS_SIDE_US),
+# so a bucket all-reduce that is not ordered after every write into its bucket reads stale
+# gradients and the ranks diverge (the negative control shows the knob does expose that).
+
+def _dl_worker(rank, world, port, lag, steps, env, q):
+    os.environ.update(env)
+    import torch.distributed as dist
+    if world > 1:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        torch.cuda.set_device(rank)
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    from paper_1810_01993_b200.models import DeepLabConfig
+    from paper_1810_01993_b200.optimizer import OptimConfig
+    from paper_1810_01993_b200.scenes import SceneConfig
+    from paper_1810_01993_b200.trainer import RunConfig, TrainingError, train_run
+    sc = SceneConfig(height=288, width=192)
+    cfg = RunConfig(lag=lag, steps=steps, local_batch=2 // world, seed=3, optim=OptimConfig(lr=0.05),
+                    net=DeepLabConfig(), scene=sc, hash_steps=tuple(range(1, steps + 1)))
+    try:
+        res = train_run(cfg)
+        q.put((rank, "ok", res.losses, res.digests, res.state))
+    except TrainingError as e:
+        q.put((rank, "diverged", str(e), None, None))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _dl_run(world, lag, steps=3, env=None):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dl_worker, args=(r, world, port, lag, steps, env or {}, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = {}
+    for _ in range(world):
+        r, *rest = q.get(timeout=900)
+        out[r] = rest
+    for p in procs:
+        p.join(timeout=120)
+    return out
+
+
+STRESS = {"B2DL_STRESS_SIDE_US": "20000", "B2DL_STRESS_CONVS": "s0.,s1.b0"}
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("lag", [0, 1])
+def test_deeplab_two_gpu_split_invariance_under_side_stream_delay(lag):
+    one = _dl_run(1, lag)[0]
+    two = _dl_run(2, lag, env=STRESS)
+    assert one[0] == "ok" and two[0][0] == "ok" and two[1][0] == "ok", (one[:2], two[0][:2], two[1][:2])
+    # bitwise-identical weights on both ranks at every step (NCCL result is byte-identical)
+    assert two[0][2] == two[1][2]
+    # the 2 x 1 trajectory follows the 1 x 2 one (bf16 bar, north star: 2e-2)
+    assert np.allclose(two[0][1], one[1], rtol=2e-2), (two[0][1], one[1])
+    worst = []
+    for k, v in one[3].items():
+        u = two[0][3][k]
+        err = np.max(np.abs(u - v)) / max(np.max(np.abs(v)), 1e-12)
+        worst.append((err, k))
+    worst.sort(reverse=True)
+    assert worst[0][0] < 2e-2, worst[:5]
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_deeplab_two_gpu_negative_control_unjoined_bucket_diverges():
+    """Without the bucket-stream join (B2DL_BUCKET_JOIN=0) the same delay makes the last bucket
+    (stem + stage 0/1) all-reduce before its side-stream wgrads land: ranks end up applying
+    different gradients, which the step-1 weight digest check reports."""
+    two = _dl_run(2, 0, steps=2, env=dict(STRESS, B2DL_BUCKET_JOIN="0"))
+    diverged = two[0][0] == "diverged" or two[1][0] == "diverged" or two[0][2] != two[1][2]
+    assert diverged
