@@ -115,6 +115,53 @@ def _dist_init(args):
     return world, rank, local
 
 
+def _deskdl():
+    """The unmodified reference package, installed by `pip install --target baseline/_ref`
+    (DESIGN.md §8), or None."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "deskdl")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    import deskdl
+    return deskdl
+
+
+def reference_step_times(steps: int, warmup: int):
+    """(seconds per step, kind, backend): the reference's own training step -- deskdl's
+    executor (ops.run_forward / run_backward, ops.py:44-106) with its stock conv backend
+    (kernels.py:19-40, NumPy im2col + OpenBLAS here: the fastest it ships) and its LARC update
+    per tensor (optimizer.py:79-83, trainer.py:364-367) -- on the bounded sample, all host
+    threads.  Falls back to the oracle port (kind "port") when deskdl is not installed."""
+    deskdl = _deskdl()
+    if deskdl is None:
+        return cpu_step_time(steps, warmup), "port", "oracle/deskdl_port.py"
+    os.environ.setdefault("DESKDL_KERNELS", "python")   # im2col+sgemm: ~9x the Cython loops here
+    from deskdl.graph import OpGraph
+    from deskdl.model import ClassWeights, kernels, ops
+    from deskdl.optimizer import LayerParam, OptimConfig, larc_sgd_step
+    from paper_1810_01993_b200 import models
+    from paper_1810_01993_b200.scenes import SceneConfig, make_scene, scene_rng
+    graph, params, head, lossn = models.build_deeplab(models.DeepLabConfig(), seed=0, graph_cls=OpGraph)
+    order = list(params)
+    lps = {k: LayerParam(k, params[k]) for k in order}
+    cfg = OptimConfig(lr=0.01, momentum=0.9, trust=0.02)
+    n, c, h, w = CPU_SAMPLE
+    f, lab = make_scene(SceneConfig(channels=c, height=h, width=w), scene_rng(0, 0, 0))
+    cw = ClassWeights((0.982, 0.017, 0.001)).vector()
+    times = []
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        values = {k: lps[k].w for k in order}
+        values.update(x=f[None], labels=lab[None], class_weights=cw)
+        out, tape = ops.run_forward(graph, values, targets=[lossn, head])
+        grads = ops.run_backward(graph, tape, lossn, wrt=order)
+        for k in order:
+            larc_sgd_step(lps[k], grads[k].reshape(lps[k].w.shape), cfg)
+        times.append(time.perf_counter() - t0)
+    return times[warmup:], "reference", f"deskdl {kernels.BACKEND} backend"
+
+
 def cpu_step_time(steps: int, warmup: int):
     """Seconds per reference CPU step on the bounded sample (oracle port, all host threads)."""
     from oracle import deskdl_port as O
@@ -135,12 +182,15 @@ def cpu_step_time(steps: int, warmup: int):
     return times[warmup:]
 
 
-def _sample_desc():
+def _sample_desc(kind="reference", backend="deskdl python backend"):
     n, c, h, w = CPU_SAMPLE
     frac = (h * w) / (H * W)
-    return (f"oracle/ NumPy port of deskdl's step (im2col + OpenBLAS sgemm, tape VJPs, LARC) on the same "
-            f"DeepLabV3+ graph at {n}x{c}x{h}x{w} = {frac:.4f} of one {H}x{W} tile; conv FLOPs scale "
-            f"linearly with pixels, so images/s = {frac:.4f} / step time"), frac
+    who = (f"the reference itself (deskdl 0.1.0 from baseline/_ref, {backend}: ops.run_forward/run_backward "
+           f"+ per-tensor larc_sgd_step)" if kind == "reference" else
+           "oracle/ NumPy port of deskdl's step (im2col + OpenBLAS sgemm, tape VJPs, LARC)")
+    return (f"{who} on the same DeepLabV3+ graph at {n}x{c}x{h}x{w} = {frac:.4f} of one {H}x{W} tile; "
+            f"EXTRAPOLATED to full tiles: conv FLOPs scale linearly with pixels, so images/s = "
+            f"{frac:.4f} / step time (a full-tile deskdl step needs ~40 GB of im2col caches and ~100+ s)"), frac
 
 
 KERNEL_OF_PASS = {
@@ -165,9 +215,19 @@ def _traffic(dom):
     return None, None
 
 
-def _config(world):
-    return {"workload": "config 2/3: DeepLabV3+ (ResNet-50 OS8, ASPP 12/18/24, full-res decoder) "
-                        "bf16 train step, fused weighted CE + LARC", "model": "DeepLabV3+",
+WORKLOADS = {
+    "reference-ops": ("config 2/3: DeepLabV3+ (ResNet-50 OS8, ASPP 12/18/24, full-res decoder) bf16 train step, "
+                      "fused weighted CE + LARC", "DeepLabV3+"),
+    "bn-bilinear": ("north-star DeepLabV3+ variant (batch norm after every conv, bilinear decoder upsampling) bf16 "
+                    "train step, fused weighted CE + LARC", "DeepLabV3+ (BN + bilinear)"),
+    "tiramisu": ("config 4: Tiramisu / FC-DenseNet (5 levels, (2,2,2,4,5) dense blocks, growth 32, 5x5) train "
+                 "step, fused weighted CE + LARC", "Tiramisu"),
+}
+
+
+def _config(world, variant="reference-ops"):
+    wl, model = WORKLOADS[variant]
+    return {"workload": wl, "model": model, "variant": variant,
             "global_batch": world * LOCAL_BATCH, "local_batch": LOCAL_BATCH, "tile": [C, H, W],
             "parallelism": f"dp{world}", "l2": "working set ~11 GB/GPU >> 126 MB L2, no flush"}
 
@@ -177,19 +237,20 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    # bounded: each CPU step is ~6 s on 16 cores, keep the whole arm within a few minutes
-    times = cpu_step_time(max(1, min(args.steps, 8)), min(args.warmup, 1))
-    desc, frac = _sample_desc()
+    # bounded: each CPU step is ~6-9 s, keep the whole arm within a few minutes
+    times, kind, backend = reference_step_times(max(1, min(args.steps, 8)), min(args.warmup, 1))
+    desc, frac = _sample_desc(kind, backend)
     ms = 1e3 * float(np.median(times))
     value = frac / (ms / 1e3)
     cores = os.cpu_count()
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world,
             "steps": len(times), "warmup": min(args.warmup, 1), "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (make_scene)",
-            "config": dict(_config(world), reference_arm="reference CPU step (oracle port, all host threads) on a "
-                           "bounded sample of the same workload, rank 0 only", sample_batch=CPU_SAMPLE[0],
-                           sample_tile=list(CPU_SAMPLE[1:])),
-            "cpu_baseline": {"value": value, "unit": "images/s", "cores": cores, "kind": "port", "sample": desc},
+            "config": dict(_config(world), reference_arm=f"reference CPU step ({kind}: {backend}, all host "
+                           "threads) on a bounded sample of the same workload, rank 0 only",
+                           sample_batch=CPU_SAMPLE[0], sample_tile=list(CPU_SAMPLE[1:])),
+            "cpu_baseline": {"value": value, "unit": "images/s", "cores": cores, "kind": kind, "sample": desc,
+                             "extrapolated": True, "step_s": ms / 1e3},
             "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(line)
     return 0
@@ -204,6 +265,7 @@ def run_ours(args):
     from paper_1810_01993_b200.net import DeepLabV3Plus
     from paper_1810_01993_b200.optimizer import OptimConfig
     from paper_1810_01993_b200.scenes import SceneConfig, device_scene_pool
+    from paper_1810_01993_b200.stats import StepRecord, sustained_stats
     from paper_1810_01993_b200.trainer import DataParallelTrainer
 
     world, rank, local = _dist_init(args)
@@ -262,11 +324,16 @@ def run_ours(args):
     # ---- timed region: device events around K steps, max over ranks
     launches0 = eng.launches
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # one event per step boundary as well: the per-step rates the reference's statistics use
+    # (stats.py:58-79 median of per-step rank-mean rates, first step dropped, p16/p84)
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     barrier()
     t_lo = time.time()
     e0.record()
+    marks[0].record()
     for i in range(args.steps):
         tr.step(*batches[i % pool])
+        marks[i + 1].record()
     e1.record()
     barrier()
     t_hi = time.time()
@@ -286,6 +353,16 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     value = world * LOCAL_BATCH / (ms / 1e3)
+    step_ms = torch.tensor([marks[i].elapsed_time(marks[i + 1]) for i in range(args.steps)], dtype=torch.float64,
+                           device=dev)
+    if world > 1:
+        allm = [torch.zeros_like(step_ms) for _ in range(world)]
+        dist.all_gather(allm, step_ms)
+    else:
+        allm = [step_ms]
+    allm = torch.stack(allm).cpu().numpy()          # [rank][step] ms
+    records = [StepRecord(step=i + 1, rates=tuple(LOCAL_BATCH / (allm[:, i] / 1e3)), wall=float(allm[:, i].max()) / 1e3,
+                          loss=0.0) for i in range(args.steps)]
 
     # ---- e2e: public API, host inputs (pinned) copied every step, loss read back every step
     host = [(b[0].cpu().pin_memory(), b[1].cpu().pin_memory()) for b in batches]
@@ -345,10 +422,10 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        times = cpu_step_time(2, 0)
-        desc, frac = _sample_desc()
+        times, kind, backend = reference_step_times(2, 0)
+        desc, frac = _sample_desc(kind, backend)
         cpu = {"value": frac / float(np.median(times)), "unit": "images/s", "cores": os.cpu_count(),
-               "kind": "port", "sample": desc, "step_s": float(np.median(times))}
+               "kind": kind, "sample": desc, "extrapolated": True, "step_s": float(np.median(times))}
 
     peak, peak_sust, hbm, src = _peaks()
     achieved_all = conv_flops / (conv_ms / 1e3) / 1e12 if conv_ms > 0 else 0.0
@@ -358,20 +435,27 @@ def run_ours(args):
     achieved = dom_fl / (dom_ms / 1e3) / 1e12 if dom_ms > 0 else 0.0
     traffic, traffic_src = _traffic(dom)
     if rank == 0:
-        sust_tf = value * flops_img / 1e12
+        rule_tf = value * flops_img / 1e12
+        exec_img = conv_flops / args.steps / LOCAL_BATCH
+        exec_tf = value * exec_img / 1e12
+        st = sustained_stats(records, per_sample_flops=exec_img)
         line = {
             "metric": metric, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (GPU-generated scenes, resident in HBM)",
-            "config": dict((dict(_config(world), variant=variant, model=type(net).__name__)
-                            if variant != "reference-ops" else _config(world)),
-                           **({"allreduce": f"hierarchical {args.hierarchy}"} if hier else {})),
-            "sustained_tflops": sust_tf, "flops_per_image": flops_img, "flops_per_image_exact": flops_img_exact,
-            # the reference FLOP rule counts full.c0 as a full-resolution 3x3 conv; the engine computes
-            # it from the low-resolution input (fewer MACs, same result): tensor-core FLOPs executed
-            "executed_conv_flops_per_image": conv_flops / args.steps / LOCAL_BATCH,
-            "executed_tflops": value * conv_flops / args.steps / LOCAL_BATCH / 1e12,
-            "frac_of_peak": sust_tf / peak,
+            "config": dict(_config(world, variant), **({"allreduce": f"hierarchical {args.hierarchy}"} if hier else {})),
+            # sustained TF/s = tensor-core FLOPs the step executes x images/s (the convs' MACs; full.c0
+            # runs from the low-resolution input, so this is below the reference-rule count)
+            "sustained_tflops": exec_tf, "frac_of_peak": exec_tf / peak,
+            "executed_conv_flops_per_image": exec_img,
+            # the reference's own statistics over the same K device-timed steps (stats.py:58-79):
+            # median / p16 / p84 of the per-step rank-mean rate, first step dropped; global = x world
+            "stats": {"global_images_per_s_median": st.global_rate, "rank_rate_median": st.median,
+                      "rank_rate_p16": st.p16, "rank_rate_p84": st.p84, "steps_used": st.steps,
+                      "sustained_tflops_median": st.flops_per_s / 1e12},
+            # reference FLOP rule (flops.py:56-112, 3 x forward, full.c0 counted at full resolution)
+            "reference_rule": {"flops_per_image": flops_img, "flops_per_image_exact": flops_img_exact,
+                               "tflops": rule_tf, "frac_of_peak": rule_tf / peak},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                          "kernel": f"{dom}: {KERNEL_OF_PASS[dom]} (all {dom} launches of one step, each timed "

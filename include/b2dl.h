@@ -57,7 +57,27 @@ typedef struct b2dl_act {
 
 /* ---------------------------------------------------------------- (1) reference-shaped */
 
-/* Workspace bytes needed by the NCHW fp32 entry points for this shape. */
+/* Reference-precision core (csrc/refconv.cu): the Cython core's fused type
+ * (_convkernels.pyx:11-13, float32 / float64) -- NCHW tensors of `dtype`, computed in
+ * that type (fp32 FFMA / fp64 DFMA), "same" padding, stride 1, any dilation.  No
+ * workspace; outputs are fully overwritten (the core zero-fills, pyx:23,42,61).
+ * These are what the drop-in backend (backend.py, BACKEND_NAME "b200") calls. */
+enum { B2DL_DTYPE_F32 = 0, B2DL_DTYPE_F64 = 1 };
+
+/* Replaces conv2d_forward_core (_convkernels.pyx:16-32) + _kernels_py.conv2d_forward (:44-55). */
+B2DL_API int b2dl_conv2d_forward_typed(int dtype, const void* x, const void* w, void* y, int n, int cin, int h,
+                                       int wd, int cout, int kh, int kw, int stride, int dilation, void* stream);
+/* Replaces conv2d_backward_input_core (_convkernels.pyx:35-51) + _kernels_cy.py:34-44. */
+B2DL_API int b2dl_conv2d_backward_input_typed(int dtype, const void* dy, const void* w, void* dx, int n, int cin,
+                                              int h, int wd, int cout, int kh, int kw, int stride, int dilation,
+                                              void* stream);
+/* Replaces conv2d_backward_weights_core (_convkernels.pyx:54-71) + _kernels_cy.py:28-31. */
+B2DL_API int b2dl_conv2d_backward_weights_typed(int dtype, const void* x, const void* dy, void* dw, int n, int cin,
+                                                int h, int wd, int cout, int kh, int kw, int dilation, void* stream);
+
+/* bf16 tensor-core variants of the same three products (fp32 NCHW in / out, operands rounded
+ * to bf16, fp32 accumulation): the training step's arithmetic, opt-in backend "b200-bf16".
+ * Workspace bytes needed by these entry points for this shape: */
 B2DL_API size_t b2dl_conv2d_workspace_size(int n, int cin, int h, int w, int cout, int kh, int kw);
 
 /* y[n,cout,h,w] = conv(x[n,cin,h,w], w[cout,cin,kh,kw]), same padding.
@@ -238,9 +258,11 @@ B2DL_API size_t b2dl_bias_grad_workspace_size(b2dl_act g);
  *   dlogits       (softmax - onehot) * w_y / (sum_p w_y * N) written as a bf16
  *                 NHWC view with `classes` channels
  *   pred          argmax over classes, ties to the lowest index (uint8)
+ *   status[0]     (optional) 1 if any label is >= classes, else 0; the loss is then NaN
+ *                 (the reference raises ValueError, loss.py:72-74; the host shim maps it)
  * logits: fp32 NHWC view with `classes` channels; labels uint8 [N*H*W]. */
 B2DL_API int b2dl_wce(b2dl_act logits, const uint8_t* labels, const float* class_weights, int classes, float* loss_out,
-             int* counts, b2dl_act dlogits, int dlogits_f32, uint8_t* pred, void* workspace,
+             int* counts, b2dl_act dlogits, int dlogits_f32, uint8_t* pred, int* status, void* workspace,
              size_t workspace_bytes, void* stream);
 B2DL_API size_t b2dl_wce_workspace_size(int n, int h, int w, int classes);
 

@@ -72,6 +72,9 @@ _SIGS = {
     "b2dl_conv2d_forward": (_c_int, [_vp, _vp, _vp] + [_c_int] * 9 + [_vp, _sz, _vp]),
     "b2dl_conv2d_backward_input": (_c_int, [_vp, _vp, _vp] + [_c_int] * 9 + [_vp, _sz, _vp]),
     "b2dl_conv2d_backward_weights": (_c_int, [_vp, _vp, _vp] + [_c_int] * 8 + [_vp, _sz, _vp]),
+    "b2dl_conv2d_forward_typed": (_c_int, [_c_int, _vp, _vp, _vp] + [_c_int] * 9 + [_vp]),
+    "b2dl_conv2d_backward_input_typed": (_c_int, [_c_int, _vp, _vp, _vp] + [_c_int] * 9 + [_vp]),
+    "b2dl_conv2d_backward_weights_typed": (_c_int, [_c_int, _vp, _vp, _vp] + [_c_int] * 8 + [_vp]),
     "b2dl_cin_pad": (_c_int, [_c_int]),
     "b2dl_conv_fprop": (_c_int, [ctypes.POINTER(ConvArgs), _vp]),
     "b2dl_wgrad_workspace_size": (_sz, [ctypes.POINTER(WgradArgs)]),
@@ -116,7 +119,7 @@ _SIGS = {
     "b2dl_dgrad_1x1_small": (_c_int, [Act, _vp, Act, _c_int, Act, _vp]),
     "b2dl_bias_grad": (_c_int, [Act, _vp, _c_int, _vp, _sz, _vp]),
     "b2dl_bias_grad_workspace_size": (_sz, [Act]),
-    "b2dl_wce": (_c_int, [Act, _vp, _vp, _c_int, _vp, _vp, Act, _c_int, _vp, _vp, _sz, _vp]),
+    "b2dl_wce": (_c_int, [Act, _vp, _vp, _c_int, _vp, _vp, Act, _c_int, _vp, _vp, _vp, _sz, _vp]),
     "b2dl_wce_workspace_size": (_sz, [_c_int] * 4),
     "b2dl_larc_workspace_size": (_sz, [ctypes.c_int64, _c_int]),
     "b2dl_larc_update": (_c_int, [ctypes.POINTER(LarcArgs), _vp]),

@@ -145,7 +145,8 @@ __global__ void k_wce_main(const float* __restrict__ logits, int ls, const uint8
 }
 
 __global__ void k_wce_final(const double* __restrict__ part, int nb, const int* __restrict__ counts,
-                            const float* __restrict__ cw, int classes, int nimg, float* __restrict__ loss) {
+                            const float* __restrict__ cw, int classes, int nimg, float* __restrict__ loss,
+                            const int* __restrict__ err, int* __restrict__ status) {
   // one warp: lane-strided partial sums, then a fixed xor tree (deterministic order)
   if (blockIdx.x != 0) return;
   const int lane = threadIdx.x & 31;
@@ -158,7 +159,13 @@ __global__ void k_wce_final(const double* __restrict__ part, int nb, const int* 
     for (int c = 0; c < classes; ++c) ws += static_cast<double>(counts[n * classes + c]) * cw[c];
     total += s / ws;
   }
-  if (lane == 0) loss[0] = static_cast<float>(total / nimg);
+  if (lane == 0) {
+    // a label outside [0, classes) (the reference raises ValueError, loss.py:72-74): the loss is
+    // NaN, so it cannot pass for a real value, and the status word says why
+    const bool bad = *err != 0;
+    loss[0] = bad ? __int_as_float(0x7fc00000) : static_cast<float>(total / nimg);
+    if (status) *status = bad ? 1 : 0;
+  }
 }
 
 }  // namespace b2
@@ -173,7 +180,7 @@ extern "C" size_t b2dl_wce_workspace_size(int n, int h, int w, int classes) {
 
 extern "C" int b2dl_wce(b2dl_act logits, const uint8_t* labels, const float* class_weights, int classes,
                         float* loss_out, int* counts, b2dl_act dlogits, int dlogits_f32, uint8_t* pred,
-                        void* workspace, size_t workspace_bytes, void* stream) {
+                        int* status, void* workspace, size_t workspace_bytes, void* stream) {
   if (classes < 2 || classes > WCE_MAX_CLASSES || logits.c != classes || dlogits.c != classes) return B2DL_E_VALUE;
   if (!logits.ptr || !labels || !class_weights || !loss_out || !counts || !dlogits.ptr) return B2DL_E_VALUE;
   if (workspace_bytes < b2dl_wce_workspace_size(logits.n, logits.h, logits.w, classes)) return B2DL_E_VALUE;
@@ -190,6 +197,6 @@ extern "C" int b2dl_wce(b2dl_act logits, const uint8_t* labels, const float* cla
   k_wce_main<<<grid, WCE_THREADS, 0, st>>>(reinterpret_cast<const float*>(logits.ptr), logits.c_stride, labels, class_weights,
                                    counts, hw, classes, logits.n, dlogits.ptr, dlogits.c_stride, dlogits_f32,
                                    pred, part);
-  k_wce_final<<<1, 32, 0, st>>>(part, nb, counts, class_weights, classes, logits.n, loss_out);
+  k_wce_final<<<1, 32, 0, st>>>(part, nb, counts, class_weights, classes, logits.n, loss_out, err, status);
   return check_launch();
 }

@@ -545,6 +545,8 @@ class Engine:
         self.class_weights = torch.ones(p.classes, dtype=f32, device=self.device)
         self.loss = torch.zeros(1, dtype=f32, device=self.device)
         self.counts = torch.zeros(n * p.classes, dtype=torch.int32, device=self.device)
+        # 1 after a step whose labels were outside [0, classes) (its loss is NaN)
+        self.label_status = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.input_shape = tuple(input_shape)
         self.launches = 0
         self.conv_timing = False
@@ -853,7 +855,7 @@ class Engine:
             self.launches += 1
         elif op.kind == "ce":
             nhwc.wce(self.v(op.ins[0]), self.labels, self.class_weights, self.loss, self.counts,
-                     self.gv(op.ins[0]), self.pred, self.ws, dlogits_f32=self.fp32)
+                     self.gv(op.ins[0]), self.pred, self.ws, dlogits_f32=self.fp32, status=self.label_status)
             self.launches += 2   # histogram + loss/dlogits + final fold (3 with the +1 below)
         self.launches += 1
 

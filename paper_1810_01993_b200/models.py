@@ -165,9 +165,10 @@ def tiramisu_config4(**kw) -> NetConfig:
     return NetConfig(**base)
 
 
-def build_minidensenet(cfg: NetConfig, seed: int = 0):
-    """Graph + params of the reference network (net.py:83-112)."""
-    g = OpGraph()
+def build_minidensenet(cfg: NetConfig, seed: int = 0, graph_cls=OpGraph):
+    """Graph + params of the reference network (net.py:83-112).  `graph_cls` may be the
+    reference's own deskdl.graph.OpGraph (same builder API) to run the graph on deskdl."""
+    g = graph_cls()
     b = _Builder(g, np.random.default_rng(seed))
     x = _io(g)
     k = cfg.growth
@@ -200,9 +201,11 @@ def build_minidensenet(cfg: NetConfig, seed: int = 0):
     return g, b.params, head, loss
 
 
-def build_deeplab(cfg: DeepLabConfig, seed: int = 0):
-    """Graph + params of the DeepLabV3+ (OS8) used for the headline benchmark."""
-    g = OpGraph()
+def build_deeplab(cfg: DeepLabConfig, seed: int = 0, graph_cls=OpGraph):
+    """Graph + params of the DeepLabV3+ (OS8) used for the headline benchmark.  With
+    graph_cls=deskdl.graph.OpGraph the reference-op variant builds as a graph the reference's own
+    executor runs (batch norm / bilinear need this package's OpGraph)."""
+    g = graph_cls()
     b = _Builder(g, np.random.default_rng(seed))
     x = _io(g)
 

@@ -130,6 +130,8 @@ class SegmentationNet:
         eng.set_batch(_dev(batch, torch.float32), _dev(lab, torch.uint8))
         eng.set_class_weights(np.ones(self.cfg.classes) if class_weights is None else class_weights)
         eng.forward()
+        if isinstance(lab, torch.Tensor) and int(eng.label_status.item()):   # device labels: kernel check
+            raise ValueError(f"labels outside [0, {self.cfg.classes})")
         self._steps += 1
         return eng
 

@@ -326,8 +326,14 @@ class DataParallelTrainer:
             self.graph, self.graphs = None, []
 
     def check_status(self):
+        self.check_labels()
         if int(self.status.item()):
             raise FloatingPointError("non-finite norm in LARC")
+
+    def check_labels(self):
+        """ValueError if the last step's labels were outside [0, classes) (loss.py:72-74)."""
+        if int(self.eng.label_status.item()):
+            raise ValueError(f"labels outside [0, {self.eng.plan.classes})")
 
     def digest(self) -> str:
         return param_digest(self.eng.export_params(), self.net.param_order)
@@ -428,6 +434,7 @@ def train_run(cfg: RunConfig, net_cls=None) -> TrainResult:
         wall = ev0.elapsed_time(ev1) / 1e3
         lv = float(loss.item())
         if not math.isfinite(lv):
+            tr.check_labels()
             raise TrainingError(f"rank {rank}: non-finite loss at step {t + 1}")
         # the LARC status of this step's update (reset by every update): a non-finite norm raises
         # on the step it happens, like optimizer.py:56-57, not at the end of the run

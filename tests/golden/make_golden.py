@@ -236,6 +236,24 @@ def gen_checkpoint():
          names=np.array(list(params.keys())))
 
 
+def gen_stats():
+    """The reference's throughput statistics (harness/stats.py:58-79, scaling.py:44-69) on seeded
+    per-step per-rank rate series."""
+    from deskdl.harness.stats import StepRecord, sustained_stats
+    out = {}
+    rng = np.random.default_rng(5)
+    for i, (steps, world, warm) in enumerate([(20, 1, 1), (9, 4, 1), (1, 2, 1), (6, 8, 2), (2, 3, 1)]):
+        rates = rng.uniform(1.0, 3.0, size=(steps, world))
+        recs = [StepRecord(step=t + 1, rates=tuple(rates[t]), wall=1.0 / rates[t].mean(), loss=0.0)
+                for t in range(steps)]
+        st = sustained_stats(recs, per_sample_flops=1.5e12, warmup=warm)
+        out[f"s{i}_rates"] = rates
+        out[f"s{i}_warmup"] = np.array(warm)
+        out[f"s{i}_result"] = np.array([st.median, st.p16, st.p84, st.world, st.steps, st.flops_per_s,
+                                        st.global_rate])
+    save("stats.npz", **out)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:   # e.g. `make_golden.py gen_checkpoint`: regenerate selected fixtures
         for fn in sys.argv[1:]:
@@ -249,3 +267,4 @@ if __name__ == "__main__":
     gen_models()
     gen_flops()
     gen_trainer()
+    gen_stats()

@@ -38,6 +38,11 @@ def test_bench_line_contract():
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     cb = d["cpu_baseline"]
     assert cb["value"] > 0 and cb["cores"] >= 1 and cb["kind"] in ("port", "reference") and cb["sample"]
+    if os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "deskdl")):
+        assert cb["kind"] == "reference"          # deskdl itself, not the port
+    st = d["stats"]                                # the reference's own statistics (stats.py:58-79)
+    assert st["rank_rate_p16"] <= st["rank_rate_median"] <= st["rank_rate_p84"]
+    assert st["global_images_per_s_median"] > 0 and d["sustained_tflops"] > 0
 
 
 def test_reference_arm_contract():

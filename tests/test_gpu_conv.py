@@ -43,7 +43,7 @@ def _ref_conv(x, w, d):
 
 @pytest.mark.parametrize("case", CASES)
 def test_conv2d_forward_nchw(case):
-    from paper_1810_01993_b200.backend import conv2d_forward_device
+    from paper_1810_01993_b200.backend_bf16 import conv2d_forward_device
     n, cin, h, w, cout, k, d = case
     g = torch.Generator(device="cuda").manual_seed(1)
     x = torch.randn(n, cin, h, w, device="cuda", generator=g)
@@ -56,7 +56,7 @@ def test_conv2d_forward_nchw(case):
 
 @pytest.mark.parametrize("case", CASES)
 def test_conv2d_backward_input_nchw(case):
-    from paper_1810_01993_b200.backend import conv2d_backward_input_device
+    from paper_1810_01993_b200.backend_bf16 import conv2d_backward_input_device
     n, cin, h, w, cout, k, d = case
     g = torch.Generator(device="cuda").manual_seed(2)
     dy = torch.randn(n, cout, h, w, device="cuda", generator=g)
@@ -69,7 +69,7 @@ def test_conv2d_backward_input_nchw(case):
 
 @pytest.mark.parametrize("case", CASES)
 def test_conv2d_backward_weights_nchw(case):
-    from paper_1810_01993_b200.backend import conv2d_backward_weights_device
+    from paper_1810_01993_b200.backend_bf16 import conv2d_backward_weights_device
     n, cin, h, w, cout, k, d = case
     g = torch.Generator(device="cuda").manual_seed(3)
     x = torch.randn(n, cin, h, w, device="cuda", generator=g)
