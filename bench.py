@@ -285,7 +285,7 @@ def run_ours(args):
     cw = ClassWeights(scene.frequencies).vector()
     hier = tuple(int(v) for v in args.hierarchy.split("x")) if getattr(args, "hierarchy", "") else None
     tr = DataParallelTrainer(net, OptimConfig(lr=0.01, momentum=0.9, trust=0.02), shape, class_weights=cw,
-                             hierarchy=hier)
+                             hierarchy=hier, lag=args.lag)
     eng = tr.eng
     # synthetic pool, resident in HBM, different tiles per rank
     pool = 4
@@ -443,7 +443,8 @@ def run_ours(args):
             "metric": metric, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (GPU-generated scenes, resident in HBM)",
-            "config": dict(_config(world, variant), **({"allreduce": f"hierarchical {args.hierarchy}"} if hier else {})),
+            "config": dict(_config(world, variant), lag=args.lag,
+                           **({"allreduce": f"hierarchical {args.hierarchy}"} if hier else {})),
             # sustained TF/s = tensor-core FLOPs the step executes x images/s (the convs' MACs; full.c0
             # runs from the low-resolution input, so this is below the reference-rule count)
             "sustained_tflops": exec_tf, "frac_of_peak": exec_tf / peak,
@@ -507,6 +508,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--lag", type=int, default=0, choices=[0, 1],
+                    help="gradient lag (trainer.py:378-383): 1 applies the previous step's reduced gradients")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a captured CUDA graph")
     ap.add_argument("--hierarchy", default="", help="GxL: three-stage hierarchical all-reduce over G groups of L "
                                                      "ranks (the paper's scheme) instead of one flat NCCL all-reduce")

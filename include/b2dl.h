@@ -337,6 +337,26 @@ B2DL_API int b2dl_f32_add(b2dl_act x, b2dl_act y, int accumulate, b2dl_act mask,
 
 B2DL_API const char* b2dl_version(void);
 
+/* ---------------------------------------------------------------- standalone op lowerings
+ * (csrc/generic.cu) -- the reference op kinds that are not part of a conv-bias-relu chain, so any
+ * graph over the reference's op set runs through the engine.  `f32` = 1: fp32 storage (parity
+ * mode), else bf16.  Parameters (bias, B) are the fp32 master. */
+
+/* y (+)= mask? . relu?( alpha . x0 . x1? + bias[c]? ): elementwise mul / scale (ops.py:142-148),
+ * standalone bias_add (:122-126) and relu (:127-128), and their VJPs (:172-177, :195-202).
+ * x1, mask: optional views (ptr NULL); bias: optional fp32 [c]. */
+B2DL_API int b2dl_ewise(b2dl_act x0, b2dl_act x1, b2dl_act mask, b2dl_act y, const float* bias, float alpha,
+                        int relu, int accumulate, int f32, void* stream);
+/* Y = X @ B over the width axis of an NCHW activation (ops.py:120): NHWC views x [n][h][wi][c],
+ * y [n][h][wo][c]; B fp32 row-major [wi][wo] (ldb = wo), or with trans = 1 the input gradient
+ * dX = dY @ B^T (x = dY with wi = W2, y = dX, ldb = x.w).  Optional mask on the output. */
+B2DL_API int b2dl_matmul_w(b2dl_act x, const float* b, int ldb, int trans, b2dl_act y, b2dl_act mask,
+                           int accumulate, int f32, void* stream);
+/* gB[i][j] (+)= sum_{n,h,c} X[n,h,i,c] G[n,h,j,c]  (ops.py:166-170), fixed order. */
+B2DL_API int b2dl_matmul_w_grad(b2dl_act x, b2dl_act g, float* gb, int accumulate, int f32, void* stream);
+/* out[c] (+)= sum over n,h,w of g (standalone bias_add VJP, ops.py:172-175), fixed order. */
+B2DL_API int b2dl_channel_sum(b2dl_act g, float* out, int accumulate, int f32, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

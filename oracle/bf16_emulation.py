@@ -22,7 +22,9 @@ class RoundGrad(torch.autograd.Function):
         return g.to(torch.bfloat16).float()
 
 
-def run(graph, params, x, labels, cw, loss_name, emulate):
+def run(graph, params, x, labels, cw, loss_name, emulate, stored=None):
+    """stored: names of the tensors the GPU engine stores in bf16 (its fused-op outputs, e.g.
+    {o.out for o in engine.Plan(...).ops}); None = the conv-bias-add-relu chain rule below."""
     P = {k: torch.tensor(v, requires_grad=True) for k, v in params.items()}
     vals = {"x": torch.tensor(x), "labels": torch.tensor(labels.astype(np.int64)), "class_weights": torch.tensor(cw)}
     vals.update(P)
@@ -39,8 +41,14 @@ def run(graph, params, x, labels, cw, loss_name, emulate):
             out = ins[0] + ins[1].view(1, -1, 1, 1)
         elif k == "relu":
             out = torch.relu(ins[0])
-        elif k == "elementwise":
+        elif k == "elementwise" and a["fn"] == "add":
             out = ins[0] + ins[1]
+        elif k == "elementwise" and a["fn"] == "mul":
+            out = ins[0] * ins[1]
+        elif k == "elementwise":
+            out = ins[0] * float(a.get("alpha", 1.0))
+        elif k == "matmul":   # parameters are read from the fp32 master by the GPU's matmul
+            out = ins[0] @ ins[1]
         elif k == "concat":
             out = torch.cat(ins, 1)
         elif k == "avgpool":
@@ -62,9 +70,12 @@ def run(graph, params, x, labels, cw, loss_name, emulate):
         else:
             raise AssertionError(k)
         # fused-op boundary = where the GPU stores a bf16 tensor (and its bf16 gradient)
-        boundary = k in ("relu", "avgpool", "upsample", "upsample_bilinear") or (
-            k in ("bias_add", "elementwise", "batchnorm")
-            and not any(c.kind in ("elementwise", "relu") for c in cons[nd.name]) and nd.name != loss_name)
+        if stored is not None:
+            boundary = nd.name in stored
+        else:
+            boundary = k in ("relu", "avgpool", "upsample", "upsample_bilinear") or (
+                k in ("bias_add", "elementwise", "batchnorm")
+                and not any(c.kind in ("elementwise", "relu") for c in cons[nd.name]) and nd.name != loss_name)
         if emulate and boundary and k != "softmax_ce":
             out = RoundGrad.apply(out)
         vals[nd.name] = out
@@ -76,9 +87,9 @@ def run(graph, params, x, labels, cw, loss_name, emulate):
 
 
 
-def emulated_grads(graph, params, x, labels, cw, loss_name):
+def emulated_grads(graph, params, x, labels, cw, loss_name, stored=None):
     """(loss, grads) with bf16 storage rounding at the GPU engine's fused-op boundaries."""
-    return run(graph, params, x, labels, cw, loss_name, True)
+    return run(graph, params, x, labels, cw, loss_name, True, stored)
 
 
 def emulated_step(graph, params, x, labels, cw, loss_name, logits_name):

@@ -19,7 +19,7 @@ OUT = os.path.join(HERE, "libb2dl.so")
 BUILD = os.path.join(ROOT, "build", "b2dl")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["conv_tc.cu", "host.cu", "elementwise.cu", "loss.cu", "larc.cu", "fp32.cu", "norm.cu", "refconv.cu"]
+SOURCES = ["conv_tc.cu", "host.cu", "elementwise.cu", "loss.cu", "larc.cu", "fp32.cu", "norm.cu", "refconv.cu", "generic.cu"]
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

@@ -75,6 +75,10 @@ _SIGS = {
     "b2dl_conv2d_forward_typed": (_c_int, [_c_int, _vp, _vp, _vp] + [_c_int] * 9 + [_vp]),
     "b2dl_conv2d_backward_input_typed": (_c_int, [_c_int, _vp, _vp, _vp] + [_c_int] * 9 + [_vp]),
     "b2dl_conv2d_backward_weights_typed": (_c_int, [_c_int, _vp, _vp, _vp] + [_c_int] * 8 + [_vp]),
+    "b2dl_ewise": (_c_int, [Act, Act, Act, Act, _vp, ctypes.c_float, _c_int, _c_int, _c_int, _vp]),
+    "b2dl_matmul_w": (_c_int, [Act, _vp, _c_int, _c_int, Act, Act, _c_int, _c_int, _vp]),
+    "b2dl_matmul_w_grad": (_c_int, [Act, Act, _vp, _c_int, _c_int, _vp]),
+    "b2dl_channel_sum": (_c_int, [Act, _vp, _c_int, _c_int, _vp]),
     "b2dl_cin_pad": (_c_int, [_c_int]),
     "b2dl_conv_fprop": (_c_int, [ctypes.POINTER(ConvArgs), _vp]),
     "b2dl_wgrad_workspace_size": (_sz, [ctypes.POINTER(WgradArgs)]),

@@ -64,6 +64,8 @@ class Op:
     # up: "nearest" | "bilinear"; bn: epsilon
     mode: str = "nearest"
     eps: float = 1e-5
+    # scale
+    alpha: float = 1.0
 
 
 class Plan:
@@ -106,11 +108,11 @@ class Plan:
                     raise NotImplementedError("square kernels only")
                 chain = [nd]
                 nxt = cons[nd.name]
-                if len(nxt) != 1 or nxt[0].kind != "bias_add" or nxt[0].inputs[0] != nd.name:
-                    raise NotImplementedError(f"{nd.name}: conv must feed exactly one bias_add")
-                bias = nxt[0]
-                chain.append(bias)
-                cur = bias
+                cur, bname = nd, ""
+                if (len(nxt) == 1 and nxt[0].kind == "bias_add" and nxt[0].inputs[0] == nd.name
+                        and g.inputs.get(nxt[0].inputs[1]) == "param"):
+                    chain.append(nxt[0])
+                    cur, bname = nxt[0], nxt[0].inputs[1]
                 res = None
                 relu = False
                 nxt = cons[cur.name]
@@ -130,7 +132,7 @@ class Plan:
                     relu = True
                 used.update(c.name for c in chain)
                 op = Op("conv", cur.name, (nd.inputs[0],), tuple(c.name for c in chain), w=nd.inputs[1],
-                        b=bias.inputs[1], res=res, relu=relu, k=a["kh"], dil=a["dilation"], cin=a["cin"],
+                        b=bname, res=res, relu=relu, k=a["kh"], dil=a["dilation"], cin=a["cin"],
                         cout=a["cout"])
                 ops.append((idx[cur.name], op))
             elif nd.kind == "batchnorm":
@@ -172,6 +174,32 @@ class Plan:
                 ops.append((idx[nd.name], Op("concat", nd.name, nd.inputs, (nd.name,))))
             elif nd.kind == "elementwise" and nd.attrs["fn"] == "add":
                 ops.append((idx[nd.name], Op("add", nd.name, nd.inputs, (nd.name,))))
+            # standalone lowerings (csrc/generic.cu): the op kinds outside conv-bias-relu chains
+            elif nd.kind == "elementwise" and nd.attrs["fn"] == "mul":
+                ops.append((idx[nd.name], Op("mul", nd.name, nd.inputs, (nd.name,))))
+            elif nd.kind == "elementwise":   # scale
+                ops.append((idx[nd.name], Op("scale", nd.name, nd.inputs, (nd.name,),
+                                             alpha=float(nd.attrs.get("alpha", 1.0)))))
+            elif nd.kind == "bias_add":
+                if g.inputs.get(nd.inputs[1]) != "param":
+                    raise NotImplementedError(f"{nd.name}: bias_add needs a parameter bias")
+                chain = [nd]
+                cur = nd
+                nxt = cons[nd.name]
+                relu = False
+                if len(nxt) == 1 and nxt[0].kind == "relu" and nxt[0].name not in used:
+                    chain.append(nxt[0])
+                    cur = nxt[0]
+                    relu = True
+                used.update(c.name for c in chain)
+                ops.append((idx[cur.name], Op("bias", cur.name, (nd.inputs[0],), tuple(c.name for c in chain),
+                                              b=nd.inputs[1], relu=relu, cout=self.shapes[nd.name][1])))
+            elif nd.kind == "relu":
+                ops.append((idx[nd.name], Op("relu", nd.name, nd.inputs, (nd.name,))))
+            elif nd.kind == "matmul":
+                if g.inputs.get(nd.inputs[1]) != "param" or len(self.shapes[nd.inputs[0]]) != 4:
+                    raise NotImplementedError(f"{nd.name}: matmul of a 4-D activation by a parameter only")
+                ops.append((idx[nd.name], Op("matmul", nd.name, (nd.inputs[0],), (nd.name,), w=nd.inputs[1])))
             elif nd.kind == "softmax_ce":
                 if nd.inputs[1:] != ("labels", "class_weights"):
                     raise NotImplementedError("softmax_ce must read the graph's labels / class_weights")
@@ -197,7 +225,8 @@ class Plan:
             for s in op.ins:
                 prod = self.producer.get(s)
                 ok = (s not in owner and prod is not None
-                      and prod.kind in ("conv", "bn", "pool", "up", "concat", "add")
+                      and prod.kind in ("conv", "bn", "pool", "up", "concat", "add", "bias", "relu", "mul",
+                                        "scale", "matmul")
                       and s != self.logits_name and off % 8 == 0)
                 if ok:
                     owner[s] = (op.out, off)
@@ -243,6 +272,8 @@ class Plan:
         for op in self.ops:
             if op.kind in ("conv", "bn"):
                 srcs = [op.ins[0], op.w, op.b] + ([op.res] if op.res else [])
+            elif op.kind in ("bias", "matmul"):
+                srcs = [op.ins[0], op.b or op.w]
             else:
                 srcs = list(op.ins)
             if any(s in live for s in srcs):
@@ -282,8 +313,10 @@ class Plan:
                 prod = self.producer.get(t)
                 if prod is None or t == self.logits_name:
                     memo[t] = False
-                elif prod.kind in ("conv", "bn"):
+                elif prod.kind in ("conv", "bn", "bias"):
                     memo[t] = prod.relu
+                elif prod.kind == "relu":
+                    memo[t] = True
                 elif prod.kind == "pool" or (prod.kind == "up" and prod.mode == "nearest"):
                     memo[t] = maskable(prod.ins[0])
                 elif prod.kind == "concat":
@@ -372,6 +405,17 @@ class Plan:
             elif op.kind == "add":
                 prog.append({"op": op, "acc": [(s_, claim(s_, maskable(s_)), maskable(s_))
                                                for s_ in op.ins if s_ in self.live]})
+            elif op.kind == "mul":
+                prog.append({"op": op, "acc": [(i, s_, claim(s_, maskable(s_)), maskable(s_))
+                                               for i, s_ in enumerate(op.ins) if s_ in self.live]})
+            elif op.kind in ("scale", "relu", "matmul", "bias"):
+                x = op.ins[0]
+                st = {"op": op, "dx": None, "mask": False,
+                      "relu_pass": op.kind == "bias" and op.relu and unmasked_into(op.out)}
+                if x in self.live:
+                    st["mask"] = maskable(x)
+                    st["dx"] = claim(x, st["mask"])
+                prog.append(st)
         for r in list(pending):
             flush_pending(r)
         self.backward_program = prog
@@ -537,7 +581,8 @@ class Engine:
             base = buf.data_ptr()
             n_w = o.k * o.k * o.cin * o.cout
             self.segs[o.w] = (base, self.slot[o.w][0], n_w, wp, 0)
-            self.segs[o.b] = (base + bo, self.slot[o.b][0], o.cout, bp, 0)
+            if o.b:   # a conv without bias_add: its bias column sums are computed and dropped
+                self.segs[o.b] = (base + bo, self.slot[o.b][0], o.cout, bp, 0)
         self.set_buckets([list(param_order)])
         n, c, h, w = input_shape
         self.labels = torch.zeros(n * h * w, dtype=torch.uint8, device=self.device)
@@ -554,6 +599,10 @@ class Engine:
         self.side = (torch.cuda.Stream(device=self.device)
                      if os.environ.get("B2DL_CONCURRENT", "1") != "0" and self.device.type == "cuda" else None)
         self.conv_events = []
+        # bias-less convs: a zero bias operand and a scratch bias-gradient target
+        cmax = max([o.cout for o in self.convs] + [8])
+        self._zero_bias = torch.zeros(cmax, dtype=f32, device=self.device)
+        self._bias_sink = torch.zeros(cmax, dtype=f32, device=self.device)
         self.load_params(params)
 
     def _plan_up_dgrad(self):
@@ -578,6 +627,20 @@ class Engine:
             self.skip_up.add(up.out)
             self.wup[o.w] = torch.zeros((o.cin, kk * kk, nhwc.cin_pad(o.cout)), dtype=torch.bfloat16,
                                         device=self.device)
+
+    def bias_of(self, op):
+        """fp32 bias operand of a conv (zeros when the graph has no bias_add after it)."""
+        if not op.b:
+            return self._zero_bias[:op.cout]
+        off, _ = self.slot[op.b]
+        return self.flat_w[off:off + op.cout]
+
+    def bias_grad_of(self, op):
+        """Where a conv's bias gradient goes (a scratch sink when it has no bias parameter)."""
+        if not op.b:
+            return self._bias_sink[:op.cout]
+        off, _ = self.slot[op.b]
+        return self.flat_g[off:off + op.cout]
 
     def serialize(self, on: bool):
         """Run every launch on the current stream (no wgrad || dgrad or ASPP overlap): used to time
@@ -791,25 +854,22 @@ class Engine:
     def _fwd_op(self, op):
         p = self.plan
         if op.kind == "conv" and self.fp32:
-            b_off, _ = self.slot[op.b]
             ev = self._tic()
             nhwc.f32_conv(self.v(op.ins[0]), self.wslice(op.w), op.cout, op.k, op.k, op.dil, self.v(op.out),
-                          bias=self.flat_w[b_off:b_off + op.cout],
+                          bias=self.bias_of(op),
                           residual=self.v(op.res) if op.res else None, relu=op.relu)
             self._toc(ev, op)
         elif op.kind == "conv" and op.out in self.up_fprop:
             up = self.up_fprop[op.out]
-            b_off, _ = self.slot[op.b]
             n, _, h, w = self.plan.shapes[up.ins[0]]
             ev = self._tic()
             nhwc.upsampled_fprop(self.v(up.ins[0]), self.wupf[op.w], op.cin, op.cout, op.k, up.factor, self.v(op.out),
-                                 bias=self.flat_w[b_off:b_off + op.cout], relu=op.relu)
+                                 bias=self.bias_of(op), relu=op.relu)
             taps = nhwc.upsampled_fprop_taps(op.k, up.factor)
             self._toc(ev, op, flops=2 * taps * op.cin * op.cout * n * h * w)
             self.launches += up.factor * up.factor - 1
         elif op.kind == "conv":
             out = op.out
-            b_off, _ = self.slot[op.b]
             ev = self._tic()
             wsrc = dict(w_packed=self.wf[op.w]) if op.w in self.wf else dict(
                 w_packed=None, w_master=self.wmaster(op.w), w_mode=1)
@@ -819,7 +879,7 @@ class Engine:
                 xin, kw = View(self.xwin), 1
             nhwc.conv_fprop(xin, cout=op.cout, kh=op.k, kw=kw, dilation=op.dil, y=self.v(out),
                             **wsrc,
-                            bias=self.flat_w[b_off:b_off + op.cout],
+                            bias=self.bias_of(op),
                             residual=self.v(op.res) if op.res else None, relu=op.relu,
                             y_f32=(out == p.logits_name))
             self._toc(ev, op)
@@ -853,6 +913,16 @@ class Engine:
             self._add(self.v(a), self.v(op.out), accumulate=False)
             self._add(self.v(b), self.v(op.out), accumulate=True)
             self.launches += 1
+        elif op.kind == "bias":
+            nhwc.ewise(self.v(op.ins[0]), self.v(op.out), bias=self.wslice(op.b), relu=op.relu, f32=self.fp32)
+        elif op.kind == "relu":
+            nhwc.ewise(self.v(op.ins[0]), self.v(op.out), relu=True, f32=self.fp32)
+        elif op.kind == "mul":
+            nhwc.ewise(self.v(op.ins[0]), self.v(op.out), x1=self.v(op.ins[1]), f32=self.fp32)
+        elif op.kind == "scale":
+            nhwc.ewise(self.v(op.ins[0]), self.v(op.out), alpha=op.alpha, f32=self.fp32)
+        elif op.kind == "matmul":
+            nhwc.matmul_w(self.v(op.ins[0]), self.wslice(op.w), self.v(op.out), f32=self.fp32)
         elif op.kind == "ce":
             nhwc.wce(self.v(op.ins[0]), self.labels, self.class_weights, self.loss, self.counts,
                      self.gv(op.ins[0]), self.pred, self.ws, dlogits_f32=self.fp32, status=self.label_status)
@@ -878,6 +948,8 @@ class Engine:
         reference reduces a tensor only once it is final, trainer.py:222-241) without making the
         compute streams wait on each other."""
         for name in names:
+            if not name:
+                continue
             i = self.bucket_of[name]
             pending[i] -= 1
             if pending[i] != 0:
@@ -925,11 +997,9 @@ class Engine:
                 if st["relu_pass"]:
                     nhwc.f32_relu_mask(gy, self.v(op.out))
                     self.launches += 1
-                w_off, _ = self.slot[op.w]
-                b_off, _ = self.slot[op.b]
                 ev = self._tic()
                 nhwc.f32_conv_wgrad(self.v(op.ins[0]), gy, op.k, op.k, op.dil, self.wslice(op.w, self.flat_g),
-                                    self.ws, bias_grad=self.flat_g[b_off:b_off + op.cout])
+                                    self.ws, bias_grad=self.bias_grad_of(op))
                 self._toc(ev, op, "wgrad")
                 self.launches += 3
                 self._param_done((op.w, op.b), pending, on_bucket_ready)
@@ -971,11 +1041,10 @@ class Engine:
                     elif op.out in self.up_wgrad:
                         up = self.up_wgrad[op.out]
                         w_off, _ = self.slot[op.w]
-                        b_off, _ = self.slot[op.b]
                         nhwc.upsampled_wgrad(self.v(up.ins[0]), gy, op.k, up.factor, self.gsum[op.w],
                                              self.partials[op.w], self.up_layout[op.w],
                                              self.flat_g[w_off:w_off + op.k * op.k * op.cin * op.cout],
-                                             self.flat_g[b_off:b_off + op.cout])
+                                             self.bias_grad_of(op))
                         n, _, h, w = self.plan.shapes[up.ins[0]]
                         self.launches += 2
                         wflops = 2 * op.k * op.k * op.cin * op.cout * n * h * w
@@ -1050,6 +1119,8 @@ class Engine:
                     self._add(View(self.grad[root], coff + off, self.plan.chans(s)), self.gv(s), accumulate=acc,
                               mask=self.v(s) if m else None)
                     self.launches += 1
+            elif op.kind in ("bias", "relu", "mul", "scale", "matmul"):
+                self._bwd_generic(st, pending, on_bucket_ready)
             elif op.kind == "add":
                 src = st.get("passthrough", op.out)
                 for s, acc, m in st["acc"]:
@@ -1063,6 +1134,36 @@ class Engine:
             ev = torch.cuda.Event()
             ev.record(self._bstream)
             torch.cuda.current_stream().wait_event(ev)
+
+    def _bwd_generic(self, st, pending, on_bucket_ready):
+        """VJPs of the standalone lowerings (ops.py:166-177, 195-202) on the main stream."""
+        op, f32 = st["op"], self.fp32
+        gy = self.gv(op.out)
+        x = op.ins[0]
+        mask_x = self.v(x) if st.get("mask") else None
+        if op.kind == "bias":
+            if st["relu_pass"]:
+                (nhwc.f32_relu_mask if f32 else nhwc.relu_mask)(gy, self.v(op.out))
+            nhwc.channel_sum(gy, self.wslice(op.b, self.flat_g), f32=f32)
+            self._param_done((op.b,), pending, on_bucket_ready)
+            if st["dx"] is not None:
+                nhwc.ewise(gy, self.gv(x), mask=mask_x, accumulate=st["dx"], f32=f32)
+        elif op.kind == "relu" and st["dx"] is not None:
+            # (relu(x) > 0) == (x > 0): the output is the mask for both the relu VJP and x's own mask
+            nhwc.ewise(gy, self.gv(x), mask=self.v(op.out), accumulate=st["dx"], f32=f32)
+        elif op.kind == "scale" and st["dx"] is not None:
+            nhwc.ewise(gy, self.gv(x), alpha=op.alpha, mask=mask_x, accumulate=st["dx"], f32=f32)
+        elif op.kind == "mul":
+            for i, s_, acc, m in st["acc"]:
+                nhwc.ewise(gy, self.gv(s_), x1=self.v(op.ins[1 - i]), mask=self.v(s_) if m else None,
+                           accumulate=acc, f32=f32)
+        elif op.kind == "matmul":
+            nhwc.matmul_w_grad(self.v(x), gy, self.wslice(op.w, self.flat_g), f32=f32)
+            self._param_done((op.w,), pending, on_bucket_ready)
+            if st["dx"] is not None:
+                nhwc.matmul_w(gy, self.wslice(op.w), self.gv(x), trans=True, mask=mask_x, accumulate=st["dx"],
+                              f32=f32)
+        self.launches += 2
 
     def _add(self, x, y, accumulate=False, mask=None):
         (nhwc.f32_add if self.fp32 else nhwc.add)(x, y, accumulate=accumulate, mask=mask)

@@ -292,6 +292,32 @@ def add(x: View, y: View, accumulate=True, mask: View | None = None):
     check(LIB.b2dl_add(x.act(), y.act(), int(accumulate), _act(mask), _stream()), "add")
 
 
+def ewise(x0: View, y: View, x1: View | None = None, mask: View | None = None, bias=None, alpha=1.0,
+          relu=False, accumulate=False, f32=False):
+    """y (+)= mask? * relu?(alpha * x0 * x1? + bias?) (b2dl_ewise): mul / scale / bias_add / relu and VJPs."""
+    check(LIB.b2dl_ewise(x0.act(), _act(x1), _act(mask), y.act(), _ptr(bias), float(alpha), int(relu),
+                         int(accumulate), int(f32), _stream()), "ewise")
+
+
+def matmul_w(x: View, b: torch.Tensor, y: View, trans=False, mask: View | None = None, accumulate=False,
+             f32=False):
+    """Y = X @ B over the width axis (b2dl_matmul_w); trans: dX = dY @ B^T."""
+    ldb = x.shape[2] if trans else y.shape[2]
+    check(LIB.b2dl_matmul_w(x.act(), ctypes.c_void_p(b.data_ptr()), ldb, int(trans), y.act(), _act(mask),
+                            int(accumulate), int(f32), _stream()), "matmul_w")
+
+
+def matmul_w_grad(x: View, g: View, gb: torch.Tensor, accumulate=False, f32=False):
+    check(LIB.b2dl_matmul_w_grad(x.act(), g.act(), ctypes.c_void_p(gb.data_ptr()), int(accumulate), int(f32),
+                                 _stream()), "matmul_w_grad")
+
+
+def channel_sum(g: View, out: torch.Tensor, accumulate=False, f32=False):
+    """out[c] (+)= sum over pixels of g (b2dl_channel_sum; bf16 or fp32 storage)."""
+    check(LIB.b2dl_channel_sum(g.act(), ctypes.c_void_p(out.data_ptr()), int(accumulate), int(f32), _stream()),
+          "channel_sum")
+
+
 def dgrad_1x1_small(dy: View, w_hwio: torch.Tensor, dx: View, accumulate=False, mask: View | None = None):
     """Input gradient of a 1x1 conv with <= 16 output channels on CUDA cores (channel expansion)."""
     check(LIB.b2dl_dgrad_1x1_small(dy.act(), ctypes.c_void_p(w_hwio.data_ptr()), dx.act(), int(accumulate),

@@ -169,10 +169,17 @@ class DataParallelTrainer:
         replay it.  `timed` adds graph event nodes around every conv launch (roofline timing).
         `buffers` = 2 records a second graph over a second input buffer pair, so `stage` can
         copy the next batch from the host while the current step runs (`step_staged`).
-        Call after at least one eager step (workspaces sized)."""
-        if self.lag != 0:
-            raise NotImplementedError("graph capture supports lag 0")
+        Call after at least one eager step (workspaces sized).
+
+        Lag 1 (trainer.py:378-383): two graphs over the two gradient buffers, replayed
+        alternately -- graph k computes into one buffer while it applies the other's (already
+        reduced) gradients, so the LARC update never waits on this step's all-reduce; the
+        collective is joined at the end of its own graph (a captured graph cannot leave a stream
+        forked), which still overlaps it with the update.  With buffers = 2 the input buffer
+        alternates with the same period."""
         eng = self.eng
+        if self.lag == 1 and not self.have_prev:
+            raise RuntimeError("lag-1 capture needs one eager step first (a pending gradient)")
         self.static_xs = [torch.empty_like(x) for _ in range(buffers)]
         self.static_ls = [torch.empty_like(labels) for _ in range(buffers)]
         for sx, sl in zip(self.static_xs, self.static_ls):
@@ -180,20 +187,27 @@ class DataParallelTrainer:
             sl.copy_(labels)
         self.static_x, self.static_l = self.static_xs[0], self.static_ls[0]
         torch.cuda.synchronize()
+        self._wait_comm()
         self.graphs = []
-        for k in range(buffers):
+        ngraphs = 2 if self.lag == 1 else buffers
+        self._capturing = True
+        self._replays = 0
+        steps0 = self.steps_done
+        for k in range(ngraphs):
             graph = torch.cuda.CUDAGraph()
             launches0 = eng.launches
             t = timed and k == 0
             eng.conv_timing, eng.conv_events, eng.graph_events = t, [], t
             with torch.cuda.graph(graph):
-                self._eager_step(self.static_xs[k], self.static_ls[k])
+                self._eager_step(self.static_xs[k % buffers], self.static_ls[k % buffers])
             eng.graph_events = False
             if k == 0:
                 self.graph_conv_events = eng.conv_events if t else []
                 self.graph_launches = eng.launches - launches0
             eng.conv_timing, eng.conv_events = False, []
             self.graphs.append(graph)
+        self._capturing = False
+        self.steps_done = steps0   # capturing ran no step
         self.graph = self.graphs[0]
         self.copy_stream = torch.cuda.Stream(device=eng.device)
         self._ready = [torch.cuda.Event() for _ in range(buffers)]
@@ -207,16 +221,27 @@ class DataParallelTrainer:
         """One training step on device-resident inputs; returns the device loss (no host sync)."""
         g = getattr(self, "graph", None)
         if g is not None:
-            if x.data_ptr() != self.static_x.data_ptr():
-                self.static_x.copy_(x, non_blocking=True)
-            if labels.data_ptr() != self.static_l.data_ptr():
-                self.static_l.copy_(labels, non_blocking=True)
-            g.replay()
-            self._consumed[0].record()
-            self.eng.launches += self.graph_launches
-            self.steps_done += 1
+            k = self._next_graph()
+            sx, sl = self.static_xs[k % len(self.static_xs)], self.static_ls[k % len(self.static_ls)]
+            if x.data_ptr() != sx.data_ptr():
+                sx.copy_(x, non_blocking=True)
+            if labels.data_ptr() != sl.data_ptr():
+                sl.copy_(labels, non_blocking=True)
+            self._replay(k)
+            self._consumed[k % len(self._consumed)].record()
             return self.eng.loss
         return self._eager_step(x, labels)
+
+    def _next_graph(self) -> int:
+        return self._replays % len(self.graphs) if self.lag == 1 else 0
+
+    def _replay(self, k: int):
+        self.graphs[k].replay()
+        self._replays += 1
+        if self.lag == 1:   # mirror the captured buffer swap: flat_g = the buffer just computed
+            self.eng.flat_g, self.g_other = self.g_other, self.eng.flat_g
+        self.eng.launches += self.graph_launches
+        self.steps_done += 1
 
     def stage(self, hx: torch.Tensor, hl: torch.Tensor):
         """Asynchronously copy a host batch (pinned) into the next free input buffer on a copy
@@ -229,16 +254,17 @@ class DataParallelTrainer:
             self.static_ls[k].copy_(hl, non_blocking=True)
             self._ready[k].record()
         self._staged.append(k)
-        self._stage_k = (k + 1) % len(self.graphs)
+        self._stage_k = (k + 1) % len(self.static_xs)
 
     def step_staged(self) -> torch.Tensor:
         """Run the training step on the oldest staged batch; returns the device loss."""
         k = self._staged.pop(0)
         torch.cuda.current_stream().wait_event(self._ready[k])
-        self.graphs[k].replay()
+        g = self._next_graph() if self.lag == 1 else k
+        if self.lag == 1 and g % len(self.static_xs) != k:
+            raise RuntimeError("lag-1 staged replay out of phase with its input buffer")
+        self._replay(g)
         self._consumed[k].record()
-        self.eng.launches += self.graph_launches
-        self.steps_done += 1
         return self.eng.loss
 
     def graph_conv_totals(self, by_pass=False):
@@ -276,6 +302,8 @@ class DataParallelTrainer:
         if self.have_prev:
             self._apply(g_prev)
         self.have_prev = True
+        if getattr(self, "_capturing", False):
+            self._wait_comm()   # join this step's collectives inside its own graph
 
     def finish(self):
         """Lag 1: apply the last step's reduced gradients (trainer.py:403-405)."""
