@@ -145,7 +145,27 @@ typedef struct b2dl_conv_args {
    * upsampling by f, computed from the low-resolution input (no upsampled tensor). */
   int out_stride;
   int out_phase_h, out_phase_w;
+  /* Batch-norm statistics from the epilogue (training-mode BN after this conv):
+   * when non-NULL, the fprop writes rows of per-channel sums and sums of squares of its stored
+   * bf16 output over the valid pixels, bn_partial[(row * 2 + k) * cout + c] (k = 0 sum, 1 sum of
+   * squares): one row per CTA (its tiles, in order) when the launch has one N tile, else one row
+   * per 128-pixel M tile -- b2dl_conv_fprop_bn_rows rows; reduced by b2dl_bn_forward_partials.
+   * Needs the TMA epilogue (bf16 y, cout % 8 == 0, aligned views), no phase view, else
+   * B2DL_E_VALUE. */
+  float* bn_partial;
+  /* Batch-norm backward statistics from the epilogue: when this launch writes g = d loss / d y of a
+   * batch norm's output y = relu(scale z + shift) (no residual; bnb_stats = that BN's stats [4][c]:
+   * mean, rstd, scale, shift), pass the BN input z as `mask`: the relu mask is recomputed from z
+   * and the launch writes rows of (sum g, sum g * (z - mean) rstd) over the stored g,
+   * bnb_partial[(row * 2 + k) * cout + c], 4 * b2dl_conv_fprop_bn_rows rows (one per TMEM lane
+   * quarter) -- reduced by b2dl_bn_backward_partials.  Requires the TMA epilogue, no residual, no
+   * accumulate, 16-byte aligned stats. */
+  const float* bnb_stats;
+  float* bnb_partial;
 } b2dl_conv_args;
+
+/* Number of bn_partial rows the b2dl_conv_fprop launch for these arguments writes. */
+B2DL_API int b2dl_conv_fprop_bn_rows(const b2dl_conv_args* a);
 
 B2DL_API int b2dl_cin_pad(int cin);
 B2DL_API int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream);
@@ -303,11 +323,25 @@ B2DL_API size_t b2dl_bn_workspace_size(int c);
 B2DL_API int b2dl_bn_forward(b2dl_act x, const float* gamma, const float* beta, float eps, b2dl_act residual,
                              int relu, b2dl_act y, float* stats, void* workspace, size_t workspace_bytes, int f32,
                              void* stream);
+/* The same forward with the statistics already in `partials` ([tiles][2][c] fp32 sums / sums of
+ * squares written by the producing conv's epilogue, b2dl_conv_args.bn_partial): a fixed-order fp64
+ * reduction over the tiles, then the normalising pass -- no statistics pass over x. */
+B2DL_API int b2dl_bn_forward_partials(const float* partials, int tiles, b2dl_act x, const float* gamma,
+                                      const float* beta, float eps, b2dl_act residual, int relu, b2dl_act y,
+                                      float* stats, void* workspace, size_t workspace_bytes, int f32,
+                                      void* stream);
 /* dgamma (+)= sum gy*xhat, dbeta (+)= sum gy (param_accumulate), and when dx.ptr != NULL
  * dx (+)= gamma*rstd*(gy - dbeta/M - xhat*dgamma/M) (accumulate); gy already relu-masked. */
 B2DL_API int b2dl_bn_backward(b2dl_act x, b2dl_act gy, const float* gamma, const float* stats, float* dgamma,
                               float* dbeta, int param_accumulate, b2dl_act dx, int accumulate, void* workspace,
                               size_t workspace_bytes, int f32, void* stream);
+/* b2dl_bn_backward with the statistics already reduced per row by the consumer conv's dgrad
+ * epilogue (b2dl_conv_args.bnb_partial: [rows][2][c] sums of gy and gy * xhat): fixed-order fp64
+ * reduction, then the input-gradient pass only (gy already relu-masked). */
+B2DL_API int b2dl_bn_backward_partials(const float* partials, int rows, b2dl_act x, b2dl_act gy, const float* gamma,
+                                       const float* stats, float* dgamma, float* dbeta, int param_accumulate,
+                                       b2dl_act dx, int accumulate, void* workspace, size_t workspace_bytes, int f32,
+                                       void* stream);
 /* bilinear upsampling by integer factor f (half-pixel centres, align_corners=False) and its VJP
  * (separable and deterministic: a row pass into an fp32 workspace of dy.n*dy.h*(dy.w/f)*dy.c
  * floats, then a column pass; dx (+)= mask(>0) * ...). */

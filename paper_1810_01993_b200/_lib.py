@@ -38,7 +38,8 @@ class ConvArgs(ctypes.Structure):
                 ("relu", ctypes.c_int), ("accumulate", ctypes.c_int), ("mask", Act),
                 ("block_n", ctypes.c_int), ("w_master", ctypes.c_void_p), ("w_mode", ctypes.c_int),
                 ("window", ctypes.c_int), ("in_stride", ctypes.c_int), ("out_stride", ctypes.c_int),
-                ("out_phase_h", ctypes.c_int), ("out_phase_w", ctypes.c_int)]
+                ("out_phase_h", ctypes.c_int), ("out_phase_w", ctypes.c_int), ("bn_partial", ctypes.c_void_p),
+                ("bnb_stats", ctypes.c_void_p), ("bnb_partial", ctypes.c_void_p)]
 
 
 class WgradArgs(ctypes.Structure):
@@ -79,6 +80,11 @@ _SIGS = {
     "b2dl_matmul_w": (_c_int, [Act, _vp, _c_int, _c_int, Act, Act, _c_int, _c_int, _vp]),
     "b2dl_matmul_w_grad": (_c_int, [Act, Act, _vp, _c_int, _c_int, _vp]),
     "b2dl_channel_sum": (_c_int, [Act, _vp, _c_int, _c_int, _vp]),
+    "b2dl_conv_fprop_bn_rows": (_c_int, [ctypes.POINTER(ConvArgs)]),
+    "b2dl_bn_forward_partials": (_c_int, [_vp, _c_int, Act, _vp, _vp, ctypes.c_float, Act, _c_int, Act, _vp,
+                                          _vp, _sz, _c_int, _vp]),
+    "b2dl_bn_backward_partials": (_c_int, [_vp, _c_int, Act, Act, _vp, _vp, _vp, _vp, _c_int, Act, _c_int, _vp, _sz,
+                                           _c_int, _vp]),
     "b2dl_cin_pad": (_c_int, [_c_int]),
     "b2dl_conv_fprop": (_c_int, [ctypes.POINTER(ConvArgs), _vp]),
     "b2dl_wgrad_workspace_size": (_sz, [ctypes.POINTER(WgradArgs)]),

@@ -126,6 +126,13 @@ struct FpropParams {
   int bias_vec;        // bias 16-byte aligned
   int in_stride;       // input pixels per output pixel (strided reads of the input)
   int y_phase;         // output is a phase view of a larger tensor: TMA epilogue only
+  float* bn_part;      // batch-norm statistics of the stored output: [row][2][cout] fp32 sum, sum of squares
+  int bn_per_cta;      // 1: one row per CTA accumulated over its tiles (single N tile); 0: one row per M tile
+  // Batch-norm backward statistics (this launch writes g = d loss / d y of a BN's output y =
+  // relu(scale z + shift)): the mask operand is the BN input z, the relu mask is recomputed as
+  // scale z + shift > 0, and rows of (sum g, sum g * xhat) with xhat = (z - mean) rstd are written.
+  const float* bnb_stats;  // [4][cout]: mean, rstd, scale, shift
+  float* bnb_part;         // [row][2][cout]; rows = 4 per CTA (per-CTA mode) or 4 per M tile
 };
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
@@ -349,7 +356,9 @@ constexpr int EPI_CHUNK = 128 * 64;  // 128 pixels x 32 bf16 channels
 __host__ __device__ constexpr int epi_sub_bytes(int nops, int slots = 2) { return (slots * nops + 2) * EPI_CHUNK; }
 constexpr int EPI_MAX_SLOTS = 4;
 
-template <int BN, int CG, int EW>
+// ST: statistics epilogue variant (compile time, so the plain kernels carry none of its registers):
+// 0 none, 1 batch-norm forward statistics (bn_part), 2 batch-norm backward statistics (bnb_part)
+template <int BN, int CG, int EW, int ST = 0>
 __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const CUtensorMap* tmY, const CUtensorMap* tmR,
                                                    const CUtensorMap* tmM, uint32_t tmem_base, uint64_t* tfull,
                                                    uint64_t* tempty, uint64_t* inbar, uint8_t* epi, int warp, int rank,
@@ -438,6 +447,10 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
     }
   };
   for (int k = 0; k < S - 1; ++k) issue_next();
+  float bn_acc[NJ];
+  float bb_acc[NJ][2];
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) bn_acc[j] = bb_acc[j][0] = bb_acc[j][1] = 0.f;
   uint32_t phbits = 0;   // wait parity per slot
   int slot = 0, ob = 0, it = 0;
   for (int tile = unit0; tile < p.num_tiles; tile += units, ++it) {
@@ -465,6 +478,8 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
       }
       uint8_t* ochunk = obuf + ob * EPI_CHUNK;
       const float4* bias4 = p.bias ? reinterpret_cast<const float4*>(p.bias + c0) : nullptr;
+      float bstat[64];   // BN backward statistics of this row's 32 channels (only with bnb_stats)
+      const bool pix_ok = img < p.n && y + row / p.bw < p.h && x + (row % p.bw) < p.w;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {  // 8-column pieces
         const int poff = row * 64 + ((k ^ swz) << 4);
@@ -497,13 +512,30 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
 #pragma unroll
           for (int e = 0; e < 8; ++e) v[e] = fmaxf(v[e], 0.f);
         }
+        float zf[8];
         if (p.mask) {
           const uint4 u = *reinterpret_cast<const uint4*>(in + (o++) * EPI_CHUNK + poff);
           const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+          if constexpr (ST == 2) {   // mask operand = BN input z: relu mask = scale z + shift > 0
+            const float4* sc4 = reinterpret_cast<const float4*>(p.bnb_stats + 2 * p.cout + c0 + 8 * k);
+            const float4* sh4 = reinterpret_cast<const float4*>(p.bnb_stats + 3 * p.cout + c0 + 8 * k);
+            const float4 sa = __ldg(sc4), sb = __ldg(sc4 + 1), ha = __ldg(sh4), hb = __ldg(sh4 + 1);
+            const float scl[8] = {sa.x, sa.y, sa.z, sa.w, sb.x, sb.y, sb.z, sb.w};
+            const float shf[8] = {ha.x, ha.y, ha.z, ha.w, hb.x, hb.y, hb.z, hb.w};
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            if (!(bf16lo(w4[e]) > 0.f)) v[2 * e] = 0.f;
-            if (!(bf16hi(w4[e]) > 0.f)) v[2 * e + 1] = 0.f;
+            for (int e = 0; e < 4; ++e) {
+              zf[2 * e] = bf16lo(w4[e]);
+              zf[2 * e + 1] = bf16hi(w4[e]);
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (!(fmaf(zf[e], scl[e], shf[e]) > 0.f)) v[e] = 0.f;
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              if (!(bf16lo(w4[e]) > 0.f)) v[2 * e] = 0.f;
+              if (!(bf16hi(w4[e]) > 0.f)) v[2 * e + 1] = 0.f;
+            }
           }
         }
         if (p.accumulate) {
@@ -521,6 +553,45 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
         pk.z = pack_bf16x2(v[4], v[5]);
         pk.w = pack_bf16x2(v[6], v[7]);
         *reinterpret_cast<uint4*>(ochunk + poff) = pk;
+        if constexpr (ST == 2) {   // this pixel's (g, g * xhat) of the STORED g, channel-major pairs
+          const float4* mu4 = reinterpret_cast<const float4*>(p.bnb_stats + c0 + 8 * k);
+          const float4* rs4 = reinterpret_cast<const float4*>(p.bnb_stats + p.cout + c0 + 8 * k);
+          const float4 ma = __ldg(mu4), mb = __ldg(mu4 + 1), ra = __ldg(rs4), rb = __ldg(rs4 + 1);
+          const float mu[8] = {ma.x, ma.y, ma.z, ma.w, mb.x, mb.y, mb.z, mb.w};
+          const float rs[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
+          const uint32_t pw[4] = {pk.x, pk.y, pk.z, pk.w};
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float g = (e & 1) ? bf16hi(pw[e >> 1]) : bf16lo(pw[e >> 1]);
+            const bool ok = pix_ok;
+            bstat[2 * (8 * k + e)] = ok ? g : 0.f;
+            bstat[2 * (8 * k + e) + 1] = ok ? g * ((zf[e] - mu[e]) * rs[e]) : 0.f;
+          }
+        }
+      }
+      if constexpr (ST == 2) {
+        // reduce-scatter over the 32 lanes (rows): lane l ends with channel l's (sum g, sum g xhat)
+#pragma unroll
+        for (int half = 32, bit = 16; half >= 2; half >>= 1, bit >>= 1) {
+          const bool hi = (lane & bit) != 0;
+#pragma unroll
+          for (int e = 0; e < half; ++e) {
+            const float send = hi ? bstat[e] : bstat[e + half];
+            const float keep = hi ? bstat[e + half] : bstat[e];
+            bstat[e] = keep + __shfl_xor_sync(0xffffffffu, send, bit);
+          }
+        }
+        if (p.bn_per_cta) {
+          bb_acc[j][0] += bstat[0];
+          bb_acc[j][1] += bstat[1];
+        } else if (c0 + lane < p.cout) {
+          const int mt = (tile / p.num_n_tiles) * CG + rank;
+          if (mt < p.num_m_tiles) {
+            const long long row = static_cast<long long>(mt) * 4 + q;
+            p.bnb_part[(row * 2) * p.cout + c0 + lane] = bstat[0];
+            p.bnb_part[(row * 2 + 1) * p.cout + c0 + lane] = bstat[1];
+          }
+        }
       }
       fence_proxy_async();
       // the other output buffer (next chunk's) must be read out by its store before anyone
@@ -531,10 +602,77 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
         tma_store_4d(tmY, ochunk, c0, x, y, img);
         bulk_commit();
       }
+      if constexpr (ST == 1) {
+        // Batch-norm statistics of this chunk (training-mode BN after the conv):
+        // per-channel sum and sum of squares of the STORED bf16 values over the tile's valid
+        // pixels, read back from the packed output box while its TMA store drains.  Warp q takes
+        // the 8 channels of 16-byte piece q over rows lane + 32 m; a reduce-scatter butterfly
+        // leaves sum / sum-of-squares value (lane >> 1) in lane pair (2i, 2i+1) -- fixed order, no
+        // shared scratch, no extra barrier (the box is rewritten only after the next sub_sync).
+        float v16[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) v16[e] = 0.f;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const int r = lane + 32 * m;
+          const int ry = r / p.bw, rx = r - ry * p.bw;
+          if (img < p.n && y + ry < p.h && x + rx < p.w) {
+            const uint4 u = *reinterpret_cast<const uint4*>(ochunk + r * 64 + ((q ^ ((r >> 1) & 3)) << 4));
+            const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float a0 = bf16lo(w4[e]), a1 = bf16hi(w4[e]);
+              v16[2 * e] += a0;
+              v16[8 + 2 * e] = fmaf(a0, a0, v16[8 + 2 * e]);
+              v16[2 * e + 1] += a1;
+              v16[8 + 2 * e + 1] = fmaf(a1, a1, v16[8 + 2 * e + 1]);
+            }
+          }
+        }
+#pragma unroll
+        for (int half = 8, bit = 16; half >= 1; half >>= 1, bit >>= 1) {
+          const bool hi = (lane & bit) != 0;
+#pragma unroll
+          for (int e = 0; e < half; ++e) {
+            const float send = hi ? v16[e] : v16[e + half];
+            const float keep = hi ? v16[e + half] : v16[e];
+            v16[e] = keep + __shfl_xor_sync(0xffffffffu, send, bit);
+          }
+        }
+        v16[0] += __shfl_xor_sync(0xffffffffu, v16[0], 1);
+        if (p.bn_per_cta) {
+          bn_acc[j] += v16[0];   // same channels in every tile (one N tile): fold across tiles
+        } else {
+          const int mt = (tile / p.num_n_tiles) * CG + rank;
+          const int idx = lane >> 1, ch = c0 + 8 * q + (idx & 7);
+          if ((lane & 1) == 0 && mt < p.num_m_tiles && ch < p.cout)
+            p.bn_part[(static_cast<long long>(mt) * 2 + (idx >> 3)) * p.cout + ch] = v16[0];
+        }
+      }
       ob ^= 1;
       slot = slot + 1 == S ? 0 : slot + 1;
     }
     if (nv == 0) release(as);
+  }
+  if (ST == 2 && p.bn_per_cta) {   // this CTA's 4 rows (one per lane quarter), in tile order
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const int ch = (SUBS * j + sub) * 32 + lane;
+      if (SUBS * j + sub < NCH && ch < p.cout) {
+        const long long row = static_cast<long long>(blockIdx.x) * 4 + q;
+        p.bnb_part[(row * 2) * p.cout + ch] = bb_acc[j][0];
+        p.bnb_part[(row * 2 + 1) * p.cout + ch] = bb_acc[j][1];
+      }
+    }
+  }
+  if (ST == 1 && p.bn_per_cta) {   // this CTA's row: its tiles' statistics, in tile order
+    const int idx = lane >> 1;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const int ch = (SUBS * j + sub) * 32 + 8 * q + (idx & 7);
+      if ((lane & 1) == 0 && SUBS * j + sub < NCH && ch < p.cout)
+        p.bn_part[(static_cast<long long>(blockIdx.x) * 2 + (idx >> 3)) * p.cout + ch] = bn_acc[j];
+    }
   }
   if (leader) bulk_wait<0>();
   __syncwarp();
@@ -542,7 +680,7 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
 
 // Epilogue role of the fprop kernels (8 warps, two per TMEM lane quarter splitting the tile's
 // column chunks): TMEM -> registers -> bias / residual / relu / mask / accumulate -> global.
-template <int BN, int CG>
+template <int BN, int CG, int ST = 0>
 __device__ __forceinline__ void fprop_epilogue_role(const FpropParams& p, const CUtensorMap* tmY, const CUtensorMap* tmR,
                                                     const CUtensorMap* tmM, uint32_t tmem_base, uint64_t* tfull,
                                                     uint64_t* tempty, uint64_t* inbar, uint8_t* epi, int warp,
@@ -559,7 +697,7 @@ __device__ __forceinline__ void fprop_epilogue_role(const FpropParams& p, const 
     constexpr int NJ = (NCH + 1) / 2;
     if constexpr (CW == 32) {
       if (p.tma_epi) {
-        fprop_epilogue_tma<BN, CG, 8>(p, tmY, tmR, tmM, tmem_base, tfull, tempty, inbar, epi, warp, rank, unit0,
+        fprop_epilogue_tma<BN, CG, 8, ST>(p, tmY, tmR, tmM, tmem_base, tfull, tempty, inbar, epi, warp, rank, unit0,
                                       units);
         return;
       }
@@ -635,7 +773,7 @@ __device__ __forceinline__ void fprop_epilogue_role(const FpropParams& p, const 
 }
 
 // EW epilogue warps: 8, or 16 for the TMA epilogue (twice the warps to hide its latency chain)
-template <int BN, int KBLK, bool BMN, int CG, int EW>
+template <int BN, int KBLK, bool BMN, int CG, int EW, int ST = 0>
 __global__ void __launch_bounds__(64 + 32 * EW, 1)
     conv_fprop_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmR,
@@ -796,7 +934,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
       fprop_epilogue_tma<BN, CG, 16>(p, &tmY, &tmR, &tmM, tmem_base, tfull, tempty, inbar, epi, warp, rank, unit0,
                                      units);
     else
-      fprop_epilogue_role<BN, CG>(p, &tmY, &tmR, &tmM, tmem_base, tfull, tempty, inbar, epi, warp, rank, unit0,
+      fprop_epilogue_role<BN, CG, ST>(p, &tmY, &tmR, &tmM, tmem_base, tfull, tempty, inbar, epi, warp, rank, unit0,
                                   units);
   }
   tc_fence_before();
@@ -823,6 +961,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
 constexpr int HALO_BW = 8, HALO_BH = 16, HALO_BN = 64;
 constexpr int HALO_BBOX = HALO_BN * 64 * 2;  // one (tap row, K half) weight box: 64 co x 64 k
 
+template <int ST>
 __global__ void __launch_bounds__(FPROP_THREADS, 1)
     conv_halo_fprop_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                            const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmR,
@@ -927,7 +1066,7 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
       }
     }
   } else {
-    fprop_epilogue_role<HALO_BN, 1>(p, &tmY, &tmR, &tmM, tmem_base, tfull, tempty, inbar, epi, warp, 0, blockIdx.x,
+    fprop_epilogue_role<HALO_BN, 1, ST>(p, &tmY, &tmR, &tmM, tmem_base, tfull, tempty, inbar, epi, warp, 0, blockIdx.x,
                                     gridDim.x);
   }
   tc_fence_before();
@@ -1498,10 +1637,10 @@ static int epi_slots_for(int ew, int nops) {
   return c;
 }
 
-template <int BN, int KBLK, bool BMN, int CG, int EW = 8>
+template <int BN, int KBLK, bool BMN, int CG, int EW = 8, int ST = 0>
 static int launch_fprop(const FpropMaps& t, FpropParams p, cudaStream_t st) {
   using C = FpropCfg<BN, KBLK, BMN, CG>;
-  auto kern = conv_fprop_kernel<BN, KBLK, BMN, CG, EW>;
+  auto kern = conv_fprop_kernel<BN, KBLK, BMN, CG, EW, ST>;
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX) != cudaSuccess)
@@ -1516,6 +1655,7 @@ static int launch_fprop(const FpropMaps& t, FpropParams p, cudaStream_t st) {
   // and costs operand stages, so two it is.
   p.epi_slots = epi_slots_for(EW, p.epi_nops);
   p.epi_bytes = p.tma_epi ? (EW / 4) * epi_sub_bytes(p.epi_nops, p.epi_slots) : EPI_LEGACY_BYTES;
+  if (p.bn_part && !p.tma_epi) return B2DL_E_VALUE;
   // deepest operand pipeline that fits beside the epilogue buffers
   p.stages = 1;
   for (int s = FPROP_MAX_STAGES; s >= 1; --s) {
@@ -1528,6 +1668,7 @@ static int launch_fprop(const FpropMaps& t, FpropParams p, cudaStream_t st) {
   p.b_region = (p.stages * C::B_BYTES + 1023) / 1024 * 1024;
   const int smem = p.stages * C::A_BYTES + p.b_region + p.epi_bytes + SMEM_FIXED;
   const int grid = CG * std::min(p.num_tiles, num_sms() / CG);
+  p.bn_per_cta = p.num_n_tiles == 1;   // must match b2dl_conv_fprop_bn_rows
   const int rc = launch_tc(kern, grid, 64 + 32 * EW, smem, st, CG, t.a, t.b, t.y, t.r, t.m, p);
   return rc ? rc : check_launch();
 }
@@ -1634,6 +1775,7 @@ static int launch_halo_fprop(const b2dl_conv_args* a, const b2dl_act& xv, cudaSt
   p.tma_epi = 1;
   p.epi_nops = (p.res != nullptr) + (p.mask != nullptr) + (p.accumulate != 0);
   p.epi_slots = 2;
+  p.bn_part = a->bn_partial;
   p.epi_bytes = 2 * epi_sub_bytes(p.epi_nops, 2);
   const int a_stage = (HALO_BH + p.taps - 1) * HALO_BW * 128;
   const int b_region = p.taps * p.num_cblk * HALO_BBOX;
@@ -1654,15 +1796,16 @@ static int launch_halo_fprop(const b2dl_conv_args* a, const b2dl_act& xv, cudaSt
       (p.res && act_map(&t.r, a->residual, 32, bwx, bhx, CU_TENSOR_MAP_SWIZZLE_64B)) ||
       (p.mask && act_map(&t.m, a->mask, 32, bwx, bhx, CU_TENSOR_MAP_SWIZZLE_64B)))
     return B2DL_E_ALIGN;
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(conv_halo_fprop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX) !=
-        cudaSuccess)
+  auto kern = p.bn_part ? conv_halo_fprop_kernel<1> : conv_halo_fprop_kernel<0>;
+  static bool attr_set[2] = {false, false};
+  if (!attr_set[p.bn_part != nullptr]) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX) != cudaSuccess)
       return B2DL_E_CUDA;
-    attr_set = true;
+    attr_set[p.bn_part != nullptr] = true;
   }
   const int grid = std::min(p.num_tiles, num_sms());
-  const int rc = launch_tc(conv_halo_fprop_kernel, grid, FPROP_THREADS, smem, st, 1, t.a, t.b, t.y, t.r, t.m, p);
+  p.bn_per_cta = 1;
+  const int rc = launch_tc(kern, grid, FPROP_THREADS, smem, st, 1, t.a, t.b, t.y, t.r, t.m, p);
   return rc ? rc : check_launch();
 }
 
@@ -1696,32 +1839,9 @@ static int window_view(const b2dl_act& x, int window, int kw, int pad_left, int 
 }
 }  // namespace b2
 
-extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
-  if (!a || !a->x.ptr || !a->y.ptr || a->w_mode < 0 || a->w_mode > 2) return B2DL_E_VALUE;
-  b2dl_act y = a->y;
-  const int s_out = a->out_stride > 0 ? a->out_stride : 1;
-  if (s_out > 1) {   // phase view: the kernel tiles the (h/f, w/f) output; the store map is strided
-    if (s_out > 8 || a->out_phase_h < 0 || a->out_phase_h >= s_out || a->out_phase_w < 0 ||
-        a->out_phase_w >= s_out || y.h % s_out || y.w % s_out || a->residual.ptr || a->mask.ptr || a->accumulate ||
-        a->y_f32 || a->window || a->in_stride > 1)
-      return B2DL_E_VALUE;
-    y.h /= s_out;
-    y.w /= s_out;
-  }
-  b2dl_act x;
-  if (window_view(a->x, a->window, a->kw, a->pad_left, y.w, &x)) return B2DL_E_VALUE;
-  const int s_in = a->in_stride > 0 ? a->in_stride : 1;
-  if (s_in > 1 && (a->window || x.h != s_in * y.h || x.w != s_in * y.w || s_in > 8)) return B2DL_E_VALUE;
-  if (s_in > 1) {   // the kernel tiles the output; the input map is strided (checked above)
-    x.h = y.h;
-    x.w = y.w;
-  }
-  if (x.n != y.n || x.h != y.h || x.w != y.w || y.c != a->cout) return B2DL_E_VALUE;
-  if (a->kh < 1 || a->kw < 1 || a->dilation < 1 || a->cout < 1 || x.c < 1) return B2DL_E_VALUE;
-  if (!view_aligned(x, 2)) return B2DL_E_ALIGN;
-  if (halo_fprop_ok(a, x)) return launch_halo_fprop(a, x, as_stream(stream));
-  const int kblk = x.c <= 16 ? 16 : 64;
-  const int cin_pad = b2dl_cin_pad(x.c);
+namespace b2 {
+// N tile width and CTA pairing of a b2dl_conv_fprop launch (shared with b2dl_conv_fprop_bn_rows)
+static void fprop_choose(const b2dl_conv_args* a, const b2dl_act& x, int kblk, int* bn_out, int* cg_out) {
   int bn = a->block_n ? a->block_n : pick_bn(a->cout);
   // 256- and 128-wide N tiles run as CTA pairs (256 pixels x BN per pair)
   auto pair_ok = [&](int b) {
@@ -1755,6 +1875,69 @@ extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
       }
     }
   }
+
+  *bn_out = bn;
+  *cg_out = cg;
+}
+}  // namespace b2
+
+extern "C" int b2dl_conv_fprop_bn_rows(const b2dl_conv_args* a) {
+  // mirrors the tiling b2dl_conv_fprop picks (halo stem: 8 x 16 pixels; else a 128-pixel box):
+  // one statistics row per CTA when the launch has a single N tile, else one per M tile
+  if (!a) return -B2DL_E_VALUE;
+  b2dl_act y = a->y;
+  const int s_out = a->out_stride > 0 ? a->out_stride : 1;
+  if (s_out > 1) {
+    y.h /= s_out;
+    y.w /= s_out;
+  }
+  b2dl_act x;
+  if (window_view(a->x, a->window, a->kw, a->pad_left, y.w, &x)) return -B2DL_E_VALUE;
+  const int s_in = a->in_stride > 0 ? a->in_stride : 1;
+  if (s_in > 1) {
+    x.h = y.h;
+    x.w = y.w;
+  }
+  if (halo_fprop_ok(a, x)) return std::min(y.n * cdiv(y.w, HALO_BW) * cdiv(y.h, HALO_BH), num_sms());
+  int bw = pow2_divisor(x.w, 128);
+  if (bw < 8 && x.w >= 8) bw = std::min(128, 1 << (31 - __builtin_clz(x.w)));
+  while (bw * s_in > 256) bw >>= 1;
+  const int m_tiles = x.n * cdiv(x.w, bw) * cdiv(x.h, BM / bw);
+  int bn, cg;
+  fprop_choose(a, x, x.c <= 16 ? 16 : 64, &bn, &cg);
+  const int n_tiles = cdiv(a->cout, bn);
+  if (n_tiles > 1) return m_tiles;
+  return cg * std::min(cdiv(m_tiles, cg) * n_tiles, num_sms() / cg);
+}
+
+extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
+  if (!a || !a->x.ptr || !a->y.ptr || a->w_mode < 0 || a->w_mode > 2) return B2DL_E_VALUE;
+  b2dl_act y = a->y;
+  const int s_out = a->out_stride > 0 ? a->out_stride : 1;
+  if (s_out > 1) {   // phase view: the kernel tiles the (h/f, w/f) output; the store map is strided
+    if (s_out > 8 || a->out_phase_h < 0 || a->out_phase_h >= s_out || a->out_phase_w < 0 ||
+        a->out_phase_w >= s_out || y.h % s_out || y.w % s_out || a->residual.ptr || a->mask.ptr || a->accumulate ||
+        a->y_f32 || a->window || a->in_stride > 1)
+      return B2DL_E_VALUE;
+    y.h /= s_out;
+    y.w /= s_out;
+  }
+  b2dl_act x;
+  if (window_view(a->x, a->window, a->kw, a->pad_left, y.w, &x)) return B2DL_E_VALUE;
+  const int s_in = a->in_stride > 0 ? a->in_stride : 1;
+  if (s_in > 1 && (a->window || x.h != s_in * y.h || x.w != s_in * y.w || s_in > 8)) return B2DL_E_VALUE;
+  if (s_in > 1) {   // the kernel tiles the output; the input map is strided (checked above)
+    x.h = y.h;
+    x.w = y.w;
+  }
+  if (x.n != y.n || x.h != y.h || x.w != y.w || y.c != a->cout) return B2DL_E_VALUE;
+  if (a->kh < 1 || a->kw < 1 || a->dilation < 1 || a->cout < 1 || x.c < 1) return B2DL_E_VALUE;
+  if (!view_aligned(x, 2)) return B2DL_E_ALIGN;
+  if (halo_fprop_ok(a, x)) return launch_halo_fprop(a, x, as_stream(stream));
+  const int kblk = x.c <= 16 ? 16 : 64;
+  const int cin_pad = b2dl_cin_pad(x.c);
+  int bn, cg;
+  fprop_choose(a, x, kblk, &bn, &cg);
 
   FpropParams p{};
   p.n = x.n;
@@ -1836,6 +2019,14 @@ extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
               ((p.res != nullptr) + (p.mask != nullptr) + (p.accumulate != 0)) <= 2;
   p.y_phase = s_out > 1;
   if (p.y_phase && !p.tma_epi) return B2DL_E_VALUE;
+  p.bn_part = a->bn_partial;
+  if (p.bn_part && (p.y_phase || !p.tma_epi)) return B2DL_E_VALUE;
+  p.bnb_stats = a->bnb_stats;
+  p.bnb_part = a->bnb_partial;
+  if ((p.bnb_stats != nullptr) != (p.bnb_part != nullptr)) return B2DL_E_VALUE;
+  if (p.bnb_stats && (!p.tma_epi || p.y_phase || !p.mask || p.res || p.accumulate ||
+                      (reinterpret_cast<uintptr_t>(p.bnb_stats) & 15) || (a->cout & 7)))
+    return B2DL_E_VALUE;
   if (p.tma_epi) {
     const int bwx = p.bw, bhx = p.bh;  // epilogue boxes: 32 channels x the whole tile
     if ((s_out > 1 ? act_map_phase(&t.y, a->y, s_out, a->out_phase_h, a->out_phase_w, 32, bwx, bhx,
@@ -1843,7 +2034,7 @@ extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
                    : act_map(&t.y, y, 32, bwx, bhx, CU_TENSOR_MAP_SWIZZLE_64B)) ||
         (p.res && act_map(&t.r, a->residual, 32, bwx, bhx, CU_TENSOR_MAP_SWIZZLE_64B)) ||
         (p.mask && act_map(&t.m, a->mask, 32, bwx, bhx, CU_TENSOR_MAP_SWIZZLE_64B))) {
-      if (p.y_phase) return B2DL_E_ALIGN;
+      if (p.y_phase || p.bn_part) return B2DL_E_ALIGN;
       p.tma_epi = 0;
     }
   }
@@ -1855,6 +2046,27 @@ extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
   const int nops = (p.res != nullptr) + (p.mask != nullptr) + (p.accumulate != 0);
   // 16 epilogue warps where the epilogue dominates (short K); long-K launches keep the deeper
   // operand ring that 8 warps' smaller buffers leave room for
+  if (p.bn_part || p.bnb_stats) {   // statistics epilogues: 8 epilogue warps, 64-wide K blocks
+    const int stv = p.bn_part ? 1 : 2;
+#define B2_FPROP_ST(BNV, CGV, STV)                                                                    \
+  if (bn == BNV && cg == CGV && kblk == 64 && stv == STV)                                             \
+    return mode == 1 ? launch_fprop<BNV, 64, true, CGV, 8, STV>(t, p, st)                             \
+                     : launch_fprop<BNV, 64, false, CGV, 8, STV>(t, p, st);
+    B2_FPROP_ST(256, 2, 1)
+    B2_FPROP_ST(128, 2, 1)
+    B2_FPROP_ST(256, 1, 1)
+    B2_FPROP_ST(128, 1, 1)
+    B2_FPROP_ST(64, 1, 1)
+    B2_FPROP_ST(32, 1, 1)
+    B2_FPROP_ST(256, 2, 2)
+    B2_FPROP_ST(128, 2, 2)
+    B2_FPROP_ST(256, 1, 2)
+    B2_FPROP_ST(128, 1, 2)
+    B2_FPROP_ST(64, 1, 2)
+    B2_FPROP_ST(32, 1, 2)
+#undef B2_FPROP_ST
+    return B2DL_E_VALUE;
+  }
   if (p.tma_epi && nops <= ew16_max_nops() && kblk == 64 && p.num_kb <= 16 && ew16_enabled()) {
     if (cg == 2 && bn == 256)
       return mode == 1 ? launch_fprop<256, 64, true, 2, 16>(t, p, st) : launch_fprop<256, 64, false, 2, 16>(t, p, st);

@@ -135,8 +135,9 @@ __global__ void __launch_bounds__(BN_THREADS) k_bn_reduce(const T* __restrict__ 
 
 // Sum of the per-block partials of channel ch in a fixed order: FIN_ROWS threads per channel
 // each take every FIN_ROWS-th block, then a fixed-shape tree over the rows (deterministic).
-constexpr int FIN_CH = 32, FIN_ROWS = 8;
-__device__ __forceinline__ void fin_sums(const double* __restrict__ part, int blocks, int c, double* red, double& s,
+constexpr int FIN_CH = 32, FIN_ROWS = 16;
+template <typename P>
+__device__ __forceinline__ void fin_sums(const P* __restrict__ part, int blocks, int c, double* red, double& s,
                                          double& q) {
   const int lc = threadIdx.x % FIN_CH, r = threadIdx.x / FIN_CH;
   const int ch = blockIdx.x * FIN_CH + lc;
@@ -157,8 +158,39 @@ __device__ __forceinline__ void fin_sums(const double* __restrict__ part, int bl
     }
 }
 
+// Fold conv-epilogue statistics partials [tiles][2][c] (fp32) into [G][2][c] fp64 rows: block
+// (channel group, g) sums its contiguous tile range with FIN_ROWS strided threads per channel and
+// a fixed-order fold -- deterministic, and wide enough for 10^4+ tiles.
+__global__ void __launch_bounds__(FIN_CH * FIN_ROWS) k_bn_fold_partials(const float* __restrict__ part, int tiles,
+                                                                        int c, double* __restrict__ fold) {
+  __shared__ double red[FIN_ROWS * 2 * FIN_CH];
+  const int lc = threadIdx.x % FIN_CH, r = threadIdx.x / FIN_CH;
+  const int ch = blockIdx.x * FIN_CH + lc, g = blockIdx.y, G = gridDim.y;
+  const long long per = (tiles + G - 1) / G;
+  const long long lo = g * per, hi = min(static_cast<long long>(tiles), lo + per);
+  double a = 0.0, b = 0.0;
+  if (ch < c)
+    for (long long k = lo + r; k < hi; k += FIN_ROWS) {
+      a += part[(k * 2) * c + ch];
+      b += part[(k * 2 + 1) * c + ch];
+    }
+  red[(r * 2) * FIN_CH + lc] = a;
+  red[(r * 2 + 1) * FIN_CH + lc] = b;
+  __syncthreads();
+  if (r == 0 && ch < c) {
+    double s = 0.0, q = 0.0;
+    for (int k = 0; k < FIN_ROWS; ++k) {
+      s += red[(k * 2) * FIN_CH + lc];
+      q += red[(k * 2 + 1) * FIN_CH + lc];
+    }
+    fold[(static_cast<long long>(g) * 2) * c + ch] = s;
+    fold[(static_cast<long long>(g) * 2 + 1) * c + ch] = q;
+  }
+}
+
 // stats [4][c]: mean, rstd, scale = gamma*rstd, shift = beta - mean*scale
-__global__ void __launch_bounds__(FIN_CH * FIN_ROWS) k_bn_finalize(const double* __restrict__ part, int blocks, int c,
+template <typename P>
+__global__ void __launch_bounds__(FIN_CH * FIN_ROWS) k_bn_finalize(const P* __restrict__ part, int blocks, int c,
                                                                    double m, float eps, const float* __restrict__ gamma,
                                                                    const float* __restrict__ beta,
                                                                    float* __restrict__ stats) {
@@ -179,8 +211,9 @@ __global__ void __launch_bounds__(FIN_CH * FIN_ROWS) k_bn_finalize(const double*
 
 // dbeta = sum gy, dgamma = sum gy*xhat.  dx = gamma*rstd*(gy - dbeta/M - xhat*dgamma/M) is
 // folded to dx = A*gy + K1*x + K0 per channel: coef [3][c] = A, K1, K0.
+template <typename P>
 __global__ void __launch_bounds__(FIN_CH * FIN_ROWS) k_bn_bwd_finalize(
-    const double* __restrict__ part, int blocks, int c, double m, const float* __restrict__ gamma,
+    const P* __restrict__ part, int blocks, int c, double m, const float* __restrict__ gamma,
     const float* __restrict__ stats, float* __restrict__ dgamma, float* __restrict__ dbeta, int acc,
     float* __restrict__ coef) {
   __shared__ double red[FIN_ROWS * 2 * FIN_CH];
@@ -498,9 +531,45 @@ extern "C" int b2dl_bn_forward(b2dl_act x, const float* gamma, const float* beta
   });
   int rc = check_launch();
   if (rc) return rc;
-  k_bn_finalize<<<cdiv(c, FIN_CH), FIN_CH * FIN_ROWS, 0, st>>>(part, blocks, c, static_cast<double>(npix), eps, gamma,
-                                                                beta, stats);
+  k_bn_finalize<double><<<cdiv(c, FIN_CH), FIN_CH * FIN_ROWS, 0, st>>>(part, blocks, c, static_cast<double>(npix),
+                                                                        eps, gamma, beta, stats);
   if ((rc = check_launch())) return rc;
+  B2_TV(f32, vec, {
+    k_bn_apply<T, V><<<stream_blocks(npix, c / V), BN_THREADS, 0, st>>>(
+        reinterpret_cast<const T*>(x.ptr), x.c_stride, stats, reinterpret_cast<const T*>(residual.ptr),
+        residual.c_stride, relu, reinterpret_cast<T*>(y.ptr), y.c_stride, npix, c);
+  });
+  return check_launch();
+}
+
+extern "C" int b2dl_bn_forward_partials(const float* partials, int tiles, b2dl_act x, const float* gamma,
+                                        const float* beta, float eps, b2dl_act residual, int relu, b2dl_act y,
+                                        float* stats, void* workspace, size_t workspace_bytes, int f32,
+                                        void* stream) {
+  if (!partials || tiles < 1 || !x.ptr || !y.ptr || !gamma || !beta || !stats || x.n != y.n || x.h != y.h ||
+      x.w != y.w || x.c != y.c)
+    return B2DL_E_VALUE;
+  if (!workspace || workspace_bytes < b2dl_bn_workspace_size(x.c)) return B2DL_E_VALUE;
+  const int c = x.c;
+  const long long npix = static_cast<long long>(x.n) * x.h * x.w;
+  const int vw = f32 ? 4 : 8;
+  const bool vec = vec_act(x, vw) && vec_act(y, vw) && vec_act(residual, vw);
+  cudaStream_t st = as_stream(stream);
+  int rc;
+  if (tiles <= 4 * FIN_ROWS) {   // per-CTA rows (or few tiles): one fixed-order pass
+    k_bn_finalize<float><<<cdiv(c, FIN_CH), FIN_CH * FIN_ROWS, 0, st>>>(partials, tiles, c,
+                                                                         static_cast<double>(npix), eps, gamma, beta,
+                                                                         stats);
+  } else {   // per-tile rows: fold contiguous tile ranges first (G rows of fp64), then finalize
+    const int G = std::min(bn_blocks(), cdiv(tiles, 4 * FIN_ROWS));
+    double* fold = reinterpret_cast<double*>(workspace);
+    k_bn_fold_partials<<<dim3(cdiv(c, FIN_CH), G), FIN_CH * FIN_ROWS, 0, st>>>(partials, tiles, c, fold);
+    if ((rc = check_launch())) return rc;
+    k_bn_finalize<double><<<cdiv(c, FIN_CH), FIN_CH * FIN_ROWS, 0, st>>>(fold, G, c, static_cast<double>(npix), eps,
+                                                                          gamma, beta, stats);
+  }
+  rc = check_launch();
+  if (rc) return rc;
   B2_TV(f32, vec, {
     k_bn_apply<T, V><<<stream_blocks(npix, c / V), BN_THREADS, 0, st>>>(
         reinterpret_cast<const T*>(x.ptr), x.c_stride, stats, reinterpret_cast<const T*>(residual.ptr),
@@ -535,7 +604,7 @@ extern "C" int b2dl_bn_backward(b2dl_act x, b2dl_act gy, const float* gamma, con
   });
   int rc = check_launch();
   if (rc) return rc;
-  k_bn_bwd_finalize<<<cdiv(c, FIN_CH), FIN_CH * FIN_ROWS, 0, st>>>(part, blocks, c, static_cast<double>(npix), gamma,
+  k_bn_bwd_finalize<double><<<cdiv(c, FIN_CH), FIN_CH * FIN_ROWS, 0, st>>>(part, blocks, c, static_cast<double>(npix), gamma,
                                                                     stats, dgamma,
                                                    dbeta, param_accumulate, coef);
   if ((rc = check_launch()) || !dx.ptr) return rc;
@@ -584,6 +653,44 @@ extern "C" int b2dl_bilinear_bwd(b2dl_act dy, b2dl_act dx, int f, int accumulate
     k_bilinear_bwd_cols<T, V><<<dim3(dx.h, dx.n), 256, 0, st>>>(
         R, reinterpret_cast<T*>(dx.ptr), dx.c_stride, reinterpret_cast<const T*>(mask.ptr), mask.c_stride, dx.h, dx.w,
         dx.c, f, accumulate);
+  });
+  return check_launch();
+}
+
+extern "C" int b2dl_bn_backward_partials(const float* partials, int rows, b2dl_act x, b2dl_act gy,
+                                         const float* gamma, const float* stats, float* dgamma, float* dbeta,
+                                         int param_accumulate, b2dl_act dx, int accumulate, void* workspace,
+                                         size_t workspace_bytes, int f32, void* stream) {
+  if (!partials || rows < 1 || !x.ptr || !gy.ptr || !gamma || !stats || x.n != gy.n || x.h != gy.h ||
+      x.w != gy.w || x.c != gy.c)
+    return B2DL_E_VALUE;
+  if (dx.ptr && (dx.n != x.n || dx.h != x.h || dx.w != x.w || dx.c != x.c)) return B2DL_E_VALUE;
+  if (!workspace || workspace_bytes < b2dl_bn_workspace_size(x.c)) return B2DL_E_VALUE;
+  const int c = x.c;
+  const long long npix = static_cast<long long>(x.n) * x.h * x.w;
+  cudaStream_t st = as_stream(stream);
+  float* coef = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) +
+                                         align_up(static_cast<size_t>(bn_blocks()) * 2 * c * sizeof(double), 256));
+  int rc;
+  if (rows <= 4 * FIN_ROWS) {
+    k_bn_bwd_finalize<float><<<cdiv(c, FIN_CH), FIN_CH * FIN_ROWS, 0, st>>>(
+        partials, rows, c, static_cast<double>(npix), gamma, stats, dgamma, dbeta, param_accumulate, coef);
+  } else {
+    const int G = std::min(bn_blocks(), cdiv(rows, 4 * FIN_ROWS));
+    double* fold = reinterpret_cast<double*>(workspace);
+    k_bn_fold_partials<<<dim3(cdiv(c, FIN_CH), G), FIN_CH * FIN_ROWS, 0, st>>>(partials, rows, c, fold);
+    if ((rc = check_launch())) return rc;
+    k_bn_bwd_finalize<double><<<cdiv(c, FIN_CH), FIN_CH * FIN_ROWS, 0, st>>>(
+        fold, G, c, static_cast<double>(npix), gamma, stats, dgamma, dbeta, param_accumulate, coef);
+  }
+  if ((rc = check_launch())) return rc;
+  if (!dx.ptr) return B2DL_OK;
+  const int vw = f32 ? 4 : 8;
+  const bool vec = vec_act(x, vw) && vec_act(gy, vw) && vec_act(dx, vw);
+  B2_TV(f32, vec, {
+    k_bn_bwd_apply<T, V><<<stream_blocks(npix, c / V), BN_THREADS, 0, st>>>(
+        reinterpret_cast<const T*>(x.ptr), x.c_stride, reinterpret_cast<const T*>(gy.ptr), gy.c_stride, coef,
+        reinterpret_cast<T*>(dx.ptr), dx.c_stride, accumulate, npix, c);
   });
   return check_launch();
 }

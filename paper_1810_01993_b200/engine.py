@@ -542,6 +542,43 @@ class Engine:
                     self.gsum[o.w] = torch.empty(n_ * h_ * w_ * o.k * o.k * o.cout, dtype=torch.bfloat16,
                                                  device=self.device)
         self.dead_up = {self.up_fprop[o].out for o in self.up_wgrad if o in self.up_dgrad}
+        # Batch norm after a conv: the conv's TMA epilogue emits per-tile channel sums and sums of
+        # squares of its stored output (b2dl_conv_args.bn_partial), so the BN forward is one
+        # normalising pass with no statistics pass over the conv output (B2DL_BN_FUSED=0: off)
+        self.bn_fused, self.bn_parts = {}, {}
+        if not self.fp32 and os.environ.get("B2DL_BN_FUSED", "1") != "0":
+            for o in p.ops:
+                if o.kind != "bn":
+                    continue
+                c = p.producer.get(o.ins[0])
+                if (c is not None and c.kind == "conv" and c.cout % 8 == 0 and c.cout > 16 and not c.relu
+                        and not c.res and (c.cin > 16 or c is self.win)
+                        and c.out not in self.up_fprop and c.out != p.logits_name and p.view_spec(c.out)[1] % 8 == 0
+                        and (c.k > 1 or c.cout >= 8)):
+                    self.bn_fused[c.out] = o
+        # ... and its backward statistics (sum gy, sum gy * xhat) from the epilogue of the one dgrad
+        # that writes d loss / d y (a single-consumer conv C; the relu mask is recomputed there from
+        # the BN input), so the BN VJP is one input-gradient pass (b2dl_conv_args.bnb_partial)
+        self.bnb_of, self.bnb_parts = {}, {}
+        if self.bn_fused:
+            users = {}
+            for o in p.ops:
+                for t in list(o.ins) + ([o.res] if o.kind in ("conv", "bn") and o.res else []):
+                    users.setdefault(t, []).append(o)
+            steps = {st["op"].out: st for st in p.backward_program if st["op"].kind == "conv"}
+            for o in p.ops:
+                if o.kind != "bn" or not o.relu or o.res or o.out not in p.live:
+                    continue
+                u = users.get(o.out, [])
+                c = u[0] if len(u) == 1 else None
+                st = steps.get(c.out) if c is not None else None
+                if (c is not None and c.kind == "conv" and c.ins[0] == o.out and c.res != o.out and st is not None
+                        and st["dx"] is False and st["mask_dx"] and not st["dx_res"] and o.cout % 8 == 0
+                        and o.cout > 16
+                        and p.view_spec(o.out) == (o.out, 0, o.cout) and p.gview_spec(o.out)[0] == o.out
+                        and c.cout > 16 and c is not self.win and c.w not in self.heads
+                        and c.out not in self.up_dgrad):
+                    self.bnb_of[c.out] = o
         hparts = nhwc.head_backward_parts()
         for o in self.convs:
             if self.fp32:   # fp32 wgrad reduces its split-K partials itself, into flat_g
@@ -877,12 +914,22 @@ class Engine:
             if op is self.win:
                 wsrc = dict(w_packed=self.wwin, window=op.k)
                 xin, kw = View(self.xwin), 1
-            nhwc.conv_fprop(xin, cout=op.cout, kh=op.k, kw=kw, dilation=op.dil, y=self.v(out),
-                            **wsrc,
-                            bias=self.bias_of(op),
-                            residual=self.v(op.res) if op.res else None, relu=op.relu,
-                            y_f32=(out == p.logits_name))
+            kwargs = dict(cout=op.cout, kh=op.k, kw=kw, dilation=op.dil, y=self.v(out), **wsrc, bias=self.bias_of(op),
+                          residual=self.v(op.res) if op.res else None, relu=op.relu, y_f32=(out == p.logits_name))
+            if out in self.bn_fused:
+                if out not in self.bn_parts:   # sized on the first (eager) step, before any capture
+                    tiles = nhwc.conv_fprop(xin, bn_rows_only=True, **kwargs)   # statistics rows
+                    self.bn_parts[out] = (torch.empty(tiles * 2 * op.cout, dtype=torch.float32, device=self.device),
+                                          tiles)
+                kwargs["bn_partial"] = self.bn_parts[out][0]
+            nhwc.conv_fprop(xin, **kwargs)
             self._toc(ev, op)
+        elif op.kind == "bn" and op.ins[0] in self.bn_parts:
+            part, tiles = self.bn_parts[op.ins[0]]
+            nhwc.bn_forward_partials(part, tiles, self.v(op.ins[0]), self.wslice(op.w), self.wslice(op.b), op.eps,
+                                     self.v(op.out), self.bn_stats[op.out], self.ws,
+                                     residual=self.v(op.res) if op.res else None, relu=op.relu)
+            self.launches += 2
         elif op.kind == "bn":
             nhwc.bn_forward(self.v(op.ins[0]), self.wslice(op.w), self.wslice(op.b), op.eps, self.v(op.out),
                             self.bn_stats[op.out], self.ws, residual=self.v(op.res) if op.res else None,
@@ -1075,9 +1122,18 @@ class Engine:
                     ev = self._tic()
                     wsrc = dict(w_dgrad=self.wd[op.w]) if op.w in self.wd else dict(
                         w_dgrad=None, w_master=self.wmaster(op.w))
-                    nhwc.conv_dgrad(gy, cin=op.cin, kh=op.k, kw=op.k, dilation=op.dil, dx=self.gv(op.ins[0]), **wsrc,
-                                    accumulate=st["dx"], mask=self.v(op.ins[0]) if st["mask_dx"] else None,
-                                    residual=self.gv(st["dx_res"]) if st["dx_res"] else None)
+                    kw = dict(cin=op.cin, kh=op.k, kw=op.k, dilation=op.dil, dx=self.gv(op.ins[0]), **wsrc,
+                              accumulate=st["dx"], mask=self.v(op.ins[0]) if st["mask_dx"] else None,
+                              residual=self.gv(st["dx_res"]) if st["dx_res"] else None)
+                    bn = self.bnb_of.get(op.out)
+                    if bn is not None:   # dx = d loss / d (BN output): BN backward statistics in the epilogue
+                        kw.update(mask=self.v(bn.ins[0]), bnb_stats=self.bn_stats[bn.out])
+                        if bn.out not in self.bnb_parts:   # sized on the first (eager) step
+                            rows = 4 * nhwc.conv_dgrad(gy, bn_rows_only=True, **kw)
+                            self.bnb_parts[bn.out] = (torch.empty(rows * 2 * bn.cout, dtype=torch.float32,
+                                                                  device=self.device), rows)
+                        kw["bnb_partial"] = self.bnb_parts[bn.out][0]
+                    nhwc.conv_dgrad(gy, **kw)
                     self._toc(ev, op, "dgrad")
                     self.launches += 1
                 # no per-layer join: gradient buffers are never reused within a step (one per
@@ -1091,11 +1147,20 @@ class Engine:
                     self.launches += 1
                 g_off, _ = self.slot[op.w]
                 b_off, _ = self.slot[op.b]
-                nhwc.bn_backward(self.v(op.ins[0]), gy, self.wslice(op.w), self.bn_stats[op.out],
-                                 self.flat_g[g_off:g_off + op.cout], self.flat_g[b_off:b_off + op.cout],
-                                 self.gv(op.ins[0]) if st["dx"] is not None else None, self.ws,
-                                 accumulate=bool(st["dx"]))
-                self.launches += 3
+                if op.out in self.bnb_parts:   # statistics came with the consumer's dgrad
+                    part, rows = self.bnb_parts[op.out]
+                    nhwc.bn_backward_partials(part, rows, self.v(op.ins[0]), gy, self.wslice(op.w),
+                                              self.bn_stats[op.out], self.flat_g[g_off:g_off + op.cout],
+                                              self.flat_g[b_off:b_off + op.cout],
+                                              self.gv(op.ins[0]) if st["dx"] is not None else None, self.ws,
+                                              accumulate=bool(st["dx"]))
+                    self.launches += 2
+                else:
+                    nhwc.bn_backward(self.v(op.ins[0]), gy, self.wslice(op.w), self.bn_stats[op.out],
+                                     self.flat_g[g_off:g_off + op.cout], self.flat_g[b_off:b_off + op.cout],
+                                     self.gv(op.ins[0]) if st["dx"] is not None else None, self.ws,
+                                     accumulate=bool(st["dx"]))
+                    self.launches += 3
                 self._param_done((op.w, op.b), pending, on_bucket_ready)
             elif op.kind == "up" and op.mode == "bilinear":
                 nhwc.bilinear_bwd(self.gv(op.out), self.gv(op.ins[0]), op.factor, accumulate=st["dx"],

@@ -69,26 +69,38 @@ def same_pads(k: int, d: int):
 def conv_fprop(x: View, w_packed: torch.Tensor | None, cout: int, kh: int, kw: int, dilation: int,
                y: View, bias=None, residual: View | None = None, relu=False, accumulate=False,
                mask: View | None = None, y_f32=False, pads=None, block_n=0, w_master=None, w_mode=0, window=0,
-               in_stride=0, out_stride=0, out_phase=(0, 0)):
+               in_stride=0, out_stride=0, out_phase=(0, 0), bn_partial=None, bn_rows_only=False,
+               bnb_stats=None, bnb_partial=None):
     """w_mode 0: w_packed bf16 [cout][taps][cin_pad]; 1: w_master bf16 HWIO of this conv;
     2: w_master bf16 HWIO of the forward conv whose input gradient this is (see b2dl.h).
-    window > 0: row-window mode over a haloed x (pass kw=1; see b2dl_conv_args.window)."""
+    window > 0: row-window mode over a haloed x (pass kw=1; see b2dl_conv_args.window).
+    bn_partial: fp32 [rows][2][cout] batch-norm statistics of the output (epilogue-computed).
+    bn_rows_only: return the number of bn_partial rows the launch writes instead of launching."""
     pt, pl = pads if pads is not None else (same_pads(kh, dilation)[0], same_pads(kw, dilation)[0])
     a = ConvArgs(x.act(), _ptr(w_packed), cout, kh, kw, dilation, pt, pl,
                  y.act(), int(y_f32), _ptr(bias), _act(residual), int(relu), int(accumulate),
-                 _act(mask), block_n, _ptr(w_master), w_mode, window, in_stride, out_stride, *out_phase)
+                 _act(mask), block_n, _ptr(w_master), w_mode, window, in_stride, out_stride, *out_phase,
+                 _ptr(bn_partial), _ptr(bnb_stats), _ptr(bnb_partial))
+    if bn_rows_only:
+        n = LIB.b2dl_conv_fprop_bn_rows(ctypes.byref(a))
+        if n < 0:
+            check(-n, "conv_fprop_bn_rows")
+        return n
     check(LIB.b2dl_conv_fprop(ctypes.byref(a), _stream()), "conv_fprop")
 
 
 def conv_dgrad(dy: View, w_dgrad: torch.Tensor | None, cin: int, kh: int, kw: int, dilation: int,
                dx: View, accumulate=False, mask: View | None = None, dx_f32=False, w_master=None,
-               residual: View | None = None, block_n=0):
+               residual: View | None = None, block_n=0, bnb_stats=None, bnb_partial=None, bn_rows_only=False):
     """Input gradient as a forward conv over dy with tap-flipped weights and 'after' pads;
-    weights from the dgrad-packed copy, or straight from the forward conv's bf16 HWIO master."""
+    weights from the dgrad-packed copy, or straight from the forward conv's bf16 HWIO master.
+    bnb_stats / bnb_partial: dx is d loss / d y of a batch norm's output; mask = the BN input
+    (see b2dl_conv_args.bnb_partial)."""
     pads = (same_pads(kh, dilation)[1], same_pads(kw, dilation)[1])
-    conv_fprop(dy, w_dgrad, cin, kh, kw, dilation, dx, accumulate=accumulate, mask=mask, residual=residual,
-               y_f32=dx_f32, pads=pads, block_n=block_n, w_master=w_master,
-               w_mode=2 if w_master is not None else 0)
+    return conv_fprop(dy, w_dgrad, cin, kh, kw, dilation, dx, accumulate=accumulate, mask=mask, residual=residual,
+                      y_f32=dx_f32, pads=pads, block_n=block_n, w_master=w_master,
+                      w_mode=2 if w_master is not None else 0, bnb_stats=bnb_stats, bnb_partial=bnb_partial,
+                      bn_rows_only=bn_rows_only)
 
 
 class Workspace:
@@ -428,6 +440,28 @@ def bn_forward(x: View, gamma: torch.Tensor, beta: torch.Tensor, eps: float, y: 
     check(LIB.b2dl_bn_forward(x.act(), _ptr(gamma), _ptr(beta), float(eps), _act(residual), int(relu), y.act(),
                               _ptr(stats), ctypes.c_void_p(buf.data_ptr()), buf.numel(), _is_f32(x), _stream()),
           "bn_forward")
+
+
+def bn_forward_partials(partials: torch.Tensor, tiles: int, x: View, gamma: torch.Tensor, beta: torch.Tensor,
+                        eps: float, y: View, stats: torch.Tensor, ws: Workspace, residual: View | None = None,
+                        relu=False):
+    """bn_forward with the statistics from the producing conv's epilogue partials."""
+    buf = ws.get(LIB.b2dl_bn_workspace_size(x.c))
+    check(LIB.b2dl_bn_forward_partials(_ptr(partials), int(tiles), x.act(), _ptr(gamma), _ptr(beta), float(eps),
+                                       _act(residual), int(relu), y.act(), _ptr(stats),
+                                       ctypes.c_void_p(buf.data_ptr()), buf.numel(), _is_f32(x), _stream()),
+          "bn_forward_partials")
+
+
+def bn_backward_partials(partials: torch.Tensor, rows: int, x: View, gy: View, gamma: torch.Tensor,
+                         stats: torch.Tensor, dgamma, dbeta, dx: View | None, ws: Workspace, accumulate=False,
+                         param_accumulate=False):
+    """bn_backward with (sum gy, sum gy*xhat) rows from the consumer dgrad's epilogue."""
+    buf = ws.get(LIB.b2dl_bn_workspace_size(x.c))
+    check(LIB.b2dl_bn_backward_partials(_ptr(partials), int(rows), x.act(), gy.act(), _ptr(gamma), _ptr(stats),
+                                        _ptr(dgamma), _ptr(dbeta), int(param_accumulate), _act(dx), int(accumulate),
+                                        ctypes.c_void_p(buf.data_ptr()), buf.numel(), _is_f32(x), _stream()),
+          "bn_backward_partials")
 
 
 def bn_backward(x: View, gy: View, gamma: torch.Tensor, stats: torch.Tensor, dgamma, dbeta, dx: View | None,

@@ -115,3 +115,18 @@ def test_fp32_trainer_matches_reference_trainer(lag):
     for k, v in res.state.items():
         ref = d[f"{tag}_state:{k}"]
         assert rel(v, ref) < FP32_TOL, k
+
+
+def test_fp32_tiramisu_config4_topology_matches_oracle():
+    """Config 4's Tiramisu topology (5x5, growth 32, (2,2,2,4,5)) on a 2 x 16 x 64 x 48 tile, fp32
+    mode vs the oracle at the north-star 1e-3."""
+    from oracle import deskdl_port as O
+    from paper_1810_01993_b200.models import tiramisu_config4
+    from paper_1810_01993_b200.net import MiniDenseNet
+    from paper_1810_01993_b200.scenes import SceneConfig, generated_batch
+    net = MiniDenseNet(tiramisu_config4(), seed=0, precision="fp32")
+    x, labels = generated_batch(SceneConfig(height=64, width=48), seed=1, step=0, rank=0, local_batch=2)
+    cw = O.class_weights((0.982, 0.017, 0.001))
+    loss_ref, logits_ref, grads_ref, _ = O.train_step(net.graph, net.params, net.param_order, x, labels, cw,
+                                                     net.loss_name, net.logits_name)
+    _check(net, x, labels, cw, loss_ref, logits_ref, grads_ref)

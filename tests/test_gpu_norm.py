@@ -158,3 +158,74 @@ def test_deeplab_batchnorm_bilinear_fp32_vs_oracle():
         elif np.max(np.abs(grads[k])) > 1e-5 * scale:   # conv bias before a batch norm: ~0
             bad[k] = float(np.max(np.abs(grads[k])))
     assert not bad, bad
+
+
+@pytest.mark.parametrize("case", [
+    # (n, h, w, cin, cout, k, window-stem)  -- pair tiles, partial edge tiles, 1x1, the halo stem
+    (2, 48, 40, 64, 256, 3, False),
+    (1, 20, 36, 128, 64, 1, False),
+    (2, 64, 32, 256, 128, 3, False),
+    (2, 32, 48, 16, 64, 7, True),
+    (1, 24, 40, 64, 512, 1, False),     # several N tiles: one statistics row per M tile
+])
+def test_conv_epilogue_bn_statistics(case):
+    """b2dl_conv_args.bn_partial: per-tile channel sums / sums of squares of the stored bf16 output
+    (the batch-norm statistics fused into the conv's TMA epilogue), summed over the tiles, equal
+    float64 sums of the output tensor itself."""
+    from paper_1810_01993_b200 import nhwc
+    n, h, w, cin, cout, k, stem = case
+    torch.manual_seed(7)
+    b = torch.randn(cout, device="cuda") * 0.1
+    y = torch.empty(n, h, w, cout, dtype=torch.bfloat16, device="cuda")
+    if stem:
+        xs = torch.randn(n, h, w, cin, device="cuda").to(torch.bfloat16)
+        xwin = torch.zeros(n, h, w + k - 1, cin, dtype=torch.bfloat16, device="cuda")
+        xwin[:, :, (k - 1) // 2:(k - 1) // 2 + w] = xs
+        wp = torch.empty(cout, k, nhwc.cin_pad(k * cin), dtype=torch.bfloat16, device="cuda")
+        nhwc.pack_weights(torch.randn(k * k, cin, cout, device="cuda") * 0.05, k, 1, k * cin, cout, fprop=wp)
+        kw = dict(cout=cout, kh=k, kw=1, dilation=1, y=nhwc.View(y), bias=b, window=k, w_packed=wp)
+        x = nhwc.View(xwin)
+    else:
+        x = nhwc.View(torch.randn(n, h, w, cin, device="cuda").to(torch.bfloat16))
+        wm = (torch.randn(k * k, cin, cout, device="cuda") / (k * k * cin) ** 0.5).to(torch.bfloat16)
+        kw = dict(cout=cout, kh=k, kw=k, dilation=1, y=nhwc.View(y), bias=b, w_packed=None, w_master=wm, w_mode=1)
+    tiles = nhwc.conv_fprop(x, bn_rows_only=True, **kw)
+    part = torch.full((tiles * 2 * cout,), float("nan"), device="cuda")
+    nhwc.conv_fprop(x, bn_partial=part, **kw)
+    torch.cuda.synchronize()
+    got = part.view(tiles, 2, cout).double().sum(0)
+    yd = y.double().reshape(-1, cout)
+    assert torch.isfinite(got).all()
+    assert torch.allclose(got[0], yd.sum(0), rtol=1e-4, atol=1e-3 * float(yd.abs().max()))
+    assert torch.allclose(got[1], (yd * yd).sum(0), rtol=1e-4)
+    # the same launch without statistics writes the same output
+    y2 = y.clone()
+    nhwc.conv_fprop(x, **dict(kw, y=nhwc.View(y2)))
+    assert torch.equal(y, y2)
+
+
+def test_bn_statistics_fused_into_conv_epilogues_match_separate_passes(monkeypatch):
+    """The batch-norm statistics computed in the conv epilogues -- forward sums of the conv output
+    (bn_partial), backward sums of gy and gy * xhat in the consumer's dgrad with the relu mask
+    recomputed from the BN input (bnb_partial) -- give the same step as the separate statistics
+    passes (B2DL_BN_FUSED=0): same loss, logits and gradients up to summation order."""
+    x, labels = _batch()
+    from oracle import deskdl_port as O
+    cw = O.class_weights((0.982, 0.017, 0.001))
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("B2DL_BN_FUSED", flag)
+        net = _bn_net("bf16")
+        loss, logits, tape = net.forward_loss(x, labels, cw)
+        eng = tape.engine
+        grads = net.backward(tape)
+        if flag == "1":
+            assert eng.bn_parts and eng.bnb_parts, (len(eng.bn_parts), len(eng.bnb_parts))
+        out[flag] = (loss, logits.cpu().numpy(), grads)
+    (l0, z0, g0), (l1, z1, g1) = out["0"], out["1"]
+    assert abs(l0 - l1) < 1e-4 * abs(l0)
+    assert rel(z1, z0) < 1e-2
+    for k in g0:
+        # a conv bias feeding a batch norm has an exactly-zero gradient (rounding noise here)
+        if not (k.endswith(".b") and k != "head.b"):
+            assert rel(g1[k], g0[k]) < 3e-2, k
