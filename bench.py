@@ -273,14 +273,16 @@ def run_ours(args):
     shape = (LOCAL_BATCH, C, H, W)
     variant = getattr(args, "variant", "reference-ops")
     metric = METRIC
+    # config 4 is FP16 (BASELINE.json); the DeepLabV3+ configs are bf16
+    precision = args.precision or ("fp16" if variant == "tiramisu" else "bf16")
     if variant == "tiramisu":   # config 4 (the paper's Tiramisu / FC-DenseNet, frozen definition)
         from paper_1810_01993_b200.models import tiramisu_config4
         from paper_1810_01993_b200.net import MiniDenseNet
-        net = MiniDenseNet(tiramisu_config4(), seed=0)
+        net = MiniDenseNet(tiramisu_config4(), seed=0, precision=precision)
         metric = "Tiramisu (FC-DenseNet, config 4) train images/s & sustained TF/s, 1152×768×16"
     else:
         net = DeepLabV3Plus(DeepLabConfig(batchnorm=variant == "bn-bilinear", bilinear=variant == "bn-bilinear"),
-                            seed=0)
+                            seed=0, precision=precision)
     scene = SceneConfig(channels=C, height=H, width=W)
     cw = ClassWeights(scene.frequencies).vector()
     hier = tuple(int(v) for v in args.hierarchy.split("x")) if getattr(args, "hierarchy", "") else None
@@ -442,8 +444,8 @@ def run_ours(args):
         line = {
             "metric": metric, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (GPU-generated scenes, resident in HBM)",
-            "config": dict(_config(world, variant), lag=args.lag,
+            "vs_baseline": None, "dtype": precision, "data": "synthetic (GPU-generated scenes, resident in HBM)",
+            "config": dict(_config(world, variant), lag=args.lag, precision=precision,
                            **({"allreduce": f"hierarchical {args.hierarchy}"} if hier else {})),
             # sustained TF/s = tensor-core FLOPs the step executes x images/s (the convs' MACs; full.c0
             # runs from the low-resolution input, so this is below the reference-rule count)
@@ -508,6 +510,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--precision", default=None, choices=["bf16", "fp16"],
+                    help="16-bit storage / MMA operand type (default: bf16; fp16 for --variant tiramisu, config 4)")
     ap.add_argument("--lag", type=int, default=0, choices=[0, 1],
                     help="gradient lag (trainer.py:378-383): 1 applies the previous step's reduced gradients")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a captured CUDA graph")

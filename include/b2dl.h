@@ -278,12 +278,14 @@ B2DL_API size_t b2dl_bias_grad_workspace_size(b2dl_act g);
  *   dlogits       (softmax - onehot) * w_y / (sum_p w_y * N) written as a bf16
  *                 NHWC view with `classes` channels
  *   pred          argmax over classes, ties to the lowest index (uint8)
+ *   dlogits_scale multiplies dlogits (1; the fp16 build's static loss scale keeps the per-pixel
+ *                 gradients, ~1e-7 at 1152 x 768, out of fp16's subnormal range)
  *   status[0]     (optional) 1 if any label is >= classes, else 0; the loss is then NaN
  *                 (the reference raises ValueError, loss.py:72-74; the host shim maps it)
  * logits: fp32 NHWC view with `classes` channels; labels uint8 [N*H*W]. */
 B2DL_API int b2dl_wce(b2dl_act logits, const uint8_t* labels, const float* class_weights, int classes, float* loss_out,
-             int* counts, b2dl_act dlogits, int dlogits_f32, uint8_t* pred, int* status, void* workspace,
-             size_t workspace_bytes, void* stream);
+             int* counts, b2dl_act dlogits, int dlogits_f32, float dlogits_scale, uint8_t* pred, int* status,
+             void* workspace, size_t workspace_bytes, void* stream);
 B2DL_API size_t b2dl_wce_workspace_size(int n, int h, int w, int classes);
 
 /* LARC + SGD momentum over many tensors (optimizer.py:48-83) in two launches:

@@ -12,14 +12,24 @@ import torch
 import torch.nn.functional as F
 
 
+HALF = torch.bfloat16   # the 16-bit storage type being emulated (torch.float16 for the fp16 build)
+LOSS_SCALE = 1.0
+
+
+def set_half(dtype, loss_scale=1.0):
+    """Emulate another 16-bit storage type (and its static loss scale)."""
+    global HALF, LOSS_SCALE
+    HALF, LOSS_SCALE = dtype, float(loss_scale)
+
+
 class RoundGrad(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x):
-        return x.to(torch.bfloat16).float()
+        return x.to(HALF).float()
 
     @staticmethod
     def backward(ctx, g):
-        return g.to(torch.bfloat16).float()
+        return g.to(HALF).float()
 
 
 def run(graph, params, x, labels, cw, loss_name, emulate, stored=None):
@@ -33,8 +43,8 @@ def run(graph, params, x, labels, cw, loss_name, emulate, stored=None):
         ins = [vals[s] for s in nd.inputs]
         k, a = nd.kind, nd.attrs
         if k == "conv2d":
-            w = ins[1].to(torch.bfloat16).float() if emulate else ins[1]
-            xin = ins[0].to(torch.bfloat16).float() if (emulate and nd.inputs[0] == "x") else ins[0]
+            w = ins[1].to(HALF).float() if emulate else ins[1]
+            xin = ins[0].to(HALF).float() if (emulate and nd.inputs[0] == "x") else ins[0]
             pad = (a["kh"] - 1) * a["dilation"] // 2
             out = F.conv2d(xin, w, padding=pad, dilation=a["dilation"])
         elif k == "bias_add":
@@ -80,7 +90,10 @@ def run(graph, params, x, labels, cw, loss_name, emulate, stored=None):
             out = RoundGrad.apply(out)
         vals[nd.name] = out
     loss = vals[loss_name]
-    loss.backward()
+    (loss * LOSS_SCALE).backward()   # the fp16 build's static loss scale (gradients stored scaled)
+    if LOSS_SCALE != 1.0:
+        for v in P.values():
+            v.grad /= LOSS_SCALE
     run.last_values = vals
     return float(loss.detach()), {k: v.grad.numpy() for k, v in P.items()}
 

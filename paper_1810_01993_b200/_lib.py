@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libb2dl.so")
@@ -129,7 +130,7 @@ _SIGS = {
     "b2dl_dgrad_1x1_small": (_c_int, [Act, _vp, Act, _c_int, Act, _vp]),
     "b2dl_bias_grad": (_c_int, [Act, _vp, _c_int, _vp, _sz, _vp]),
     "b2dl_bias_grad_workspace_size": (_sz, [Act]),
-    "b2dl_wce": (_c_int, [Act, _vp, _vp, _c_int, _vp, _vp, Act, _c_int, _vp, _vp, _vp, _sz, _vp]),
+    "b2dl_wce": (_c_int, [Act, _vp, _vp, _c_int, _vp, _vp, Act, _c_int, ctypes.c_float, _vp, _vp, _vp, _sz, _vp]),
     "b2dl_wce_workspace_size": (_sz, [_c_int] * 4),
     "b2dl_larc_workspace_size": (_sz, [ctypes.c_int64, _c_int]),
     "b2dl_larc_update": (_c_int, [ctypes.POINTER(LarcArgs), _vp]),
@@ -138,12 +139,12 @@ _SIGS = {
 EXPORTED_SYMBOLS = tuple(_SIGS)
 
 
-def _load():
-    if not os.path.exists(LIB_PATH):
+def _load(path=LIB_PATH):
+    if not os.path.exists(path):
         raise ImportError(
-            f"{LIB_PATH} is missing: build it with `python -m paper_1810_01993_b200._build` "
+            f"{path} is missing: build it with `python -m paper_1810_01993_b200._build` "
             "(this package has no CPU fallback)")
-    lib = ctypes.CDLL(LIB_PATH)
+    lib = ctypes.CDLL(path)
     for name, (res, args) in _SIGS.items():
         fn = getattr(lib, name)
         fn.restype = res
@@ -151,7 +152,43 @@ def _load():
     return lib
 
 
-LIB = _load()
+LIB_F16_PATH = os.path.join(HERE, "libb2dl_f16.so")
+_LIBS = {"bf16": _load()}
+_current = threading.local()
+
+
+def library(half: str = "bf16"):
+    """The build whose 16-bit storage type is `half` ("bf16": libb2dl.so, "fp16": libb2dl_f16.so)."""
+    if half not in _LIBS:
+        if half != "fp16":
+            raise ValueError(f"no {half!r} build")
+        _LIBS[half] = _load(LIB_F16_PATH)
+    return _LIBS[half]
+
+
+class _Dispatch:
+    """`LIB`: the bf16 build, or inside `use(\"fp16\")` the fp16 build (same symbols)."""
+
+    def __getattr__(self, name):
+        return getattr(getattr(_current, "lib", None) or _LIBS["bf16"], name)
+
+
+LIB = _Dispatch()
+
+
+class use:
+    """Context: route LIB calls of this thread to the build of the given 16-bit type (re-entrant)."""
+
+    def __init__(self, half: str):
+        self.lib = library(half) if half == "fp16" else _LIBS["bf16"]
+
+    def __enter__(self):
+        self.prev = getattr(_current, "lib", None)
+        _current.lib = self.lib
+        return self.lib
+
+    def __exit__(self, *exc):
+        _current.lib = self.prev
 
 
 class B2DLError(RuntimeError):

@@ -110,9 +110,9 @@ struct FpropParams {
   long long y_stride;
   int y_f32;
   const float* bias;
-  const __nv_bfloat16* res;
+  const b2h* res;
   long long res_stride;
-  const __nv_bfloat16* mask;
+  const b2h* mask;
   long long mask_stride;
   int relu, accumulate, vec_ok;
   int b_mode;  // 0 packed [cout][taps][cin_pad]; 1 master HWIO, MN-major; 2 master HWIO, dgrad (flipped taps)
@@ -156,7 +156,7 @@ struct CoopRows {
 };
 
 template <int CW>
-__device__ __forceinline__ void coop_load(const __nv_bfloat16* base, long long stride, int c0, int cout,
+__device__ __forceinline__ void coop_load(const b2h* base, long long stride, int c0, int cout,
                                           const CoopRows<CW>& L, uint8_t* st, bool nc) {
   using R = CoopRows<CW>;
   const int lane = lane_id(), piece = lane % R::PIECES;
@@ -172,7 +172,7 @@ __device__ __forceinline__ void coop_load(const __nv_bfloat16* base, long long s
   }
 }
 template <int CW>
-__device__ __forceinline__ void coop_store(__nv_bfloat16* base, long long stride, int c0, int cout,
+__device__ __forceinline__ void coop_store(b2h* base, long long stride, int c0, int cout,
                                            const CoopRows<CW>& L, const uint8_t* st) {
   using R = CoopRows<CW>;
   const int lane = lane_id(), piece = lane % R::PIECES;
@@ -215,7 +215,7 @@ __device__ __forceinline__ void row_put(uint8_t* st, const float* v) {
 // Register prefetch of one cooperative 32 x CW tile (the epilogue's first global operand),
 // issued before the accumulator is ready so the DRAM latency overlaps the MMA main loop.
 template <int CW>
-__device__ __forceinline__ void coop_prefetch(const __nv_bfloat16* base, long long stride, int c0, int cout,
+__device__ __forceinline__ void coop_prefetch(const b2h* base, long long stride, int c0, int cout,
                                               const CoopRows<CW>& L, uint4* r) {
   using R = CoopRows<CW>;
   const int piece = lane_id() % R::PIECES;
@@ -272,7 +272,7 @@ __device__ __forceinline__ void fprop_epilogue_vec(const FpropParams& p, float* 
       if (!(t[i] > 0.f)) v[i] = 0.f;
     __syncwarp();
   }
-  __nv_bfloat16* y = reinterpret_cast<__nv_bfloat16*>(p.y);
+  b2h* y = reinterpret_cast<b2h*>(p.y);
   if (p.accumulate) {
     coop_load<CW>(y, p.y_stride, c0, p.cout, L, st, false);
     __syncwarp();
@@ -300,16 +300,16 @@ __device__ __forceinline__ void fprop_epilogue_scalar(const FpropParams& p, floa
   for (int i = 0; i < CW; ++i) {
     if (i >= nvalid) break;
     float x = v[i];
-    if (p.res) x += __bfloat162float(p.res[pix * p.res_stride + c0 + i]);
+    if (p.res) x += h_to_f(p.res[pix * p.res_stride + c0 + i]);
     if (p.relu) x = fmaxf(x, 0.f);
-    if (p.mask && !(__bfloat162float(p.mask[pix * p.mask_stride + c0 + i]) > 0.f)) x = 0.f;
+    if (p.mask && !(h_to_f(p.mask[pix * p.mask_stride + c0 + i]) > 0.f)) x = 0.f;
     if (p.y_f32) {
       float* d = reinterpret_cast<float*>(p.y) + pix * p.y_stride + c0 + i;
       *d = p.accumulate ? *d + x : x;
     } else {
-      __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(p.y) + pix * p.y_stride + c0 + i;
-      if (p.accumulate) x += __bfloat162float(*d);
-      *d = __float2bfloat16_rn(x);
+      b2h* d = reinterpret_cast<b2h*>(p.y) + pix * p.y_stride + c0 + i;
+      if (p.accumulate) x += h_to_f(*d);
+      *d = f_to_h(x);
     }
   }
 }
@@ -727,7 +727,7 @@ __device__ __forceinline__ void fprop_epilogue_role(const FpropParams& p, const 
       }
       // prefetch the first global epilogue operand of all of this warp's chunks
       uint4 pre[NJ][R::PIECES];
-      const __nv_bfloat16* pbase = p.res ? p.res : p.mask;
+      const b2h* pbase = p.res ? p.res : p.mask;
       const long long pstride = p.res ? p.res_stride : p.mask_stride;
       if (vec && pbase) {
 #pragma unroll
@@ -780,7 +780,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
                       const __grid_constant__ CUtensorMap tmM, const FpropParams p) {
   using C = FpropCfg<BN, KBLK, BMN, CG>;
   const int STAGES = p.stages;
-  constexpr uint32_t LAYOUT = KBLK == 64 ? LAYOUT_SW128 : LAYOUT_SW32;
+  constexpr uint32_t LAYOUT = KBLK == 64 ? LAYOUT_SW128 : KBLK == 32 ? LAYOUT_SW64 : LAYOUT_SW32;
   constexpr uint32_t SBO = KBLK * 2 * 8;  // 8 rows of KBLK bf16
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
@@ -1439,7 +1439,7 @@ __global__ void __launch_bounds__(192, 1)
         const uint8_t* dyt = smem + stage * stage_bytes + 2 * xbox;
 #pragma unroll 8
         for (int px = ph * 64; px < ph * 64 + 64; ++px)
-          bs += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(
+          bs += h_to_f(*reinterpret_cast<const b2h*>(
               dyt + px * 128 + ((((co >> 3) ^ (px & 7))) << 4) + (co & 7) * 2));
       }
       __syncwarp();
@@ -1765,9 +1765,9 @@ static int launch_halo_fprop(const b2dl_conv_args* a, const b2dl_act& xv, cudaSt
   p.y_stride = y.c_stride;
   p.bias = a->bias;
   p.bias_vec = a->bias && (reinterpret_cast<uintptr_t>(a->bias) % 16 == 0);
-  p.res = reinterpret_cast<const __nv_bfloat16*>(a->residual.ptr);
+  p.res = reinterpret_cast<const b2h*>(a->residual.ptr);
   p.res_stride = a->residual.c_stride;
-  p.mask = reinterpret_cast<const __nv_bfloat16*>(a->mask.ptr);
+  p.mask = reinterpret_cast<const b2h*>(a->mask.ptr);
   p.mask_stride = a->mask.c_stride;
   p.relu = a->relu;
   p.accumulate = a->accumulate;
@@ -1790,7 +1790,7 @@ static int launch_halo_fprop(const b2dl_conv_args* a, const b2dl_act& xv, cudaSt
   const uint64_t wsd[1] = {ktot * 2};
   const uint32_t wb[2] = {64u, static_cast<uint32_t>(HALO_BN)};
   if (window_map(&t.a, a->x, xv.c, y.w, 64, HALO_BW, HALO_BH + p.taps - 1, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      encode_tiled(&t.b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a->w_packed), wd, wsd, wb,
+      encode_tiled(&t.b, B2H_TMA, 2, const_cast<void*>(a->w_packed), wd, wsd, wb,
                    CU_TENSOR_MAP_SWIZZLE_128B) ||
       act_map(&t.y, y, 32, bwx, bhx, CU_TENSOR_MAP_SWIZZLE_64B) ||
       (p.res && act_map(&t.r, a->residual, 32, bwx, bhx, CU_TENSOR_MAP_SWIZZLE_64B)) ||
@@ -1840,6 +1840,11 @@ static int window_view(const b2dl_act& x, int window, int kw, int pad_left, int 
 }  // namespace b2
 
 namespace b2 {
+static int fprop_kblk(const b2dl_conv_args* a, const b2dl_act& x) {
+  if (x.c <= 16) return 16;
+  if (x.c <= 32 && a->w_mode != 0 && !a->window) return 32;
+  return 64;
+}
 // N tile width and CTA pairing of a b2dl_conv_fprop launch (shared with b2dl_conv_fprop_bn_rows)
 static void fprop_choose(const b2dl_conv_args* a, const b2dl_act& x, int kblk, int* bn_out, int* cg_out) {
   int bn = a->block_n ? a->block_n : pick_bn(a->cout);
@@ -1904,7 +1909,7 @@ extern "C" int b2dl_conv_fprop_bn_rows(const b2dl_conv_args* a) {
   while (bw * s_in > 256) bw >>= 1;
   const int m_tiles = x.n * cdiv(x.w, bw) * cdiv(x.h, BM / bw);
   int bn, cg;
-  fprop_choose(a, x, x.c <= 16 ? 16 : 64, &bn, &cg);
+  fprop_choose(a, x, fprop_kblk(a, x), &bn, &cg);
   const int n_tiles = cdiv(a->cout, bn);
   if (n_tiles > 1) return m_tiles;
   return cg * std::min(cdiv(m_tiles, cg) * n_tiles, num_sms() / cg);
@@ -1934,8 +1939,11 @@ extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
   if (a->kh < 1 || a->kw < 1 || a->dilation < 1 || a->cout < 1 || x.c < 1) return B2DL_E_VALUE;
   if (!view_aligned(x, 2)) return B2DL_E_ALIGN;
   if (halo_fprop_ok(a, x)) return launch_halo_fprop(a, x, as_stream(stream));
-  const int kblk = x.c <= 16 ? 16 : 64;
-  const int cin_pad = b2dl_cin_pad(x.c);
+  // K block: 16 channels for narrow inputs, 32 for 17..32-channel inputs read through master
+  // weights (e.g. the dgrad over a growth-32 dense layer's dy: half the padded MMA work of a
+  // 64-wide block), else 64
+  const int kblk = fprop_kblk(a, x);
+  const int cin_pad = kblk == 32 ? 32 : b2dl_cin_pad(x.c);
   int bn, cg;
   fprop_choose(a, x, kblk, &bn, &cg);
 
@@ -1965,9 +1973,9 @@ extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
   p.y_stride = y.c_stride;
   p.y_f32 = a->y_f32;
   p.bias = a->bias;
-  p.res = reinterpret_cast<const __nv_bfloat16*>(a->residual.ptr);
+  p.res = reinterpret_cast<const b2h*>(a->residual.ptr);
   p.res_stride = a->residual.c_stride;
-  p.mask = reinterpret_cast<const __nv_bfloat16*>(a->mask.ptr);
+  p.mask = reinterpret_cast<const b2h*>(a->mask.ptr);
   p.mask_stride = a->mask.c_stride;
   p.relu = a->relu;
   p.accumulate = a->accumulate;
@@ -1975,7 +1983,9 @@ extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
              (!p.mask || view_aligned(a->mask, 2));
 
   FpropMaps t;
-  const CUtensorMapSwizzle sw = kblk == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B;
+  const CUtensorMapSwizzle sw = kblk == 64   ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : kblk == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                             : CU_TENSOR_MAP_SWIZZLE_32B;
   if (a->window ? window_map(&t.a, a->x, x.c, y.w, kblk, p.bw, p.bh, sw)
                 : s_in > 1 ? act_map_strided(&t.a, a->x, kblk, p.bw, p.bh, s_in, sw)
                            : act_map(&t.a, x, kblk, p.bw, p.bh, sw))
@@ -1989,7 +1999,7 @@ extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
     const uint64_t wd[2] = {ktot, static_cast<uint64_t>(a->cout)};
     const uint64_t ws[1] = {ktot * 2};
     const uint32_t wb[2] = {static_cast<uint32_t>(kblk), static_cast<uint32_t>(bn / cg)};
-    if (encode_tiled(&t.b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a->w_packed), wd, ws, wb, sw))
+    if (encode_tiled(&t.b, B2H_TMA, 2, const_cast<void*>(a->w_packed), wd, ws, wb, sw))
       return B2DL_E_ALIGN;
   } else {
     // master HWIO bf16 [taps][cin_f][cout_f] of the forward conv; fprop: cin_f = x.c, cout_f = cout;
@@ -2002,12 +2012,12 @@ extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
     const uint64_t ws[2] = {cf * 2, cf * kf * 2};
     if (mode == 1) {
       const uint32_t wb[3] = {64u, static_cast<uint32_t>(kblk), 1u};
-      if (encode_tiled(&t.b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(a->w_master), wd, ws, wb,
+      if (encode_tiled(&t.b, B2H_TMA, 3, const_cast<void*>(a->w_master), wd, ws, wb,
                        CU_TENSOR_MAP_SWIZZLE_128B))
         return B2DL_E_ALIGN;
     } else {
       const uint32_t wb[3] = {static_cast<uint32_t>(kblk), static_cast<uint32_t>(bn / cg), 1u};
-      if (encode_tiled(&t.b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(a->w_master), wd, ws, wb, sw))
+      if (encode_tiled(&t.b, B2H_TMA, 3, const_cast<void*>(a->w_master), wd, ws, wb, sw))
         return B2DL_E_ALIGN;
     }
   }
@@ -2084,6 +2094,11 @@ extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
   B2_FPROP(64, 64)
   B2_FPROP(32, 64)
   B2_FPROP(16, 64)
+  B2_FPROP(256, 32)
+  B2_FPROP(128, 32)
+  B2_FPROP(64, 32)
+  B2_FPROP(32, 32)
+  B2_FPROP(16, 32)
   B2_FPROP(256, 16)
   B2_FPROP(128, 16)
   B2_FPROP(64, 16)

@@ -12,9 +12,9 @@
 
 namespace b2 {
 
-__device__ __forceinline__ float ld_bf(const __nv_bfloat16* p) { return __bfloat162float(*p); }
-__device__ __forceinline__ float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
-__device__ __forceinline__ float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }
+__device__ __forceinline__ float ld_bf(const b2h* p) { return h_to_f(*p); }
+__device__ __forceinline__ float bf16_lo(uint32_t v) { return h_lo(v); }
+__device__ __forceinline__ float bf16_hi(uint32_t v) { return h_hi(v); }
 
 static int grid1d(long long total, int per_thread = 1) {
   long long blocks = (total / per_thread + 255) / 256;
@@ -38,23 +38,23 @@ __global__ void k_nchw_to_nhwc(const float* __restrict__ x, void* __restrict__ y
     if (f32)
       reinterpret_cast<float*>(y)[d] = x[i];
     else
-      reinterpret_cast<__nv_bfloat16*>(y)[d] = __float2bfloat16_rn(x[i]);
+      reinterpret_cast<b2h*>(y)[d] = f_to_h(x[i]);
   }
 }
 constexpr int HALO_COLS = 256;  // one thread per pixel column of a row
 __device__ __forceinline__ uint32_t halo_pack2(float a, float b) {  // a -> low half
-  const __nv_bfloat162 t = __floats2bfloat162_rn(a, b);
+  const b2h2 t = h2_from(a, b);
   return *reinterpret_cast<const uint32_t*>(&t);
 }
 // NCHW fp32 -> NHWC bf16 with zeroed halo columns.  One thread per pixel: each of its c channel
 // loads is a coalesced 128-byte warp access of one plane row, and its 2c output bytes are
 // written as 16-byte pieces adjacent to the neighbouring threads' (no shared-memory transpose).
 __global__ void __launch_bounds__(HALO_COLS) k_nchw_to_nhwc_halo(const float* __restrict__ x,
-                                                                 __nv_bfloat16* __restrict__ y, int c, int h, int w,
+                                                                 b2h* __restrict__ y, int c, int h, int w,
                                                                  int wp, int left) {
   const int col = blockIdx.x * HALO_COLS + threadIdx.x, row = blockIdx.y, img = blockIdx.z;
   const long long plane = static_cast<long long>(h) * w;
-  __nv_bfloat16* dst_row = y + (static_cast<long long>(img) * h + row) * wp * c;
+  b2h* dst_row = y + (static_cast<long long>(img) * h + row) * wp * c;
   const int vec = c / 8;  // 16-byte pieces per pixel
   if (col < w) {
     const float* src = x + static_cast<long long>(img) * c * plane + static_cast<long long>(row) * w + col;
@@ -92,57 +92,57 @@ __global__ void k_nhwc_to_nchw(const void* __restrict__ x, int f32, float* __res
     int ch = static_cast<int>(r % c);
     long long img = r / c;
     long long src = (img * hw + pix) * cs + ch;
-    y[i] = f32 ? reinterpret_cast<const float*>(x)[src] : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(x)[src]);
+    y[i] = f32 ? reinterpret_cast<const float*>(x)[src] : h_to_f(reinterpret_cast<const b2h*>(x)[src]);
   }
 }
 
 // ------------------------------------------------------------------ pool / upsample
 // 8-channel (16 B) vector helpers; G = 8 on aligned views, 1 otherwise
 template <int G>
-__device__ __forceinline__ void ldv(const __nv_bfloat16* p, float* v) {
+__device__ __forceinline__ void ldv(const b2h* p, float* v) {
   if constexpr (G == 8) {
     uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
     const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      v[2 * e] = __uint_as_float(w[e] << 16);
-      v[2 * e + 1] = __uint_as_float(w[e] & 0xFFFF0000u);
+      v[2 * e] = h_lo(w[e]);
+      v[2 * e + 1] = h_hi(w[e]);
     }
   } else {
     v[0] = ld_bf(p);
   }
 }
 template <int G>
-__device__ __forceinline__ void ldv_rw(const __nv_bfloat16* p, float* v) {  // plain load (data written in place)
+__device__ __forceinline__ void ldv_rw(const b2h* p, float* v) {  // plain load (data written in place)
   if constexpr (G == 8) {
     uint4 u = *reinterpret_cast<const uint4*>(p);
     const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      v[2 * e] = __uint_as_float(w[e] << 16);
-      v[2 * e + 1] = __uint_as_float(w[e] & 0xFFFF0000u);
+      v[2 * e] = h_lo(w[e]);
+      v[2 * e + 1] = h_hi(w[e]);
     }
   } else {
     v[0] = ld_bf(p);
   }
 }
 template <int G>
-__device__ __forceinline__ void stv(__nv_bfloat16* p, const float* v) {
+__device__ __forceinline__ void stv(b2h* p, const float* v) {
   if constexpr (G == 8) {
     uint32_t w[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      __nv_bfloat162 t = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+      b2h2 t = h2_from(v[2 * e], v[2 * e + 1]);
       w[e] = *reinterpret_cast<uint32_t*>(&t);
     }
     *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
   } else {
-    *p = __float2bfloat16_rn(v[0]);
+    *p = f_to_h(v[0]);
   }
 }
 // d <- mask(m) * v  [+ d]
 template <int G>
-__device__ __forceinline__ void finish(float* v, const __nv_bfloat16* m, __nv_bfloat16* d, int acc) {
+__device__ __forceinline__ void finish(float* v, const b2h* m, b2h* d, int acc) {
   if (m) {
     float mv[G];
     ldv<G>(m, mv);
@@ -160,7 +160,7 @@ __device__ __forceinline__ void finish(float* v, const __nv_bfloat16* m, __nv_bf
 }
 
 template <int G>
-__global__ void k_avgpool_fwd(const __nv_bfloat16* __restrict__ x, int xs, __nv_bfloat16* __restrict__ y, int ys,
+__global__ void k_avgpool_fwd(const b2h* __restrict__ x, int xs, b2h* __restrict__ y, int ys,
                               int n, int ho, int wo, int c, int k) {
   const int W = wo * k;
   const int cg = c / G;
@@ -189,8 +189,8 @@ __global__ void k_avgpool_fwd(const __nv_bfloat16* __restrict__ x, int xs, __nv_
           const uint32_t w4[4] = {raw[t].x, raw[t].y, raw[t].z, raw[t].w};
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            s[2 * e] += __uint_as_float(w4[e] << 16);
-            s[2 * e + 1] += __uint_as_float(w4[e] & 0xFFFF0000u);
+            s[2 * e] += h_lo(w4[e]);
+            s[2 * e + 1] += h_hi(w4[e]);
           }
         }
 #pragma unroll
@@ -200,7 +200,7 @@ __global__ void k_avgpool_fwd(const __nv_bfloat16* __restrict__ x, int xs, __nv_
       }
     }
     for (int a = 0; a < k; ++a) {
-      const __nv_bfloat16* row = x + ((img * ho * k + oy * k + a) * W + ox * k) * xs + ch;
+      const b2h* row = x + ((img * ho * k + oy * k + a) * W + ox * k) * xs + ch;
       for (int b = 0; b < k; ++b) {
         float v[G];
         ldv<G>(row + static_cast<long long>(b) * xs, v);
@@ -215,8 +215,8 @@ __global__ void k_avgpool_fwd(const __nv_bfloat16* __restrict__ x, int xs, __nv_
 }
 // dx[p] (+)= mask(x)[p] * dy[pool(p)] / k^2
 template <int G>
-__global__ void k_avgpool_bwd(const __nv_bfloat16* __restrict__ dy, int dys, __nv_bfloat16* __restrict__ dx, int dxs,
-                              const __nv_bfloat16* __restrict__ mask, int ms, int n, int h, int w, int c, int k,
+__global__ void k_avgpool_bwd(const b2h* __restrict__ dy, int dys, b2h* __restrict__ dx, int dxs,
+                              const b2h* __restrict__ mask, int ms, int n, int h, int w, int c, int k,
                               int acc) {
   // one thread per (pooled pixel, channel group): dy read once, the k x k outputs written from it;
   // 32-bit index math (the launcher checks the pooled element count fits)
@@ -250,8 +250,8 @@ __global__ void k_avgpool_bwd(const __nv_bfloat16* __restrict__ dy, int dys, __n
             float o[8];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              o[2 * e] = __uint_as_float(mw[e] << 16) > 0.f ? v[2 * e] : 0.f;
-              o[2 * e + 1] = __uint_as_float(mw[e] & 0xFFFF0000u) > 0.f ? v[2 * e + 1] : 0.f;
+              o[2 * e] = h_lo(mw[e]) > 0.f ? v[2 * e] : 0.f;
+              o[2 * e + 1] = h_hi(mw[e]) > 0.f ? v[2 * e + 1] : 0.f;
             }
             stv<8>(dx + (p0 + a * w + b) * dxs + ch, o);
           }
@@ -269,7 +269,7 @@ __global__ void k_avgpool_bwd(const __nv_bfloat16* __restrict__ dy, int dys, __n
   }
 }
 template <int G>
-__global__ void k_upsample_fwd(const __nv_bfloat16* __restrict__ x, int xs, __nv_bfloat16* __restrict__ y, int ys,
+__global__ void k_upsample_fwd(const b2h* __restrict__ x, int xs, b2h* __restrict__ y, int ys,
                                int n, int h, int w, int c, int f) {
   // one thread per (input pixel, channel group): read once, write the f x f replicas
   const int W = w * f;
@@ -290,8 +290,8 @@ __global__ void k_upsample_fwd(const __nv_bfloat16* __restrict__ x, int xs, __nv
 }
 // dx[q] (+)= mask(x)[q] * sum over the f x f block of dy
 template <int G>
-__global__ void k_upsample_bwd(const __nv_bfloat16* __restrict__ dy, int dys, __nv_bfloat16* __restrict__ dx, int dxs,
-                               const __nv_bfloat16* __restrict__ mask, int ms, int n, int h, int w, int c, int f,
+__global__ void k_upsample_bwd(const b2h* __restrict__ dy, int dys, b2h* __restrict__ dx, int dxs,
+                               const b2h* __restrict__ mask, int ms, int n, int h, int w, int c, int f,
                                int acc) {
   const int W = w * f;
   const int cg = c / G;
@@ -320,8 +320,8 @@ __global__ void k_upsample_bwd(const __nv_bfloat16* __restrict__ dy, int dys, __
 
 // ------------------------------------------------------------------ add / mask
 template <int G>
-__global__ void k_add(const __nv_bfloat16* __restrict__ x, int xs, __nv_bfloat16* __restrict__ y, int ys,
-                      const __nv_bfloat16* __restrict__ mask, int ms, long long npix, int c, int acc) {
+__global__ void k_add(const b2h* __restrict__ x, int xs, b2h* __restrict__ y, int ys,
+                      const b2h* __restrict__ mask, int ms, long long npix, int c, int acc) {
   const int cg = c / G;
   const long long total = npix * cg;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
@@ -334,7 +334,7 @@ __global__ void k_add(const __nv_bfloat16* __restrict__ x, int xs, __nv_bfloat16
   }
 }
 template <int G>
-__global__ void k_relu_mask(__nv_bfloat16* __restrict__ g, int gs, const __nv_bfloat16* __restrict__ a, int as,
+__global__ void k_relu_mask(b2h* __restrict__ g, int gs, const b2h* __restrict__ a, int as,
                             long long npix, int c) {
   const int cg = c / G;
   const long long total = npix * cg;
@@ -353,7 +353,7 @@ __global__ void k_relu_mask(__nv_bfloat16* __restrict__ g, int gs, const __nv_bf
 //         stride over rows, rows are folded in shared memory -> part[b][c]
 // pass 2: out[c] (+)= sum_b part[b][c] in a fixed order (deterministic)
 template <int G>
-__global__ void k_colsum_partial(const __nv_bfloat16* __restrict__ g, int gs, long long npix, int c,
+__global__ void k_colsum_partial(const b2h* __restrict__ g, int gs, long long npix, int c,
                                  float* __restrict__ part) {
   extern __shared__ float red[];
   const int cg = c / G;
@@ -406,9 +406,9 @@ static int colsum_blocks(long long npix) {
 // dx[p][ci] (+)= mask * sum_k dy[p][k] * w[ci][k]   (1x1 conv, k = dy channels <= 8)
 // weights transposed into shared memory as [k][cin] so a thread's 8 channels are 2 float4 reads
 template <int G>
-__global__ void k_dgrad_1x1_small(const __nv_bfloat16* __restrict__ dy, int dys, int kc,
-                                  const float* __restrict__ w, int cin, __nv_bfloat16* __restrict__ dx, int dxs,
-                                  const __nv_bfloat16* __restrict__ mask, int ms, long long npix, int acc) {
+__global__ void k_dgrad_1x1_small(const b2h* __restrict__ dy, int dys, int kc,
+                                  const float* __restrict__ w, int cin, b2h* __restrict__ dx, int dxs,
+                                  const b2h* __restrict__ mask, int ms, long long npix, int acc) {
   extern __shared__ float wsm[];  // [kc][cin]
   for (int i = threadIdx.x; i < cin * kc; i += blockDim.x) {
     const int ci = i / kc, k = i - ci * kc;
@@ -463,8 +463,8 @@ __global__ void k_dgrad_1x1_small(const __nv_bfloat16* __restrict__ dy, int dys,
 constexpr int HEAD_THREADS = 256;
 template <int KC, bool DYV>
 __global__ void __launch_bounds__(HEAD_THREADS, 2) k_head_backward(
-    const __nv_bfloat16* __restrict__ dy, int dys, const float* __restrict__ w, int cin,
-    const __nv_bfloat16* __restrict__ x, int xs, __nv_bfloat16* __restrict__ dx, int dxs, int acc, int mask_dx,
+    const b2h* __restrict__ dy, int dys, const float* __restrict__ w, int cin,
+    const b2h* __restrict__ x, int xs, b2h* __restrict__ dx, int dxs, int acc, int mask_dx,
     int npix, float* __restrict__ dwp, float* __restrict__ dbp) {
   constexpr int kc = KC;
   extern __shared__ float hsm[];  // w^T [kc][cin], then reduction scratch [ppb][cin * kc + kc]
@@ -553,7 +553,7 @@ __global__ void __launch_bounds__(HEAD_THREADS, 2) k_head_backward(
           for (int e = 0; e < 8; ++e)
             if (!(xv[e] > 0.f)) v[e] = 0.f;
         }
-        __nv_bfloat16* o = dx + static_cast<long long>(p) * dxs + ch;
+        b2h* o = dx + static_cast<long long>(p) * dxs + ch;
         if (acc) {
           float old[8];
           ldv_rw<8>(o, old);
@@ -594,7 +594,7 @@ static bool vec_ok(const b2dl_act& a, const b2dl_act& b, const b2dl_act& m) {
 
 // ------------------------------------------------------------------ weight packing
 // master HWIO fp32 [taps][cin][cout] -> fprop [cout][taps][cin_pad] and dgrad [cin][taps'][cout_pad]
-__global__ void k_pack_fprop(const float* __restrict__ w, __nv_bfloat16* __restrict__ out, int taps, int cin,
+__global__ void k_pack_fprop(const float* __restrict__ w, b2h* __restrict__ out, int taps, int cin,
                              int cout, int cin_pad) {
   const long long total = static_cast<long long>(cout) * taps * cin_pad;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
@@ -603,10 +603,10 @@ __global__ void k_pack_fprop(const float* __restrict__ w, __nv_bfloat16* __restr
     long long r = i / cin_pad;
     int t = static_cast<int>(r % taps);
     int co = static_cast<int>(r / taps);
-    out[i] = __float2bfloat16_rn(ci < cin ? w[(static_cast<long long>(t) * cin + ci) * cout + co] : 0.f);
+    out[i] = f_to_h(ci < cin ? w[(static_cast<long long>(t) * cin + ci) * cout + co] : 0.f);
   }
 }
-__global__ void k_pack_dgrad(const float* __restrict__ w, __nv_bfloat16* __restrict__ out, int taps, int cin,
+__global__ void k_pack_dgrad(const float* __restrict__ w, b2h* __restrict__ out, int taps, int cin,
                              int cout, int cout_pad) {
   const long long total = static_cast<long long>(cin) * taps * cout_pad;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
@@ -616,15 +616,15 @@ __global__ void k_pack_dgrad(const float* __restrict__ w, __nv_bfloat16* __restr
     int tf = static_cast<int>(r % taps);
     int ci = static_cast<int>(r / taps);
     int t = taps - 1 - tf;
-    out[i] = __float2bfloat16_rn(co < cout ? w[(static_cast<long long>(t) * cin + ci) * cout + co] : 0.f);
+    out[i] = f_to_h(co < cout ? w[(static_cast<long long>(t) * cin + ci) * cout + co] : 0.f);
   }
 }
 
 }  // namespace b2
 
 using namespace b2;
-#define BF(p) reinterpret_cast<__nv_bfloat16*>(p)
-#define CBF(p) reinterpret_cast<const __nv_bfloat16*>(p)
+#define BF(p) reinterpret_cast<b2h*>(p)
+#define CBF(p) reinterpret_cast<const b2h*>(p)
 
 extern "C" int b2dl_nchw_to_nhwc(const float* x, b2dl_act y, int dst_f32, void* stream) {
   if (!x || !y.ptr) return B2DL_E_VALUE;
@@ -759,7 +759,7 @@ extern "C" int b2dl_pack_weights(const float* w_hwio, int kh, int kw, int cin, i
 // b = i + t - (k - 1) lies in [0, f) on both axes (K' = k + f - 1): the input gradient of a k x k
 // "same" conv over a nearest x f upsampling, summed over each f x f block, as one K'-tap conv
 // with input stride f over dy.
-__global__ void k_pack_upsampled_dgrad(const float* __restrict__ w, __nv_bfloat16* __restrict__ out, int k, int cin,
+__global__ void k_pack_upsampled_dgrad(const float* __restrict__ w, b2h* __restrict__ out, int k, int cin,
                                        int cout, int f, int cp) {
   const int kk = k + f - 1;
   const long long total = static_cast<long long>(cin) * kk * kk * cp;
@@ -781,7 +781,7 @@ __global__ void k_pack_upsampled_dgrad(const float* __restrict__ w, __nv_bfloat1
           v += w[(static_cast<long long>(ti * k + tj) * cin + ci) * cout + co];
         }
       }
-    out[idx] = __float2bfloat16_rn(v);
+    out[idx] = f_to_h(v);
   }
 }
 
@@ -805,7 +805,7 @@ struct UpTaps {
   uint32_t mask[256];   // per merged tap (phase blocks in order): bit ty*k+tx set if that tap is summed in
 };
 
-__global__ void k_pack_upsampled_fprop(const float* __restrict__ w, __nv_bfloat16* __restrict__ out, long long per,
+__global__ void k_pack_upsampled_fprop(const float* __restrict__ w, b2h* __restrict__ out, long long per,
                                        int taps, int kk, const UpTaps tab) {
   const long long total = static_cast<long long>(taps) * per;
   for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
@@ -815,7 +815,7 @@ __global__ void k_pack_upsampled_fprop(const float* __restrict__ w, __nv_bfloat1
     float v = 0.f;
     for (int t = 0; t < kk; ++t)
       if (m >> t & 1u) v += w[t * per + e];
-    out[idx] = __float2bfloat16_rn(v);
+    out[idx] = f_to_h(v);
   }
 }
 
@@ -902,8 +902,8 @@ __device__ __forceinline__ void upw_block_sums(const uint32_t (&v)[F + K - 1][F 
 // for W = 1, 256 for W = 2).  32-bit index math and an unpredicated interior path: the kernel is
 // instruction-bound, so wider words amortise the address arithmetic over more channels.
 template <int K, int F, int W>
-__global__ void __launch_bounds__(256) k_upsampled_wgrad_sums(const __nv_bfloat16* __restrict__ dy, int dys, int H,
-                                                              int Wd, int c, __nv_bfloat16* __restrict__ g) {
+__global__ void __launch_bounds__(256) k_upsampled_wgrad_sums(const b2h* __restrict__ dy, int dys, int H,
+                                                              int Wd, int c, b2h* __restrict__ g) {
   constexpr int P = (K - 1) / 2, R = F + K - 1, CPT = 2 * W;
   const int h = H / F, w = Wd / F, cv = c / CPT;
   const int t = blockIdx.x * 256 + threadIdx.x;
@@ -911,9 +911,9 @@ __global__ void __launch_bounds__(256) k_upsampled_wgrad_sums(const __nv_bfloat1
   const int j = t / cv, ch = (t - j * cv) * CPT;
   const int i = blockIdx.y, b = blockIdx.z;
   const int y0 = F * i - (K - 1 - P), x0 = F * j - (K - 1 - P);
-  const __nv_bfloat16* img = dy + static_cast<size_t>(b) * H * Wd * dys + ch;
+  const b2h* img = dy + static_cast<size_t>(b) * H * Wd * dys + ch;
   uint32_t v[R][R][W];
-  auto ld = [&](const __nv_bfloat16* ptr, uint32_t (&dst)[W]) {
+  auto ld = [&](const b2h* ptr, uint32_t (&dst)[W]) {
     if constexpr (W == 2) {
       const uint2 u = __ldg(reinterpret_cast<const uint2*>(ptr));
       dst[0] = u.x;
@@ -923,7 +923,7 @@ __global__ void __launch_bounds__(256) k_upsampled_wgrad_sums(const __nv_bfloat1
     }
   };
   if (y0 >= 0 && y0 + R <= H && x0 >= 0 && x0 + R <= Wd) {
-    const __nv_bfloat16* p0 = img + (static_cast<size_t>(y0) * Wd + x0) * dys;
+    const b2h* p0 = img + (static_cast<size_t>(y0) * Wd + x0) * dys;
 #pragma unroll
     for (int rr = 0; rr < R; ++rr)
 #pragma unroll
@@ -942,7 +942,7 @@ __global__ void __launch_bounds__(256) k_upsampled_wgrad_sums(const __nv_bfloat1
         }
       }
   }
-  __nv_bfloat16* out = g + ((static_cast<size_t>(b) * h + i) * w + j) * (K * K) * c + ch;
+  b2h* out = g + ((static_cast<size_t>(b) * h + i) * w + j) * (K * K) * c + ch;
   // tap (ty, tx) sums rows / cols [K-1-ty, K-1-ty+F) of the loaded window
   float o[K * K][CPT];
   upw_block_sums<K, F, W>(v, o);
@@ -951,7 +951,7 @@ __global__ void __launch_bounds__(256) k_upsampled_wgrad_sums(const __nv_bfloat1
     uint32_t wd[W];
 #pragma unroll
     for (int u = 0; u < W; ++u) {
-      const __nv_bfloat162 hv = __floats2bfloat162_rn(o[q][2 * u], o[q][2 * u + 1]);
+      const b2h2 hv = h2_from(o[q][2 * u], o[q][2 * u + 1]);
       wd[u] = *reinterpret_cast<const uint32_t*>(&hv);
     }
     if constexpr (W == 2)

@@ -26,8 +26,8 @@ __device__ __forceinline__ float ldf<float>(const float* p) {
   return *p;
 }
 template <>
-__device__ __forceinline__ float ldf<__nv_bfloat16>(const __nv_bfloat16* p) {
-  return __bfloat162float(*p);
+__device__ __forceinline__ float ldf<b2h>(const b2h* p) {
+  return h_to_f(*p);
 }
 template <typename T>
 __device__ __forceinline__ void stf(T* p, float v);
@@ -36,8 +36,8 @@ __device__ __forceinline__ void stf<float>(float* p, float v) {
   *p = v;
 }
 template <>
-__device__ __forceinline__ void stf<__nv_bfloat16>(__nv_bfloat16* p, float v) {
-  *p = __float2bfloat16_rn(v);
+__device__ __forceinline__ void stf<b2h>(b2h* p, float v) {
+  *p = f_to_h(v);
 }
 
 struct EwiseP {
@@ -176,7 +176,7 @@ extern "C" int b2dl_ewise(b2dl_act x0, b2dl_act x1, b2dl_act mask, b2dl_act y, c
   if (f32)
     k_ewise<float><<<grid, 256, 0, as_stream(stream)>>>(p);
   else
-    k_ewise<__nv_bfloat16><<<grid, 256, 0, as_stream(stream)>>>(p);
+    k_ewise<b2h><<<grid, 256, 0, as_stream(stream)>>>(p);
   return check_launch();
 }
 
@@ -193,7 +193,7 @@ extern "C" int b2dl_matmul_w(b2dl_act x, const float* b, int ldb, int trans, b2d
   if (f32)
     k_matmul_w<float><<<grid, MM_TJ * MM_TC, 0, as_stream(stream)>>>(p);
   else
-    k_matmul_w<__nv_bfloat16><<<grid, MM_TJ * MM_TC, 0, as_stream(stream)>>>(p);
+    k_matmul_w<b2h><<<grid, MM_TJ * MM_TC, 0, as_stream(stream)>>>(p);
   return check_launch();
 }
 
@@ -205,7 +205,7 @@ extern "C" int b2dl_matmul_w_grad(b2dl_act x, b2dl_act g, float* gb, int accumul
   if (f32)
     k_matmul_w_grad<float><<<grid, 256, 0, as_stream(stream)>>>(p);
   else
-    k_matmul_w_grad<__nv_bfloat16><<<grid, 256, 0, as_stream(stream)>>>(p);
+    k_matmul_w_grad<b2h><<<grid, 256, 0, as_stream(stream)>>>(p);
   return check_launch();
 }
 
@@ -217,7 +217,7 @@ extern "C" int b2dl_channel_sum(b2dl_act g, float* out, int accumulate, int f32,
     k_channel_sum<float><<<cdiv(g.c, 32), 256, 0, as_stream(stream)>>>(static_cast<const float*>(g.ptr), g.c_stride,
                                                                         npix, g.c, out, accumulate);
   else
-    k_channel_sum<__nv_bfloat16><<<cdiv(g.c, 32), 256, 0, as_stream(stream)>>>(
-        static_cast<const __nv_bfloat16*>(g.ptr), g.c_stride, npix, g.c, out, accumulate);
+    k_channel_sum<b2h><<<cdiv(g.c, 32), 256, 0, as_stream(stream)>>>(
+        static_cast<const b2h*>(g.ptr), g.c_stride, npix, g.c, out, accumulate);
   return check_launch();
 }

@@ -60,7 +60,7 @@ int act_map(CUtensorMap* m, const b2dl_act& a, int box_c, int box_w, int box_h, 
   const uint64_t strides[3] = {cs, cs * a.w, cs * a.w * a.h};
   const uint32_t box[4] = {static_cast<uint32_t>(box_c), static_cast<uint32_t>(box_w), static_cast<uint32_t>(box_h),
                            1u};
-  return encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, a.ptr, dims, strides, box, sw);
+  return encode_tiled(m, B2H_TMA, 4, a.ptr, dims, strides, box, sw);
 }
 
 // Strided traversal: a box of bw x bh pixels taken every `stride` pixels in W and H (the TMA
@@ -74,7 +74,7 @@ int act_map_strided(CUtensorMap* m, const b2dl_act& a, int box_c, int box_w, int
   const uint32_t box[4] = {static_cast<uint32_t>(box_c), static_cast<uint32_t>(box_w * stride),
                            static_cast<uint32_t>(box_h * stride), 1u};
   const uint32_t es[4] = {1u, static_cast<uint32_t>(stride), static_cast<uint32_t>(stride), 1u};
-  return encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, a.ptr, dims, strides, box, sw, es);
+  return encode_tiled(m, B2H_TMA, 4, a.ptr, dims, strides, box, sw, es);
 }
 
 // Phase view of a full-resolution NHWC tensor: pixel (i, j) of the (h/f, w/f) view is pixel
@@ -88,7 +88,7 @@ int act_map_phase(CUtensorMap* m, const b2dl_act& a, int f, int ph, int pw, int 
   const uint32_t box[4] = {static_cast<uint32_t>(box_c), static_cast<uint32_t>(box_w), static_cast<uint32_t>(box_h),
                            1u};
   char* base = static_cast<char*>(a.ptr) + (static_cast<uint64_t>(ph) * a.w + pw) * cs;
-  return encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, sw);
+  return encode_tiled(m, B2H_TMA, 4, base, dims, strides, box, sw);
 }
 
 // Row-window view of a haloed NHWC image (conv window mode): virtual pixel (y, xx) holds the
@@ -102,7 +102,7 @@ int window_map(CUtensorMap* m, const b2dl_act& x, int c_v, int w_v, int box_c, i
   const uint64_t strides[3] = {ps, ps * x.w, ps * x.w * x.h};
   const uint32_t box[4] = {static_cast<uint32_t>(box_c), static_cast<uint32_t>(box_w), static_cast<uint32_t>(box_h),
                            1u};
-  return encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, x.ptr, dims, strides, box, sw);
+  return encode_tiled(m, B2H_TMA, 4, x.ptr, dims, strides, box, sw);
 }
 
 // 5-D map (64-channel inner, W, H, N, channel block): one box = g chunks of [pixels][64 ch],
@@ -114,12 +114,12 @@ int act_map5(CUtensorMap* m, const b2dl_act& a, int box_w, int box_h, int g) {
   const uint64_t strides[4] = {cs, cs * a.w, cs * a.w * a.h, 128u};
   const uint32_t box[5] = {64u, static_cast<uint32_t>(box_w), static_cast<uint32_t>(box_h), 1u,
                            static_cast<uint32_t>(g)};
-  return encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, a.ptr, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+  return encode_tiled(m, B2H_TMA, 5, a.ptr, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
 // -------------------------------------------------------------- layout kernels
 // OIHW fp32 -> fprop packed bf16 [cout][taps][cin_pad]  (zero padded)
-__global__ void pack_oihw_fprop(const float* __restrict__ w, __nv_bfloat16* __restrict__ out, int cout, int cin,
+__global__ void pack_oihw_fprop(const float* __restrict__ w, b2h* __restrict__ out, int cout, int cin,
                                 int taps, int cin_pad) {
   long long total = static_cast<long long>(cout) * taps * cin_pad;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
@@ -129,11 +129,11 @@ __global__ void pack_oihw_fprop(const float* __restrict__ w, __nv_bfloat16* __re
     int t = static_cast<int>(r % taps);
     int co = static_cast<int>(r / taps);
     float v = ci < cin ? w[(static_cast<long long>(co) * cin + ci) * taps + t] : 0.f;
-    out[i] = __float2bfloat16_rn(v);
+    out[i] = f_to_h(v);
   }
 }
 // OIHW fp32 -> dgrad packed bf16 [cin][taps flipped][cout_pad]
-__global__ void pack_oihw_dgrad(const float* __restrict__ w, __nv_bfloat16* __restrict__ out, int cout, int cin,
+__global__ void pack_oihw_dgrad(const float* __restrict__ w, b2h* __restrict__ out, int cout, int cin,
                                 int taps, int cout_pad) {
   long long total = static_cast<long long>(cin) * taps * cout_pad;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
@@ -144,7 +144,7 @@ __global__ void pack_oihw_dgrad(const float* __restrict__ w, __nv_bfloat16* __re
     int ci = static_cast<int>(r / taps);
     int t = taps - 1 - tf;  // 180-degree rotation of the kernel window
     float v = co < cout ? w[(static_cast<long long>(co) * cin + ci) * taps + t] : 0.f;
-    out[i] = __float2bfloat16_rn(v);
+    out[i] = f_to_h(v);
   }
 }
 // HWIO fp32 -> OIHW fp32
@@ -234,7 +234,7 @@ extern "C" int b2dl_conv2d_forward(const float* x, const float* w, float* y, int
   int rc = b2dl_nchw_to_nhwc(x, xa, 0, stream);
   if (rc) return rc;
   long long tot = static_cast<long long>(cout) * taps * b2dl_cin_pad(cin);
-  pack_oihw_fprop<<<grid_for(tot), 256, 0, st>>>(w, reinterpret_cast<__nv_bfloat16*>(wp), cout, cin, taps,
+  pack_oihw_fprop<<<grid_for(tot), 256, 0, st>>>(w, reinterpret_cast<b2h*>(wp), cout, cin, taps,
                                                  b2dl_cin_pad(cin));
   if ((rc = check_launch())) return rc;
   b2dl_conv_args a{};
@@ -268,7 +268,7 @@ extern "C" int b2dl_conv2d_backward_input(const float* dy, const float* w, float
   int rc = b2dl_nchw_to_nhwc(dy, dya, 0, stream);
   if (rc) return rc;
   long long tot = static_cast<long long>(cin) * taps * b2dl_cin_pad(cout);
-  pack_oihw_dgrad<<<grid_for(tot), 256, 0, st>>>(w, reinterpret_cast<__nv_bfloat16*>(wp), cout, cin, taps,
+  pack_oihw_dgrad<<<grid_for(tot), 256, 0, st>>>(w, reinterpret_cast<b2h*>(wp), cout, cin, taps,
                                                  b2dl_cin_pad(cout));
   if ((rc = check_launch())) return rc;
   b2dl_conv_args a{};

@@ -7,6 +7,7 @@
 #include <cstdio>
 
 #include "../../include/b2dl.h"
+#include "half.cuh"
 
 namespace b2 {
 

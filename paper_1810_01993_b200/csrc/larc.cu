@@ -84,7 +84,7 @@ __global__ void k_larc_rates(const double* __restrict__ part, int ntensors, int 
 
 // w, m, g segment update, 4 elements per thread on aligned interiors; optionally also
 // writes the bf16 mirror of w that the conv kernels read as their weight operand.
-__device__ __forceinline__ void larc_one(float* w, float* m, const float* g, __nv_bfloat16* wb, int64_t i, float r,
+__device__ __forceinline__ void larc_one(float* w, float* m, const float* g, b2h* wb, int64_t i, float r,
                                          float beta, float wd, float gs) {
   float mv = m[i] * beta;
   mv += g[i] * gs;
@@ -93,11 +93,11 @@ __device__ __forceinline__ void larc_one(float* w, float* m, const float* g, __n
   m[i] = mv;
   const float nw = wv - r * mv;
   w[i] = nw;
-  if (wb) wb[i] = __float2bfloat16_rn(nw);
+  if (wb) wb[i] = f_to_h(nw);
 }
 
 __global__ void k_larc_apply(float* __restrict__ w, float* __restrict__ m, const float* __restrict__ g,
-                             __nv_bfloat16* __restrict__ wb, const int64_t* __restrict__ off,
+                             b2h* __restrict__ wb, const int64_t* __restrict__ off,
                              const float* __restrict__ lr_t, float beta, float wd, float grad_scale,
                              const int* __restrict__ status, int cast_only) {
   if (*status) return;
@@ -110,7 +110,7 @@ __global__ void k_larc_apply(float* __restrict__ w, float* __restrict__ m, const
   if (a0 >= a1) {
     for (int64_t i = lo + tid; i < hi; i += nth) {
       if (cast_only)
-        wb[i] = __float2bfloat16_rn(w[i]);
+        wb[i] = f_to_h(w[i]);
       else
         larc_one(w, m, g, wb, i, r, beta, wd, grad_scale);
     }
@@ -118,13 +118,13 @@ __global__ void k_larc_apply(float* __restrict__ w, float* __restrict__ m, const
   }
   for (int64_t i = lo + tid; i < a0; i += nth) {
     if (cast_only)
-      wb[i] = __float2bfloat16_rn(w[i]);
+      wb[i] = f_to_h(w[i]);
     else
       larc_one(w, m, g, wb, i, r, beta, wd, grad_scale);
   }
   for (int64_t i = a1 + tid; i < hi; i += nth) {
     if (cast_only)
-      wb[i] = __float2bfloat16_rn(w[i]);
+      wb[i] = f_to_h(w[i]);
     else
       larc_one(w, m, g, wb, i, r, beta, wd, grad_scale);
   }
@@ -148,7 +148,7 @@ __global__ void k_larc_apply(float* __restrict__ w, float* __restrict__ m, const
       reinterpret_cast<float4*>(w)[v] = wv;
     }
     if (wb) {
-      __nv_bfloat162 lo2 = __floats2bfloat162_rn(wv.x, wv.y), hi2 = __floats2bfloat162_rn(wv.z, wv.w);
+      b2h2 lo2 = h2_from(wv.x, wv.y), hi2 = h2_from(wv.z, wv.w);
       uint2 u;
       u.x = *reinterpret_cast<uint32_t*>(&lo2);
       u.y = *reinterpret_cast<uint32_t*>(&hi2);
@@ -184,7 +184,7 @@ extern "C" int b2dl_larc_update(const b2dl_larc_args* a, void* stream) {
         a->status);
   }
   if (a->mode == 1) return check_launch();
-  k_larc_apply<<<grid, 256, 0, st>>>(a->w, a->m, a->g, reinterpret_cast<__nv_bfloat16*>(a->w_bf16), a->offsets,
+  k_larc_apply<<<grid, 256, 0, st>>>(a->w, a->m, a->g, reinterpret_cast<b2h*>(a->w_bf16), a->offsets,
                                      a->lr_out, a->momentum, a->weight_decay, a->grad_scale, a->status,
                                      a->mode == 3);
   return check_launch();

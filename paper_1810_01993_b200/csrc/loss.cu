@@ -62,8 +62,8 @@ __global__ void k_wce_hist(const uint8_t* __restrict__ labels, long long hw, int
 
 __global__ void k_wce_main(const float* __restrict__ logits, int ls, const uint8_t* __restrict__ labels,
                            const float* __restrict__ cw, const int* __restrict__ counts, long long hw, int classes,
-                           int nimg, void* __restrict__ dl, int ds, int dl_f32, uint8_t* __restrict__ pred,
-                           double* __restrict__ part) {
+                           int nimg, void* __restrict__ dl, int ds, int dl_f32, float dl_scale,
+                           uint8_t* __restrict__ pred, double* __restrict__ part) {
   const int img = blockIdx.y;
   __shared__ float s_w[WCE_MAX_CLASSES];
   __shared__ float s_scale;
@@ -72,7 +72,7 @@ __global__ void k_wce_main(const float* __restrict__ logits, int ls, const uint8
   if (threadIdx.x == 0) {
     double ws = 0.0;
     for (int c = 0; c < classes; ++c) ws += static_cast<double>(counts[img * classes + c]) * cw[c];
-    s_scale = static_cast<float>(1.0 / (ws * nimg));
+    s_scale = static_cast<float>(dl_scale / (ws * nimg));   // dl_scale: the fp16 build's loss scale
   }
   __syncthreads();
   const float scale = s_scale;
@@ -111,12 +111,12 @@ __global__ void k_wce_main(const float* __restrict__ logits, int ls, const uint8
     acc += static_cast<double>(wy) * nll;
     const float gs = wy * scale;
     if (vec8) {  // bf16 dlogits padded to 8 channels: one 16-byte store per pixel
-      __align__(16) __nv_bfloat16 g8[8];
+      __align__(16) b2h g8[8];
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         float g = 0.f;
         if (c < classes) g = (__expf(zv[c] - mx - lse) - (c == y ? 1.f : 0.f)) * gs;
-        g8[c] = __float2bfloat16_rn(g);
+        g8[c] = f_to_h(g);
       }
       reinterpret_cast<uint4*>(dl)[p] = *reinterpret_cast<const uint4*>(g8);
     } else {
@@ -128,7 +128,7 @@ __global__ void k_wce_main(const float* __restrict__ logits, int ls, const uint8
         if (dl_f32)
           reinterpret_cast<float*>(dl)[p * ds + c] = g;
         else
-          reinterpret_cast<__nv_bfloat16*>(dl)[p * ds + c] = __float2bfloat16_rn(g);
+          reinterpret_cast<b2h*>(dl)[p * ds + c] = f_to_h(g);
       }
     }
     if (pred) pred[p] = static_cast<uint8_t>(am);
@@ -179,7 +179,8 @@ extern "C" size_t b2dl_wce_workspace_size(int n, int h, int w, int classes) {
 }
 
 extern "C" int b2dl_wce(b2dl_act logits, const uint8_t* labels, const float* class_weights, int classes,
-                        float* loss_out, int* counts, b2dl_act dlogits, int dlogits_f32, uint8_t* pred,
+                        float* loss_out, int* counts, b2dl_act dlogits, int dlogits_f32, float dlogits_scale,
+                        uint8_t* pred,
                         int* status, void* workspace, size_t workspace_bytes, void* stream) {
   if (classes < 2 || classes > WCE_MAX_CLASSES || logits.c != classes || dlogits.c != classes) return B2DL_E_VALUE;
   if (!logits.ptr || !labels || !class_weights || !loss_out || !counts || !dlogits.ptr) return B2DL_E_VALUE;
@@ -196,6 +197,7 @@ extern "C" int b2dl_wce(b2dl_act logits, const uint8_t* labels, const float* cla
   k_wce_hist<<<grid, WCE_THREADS, 0, st>>>(labels, hw, classes, counts, err);
   k_wce_main<<<grid, WCE_THREADS, 0, st>>>(reinterpret_cast<const float*>(logits.ptr), logits.c_stride, labels, class_weights,
                                    counts, hw, classes, logits.n, dlogits.ptr, dlogits.c_stride, dlogits_f32,
+                                   dlogits_scale,
                                    pred, part);
   k_wce_final<<<1, 32, 0, st>>>(part, nb, counts, class_weights, classes, logits.n, loss_out, err, status);
   return check_launch();

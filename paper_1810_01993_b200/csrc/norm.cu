@@ -23,22 +23,22 @@ namespace b2 {
 template <typename T, int V>
 struct Vec;
 template <>
-struct Vec<__nv_bfloat16, 8> {
-  static __device__ __forceinline__ void load(const __nv_bfloat16* p, float* v) {
+struct Vec<b2h, 8> {
+  static __device__ __forceinline__ void load(const b2h* p, float* v) {
     const uint4 u = *reinterpret_cast<const uint4*>(p);
     const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      v[2 * e] = __uint_as_float(w[e] << 16);
-      v[2 * e + 1] = __uint_as_float(w[e] & 0xFFFF0000u);
+      v[2 * e] = h_lo(w[e]);
+      v[2 * e + 1] = h_hi(w[e]);
     }
   }
-  static __device__ __forceinline__ void store(__nv_bfloat16* p, const float* v) {
+  static __device__ __forceinline__ void store(b2h* p, const float* v) {
     uint4 u;
     uint32_t* w = reinterpret_cast<uint32_t*>(&u);
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+      const b2h2 h = h2_from(v[2 * e], v[2 * e + 1]);
       w[e] = *reinterpret_cast<const uint32_t*>(&h);
     }
     *reinterpret_cast<uint4*>(p) = u;
@@ -63,9 +63,9 @@ struct Vec<T, 1> {
   static __device__ __forceinline__ void store(T* p, const float* v) { *p = static_cast<T>(v[0]); }
 };
 template <>
-struct Vec<__nv_bfloat16, 1> {
-  static __device__ __forceinline__ void load(const __nv_bfloat16* p, float* v) { v[0] = __bfloat162float(*p); }
-  static __device__ __forceinline__ void store(__nv_bfloat16* p, const float* v) { *p = __float2bfloat16_rn(v[0]); }
+struct Vec<b2h, 1> {
+  static __device__ __forceinline__ void load(const b2h* p, float* v) { v[0] = h_to_f(*p); }
+  static __device__ __forceinline__ void store(b2h* p, const float* v) { *p = f_to_h(v[0]); }
 };
 
 constexpr int BN_THREADS = 256;
@@ -489,11 +489,11 @@ static size_t bn_red_smem(int c, int v) {
       }                                             \
     } else {                                        \
       if (VEC) {                                    \
-        using T = __nv_bfloat16;                    \
+        using T = b2h;                    \
         constexpr int V = 8;                        \
         __VA_ARGS__;                                \
       } else {                                      \
-        using T = __nv_bfloat16;                    \
+        using T = b2h;                    \
         constexpr int V = 1;                        \
         __VA_ARGS__;                                \
       }                                             \

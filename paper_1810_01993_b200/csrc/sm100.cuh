@@ -283,22 +283,19 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo_byte
   return d;
 }
 
-// Instruction descriptor, kind::f16 with bf16 A/B and fp32 D.
+// Instruction descriptor, kind::f16 with bf16 (or, in the f16 build, fp16) A/B and fp32 D.
 //   [4,6) c_format (1=F32) [7,10) a_format (1=BF16) [10,13) b_format (1=BF16)
 //   [15] a_major (0=K,1=MN) [16] b_major  [17,23) N>>3  [24,29) M>>4
 __host__ __device__ constexpr uint32_t make_idesc_bf16(int M, int N, bool a_mn_major, bool b_mn_major) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn_major ? 1u : 0u) << 15) | ((b_mn_major ? 1u : 0u) << 16) |
+  return (1u << 4) | (B2H_MMA_FMT << 7) | (B2H_MMA_FMT << 10) | ((a_mn_major ? 1u : 0u) << 15) | ((b_mn_major ? 1u : 0u) << 16) |
          ((static_cast<uint32_t>(N) >> 3) << 17) | ((static_cast<uint32_t>(M) >> 4) << 24);
 }
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
-__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
-  uint32_t r;
-  asm("cvt.rn.bf16x2.f32 %0, %2, %1;" : "=r"(r) : "f"(a), "f"(b));
-  return r;
-}
-__device__ __forceinline__ float bf16lo(uint32_t v) { return __uint_as_float(v << 16); }
-__device__ __forceinline__ float bf16hi(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }
+// 16-bit storage helpers (bf16, or fp16 in the -DB2DL_F16 build; half.cuh)
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) { return pack_h2(a, b); }
+__device__ __forceinline__ float bf16lo(uint32_t v) { return h_lo(v); }
+__device__ __forceinline__ float bf16hi(uint32_t v) { return h_hi(v); }
 
 }  // namespace b2

@@ -33,7 +33,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from . import nhwc
+from . import _lib, nhwc
 from .graph import OpGraph, infer_shapes
 from .nhwc import View
 
@@ -422,6 +422,15 @@ class Plan:
         self.relu_passes = sum(1 for st in prog if st.get("relu_pass"))
 
 
+def _in_lib(fn):
+    """Run an Engine method's launches on the engine's build (bf16 or fp16 storage)."""
+    def wrapped(self, *a, **k):
+        with _lib.use(self.half):
+            return fn(self, *a, **k)
+    wrapped.__name__, wrapped.__doc__ = fn.__name__, fn.__doc__
+    return wrapped
+
+
 def conv_event_totals(events, by_pass=False):
     """Sum (ms, FLOPs) over recorded (start, end, FLOPs, pass) conv events."""
     if not by_pass:
@@ -438,8 +447,8 @@ class Engine:
 
     def __init__(self, graph: OpGraph, params: dict, param_order, input_shape, loss_name, logits_name,
                  device="cuda", precision="bf16"):
-        if precision not in ("bf16", "fp32"):
-            raise ValueError(f"precision must be 'bf16' or 'fp32', not {precision!r}")
+        if precision not in ("bf16", "fp16", "fp32"):
+            raise ValueError(f"precision must be 'bf16', 'fp16' or 'fp32', not {precision!r}")
         # fp32: the parity mode -- fp32 NHWC buffers, fp32 HWIO weights, CUDA-core kernels
         # (b2dl.h group 3); same program, same fusion points
         self.fp32 = precision == "fp32"
@@ -450,7 +459,11 @@ class Engine:
                          logits_name)
         p = self.plan
         self.ws = nhwc.Workspace(self.device)
-        bf, f32 = torch.bfloat16, torch.float32
+        # 16-bit storage: bf16 (libb2dl.so) or IEEE fp16 (libb2dl_f16.so, same kernels, kind::f16
+        # MMAs on f16 operands; config 4's FP16); every launch of this engine goes to its build
+        self.half = "fp16" if precision == "fp16" else "bf16"
+        bf, f32 = (torch.float16 if precision == "fp16" else torch.bfloat16), torch.float32
+        self.hdt = bf
         adt = f32 if self.fp32 else bf
         self.act = {r: torch.empty((n, h, w, c), dtype=f32 if isf else adt, device=self.device)
                     for r, (n, h, w, c, isf) in p.buffers.items()}
@@ -528,7 +541,7 @@ class Engine:
                         and o.out != p.logits_name and o is not self.win and o.w not in self.wf):
                     self.up_fprop[o.out] = up
                     self.wupf[o.w] = torch.zeros(nhwc.upsampled_fprop_taps(o.k, up.factor) * o.cin * o.cout,
-                                                 dtype=torch.bfloat16, device=self.device)
+                                                 dtype=self.hdt, device=self.device)
         # ... and its weight gradient: x_low^T (shifted f x f block sums of dy), one 1x1 wgrad at the
         # low resolution (b2dl_upsampled_wgrad_sums / _reduce).  With all three the upsampled
         # tensor itself is never formed.
@@ -539,7 +552,7 @@ class Engine:
                 if up is not None and o.k in (1, 3) and up.factor in (2, 4):
                     n_, _, h_, w_ = p.shapes[up.ins[0]]
                     self.up_wgrad[o.out] = up
-                    self.gsum[o.w] = torch.empty(n_ * h_ * w_ * o.k * o.k * o.cout, dtype=torch.bfloat16,
+                    self.gsum[o.w] = torch.empty(n_ * h_ * w_ * o.k * o.k * o.cout, dtype=self.hdt,
                                                  device=self.device)
         self.dead_up = {self.up_fprop[o].out for o in self.up_wgrad if o in self.up_dgrad}
         # Batch norm after a conv: the conv's TMA epilogue emits per-tile channel sums and sums of
@@ -630,6 +643,11 @@ class Engine:
         # 1 after a step whose labels were outside [0, classes) (its loss is NaN)
         self.label_status = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.input_shape = tuple(input_shape)
+        # fp16 storage: a static loss scale keeps the per-pixel dlogits (~1 / (N H W), 2.6e-7 at
+        # 2 x 1152 x 768) out of fp16's subnormals; every weight gradient is divided by it again in
+        # the update (and on export).  A power of two, so the scaling is exact.
+        self.loss_scale = (float(2 ** max(0, int(np.log2(max(1.0, n * h * w / 16.0)))))
+                           if self.half == "fp16" and not self.fp32 else 1.0)
         self.launches = 0
         self.conv_timing = False
         # side stream for wgrad || dgrad overlap (B2DL_CONCURRENT=0 serialises them)
@@ -662,7 +680,7 @@ class Engine:
             kk = o.k + up.factor - 1
             self.up_dgrad[o.out] = (up, nxt)
             self.skip_up.add(up.out)
-            self.wup[o.w] = torch.zeros((o.cin, kk * kk, nhwc.cin_pad(o.cout)), dtype=torch.bfloat16,
+            self.wup[o.w] = torch.zeros((o.cin, kk * kk, nhwc.cin_pad(o.cout)), dtype=self.hdt,
                                         device=self.device)
 
     def bias_of(self, op):
@@ -760,6 +778,7 @@ class Engine:
         return (self.flat_w if buf is None else buf)[off:off + int(np.prod(shp))]
 
     # ---------------------------------------------------------------- params
+    @_in_lib
     def load_params(self, params: dict):
         for name in self.order:
             a = np.asarray(params[name], dtype=np.float32)
@@ -792,12 +811,16 @@ class Engine:
             self.wslice(name, buf).copy_(a.reshape(-1).to(self.device))
 
     def export_grads(self) -> dict:
-        return self._export(self.flat_g)
+        g = self._export(self.flat_g)
+        if self.loss_scale != 1.0:
+            g = {k: v / np.float32(self.loss_scale) for k, v in g.items()}
+        return g
 
     def wmaster(self, name):
         off, shp = self.slot[name]
         return self.flat_wbf[off:off + int(np.prod(shp))]
 
+    @_in_lib
     def refresh_mirror(self):
         """bf16 mirror <- flat fp32 parameters (after loading weights from the host)."""
         if self.fp32:
@@ -806,6 +829,7 @@ class Engine:
                          self._lr_scratch, self._status, self.ws, mode=3, w_bf16=self.flat_wbf)
         self.launches += 1
 
+    @_in_lib
     def repack(self, mirror=True):
         """Refresh the weight operands after an update; the LARC kernel already writes the mirror
         during training (mirror=False), leaving only the packed copies of ragged-channel convs."""
@@ -830,6 +854,7 @@ class Engine:
                 self.launches += 1
 
     # ---------------------------------------------------------------- inputs
+    @_in_lib
     def set_batch(self, x_nchw: torch.Tensor, labels: torch.Tensor):
         """x fp32 NCHW and labels uint8 [N,H,W] already on the device."""
         if tuple(x_nchw.shape) != self.input_shape:
@@ -845,6 +870,7 @@ class Engine:
         self.class_weights.copy_(torch.as_tensor(np.asarray(w, dtype=np.float32)))
 
     # ---------------------------------------------------------------- forward
+    @_in_lib
     def forward(self):
         """Fused forward program.  Runs of convs reading the same input (the ASPP branches) are
         spread over the main and side streams so their tail waves overlap."""
@@ -972,7 +998,8 @@ class Engine:
             nhwc.matmul_w(self.v(op.ins[0]), self.wslice(op.w), self.v(op.out), f32=self.fp32)
         elif op.kind == "ce":
             nhwc.wce(self.v(op.ins[0]), self.labels, self.class_weights, self.loss, self.counts,
-                     self.gv(op.ins[0]), self.pred, self.ws, dlogits_f32=self.fp32, status=self.label_status)
+                     self.gv(op.ins[0]), self.pred, self.ws, dlogits_f32=self.fp32, status=self.label_status,
+                     dlogits_scale=self.loss_scale)
             self.launches += 2   # histogram + loss/dlogits + final fold (3 with the +1 below)
         self.launches += 1
 
@@ -1031,6 +1058,7 @@ class Engine:
         if any(op.w.startswith(p) for p in pref.split(",")):
             torch.cuda._sleep(int(us * 1900))   # ~1.9 cycles per ns at the boost clock
 
+    @_in_lib
     def backward(self, on_bucket_ready=None):
         """Fill flat_g with d loss / d params (param layout HWIO for conv weights).
 
@@ -1233,6 +1261,7 @@ class Engine:
     def _add(self, x, y, accumulate=False, mask=None):
         (nhwc.f32_add if self.fp32 else nhwc.add)(x, y, accumulate=accumulate, mask=mask)
 
+    @_in_lib
     def logits_nchw(self) -> torch.Tensor:
         n, c, h, w = self.plan.shapes[self.plan.logits_name]
         out = torch.empty((n, c, h, w), dtype=torch.float32, device=self.device)

@@ -350,14 +350,15 @@ def bias_grad(g: View, out: torch.Tensor, ws: Workspace, accumulate=False):
 
 def wce(logits: View, labels: torch.Tensor, class_weights: torch.Tensor, loss_out: torch.Tensor,
         counts: torch.Tensor, dlogits: View, pred: torch.Tensor | None, ws: Workspace, dlogits_f32=False,
-        status: torch.Tensor | None = None):
+        status: torch.Tensor | None = None, dlogits_scale: float = 1.0):
     n, h, w, c = logits.shape
     need = LIB.b2dl_wce_workspace_size(n, h, w, c)
     buf = ws.get(need)
     check(LIB.b2dl_wce(logits.act(), ctypes.c_void_p(labels.data_ptr()),
                        ctypes.c_void_p(class_weights.data_ptr()), c,
                        ctypes.c_void_p(loss_out.data_ptr()), ctypes.c_void_p(counts.data_ptr()),
-                       dlogits.act(), int(dlogits_f32), _ptr(pred), _ptr(status), ctypes.c_void_p(buf.data_ptr()),
+                       dlogits.act(), int(dlogits_f32), float(dlogits_scale), _ptr(pred), _ptr(status),
+                       ctypes.c_void_p(buf.data_ptr()),
                        buf.numel(), _stream()), "wce")
 
 

@@ -27,7 +27,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from . import nhwc
+from . import _lib, nhwc
 from .flops import count_graph, train_flops_per_sample
 from .loss import ClassWeights, uniform_weights
 from .models import NetConfig
@@ -157,9 +157,10 @@ class DataParallelTrainer:
         eng = self.eng
         o = self.optim
         # LARC + momentum update; the same pass writes the bf16 weight mirror the convs read
-        nhwc.larc_update(eng.flat_w, eng.flat_m, g, eng.offsets, o.lr, o.momentum, o.trust, o.weight_decay,
-                         o.eps, 1.0 / self.world, self.lr_out, self.status, eng.ws,
-                         w_bf16=None if eng.fp32 else eng.flat_wbf)
+        with _lib.use(eng.half):   # the mirror is written in the engine's 16-bit type
+            nhwc.larc_update(eng.flat_w, eng.flat_m, g, eng.offsets, o.lr, o.momentum, o.trust, o.weight_decay,
+                             o.eps, 1.0 / (self.world * eng.loss_scale), self.lr_out, self.status, eng.ws,
+                             w_bf16=None if eng.fp32 else eng.flat_wbf)
         eng.launches += 3
         eng.repack(mirror=False)
 
@@ -323,7 +324,7 @@ class DataParallelTrainer:
         # the pending lag-1 gradient is the rank SUM (the 1/P is applied in the update): export
         # the mean so the state is independent of the number of ranks that wrote it
         return {"params": eng.export_params(), "momentum": eng._export(eng.flat_m),
-                "lag_grad": ({k: v / np.float32(self.world) for k, v in eng._export(eng.flat_g).items()}
+                "lag_grad": ({k: v / np.float32(self.world * eng.loss_scale) for k, v in eng._export(eng.flat_g).items()}
                              if pending else None),
                 "steps": self.steps_done, "have_prev": bool(pending), "world": self.world}
 
@@ -337,7 +338,7 @@ class DataParallelTrainer:
                 raise ValueError("state carries a pending lag-1 gradient but the trainer has lag 0")
             # mean -> this run's rank sum (bitwise when the world sizes match: x / P * P with P a
             # power of two is exact)
-            eng.import_flat(eng.flat_g, {k: np.asarray(v, np.float32) * np.float32(self.world)
+            eng.import_flat(eng.flat_g, {k: np.asarray(v, np.float32) * np.float32(self.world * eng.loss_scale)
                                          for k, v in st["lag_grad"].items()})
         self.have_prev = bool(st.get("have_prev")) and self.lag == 1
         self.steps_done = int(st.get("steps", 0))
@@ -390,7 +391,7 @@ class RunConfig:
     scene: SceneConfig = field(default_factory=SceneConfig)
     class_weighting: str = "inv_sqrt"
     hash_steps: tuple = ()
-    precision: str = "bf16"   # "fp32": the parity mode (b2dl.h group 3)
+    precision: str = "bf16"   # "fp16": IEEE-half storage (libb2dl_f16.so); "fp32": the parity mode (group 3)
     hierarchy: tuple | None = None   # (groups, per_group): three-stage hierarchical all-reduce
     prefetch_workers: int = 0        # > 0: scenes made by a W-worker bounded prefetch pipeline
     prefetch_capacity: int = 4

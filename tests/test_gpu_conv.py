@@ -385,3 +385,29 @@ def test_upsampled_wgrad_sums_vs_torch(c):
                        for ty in range(k) for tx in range(k)], 1)      # [n, taps, c, h, w]
     ref = ref.permute(0, 3, 4, 1, 2)                                   # [n, h, w, taps, c]
     assert _rel(g.view(ref.shape), ref) < 1e-2
+
+
+@pytest.mark.parametrize("c32,k,cout", [(32, 5, 48), (24, 3, 256), (32, 1, 64)])
+def test_kblk32_fprop_and_dgrad_vs_fp64(c32, k, cout):
+    """17..32-channel inputs through the master-weight modes use 32-channel K blocks (SW64): the
+    forward over a growth-32 tensor and the dgrad over a 32-channel dy (Tiramisu dense layers)."""
+    from paper_1810_01993_b200 import nhwc
+    torch.manual_seed(5)
+    n, h, w = 2, 24, 40
+    x = torch.randn(n, h, w, c32, device="cuda").to(torch.bfloat16)
+    wm = (torch.randn(k * k, c32, cout, device="cuda") / (k * k * c32) ** 0.5).to(torch.bfloat16)
+    y = torch.empty(n, h, w, cout, dtype=torch.bfloat16, device="cuda")
+    nhwc.conv_fprop(nhwc.View(x), None, cout, k, k, 1, nhwc.View(y), w_master=wm, w_mode=1)
+    xr = x.permute(0, 3, 1, 2).double()
+    wr = wm.double().view(k, k, c32, cout).permute(3, 2, 0, 1)
+    ref = F.conv2d(xr, wr, padding=(k - 1) // 2)
+    assert _rel(y.permute(0, 3, 1, 2), ref) < 1e-2
+    # dgrad over a 32-channel dy: this conv maps cout -> c32; dx has c32... use (co=c32, ci=cout)
+    dy = torch.randn(n, h, w, c32, device="cuda").to(torch.bfloat16)
+    wd = (torch.randn(k * k, cout, c32, device="cuda") / (k * k * c32) ** 0.5).to(torch.bfloat16)  # HWIO cin=cout
+    dx = torch.empty(n, h, w, cout, dtype=torch.bfloat16, device="cuda")
+    nhwc.conv_dgrad(nhwc.View(dy), None, cout, k, k, 1, nhwc.View(dx), w_master=wd)
+    xg = torch.zeros(n, cout, h, w, dtype=torch.float64, device="cuda", requires_grad=True)
+    F.conv2d(xg, wd.double().view(k, k, cout, c32).permute(3, 2, 0, 1), padding=(k - 1) // 2).backward(
+        dy.permute(0, 3, 1, 2).double())
+    assert _rel(dx.permute(0, 3, 1, 2), xg.grad) < 1e-2
