@@ -1077,6 +1077,134 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
   }
 }
 
+// ------------------------------------------------------------------ row-tap fprop (narrow N)
+// Narrow-output convs (N = BN <= 64, e.g. the growth-32 5x5 dense layers of the Tiramisu): with one
+// 128-pixel box per (tap, K block) the operand loads, not the MMAs, bound the kernel (each input
+// element crosses L2 -> SM kh*kw times for only 2*BN FLOPs per byte).  Here an 8 x 16-pixel tile
+// loads, per (column tap j, 64-channel block), ONE tall box of 8 x (16 + (kh-1) dil) pixels and
+// the kh row taps address it at i*dil KB offsets (one SW128 atom per image row of 8 pixels), with
+// the kh weight boxes of that column streamed in the same stage: kh times fewer activation loads.
+constexpr int RT_BW = 8, RT_BH = 16;
+
+template <int BN>
+__global__ void __launch_bounds__(FPROP_THREADS, 1)
+    conv_rowtap_fprop_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                             const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmR,
+                             const __grid_constant__ CUtensorMap tmM, const FpropParams p, int kh) {
+  const int a_stage = (RT_BH + (kh - 1) * p.dil) * RT_BW * 128;
+  const int b_box = BN * 64 * 2;
+  const int stage_bytes = a_stage + kh * b_box;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* sS = smem;   // stages: [A tall box][kh weight boxes]
+  uint8_t* epi = sS + p.stages * stage_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi + p.epi_bytes);
+  uint64_t* empty = full + FPROP_MAX_STAGES;
+  uint64_t* tfull = empty + FPROP_MAX_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* inbar = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(inbar + 16);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = lane_id();
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 8);
+    }
+    for (int s = 0; s < 16; ++s) mbar_init(&inbar[s], 1);
+    tma_prefetch(&tmY);
+    if (p.res) tma_prefetch(&tmR);
+    if (p.mask) tma_prefetch(&tmM);
+    fence_barrier_init();
+  }
+  constexpr uint32_t TCOLS = tmem_cols_for(2 * BN);
+  if (warp == 1) tmem_alloc(tmem_slot, TCOLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  griddep_launch_dependents();
+  griddep_wait();
+  const int per_img = p.tiles_x * p.tiles_y;
+  const int nsteps = p.kw * p.num_cblk;   // (column tap, channel block) stages per tile
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        const int img = tile / per_img, r = tile - img * per_img;
+        const int ty = r / p.tiles_x, tx = r - ty * p.tiles_x;
+        for (int st = 0; st < nsteps; ++st) {
+          const int j = st / p.num_cblk, cb = st - j * p.num_cblk;
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], stage_bytes);
+          uint8_t* dst = sS + stage * stage_bytes;
+          tma_load_4d(dst, &tmA, &full[stage], cb * 64, tx * RT_BW + j * p.dil - p.pad_left, ty * RT_BH - p.pad_top,
+                      img);
+          for (int i = 0; i < kh; ++i)
+            tma_load_2d(dst + a_stage + i * b_box, &tmB, &full[stage], (i * p.kw + j) * p.cin_pad + cb * 64, 0);
+          if (++stage == p.stages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc_bf16(BM, BN, false, false);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++it) {
+        const int as = it & 1;
+        const uint32_t ap = (it >> 1) & 1;
+        mbar_wait(&tempty[as], ap ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + as * BN;
+        for (int st = 0; st < nsteps; ++st) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sS + stage * stage_bytes);
+          const uint64_t ad0 = make_sdesc(a0, 16, 1024, LAYOUT_SW128);
+          const uint64_t bd0 = make_sdesc(a0 + a_stage, 16, 1024, LAYOUT_SW128);
+          for (int i = 0; i < kh; ++i) {
+            // row tap i: the tall box shifted down i*dil image rows (1 KB each); descriptors
+            // advance by (byte offset >> 4) in their start-address field
+            const uint64_t ai = ad0 + ((i * p.dil * RT_BW * 128) >> 4);
+            const uint64_t bi = bd0 + ((i * b_box) >> 4);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) umma_bf16(d, ai + 2 * k, bi + 2 * k, idesc, (st | i | k) != 0);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == p.stages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[as]);
+      }
+    }
+  } else {
+    fprop_epilogue_role<BN, 1>(p, &tmY, &tmR, &tmM, tmem_base, tfull, tempty, inbar, epi, warp, 0, blockIdx.x,
+                               gridDim.x);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, TCOLS);
+  }
+}
+
 // ------------------------------------------------------------------ wgrad
 // D[(tap, ci)][co] = sum_p x[p + off(tap), ci] * dy[p, co].  A CTA tile covers NACC x 128
 // (tap, ci) rows -- NXC x-chunks of XW channels in NACC TMEM accumulators -- against BN output
@@ -1809,6 +1937,93 @@ static int launch_halo_fprop(const b2dl_conv_args* a, const b2dl_act& xv, cudaSt
   return rc ? rc : check_launch();
 }
 
+// Row-tap path for narrow outputs (B2DL_ROWTAP=0 disables): packed weights, cout <= 64, >= 2 tap
+// rows, bf16 output through the TMA epilogue.
+static bool rowtap_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("B2DL_ROWTAP");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+static bool rowtap_fprop_ok(const b2dl_conv_args* a, const b2dl_act& x) {
+  const b2dl_act& y = a->y;
+  const int nops = (a->residual.ptr != nullptr) + (a->mask.ptr != nullptr) + (a->accumulate != 0);
+  return rowtap_enabled() && !a->window && a->w_mode == 0 && a->w_packed && a->kh >= 2 && a->cout <= 64 &&
+         a->cout % 8 == 0 && x.c > 16 && RT_BH + (a->kh - 1) * a->dilation <= 256 &&
+         (a->in_stride <= 1) && (a->out_stride <= 1) && !a->bn_partial && !a->bnb_stats &&
+         (!a->bias || (reinterpret_cast<uintptr_t>(a->bias) % 16 == 0)) && !a->y_f32 && view_aligned(y, 2) &&
+         nops <= 2 && (!a->residual.ptr || view_aligned(a->residual, 2)) &&
+         (!a->mask.ptr || view_aligned(a->mask, 2)) && tma_epilogue_enabled();
+}
+
+static int launch_rowtap_fprop(const b2dl_conv_args* a, const b2dl_act& x, cudaStream_t st) {
+  const b2dl_act& y = a->y;
+  const int bn = a->cout <= 32 ? 32 : 64;
+  FpropParams p{};
+  p.n = y.n;
+  p.h = y.h;
+  p.w = y.w;
+  p.bw = RT_BW;
+  p.bh = RT_BH;
+  p.tiles_x = cdiv(y.w, RT_BW);
+  p.tiles_y = cdiv(y.h, RT_BH);
+  p.num_m_tiles = y.n * p.tiles_x * p.tiles_y;
+  p.num_n_tiles = 1;
+  p.num_tiles = p.num_m_tiles;
+  p.kw = a->kw;
+  p.dil = a->dilation;
+  p.pad_top = a->pad_top;
+  p.pad_left = a->pad_left;
+  p.cin_pad = b2dl_cin_pad(x.c);
+  p.num_cblk = p.cin_pad / 64;
+  p.taps = a->kh * a->kw;
+  p.num_kb = p.taps * p.num_cblk;
+  p.cout = a->cout;
+  p.y = y.ptr;
+  p.y_stride = y.c_stride;
+  p.bias = a->bias;
+  p.bias_vec = a->bias != nullptr;
+  p.res = reinterpret_cast<const b2h*>(a->residual.ptr);
+  p.res_stride = a->residual.c_stride;
+  p.mask = reinterpret_cast<const b2h*>(a->mask.ptr);
+  p.mask_stride = a->mask.c_stride;
+  p.relu = a->relu;
+  p.accumulate = a->accumulate;
+  p.vec_ok = 1;
+  p.tma_epi = 1;
+  p.epi_nops = (p.res != nullptr) + (p.mask != nullptr) + (p.accumulate != 0);
+  p.epi_slots = 2;
+  p.epi_bytes = 2 * epi_sub_bytes(p.epi_nops, 2);
+  const int a_stage = (RT_BH + (a->kh - 1) * a->dilation) * RT_BW * 128;
+  const int stage_bytes = a_stage + a->kh * bn * 64 * 2;
+  p.stages = std::min(FPROP_MAX_STAGES, (SMEM_MAX - SMEM_FIXED - p.epi_bytes) / stage_bytes);
+  if (p.stages < 2) return B2DL_E_NOT_IMPLEMENTED;
+  const int smem = p.stages * stage_bytes + p.epi_bytes + SMEM_FIXED;
+
+  FpropMaps t;
+  const uint64_t ktot = static_cast<uint64_t>(p.taps) * p.cin_pad;
+  const uint64_t wd[2] = {ktot, static_cast<uint64_t>(a->cout)};
+  const uint64_t wsd[1] = {ktot * 2};
+  const uint32_t wb[2] = {64u, static_cast<uint32_t>(bn)};
+  if (act_map(&t.a, x, 64, RT_BW, RT_BH + (a->kh - 1) * a->dilation, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      encode_tiled(&t.b, B2H_TMA, 2, const_cast<void*>(a->w_packed), wd, wsd, wb, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      act_map(&t.y, y, 32, RT_BW, RT_BH, CU_TENSOR_MAP_SWIZZLE_64B) ||
+      (p.res && act_map(&t.r, a->residual, 32, RT_BW, RT_BH, CU_TENSOR_MAP_SWIZZLE_64B)) ||
+      (p.mask && act_map(&t.m, a->mask, 32, RT_BW, RT_BH, CU_TENSOR_MAP_SWIZZLE_64B)))
+    return B2DL_E_ALIGN;
+  auto kern = bn == 32 ? conv_rowtap_fprop_kernel<32> : conv_rowtap_fprop_kernel<64>;
+  static bool attr_set[2] = {false, false};
+  if (!attr_set[bn == 64]) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX) != cudaSuccess)
+      return B2DL_E_CUDA;
+    attr_set[bn == 64] = true;
+  }
+  const int grid = std::min(p.num_tiles, num_sms());
+  const int rc = launch_tc(kern, grid, FPROP_THREADS, smem, st, 1, t.a, t.b, t.y, t.r, t.m, p, static_cast<int>(a->kh));
+  return rc ? rc : check_launch();
+}
+
 static bool halo_fprop_ok(const b2dl_conv_args* a, const b2dl_act& xv) {
   const b2dl_act& y = a->y;
   const int nops = (a->residual.ptr != nullptr) + (a->mask.ptr != nullptr) + (a->accumulate != 0);
@@ -1939,6 +2154,7 @@ extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
   if (a->kh < 1 || a->kw < 1 || a->dilation < 1 || a->cout < 1 || x.c < 1) return B2DL_E_VALUE;
   if (!view_aligned(x, 2)) return B2DL_E_ALIGN;
   if (halo_fprop_ok(a, x)) return launch_halo_fprop(a, x, as_stream(stream));
+  if (rowtap_fprop_ok(a, x)) return launch_rowtap_fprop(a, x, as_stream(stream));
   // K block: 16 channels for narrow inputs, 32 for 17..32-channel inputs read through master
   // weights (e.g. the dgrad over a growth-32 dense layer's dy: half the padded MMA work of a
   // 64-wide block), else 64

@@ -411,3 +411,40 @@ def test_kblk32_fprop_and_dgrad_vs_fp64(c32, k, cout):
     F.conv2d(xg, wd.double().view(k, k, cout, c32).permute(3, 2, 0, 1), padding=(k - 1) // 2).backward(
         dy.permute(0, 3, 1, 2).double())
     assert _rel(dx.permute(0, 3, 1, 2), xg.grad) < 1e-2
+
+
+@pytest.mark.parametrize("cin,cout,k,d,ops,hw", [(96, 32, 5, 1, "", (37, 45)), (200, 64, 5, 1, "rm", (37, 45)),
+                                                  (48, 32, 3, 2, "a", (37, 45)), (40, 24, 5, 1, "", (37, 45)),
+                                                  (416, 32, 5, 1, "", (4, 3)), (96, 32, 5, 1, "", (8, 6)),
+                                                  (64, 32, 5, 1, "", (16, 12))])
+def test_rowtap_fprop_vs_fp64(cin, cout, k, d, ops, hw):
+    """Narrow-output convs through the row-tap kernel (one tall input box per column tap and
+    channel block, row taps at 1 KB offsets): bias, relu, residual / mask / accumulate epilogue
+    operands, dilation, ragged image edges, against fp64 on the same bf16 operands."""
+    from paper_1810_01993_b200 import nhwc
+    torch.manual_seed(11)
+    n, (h, w) = 2, hw
+    x = torch.randn(n, h, w, cin, device="cuda").to(torch.bfloat16)
+    whwio = torch.randn(k * k, cin, cout, device="cuda") / (k * k * cin) ** 0.5
+    wp = torch.empty(cout, k * k, nhwc.cin_pad(cin), dtype=torch.bfloat16, device="cuda")
+    nhwc.pack_weights(whwio, k, k, cin, cout, fprop=wp)
+    b = torch.randn(cout, device="cuda") * 0.1
+    cs = (cout + 7) // 8 * 8
+    y = torch.randn(n, h, w, cs, device="cuda").to(torch.bfloat16)
+    y0 = y.clone()
+    res = torch.randn(n, h, w, cs, device="cuda").to(torch.bfloat16) if "r" in ops else None
+    mask = torch.randn(n, h, w, cs, device="cuda").to(torch.bfloat16) if "m" in ops else None
+    acc = "a" in ops
+    nhwc.conv_fprop(nhwc.View(x), wp, cout, k, k, d, nhwc.View(y, 0, cout), bias=b,
+                    residual=nhwc.View(res, 0, cout) if res is not None else None,
+                    mask=nhwc.View(mask, 0, cout) if mask is not None else None, relu=True, accumulate=acc)
+    wr = whwio.to(torch.bfloat16).double().view(k, k, cin, cout).permute(3, 2, 0, 1)
+    ref = F.conv2d(x.permute(0, 3, 1, 2).double(), wr, padding=(k - 1) * d // 2, dilation=d) + b.double()[None, :, None, None]
+    if res is not None:
+        ref = ref + res[..., :cout].permute(0, 3, 1, 2).double()
+    ref = ref.clamp_min(0)
+    if mask is not None:
+        ref = ref * (mask[..., :cout].permute(0, 3, 1, 2).double() > 0)
+    if acc:
+        ref = ref + y0[..., :cout].permute(0, 3, 1, 2).double()
+    assert _rel(y[..., :cout].permute(0, 3, 1, 2), ref) < 1e-2
