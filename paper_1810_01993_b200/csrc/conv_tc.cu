@@ -1612,6 +1612,162 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
+// ------------------------------------------------------------------ row-tap wgrad (narrow N)
+// dW[(i, j, ci)][co] for narrow outputs (cout <= 64, the growth-32 dense layers): a CTA owns one
+// column tap j and a pair of 64-channel blocks (the two 64-row halves of a 128-row M tile, LBO =
+// one tall box) over a range of 8 x 16-pixel K blocks, with one TMEM accumulator per tap row i.
+// Per K block it loads two tall x boxes (16 + (kh-1) dil rows) and one dy box, and every tap row
+// reads the tall boxes at an i*dil KB offset: kh times fewer x loads than a box per tap.  Partial
+// layout = the generic wgrad's ([split][tap][cin][cout], bias sums [split][cout] from tile 0).
+template <int BN>
+__global__ void __launch_bounds__(192, 1)
+    conv_rowtap_wgrad_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmDY,
+                             const WgradParams p, int kh, int stages, int tiles) {
+  const int xbox = (HW_BH + (kh - 1) * p.dil) * HW_BW * 128;  // one tall x box (64 channels)
+  const int stage_bytes = 2 * xbox + HW_BW * HW_BH * 128;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes);
+  uint64_t* empty = full + FPROP_MAX_STAGES;
+  uint64_t* tfull = empty + FPROP_MAX_STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  float* bred = reinterpret_cast<float*>(tmem_slot + 4);  // [64] bias half-sums
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = lane_id();
+  const int tile = blockIdx.x % tiles, split = blockIdx.x / tiles;
+  const int npair = (p.cblk + 1) / 2;
+  const int j = tile / npair, cb0 = 2 * (tile - j * npair);
+  const int pb_lo = split * p.pb_per_split;
+  const int pb_hi = min(p.num_pb, pb_lo + p.pb_per_split);
+  const bool do_bias = p.bsum != nullptr && tile == 0;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmX);
+    tma_prefetch(&tmDY);
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1 + 4);  // MMA commit + the 4 epilogue warps (dy column sums)
+    }
+    mbar_init(tfull, 1);
+    fence_barrier_init();
+  }
+  constexpr int COLS = 512;
+  if (warp == 1) tmem_alloc(tmem_slot, COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  griddep_launch_dependents();
+  griddep_wait();
+  const int per_img = p.pbx * p.pby;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int pb = pb_lo; pb < pb_hi; ++pb) {
+        const int img = pb / per_img, r = pb - img * per_img;
+        const int by = r / p.pbx, bx = r - by * p.pbx;
+        mbar_wait(&empty[stage], phase ^ 1);
+        mbar_arrive_expect_tx(&full[stage], stage_bytes);
+        uint8_t* st = smem + stage * stage_bytes;
+        for (int h = 0; h < 2; ++h)
+          tma_load_4d(st + h * xbox, &tmX, &full[stage], (cb0 + h) * 64, bx * HW_BW + j * p.dil - p.pad_left,
+                      by * HW_BH - p.pad_top, img);
+        tma_load_4d(st + 2 * xbox, &tmDY, &full[stage], 0, bx * HW_BW, by * HW_BH, img);
+        if (++stage == stages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc_bf16(128, BN, true, true);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int pb = pb_lo; pb < pb_hi; ++pb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        const uint32_t x0 = smem_u32(smem + stage * stage_bytes);
+        const uint64_t ad0 = make_sdesc(x0, xbox, 1024, LAYOUT_SW128);
+        const uint64_t bd0 = make_sdesc(x0 + 2 * xbox, 16384, 1024, LAYOUT_SW128);
+        const uint32_t acc = pb > pb_lo;
+        for (int i = 0; i < kh; ++i) {
+          const uint64_t ai = ad0 + ((i * p.dil * HW_BW * 128) >> 4);
+#pragma unroll
+          for (int k = 0; k < HW_BW * HW_BH / 16; ++k)  // 16 pixels (2 KB) per K step
+            umma_bf16(tmem_base + i * BN, ai + k * 128, bd0 + k * 128, idesc, acc | k);
+        }
+        umma_commit(&empty[stage]);
+        if (++stage == stages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      umma_commit(tfull);
+    }
+  } else {
+    const int t = threadIdx.x - 64;  // 0..127
+    const int co = t & 63, ph = t >> 6;
+    float bs = 0.f;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int pb = pb_lo; pb < pb_hi; ++pb) {
+      mbar_wait(&full[stage], phase);
+      if (do_bias) {
+        const uint8_t* dyt = smem + stage * stage_bytes + 2 * xbox;
+#pragma unroll 8
+        for (int px = ph * 64; px < ph * 64 + 64; ++px)
+          bs += h_to_f(*reinterpret_cast<const b2h*>(
+              dyt + px * 128 + ((((co >> 3) ^ (px & 7))) << 4) + (co & 7) * 2));
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == stages) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+    if (ph == 1) bred[co] = bs;
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (ph == 0 && do_bias && co < p.cout) p.bsum[static_cast<long long>(split) * p.cout + co] = bs + bred[co];
+    // weight partial: TMEM lane = (half, channel) row of the 128-row accumulators
+    mbar_wait(tfull, 0);
+    tc_fence_after();
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const int ci = (cb0 + row / 64) * 64 + (row & 63);
+    float* out = p.ws + static_cast<long long>(split) * p.krows * p.cout;
+    for (int i = 0; i < kh; ++i) {
+      float v[BN];
+      if constexpr (BN == 64) {
+        tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + i * BN, v);
+        tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + i * BN + 32, v + 32);
+      } else {
+        tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + i * BN, v);
+      }
+      if (ci < p.cin) {
+        float* dst = out + (static_cast<long long>(i * p.kw + j) * p.cin + ci) * p.cout;
+        if (p.cout == BN) {
+#pragma unroll
+          for (int c = 0; c < BN; c += 4) *reinterpret_cast<float4*>(dst + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < BN; ++c)
+            if (c < p.cout) dst[c] = v[c];
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, COLS);
+  }
+}
+
 __global__ void reduce_segments_kernel(const b2dl_segment* __restrict__ segs, float* __restrict__ base) {
   const b2dl_segment sg = segs[blockIdx.y];
   float* dst = base + sg.dst_off;
@@ -2368,6 +2524,42 @@ static int plan_wgrad(const b2dl_wgrad_args* a, WgradPlan* out) {
     out->bsum_bytes = static_cast<size_t>(p.splits) * p.cout * sizeof(float);
     return B2DL_OK;
   }
+  if (!a->window && rowtap_enabled() && dy.c <= 64 && a->kh >= 2 && a->kh * (dy.c <= 32 ? 32 : 64) <= 512 &&
+      x.c > 16 && HW_BH + (a->kh - 1) * a->dilation <= 256) {
+    // row-tap wgrad (narrow N): a unit = (column tap, pair of 64-channel blocks, pixel split)
+    WgradParams p{};
+    p.n = x.n;
+    p.h = x.h;
+    p.w = x.w;
+    p.bwk = HW_BW;
+    p.bhk = HW_BH;
+    p.pbx = cdiv(x.w, HW_BW);
+    p.pby = cdiv(x.h, HW_BH);
+    p.num_pb = x.n * p.pbx * p.pby;
+    p.kw = a->kw;
+    p.dil = a->dilation;
+    p.pad_top = a->pad_top;
+    p.pad_left = a->pad_left;
+    p.cblk = cdiv(x.c, 64);
+    p.cin = x.c;
+    p.cout = dy.c;
+    p.krows = static_cast<long long>(a->kh) * a->kw * x.c;
+    p.m_tiles = 1;
+    p.n_tiles = 1;
+    const int tiles = a->kw * ((p.cblk + 1) / 2);
+    int splits = a->splits > 0 ? a->splits : std::max(1, (num_sms() + tiles - 1) / tiles);
+    splits = std::min(splits, p.num_pb);
+    p.pb_per_split = cdiv(p.num_pb, splits);
+    p.splits = cdiv(p.num_pb, p.pb_per_split);
+    p.num_tiles = tiles * p.splits;
+    out->p = p;
+    out->bn = dy.c <= 32 ? 32 : 64;
+    out->xw = 64;
+    out->halo = 2;
+    out->ws_bytes = static_cast<size_t>(p.splits) * p.krows * p.cout * sizeof(float);
+    out->bsum_bytes = static_cast<size_t>(p.splits) * p.cout * sizeof(float);
+    return B2DL_OK;
+  }
   WgradParams p{};
   p.n = x.n;
   p.h = x.h;
@@ -2449,7 +2641,28 @@ extern "C" int b2dl_conv_wgrad(const b2dl_wgrad_args* a, void* stream) {
                            : nullptr;
   CUtensorMap tx, tdy;
   cudaStream_t st = as_stream(stream);
-  if (pl.halo) {
+  if (pl.halo == 2) {
+    const int kh = a->kh;
+    const int xrows = HW_BH + (kh - 1) * a->dilation;
+    if (act_map(&tx, a->x, 64, HW_BW, xrows, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        act_map(&tdy, a->dy, 64, HW_BW, HW_BH, CU_TENSOR_MAP_SWIZZLE_128B))
+      return B2DL_E_ALIGN;
+    const int stage_bytes = 2 * xrows * HW_BW * 128 + HW_BW * HW_BH * 128;
+    const int stages = std::min(FPROP_MAX_STAGES, (SMEM_MAX - SMEM_FIXED) / stage_bytes);
+    if (stages < 2) return B2DL_E_NOT_IMPLEMENTED;
+    const int tiles = a->kw * ((pl.p.cblk + 1) / 2);
+    auto kern = pl.bn == 32 ? conv_rowtap_wgrad_kernel<32> : conv_rowtap_wgrad_kernel<64>;
+    static bool attr_set[2] = {false, false};
+    if (!attr_set[pl.bn == 64]) {
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX) != cudaSuccess)
+        return B2DL_E_CUDA;
+      attr_set[pl.bn == 64] = true;
+    }
+    rc = launch_tc(kern, pl.p.num_tiles, 192, stages * stage_bytes + SMEM_FIXED, st, 1, tx, tdy, pl.p, kh, stages,
+                   tiles);
+    if (!rc) rc = check_launch();
+    if (rc) return rc;
+  } else if (pl.halo) {
     const int taps = a->kh;
     if (window_map(&tx, a->x, pl.p.cin, a->dy.w, 64, HW_BW, HW_BH + taps - 1, CU_TENSOR_MAP_SWIZZLE_128B) ||
         act_map(&tdy, a->dy, 64, HW_BW, HW_BH, CU_TENSOR_MAP_SWIZZLE_128B))

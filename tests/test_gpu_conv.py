@@ -134,7 +134,9 @@ def test_master_layout_weight_modes(case):
     dx1 = torch.zeros_like(dx0)
     nhwc.conv_dgrad(nhwc.View(dy), wd, cin, k, k, d, nhwc.View(dx0))
     nhwc.conv_dgrad(nhwc.View(dy), None, cin, k, k, d, nhwc.View(dx1), w_master=wm)
-    assert _rel(dx1, dx0) < 1e-6
+    # a narrow packed dgrad (cin <= 64) runs on the row-tap kernel: same products, another fp32
+    # summation order, so single bf16 output ulps may differ
+    assert _rel(dx1, dx0) < (5e-3 if cin <= 64 and k > 1 else 1e-6)
 
 
 @pytest.mark.parametrize("case", [(1, 256, 36, 24, 256, 3, 4), (2, 128, 24, 48, 512, 3, 2), (1, 64, 9, 13, 320, 1, 1),
@@ -448,3 +450,25 @@ def test_rowtap_fprop_vs_fp64(cin, cout, k, d, ops, hw):
     if acc:
         ref = ref + y0[..., :cout].permute(0, 3, 1, 2).double()
     assert _rel(y[..., :cout].permute(0, 3, 1, 2), ref) < 1e-2
+
+
+@pytest.mark.parametrize("cin,cout,k,d,hw", [(96, 32, 5, 1, (37, 45)), (416, 32, 5, 1, (64, 48)),
+                                             (200, 64, 3, 2, (33, 29)), (40, 24, 5, 1, (16, 12)),
+                                             (64, 32, 5, 1, (4, 3))])
+def test_rowtap_wgrad_vs_fp64(cin, cout, k, d, hw):
+    """Narrow-output weight gradient through the row-tap kernel (tall x boxes shared by the kh tap
+    rows, one TMEM accumulator per tap row): dW and the bias gradient vs fp64 on bf16 operands."""
+    from paper_1810_01993_b200 import nhwc
+    torch.manual_seed(13)
+    n, (h, w) = 2, hw
+    x = torch.randn(n, h, w, cin, device="cuda").to(torch.bfloat16)
+    dy = torch.randn(n, h, w, cout, device="cuda").to(torch.bfloat16)
+    dw = torch.empty(k * k * cin * cout, device="cuda")
+    db = torch.empty(cout, device="cuda")
+    nhwc.conv_wgrad(nhwc.View(x), nhwc.View(dy), k, k, d, dw, nhwc.Workspace(), bias_grad=db)
+    wr = torch.zeros(cout, cin, k, k, dtype=torch.float64, device="cuda", requires_grad=True)
+    F.conv2d(x.permute(0, 3, 1, 2).double(), wr, padding=(k - 1) * d // 2, dilation=d).backward(
+        dy.permute(0, 3, 1, 2).double())
+    got = dw.view(k, k, cin, cout).permute(3, 2, 0, 1)
+    assert _rel(got, wr.grad) < 1e-3
+    assert _rel(db, dy.double().sum(dim=(0, 1, 2))) < 1e-4
