@@ -1086,24 +1086,33 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
 // the kh weight boxes of that column streamed in the same stage: kh times fewer activation loads.
 constexpr int RT_BW = 8, RT_BH = 16;
 
-template <int BN>
+// KB = channels per K block (64, or 32 for 17..32-channel inputs: SW64, 512-byte image rows).  When
+// all the weights fit (p.b_region > 0) they are loaded once and stay resident; the stages then carry
+// only the tall input boxes.
+template <int BN, int KB>
 __global__ void __launch_bounds__(FPROP_THREADS, 1)
     conv_rowtap_fprop_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                              const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmR,
                              const __grid_constant__ CUtensorMap tmM, const FpropParams p, int kh) {
-  const int a_stage = (RT_BH + (kh - 1) * p.dil) * RT_BW * 128;
-  const int b_box = BN * 64 * 2;
-  const int stage_bytes = a_stage + kh * b_box;
+  constexpr int ROW = RT_BW * KB * 2;              // bytes per image row of the tall box
+  constexpr uint32_t LAYOUT = KB == 64 ? LAYOUT_SW128 : LAYOUT_SW64;
+  constexpr uint32_t SBO = 8 * KB * 2;             // 8 rows of KB bf16
+  const int a_stage = (RT_BH + (kh - 1) * p.dil) * ROW;
+  const int b_box = BN * KB * 2;
+  const bool resident = p.b_region > 0;
+  const int stage_bytes = a_stage + (resident ? 0 : kh * b_box);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  uint8_t* sS = smem;   // stages: [A tall box][kh weight boxes]
+  uint8_t* sW = smem;                                // resident weights [tap][cblk] boxes
+  uint8_t* sS = smem + (resident ? p.b_region : 0);  // stages: [A tall box][kh weight boxes]
   uint8_t* epi = sS + p.stages * stage_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(epi + p.epi_bytes);
   uint64_t* empty = full + FPROP_MAX_STAGES;
   uint64_t* tfull = empty + FPROP_MAX_STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* inbar = tempty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(inbar + 16);
+  uint64_t* bfull = inbar + 16;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = lane_id();
@@ -1119,6 +1128,7 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
       mbar_init(&tempty[s], 8);
     }
     for (int s = 0; s < 16; ++s) mbar_init(&inbar[s], 1);
+    mbar_init(bfull, 1);
     tma_prefetch(&tmY);
     if (p.res) tma_prefetch(&tmR);
     if (p.mask) tma_prefetch(&tmM);
@@ -1137,6 +1147,12 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {
+      if (resident) {
+        mbar_arrive_expect_tx(bfull, p.taps * p.num_cblk * b_box);
+        for (int t = 0; t < p.taps; ++t)
+          for (int cb = 0; cb < p.num_cblk; ++cb)
+            tma_load_2d(sW + (t * p.num_cblk + cb) * b_box, &tmB, bfull, t * p.cin_pad + cb * KB, 0);
+      }
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
@@ -1147,10 +1163,11 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], stage_bytes);
           uint8_t* dst = sS + stage * stage_bytes;
-          tma_load_4d(dst, &tmA, &full[stage], cb * 64, tx * RT_BW + j * p.dil - p.pad_left, ty * RT_BH - p.pad_top,
+          tma_load_4d(dst, &tmA, &full[stage], cb * KB, tx * RT_BW + j * p.dil - p.pad_left, ty * RT_BH - p.pad_top,
                       img);
-          for (int i = 0; i < kh; ++i)
-            tma_load_2d(dst + a_stage + i * b_box, &tmB, &full[stage], (i * p.kw + j) * p.cin_pad + cb * 64, 0);
+          if (!resident)
+            for (int i = 0; i < kh; ++i)
+              tma_load_2d(dst + a_stage + i * b_box, &tmB, &full[stage], (i * p.kw + j) * p.cin_pad + cb * KB, 0);
           if (++stage == p.stages) {
             stage = 0;
             phase ^= 1;
@@ -1161,6 +1178,7 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = make_idesc_bf16(BM, BN, false, false);
+      if (resident) mbar_wait(bfull, 0);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -1171,18 +1189,20 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
         tc_fence_after();
         const uint32_t d = tmem_base + as * BN;
         for (int st = 0; st < nsteps; ++st) {
+          const int j = st / p.num_cblk, cb = st - j * p.num_cblk;
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a0 = smem_u32(sS + stage * stage_bytes);
-          const uint64_t ad0 = make_sdesc(a0, 16, 1024, LAYOUT_SW128);
-          const uint64_t bd0 = make_sdesc(a0 + a_stage, 16, 1024, LAYOUT_SW128);
+          const uint64_t ad0 = make_sdesc(a0, 16, SBO, LAYOUT);
           for (int i = 0; i < kh; ++i) {
-            // row tap i: the tall box shifted down i*dil image rows (1 KB each); descriptors
-            // advance by (byte offset >> 4) in their start-address field
-            const uint64_t ai = ad0 + ((i * p.dil * RT_BW * 128) >> 4);
-            const uint64_t bi = bd0 + ((i * b_box) >> 4);
+            // row tap i: the tall box shifted down i*dil image rows (one swizzle atom each);
+            // descriptors advance by (byte offset >> 4) in their start-address field
+            const uint64_t ai = ad0 + ((i * p.dil * ROW) >> 4);
+            const uint32_t b0 = resident ? smem_u32(sW + ((i * p.kw + j) * p.num_cblk + cb) * b_box)
+                                         : a0 + a_stage + i * b_box;
+            const uint64_t bi = make_sdesc(b0, 16, SBO, LAYOUT);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) umma_bf16(d, ai + 2 * k, bi + 2 * k, idesc, (st | i | k) != 0);
+            for (int k = 0; k < KB / 16; ++k) umma_bf16(d, ai + 2 * k, bi + 2 * k, idesc, (st | i | k) != 0);
           }
           umma_commit(&empty[stage]);
           if (++stage == p.stages) {
@@ -1613,9 +1633,9 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 // ------------------------------------------------------------------ row-tap wgrad (narrow N)
-// dW[(i, j, ci)][co] for narrow outputs (cout <= 64, the growth-32 dense layers): a CTA owns one
-// column tap j and a pair of 64-channel blocks (the two 64-row halves of a 128-row M tile, LBO =
-// one tall box) over a range of 8 x 16-pixel K blocks, with one TMEM accumulator per tap row i.
+// dW[(i, j, ci)][co] for narrow outputs (cout <= 64, the growth-32 dense layers): a CTA owns two
+// (column tap j, 64-channel block) combinations -- the two 64-row halves of a 128-row M tile, LBO =
+// one tall box -- over a range of 8 x 16-pixel K blocks, with one TMEM accumulator per tap row i.
 // Per K block it loads two tall x boxes (16 + (kh-1) dil rows) and one dy box, and every tap row
 // reads the tall boxes at an i*dil KB offset: kh times fewer x loads than a box per tap.  Partial
 // layout = the generic wgrad's ([split][tap][cin][cout], bias sums [split][cout] from tile 0).
@@ -1636,8 +1656,8 @@ __global__ void __launch_bounds__(192, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = lane_id();
   const int tile = blockIdx.x % tiles, split = blockIdx.x / tiles;
-  const int npair = (p.cblk + 1) / 2;
-  const int j = tile / npair, cb0 = 2 * (tile - j * npair);
+  const int ncombo = p.kw * p.cblk;   // (column tap, channel block) combinations, two per tile
+  const int c0 = 2 * tile, nh = c0 + 1 < ncombo ? 2 : 1;
   const int pb_lo = split * p.pb_per_split;
   const int pb_hi = min(p.num_pb, pb_lo + p.pb_per_split);
   const bool do_bias = p.bsum != nullptr && tile == 0;
@@ -1669,11 +1689,13 @@ __global__ void __launch_bounds__(192, 1)
         const int img = pb / per_img, r = pb - img * per_img;
         const int by = r / p.pbx, bx = r - by * p.pbx;
         mbar_wait(&empty[stage], phase ^ 1);
-        mbar_arrive_expect_tx(&full[stage], stage_bytes);
+        mbar_arrive_expect_tx(&full[stage], stage_bytes - (2 - nh) * xbox);
         uint8_t* st = smem + stage * stage_bytes;
-        for (int h = 0; h < 2; ++h)
-          tma_load_4d(st + h * xbox, &tmX, &full[stage], (cb0 + h) * 64, bx * HW_BW + j * p.dil - p.pad_left,
+        for (int h = 0; h < nh; ++h) {   // a missing second half computes rows nobody writes back
+          const int jj = (c0 + h) / p.cblk, cb = (c0 + h) - jj * p.cblk;
+          tma_load_4d(st + h * xbox, &tmX, &full[stage], cb * 64, bx * HW_BW + jj * p.dil - p.pad_left,
                       by * HW_BH - p.pad_top, img);
+        }
         tma_load_4d(st + 2 * xbox, &tmDY, &full[stage], 0, bx * HW_BW, by * HW_BH, img);
         if (++stage == stages) {
           stage = 0;
@@ -1737,7 +1759,9 @@ __global__ void __launch_bounds__(192, 1)
     tc_fence_after();
     const int q = warp & 3;
     const int row = q * 32 + lane;
-    const int ci = (cb0 + row / 64) * 64 + (row & 63);
+    const int cmb = c0 + row / 64;
+    const int j = cmb / p.cblk;
+    const int ci = (cmb - j * p.cblk) * 64 + (row & 63);
     float* out = p.ws + static_cast<long long>(split) * p.krows * p.cout;
     for (int i = 0; i < kh; ++i) {
       float v[BN];
@@ -1747,7 +1771,7 @@ __global__ void __launch_bounds__(192, 1)
       } else {
         tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + i * BN, v);
       }
-      if (ci < p.cin) {
+      if (cmb < ncombo && ci < p.cin) {
         float* dst = out + (static_cast<long long>(i * p.kw + j) * p.cin + ci) * p.cout;
         if (p.cout == BN) {
 #pragma unroll
@@ -2093,8 +2117,9 @@ static int launch_halo_fprop(const b2dl_conv_args* a, const b2dl_act& xv, cudaSt
   return rc ? rc : check_launch();
 }
 
-// Row-tap path for narrow outputs (B2DL_ROWTAP=0 disables): packed weights, cout <= 64, >= 2 tap
-// rows, bf16 output through the TMA epilogue.
+// Row-tap path for narrow outputs (B2DL_ROWTAP=0 disables): packed weights, cout <= 64, >= 5 tap
+// rows (3x3 narrow layers measured faster on the generic kernel), bf16 output through the TMA
+// epilogue.
 static bool rowtap_enabled() {
   static const bool on = [] {
     const char* e = getenv("B2DL_ROWTAP");
@@ -2102,10 +2127,17 @@ static bool rowtap_enabled() {
   }();
   return on;
 }
+static bool rowtap_resident_enabled() {   // B2DL_ROWTAP_RESIDENT=0: always stream the weights
+  static const bool on = [] {
+    const char* e = getenv("B2DL_ROWTAP_RESIDENT");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 static bool rowtap_fprop_ok(const b2dl_conv_args* a, const b2dl_act& x) {
   const b2dl_act& y = a->y;
   const int nops = (a->residual.ptr != nullptr) + (a->mask.ptr != nullptr) + (a->accumulate != 0);
-  return rowtap_enabled() && !a->window && a->w_mode == 0 && a->w_packed && a->kh >= 2 && a->cout <= 64 &&
+  return rowtap_enabled() && !a->window && a->w_mode == 0 && a->w_packed && a->kh >= 5 && a->cout <= 64 &&
          a->cout % 8 == 0 && x.c > 16 && RT_BH + (a->kh - 1) * a->dilation <= 256 &&
          (a->in_stride <= 1) && (a->out_stride <= 1) && !a->bn_partial && !a->bnb_stats &&
          (!a->bias || (reinterpret_cast<uintptr_t>(a->bias) % 16 == 0)) && !a->y_f32 && view_aligned(y, 2) &&
@@ -2131,8 +2163,9 @@ static int launch_rowtap_fprop(const b2dl_conv_args* a, const b2dl_act& x, cudaS
   p.dil = a->dilation;
   p.pad_top = a->pad_top;
   p.pad_left = a->pad_left;
-  p.cin_pad = b2dl_cin_pad(x.c);
-  p.num_cblk = p.cin_pad / 64;
+  const int kb = x.c <= 32 ? 32 : 64;   // K block: a 17..32-channel input needs only half a block
+  p.cin_pad = b2dl_cin_pad(x.c);      // packed weights' K stride per tap
+  p.num_cblk = cdiv(x.c, kb);
   p.taps = a->kh * a->kw;
   p.num_kb = p.taps * p.num_cblk;
   p.cout = a->cout;
@@ -2151,29 +2184,37 @@ static int launch_rowtap_fprop(const b2dl_conv_args* a, const b2dl_act& x, cudaS
   p.epi_nops = (p.res != nullptr) + (p.mask != nullptr) + (p.accumulate != 0);
   p.epi_slots = 2;
   p.epi_bytes = 2 * epi_sub_bytes(p.epi_nops, 2);
-  const int a_stage = (RT_BH + (a->kh - 1) * a->dilation) * RT_BW * 128;
-  const int stage_bytes = a_stage + a->kh * bn * 64 * 2;
-  p.stages = std::min(FPROP_MAX_STAGES, (SMEM_MAX - SMEM_FIXED - p.epi_bytes) / stage_bytes);
+  const int a_stage = (RT_BH + (a->kh - 1) * a->dilation) * RT_BW * kb * 2;
+  const int b_box = bn * kb * 2;
+  // weights resident when they fit beside >= 3 input stages, else streamed with each stage
+  const int w_bytes = (p.taps * p.num_cblk * b_box + 1023) / 1024 * 1024;
+  const int room = SMEM_MAX - SMEM_FIXED - p.epi_bytes;
+  p.b_region = (w_bytes + 3 * a_stage <= room && rowtap_resident_enabled()) ? w_bytes : 0;
+  const int stage_bytes = a_stage + (p.b_region ? 0 : a->kh * b_box);
+  p.stages = std::min(FPROP_MAX_STAGES, (room - p.b_region) / stage_bytes);
   if (p.stages < 2) return B2DL_E_NOT_IMPLEMENTED;
-  const int smem = p.stages * stage_bytes + p.epi_bytes + SMEM_FIXED;
+  const int smem = p.b_region + p.stages * stage_bytes + p.epi_bytes + SMEM_FIXED;
 
   FpropMaps t;
   const uint64_t ktot = static_cast<uint64_t>(p.taps) * p.cin_pad;
   const uint64_t wd[2] = {ktot, static_cast<uint64_t>(a->cout)};
   const uint64_t wsd[1] = {ktot * 2};
-  const uint32_t wb[2] = {64u, static_cast<uint32_t>(bn)};
-  if (act_map(&t.a, x, 64, RT_BW, RT_BH + (a->kh - 1) * a->dilation, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      encode_tiled(&t.b, B2H_TMA, 2, const_cast<void*>(a->w_packed), wd, wsd, wb, CU_TENSOR_MAP_SWIZZLE_128B) ||
+  const uint32_t wb[2] = {static_cast<uint32_t>(kb), static_cast<uint32_t>(bn)};
+  const CUtensorMapSwizzle sw = kb == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+  if (act_map(&t.a, x, kb, RT_BW, RT_BH + (a->kh - 1) * a->dilation, sw) ||
+      encode_tiled(&t.b, B2H_TMA, 2, const_cast<void*>(a->w_packed), wd, wsd, wb, sw) ||
       act_map(&t.y, y, 32, RT_BW, RT_BH, CU_TENSOR_MAP_SWIZZLE_64B) ||
       (p.res && act_map(&t.r, a->residual, 32, RT_BW, RT_BH, CU_TENSOR_MAP_SWIZZLE_64B)) ||
       (p.mask && act_map(&t.m, a->mask, 32, RT_BW, RT_BH, CU_TENSOR_MAP_SWIZZLE_64B)))
     return B2DL_E_ALIGN;
-  auto kern = bn == 32 ? conv_rowtap_fprop_kernel<32> : conv_rowtap_fprop_kernel<64>;
-  static bool attr_set[2] = {false, false};
-  if (!attr_set[bn == 64]) {
+  auto kern = bn == 32 ? (kb == 64 ? conv_rowtap_fprop_kernel<32, 64> : conv_rowtap_fprop_kernel<32, 32>)
+                       : (kb == 64 ? conv_rowtap_fprop_kernel<64, 64> : conv_rowtap_fprop_kernel<64, 32>);
+  static bool attr_set[4] = {false, false, false, false};
+  const int ai = (bn == 64) * 2 + (kb == 64);
+  if (!attr_set[ai]) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX) != cudaSuccess)
       return B2DL_E_CUDA;
-    attr_set[bn == 64] = true;
+    attr_set[ai] = true;
   }
   const int grid = std::min(p.num_tiles, num_sms());
   const int rc = launch_tc(kern, grid, FPROP_THREADS, smem, st, 1, t.a, t.b, t.y, t.r, t.m, p, static_cast<int>(a->kh));
@@ -2213,7 +2254,8 @@ static int window_view(const b2dl_act& x, int window, int kw, int pad_left, int 
 namespace b2 {
 static int fprop_kblk(const b2dl_conv_args* a, const b2dl_act& x) {
   if (x.c <= 16) return 16;
-  if (x.c <= 32 && a->w_mode != 0 && !a->window) return 32;
+  // (the statistics epilogue variants are instantiated for 64-channel K blocks only)
+  if (x.c <= 32 && a->w_mode != 0 && !a->window && !a->bn_partial && !a->bnb_stats) return 32;
   return 64;
 }
 // N tile width and CTA pairing of a b2dl_conv_fprop launch (shared with b2dl_conv_fprop_bn_rows)
@@ -2524,7 +2566,7 @@ static int plan_wgrad(const b2dl_wgrad_args* a, WgradPlan* out) {
     out->bsum_bytes = static_cast<size_t>(p.splits) * p.cout * sizeof(float);
     return B2DL_OK;
   }
-  if (!a->window && rowtap_enabled() && dy.c <= 64 && a->kh >= 2 && a->kh * (dy.c <= 32 ? 32 : 64) <= 512 &&
+  if (!a->window && rowtap_enabled() && dy.c <= 64 && a->kh >= 5 && a->kh * (dy.c <= 32 ? 32 : 64) <= 512 &&
       x.c > 16 && HW_BH + (a->kh - 1) * a->dilation <= 256) {
     // row-tap wgrad (narrow N): a unit = (column tap, pair of 64-channel blocks, pixel split)
     WgradParams p{};
@@ -2546,8 +2588,9 @@ static int plan_wgrad(const b2dl_wgrad_args* a, WgradPlan* out) {
     p.krows = static_cast<long long>(a->kh) * a->kw * x.c;
     p.m_tiles = 1;
     p.n_tiles = 1;
-    const int tiles = a->kw * ((p.cblk + 1) / 2);
-    int splits = a->splits > 0 ? a->splits : std::max(1, (num_sms() + tiles - 1) / tiles);
+    const int tiles = (a->kw * p.cblk + 1) / 2;
+    // one unit per CTA, all resident in one wave (a 149th unit would double the kernel's time)
+    int splits = a->splits > 0 ? a->splits : std::max(1, num_sms() / tiles);
     splits = std::min(splits, p.num_pb);
     p.pb_per_split = cdiv(p.num_pb, splits);
     p.splits = cdiv(p.num_pb, p.pb_per_split);
@@ -2650,7 +2693,7 @@ extern "C" int b2dl_conv_wgrad(const b2dl_wgrad_args* a, void* stream) {
     const int stage_bytes = 2 * xrows * HW_BW * 128 + HW_BW * HW_BH * 128;
     const int stages = std::min(FPROP_MAX_STAGES, (SMEM_MAX - SMEM_FIXED) / stage_bytes);
     if (stages < 2) return B2DL_E_NOT_IMPLEMENTED;
-    const int tiles = a->kw * ((pl.p.cblk + 1) / 2);
+    const int tiles = (a->kw * pl.p.cblk + 1) / 2;
     auto kern = pl.bn == 32 ? conv_rowtap_wgrad_kernel<32> : conv_rowtap_wgrad_kernel<64>;
     static bool attr_set[2] = {false, false};
     if (!attr_set[pl.bn == 64]) {

@@ -569,17 +569,27 @@ class Engine:
                         and c.out not in self.up_fprop and c.out != p.logits_name and p.view_spec(c.out)[1] % 8 == 0
                         and (c.k > 1 or c.cout >= 8)):
                     self.bn_fused[c.out] = o
-        # Narrow-output convs with >= 2 tap rows (the growth-32 5x5 dense layers): the row-tap fprop
+        # Narrow-output convs with >= 5 tap rows (the growth-32 5x5 dense layers): the row-tap fprop
         # kernel reads one tall input box per (column tap, channel block) and packed weights
         # (b2dl_conv_fprop picks it for w_packed, cout <= 64; B2DL_ROWTAP=0: the generic kernel)
         self.rowtap = []
         if not self.fp32 and os.environ.get("B2DL_ROWTAP", "1") != "0":
             for o in self.convs:
-                if (o.k >= 2 and o.cout <= 64 and o.cout % 8 == 0 and o.cin > 16 and o is not self.win
+                if (o.k >= 5 and o.cout <= 64 and o.cout % 8 == 0 and o.cin > 16 and o is not self.win
                         and o.out not in self.up_fprop and o.out not in self.bn_fused and o.w not in self.wf
                         and o.out != p.logits_name):
                     self.rowtap.append(o)
                     self.wf[o.w] = torch.zeros((o.cout, o.k * o.k, nhwc.cin_pad(o.cin)), dtype=bf, device=self.device)
+        # ... and narrow input gradients (cin <= 64: the dgrad's output is narrow) with >= 5 tap
+        # rows: packed dgrad weights, so b2dl_conv_fprop runs them on the row-tap kernel too
+        self.rowtap_dgrad = []
+        if not self.fp32 and os.environ.get("B2DL_ROWTAP", "1") != "0":
+            for o in self.convs:
+                if (o.k >= 5 and o.cin <= 64 and o.cin % 8 == 0 and o.cout > 16 and o.ins[0] in p.live
+                        and o is not self.win and o.w not in self.heads and o.w not in self.wd
+                        and o.out not in self.up_fprop and o.out not in self.up_dgrad):
+                    self.rowtap_dgrad.append(o)
+                    self.wd[o.w] = torch.zeros((o.cin, o.k * o.k, nhwc.cin_pad(o.cout)), dtype=bf, device=self.device)
         # ... and its backward statistics (sum gy, sum gy * xhat) from the epilogue of the one dgrad
         # that writes d loss / d y (a single-consumer conv C; the relu mask is recomputed there from
         # the BN input), so the BN VJP is one input-gradient pass (b2dl_conv_args.bnb_partial)
@@ -852,6 +862,9 @@ class Engine:
             self.launches += 1 + (o.w in self.wd)
         for o in self.rowtap:
             nhwc.pack_weights(self.wslice(o.w), o.k, o.k, o.cin, o.cout, fprop=self.wf[o.w])
+            self.launches += 1
+        for o in self.rowtap_dgrad:
+            nhwc.pack_weights(self.wslice(o.w), o.k, o.k, o.cin, o.cout, dgrad=self.wd[o.w])
             self.launches += 1
         if self.win is not None:   # HWIO [k][k][cin][cout] is HWIO [k][1][k*cin][cout]
             o = self.win
