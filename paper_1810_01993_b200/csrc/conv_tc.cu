@@ -2127,6 +2127,13 @@ static bool rowtap_enabled() {
   }();
   return on;
 }
+static int rowtap_min_kh() {   // fewest tap rows for the row-tap kernels (B2DL_ROWTAP_MINK, default 5)
+  static const int v = [] {
+    const char* e = getenv("B2DL_ROWTAP_MINK");
+    return e && e[0] ? atoi(e) : 5;
+  }();
+  return v;
+}
 static bool rowtap_resident_enabled() {   // B2DL_ROWTAP_RESIDENT=0: always stream the weights
   static const bool on = [] {
     const char* e = getenv("B2DL_ROWTAP_RESIDENT");
@@ -2137,7 +2144,8 @@ static bool rowtap_resident_enabled() {   // B2DL_ROWTAP_RESIDENT=0: always stre
 static bool rowtap_fprop_ok(const b2dl_conv_args* a, const b2dl_act& x) {
   const b2dl_act& y = a->y;
   const int nops = (a->residual.ptr != nullptr) + (a->mask.ptr != nullptr) + (a->accumulate != 0);
-  return rowtap_enabled() && !a->window && a->w_mode == 0 && a->w_packed && a->kh >= 5 && a->cout <= 64 &&
+  return rowtap_enabled() && !a->window && a->w_mode == 0 && a->w_packed && a->kh >= rowtap_min_kh() &&
+         a->cout <= 64 &&
          a->cout % 8 == 0 && x.c > 16 && RT_BH + (a->kh - 1) * a->dilation <= 256 &&
          (a->in_stride <= 1) && (a->out_stride <= 1) && !a->bn_partial && !a->bnb_stats &&
          (!a->bias || (reinterpret_cast<uintptr_t>(a->bias) % 16 == 0)) && !a->y_f32 && view_aligned(y, 2) &&
@@ -2566,7 +2574,10 @@ static int plan_wgrad(const b2dl_wgrad_args* a, WgradPlan* out) {
     out->bsum_bytes = static_cast<size_t>(p.splits) * p.cout * sizeof(float);
     return B2DL_OK;
   }
-  if (!a->window && rowtap_enabled() && dy.c <= 64 && a->kh >= 5 && a->kh * (dy.c <= 32 ? 32 : 64) <= 512 &&
+  // (from 5 tap rows: alone the 3x3 64->64 stage-0 wgrads take 32 instead of 53 us at 2 x 288 x 192,
+  // but inside the DeepLab step, beside the concurrent dgrads, the generic kernel measured no slower)
+  if (!a->window && rowtap_enabled() && dy.c <= 64 && a->kh >= rowtap_min_kh() &&
+      a->kh * (dy.c <= 32 ? 32 : 64) <= 512 &&
       x.c > 16 && HW_BH + (a->kh - 1) * a->dilation <= 256) {
     // row-tap wgrad (narrow N): a unit = (column tap, pair of 64-channel blocks, pixel split)
     WgradParams p{};

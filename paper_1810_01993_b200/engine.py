@@ -573,9 +573,10 @@ class Engine:
         # kernel reads one tall input box per (column tap, channel block) and packed weights
         # (b2dl_conv_fprop picks it for w_packed, cout <= 64; B2DL_ROWTAP=0: the generic kernel)
         self.rowtap = []
+        rt_min_k = int(os.environ.get("B2DL_ROWTAP_MINK", "5"))
         if not self.fp32 and os.environ.get("B2DL_ROWTAP", "1") != "0":
             for o in self.convs:
-                if (o.k >= 5 and o.cout <= 64 and o.cout % 8 == 0 and o.cin > 16 and o is not self.win
+                if (o.k >= rt_min_k and o.cout <= 64 and o.cout % 8 == 0 and o.cin > 16 and o is not self.win
                         and o.out not in self.up_fprop and o.out not in self.bn_fused and o.w not in self.wf
                         and o.out != p.logits_name):
                     self.rowtap.append(o)
@@ -585,7 +586,7 @@ class Engine:
         self.rowtap_dgrad = []
         if not self.fp32 and os.environ.get("B2DL_ROWTAP", "1") != "0":
             for o in self.convs:
-                if (o.k >= 5 and o.cin <= 64 and o.cin % 8 == 0 and o.cout > 16 and o.ins[0] in p.live
+                if (o.k >= rt_min_k and o.cin <= 64 and o.cin % 8 == 0 and o.cout > 16 and o.ins[0] in p.live
                         and o is not self.win and o.w not in self.heads and o.w not in self.wd
                         and o.out not in self.up_fprop and o.out not in self.up_dgrad):
                     self.rowtap_dgrad.append(o)
