@@ -137,6 +137,9 @@ def reference_step_times(steps: int, warmup: int):
     if deskdl is None:
         return cpu_step_time(steps, warmup), "port", "oracle/deskdl_port.py"
     os.environ.setdefault("DESKDL_KERNELS", "python")   # im2col+sgemm: ~9x the Cython loops here
+    # all host threads for OpenBLAS even under torchrun (which exports OMP_NUM_THREADS=1)
+    from threadpoolctl import threadpool_limits
+    _limits = threadpool_limits(limits=os.cpu_count())   # noqa: F841  (kept for the run)
     from deskdl.graph import OpGraph
     from deskdl.model import ClassWeights, kernels, ops
     from deskdl.optimizer import LayerParam, OptimConfig, larc_sgd_step
@@ -164,6 +167,8 @@ def reference_step_times(steps: int, warmup: int):
 
 def cpu_step_time(steps: int, warmup: int):
     """Seconds per reference CPU step on the bounded sample (oracle port, all host threads)."""
+    from threadpoolctl import threadpool_limits
+    _limits = threadpool_limits(limits=os.cpu_count())   # noqa: F841
     from oracle import deskdl_port as O
     from paper_1810_01993_b200 import models
     from paper_1810_01993_b200.scenes import SceneConfig, make_scene, scene_rng
@@ -286,7 +291,9 @@ def run_ours(args):
     scene = SceneConfig(channels=C, height=H, width=W)
     cw = ClassWeights(scene.frequencies).vector()
     hier = tuple(int(v) for v in args.hierarchy.split("x")) if getattr(args, "hierarchy", "") else None
-    tr = DataParallelTrainer(net, OptimConfig(lr=0.01, momentum=0.9, trust=0.02), shape, class_weights=cw,
+    # lr 0.002: at 0.01 the synthetic run's first steps spike (loss 2 -> 11 at lag 0, -> 158 at lag 1,
+    # NaN later); the step's work does not depend on it
+    tr = DataParallelTrainer(net, OptimConfig(lr=0.002, momentum=0.9, trust=0.02), shape, class_weights=cw,
                              hierarchy=hier, lag=args.lag)
     eng = tr.eng
     # synthetic pool, resident in HBM, different tiles per rank
