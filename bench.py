@@ -294,7 +294,7 @@ def run_ours(args):
     # lr 0.002: at 0.01 the synthetic run's first steps spike (loss 2 -> 11 at lag 0, -> 158 at lag 1,
     # NaN later); the step's work does not depend on it
     tr = DataParallelTrainer(net, OptimConfig(lr=0.002, momentum=0.9, trust=0.02), shape, class_weights=cw,
-                             hierarchy=hier, lag=args.lag)
+                             hierarchy=hier, lag=args.lag, bucket_mb=args.bucket_mb)
     eng = tr.eng
     # synthetic pool, resident in HBM, different tiles per rank
     pool = 4
@@ -519,6 +519,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--precision", default=None, choices=["bf16", "fp16"],
                     help="16-bit storage / MMA operand type (default: bf16; fp16 for --variant tiramisu, config 4)")
+    ap.add_argument("--bucket-mb", type=float, default=32.0, help="gradient all-reduce bucket size (N > 1)")
     ap.add_argument("--lag", type=int, default=0, choices=[0, 1],
                     help="gradient lag (trainer.py:378-383): 1 applies the previous step's reduced gradients")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a captured CUDA graph")
