@@ -42,6 +42,18 @@ def _r8(c: int) -> int:
     return (c + 7) // 8 * 8
 
 
+_PITCH64 = os.environ.get("B2DL_PITCH64", "0") == "1"   # measured: no step-time change (off)
+
+
+def _pitch(c: int) -> int:
+    """Channel pitch of an NHWC buffer: a multiple of 8 (16-byte rows for TMA), and above 64
+    channels a multiple of 64, so every 64-channel TMA box row of every pixel is one aligned
+    128-byte line (e.g. the decoder's 304-channel concat: 320, no box straddling two lines)."""
+    if _PITCH64 and c > 64:
+        return (c + 63) // 64 * 64
+    return _r8(c)
+
+
 @dataclass
 class Op:
     kind: str                      # conv | pool | up | concat | add | ce
@@ -253,7 +265,7 @@ class Plan:
             root, _ = resolve(t)
             n, c, h, w = self.shapes[root]
             f32 = root == self.logits_name
-            self.buffers[root] = (n, h, w, c if f32 else _r8(c), f32)
+            self.buffers[root] = (n, h, w, c if f32 else _pitch(c), f32)
 
     def view_spec(self, t):
         root, off = self.view_of[t]
@@ -298,7 +310,7 @@ class Plan:
             if t in self.view_of:
                 root = self.gview_spec(t)[0]
                 n, h, w, _, _ = self.buffers[root]
-                self.grad_buffers[root] = (n, h, w, _r8(self.chans(root)))
+                self.grad_buffers[root] = (n, h, w, _pitch(self.chans(root)))
         # static backward program: overwrite/accumulate and relu masking decided per contribution.
         # A contribution to the gradient of a "maskable" tensor (a relu output, or a pool /
         # nearest-upsample / concat of relu outputs -- all non-negative, zero exactly where every
