@@ -26,13 +26,20 @@ def test_every_declared_symbol_is_bound_and_exported():
     for n in names:
         assert hasattr(_lib.LIB, n), n
     assert _lib.LIB.b2dl_version().startswith(b"b2dl")
+    # the fp16 build (libb2dl_f16.so) exports the same ABI, and _lib.use routes LIB to it
+    f16 = _lib.library("fp16")
+    for n in names:
+        assert hasattr(f16, n), n
+    with _lib.use("fp16") as lib:
+        assert lib is f16 and _lib.LIB.b2dl_cin_pad is f16.b2dl_cin_pad
+    assert _lib.LIB.b2dl_cin_pad is _lib.library("bf16").b2dl_cin_pad
 
 
 def test_struct_layouts_match_c(tmp_path):
     from paper_1810_01993_b200 import _lib
     structs = {"b2dl_act": _lib.Act, "b2dl_conv_args": _lib.ConvArgs, "b2dl_wgrad_args": _lib.WgradArgs,
                "b2dl_larc_args": _lib.LarcArgs}
-    fields = {"b2dl_conv_args": ["y", "bias", "mask", "block_n"], "b2dl_wgrad_args": ["dw", "workspace", "splits"],
+    fields = {"b2dl_conv_args": ["y", "bias", "mask", "block_n", "bn_partial", "bnb_stats", "bnb_partial"], "b2dl_wgrad_args": ["dw", "workspace", "splits"],
               "b2dl_larc_args": ["lr", "lr_out", "workspace_bytes", "mode"], "b2dl_act": ["c", "c_stride"]}
     lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HDR}"', "int main(void){"]
     for s in structs:
