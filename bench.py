@@ -208,8 +208,8 @@ KERNEL_OF_PASS = {
 
 def _traffic(dom):
     """DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
-    (profiles/round1/roofline_traffic.json, written by tools/ncu_summary.py), else None."""
-    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "round1", "roofline_traffic.json")
+    (profiles/round2/roofline_traffic.json, written by tools/make_traffic.py), else None."""
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "round2", "roofline_traffic.json")
     try:
         d = json.load(open(p))
         e = d.get(dom)

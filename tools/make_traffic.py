@@ -1,4 +1,4 @@
-"""profiles/round1/roofline_traffic.json from an ncu --set full report of tools/prof_conv.py
+"""roofline_traffic.json (profiles/round<N>/) from an ncu --set full report of tools/prof_conv.py
 fprop_mn dgrad_m wgrad (first three conv launches): DRAM bytes per launch of each pass's kernel
 at the full-resolution 3x3x256 shape, next to its algorithmic operand bytes."""
 import csv
