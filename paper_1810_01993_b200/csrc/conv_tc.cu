@@ -2267,6 +2267,20 @@ static int fprop_kblk(const b2dl_conv_args* a, const b2dl_act& x) {
   return 64;
 }
 // N tile width and CTA pairing of a b2dl_conv_fprop launch (shared with b2dl_conv_fprop_bn_rows)
+// Output tile width of the generic fprop (tile = bw x (128 / bw) pixels).  A strided input
+// (the upsampled conv's dgrad reads dy at s_in x the output resolution) re-reads the kernel's
+// (k - 1)-pixel halo of every tile, so it takes squarer tiles (B2DL_STRIDED_BW caps the width).
+static int fprop_tile_w(int w, int s_in) {
+  int bw = pow2_divisor(w, 128);
+  if (bw < 8 && w >= 8) bw = std::min(128, 1 << (31 - __builtin_clz(w)));
+  while (bw * s_in > 256) bw >>= 1;   // strided input box: traversal extent <= 256
+  if (s_in > 1) {
+    static const int cap = env_int("B2DL_STRIDED_BW", 0);
+    if (cap >= 8 && bw > cap) bw = cap;
+  }
+  return bw;
+}
+
 static void fprop_choose(const b2dl_conv_args* a, const b2dl_act& x, int kblk, int* bn_out, int* cg_out) {
   int bn = a->block_n ? a->block_n : pick_bn(a->cout);
   // 256- and 128-wide N tiles run as CTA pairs (256 pixels x BN per pair)
@@ -2277,8 +2291,7 @@ static void fprop_choose(const b2dl_conv_args* a, const b2dl_act& x, int kblk, i
   if (!a->block_n && (bn == 256 || bn == 128) && kblk == 64) {
     // wave quantisation: pick the (N tile, pairing) that fills the persistent grid best,
     // weighted by the relative speed of each tile shape
-    const int bw = pow2_divisor(x.w, 128) < 8 && x.w >= 8 ? std::min(128, 1 << (31 - __builtin_clz(x.w)))
-                                                         : pow2_divisor(x.w, 128);
+    const int bw = fprop_tile_w(x.w, a->in_stride > 0 ? a->in_stride : 1);
     const long long mt = static_cast<long long>(x.n) * cdiv(x.w, bw) * cdiv(x.h, BM / bw);
     auto score = [&](int b, int g, double speed) {
       const long long units = (mt + g - 1) / g * cdiv(a->cout, b), slots = num_sms() / g;
@@ -2325,9 +2338,7 @@ extern "C" int b2dl_conv_fprop_bn_rows(const b2dl_conv_args* a) {
     x.w = y.w;
   }
   if (halo_fprop_ok(a, x)) return std::min(y.n * cdiv(y.w, HALO_BW) * cdiv(y.h, HALO_BH), num_sms());
-  int bw = pow2_divisor(x.w, 128);
-  if (bw < 8 && x.w >= 8) bw = std::min(128, 1 << (31 - __builtin_clz(x.w)));
-  while (bw * s_in > 256) bw >>= 1;
+  const int bw = fprop_tile_w(x.w, s_in);
   const int m_tiles = x.n * cdiv(x.w, bw) * cdiv(x.h, BM / bw);
   int bn, cg;
   fprop_choose(a, x, fprop_kblk(a, x), &bn, &cg);
@@ -2374,9 +2385,7 @@ extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
   p.h = x.h;
   p.w = x.w;
   p.in_stride = s_in;
-  p.bw = pow2_divisor(x.w, 128);
-  if (p.bw < 8 && x.w >= 8) p.bw = std::min(128, 1 << (31 - __builtin_clz(x.w)));
-  while (p.bw * s_in > 256) p.bw >>= 1;   // strided input box: traversal extent <= 256
+  p.bw = fprop_tile_w(x.w, s_in);
   p.bh = BM / p.bw;
   p.tiles_x = cdiv(x.w, p.bw);
   p.tiles_y = cdiv(x.h, p.bh);
