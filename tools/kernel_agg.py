@@ -12,7 +12,7 @@ def load(path):
     out = []
     for r in rows[1:]:
         v = float(r[vi].replace(",", ""))
-        v = {"nsecond": v / 1e3, "usecond": v, "msecond": v * 1e3}.get(r[ui], v)
+        v = {"nsecond": v / 1e3, "ns": v / 1e3, "usecond": v, "us": v, "msecond": v * 1e3, "ms": v * 1e3}.get(r[ui], v)
         out.append((r[ki], v))
     return out
 
