@@ -123,6 +123,9 @@ struct FpropParams {
   int tma_epi;         // 1: TMA-staged epilogue (operands + output through swizzled boxes)
   int epi_nops;        // operands per chunk in the TMA epilogue (residual, mask, accumulated y)
   int epi_slots;       // operand slots per sub-group (prefetch depth + 1)
+  int epi_pw;          // 1: per-warp epilogue boxes (32 pixels x 32 channels; no sub-group barrier)
+  int epi_obufs;       // output buffers per sub-group (2; per-warp mode up to 4)
+  int dbg_epi;         // development: 1 = epilogue only drains TMEM (wrong results; timing aid)
   int bias_vec;        // bias 16-byte aligned
   int in_stride;       // input pixels per output pixel (strided reads of the input)
   int y_phase;         // output is a phase view of a larger tensor: TMA epilogue only
@@ -353,7 +356,9 @@ __device__ __forceinline__ void box_row_put(uint8_t* box, const float* v) {
 constexpr int EPI_CHUNK = 128 * 64;  // 128 pixels x 32 bf16 channels
 // per sub-group: `slots` operand slots of nops chunks (operands run slots-1 chunks ahead) + 2
 // output buffers
-__host__ __device__ constexpr int epi_sub_bytes(int nops, int slots = 2) { return (slots * nops + 2) * EPI_CHUNK; }
+__host__ __device__ constexpr int epi_sub_bytes(int nops, int slots = 2, int obufs = 2) {
+  return (slots * nops + obufs) * EPI_CHUNK;
+}
 constexpr int EPI_MAX_SLOTS = 4;
 
 // ST: statistics epilogue variant (compile time, so the plain kernels carry none of its registers):
@@ -372,11 +377,21 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
   const int q = warp & 3;
   const int sub = ew >> 2;
   const bool leader = (q == 0) && (lane == 0);  // warp with lane quarter 0 of the sub-group
+  // Per-warp mode (epi_pw, not with forward statistics, which read all four quarters back): each
+  // warp moves its own 32 rows of a chunk as one 32-pixel x 32-channel box -- the same bytes of the
+  // same swizzled buffers -- with its own operand barriers and bulk groups, so the four warps of a
+  // sub-group never rendezvous; the tensor maps carry the per-warp box (host side).
+  const bool pw = ST != 1 && p.epi_pw;
+  const bool issuer = pw ? lane == 0 : leader;
+  const int qoff = pw ? q * (EPI_CHUNK / 4) : 0;
+  const int wdx = pw ? (32 * q) % p.bw : 0, wdy = pw ? (32 * q) / p.bw : 0;
+  const uint32_t box_tx = pw ? EPI_CHUNK / 4 : EPI_CHUNK;
   const int nops = p.epi_nops;
   const int S = p.epi_slots;   // operand slots: loads run S-1 chunks ahead of use
-  uint8_t* sbuf = epi + sub * epi_sub_bytes(nops, S);
+  const int OB = pw ? p.epi_obufs : 2;
+  uint8_t* sbuf = epi + sub * epi_sub_bytes(nops, S, OB);
   uint8_t* obuf = sbuf + S * nops * EPI_CHUNK;
-  uint64_t* ib = inbar + EPI_MAX_SLOTS * sub;
+  uint64_t* ib = pw ? inbar + 2 * ew : inbar + EPI_MAX_SLOTS * sub;   // pw: S <= 2 (host)
   auto locate = [&](int tile, int& img, int& x, int& y, int& nt) {
     const int pmt = tile / p.num_n_tiles;
     nt = tile - pmt * p.num_n_tiles;
@@ -395,13 +410,15 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
     return n;
   };
   auto issue = [&](int tile, int j, int slot) {
-    if (leader) {
+    if (issuer) {
       int img, x, y, nt;
       locate(tile, img, x, y, nt);
+      x += wdx;
+      y += wdy;
       const int c0 = nt * BN + (SUBS * j + sub) * 32;
-      uint8_t* dst = sbuf + slot * nops * EPI_CHUNK;
+      uint8_t* dst = sbuf + slot * nops * EPI_CHUNK + qoff;
       fence_proxy_async();
-      mbar_arrive_expect_tx(&ib[slot], nops * EPI_CHUNK);
+      mbar_arrive_expect_tx(&ib[slot], nops * box_tx);
       int o = 0;
       if (p.res) tma_load_4d(dst + (o++) * EPI_CHUNK, tmR, &ib[slot], c0, x, y, img);
       if (p.mask) tma_load_4d(dst + (o++) * EPI_CHUNK, tmM, &ib[slot], c0, x, y, img);
@@ -433,10 +450,10 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
     int_nt += units_nt;
     if (int_nt >= p.num_n_tiles) int_nt -= p.num_n_tiles;
   };
-  if (leader)
+  if (issuer)
     while (itile < p.num_tiles && nv_at(int_nt) == 0) step_tile();
   auto issue_next = [&]() {
-    if (!leader || !nops || itile >= p.num_tiles) return;
+    if (!issuer || !nops || itile >= p.num_tiles) return;
     issue(itile, ij, islot);
     islot = islot + 1 == S ? 0 : islot + 1;
     if (++ij >= nv_at(int_nt)) {
@@ -446,7 +463,7 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
       } while (itile < p.num_tiles && nv_at(int_nt) == 0);
     }
   };
-  for (int k = 0; k < S - 1; ++k) issue_next();
+  for (int k = 0; k < S - 1 && !p.dbg_epi; ++k) issue_next();
   float bn_acc[NJ];
   float bb_acc[NJ][2];
 #pragma unroll
@@ -462,9 +479,14 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
     mbar_wait(&tfull[as], ap);
     tc_fence_after();
     const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + as * BN;
+    if (p.dbg_epi) {
+      release(as);
+      continue;
+    }
 #pragma unroll 1
     for (int j = 0; j < NJ; ++j) {
       if (j >= nv) break;  // uniform over the sub-group
+      if (pw) __syncwarp();   // the slot refilled next was read by this warp's lanes last chunk
       issue_next();        // keeps S-1 chunks of operands in flight
       const int c0 = nt * BN + (SUBS * j + sub) * 32;
       uint32_t cur[32];
@@ -480,6 +502,17 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
       const float4* bias4 = p.bias ? reinterpret_cast<const float4*>(p.bias + c0) : nullptr;
       float bstat[64];   // BN backward statistics of this row's 32 channels (only with bnb_stats)
       const bool pix_ok = img < p.n && y + row / p.bw < p.h && x + (row % p.bw) < p.w;
+      if (pw) {   // this buffer's store (OB chunks ago) must have read it out
+        if (lane == 0) {
+          if (OB >= 4)
+            bulk_wait_read<3>();
+          else if (OB == 3)
+            bulk_wait_read<2>();
+          else
+            bulk_wait_read<1>();
+        }
+        __syncwarp();
+      }
 #pragma unroll
       for (int k = 0; k < 4; ++k) {  // 8-column pieces
         const int poff = row * 64 + ((k ^ swz) << 4);
@@ -559,10 +592,10 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
           const float4 ma = __ldg(mu4), mb = __ldg(mu4 + 1), ra = __ldg(rs4), rb = __ldg(rs4 + 1);
           const float mu[8] = {ma.x, ma.y, ma.z, ma.w, mb.x, mb.y, mb.z, mb.w};
           const float rs[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
-          const uint32_t pw[4] = {pk.x, pk.y, pk.z, pk.w};
+          const uint32_t pkw[4] = {pk.x, pk.y, pk.z, pk.w};
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
-            const float g = (e & 1) ? bf16hi(pw[e >> 1]) : bf16lo(pw[e >> 1]);
+            const float g = (e & 1) ? bf16hi(pkw[e >> 1]) : bf16lo(pkw[e >> 1]);
             const bool ok = pix_ok;
             bstat[2 * (8 * k + e)] = ok ? g : 0.f;
             bstat[2 * (8 * k + e) + 1] = ok ? g * ((zf[e] - mu[e]) * rs[e]) : 0.f;
@@ -594,13 +627,21 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
         }
       }
       fence_proxy_async();
-      // the other output buffer (next chunk's) must be read out by its store before anyone
-      // packs into it: its store was the only one outstanding before this chunk's
-      if (leader) bulk_wait_read<0>();
-      sub_sync();
-      if (leader) {
-        tma_store_4d(tmY, ochunk, c0, x, y, img);
-        bulk_commit();
+      if (pw) {
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_4d(tmY, ochunk + qoff, c0, x + wdx, y + wdy, img);
+          bulk_commit();
+        }
+      } else {
+        // the other output buffer (next chunk's) must be read out by its store before anyone
+        // packs into it: its store was the only one outstanding before this chunk's
+        if (leader) bulk_wait_read<0>();
+        sub_sync();
+        if (leader) {
+          tma_store_4d(tmY, ochunk, c0, x, y, img);
+          bulk_commit();
+        }
       }
       if constexpr (ST == 1) {
         // Batch-norm statistics of this chunk (training-mode BN after the conv):
@@ -649,7 +690,7 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
             p.bn_part[(static_cast<long long>(mt) * 2 + (idx >> 3)) * p.cout + ch] = v16[0];
         }
       }
-      ob ^= 1;
+      ob = ob + 1 == OB ? 0 : ob + 1;
       slot = slot + 1 == S ? 0 : slot + 1;
     }
     if (nv == 0) release(as);
@@ -674,7 +715,7 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
         p.bn_part[(static_cast<long long>(blockIdx.x) * 2 + (idx >> 3)) * p.cout + ch] = bn_acc[j];
     }
   }
-  if (leader) bulk_wait<0>();
+  if (issuer) bulk_wait<0>();
   __syncwarp();
 }
 
@@ -1931,8 +1972,23 @@ static int env_int(const char* name, int dflt) {
   return e && e[0] ? atoi(e) : dflt;
 }
 static int ew16_max_nops() {
-  static const int v = env_int("B2DL_EW16_NOPS", 1);
+  static const int v = env_int("B2DL_EW16_NOPS", 2);
   return v;
+}
+// B2DL_EPI_PW: per-warp TMA epilogue boxes (fprop_epilogue_tma)
+static bool epi_pw_enabled() {
+  static const int v = env_int("B2DL_EPI_PW", 1);
+  return v != 0;
+}
+static int epi_obufs_for(int ew, int nops) {
+  static int cache[2][4] = {{-1, -1, -1, -1}, {-1, -1, -1, -1}};
+  int& c = cache[ew == 16][nops & 3];
+  if (c < 0) {
+    char name[40];
+    snprintf(name, sizeof(name), "B2DL_EPI_OBUFS_%d_%d", ew, nops);
+    c = std::max(2, std::min(4, env_int(name, 2)));
+  }
+  return c;
 }
 static int epi_slots_for(int ew, int nops) {
   static int cache[2][4] = {{-1, -1, -1, -1}, {-1, -1, -1, -1}};
@@ -1940,7 +1996,9 @@ static int epi_slots_for(int ew, int nops) {
   if (c < 0) {
     char name[40];
     snprintf(name, sizeof(name), "B2DL_EPI_SLOTS_%d_%d", ew, nops);
-    c = std::max(1, std::min(EPI_MAX_SLOTS, env_int(name, 2)));
+    // 16 warps x 2 operands: one slot (no prefetch) -- the 4 sub-groups' buffers otherwise leave
+    // the main loop too few stages (measured on the 1/8-resolution 1x1 dgrads: 107 -> 95 us)
+    c = std::max(1, std::min(EPI_MAX_SLOTS, env_int(name, ew == 16 && nops >= 2 ? 1 : 2)));
   }
   return c;
 }
@@ -1962,7 +2020,11 @@ static int launch_fprop(const FpropMaps& t, FpropParams p, cudaStream_t st) {
   // the epilogue-bound 1x1 layers (their chunks wait on instruction latency, not on the loads)
   // and costs operand stages, so two it is.
   p.epi_slots = epi_slots_for(EW, p.epi_nops);
-  p.epi_bytes = p.tma_epi ? (EW / 4) * epi_sub_bytes(p.epi_nops, p.epi_slots) : EPI_LEGACY_BYTES;
+  if (!p.tma_epi || ST == 1) p.epi_pw = 0;
+  if (p.epi_pw) p.epi_slots = std::min(p.epi_slots, 2);   // two operand barriers per epilogue warp
+  p.epi_obufs = p.epi_pw ? epi_obufs_for(EW, p.epi_nops) : 2;
+  p.dbg_epi = env_int("B2DL_DBG_EPI", 0);
+  p.epi_bytes = p.tma_epi ? (EW / 4) * epi_sub_bytes(p.epi_nops, p.epi_slots, p.epi_obufs) : EPI_LEGACY_BYTES;
   if (p.bn_part && !p.tma_epi) return B2DL_E_VALUE;
   // deepest operand pipeline that fits beside the epilogue buffers
   p.stages = 1;
@@ -2469,7 +2531,9 @@ extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
                       (reinterpret_cast<uintptr_t>(p.bnb_stats) & 15) || (a->cout & 7)))
     return B2DL_E_VALUE;
   if (p.tma_epi) {
-    const int bwx = p.bw, bhx = p.bh;  // epilogue boxes: 32 channels x the whole tile
+    // epilogue boxes: 32 channels x the whole tile, or x one warp's 32 pixels (per-warp mode)
+    p.epi_pw = epi_pw_enabled() && !p.bn_part;
+    const int bwx = p.epi_pw ? std::min(p.bw, 32) : p.bw, bhx = p.epi_pw ? 32 / bwx : p.bh;
     if ((s_out > 1 ? act_map_phase(&t.y, a->y, s_out, a->out_phase_h, a->out_phase_w, 32, bwx, bhx,
                                    CU_TENSOR_MAP_SWIZZLE_64B)
                    : act_map(&t.y, y, 32, bwx, bhx, CU_TENSOR_MAP_SWIZZLE_64B)) ||
