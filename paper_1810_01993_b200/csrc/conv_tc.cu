@@ -502,6 +502,9 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
       const float4* bias4 = p.bias ? reinterpret_cast<const float4*>(p.bias + c0) : nullptr;
       float bstat[64];   // BN backward statistics of this row's 32 channels (only with bnb_stats)
       const bool pix_ok = img < p.n && y + row / p.bw < p.h && x + (row % p.bw) < p.w;
+      // without an accumulated operand the relu mask can zero the packed result: one packed
+      // compare + AND per pair instead of unpack / compare / select per value (same bits)
+      const bool late_mask = ST != 2 && !p.accumulate;
       if (pw) {   // this buffer's store (OB chunks ago) must have read it out
         if (lane == 0) {
           if (OB >= 4)
@@ -546,10 +549,14 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
           for (int e = 0; e < 8; ++e) v[e] = fmaxf(v[e], 0.f);
         }
         float zf[8];
+        uint32_t mbits[4] = {~0u, ~0u, ~0u, ~0u};
         if (p.mask) {
           const uint4 u = *reinterpret_cast<const uint4*>(in + (o++) * EPI_CHUNK + poff);
           const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
-          if constexpr (ST == 2) {   // mask operand = BN input z: relu mask = scale z + shift > 0
+          if (late_mask) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) mbits[e] = pos_mask_h2(w4[e]);
+          } else if constexpr (ST == 2) {   // mask operand = BN input z: relu mask = scale z + shift > 0
             const float4* sc4 = reinterpret_cast<const float4*>(p.bnb_stats + 2 * p.cout + c0 + 8 * k);
             const float4* sh4 = reinterpret_cast<const float4*>(p.bnb_stats + 3 * p.cout + c0 + 8 * k);
             const float4 sa = __ldg(sc4), sb = __ldg(sc4 + 1), ha = __ldg(sh4), hb = __ldg(sh4 + 1);
@@ -581,10 +588,10 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
           }
         }
         uint4 pk;
-        pk.x = pack_bf16x2(v[0], v[1]);
-        pk.y = pack_bf16x2(v[2], v[3]);
-        pk.z = pack_bf16x2(v[4], v[5]);
-        pk.w = pack_bf16x2(v[6], v[7]);
+        pk.x = pack_bf16x2(v[0], v[1]) & mbits[0];
+        pk.y = pack_bf16x2(v[2], v[3]) & mbits[1];
+        pk.z = pack_bf16x2(v[4], v[5]) & mbits[2];
+        pk.w = pack_bf16x2(v[6], v[7]) & mbits[3];
         *reinterpret_cast<uint4*>(ochunk + poff) = pk;
         if constexpr (ST == 2) {   // this pixel's (g, g * xhat) of the STORED g, channel-major pairs
           const float4* mu4 = reinterpret_cast<const float4*>(p.bnb_stats + c0 + 8 * k);

@@ -43,3 +43,9 @@ __device__ __forceinline__ b2h f_to_h(float x) { return __float2bfloat16_rn(x); 
 __device__ __forceinline__ float h_to_f(b2h x) { return __bfloat162float(x); }
 __device__ __forceinline__ b2h2 h2_from(float a, float b) { return __floats2bfloat162_rn(a, b); }
 #endif
+
+// 0xFFFF in each 16-bit half of w whose value is > 0, else 0 (an IEEE compare: -0, negatives and
+// NaN give 0) -- the relu-VJP mask of a packed pair, applied to a packed result with one AND
+__device__ __forceinline__ uint32_t pos_mask_h2(uint32_t w) {
+  return __hgt2_mask(*reinterpret_cast<const b2h2*>(&w), h2_from(0.f, 0.f));
+}
