@@ -12,7 +12,8 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libb2dl.so")
+# B2DL_LIB_PATH: load another build of the same ABI (A/B timing of two builds on one box)
+LIB_PATH = os.environ.get("B2DL_LIB_PATH") or os.path.join(HERE, "libb2dl.so")
 
 B2DL_OK = 0
 B2DL_E_NOT_IMPLEMENTED = 1
