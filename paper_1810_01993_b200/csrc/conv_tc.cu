@@ -502,9 +502,6 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
       const float4* bias4 = p.bias ? reinterpret_cast<const float4*>(p.bias + c0) : nullptr;
       float bstat[64];   // BN backward statistics of this row's 32 channels (only with bnb_stats)
       const bool pix_ok = img < p.n && y + row / p.bw < p.h && x + (row % p.bw) < p.w;
-      // without an accumulated operand the relu mask can zero the packed result: one packed
-      // compare + AND per pair instead of unpack / compare / select per value (same bits)
-      const bool late_mask = ST != 2 && !p.accumulate;
       if (pw) {   // this buffer's store (OB chunks ago) must have read it out
         if (lane == 0) {
           if (OB >= 4)
@@ -516,6 +513,77 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
         }
         __syncwarp();
       }
+      if constexpr (ST != 2) {
+        // operation-major over the chunk's 32 values: one uniform branch per operand per chunk,
+        // operand pointers fixed per chunk (the per-piece form below re-derives both per 8 values)
+        float v[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(cur[e]);
+        auto poff = [&](int k) { return row * 64 + ((k ^ swz) << 4); };
+        auto add16 = [&](const uint8_t* src) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint4 u = *reinterpret_cast<const uint4*>(src + poff(k));
+            const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              v[8 * k + 2 * e] += bf16lo(w4[e]);
+              v[8 * k + 2 * e + 1] += bf16hi(w4[e]);
+            }
+          }
+        };
+        if (bias4) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (c0 + 8 * k < p.cout) {  // TMA epilogue: bias 16-byte aligned, cout % 8 == 0
+              const float4 b0 = __ldg(bias4 + 2 * k), b1 = __ldg(bias4 + 2 * k + 1);
+              v[8 * k + 0] += b0.x;
+              v[8 * k + 1] += b0.y;
+              v[8 * k + 2] += b0.z;
+              v[8 * k + 3] += b0.w;
+              v[8 * k + 4] += b1.x;
+              v[8 * k + 5] += b1.y;
+              v[8 * k + 6] += b1.z;
+              v[8 * k + 7] += b1.w;
+            }
+        }
+        const uint8_t* mop = in + (p.res ? EPI_CHUNK : 0);   // operand order: residual, mask, y
+        if (p.res) add16(in);
+        if (p.relu) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = fmaxf(v[e], 0.f);
+        }
+        if (p.mask && p.accumulate) {   // mask before the accumulated value: per element
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint4 u = *reinterpret_cast<const uint4*>(mop + poff(k));
+            const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              if (!(bf16lo(w4[e]) > 0.f)) v[8 * k + 2 * e] = 0.f;
+              if (!(bf16hi(w4[e]) > 0.f)) v[8 * k + 2 * e + 1] = 0.f;
+            }
+          }
+        }
+        if (p.accumulate) add16(mop + (p.mask ? EPI_CHUNK : 0));
+        uint32_t pkw[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) pkw[e] = pack_bf16x2(v[2 * e], v[2 * e + 1]);
+        if (p.mask && !p.accumulate) {   // relu mask on the packed pairs (same bits as zeroing)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint4 u = *reinterpret_cast<const uint4*>(mop + poff(k));
+            pkw[4 * k + 0] &= pos_mask_h2(u.x);
+            pkw[4 * k + 1] &= pos_mask_h2(u.y);
+            pkw[4 * k + 2] &= pos_mask_h2(u.z);
+            pkw[4 * k + 3] &= pos_mask_h2(u.w);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          *reinterpret_cast<uint4*>(ochunk + poff(k)) =
+              make_uint4(pkw[4 * k], pkw[4 * k + 1], pkw[4 * k + 2], pkw[4 * k + 3]);
+      } else {
 #pragma unroll
       for (int k = 0; k < 4; ++k) {  // 8-column pieces
         const int poff = row * 64 + ((k ^ swz) << 4);
@@ -549,14 +617,10 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
           for (int e = 0; e < 8; ++e) v[e] = fmaxf(v[e], 0.f);
         }
         float zf[8];
-        uint32_t mbits[4] = {~0u, ~0u, ~0u, ~0u};
         if (p.mask) {
           const uint4 u = *reinterpret_cast<const uint4*>(in + (o++) * EPI_CHUNK + poff);
           const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
-          if (late_mask) {
-#pragma unroll
-            for (int e = 0; e < 4; ++e) mbits[e] = pos_mask_h2(w4[e]);
-          } else if constexpr (ST == 2) {   // mask operand = BN input z: relu mask = scale z + shift > 0
+          if constexpr (ST == 2) {   // mask operand = BN input z: relu mask = scale z + shift > 0
             const float4* sc4 = reinterpret_cast<const float4*>(p.bnb_stats + 2 * p.cout + c0 + 8 * k);
             const float4* sh4 = reinterpret_cast<const float4*>(p.bnb_stats + 3 * p.cout + c0 + 8 * k);
             const float4 sa = __ldg(sc4), sb = __ldg(sc4 + 1), ha = __ldg(sh4), hb = __ldg(sh4 + 1);
@@ -588,10 +652,10 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
           }
         }
         uint4 pk;
-        pk.x = pack_bf16x2(v[0], v[1]) & mbits[0];
-        pk.y = pack_bf16x2(v[2], v[3]) & mbits[1];
-        pk.z = pack_bf16x2(v[4], v[5]) & mbits[2];
-        pk.w = pack_bf16x2(v[6], v[7]) & mbits[3];
+        pk.x = pack_bf16x2(v[0], v[1]);
+        pk.y = pack_bf16x2(v[2], v[3]);
+        pk.z = pack_bf16x2(v[4], v[5]);
+        pk.w = pack_bf16x2(v[6], v[7]);
         *reinterpret_cast<uint4*>(ochunk + poff) = pk;
         if constexpr (ST == 2) {   // this pixel's (g, g * xhat) of the STORED g, channel-major pairs
           const float4* mu4 = reinterpret_cast<const float4*>(p.bnb_stats + c0 + 8 * k);
@@ -608,6 +672,7 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
             bstat[2 * (8 * k + e) + 1] = ok ? g * ((zf[e] - mu[e]) * rs[e]) : 0.f;
           }
         }
+      }
       }
       if constexpr (ST == 2) {
         // reduce-scatter over the 32 lanes (rows): lane l ends with channel l's (sum g, sum g xhat)
@@ -2196,10 +2261,10 @@ static bool rowtap_enabled() {
   }();
   return on;
 }
-static int rowtap_min_kh() {   // fewest tap rows for the row-tap kernels (B2DL_ROWTAP_MINK, default 5)
+static int rowtap_min_kh() {   // fewest tap rows for the row-tap kernels (B2DL_ROWTAP_MINK, default 3)
   static const int v = [] {
     const char* e = getenv("B2DL_ROWTAP_MINK");
-    return e && e[0] ? atoi(e) : 5;
+    return e && e[0] ? atoi(e) : 3;
   }();
   return v;
 }

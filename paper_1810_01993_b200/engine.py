@@ -585,7 +585,7 @@ class Engine:
         # kernel reads one tall input box per (column tap, channel block) and packed weights
         # (b2dl_conv_fprop picks it for w_packed, cout <= 64; B2DL_ROWTAP=0: the generic kernel)
         self.rowtap = []
-        rt_min_k = int(os.environ.get("B2DL_ROWTAP_MINK", "5"))
+        rt_min_k = int(os.environ.get("B2DL_ROWTAP_MINK", "3"))
         if not self.fp32 and os.environ.get("B2DL_ROWTAP", "1") != "0":
             for o in self.convs:
                 if (o.k >= rt_min_k and o.cout <= 64 and o.cout % 8 == 0 and o.cin > 16 and o is not self.win

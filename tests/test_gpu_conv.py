@@ -419,7 +419,8 @@ def test_kblk32_fprop_and_dgrad_vs_fp64(c32, k, cout):
                                                   (24, 32, 5, 1, "", (37, 45)), (32, 64, 7, 1, "m", (20, 30)),
                                                   (48, 32, 5, 2, "a", (37, 45)), (40, 24, 5, 1, "", (37, 45)),
                                                   (416, 32, 5, 1, "", (4, 3)), (96, 32, 5, 1, "", (8, 6)),
-                                                  (64, 32, 5, 1, "", (16, 12))])
+                                                  (64, 32, 5, 1, "", (16, 12)), (64, 64, 3, 1, "m", (37, 45)),
+                                                  (64, 64, 3, 2, "rm", (37, 45)), (48, 32, 3, 1, "a", (20, 30))])
 def test_rowtap_fprop_vs_fp64(cin, cout, k, d, ops, hw):
     """Narrow-output convs through the row-tap kernel (one tall input box per column tap and
     channel block, row taps at 1 KB offsets): bias, relu, residual / mask / accumulate epilogue
@@ -455,7 +456,8 @@ def test_rowtap_fprop_vs_fp64(cin, cout, k, d, ops, hw):
 
 @pytest.mark.parametrize("cin,cout,k,d,hw", [(96, 32, 5, 1, (37, 45)), (416, 32, 5, 1, (64, 48)),
                                              (200, 64, 5, 2, (33, 29)), (40, 24, 5, 1, (16, 12)),
-                                             (64, 32, 5, 1, (4, 3))])
+                                             (64, 32, 5, 1, (4, 3)), (64, 64, 3, 1, (72, 48)),
+                                             (64, 64, 3, 2, (33, 29)), (48, 32, 3, 1, (16, 12))])
 def test_rowtap_wgrad_vs_fp64(cin, cout, k, d, hw):
     """Narrow-output weight gradient through the row-tap kernel (tall x boxes shared by the kh tap
     rows, one TMEM accumulator per tap row): dW and the bias gradient vs fp64 on bf16 operands."""
