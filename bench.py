@@ -379,7 +379,7 @@ def run_ours(args):
     dx = tr.static_x if graphed else torch.empty_like(batches[0][0])
     dl = tr.static_l if graphed else torch.empty_like(batches[0][1])
     barrier()
-    e_steps = max(2, args.steps // 2)
+    e_steps = max(2, args.steps)   # the same K steps as the device-timed region
     e0.record()
     if graphed:
         # the next step's host->device copy runs on a copy stream under the current step; every
