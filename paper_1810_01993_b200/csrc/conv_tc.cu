@@ -1202,7 +1202,10 @@ constexpr int RT_BW = 8, RT_BH = 16;
 // KB = channels per K block (64, or 32 for 17..32-channel inputs: SW64, 512-byte image rows).  When
 // all the weights fit (p.b_region > 0) they are loaded once and stay resident; the stages then carry
 // only the tall input boxes.
-template <int BN, int KB>
+// CG = 2: a CTA pair (cluster of 2) runs two vertically adjacent tiles as one M = 256 MMA; each CTA
+// stages its own tall box and half of the weight rows (BN / 2), and the even CTA issues
+// 256 x BN x 16 instructions -- half the MMA issue count per FLOP, which bounds the N = 32 kernel.
+template <int BN, int KB, int CG = 1>
 __global__ void __launch_bounds__(FPROP_THREADS, 1)
     conv_rowtap_fprop_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                              const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmR,
@@ -1211,7 +1214,7 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
   constexpr uint32_t LAYOUT = KB == 64 ? LAYOUT_SW128 : LAYOUT_SW64;
   constexpr uint32_t SBO = 8 * KB * 2;             // 8 rows of KB bf16
   const int a_stage = (RT_BH + (kh - 1) * p.dil) * ROW;
-  const int b_box = BN * KB * 2;
+  const int b_box = (BN / CG) * KB * 2;          // this CTA's weight rows of one (tap, K block)
   const bool resident = p.b_region > 0;
   const int stage_bytes = a_stage + (resident ? 0 : kh * b_box);
   extern __shared__ uint8_t smem_raw[];
@@ -1229,6 +1232,7 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = lane_id();
+  const int rank = CG == 2 ? static_cast<int>(cluster_ctarank()) : 0;
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
@@ -1238,7 +1242,7 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 8);
+      mbar_init(&tempty[s], 8 * CG);
     }
     for (int s = 0; s < 16; ++s) mbar_init(&inbar[s], 1);
     mbar_init(bfull, 1);
@@ -1248,39 +1252,67 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
     fence_barrier_init();
   }
   constexpr uint32_t TCOLS = tmem_cols_for(2 * BN);
-  if (warp == 1) tmem_alloc(tmem_slot, TCOLS);
+  if (warp == 1) {
+    if constexpr (CG == 2)
+      tmem_alloc_pair(tmem_slot, TCOLS);
+    else
+      tmem_alloc(tmem_slot, TCOLS);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2)
+    cluster_sync();
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   griddep_launch_dependents();
   griddep_wait();
   const int per_img = p.tiles_x * p.tiles_y;
   const int nsteps = p.kw * p.num_cblk;   // (column tap, channel block) stages per tile
+  const int unit0 = blockIdx.x / CG, units = gridDim.x / CG;
+  const int n0 = rank * (BN / CG);        // this CTA's weight rows
 
   if (warp == 0) {
     if (lane == 0) {
       if (resident) {
-        mbar_arrive_expect_tx(bfull, p.taps * p.num_cblk * b_box);
-        for (int t = 0; t < p.taps; ++t)
-          for (int cb = 0; cb < p.num_cblk; ++cb)
-            tma_load_2d(sW + (t * p.num_cblk + cb) * b_box, &tmB, bfull, t * p.cin_pad + cb * KB, 0);
+        if constexpr (CG == 2) {   // both halves complete on the even CTA's barrier
+          if (rank == 0) mbar_arrive_expect_tx(bfull, 2 * p.taps * p.num_cblk * b_box);
+          const uint32_t fb = mapa_shared(smem_u32(bfull), 0);
+          for (int t = 0; t < p.taps; ++t)
+            for (int cb = 0; cb < p.num_cblk; ++cb)
+              tma_load_2d_pair(sW + (t * p.num_cblk + cb) * b_box, &tmB, fb, t * p.cin_pad + cb * KB, n0);
+        } else {
+          mbar_arrive_expect_tx(bfull, p.taps * p.num_cblk * b_box);
+          for (int t = 0; t < p.taps; ++t)
+            for (int cb = 0; cb < p.num_cblk; ++cb)
+              tma_load_2d(sW + (t * p.num_cblk + cb) * b_box, &tmB, bfull, t * p.cin_pad + cb * KB, 0);
+        }
       }
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-        const int img = tile / per_img, r = tile - img * per_img;
+      for (int tile = unit0; tile < p.num_tiles; tile += units) {
+        const int mt = tile * CG + rank;   // an odd last pair's second tile is past the end: zero fill
+        const int img = mt / per_img, r = mt - img * per_img;
         const int ty = r / p.tiles_x, tx = r - ty * p.tiles_x;
         for (int st = 0; st < nsteps; ++st) {
           const int j = st / p.num_cblk, cb = st - j * p.num_cblk;
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], stage_bytes);
           uint8_t* dst = sS + stage * stage_bytes;
-          tma_load_4d(dst, &tmA, &full[stage], cb * KB, tx * RT_BW + j * p.dil - p.pad_left, ty * RT_BH - p.pad_top,
-                      img);
-          if (!resident)
-            for (int i = 0; i < kh; ++i)
-              tma_load_2d(dst + a_stage + i * b_box, &tmB, &full[stage], (i * p.kw + j) * p.cin_pad + cb * KB, 0);
+          const int ax = tx * RT_BW + j * p.dil - p.pad_left, ay = ty * RT_BH - p.pad_top;
+          if constexpr (CG == 2) {
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * stage_bytes);
+            const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
+            tma_load_4d_pair(dst, &tmA, fb, cb * KB, ax, ay, img);
+            if (!resident)
+              for (int i = 0; i < kh; ++i)
+                tma_load_2d_pair(dst + a_stage + i * b_box, &tmB, fb, (i * p.kw + j) * p.cin_pad + cb * KB, n0);
+          } else {
+            mbar_arrive_expect_tx(&full[stage], stage_bytes);
+            tma_load_4d(dst, &tmA, &full[stage], cb * KB, ax, ay, img);
+            if (!resident)
+              for (int i = 0; i < kh; ++i)
+                tma_load_2d(dst + a_stage + i * b_box, &tmB, &full[stage], (i * p.kw + j) * p.cin_pad + cb * KB, 0);
+          }
           if (++stage == p.stages) {
             stage = 0;
             phase ^= 1;
@@ -1289,13 +1321,15 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = make_idesc_bf16(BM, BN, false, false);
+    // the whole warp walks the schedule (waits, descriptors: warp-uniform); one elected lane issues
+    // the MMAs and their commits -- no per-instruction single-thread issue loop around each UTCHMMA
+    if (rank == 0) {
+      constexpr uint32_t idesc = make_idesc_bf16(BM * CG, BN, false, false);
       if (resident) mbar_wait(bfull, 0);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++it) {
+      for (int tile = unit0; tile < p.num_tiles; tile += units, ++it) {
         const int as = it & 1;
         const uint32_t ap = (it >> 1) & 1;
         mbar_wait(&tempty[as], ap ^ 1);
@@ -1307,34 +1341,57 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
           tc_fence_after();
           const uint32_t a0 = smem_u32(sS + stage * stage_bytes);
           const uint64_t ad0 = make_sdesc(a0, 16, SBO, LAYOUT);
-          for (int i = 0; i < kh; ++i) {
-            // row tap i: the tall box shifted down i*dil image rows (one swizzle atom each);
-            // descriptors advance by (byte offset >> 4) in their start-address field
-            const uint64_t ai = ad0 + ((i * p.dil * ROW) >> 4);
-            const uint32_t b0 = resident ? smem_u32(sW + ((i * p.kw + j) * p.num_cblk + cb) * b_box)
-                                         : a0 + a_stage + i * b_box;
-            const uint64_t bi = make_sdesc(b0, 16, SBO, LAYOUT);
+          if (elect_one_sync()) {
+            for (int i = 0; i < kh; ++i) {
+              // row tap i: the tall box shifted down i*dil image rows (one swizzle atom each);
+              // descriptors advance by (byte offset >> 4) in their start-address field
+              const uint64_t ai = ad0 + ((i * p.dil * ROW) >> 4);
+              const uint32_t b0 = resident ? smem_u32(sW + ((i * p.kw + j) * p.num_cblk + cb) * b_box)
+                                           : a0 + a_stage + i * b_box;
+              const uint64_t bi = make_sdesc(b0, 16, SBO, LAYOUT);
 #pragma unroll
-            for (int k = 0; k < KB / 16; ++k) umma_bf16(d, ai + 2 * k, bi + 2 * k, idesc, (st | i | k) != 0);
+              for (int k = 0; k < KB / 16; ++k) {
+                if constexpr (CG == 2)
+                  umma_bf16_pair(d, ai + 2 * k, bi + 2 * k, idesc, (st | i | k) != 0);
+                else
+                  umma_bf16(d, ai + 2 * k, bi + 2 * k, idesc, (st | i | k) != 0);
+              }
+            }
+            if constexpr (CG == 2)
+              umma_commit_pair(&empty[stage]);
+            else
+              umma_commit(&empty[stage]);
           }
-          umma_commit(&empty[stage]);
+          __syncwarp();
           if (++stage == p.stages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(&tfull[as]);
+        if (elect_one_sync()) {
+          if constexpr (CG == 2)
+            umma_commit_pair(&tfull[as]);
+          else
+            umma_commit(&tfull[as]);
+        }
+        __syncwarp();
       }
     }
   } else {
-    fprop_epilogue_role<BN, 1>(p, &tmY, &tmR, &tmM, tmem_base, tfull, tempty, inbar, epi, warp, 0, blockIdx.x,
-                               gridDim.x);
+    fprop_epilogue_role<BN, CG>(p, &tmY, &tmR, &tmM, tmem_base, tfull, tempty, inbar, epi, warp, rank, unit0,
+                                units);
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2)
+    cluster_sync();
+  else
+    __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, TCOLS);
+    if constexpr (CG == 2)
+      tmem_dealloc_pair(tmem_base, TCOLS);
+    else
+      tmem_dealloc(tmem_base, TCOLS);
   }
 }
 
@@ -2300,7 +2357,10 @@ static int launch_rowtap_fprop(const b2dl_conv_args* a, const b2dl_act& x, cudaS
   p.tiles_y = cdiv(y.h, RT_BH);
   p.num_m_tiles = y.n * p.tiles_x * p.tiles_y;
   p.num_n_tiles = 1;
-  p.num_tiles = p.num_m_tiles;
+  // CTA pairs (M = 256 per MMA) unless B2DL_ROWTAP_PAIRS=0 or there is a single tile
+  static const int pairs_on = env_int("B2DL_ROWTAP_PAIRS", 1);
+  const int cg = pairs_on && p.num_m_tiles >= 2 ? 2 : 1;
+  p.num_tiles = cdiv(p.num_m_tiles, cg);
   p.kw = a->kw;
   p.dil = a->dilation;
   p.pad_top = a->pad_top;
@@ -2329,7 +2389,7 @@ static int launch_rowtap_fprop(const b2dl_conv_args* a, const b2dl_act& x, cudaS
   p.epi_slots = 2;
   p.epi_bytes = 2 * epi_sub_bytes(p.epi_nops, 2);
   const int a_stage = (RT_BH + (a->kh - 1) * a->dilation) * RT_BW * kb * 2;
-  const int b_box = bn * kb * 2;
+  const int b_box = (bn / cg) * kb * 2;   // per CTA: a pair splits the weight rows
   // weights resident when they fit beside >= 3 input stages, else streamed with each stage
   const int w_bytes = (p.taps * p.num_cblk * b_box + 1023) / 1024 * 1024;
   const int room = SMEM_MAX - SMEM_FIXED - p.epi_bytes;
@@ -2343,7 +2403,7 @@ static int launch_rowtap_fprop(const b2dl_conv_args* a, const b2dl_act& x, cudaS
   const uint64_t ktot = static_cast<uint64_t>(p.taps) * p.cin_pad;
   const uint64_t wd[2] = {ktot, static_cast<uint64_t>(a->cout)};
   const uint64_t wsd[1] = {ktot * 2};
-  const uint32_t wb[2] = {static_cast<uint32_t>(kb), static_cast<uint32_t>(bn)};
+  const uint32_t wb[2] = {static_cast<uint32_t>(kb), static_cast<uint32_t>(bn / cg)};
   const CUtensorMapSwizzle sw = kb == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
   if (act_map(&t.a, x, kb, RT_BW, RT_BH + (a->kh - 1) * a->dilation, sw) ||
       encode_tiled(&t.b, B2H_TMA, 2, const_cast<void*>(a->w_packed), wd, wsd, wb, sw) ||
@@ -2351,17 +2411,22 @@ static int launch_rowtap_fprop(const b2dl_conv_args* a, const b2dl_act& x, cudaS
       (p.res && act_map(&t.r, a->residual, 32, RT_BW, RT_BH, CU_TENSOR_MAP_SWIZZLE_64B)) ||
       (p.mask && act_map(&t.m, a->mask, 32, RT_BW, RT_BH, CU_TENSOR_MAP_SWIZZLE_64B)))
     return B2DL_E_ALIGN;
-  auto kern = bn == 32 ? (kb == 64 ? conv_rowtap_fprop_kernel<32, 64> : conv_rowtap_fprop_kernel<32, 32>)
-                       : (kb == 64 ? conv_rowtap_fprop_kernel<64, 64> : conv_rowtap_fprop_kernel<64, 32>);
-  static bool attr_set[4] = {false, false, false, false};
-  const int ai = (bn == 64) * 2 + (kb == 64);
+  decltype(&conv_rowtap_fprop_kernel<32, 64>) kern;
+  if (cg == 2)
+    kern = bn == 32 ? (kb == 64 ? conv_rowtap_fprop_kernel<32, 64, 2> : conv_rowtap_fprop_kernel<32, 32, 2>)
+                    : (kb == 64 ? conv_rowtap_fprop_kernel<64, 64, 2> : conv_rowtap_fprop_kernel<64, 32, 2>);
+  else
+    kern = bn == 32 ? (kb == 64 ? conv_rowtap_fprop_kernel<32, 64> : conv_rowtap_fprop_kernel<32, 32>)
+                    : (kb == 64 ? conv_rowtap_fprop_kernel<64, 64> : conv_rowtap_fprop_kernel<64, 32>);
+  static bool attr_set[8] = {false, false, false, false, false, false, false, false};
+  const int ai = (cg == 2) * 4 + (bn == 64) * 2 + (kb == 64);
   if (!attr_set[ai]) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX) != cudaSuccess)
       return B2DL_E_CUDA;
     attr_set[ai] = true;
   }
-  const int grid = std::min(p.num_tiles, num_sms());
-  const int rc = launch_tc(kern, grid, FPROP_THREADS, smem, st, 1, t.a, t.b, t.y, t.r, t.m, p, static_cast<int>(a->kh));
+  const int grid = cg * std::min(p.num_tiles, num_sms() / cg);
+  const int rc = launch_tc(kern, grid, FPROP_THREADS, smem, st, cg, t.a, t.b, t.y, t.r, t.m, p, static_cast<int>(a->kh));
   return rc ? rc : check_launch();
 }
 
