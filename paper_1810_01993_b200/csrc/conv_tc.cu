@@ -1001,7 +1001,8 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
+    // converged warp, elected issuer (see the row-tap kernel): no per-MMA single-thread issue loop
+    if (rank == 0) {
       constexpr uint32_t idesc = make_idesc_bf16(BM * CG, BN, false, BMN);
       int stage = 0;
       uint32_t phase = 0;
@@ -1017,29 +1018,35 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
           const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
+          if (elect_one_sync()) {
 #pragma unroll
-          for (int k = 0; k < KBLK / 16; ++k) {
-            const uint64_t ad = make_sdesc(a0 + k * 32, 16, SBO, LAYOUT);
-            const uint64_t bd = BMN ? make_sdesc(b0 + k * 2048, C::B_CHUNK, 1024, LAYOUT_SW128)
-                                    : make_sdesc(b0 + k * 32, 16, SBO, LAYOUT);
+            for (int k = 0; k < KBLK / 16; ++k) {
+              const uint64_t ad = make_sdesc(a0 + k * 32, 16, SBO, LAYOUT);
+              const uint64_t bd = BMN ? make_sdesc(b0 + k * 2048, C::B_CHUNK, 1024, LAYOUT_SW128)
+                                      : make_sdesc(b0 + k * 32, 16, SBO, LAYOUT);
+              if constexpr (CG == 2)
+                umma_bf16_pair(d, ad, bd, idesc, (kb | k) != 0);
+              else
+                umma_bf16(d, ad, bd, idesc, (kb | k) != 0);
+            }
             if constexpr (CG == 2)
-              umma_bf16_pair(d, ad, bd, idesc, (kb | k) != 0);
+              umma_commit_pair(&empty[stage]);
             else
-              umma_bf16(d, ad, bd, idesc, (kb | k) != 0);
+              umma_commit(&empty[stage]);
           }
-          if constexpr (CG == 2)
-            umma_commit_pair(&empty[stage]);
-          else
-            umma_commit(&empty[stage]);
+          __syncwarp();
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        if constexpr (CG == 2)
-          umma_commit_pair(&tfull[as]);
-        else
-          umma_commit(&tfull[as]);
+        if (elect_one_sync()) {
+          if constexpr (CG == 2)
+            umma_commit_pair(&tfull[as]);
+          else
+            umma_commit(&tfull[as]);
+        }
+        __syncwarp();
       }
     }
   } else {
@@ -1145,7 +1152,7 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {   // converged warp, elected issuer (see the row-tap kernel)
       constexpr uint32_t idesc = make_idesc_bf16(BM, HALO_BN, false, false);
       mbar_wait(bfull, 0);
       int stage = 0;
@@ -1163,19 +1170,23 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
           // descriptors advance by (byte offset >> 4) in their start-address field
           const uint64_t ad0 = make_sdesc(smem_u32(sA + stage * a_stage), 16, 1024, LAYOUT_SW128);
           const uint64_t bd0 = make_sdesc(smem_u32(sB + h * HALO_BBOX), 16, 1024, LAYOUT_SW128);
-          for (int i = 0; i < taps; ++i) {
-            const uint64_t ai = ad0 + ((i * HALO_BW * 128) >> 4);  // tap row i: the box shifted down i rows
-            const uint64_t bi = bd0 + ((i * nh * HALO_BBOX) >> 4);
+          if (elect_one_sync()) {
+            for (int i = 0; i < taps; ++i) {
+              const uint64_t ai = ad0 + ((i * HALO_BW * 128) >> 4);  // tap row i: the box shifted down i rows
+              const uint64_t bi = bd0 + ((i * nh * HALO_BBOX) >> 4);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) umma_bf16(d, ai + 2 * k, bi + 2 * k, idesc, (h | i | k) != 0);
+              for (int k = 0; k < 4; ++k) umma_bf16(d, ai + 2 * k, bi + 2 * k, idesc, (h | i | k) != 0);
+            }
+            umma_commit(&empty[stage]);
           }
-          umma_commit(&empty[stage]);
+          __syncwarp();
           if (++stage == p.stages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(&tfull[as]);
+        if (elect_one_sync()) umma_commit(&tfull[as]);
+        __syncwarp();
       }
     }
   } else {
@@ -1525,7 +1536,7 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {   // converged warp, elected issuer (see the row-tap fprop kernel)
       constexpr uint32_t idesc = make_idesc_bf16(BM, BN, true, true);
       int stage = 0;
       uint32_t phase = 0;
@@ -1543,25 +1554,29 @@ __global__ void __launch_bounds__(192, 1)
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
           const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
+          if (elect_one_sync()) {
 #pragma unroll
-          for (int k = 0; k < C::KSTEPS; ++k) {
-            const uint32_t acc = (pb != pb_lo) || (k != 0);
-            const uint64_t bd = make_sdesc(b0 + k * 2048, C::DCHUNK, 1024, LAYOUT_SW128);
-            const uint64_t ad0 = make_sdesc(a0 + k * C::XKSTEP, C::XCHUNK, C::XSBO, C::XLAYOUT);
-            umma_bf16(tmem_base, ad0, bd, idesc, acc);
-            if (second) {
-              const uint64_t ad1 =
-                  make_sdesc(a0 + (C::NXC / 2) * C::XCHUNK + k * C::XKSTEP, C::XCHUNK, C::XSBO, C::XLAYOUT);
-              umma_bf16(tmem_base + BN, ad1, bd, idesc, acc);
+            for (int k = 0; k < C::KSTEPS; ++k) {
+              const uint32_t acc = (pb != pb_lo) || (k != 0);
+              const uint64_t bd = make_sdesc(b0 + k * 2048, C::DCHUNK, 1024, LAYOUT_SW128);
+              const uint64_t ad0 = make_sdesc(a0 + k * C::XKSTEP, C::XCHUNK, C::XSBO, C::XLAYOUT);
+              umma_bf16(tmem_base, ad0, bd, idesc, acc);
+              if (second) {
+                const uint64_t ad1 =
+                    make_sdesc(a0 + (C::NXC / 2) * C::XCHUNK + k * C::XKSTEP, C::XCHUNK, C::XSBO, C::XLAYOUT);
+                umma_bf16(tmem_base + BN, ad1, bd, idesc, acc);
+              }
             }
+            umma_commit(&empty[stage]);
           }
-          umma_commit(&empty[stage]);
+          __syncwarp();
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(tfull);
+        if (elect_one_sync()) umma_commit(tfull);
+        __syncwarp();
       }
     }
   } else {
@@ -1720,7 +1735,7 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {   // converged warp, elected issuer (see the row-tap fprop kernel)
       constexpr uint32_t idesc = make_idesc_bf16(128, 64, true, true);
       int stage = 0;
       uint32_t phase = 0;
@@ -1731,19 +1746,23 @@ __global__ void __launch_bounds__(192, 1)
         const uint64_t ad0 = make_sdesc(x0, xbox, 1024, LAYOUT_SW128);
         const uint64_t bd0 = make_sdesc(x0 + 2 * xbox, 16384, 1024, LAYOUT_SW128);
         const uint32_t acc = pb > pb_lo;
-        for (int i = 0; i < taps; ++i) {
-          const uint64_t ai = ad0 + ((i * HW_BW * 128) >> 4);
+        if (elect_one_sync()) {
+          for (int i = 0; i < taps; ++i) {
+            const uint64_t ai = ad0 + ((i * HW_BW * 128) >> 4);
 #pragma unroll
-          for (int k = 0; k < HW_BW * HW_BH / 16; ++k)  // 16 pixels (2 KB) per K step
-            umma_bf16(tmem_base + i * 64, ai + k * 128, bd0 + k * 128, idesc, acc | k);
+            for (int k = 0; k < HW_BW * HW_BH / 16; ++k)  // 16 pixels (2 KB) per K step
+              umma_bf16(tmem_base + i * 64, ai + k * 128, bd0 + k * 128, idesc, acc | k);
+          }
+          umma_commit(&empty[stage]);
         }
-        umma_commit(&empty[stage]);
+        __syncwarp();
         if (++stage == stages) {
           stage = 0;
           phase ^= 1;
         }
       }
-      umma_commit(tfull);
+      if (elect_one_sync()) umma_commit(tfull);
+      __syncwarp();
     }
   } else {
     const int t = threadIdx.x - 64;  // 0..127
@@ -1874,7 +1893,7 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {   // converged warp, elected issuer (see the row-tap fprop kernel)
       constexpr uint32_t idesc = make_idesc_bf16(128, BN, true, true);
       int stage = 0;
       uint32_t phase = 0;
@@ -1885,19 +1904,23 @@ __global__ void __launch_bounds__(192, 1)
         const uint64_t ad0 = make_sdesc(x0, xbox, 1024, LAYOUT_SW128);
         const uint64_t bd0 = make_sdesc(x0 + 2 * xbox, 16384, 1024, LAYOUT_SW128);
         const uint32_t acc = pb > pb_lo;
-        for (int i = 0; i < kh; ++i) {
-          const uint64_t ai = ad0 + ((i * p.dil * HW_BW * 128) >> 4);
+        if (elect_one_sync()) {
+          for (int i = 0; i < kh; ++i) {
+            const uint64_t ai = ad0 + ((i * p.dil * HW_BW * 128) >> 4);
 #pragma unroll
-          for (int k = 0; k < HW_BW * HW_BH / 16; ++k)  // 16 pixels (2 KB) per K step
-            umma_bf16(tmem_base + i * BN, ai + k * 128, bd0 + k * 128, idesc, acc | k);
+            for (int k = 0; k < HW_BW * HW_BH / 16; ++k)  // 16 pixels (2 KB) per K step
+              umma_bf16(tmem_base + i * BN, ai + k * 128, bd0 + k * 128, idesc, acc | k);
+          }
+          umma_commit(&empty[stage]);
         }
-        umma_commit(&empty[stage]);
+        __syncwarp();
         if (++stage == stages) {
           stage = 0;
           phase ^= 1;
         }
       }
-      umma_commit(tfull);
+      if (elect_one_sync()) umma_commit(tfull);
+      __syncwarp();
     }
   } else {
     const int t = threadIdx.x - 64;  // 0..127
