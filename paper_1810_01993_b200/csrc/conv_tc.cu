@@ -950,7 +950,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
   const int unit0 = blockIdx.x / CG, units = gridDim.x / CG;
 
   if (warp == 0) {
-    if (lane == 0) {
+    {   // converged producer warp: waits and coordinates warp-uniform, one elected lane issues
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = unit0; tile < p.num_tiles; tile += units) {
@@ -966,7 +966,9 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
           uint8_t* a_dst = sA + stage * C::A_BYTES;
           uint8_t* b_dst = sB + stage * C::B_BYTES;
           const int ax = x0 * p.in_stride + j * p.dil - p.pad_left, ay = y0 * p.in_stride + i * p.dil - p.pad_top;
-          if constexpr (CG == 2) {
+          if (!elect_one_sync()) {
+            // the other lanes only keep the stage / phase walk
+          } else if constexpr (CG == 2) {
             // both CTAs' loads complete on the even CTA's barrier, which expects both halves
             if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
             const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
@@ -993,6 +995,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
               tma_load_2d(b_dst, &tmB, &full[stage], tap * p.cin_pad + cb * KBLK, n0);
             }
           }
+          __syncwarp();
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -1130,11 +1133,14 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
   const int per_img = p.tiles_x * p.tiles_y;
 
   if (warp == 0) {
-    if (lane == 0) {
-      mbar_arrive_expect_tx(bfull, taps * nh * HALO_BBOX);
-      for (int i = 0; i < taps; ++i)
-        for (int h = 0; h < nh; ++h)
-          tma_load_2d(sB + (i * nh + h) * HALO_BBOX, &tmB, bfull, i * p.cin_pad + h * 64, 0);
+    {   // converged producer warp, elected issuer
+      if (elect_one_sync()) {
+        mbar_arrive_expect_tx(bfull, taps * nh * HALO_BBOX);
+        for (int i = 0; i < taps; ++i)
+          for (int h = 0; h < nh; ++h)
+            tma_load_2d(sB + (i * nh + h) * HALO_BBOX, &tmB, bfull, i * p.cin_pad + h * 64, 0);
+      }
+      __syncwarp();
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
@@ -1142,8 +1148,12 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
         const int ty = r / p.tiles_x, tx = r - ty * p.tiles_x;
         for (int h = 0; h < nh; ++h) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], a_stage);
-          tma_load_4d(sA + stage * a_stage, &tmA, &full[stage], h * 64, tx * HALO_BW, ty * HALO_BH - p.pad_top, img);
+          if (elect_one_sync()) {
+            mbar_arrive_expect_tx(&full[stage], a_stage);
+            tma_load_4d(sA + stage * a_stage, &tmA, &full[stage], h * 64, tx * HALO_BW, ty * HALO_BH - p.pad_top,
+                        img);
+          }
+          __syncwarp();
           if (++stage == p.stages) {
             stage = 0;
             phase ^= 1;
@@ -1284,8 +1294,8 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
   const int n0 = rank * (BN / CG);        // this CTA's weight rows
 
   if (warp == 0) {
-    if (lane == 0) {
-      if (resident) {
+    {   // converged producer warp: waits and coordinates warp-uniform, one elected lane issues
+      if (resident && elect_one_sync()) {
         if constexpr (CG == 2) {   // both halves complete on the even CTA's barrier
           if (rank == 0) mbar_arrive_expect_tx(bfull, 2 * p.taps * p.num_cblk * b_box);
           const uint32_t fb = mapa_shared(smem_u32(bfull), 0);
@@ -1299,6 +1309,7 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
               tma_load_2d(sW + (t * p.num_cblk + cb) * b_box, &tmB, bfull, t * p.cin_pad + cb * KB, 0);
         }
       }
+      __syncwarp();
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = unit0; tile < p.num_tiles; tile += units) {
@@ -1310,20 +1321,24 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* dst = sS + stage * stage_bytes;
           const int ax = tx * RT_BW + j * p.dil - p.pad_left, ay = ty * RT_BH - p.pad_top;
-          if constexpr (CG == 2) {
-            if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * stage_bytes);
-            const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
-            tma_load_4d_pair(dst, &tmA, fb, cb * KB, ax, ay, img);
-            if (!resident)
-              for (int i = 0; i < kh; ++i)
-                tma_load_2d_pair(dst + a_stage + i * b_box, &tmB, fb, (i * p.kw + j) * p.cin_pad + cb * KB, n0);
-          } else {
-            mbar_arrive_expect_tx(&full[stage], stage_bytes);
-            tma_load_4d(dst, &tmA, &full[stage], cb * KB, ax, ay, img);
-            if (!resident)
-              for (int i = 0; i < kh; ++i)
-                tma_load_2d(dst + a_stage + i * b_box, &tmB, &full[stage], (i * p.kw + j) * p.cin_pad + cb * KB, 0);
+          if (elect_one_sync()) {
+            if constexpr (CG == 2) {
+              if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * stage_bytes);
+              const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
+              tma_load_4d_pair(dst, &tmA, fb, cb * KB, ax, ay, img);
+              if (!resident)
+                for (int i = 0; i < kh; ++i)
+                  tma_load_2d_pair(dst + a_stage + i * b_box, &tmB, fb, (i * p.kw + j) * p.cin_pad + cb * KB, n0);
+            } else {
+              mbar_arrive_expect_tx(&full[stage], stage_bytes);
+              tma_load_4d(dst, &tmA, &full[stage], cb * KB, ax, ay, img);
+              if (!resident)
+                for (int i = 0; i < kh; ++i)
+                  tma_load_2d(dst + a_stage + i * b_box, &tmB, &full[stage], (i * p.kw + j) * p.cin_pad + cb * KB,
+                              0);
+            }
           }
+          __syncwarp();
           if (++stage == p.stages) {
             stage = 0;
             phase ^= 1;
@@ -1490,7 +1505,7 @@ __global__ void __launch_bounds__(192, 1)
   const int per_img = p.pbx * p.pby;
 
   if (warp == 0) {
-    if (lane == 0) {
+    {   // converged producer warp, elected issuer
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
@@ -1506,6 +1521,7 @@ __global__ void __launch_bounds__(192, 1)
           const int by = r / p.pbx, bx = r - by * p.pbx;
           const int x0 = bx * p.bwk, y0 = by * p.bhk;
           mbar_wait(&empty[stage], phase ^ 1);
+          if (elect_one_sync()) {
           mbar_arrive_expect_tx(&full[stage], tx_bytes);
           // few large TMA ops: a 5-D map loads xg (dyg) 64-channel chunks of one tap per op
           const int xstep = p.xg ? p.xg : 1;
@@ -1528,6 +1544,8 @@ __global__ void __launch_bounds__(192, 1)
               tma_load_4d(sB + stage * C::B_BYTES + qq * C::DCHUNK, &tmDY, &full[stage], nt * BN + qq * 64, x0, y0,
                           img);
           }
+          }
+          __syncwarp();
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -1716,18 +1734,21 @@ __global__ void __launch_bounds__(192, 1)
   const int per_img = p.pbx * p.pby;
 
   if (warp == 0) {
-    if (lane == 0) {
+    {   // converged producer warp, elected issuer
       int stage = 0;
       uint32_t phase = 0;
       for (int pb = pb_lo; pb < pb_hi; ++pb) {
         const int img = pb / per_img, r = pb - img * per_img;
         const int by = r / p.pbx, bx = r - by * p.pbx;
         mbar_wait(&empty[stage], phase ^ 1);
-        mbar_arrive_expect_tx(&full[stage], stage_bytes);
-        uint8_t* st = smem + stage * stage_bytes;
-        for (int h = 0; h < 2; ++h)
-          tma_load_4d(st + h * xbox, &tmX, &full[stage], h * 64, bx * HW_BW, by * HW_BH - p.pad_top, img);
-        tma_load_4d(st + 2 * xbox, &tmDY, &full[stage], 0, bx * HW_BW, by * HW_BH, img);
+        if (elect_one_sync()) {
+          mbar_arrive_expect_tx(&full[stage], stage_bytes);
+          uint8_t* st = smem + stage * stage_bytes;
+          for (int h = 0; h < 2; ++h)
+            tma_load_4d(st + h * xbox, &tmX, &full[stage], h * 64, bx * HW_BW, by * HW_BH - p.pad_top, img);
+          tma_load_4d(st + 2 * xbox, &tmDY, &full[stage], 0, bx * HW_BW, by * HW_BH, img);
+        }
+        __syncwarp();
         if (++stage == stages) {
           stage = 0;
           phase ^= 1;
@@ -1871,21 +1892,24 @@ __global__ void __launch_bounds__(192, 1)
   const int per_img = p.pbx * p.pby;
 
   if (warp == 0) {
-    if (lane == 0) {
+    {   // converged producer warp, elected issuer
       int stage = 0;
       uint32_t phase = 0;
       for (int pb = pb_lo; pb < pb_hi; ++pb) {
         const int img = pb / per_img, r = pb - img * per_img;
         const int by = r / p.pbx, bx = r - by * p.pbx;
         mbar_wait(&empty[stage], phase ^ 1);
-        mbar_arrive_expect_tx(&full[stage], stage_bytes - (2 - nh) * xbox);
-        uint8_t* st = smem + stage * stage_bytes;
-        for (int h = 0; h < nh; ++h) {   // a missing second half computes rows nobody writes back
-          const int jj = (c0 + h) / p.cblk, cb = (c0 + h) - jj * p.cblk;
-          tma_load_4d(st + h * xbox, &tmX, &full[stage], cb * 64, bx * HW_BW + jj * p.dil - p.pad_left,
-                      by * HW_BH - p.pad_top, img);
+        if (elect_one_sync()) {
+          mbar_arrive_expect_tx(&full[stage], stage_bytes - (2 - nh) * xbox);
+          uint8_t* st = smem + stage * stage_bytes;
+          for (int h = 0; h < nh; ++h) {   // a missing second half computes rows nobody writes back
+            const int jj = (c0 + h) / p.cblk, cb = (c0 + h) - jj * p.cblk;
+            tma_load_4d(st + h * xbox, &tmX, &full[stage], cb * 64, bx * HW_BW + jj * p.dil - p.pad_left,
+                        by * HW_BH - p.pad_top, img);
+          }
+          tma_load_4d(st + 2 * xbox, &tmDY, &full[stage], 0, bx * HW_BW, by * HW_BH, img);
         }
-        tma_load_4d(st + 2 * xbox, &tmDY, &full[stage], 0, bx * HW_BW, by * HW_BH, img);
+        __syncwarp();
         if (++stage == stages) {
           stage = 0;
           phase ^= 1;
