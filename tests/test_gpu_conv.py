@@ -134,9 +134,9 @@ def test_master_layout_weight_modes(case):
     dx1 = torch.zeros_like(dx0)
     nhwc.conv_dgrad(nhwc.View(dy), wd, cin, k, k, d, nhwc.View(dx0))
     nhwc.conv_dgrad(nhwc.View(dy), None, cin, k, k, d, nhwc.View(dx1), w_master=wm)
-    # a narrow packed dgrad (cin <= 64) runs on the row-tap kernel: same products, another fp32
+    # a narrow packed dgrad (cin <= 128) runs on the row-tap kernel: same products, another fp32
     # summation order, so single bf16 output ulps may differ
-    assert _rel(dx1, dx0) < (5e-3 if cin <= 64 and k > 1 else 1e-6)
+    assert _rel(dx1, dx0) < (5e-3 if cin <= 128 and k > 1 else 1e-6)
 
 
 @pytest.mark.parametrize("case", [(1, 256, 36, 24, 256, 3, 4), (2, 128, 24, 48, 512, 3, 2), (1, 64, 9, 13, 320, 1, 1),
@@ -420,7 +420,9 @@ def test_kblk32_fprop_and_dgrad_vs_fp64(c32, k, cout):
                                                   (48, 32, 5, 2, "a", (37, 45)), (40, 24, 5, 1, "", (37, 45)),
                                                   (416, 32, 5, 1, "", (4, 3)), (96, 32, 5, 1, "", (8, 6)),
                                                   (64, 32, 5, 1, "", (16, 12)), (64, 64, 3, 1, "m", (37, 45)),
-                                                  (64, 64, 3, 2, "rm", (37, 45)), (48, 32, 3, 1, "a", (20, 30))])
+                                                  (64, 64, 3, 2, "rm", (37, 45)), (48, 32, 3, 1, "a", (20, 30)),
+                                                  (32, 96, 5, 1, "m", (37, 45)), (32, 128, 5, 1, "", (20, 30)),
+                                                  (128, 128, 3, 1, "rm", (37, 45)), (64, 80, 3, 2, "a", (16, 12))])
 def test_rowtap_fprop_vs_fp64(cin, cout, k, d, ops, hw):
     """Narrow-output convs through the row-tap kernel (one tall input box per column tap and
     channel block, row taps at 1 KB offsets): bias, relu, residual / mask / accumulate epilogue
