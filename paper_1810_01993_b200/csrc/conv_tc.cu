@@ -2383,7 +2383,7 @@ static bool rowtap_fprop_ok(const b2dl_conv_args* a, const b2dl_act& x) {
   const b2dl_act& y = a->y;
   const int nops = (a->residual.ptr != nullptr) + (a->mask.ptr != nullptr) + (a->accumulate != 0);
   return rowtap_enabled() && !a->window && a->w_mode == 0 && a->w_packed && a->kh >= rowtap_min_kh() &&
-         a->cout <= 128 &&
+         (a->cout <= 128 || (a->cout <= 256 && x.c <= 64)) &&   // wide N only over a narrow K
          a->cout % 8 == 0 && x.c > 16 && RT_BH + (a->kh - 1) * a->dilation <= 256 &&
          (a->in_stride <= 1) && (a->out_stride <= 1) && !a->bn_partial && !a->bnb_stats &&
          (!a->bias || (reinterpret_cast<uintptr_t>(a->bias) % 16 == 0)) && !a->y_f32 && view_aligned(y, 2) &&
@@ -2393,7 +2393,7 @@ static bool rowtap_fprop_ok(const b2dl_conv_args* a, const b2dl_act& x) {
 
 static int launch_rowtap_fprop(const b2dl_conv_args* a, const b2dl_act& x, cudaStream_t st) {
   const b2dl_act& y = a->y;
-  const int bn = a->cout <= 32 ? 32 : a->cout <= 64 ? 64 : 128;
+  const int bn = a->cout <= 32 ? 32 : a->cout <= 64 ? 64 : a->cout <= 128 ? 128 : 256;
   FpropParams p{};
   p.n = y.n;
   p.h = y.h;
@@ -2461,16 +2461,18 @@ static int launch_rowtap_fprop(const b2dl_conv_args* a, const b2dl_act& x, cudaS
   decltype(&conv_rowtap_fprop_kernel<32, 64>) kern;
 #define B2_RT(BNV, KBV, CGV) conv_rowtap_fprop_kernel<BNV, KBV, CGV>
   if (cg == 2)
-    kern = bn == 32   ? (kb == 64 ? B2_RT(32, 64, 2) : B2_RT(32, 32, 2))
-           : bn == 64 ? (kb == 64 ? B2_RT(64, 64, 2) : B2_RT(64, 32, 2))
-                      : (kb == 64 ? B2_RT(128, 64, 2) : B2_RT(128, 32, 2));
+    kern = bn == 32    ? (kb == 64 ? B2_RT(32, 64, 2) : B2_RT(32, 32, 2))
+           : bn == 64  ? (kb == 64 ? B2_RT(64, 64, 2) : B2_RT(64, 32, 2))
+           : bn == 128 ? (kb == 64 ? B2_RT(128, 64, 2) : B2_RT(128, 32, 2))
+                       : (kb == 64 ? B2_RT(256, 64, 2) : B2_RT(256, 32, 2));
   else
-    kern = bn == 32   ? (kb == 64 ? B2_RT(32, 64, 1) : B2_RT(32, 32, 1))
-           : bn == 64 ? (kb == 64 ? B2_RT(64, 64, 1) : B2_RT(64, 32, 1))
-                      : (kb == 64 ? B2_RT(128, 64, 1) : B2_RT(128, 32, 1));
+    kern = bn == 32    ? (kb == 64 ? B2_RT(32, 64, 1) : B2_RT(32, 32, 1))
+           : bn == 64  ? (kb == 64 ? B2_RT(64, 64, 1) : B2_RT(64, 32, 1))
+           : bn == 128 ? (kb == 64 ? B2_RT(128, 64, 1) : B2_RT(128, 32, 1))
+                       : (kb == 64 ? B2_RT(256, 64, 1) : B2_RT(256, 32, 1));
 #undef B2_RT
-  static bool attr_set[12] = {};
-  const int ai = (cg == 2) * 6 + (bn == 32 ? 0 : bn == 64 ? 2 : 4) + (kb == 64);
+  static bool attr_set[16] = {};
+  const int ai = (cg == 2) * 8 + (bn == 32 ? 0 : bn == 64 ? 2 : bn == 128 ? 4 : 6) + (kb == 64);
   if (!attr_set[ai]) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX) != cudaSuccess)
       return B2DL_E_CUDA;

@@ -593,13 +593,15 @@ class Engine:
                         and o.out != p.logits_name):
                     self.rowtap.append(o)
                     self.wf[o.w] = torch.zeros((o.cout, o.k * o.k, nhwc.cin_pad(o.cin)), dtype=bf, device=self.device)
-        # ... and narrow input gradients (cin <= 128: the dgrad's output is narrow) with >= 3 tap
-        # rows: packed dgrad weights, so b2dl_conv_fprop runs them on the row-tap kernel too
+        # ... and narrow input gradients (cin <= 128, or <= 256 over a <= 64-channel dy: the dgrad's
+        # output is narrow) with >= 3 tap rows: packed dgrad weights, so b2dl_conv_fprop runs them
+        # on the row-tap kernel too
         self.rowtap_dgrad = []
         rt_dg_max = int(os.environ.get("B2DL_ROWTAP_DGRAD_MAXC", "128"))
         if not self.fp32 and os.environ.get("B2DL_ROWTAP", "1") != "0":
             for o in self.convs:
-                if (o.k >= rt_min_k and o.cin <= rt_dg_max and o.cin % 8 == 0 and o.cout > 16 and o.ins[0] in p.live
+                if (o.k >= rt_min_k and (o.cin <= rt_dg_max or (o.cin <= 256 and o.cout <= 64)) and o.cin % 8 == 0
+                        and o.cout > 16 and o.ins[0] in p.live
                         and o is not self.win and o.w not in self.heads and o.w not in self.wd
                         and o.out not in self.up_fprop and o.out not in self.up_dgrad):
                     self.rowtap_dgrad.append(o)
