@@ -2547,16 +2547,23 @@ static void fprop_choose(const b2dl_conv_args* a, const b2dl_act& x, int kblk, i
     // weighted by the relative speed of each tile shape
     const int bw = fprop_tile_w(x.w, a->in_stride > 0 ? a->in_stride : 1);
     const long long mt = static_cast<long long>(x.n) * cdiv(x.w, bw) * cdiv(x.h, BM / bw);
+    // ... and by the share of computed columns that are real output channels (N padding)
     auto score = [&](int b, int g, double speed) {
       const long long units = (mt + g - 1) / g * cdiv(a->cout, b), slots = num_sms() / g;
       const long long waves = (units + slots - 1) / slots;
-      return speed * static_cast<double>(units) / (waves * slots);
+      const double cols = static_cast<double>(a->cout) / (cdiv(a->cout, b) * b);
+      return speed * cols * static_cast<double>(units) / (waves * slots);
     };
     struct Cand {
       int b, g;
       double speed;
     };
-    const Cand cands[3] = {{256, 2, 1.0}, {128, 2, 0.6}, {128, 1, 0.7}};
+    // relative speeds measured with tools/prof_tiles.py: 128-wide tiles run at ~0.6 of the 256-wide
+    // pair on long-K (tensor-bound) launches, but at par on short-K (epilogue / HBM-bound) ones
+    // (e.g. 96 -> 320 channels at full resolution: 404 us on 128-wide tiles, 487 us on 256-pairs)
+    const int taps = a->kh * a->kw;
+    const bool short_k = taps * cdiv(x.c, kblk) <= 4;
+    const Cand cands[3] = {{256, 2, 1.0}, {128, 2, short_k ? 0.85 : 0.6}, {128, 1, short_k ? 1.0 : 0.7}};
     double best = -1.0;
     for (const Cand& c : cands) {
       if (c.b > bn || (c.g == 2 && !pair_ok(c.b)) || (c.b == 256 && a->cout <= 128)) continue;
