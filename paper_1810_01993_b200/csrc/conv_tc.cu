@@ -1054,7 +1054,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
     }
   } else {
     if constexpr (EW == 16)
-      fprop_epilogue_tma<BN, CG, 16>(p, &tmY, &tmR, &tmM, tmem_base, tfull, tempty, inbar, epi, warp, rank, unit0,
+      fprop_epilogue_tma<BN, CG, 16, ST>(p, &tmY, &tmR, &tmM, tmem_base, tfull, tempty, inbar, epi, warp, rank, unit0,
                                      units);
     else
       fprop_epilogue_role<BN, CG, ST>(p, &tmY, &tmR, &tmM, tmem_base, tfull, tempty, inbar, epi, warp, rank, unit0,
@@ -2755,6 +2755,16 @@ extern "C" int b2dl_conv_fprop(const b2dl_conv_args* a, void* stream) {
   // operand ring that 8 warps' smaller buffers leave room for
   if (p.bn_part || p.bnb_stats) {   // statistics epilogues: 8 epilogue warps, 64-wide K blocks
     const int stv = p.bn_part ? 1 : 2;
+    // forward statistics on short-K launches: 16 epilogue warps, as for the plain epilogue
+    if (stv == 1 && p.tma_epi && nops <= ew16_max_nops() && p.num_kb <= 16 && ew16_enabled() &&
+        env_int("B2DL_ST_EW16", 1)) {
+      if (cg == 2 && bn == 256)
+        return mode == 1 ? launch_fprop<256, 64, true, 2, 16, 1>(t, p, st) : launch_fprop<256, 64, false, 2, 16, 1>(t, p, st);
+      if (cg == 1 && bn == 256)
+        return mode == 1 ? launch_fprop<256, 64, true, 1, 16, 1>(t, p, st) : launch_fprop<256, 64, false, 1, 16, 1>(t, p, st);
+      if (cg == 1 && bn == 128)
+        return mode == 1 ? launch_fprop<128, 64, true, 1, 16, 1>(t, p, st) : launch_fprop<128, 64, false, 1, 16, 1>(t, p, st);
+    }
 #define B2_FPROP_ST(BNV, CGV, STV)                                                                    \
   if (bn == BNV && cg == CGV && kblk == 64 && stv == STV)                                             \
     return mode == 1 ? launch_fprop<BNV, 64, true, CGV, 8, STV>(t, p, st)                             \

@@ -424,13 +424,13 @@ def test_kblk32_fprop_and_dgrad_vs_fp64(c32, k, cout):
                                                   (32, 96, 5, 1, "m", (37, 45)), (32, 128, 5, 1, "", (20, 30)),
                                                   (128, 128, 3, 1, "rm", (37, 45)), (64, 80, 3, 2, "a", (16, 12)),
                                                   (32, 192, 5, 1, "m", (20, 30)), (32, 256, 3, 1, "", (37, 45))])
-def test_rowtap_fprop_vs_fp64(cin, cout, k, d, ops, hw):
+def test_rowtap_fprop_vs_fp64(cin, cout, k, d, ops, hw, n=2):
     """Narrow-output convs through the row-tap kernel (one tall input box per column tap and
     channel block, row taps at 1 KB offsets): bias, relu, residual / mask / accumulate epilogue
     operands, dilation, ragged image edges, against fp64 on the same bf16 operands."""
     from paper_1810_01993_b200 import nhwc
     torch.manual_seed(11)
-    n, (h, w) = 2, hw
+    h, w = hw
     x = torch.randn(n, h, w, cin, device="cuda").to(torch.bfloat16)
     whwio = torch.randn(k * k, cin, cout, device="cuda") / (k * k * cin) ** 0.5
     wp = torch.empty(cout, k * k, nhwc.cin_pad(cin), dtype=torch.bfloat16, device="cuda")
@@ -455,6 +455,14 @@ def test_rowtap_fprop_vs_fp64(cin, cout, k, d, ops, hw):
     if acc:
         ref = ref + y0[..., :cout].permute(0, 3, 1, 2).double()
     assert _rel(y[..., :cout].permute(0, 3, 1, 2), ref) < 1e-2
+
+
+@pytest.mark.parametrize("cin,cout,k,d,ops,hw", [(96, 32, 5, 1, "m", (16, 24)), (32, 128, 3, 1, "", (16, 40)),
+                                                  (64, 64, 3, 1, "r", (48, 8))])
+def test_rowtap_fprop_odd_tile_count(cin, cout, k, d, ops, hw):
+    """One image with an odd number of 8 x 16 tiles: the CTA pair's second tile of the last pair is
+    past the end (zero-filled loads, no stores)."""
+    test_rowtap_fprop_vs_fp64(cin, cout, k, d, ops, hw, n=1)
 
 
 @pytest.mark.parametrize("cin,cout,k,d,hw", [(96, 32, 5, 1, (37, 45)), (416, 32, 5, 1, (64, 48)),
