@@ -125,6 +125,8 @@ struct FpropParams {
   int epi_slots;       // operand slots per sub-group (prefetch depth + 1)
   int epi_pw;          // 1: per-warp epilogue boxes (32 pixels x 32 channels; no sub-group barrier)
   int epi_obufs;       // output buffers per sub-group (2; per-warp mode up to 4)
+  int rt_cs;           // row-tap kernel: width (pixels) of the wide input box whose column taps are
+                       // descriptor offsets (8 + (kw - 1) dil); 0: one 8-pixel box per column tap
   int dbg_epi;         // development: 1 = epilogue only drains TMEM (wrong results; timing aid)
   int bias_vec;        // bias 16-byte aligned
   int in_stride;       // input pixels per output pixel (strided reads of the input)
@@ -1234,7 +1236,8 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
   constexpr int ROW = RT_BW * KB * 2;              // bytes per image row of the tall box
   constexpr uint32_t LAYOUT = KB == 64 ? LAYOUT_SW128 : LAYOUT_SW64;
   constexpr uint32_t SBO = 8 * KB * 2;             // 8 rows of KB bf16
-  const int a_stage = (RT_BH + (kh - 1) * p.dil) * ROW;
+  const int row_b = p.rt_cs ? p.rt_cs * KB * 2 : ROW;   // bytes per image row of the staged box
+  const int a_stage = (RT_BH + (kh - 1) * p.dil) * row_b;
   const int b_box = (BN / CG) * KB * 2;          // this CTA's weight rows of one (tap, K block)
   const bool resident = p.b_region > 0;
   const int stage_bytes = a_stage + (resident ? 0 : kh * b_box);
@@ -1289,7 +1292,10 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
   griddep_launch_dependents();
   griddep_wait();
   const int per_img = p.tiles_x * p.tiles_y;
-  const int nsteps = p.kw * p.num_cblk;   // (column tap, channel block) stages per tile
+  // stages per tile: (column tap, channel block); with the wide box and resident weights one box
+  // per channel block serves every column tap (descriptor start + j * dil pixels)
+  const bool reuse = p.rt_cs && resident;
+  const int nsteps = reuse ? p.num_cblk : p.kw * p.num_cblk;
   const int unit0 = blockIdx.x / CG, units = gridDim.x / CG;
   const int n0 = rank * (BN / CG);        // this CTA's weight rows
 
@@ -1317,10 +1323,10 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
         const int img = mt / per_img, r = mt - img * per_img;
         const int ty = r / p.tiles_x, tx = r - ty * p.tiles_x;
         for (int st = 0; st < nsteps; ++st) {
-          const int j = st / p.num_cblk, cb = st - j * p.num_cblk;
+          const int j = reuse ? 0 : st / p.num_cblk, cb = st - j * p.num_cblk;
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* dst = sS + stage * stage_bytes;
-          const int ax = tx * RT_BW + j * p.dil - p.pad_left, ay = ty * RT_BH - p.pad_top;
+          const int ax = tx * RT_BW + (p.rt_cs ? 0 : j * p.dil) - p.pad_left, ay = ty * RT_BH - p.pad_top;
           if (elect_one_sync()) {
             if constexpr (CG == 2) {
               if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * stage_bytes);
@@ -1362,25 +1368,31 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
         tc_fence_after();
         const uint32_t d = tmem_base + as * BN;
         for (int st = 0; st < nsteps; ++st) {
-          const int j = st / p.num_cblk, cb = st - j * p.num_cblk;
+          const int j0 = reuse ? 0 : st / p.num_cblk, cb = st - j0 * p.num_cblk;
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a0 = smem_u32(sS + stage * stage_bytes);
-          const uint64_t ad0 = make_sdesc(a0, 16, SBO, LAYOUT);
           if (elect_one_sync()) {
-            for (int i = 0; i < kh; ++i) {
-              // row tap i: the tall box shifted down i*dil image rows (one swizzle atom each);
-              // descriptors advance by (byte offset >> 4) in their start-address field
-              const uint64_t ai = ad0 + ((i * p.dil * ROW) >> 4);
-              const uint32_t b0 = resident ? smem_u32(sW + ((i * p.kw + j) * p.num_cblk + cb) * b_box)
-                                           : a0 + a_stage + i * b_box;
-              const uint64_t bi = make_sdesc(b0, 16, SBO, LAYOUT);
+            for (int jj = 0; jj < (reuse ? p.kw : 1); ++jj) {
+              const int j = j0 + jj;
+              // wide box: column tap j starts j * dil pixels (128 B each) into every box row; the
+              // 128B swizzle follows the address bits, so no descriptor base offset is involved
+              const int cs = p.rt_cs ? j * p.dil : 0;
+              const uint64_t ad0 = make_sdesc(a0 + cs * 128, 16, p.rt_cs ? row_b : SBO, LAYOUT);
+              for (int i = 0; i < kh; ++i) {
+                // row tap i: the tall box shifted down i*dil image rows (whole swizzle atoms);
+                // descriptors advance by (byte offset >> 4) in their start-address field
+                const uint64_t ai = ad0 + ((i * p.dil * row_b) >> 4);
+                const uint32_t b0 = resident ? smem_u32(sW + ((i * p.kw + j) * p.num_cblk + cb) * b_box)
+                                             : a0 + a_stage + i * b_box;
+                const uint64_t bi = make_sdesc(b0, 16, SBO, LAYOUT);
 #pragma unroll
-              for (int k = 0; k < KB / 16; ++k) {
-                if constexpr (CG == 2)
-                  umma_bf16_pair(d, ai + 2 * k, bi + 2 * k, idesc, (st | i | k) != 0);
-                else
-                  umma_bf16(d, ai + 2 * k, bi + 2 * k, idesc, (st | i | k) != 0);
+                for (int k = 0; k < KB / 16; ++k) {
+                  if constexpr (CG == 2)
+                    umma_bf16_pair(d, ai + 2 * k, bi + 2 * k, idesc, (st | jj | i | k) != 0);
+                  else
+                    umma_bf16(d, ai + 2 * k, bi + 2 * k, idesc, (st | jj | i | k) != 0);
+                }
               }
             }
             if constexpr (CG == 2)
@@ -2435,12 +2447,23 @@ static int launch_rowtap_fprop(const b2dl_conv_args* a, const b2dl_act& x, cudaS
   p.epi_nops = (p.res != nullptr) + (p.mask != nullptr) + (p.accumulate != 0);
   p.epi_slots = 2;
   p.epi_bytes = 2 * epi_sub_bytes(p.epi_nops, 2);
-  const int a_stage = (RT_BH + (a->kh - 1) * a->dilation) * RT_BW * kb * 2;
+  // wide box (SW128 only): 8 + (kw - 1) dil pixels per row (B2DL_RT_COLSHIFT=2: 16, 0: off); the
+  // 8-row core matrices then start at any 128-byte row, which the address-based swizzle allows
+  static const int rt_cs_env = env_int("B2DL_RT_COLSHIFT", 1);
+  const int wide = RT_BW + (a->kw - 1) * a->dilation;
+  p.rt_cs = (rt_cs_env && kb == 64 && wide <= 2 * RT_BW) ? (rt_cs_env == 2 ? 2 * RT_BW : wide) : 0;
+  const int box_rows = RT_BH + (a->kh - 1) * a->dilation;
+  int a_stage = box_rows * (p.rt_cs ? p.rt_cs : RT_BW) * kb * 2;
   const int b_box = (bn / cg) * kb * 2;   // per CTA: a pair splits the weight rows
   // weights resident when they fit beside >= 3 input stages, else streamed with each stage
   const int w_bytes = (p.taps * p.num_cblk * b_box + 1023) / 1024 * 1024;
   const int room = SMEM_MAX - SMEM_FIXED - p.epi_bytes;
   p.b_region = (w_bytes + 3 * a_stage <= room && rowtap_resident_enabled()) ? w_bytes : 0;
+  if (!p.b_region && p.rt_cs) {   // the wide box pays only when it is reused (resident weights)
+    p.rt_cs = 0;
+    a_stage = box_rows * RT_BW * kb * 2;
+    p.b_region = (w_bytes + 3 * a_stage <= room && rowtap_resident_enabled()) ? w_bytes : 0;
+  }
   const int stage_bytes = a_stage + (p.b_region ? 0 : a->kh * b_box);
   p.stages = std::min(FPROP_MAX_STAGES, (room - p.b_region) / stage_bytes);
   if (p.stages < 2) return B2DL_E_NOT_IMPLEMENTED;
@@ -2452,7 +2475,7 @@ static int launch_rowtap_fprop(const b2dl_conv_args* a, const b2dl_act& x, cudaS
   const uint64_t wsd[1] = {ktot * 2};
   const uint32_t wb[2] = {static_cast<uint32_t>(kb), static_cast<uint32_t>(bn / cg)};
   const CUtensorMapSwizzle sw = kb == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
-  if (act_map(&t.a, x, kb, RT_BW, RT_BH + (a->kh - 1) * a->dilation, sw) ||
+  if (act_map(&t.a, x, kb, p.rt_cs ? p.rt_cs : RT_BW, RT_BH + (a->kh - 1) * a->dilation, sw) ||
       encode_tiled(&t.b, B2H_TMA, 2, const_cast<void*>(a->w_packed), wd, wsd, wb, sw) ||
       act_map(&t.y, y, 32, RT_BW, RT_BH, CU_TENSOR_MAP_SWIZZLE_64B) ||
       (p.res && act_map(&t.r, a->residual, 32, RT_BW, RT_BH, CU_TENSOR_MAP_SWIZZLE_64B)) ||
