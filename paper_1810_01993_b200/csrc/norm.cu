@@ -96,12 +96,8 @@ __global__ void __launch_bounds__(BN_THREADS) k_bn_reduce(const T* __restrict__ 
       }
     }
     if (threadIdx.x < rows * lanes) {
-      for (long long p = p0 + row; p < p1; p += rows) {
-        float xv[V];
-        Vec<T, V>::load(x + p * xs + g * V, xv);
+      auto accum = [&](const float* xv, const float* gv) {
         if constexpr (BWD) {
-          float gv[V];
-          Vec<T, V>::load(gy + p * gs + g * V, gv);
 #pragma unroll
           for (int e = 0; e < V; ++e) {
             s[e] += gv[e];
@@ -114,6 +110,53 @@ __global__ void __launch_bounds__(BN_THREADS) k_bn_reduce(const T* __restrict__ 
             q[e] += static_cast<double>(xv[e]) * xv[e];
           }
         }
+      };
+      // U pixels' loads in flight per thread (one load in flight left the pass latency-bound)
+      constexpr int U = BWD ? 4 : 8;   // two input streams backward, one forward
+      long long p = p0 + row;
+      for (; p + (U - 1) * rows < p1; p += U * rows) {
+        float xv[U][V], gv[U][V];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          Vec<T, V>::load(x + (p + u * rows) * xs + g * V, xv[u]);
+          if constexpr (BWD) Vec<T, V>::load(gy + (p + u * rows) * gs + g * V, gv[u]);
+        }
+        // the U pixels are summed in fp32 first (fixed order), then folded into the fp64 sums:
+        // a quarter of the f32 -> f64 conversions and fp64 adds, which bound the pass
+        float sf[V], qf[V];
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          if constexpr (BWD) {
+            sf[e] = gv[0][e];
+            qf[e] = gv[0][e] * ((xv[0][e] - mean[e]) * rstd[e]);
+          } else {
+            sf[e] = xv[0][e];
+            qf[e] = xv[0][e] * xv[0][e];
+          }
+        }
+#pragma unroll
+        for (int u = 1; u < U; ++u)
+#pragma unroll
+          for (int e = 0; e < V; ++e) {
+            if constexpr (BWD) {
+              sf[e] += gv[u][e];
+              qf[e] = fmaf(gv[u][e], (xv[u][e] - mean[e]) * rstd[e], qf[e]);
+            } else {
+              sf[e] += xv[u][e];
+              qf[e] = fmaf(xv[u][e], xv[u][e], qf[e]);
+            }
+          }
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          s[e] += sf[e];
+          q[e] += qf[e];
+        }
+      }
+      for (; p < p1; p += rows) {
+        float xv[V], gv[V];
+        Vec<T, V>::load(x + p * xs + g * V, xv);
+        if constexpr (BWD) Vec<T, V>::load(gy + p * gs + g * V, gv);
+        accum(xv, gv);
       }
     }
     if (threadIdx.x < rows * lanes) {
