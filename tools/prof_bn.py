@@ -42,3 +42,15 @@ for (n, h, w, c) in [(2, 1152, 768, 256), (2, 288, 192, 256), (2, 144, 96, 2048)
     print(f"{n}x{h}x{w}x{c} bn_forward+res          {ms * 1e3:7.1f} us  {4 * nb / ms / 1e6:6.0f} GB/s (4 passes)")
     ms = timeit(lambda: nhwc.bn_backward(V(x), V(g), gamma, stats, dg, db, V(dx), ws))
     print(f"{n}x{h}x{w}x{c} bn_backward             {ms * 1e3:7.1f} us  {5 * nb / ms / 1e6:6.0f} GB/s (5 passes)")
+
+# bilinear x4 (decoder -> full resolution, 256 channels) and x2 (ASPP -> decoder)
+for (n, h, w, c, f) in [(2, 288, 192, 256, 4), (2, 144, 96, 256, 2)]:
+    x = torch.randn(n, h, w, c, device="cuda").to(torch.bfloat16)
+    y = torch.empty(n, h * f, w * f, c, dtype=torch.bfloat16, device="cuda")
+    m = torch.randn(n, h, w, c, device="cuda").to(torch.bfloat16)
+    dx = torch.empty_like(x)
+    ms = timeit(lambda: nhwc.bilinear_fwd(V(x), V(y), f))
+    nb = (x.numel() + y.numel()) * 2
+    print(f"bilinear_fwd x{f} {n}x{h}x{w}x{c}  {ms * 1e3:7.1f} us  {nb / ms / 1e6:6.0f} GB/s")
+    ms = timeit(lambda: nhwc.bilinear_bwd(V(y), V(dx), f, mask=V(m), ws=ws))
+    print(f"bilinear_bwd x{f} {n}x{h}x{w}x{c}  {ms * 1e3:7.1f} us  {(nb + m.numel() * 2) / ms / 1e6:6.0f} GB/s (dy+dx+mask)")
