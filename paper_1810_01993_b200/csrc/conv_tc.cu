@@ -412,7 +412,9 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
     return n;
   };
   auto issue = [&](int tile, int j, int slot) {
-    if (issuer) {
+    // per-warp mode: called by the converged warp, one elected lane (lane 0) issues -- no
+    // single-thread issue loop around each TMA instruction; it also owns the bulk groups
+    if (pw ? elect_one_sync() : leader) {
       int img, x, y, nt;
       locate(tile, img, x, y, nt);
       x += wdx;
@@ -452,10 +454,10 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
     int_nt += units_nt;
     if (int_nt >= p.num_n_tiles) int_nt -= p.num_n_tiles;
   };
-  if (issuer)
-    while (itile < p.num_tiles && nv_at(int_nt) == 0) step_tile();
+  // (every lane keeps the cursor: warp-uniform, cheap)
+  while (itile < p.num_tiles && nv_at(int_nt) == 0) step_tile();
   auto issue_next = [&]() {
-    if (!issuer || !nops || itile >= p.num_tiles) return;
+    if (!nops || itile >= p.num_tiles || !(pw || leader)) return;
     issue(itile, ij, islot);
     islot = islot + 1 == S ? 0 : islot + 1;
     if (++ij >= nv_at(int_nt)) {
@@ -703,7 +705,7 @@ __device__ __forceinline__ void fprop_epilogue_tma(const FpropParams& p, const C
       fence_proxy_async();
       if (pw) {
         __syncwarp();
-        if (lane == 0) {
+        if (elect_one_sync()) {   // lane 0 of the converged warp
           tma_store_4d(tmY, ochunk + qoff, c0, x + wdx, y + wdy, img);
           bulk_commit();
         }
