@@ -22,11 +22,37 @@ __global__ void k_larc_norms(const float* __restrict__ w, const float* __restric
   const int t = blockIdx.y;
   const int64_t lo = off[t], hi = off[t + 1];
   double sw = 0.0, sg = 0.0;
-  for (int64_t i = lo + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < hi;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t nth = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  // 16-byte loads over the 4-aligned interior (segments start 64-aligned), each float4's four
+  // squares summed in fp32 and then folded into fp64 (fixed order; a quarter of the f32 -> f64
+  // conversions), two float4 of each tensor in flight; head / tail (or a short segment) element-wise
+  const int64_t a0 = (lo + 3) & ~int64_t(3), a1 = hi & ~int64_t(3);
+  auto one = [&](int64_t i) {
     const double a = w[i], b = g[i];
     sw += a * a;
     sg += b * b;
+  };
+  if (a0 >= a1) {
+    for (int64_t i = lo + tid; i < hi; i += nth) one(i);
+  } else {
+    for (int64_t i = lo + tid; i < a0; i += nth) one(i);
+    const float4* w4 = reinterpret_cast<const float4*>(w);
+    const float4* g4 = reinterpret_cast<const float4*>(g);
+    auto sq4 = [](float4 q) { return fmaf(q.w, q.w, fmaf(q.z, q.z, fmaf(q.y, q.y, q.x * q.x))); };
+    int64_t v = a0 / 4 + tid;
+    for (; v + nth < a1 / 4; v += 2 * nth) {
+      const float4 wa = w4[v], wb = w4[v + nth], ga = g4[v], gb = g4[v + nth];
+      sw += sq4(wa);
+      sw += sq4(wb);
+      sg += sq4(ga);
+      sg += sq4(gb);
+    }
+    for (; v < a1 / 4; v += nth) {
+      sw += sq4(w4[v]);
+      sg += sq4(g4[v]);
+    }
+    for (int64_t i = a1 + tid; i < hi; i += nth) one(i);
   }
   __shared__ double rw[32], rg[32];
   for (int o = 16; o > 0; o >>= 1) {
@@ -128,6 +154,8 @@ __global__ void k_larc_apply(float* __restrict__ w, float* __restrict__ m, const
     else
       larc_one(w, m, g, wb, i, r, beta, wd, grad_scale);
   }
+  // two float4 groups per thread in flight (the loop body is independent per group)
+#pragma unroll 2
   for (int64_t v = a0 / 4 + tid; v < a1 / 4; v += nth) {
     float4 wv = reinterpret_cast<float4*>(w)[v];
     if (!cast_only) {
