@@ -1239,7 +1239,8 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
   constexpr uint32_t LAYOUT = KB == 64 ? LAYOUT_SW128 : LAYOUT_SW64;
   constexpr uint32_t SBO = 8 * KB * 2;             // 8 rows of KB bf16
   const int row_b = p.rt_cs ? p.rt_cs * KB * 2 : ROW;   // bytes per image row of the staged box
-  const int a_stage = (RT_BH + (kh - 1) * p.dil) * row_b;
+  const int a_box = (RT_BH + (kh - 1) * p.dil) * row_b;        // bytes the TMA box delivers
+  const int a_stage = (a_box + 1023) / 1024 * 1024;               // 1 KB-aligned stage buffers
   const int b_box = (BN / CG) * KB * 2;          // this CTA's weight rows of one (tap, K block)
   const bool resident = p.b_region > 0;
   const int stage_bytes = a_stage + (resident ? 0 : kh * b_box);
@@ -1331,14 +1332,14 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
           const int ax = tx * RT_BW + (p.rt_cs ? 0 : j * p.dil) - p.pad_left, ay = ty * RT_BH - p.pad_top;
           if (elect_one_sync()) {
             if constexpr (CG == 2) {
-              if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * stage_bytes);
+              if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * (stage_bytes - (a_stage - a_box)));
               const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
               tma_load_4d_pair(dst, &tmA, fb, cb * KB, ax, ay, img);
               if (!resident)
                 for (int i = 0; i < kh; ++i)
                   tma_load_2d_pair(dst + a_stage + i * b_box, &tmB, fb, (i * p.kw + j) * p.cin_pad + cb * KB, n0);
             } else {
-              mbar_arrive_expect_tx(&full[stage], stage_bytes);
+              mbar_arrive_expect_tx(&full[stage], stage_bytes - (a_stage - a_box));
               tma_load_4d(dst, &tmA, &full[stage], cb * KB, ax, ay, img);
               if (!resident)
                 for (int i = 0; i < kh; ++i)
@@ -1377,10 +1378,10 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
           if (elect_one_sync()) {
             for (int jj = 0; jj < (reuse ? p.kw : 1); ++jj) {
               const int j = j0 + jj;
-              // wide box: column tap j starts j * dil pixels (128 B each) into every box row; the
-              // 128B swizzle follows the address bits, so no descriptor base offset is involved
+              // wide box: column tap j starts j * dil pixels (KB * 2 bytes each) into every box row;
+              // the swizzle follows the address bits, so no descriptor base offset is involved
               const int cs = p.rt_cs ? j * p.dil : 0;
-              const uint64_t ad0 = make_sdesc(a0 + cs * 128, 16, p.rt_cs ? row_b : SBO, LAYOUT);
+              const uint64_t ad0 = make_sdesc(a0 + cs * KB * 2, 16, p.rt_cs ? row_b : SBO, LAYOUT);
               for (int i = 0; i < kh; ++i) {
                 // row tap i: the tall box shifted down i*dil image rows (whole swizzle atoms);
                 // descriptors advance by (byte offset >> 4) in their start-address field
@@ -2449,13 +2450,15 @@ static int launch_rowtap_fprop(const b2dl_conv_args* a, const b2dl_act& x, cudaS
   p.epi_nops = (p.res != nullptr) + (p.mask != nullptr) + (p.accumulate != 0);
   p.epi_slots = 2;
   p.epi_bytes = 2 * epi_sub_bytes(p.epi_nops, 2);
-  // wide box (SW128 only): 8 + (kw - 1) dil pixels per row (B2DL_RT_COLSHIFT=2: 16, 0: off); the
-  // 8-row core matrices then start at any 128-byte row, which the address-based swizzle allows
+  // wide box: 8 + (kw - 1) dil pixels per row (B2DL_RT_COLSHIFT=2: 16, 0: off; SW128 and SW64
+  // alike); the 8-row core matrices then start at any pixel row, which the address-based
+  // swizzle allows
   static const int rt_cs_env = env_int("B2DL_RT_COLSHIFT", 1);
   const int wide = RT_BW + (a->kw - 1) * a->dilation;
-  p.rt_cs = (rt_cs_env && kb == 64 && wide <= 2 * RT_BW) ? (rt_cs_env == 2 ? 2 * RT_BW : wide) : 0;
+  p.rt_cs = (rt_cs_env && wide <= 2 * RT_BW) ? (rt_cs_env == 2 ? 2 * RT_BW : wide) : 0;
   const int box_rows = RT_BH + (a->kh - 1) * a->dilation;
-  int a_stage = box_rows * (p.rt_cs ? p.rt_cs : RT_BW) * kb * 2;
+  // (stage buffers 1 KB aligned: a wide SW64 box on a 256-byte boundary read back wrong in pairs)
+  int a_stage = (box_rows * (p.rt_cs ? p.rt_cs : RT_BW) * kb * 2 + 1023) / 1024 * 1024;
   const int b_box = (bn / cg) * kb * 2;   // per CTA: a pair splits the weight rows
   // weights resident when they fit beside >= 3 input stages, else streamed with each stage
   const int w_bytes = (p.taps * p.num_cblk * b_box + 1023) / 1024 * 1024;
@@ -2463,7 +2466,7 @@ static int launch_rowtap_fprop(const b2dl_conv_args* a, const b2dl_act& x, cudaS
   p.b_region = (w_bytes + 3 * a_stage <= room && rowtap_resident_enabled()) ? w_bytes : 0;
   if (!p.b_region && p.rt_cs) {   // the wide box pays only when it is reused (resident weights)
     p.rt_cs = 0;
-    a_stage = box_rows * RT_BW * kb * 2;
+    a_stage = (box_rows * RT_BW * kb * 2 + 1023) / 1024 * 1024;
     p.b_region = (w_bytes + 3 * a_stage <= room && rowtap_resident_enabled()) ? w_bytes : 0;
   }
   const int stage_bytes = a_stage + (p.b_region ? 0 : a->kh * b_box);

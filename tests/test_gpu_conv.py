@@ -423,7 +423,8 @@ def test_kblk32_fprop_and_dgrad_vs_fp64(c32, k, cout):
                                                   (64, 64, 3, 2, "rm", (37, 45)), (48, 32, 3, 1, "a", (20, 30)),
                                                   (32, 96, 5, 1, "m", (37, 45)), (32, 128, 5, 1, "", (20, 30)),
                                                   (128, 128, 3, 1, "rm", (37, 45)), (64, 80, 3, 2, "a", (16, 12)),
-                                                  (32, 192, 5, 1, "m", (20, 30)), (32, 256, 3, 1, "", (37, 45))])
+                                                  (32, 192, 5, 1, "m", (20, 30)), (32, 256, 3, 1, "", (37, 45)),
+                                                  (24, 32, 7, 1, "", (20, 30)), (32, 32, 7, 1, "r", (37, 45))])
 def test_rowtap_fprop_vs_fp64(cin, cout, k, d, ops, hw, n=2):
     """Narrow-output convs through the row-tap kernel (one tall input box per column tap and
     channel block, row taps at 1 KB offsets): bias, relu, residual / mask / accumulate epilogue
