@@ -258,6 +258,28 @@ __global__ void k_avgpool_bwd(const b2h* __restrict__ dy, int dys, b2h* __restri
         continue;
       }
     }
+    if (k == 2) {   // 2x2 pool (the Tiramisu transitions): the mask / accumulated loads of the four
+                    // outputs in flight before any store, same per-output arithmetic as finish()
+      const long long pp[4] = {p0, p0 + 1, p0 + w, p0 + w + 1};
+      float mv[4][G], ov[4][G];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (mask) ldv<G>(mask + pp[u] * ms + ch, mv[u]);
+        if (acc) ldv_rw<G>(dx + pp[u] * dxs + ch, ov[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        float o[G];
+#pragma unroll
+        for (int e = 0; e < G; ++e) {
+          o[e] = v[e];
+          if (mask && !(mv[u][e] > 0.f)) o[e] = 0.f;
+          if (acc) o[e] += ov[u][e];
+        }
+        stv<G>(dx + pp[u] * dxs + ch, o);
+      }
+      continue;
+    }
     for (int a = 0; a < k; ++a)
       for (int b = 0; b < k; ++b) {
         const long long p = p0 + static_cast<long long>(a) * w + b;
@@ -305,13 +327,26 @@ __global__ void k_upsample_bwd(const b2h* __restrict__ dy, int dys, b2h* __restr
     const int yy = static_cast<int>(r % h);
     const long long img = r / h;
     float s[G] = {};
-    for (int a = 0; a < f; ++a) {
-      const long long rowp = (img * h * f + yy * f + a) * W + xx * f;
-      for (int b = 0; b < f; ++b) {
-        float v[G];
-        ldv<G>(dy + (rowp + b) * dys + ch, v);
+    if (f == 2) {   // the four dy loads in flight at once, summed in the same order
+      const long long r0 = (img * h * f + yy * f) * W + xx * f, r1 = r0 + W;
+      float v[4][G];
+      ldv<G>(dy + r0 * dys + ch, v[0]);
+      ldv<G>(dy + (r0 + 1) * dys + ch, v[1]);
+      ldv<G>(dy + r1 * dys + ch, v[2]);
+      ldv<G>(dy + (r1 + 1) * dys + ch, v[3]);
 #pragma unroll
-        for (int e = 0; e < G; ++e) s[e] += v[e];
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int e = 0; e < G; ++e) s[e] += v[u][e];
+    } else {
+      for (int a = 0; a < f; ++a) {
+        const long long rowp = (img * h * f + yy * f + a) * W + xx * f;
+        for (int b = 0; b < f; ++b) {
+          float v[G];
+          ldv<G>(dy + (rowp + b) * dys + ch, v);
+#pragma unroll
+          for (int e = 0; e < G; ++e) s[e] += v[e];
+        }
       }
     }
     finish<G>(s, mask ? mask + q * ms + ch : nullptr, dx + q * dxs + ch, acc);
