@@ -1216,12 +1216,13 @@ __global__ void __launch_bounds__(FPROP_THREADS, 1)
 }
 
 // ------------------------------------------------------------------ row-tap fprop (narrow N)
-// Narrow-output convs (N = BN <= 64, e.g. the growth-32 5x5 dense layers of the Tiramisu): with one
-// 128-pixel box per (tap, K block) the operand loads, not the MMAs, bound the kernel (each input
-// element crosses L2 -> SM kh*kw times for only 2*BN FLOPs per byte).  Here an 8 x 16-pixel tile
-// loads, per (column tap j, 64-channel block), ONE tall box of 8 x (16 + (kh-1) dil) pixels and
-// the kh row taps address it at i*dil KB offsets (one SW128 atom per image row of 8 pixels), with
-// the kh weight boxes of that column streamed in the same stage: kh times fewer activation loads.
+// Narrow convs (forward N = BN <= 64, e.g. the growth-32 5x5 dense layers of the Tiramisu; dgrads
+// up to N = 256 over a narrow K): with one 128-pixel box per (tap, K block) the operand loads, not
+// the MMAs, bound the kernel (each input element crosses L2 -> SM kh*kw times for only 2*BN FLOPs
+// per byte).  Here an 8 x 16-pixel tile loads, per (column tap j, channel block), ONE tall box of
+// 8 x (16 + (kh-1) dil) pixels and the kh row taps address it at i*dil image-row offsets, with the
+// kh weight boxes of that column streamed in the same stage: kh times fewer activation loads.
+// With resident weights one wide box of (8 + (kw-1) dil) columns serves the column taps as well.
 constexpr int RT_BW = 8, RT_BH = 16;
 
 // KB = channels per K block (64, or 32 for 17..32-channel inputs: SW64, 512-byte image rows).  When
@@ -1858,7 +1859,7 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 // ------------------------------------------------------------------ row-tap wgrad (narrow N)
-// dW[(i, j, ci)][co] for narrow outputs (cout <= 64, the growth-32 dense layers): a CTA owns two
+// dW[(i, j, ci)][co] for narrow outputs (cout <= 64: the growth-32 dense layers, 3x3 64-channel convs): a CTA owns two
 // (column tap j, 64-channel block) combinations -- the two 64-row halves of a 128-row M tile, LBO =
 // one tall box -- over a range of 8 x 16-pixel K blocks, with one TMEM accumulator per tap row i.
 // Per K block it loads two tall x boxes (16 + (kh-1) dil rows) and one dy box, and every tap row
@@ -2370,8 +2371,8 @@ static int launch_halo_fprop(const b2dl_conv_args* a, const b2dl_act& xv, cudaSt
   return rc ? rc : check_launch();
 }
 
-// Row-tap path for narrow outputs (B2DL_ROWTAP=0 disables): packed weights, cout <= 64, >= 5 tap
-// rows (3x3 narrow layers measured faster on the generic kernel), bf16 output through the TMA
+// Row-tap path for narrow outputs (B2DL_ROWTAP=0 disables): packed weights, cout <= 128 (<= 256
+// over a <= 64-channel input), >= B2DL_ROWTAP_MINK (3) tap rows, bf16 output through the TMA
 // epilogue.
 static bool rowtap_enabled() {
   static const bool on = [] {

@@ -583,7 +583,7 @@ class Engine:
                     self.bn_fused[c.out] = o
         # Narrow-output convs with >= 5 tap rows (the growth-32 5x5 dense layers): the row-tap fprop
         # kernel reads one tall input box per (column tap, channel block) and packed weights
-        # (b2dl_conv_fprop picks it for w_packed, cout <= 64; B2DL_ROWTAP=0: the generic kernel)
+        # (b2dl_conv_fprop picks it for w_packed, cout <= 64 here; B2DL_ROWTAP=0: the generic kernel)
         self.rowtap = []
         rt_min_k = int(os.environ.get("B2DL_ROWTAP_MINK", "3"))
         if not self.fp32 and os.environ.get("B2DL_ROWTAP", "1") != "0":
