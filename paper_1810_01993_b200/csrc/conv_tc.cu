@@ -1859,8 +1859,8 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 // ------------------------------------------------------------------ row-tap wgrad (narrow N)
-// dW[(i, j, ci)][co] for narrow outputs (cout <= 64: the growth-32 dense layers, 3x3 64-channel convs): a CTA owns two
-// (column tap j, 64-channel block) combinations -- the two 64-row halves of a 128-row M tile, LBO =
+// dW[(i, j, ci)][co] for narrow outputs (cout <= 64: the growth-32 dense layers, 3x3 64-channel
+// convs): a CTA owns two (column tap j, 64-channel block) combinations -- the two 64-row halves of a 128-row M tile, LBO =
 // one tall box -- over a range of 8 x 16-pixel K blocks, with one TMEM accumulator per tap row i.
 // Per K block it loads two tall x boxes (16 + (kh-1) dil rows) and one dy box, and every tap row
 // reads the tall boxes at an i*dil KB offset: kh times fewer x loads than a box per tap.  Partial
