@@ -65,3 +65,25 @@ def test_config2_bf16_step_vs_fp32_engine(step):
     tab = prodshape.grad_table(g16, g32, net.param_order)
     worst = max(tab, key=lambda t: t[1])
     assert worst[1] < 2e-2, sorted(tab, key=lambda t: -t[1])[:5]
+
+
+def test_every_conv_launch_at_config4_shape_vs_fp64():
+    """The Tiramisu (config 4) step at 2 x 16 x 1152 x 768 in bf16: every conv launch -- the row-tap
+    forward / dgrad kernels with CTA pairs, wide boxes and N up to 256, the row-tap wgrads, the
+    128-wide short-K tiles of the squeeze dgrads -- against float64 on its own operands."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    import prodshape
+    from paper_1810_01993_b200.loss import ClassWeights
+    from paper_1810_01993_b200.models import tiramisu_config4
+    from paper_1810_01993_b200.net import MiniDenseNet
+    torch.cuda.set_device(0)
+    x, lab = prodshape.config2_batch(seed=2)
+    cw = ClassWeights((0.982, 0.017, 0.001)).vector()
+    net = MiniDenseNet(tiramisu_config4(), seed=0)
+    eng, loss, logits = prodshape.run_step(net, x, lab, cw)
+    rows = prodshape.Checker(net, eng, x, lab, cw, seed=3, pixels=24).run()
+    kinds = {r[0] for r in rows}
+    assert {"fprop", "wgrad", "dgrad"} <= kinds
+    bad = [r for r in rows if r[4] > (TOL_WGRAD if r[0] in ("wgrad", "bias grad") else TOL_ACT)]
+    assert not bad, bad[:10]
